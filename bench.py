@@ -1,0 +1,380 @@
+"""Benchmark of the configurator hot path (BASELINE.json metric) on B200.
+
+Workload (BASELINE.json configs[1]): one profile table of 4,096
+configurations (sampling x variant x batch x cores / GPU memory x {cpu, gpu}) and 2^20
+synthetic invocations per GPU.  A step is one batched OpTable.select pass over all 2^20
+invocations (K2, staircase kernel) with alpha rotating over {0, 1, 100, 1000} by step.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One JSON line on rank 0:
+  value     invocation x configuration evaluations / s, inputs resident in HBM, L2 flushed
+            between steps (256 MB write), device time (CUDA events on the launching stream),
+            max over ranks; decisions_per_s alongside.
+  e2e       the same metric through the reference-facing call with HOST (pinned) buffers:
+            H2D of the step's inputs, kernel, D2H of every decision, inside the timed region.
+  roofline  K2 kernel: algorithmic bytes per launch / mean launch time
+            vs the measured HBM copy bandwidth in MEASURED_PEAKS.json.
+  cpu_baseline  the oracle restatement of OpTable.select (numpy, same ops as the reference)
+            on all host cores, bounded sample (rank 0, N=1 only).
+--impl reference times only that CPU implementation (rank 0; other ranks exit 0).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "config decisions/sec (invocation x config evals/s) at 1/2/4/8 B200; % HBM roofline"
+UNIT = "evals/s"
+ALPHAS = (0.0, 1.0, 100.0, 1000.0)
+K_KINDS = 2
+B_IN = 8 * K_KINDS + 16      # slack[K] f64 + avail, supply, min_batch i32 + flags u32
+B_OUT = 4 + 4 + 4 + 8 + 8 + 8  # idx, code, fill i32 + objective, slack, wait f64
+B_CFG = 40                   # per configuration: lat, cost, costpen, res f64 + batch, kind|id
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def workload_config(n_inv: int, M: int, mode: str, world: int) -> dict:
+    return {
+        "workload": "config2: 2^20 invocations x 4,096 configs per GPU "
+                    "(sampling x variant x batch x cores/GPU-mem x {cpu,gpu}); SURVEY.md §8(d)",
+        "invocations_per_gpu": n_inv, "configs": M, "kinds": K_KINDS, "alphas": list(ALPHAS),
+        "kernel": "k_select_plan (K2b staircase)" if mode == "plan" else "k_select_scan (K2a)",
+        "l2": "flushed between timed steps (256 MB write, outside the events)",
+        "parallelism": f"replicated tables, invocations sharded, {world} GPU(s), no data-path collective",
+    }
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows: list[list[str]] = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self) -> dict:
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[3:7]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def load_peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "MEASURED_PEAKS.json (burst copy)"}
+    return {"hbm_gbs": 6650.0, "source": "fallback 6.65 TB/s (B200_PROFILING.md)"}
+
+
+def ncu_traffic() -> tuple[float | None, str | None]:
+    p = ROOT / "profiles" / "ncu_k2_summary.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d.get("dram_bytes_per_launch"), d.get("source")
+    return None, None
+
+
+# ---- CPU baseline (oracle restatement, all host cores) ----------------------------------------
+
+def cpu_baseline(target_s: float = 12.0) -> dict:
+    from oracle import optable
+    from paper_2102_01887_b200 import synth
+
+    spec = synth.synth_spec(False)
+    t = optable.from_spec(spec, synth.synth_scenario(), ["cpu", "gpu"])
+    M = len(t.lat)
+    cores = os.cpu_count() or 1
+    inv = synth.synth_invocations(1 << 16, t.lat, t.gkind)
+    # calibrate on one core, then size the all-core sample for ~target_s
+    t0 = time.perf_counter()
+    optable.select_many([t], inv.slack, 100.0, inv.avail, inv.supply, inv.min_batch, inv.flags, None, 0, 200)
+    rate1 = 200 / (time.perf_counter() - t0)
+    S = int(min(len(inv.avail), max(cores * 200, rate1 * cores * target_s)))
+    sub = inv.take(slice(0, S))
+    best = None
+    for _ in range(1):
+        t0 = time.perf_counter()
+        optable.select_many_parallel([t], sub.slack, 100.0, sub.avail, sub.supply, sub.min_batch,
+                                     sub.flags, processes=cores)
+        dt = time.perf_counter() - t0
+        best = dt if best is None else min(best, dt)
+    return {
+        "value": S * M / best, "unit": UNIT, "cores": cores, "kind": "port",
+        "decisions_per_s": S / best, "single_core_decisions_per_s": rate1,
+        "sample": f"{S} config-2 invocations x {M} configs (alpha=100), oracle/optable.py numpy "
+                  f"restatement of OpTable.select, multiprocessing over {cores} host cores",
+    }
+
+
+def reference_arm(args) -> None:
+    rank, world, local = dist_env()
+    if rank != 0:
+        return
+    from oracle import optable
+    from paper_2102_01887_b200 import synth
+
+    spec = synth.synth_spec(False)
+    t = optable.from_spec(spec, synth.synth_scenario(), ["cpu", "gpu"])
+    M = len(t.lat)
+    cores = os.cpu_count() or 1
+    inv = synth.synth_invocations(1 << 16, t.lat, t.gkind)
+    t0 = time.perf_counter()
+    optable.select_many([t], inv.slack, 100.0, inv.avail, inv.supply, inv.min_batch, inv.flags, None, 0, 200)
+    rate1 = 200 / (time.perf_counter() - t0)
+    S = int(min(len(inv.avail), max(cores * 100, rate1 * cores * args.ref_step_s)))
+    times = []
+    for step in range(args.warmup + args.steps):
+        a = ALPHAS[step % len(ALPHAS)]
+        off = (step * S) % max(1, len(inv.avail) - S)
+        sub = inv.take(slice(off, off + S))
+        t0 = time.perf_counter()
+        optable.select_many_parallel([t], sub.slack, a, sub.avail, sub.supply, sub.min_batch, sub.flags,
+                                     processes=cores)
+        dt = time.perf_counter() - t0
+        if step >= args.warmup:
+            times.append(dt)
+    tot = sum(times)
+    value = args.steps * S * M / tot
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (SURVEY.md §8(d) config 2, seed 20261017)",
+        "config": workload_config(1 << 20, M, "cpu", world),
+        "decisions_per_s": args.steps * S / tot,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"{S} invocations per step x {M} configs, oracle/optable.py numpy "
+                                   f"restatement of OpTable.select (configurator.py:239-300) over "
+                                   f"{cores} processes; the reference package is pure Python and "
+                                   f"is not present on the GPU box"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---- our arm ------------------------------------------------------------------------------------
+
+def our_arm(args) -> None:
+    import torch
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2102_01887_b200 as sp
+    from paper_2102_01887_b200 import synth
+
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    ctx = sp.get_context(local)
+    ctx.set_stream(stream.cuda_stream)
+
+    spec = synth.synth_spec(False)
+    table = sp.OpTable(spec, synth.synth_scenario(), device=local)
+    M = len(table.entries)
+    N = args.n
+    gk = table.gkind
+    inv = synth.synth_invocations(N, table.lat, gk, seed=20261017 + rank)
+    d_in = {
+        "slack": torch.from_numpy(inv.slack).to(dev), "avail": torch.from_numpy(inv.avail).to(dev),
+        "supply": torch.from_numpy(inv.supply).to(dev), "min_batch": torch.from_numpy(inv.min_batch).to(dev),
+        "flags": torch.from_numpy(inv.flags.astype(np.int32)).to(dev),
+    }
+    out = {
+        "idx": torch.empty(N, dtype=torch.int32, device=dev), "code": torch.empty(N, dtype=torch.int32, device=dev),
+        "fill": torch.empty(N, dtype=torch.int32, device=dev), "obj": torch.empty(N, dtype=torch.float64, device=dev),
+        "slack": torch.empty(N, dtype=torch.float64, device=dev), "wait": torch.empty(N, dtype=torch.float64, device=dev),
+    }
+
+    # plan build for every alpha (table is static: plans are reused across steps) — timed once
+    plan_ms = {}
+    for a in ALPHAS:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        table.prepare(a)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        plan_ms[str(a)] = e0.elapsed_time(e1)
+    plan_bytes = table.plan_bytes(100.0)
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def step(i, host=None):
+        a = ALPHAS[i % len(ALPHAS)]
+        if host is None:
+            table.select_batch(d_in["slack"], a, d_in["avail"], upstream_supply=d_in["supply"],
+                               min_batch=d_in["min_batch"], flags=d_in["flags"], mode=args.mode, out=out)
+        else:
+            table.select_batch(host["slack"], a, host["avail"], upstream_supply=host["supply"],
+                               min_batch=host["min_batch"], flags=host["flags"], mode=args.mode,
+                               out=host["out"])
+
+    for i in range(args.warmup):
+        flush.zero_()
+        step(i)
+    torch.cuda.synchronize(dev)
+
+    # ---- timed: device-resident ----
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize(dev)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches0 = ctx.launch_count
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.zero_()
+            evs[i][0].record(stream)
+            step(args.warmup + i)
+            evs[i][1].record(stream)
+        torch.cuda.synchronize(dev)
+    launches = ctx.launch_count - launches0
+    if world > 1:
+        torch.distributed.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    t_local = sum(step_ms) / 1e3
+    t_max = t_local
+    if world > 1:
+        tt = torch.tensor([t_local], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t_max = float(tt.item())
+    evals = args.steps * N * M * world
+    value = evals / t_max
+
+    # ---- e2e: host pinned buffers through the reference-facing call ----
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+    host = {"slack": pin(inv.slack), "avail": pin(inv.avail), "supply": pin(inv.supply),
+            "min_batch": pin(inv.min_batch), "flags": pin(inv.flags)}
+    host["out"] = {"idx": pin(np.empty(N, np.int32)), "code": pin(np.empty(N, np.int32)),
+                   "fill": pin(np.empty(N, np.int32)), "obj": pin(np.empty(N)), "slack": pin(np.empty(N)),
+                   "wait": pin(np.empty(N))}
+    h2d = sum(host[k].nbytes for k in ("slack", "avail", "supply", "min_batch", "flags"))
+    d2h = sum(v.nbytes for v in host["out"].values())
+    for i in range(2):
+        step(i, host)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize(dev)
+    e2e_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for i in range(args.steps):
+        flush.zero_()
+        e2e_ev[i][0].record(stream)
+        step(i, host)
+        e2e_ev[i][1].record(stream)
+    torch.cuda.synchronize(dev)
+    t_e2e = sum(a.elapsed_time(b) for a, b in e2e_ev) / 1e3
+    if world > 1:
+        tt = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t_e2e = float(tt.item())
+    e2e_value = evals / t_e2e
+
+    # ---- roofline of the K2 kernel ----
+    peaks = load_peaks()
+    kernel_s = t_local / args.steps
+    alg_bytes = N * (B_IN + B_OUT) + M * B_CFG
+    achieved = alg_bytes / kernel_s / 1e9
+    traffic, traffic_src = ncu_traffic()
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * t_max / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (SURVEY.md §8(d) config 2, invocation seed 20261017 + rank)",
+        "config": workload_config(N, M, args.mode, world),
+        "decisions_per_s": args.steps * N * world / t_max,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "decisions_per_s": args.steps * N * world / t_e2e,
+                "path": "OpTable.select_batch(numpy pinned) -> sp_select_batch(SP_MEM_HOST)"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                     "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
+                     "algorithmic_bytes_per_launch": alg_bytes,
+                     "bytes_model": f"N*(B_in {B_IN} + B_out {B_OUT}) + M*{B_CFG}",
+                     "kernel_ms": kernel_s * 1e3, "peak_source": peaks["source"],
+                     "traffic_source": traffic_src},
+        "gpu_launches": launches,
+        "plan": {"build_ms_per_alpha": plan_ms, "bytes": plan_bytes,
+                 "note": "staircase plan built once per (profile version, alpha); table static in config 2"},
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args.cpu_seconds)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=1 << 20)
+    ap.add_argument("--mode", default="plan", choices=["plan", "scan", "auto"])
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--ref-step-s", type=float, default=4.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        reference_arm(args)
+    else:
+        our_arm(args)
+
+
+if __name__ == "__main__":
+    main()

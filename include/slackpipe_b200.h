@@ -1,0 +1,185 @@
+/*
+ * slackpipe_b200.h — C-ABI of the B200-native configuration-optimizer hot path.
+ *
+ * The reference (`slackpipe`, arXiv 2102.01887 "Llama") has no FFI: its hot path is
+ * in-process Python + numpy in /root/reference/pkg/src/slackpipe/configurator.py and
+ * manager.py.  Every entry point below replaces one reference interface (cited per
+ * function).  The Python host mirror (paper_2102_01887_b200/configurator.py) binds these
+ * through ctypes with the same class/function names as the reference; INTEGRATION.md shows
+ * the binding a maintainer of the reference would add.
+ *
+ * Conventions
+ *   - Every function returns SP_OK (0) or a negative SP_E* code; the message is available
+ *     from sp_last_error().  No C++ exception crosses this boundary.
+ *   - All floating point is IEEE binary64 evaluated in exactly the reference's numpy order,
+ *     with no FMA contraction (SURVEY.md §8 rules P1-P3), so results are bit-identical.
+ *   - `mem` arguments say where the caller's I/O buffers live:
+ *       SP_MEM_HOST   host pointers (pinned or pageable).  The library copies them to the
+ *                     device, launches, copies results back and synchronises before it
+ *                     returns (the reference-facing path; bench.py's `e2e`).
+ *       SP_MEM_DEVICE device pointers (e.g. torch CUDA tensors' data_ptr()).  Work is
+ *                     stream-ordered on the context stream and the call returns without
+ *                     synchronising (bench.py's device-resident `value`).
+ *   - A context is bound to one device and one stream and is not re-entrant.
+ */
+#ifndef SLACKPIPE_B200_H
+#define SLACKPIPE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SP_OK 0
+#define SP_E_INVALID (-1)   /* maps to Python ValueError   */
+#define SP_E_CUDA (-2)      /* CUDA runtime / launch error  */
+#define SP_E_NOMEM (-3)     /* device or host allocation    */
+#define SP_E_UNSUPPORTED (-4)
+#define SP_E_RUNTIME (-5)   /* maps to Python RuntimeError */
+
+#define SP_MEM_HOST 0
+#define SP_MEM_DEVICE 1
+
+/* decision codes (out_code bits 0-1) — OpTable.select return shapes (configurator.py:239-300) */
+#define SP_DEC_NONE 0      /* select returned None (configurator.py:266-267) */
+#define SP_DEC_ASSIGN 1    /* Decision(kind="assign") (configurator.py:293-300) */
+#define SP_DEC_DELAY 2     /* Decision(kind="delay")  (configurator.py:278-286) */
+#define SP_DEC_FEASIBLE 4  /* bit 2: decision-time SLO flag L(x*) < slack[kind(x*)] (configurator.py:226) */
+
+/* per-invocation flags word (in_flags) */
+#define SP_FLAG_ALLOW_DELAY 1u       /* bit 0: allow_delay (configurator.py:245) */
+#define SP_FLAG_EXCL_SHIFT 8         /* bits 8..15: excluded_kinds as a mask over the K kinds */
+
+/* select modes */
+#define SP_MODE_AUTO 0   /* staircase kernel when the table's plan allows it, else scan */
+#define SP_MODE_PLAN 1   /* K2b: staircase (sorted prefix-min) decision kernel */
+#define SP_MODE_SCAN 2   /* K2a: brute-force fused scan over every entry */
+
+#define SP_MAX_KINDS 8
+#define SP_MAX_BATCH_VALUES 16
+
+typedef struct sp_ctx sp_ctx;
+typedef struct sp_table sp_table;
+typedef struct sp_dag sp_dag;
+
+/* ---- context ---------------------------------------------------------------------- */
+int sp_version(void);
+/* device: CUDA ordinal.  The context owns a non-blocking stream unless sp_ctx_set_stream
+ * installs a caller stream (cudaStream_t passed as void*). */
+int sp_ctx_create(int device, sp_ctx** out);
+int sp_ctx_destroy(sp_ctx* ctx);
+int sp_ctx_set_stream(sp_ctx* ctx, void* stream);
+int sp_ctx_synchronize(sp_ctx* ctx);
+/* Last error message of this thread (ctx may be NULL). */
+const char* sp_last_error(const sp_ctx* ctx);
+/* Kernels launched through this context since creation (evidence for bench gpu_launches). */
+int64_t sp_ctx_launch_count(const sp_ctx* ctx);
+
+/* ---- profile tables: OpTable (configurator.py:159-213) ------------------------------ */
+/* Replaces OpTable.__init__ (configurator.py:166-209).  Arrays are the OpTable SoA after
+ * filtering (host, length M): lat = latency_s, lat_init = latency_initial_s,
+ * res = resource_request, batch = batch_size, pool/price = backend pool_resources /
+ * price_rate, kind = index of backend_kind in the caller's global kind list (0..K-1),
+ * id_rank = rank of config_id in Python str order (configurator.py:195-198).
+ * ref_index = OpTable.ref_index (-1 when the reference is unschedulable). */
+int sp_table_create(sp_ctx* ctx, int32_t M, const double* lat, const double* lat_init,
+                    const double* res, const int32_t* batch, const double* pool,
+                    const double* price, const int32_t* kind, const int32_t* id_rank,
+                    int32_t K, int32_t ref_index, sp_table** out);
+int sp_table_destroy(sp_ctx* ctx, sp_table* t);
+/* OpTable.set_latency (configurator.py:211-213), batched: lat[idx[i]] = val[i] in order. */
+int sp_table_set_latency(sp_ctx* ctx, sp_table* t, int32_t n, const int32_t* idx,
+                         const double* val);
+/* Copy the live device latency vector (length M) to host memory (OpTable.lat). */
+int sp_table_get_latency(sp_ctx* ctx, sp_table* t, double* out_lat);
+/* Build (or reuse) the per-alpha decision plan: cost/costpen precompute + staircase
+ * index.  Called implicitly by the select entry points. */
+int sp_table_prepare(sp_ctx* ctx, sp_table* t, double alpha);
+/* 1 when the table's staircase plan is available (<= 16 distinct batch sizes, M < 65535). */
+int sp_table_plan_supported(const sp_table* t);
+/* Plan byte size for alpha after sp_table_prepare (synchronises); for DESIGN/bench. */
+int sp_table_plan_bytes(sp_ctx* ctx, sp_table* t, double alpha, int64_t* out_bytes);
+
+/* ---- Eq. 1 vector: OpTable.scores (configurator.py:219-227) -------------------------- */
+/* slack_by_kind: K doubles (host).  Outputs length M (host, synchronous). */
+int sp_scores(sp_ctx* ctx, sp_table* t, const double* slack_by_kind, double alpha,
+              double* out_score, double* out_cost);
+
+/* ---- K2: batched OpTable.select (configurator.py:239-300) --------------------------- */
+/* For every invocation i (0..N-1) against table tables[op[i]] (op may be NULL: table 0):
+ *   slack[i*K + k]  slack_by_kind for global kind k
+ *   avail[i]        `available`       supply[i]   `upstream_supply`
+ *   min_batch[i]    `min_batch`       flags[i]    SP_FLAG_* (allow_delay, excluded mask)
+ * Outputs per invocation:
+ *   out_idx   Decision.entry_index (-1 for None)      out_code SP_DEC_* | SP_DEC_FEASIBLE
+ *   out_fill  Decision.fill                           out_obj  Decision.objective_value
+ *   out_slack Decision.slack_s                        out_wait Decision.wait_budget_s
+ *   out_kind_min (optional, N*K): per-kind unmasked min score, +inf for kinds absent from
+ *             the table — the Eq. 3 operands of OpTable.affinity (configurator.py:302-318).
+ * Any output pointer may be NULL except out_idx and out_code. */
+int sp_select_batch(sp_ctx* ctx, int32_t n_tables, sp_table* const* tables, double alpha,
+                    int32_t N, const int32_t* op, const double* slack, const int32_t* avail,
+                    const int32_t* supply, const int32_t* min_batch, const uint32_t* flags,
+                    int32_t* out_idx, int32_t* out_code, int32_t* out_fill, double* out_obj,
+                    double* out_slack, double* out_wait, double* out_kind_min, int32_t mode,
+                    int32_t mem);
+
+/* Eq. 3 epilogue of OpTable.affinity (configurator.py:302-318) on the device: for invocation i
+ * and query kind q = query_kind[i], out[i] = min_{k != q} kind_min[i*K+k] / kind_min[i*K+q]
+ * (kind_min as produced by sp_select_batch; +inf marks kinds absent from the table, so an
+ * operation that runs only on q yields +inf exactly like the reference).  reserved must be
+ * NULL.  The caller maps "q absent from the table" to None before calling. */
+int sp_affinity_from_minima(sp_ctx* ctx, int32_t N, int32_t K, const double* kind_min,
+                            const int32_t* query_kind, double* out, void* reserved,
+                            int32_t mem);
+
+/* ---- K1: Alg. 1 slack over a DAG (configurator.py:493-543, compute_slack 76-106) ----- */
+/* A slack graph: V vertices in topological order (every pred index < vertex index),
+ * predecessor CSR (pred_ptr V+1, pred_idx), val_idx[v] = which per-instance reference
+ * latency the vertex carries, terminal[v] = 1 where a decomposed path may end (DAG sinks,
+ * or suffix ends for an explicit path list).  sources[s] = vertex whose slack is wanted
+ * (the operation itself, first element of its suffixes). */
+int sp_dag_create(sp_ctx* ctx, int32_t V, const int32_t* pred_ptr, const int32_t* pred_idx,
+                  const int32_t* val_idx, const uint8_t* terminal, int32_t n_src,
+                  const int32_t* sources, sp_dag** out);
+int sp_dag_destroy(sp_ctx* ctx, sp_dag* g);
+/* For instance i: ref = ref_lat + i*ref_stride (ref_stride 0 = shared by all instances),
+ * budget_k = (target[i] - now[i]) - Q[i*K+k]; out_slack[(i*n_src + s)*K + k] =
+ * min over suffixes of (ref[own]/suffix_total) * budget_k, bit-identical to
+ * Configurator.slack_by_kind / compute_slack.  out_ratio (optional, I*n_src*2) receives
+ * (own/Tmax, own/Tmin). */
+int sp_slack_batch(sp_ctx* ctx, sp_dag* g, int32_t I, const double* ref_lat,
+                   int32_t ref_stride, const double* target, const double* now, int32_t K,
+                   const double* Q, double* out_slack, double* out_ratio, int32_t mem);
+
+/* ---- Eq. 2: queueing_by_kind / estimate_queueing (configurator.py:109-119, 511-524) --- */
+/* Ordered sequential sum per kind: out[k] = (sum_{j in [ptr[k],ptr[k+1])} cnt[j]*(lat[j]*res[j]))
+ * / pool[k] when cnt != NULL (queueing_by_kind order), else sum of lat[j]*res[j]/pool[k]
+ * (estimate_queueing order).  Host arrays, synchronous. */
+int sp_queueing(sp_ctx* ctx, int32_t K, const int32_t* ptr, const double* lat,
+                const double* res, const int32_t* cnt, const double* pool, double* out);
+
+/* ---- K3: feedback fold (manager.py:436-457, configurator.py:463-491) ---------------- */
+/* Folds n observations (in completion order) into the tables: for observation j on table
+ * tables[op[j]], entry idx[j], value obs[j]:
+ *   completed_ref += (idx == ref_index);  obs_count[idx] += 1;
+ *   unless fb_frozen: lat[idx] = beta*obs + (1-beta)*lat[idx]            (manager.py:45-47)
+ *   if idx == ref_index && completed_ref == dfp_count && dfp_on:        (manager.py:449-457)
+ *       every entry never observed so far (obs_count == 0), except the reference, gets
+ *       lat = lat_init * (lat[ref] / lat_init[ref])                   (configurator.py:470-491)
+ * Bit-identical to the sequential reference loop.  out_ref_lat (optional, n_tables) gets the
+ * final reference latency (Configurator._ref_latency refresh, configurator.py:466-468). */
+int sp_feedback_fold(sp_ctx* ctx, int32_t n_tables, sp_table* const* tables, int32_t n,
+                     const int32_t* op, const int32_t* idx, const double* obs, double beta,
+                     int32_t dfp_count, int32_t dfp_on, int32_t fb_frozen, int32_t mem);
+/* Per-table counters maintained by sp_feedback_fold (host out). */
+int sp_table_get_counters(sp_ctx* ctx, sp_table* t, int32_t* completed_ref,
+                          int32_t* out_obs_count /* M, may be NULL */);
+int sp_table_set_counters(sp_ctx* ctx, sp_table* t, int32_t completed_ref,
+                          const int32_t* obs_count /* M, may be NULL */);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SLACKPIPE_B200_H */

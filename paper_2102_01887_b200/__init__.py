@@ -1,0 +1,42 @@
+"""B200-native configuration-optimizer hot path of Llama (arXiv 2102.01887, ref. pkg `slackpipe`).
+
+Drop-in for the reference's configurator path: ``OpTable`` / ``select_config`` /
+``affinity`` / ``compute_slack`` / ``estimate_queueing`` / ``objective`` /
+``apply_feedback`` keep the reference's names and semantics; batched entry points
+(``select_batch``, ``SlackGraph.slack_batch``, ``fold_observations``) run the same
+functions over millions of invocations on sm_100a kernels in libslackpipe_b200.so.
+"""
+from ._lib import SlackpipeError, get_context, load_library
+from .configurator import (
+    ABLATION_TOKENS,
+    AffinityScore,
+    Decision,
+    OpTable,
+    RawTable,
+    SelectResult,
+    Slack,
+    TuningParams,
+    affinity,
+    affinity_from_minima,
+    estimate_queueing,
+    make_flags,
+    objective,
+    remaining_path_latency,
+    select_batch,
+    select_config,
+)
+from .feedback import apply_feedback, fold_observations, set_table_counters, table_counters
+from .pipeline import ConfigEntry, ConfigSpec, PipelineDag, reference_config
+from .scenario import BackendSpec, Scenario
+from .slack import SlackGraph, compute_slack
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "ABLATION_TOKENS", "AffinityScore", "BackendSpec", "ConfigEntry", "ConfigSpec", "Decision",
+    "OpTable", "PipelineDag", "RawTable", "Scenario", "SelectResult", "Slack", "SlackGraph",
+    "SlackpipeError", "TuningParams", "affinity", "affinity_from_minima", "apply_feedback",
+    "compute_slack", "estimate_queueing", "fold_observations", "get_context", "load_library",
+    "make_flags", "objective", "reference_config", "remaining_path_latency", "select_batch",
+    "select_config", "set_table_counters", "table_counters",
+]

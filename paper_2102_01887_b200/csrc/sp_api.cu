@@ -1,0 +1,686 @@
+// sp_api.cu — C-ABI of libslackpipe_b200.so (declared in include/slackpipe_b200.h).
+//
+// Host-side responsibilities only: validation (mirroring the reference's ValueErrors),
+// device allocation, host<->device staging for SP_MEM_HOST calls, and launching the
+// kernels of sp_plan.cu / sp_select.cu / sp_slack.cu / sp_fold.cu.  No decision, score or
+// slack is ever computed on the host.
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "sp_internal.cuh"
+
+namespace sp {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+int cuda_fail(cudaError_t e, const char* what) {
+  g_last_error = std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e);
+  return SP_E_CUDA;
+}
+
+void* ctx_tmp(sp_ctx* ctx, size_t bytes, int* rc) {
+  if (bytes <= ctx->tmp_cap) return ctx->tmp_dev;
+  if (ctx->tmp_dev) {
+    cudaStreamSynchronize(ctx->stream);
+    cudaFree(ctx->tmp_dev);
+    ctx->tmp_dev = nullptr;
+    ctx->tmp_cap = 0;
+  }
+  size_t cap = std::max(bytes, (size_t)1 << 20);
+  cudaError_t e = cudaMalloc(&ctx->tmp_dev, cap);
+  if (e != cudaSuccess) {
+    if (rc) *rc = cuda_fail(e, "cudaMalloc(tmp)");
+    ctx->tmp_dev = nullptr;
+    return nullptr;
+  }
+  ctx->tmp_cap = cap;
+  return ctx->tmp_dev;
+}
+
+static void* ctx_io(sp_ctx* ctx, size_t bytes, int* rc) {
+  if (bytes <= ctx->io_cap) return ctx->io_dev;
+  if (ctx->io_dev) {
+    cudaStreamSynchronize(ctx->stream);
+    cudaFree(ctx->io_dev);
+    ctx->io_dev = nullptr;
+    ctx->io_cap = 0;
+  }
+  size_t cap = std::max(bytes, (size_t)4 << 20);
+  cudaError_t e = cudaMalloc(&ctx->io_dev, cap);
+  if (e != cudaSuccess) {
+    *rc = cuda_fail(e, "cudaMalloc(io)");
+    return nullptr;
+  }
+  ctx->io_cap = cap;
+  return ctx->io_dev;
+}
+
+// Simple bump allocator over the I/O arena.
+struct Bump {
+  uint8_t* base;
+  size_t off = 0;
+  template <typename T>
+  T* take(size_t n) {
+    T* p = reinterpret_cast<T*>(base + off);
+    off += (n * sizeof(T) + 255) & ~(size_t)255;
+    return p;
+  }
+};
+template <typename T>
+static size_t rsz(size_t n) {
+  return (n * sizeof(T) + 255) & ~(size_t)255;
+}
+
+__global__ void k_scatter(int m, const int32_t* __restrict__ idx, const double* __restrict__ val,
+                          double* __restrict__ dst) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < m) dst[idx[i]] = val[i];
+}
+
+static void free_table(sp_table* t) {
+  double* dd[] = {t->lat, t->lat_init, t->res, t->pool, t->price, t->thrscratch};
+  for (double* p : dd) cudaFree(p);
+  int32_t* ii[] = {t->batch, t->bidx, t->kind, t->id_rank, t->obs_count, t->kind_slot,
+                   t->ent_r1, t->ent_r2, t->order, t->rows_per_kind, t->dev_counters};
+  for (int32_t* p : ii) cudaFree(p);
+  uint32_t* uu[] = {t->r1, t->r2, t->lpos, t->pf, t->sf, t->rowscratch,
+                    t->candf, t->cands, t->cidf, t->cids};
+  for (uint32_t* p : uu) cudaFree(p);
+  for (auto& p : t->plans) {
+    cudaFree(p.cost);
+    cudaFree(p.costpen);
+    cudaFree(p.image);
+  }
+  delete t;
+}
+
+}  // namespace sp
+
+using namespace sp;
+
+extern "C" {
+
+int sp_version(void) { return 10000; }
+
+const char* sp_last_error(const sp_ctx*) { return g_last_error.c_str(); }
+
+int sp_ctx_create(int device, sp_ctx** out) {
+  if (!out) return fail(SP_E_INVALID, "ctx_create: null out");
+  int n = 0;
+  SP_CUDA(cudaGetDeviceCount(&n));
+  if (device < 0 || device >= n) return fail(SP_E_INVALID, "ctx_create: bad device ordinal");
+  SP_CUDA(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  SP_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major < 10)
+    return fail(SP_E_UNSUPPORTED, "ctx_create: this library is built for sm_100a (B200) only");
+  sp_ctx* c = new (std::nothrow) sp_ctx();
+  if (!c) return fail(SP_E_NOMEM, "ctx_create: host allocation");
+  c->device = device;
+  c->num_sms = prop.multiProcessorCount;
+  c->max_smem_optin = (int)prop.sharedMemPerBlockOptin;
+  cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete c;
+    return cuda_fail(e, "cudaStreamCreate");
+  }
+  c->own_stream = true;
+  *out = c;
+  return SP_OK;
+}
+
+int sp_ctx_destroy(sp_ctx* ctx) {
+  if (!ctx) return SP_OK;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  cudaFree(ctx->io_dev);
+  cudaFree(ctx->ptr_dev);
+  cudaFree(ctx->tmp_dev);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return SP_OK;
+}
+
+int sp_ctx_set_stream(sp_ctx* ctx, void* stream) {
+  if (!ctx) return fail(SP_E_INVALID, "null ctx");
+  SP_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+  ctx->stream = (cudaStream_t)stream;
+  ctx->own_stream = false;
+  return SP_OK;
+}
+
+int sp_ctx_synchronize(sp_ctx* ctx) {
+  if (!ctx) return fail(SP_E_INVALID, "null ctx");
+  SP_CUDA(cudaStreamSynchronize(ctx->stream));
+  return SP_OK;
+}
+
+int64_t sp_ctx_launch_count(const sp_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int sp_table_create(sp_ctx* ctx, int32_t M, const double* lat, const double* lat_init,
+                    const double* res, const int32_t* batch, const double* pool,
+                    const double* price, const int32_t* kind, const int32_t* id_rank,
+                    int32_t K, int32_t ref_index, sp_table** out) {
+  if (!ctx || !out) return fail(SP_E_INVALID, "table_create: null argument");
+  // configurator.py:178-179
+  if (M < 1) return fail(SP_E_INVALID, "operation has no schedulable configuration");
+  if (K < 1 || K > kMaxKinds) return fail(SP_E_UNSUPPORTED, "table_create: 1..8 kinds supported");
+  if (ref_index < -1 || ref_index >= M) return fail(SP_E_INVALID, "table_create: bad ref_index");
+  std::vector<int32_t> bv;
+  for (int j = 0; j < M; ++j) {
+    if (kind[j] < 0 || kind[j] >= K) return fail(SP_E_INVALID, "table_create: kind out of range");
+    if (batch[j] < 1) return fail(SP_E_INVALID, "table_create: batch size must be >= 1");
+    bv.push_back(batch[j]);
+  }
+  std::sort(bv.begin(), bv.end());
+  bv.erase(std::unique(bv.begin(), bv.end()), bv.end());
+  sp_table* t = new (std::nothrow) sp_table();
+  if (!t) return fail(SP_E_NOMEM, "table_create: host allocation");
+  t->M = M;
+  t->K = K;
+  t->ref_index = ref_index;
+  t->nB = (int)bv.size();
+  t->plan_ok = t->nB <= kMaxB && M < 65535;
+  for (int b = 0; b < kMaxB; ++b) t->batch_vals[b] = b < t->nB ? bv[b] : INT32_MAX;
+  std::vector<int32_t> bidx(M), kslot(M);
+  for (int j = 0; j < M; ++j)
+    bidx[j] = (int32_t)(std::lower_bound(bv.begin(), bv.end(), batch[j]) - bv.begin());
+  int cnt[kMaxKinds] = {0};
+  for (int j = 0; j < M; ++j) kslot[j] = cnt[kind[j]]++;
+  int base = 0;
+  for (int k = 0; k < kMaxKinds; ++k) {
+    t->kind_count[k] = k < K ? cnt[k] : 0;
+    t->kind_base[k] = base;
+    if (k < K) base += cnt[k];
+  }
+  cudaStream_t st = ctx->stream;
+  int rc = SP_OK;
+#define ALLOC_COPY(field, src, T)                                                  \
+  do {                                                                             \
+    cudaError_t _e = cudaMalloc(&t->field, sizeof(T) * M);                         \
+    if (_e == cudaSuccess && (src))                                                \
+      _e = cudaMemcpyAsync(t->field, (src), sizeof(T) * M, cudaMemcpyHostToDevice, st); \
+    if (_e != cudaSuccess) {                                                       \
+      rc = cuda_fail(_e, "table_create(" #field ")");                              \
+      free_table(t);                                                               \
+      return rc;                                                                   \
+    }                                                                              \
+  } while (0)
+  ALLOC_COPY(lat, lat, double);
+  ALLOC_COPY(lat_init, lat_init ? lat_init : lat, double);
+  ALLOC_COPY(res, res, double);
+  ALLOC_COPY(pool, pool, double);
+  ALLOC_COPY(price, price, double);
+  ALLOC_COPY(batch, batch, int32_t);
+  ALLOC_COPY(bidx, bidx.data(), int32_t);
+  ALLOC_COPY(kind, kind, int32_t);
+  ALLOC_COPY(id_rank, id_rank, int32_t);
+  ALLOC_COPY(kind_slot, kslot.data(), int32_t);
+  ALLOC_COPY(obs_count, (const int32_t*)nullptr, int32_t);
+#undef ALLOC_COPY
+  cudaError_t e = cudaMemsetAsync(t->obs_count, 0, sizeof(int32_t) * M, st);
+  if (e == cudaSuccess) e = cudaMalloc(&t->dev_counters, sizeof(int32_t) * 4);
+  if (e == cudaSuccess) e = cudaMemsetAsync(t->dev_counters, 0, sizeof(int32_t) * 4, st);
+  if (e != cudaSuccess) {
+    rc = cuda_fail(e, "table_create(counters)");
+    free_table(t);
+    return rc;
+  }
+  rc = plan_scratch_alloc(t);
+  if (rc != SP_OK) {
+    free_table(t);
+    return rc;
+  }
+  // host arrays may be released by the caller once we return
+  e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) {
+    rc = cuda_fail(e, "table_create(sync)");
+    free_table(t);
+    return rc;
+  }
+  *out = t;
+  return SP_OK;
+}
+
+int sp_table_destroy(sp_ctx* ctx, sp_table* t) {
+  if (!t) return SP_OK;
+  if (ctx) cudaStreamSynchronize(ctx->stream);
+  free_table(t);
+  return SP_OK;
+}
+
+int sp_table_set_latency(sp_ctx* ctx, sp_table* t, int32_t n, const int32_t* idx,
+                         const double* val) {
+  if (!ctx || !t || n < 0 || (n > 0 && (!idx || !val)))
+    return fail(SP_E_INVALID, "set_latency: bad argument");
+  // Repeated OpTable.set_latency calls: the last write to an index wins.
+  std::map<int32_t, double> last;
+  for (int i = 0; i < n; ++i) {
+    if (idx[i] < 0 || idx[i] >= t->M) return fail(SP_E_INVALID, "set_latency: index out of range");
+    last[idx[i]] = val[i];
+  }
+  if (last.empty()) return SP_OK;
+  std::vector<int32_t> ui;
+  std::vector<double> uv;
+  for (auto& kv : last) {
+    ui.push_back(kv.first);
+    uv.push_back(kv.second);
+  }
+  const int m = (int)ui.size();
+  int rc = SP_OK;
+  void* io = ctx_io(ctx, rsz<int32_t>(m) + rsz<double>(m), &rc);
+  if (!io) return rc;
+  Bump b{(uint8_t*)io};
+  int32_t* d_i = b.take<int32_t>(m);
+  double* d_v = b.take<double>(m);
+  SP_CUDA(cudaMemcpyAsync(d_i, ui.data(), sizeof(int32_t) * m, cudaMemcpyHostToDevice, ctx->stream));
+  SP_CUDA(cudaMemcpyAsync(d_v, uv.data(), sizeof(double) * m, cudaMemcpyHostToDevice, ctx->stream));
+  k_scatter<<<(m + 255) / 256, 256, 0, ctx->stream>>>(m, d_i, d_v, t->lat);
+  SP_CHECK_LAUNCH(ctx);
+  SP_CUDA(cudaStreamSynchronize(ctx->stream));
+  t->version++;
+  return SP_OK;
+}
+
+int sp_table_get_latency(sp_ctx* ctx, sp_table* t, double* out_lat) {
+  if (!ctx || !t || !out_lat) return fail(SP_E_INVALID, "get_latency: null argument");
+  SP_CUDA(cudaMemcpyAsync(out_lat, t->lat, sizeof(double) * t->M, cudaMemcpyDeviceToHost,
+                          ctx->stream));
+  SP_CUDA(cudaStreamSynchronize(ctx->stream));
+  return SP_OK;
+}
+
+int sp_table_prepare(sp_ctx* ctx, sp_table* t, double alpha) {
+  if (!ctx || !t) return fail(SP_E_INVALID, "prepare: null argument");
+  int rc;
+  Plan* p = plan_get(ctx, t, alpha, &rc);
+  return p ? SP_OK : rc;
+}
+
+int sp_table_plan_supported(const sp_table* t) { return t && t->plan_ok ? 1 : 0; }
+
+int sp_table_plan_bytes(sp_ctx* ctx, sp_table* t, double alpha, int64_t* out_bytes) {
+  if (!ctx || !t || !out_bytes) return fail(SP_E_INVALID, "plan_bytes: null argument");
+  int rc;
+  Plan* p = plan_get(ctx, t, alpha, &rc);
+  if (!p) return rc;
+  if (!t->plan_ok) {
+    *out_bytes = 0;
+    return SP_OK;
+  }
+  PlanHdr h;
+  SP_CUDA(cudaMemcpyAsync(&h, p->image, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+  SP_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (h.magic != kPlanMagic) return fail(SP_E_RUNTIME, "plan_bytes: plan image corrupt");
+  if (h.total_bytes > p->image_cap) return fail(SP_E_RUNTIME, "plan_bytes: plan overflow");
+  *out_bytes = h.total_bytes;
+  return SP_OK;
+}
+
+int sp_scores(sp_ctx* ctx, sp_table* t, const double* slack_by_kind, double alpha,
+              double* out_score, double* out_cost) {
+  if (!ctx || !t || !slack_by_kind || !out_score || !out_cost)
+    return fail(SP_E_INVALID, "scores: null argument");
+  int rc;
+  Plan* p = plan_get(ctx, t, alpha, &rc);
+  if (!p) return rc;
+  size_t need = rsz<double>(t->K) + 2 * rsz<double>(t->M);
+  void* io = ctx_io(ctx, need, &rc);
+  if (!io) return rc;
+  Bump b{(uint8_t*)io};
+  double* d_slack = b.take<double>(t->K);
+  double* d_score = b.take<double>(t->M);
+  double* d_cost = b.take<double>(t->M);
+  SP_CUDA(cudaMemcpyAsync(d_slack, slack_by_kind, sizeof(double) * t->K, cudaMemcpyHostToDevice,
+                          ctx->stream));
+  rc = scores_launch(ctx, t, p, d_slack, d_score, d_cost);
+  if (rc != SP_OK) return rc;
+  SP_CUDA(cudaMemcpyAsync(out_score, d_score, sizeof(double) * t->M, cudaMemcpyDeviceToHost,
+                          ctx->stream));
+  SP_CUDA(cudaMemcpyAsync(out_cost, d_cost, sizeof(double) * t->M, cudaMemcpyDeviceToHost,
+                          ctx->stream));
+  SP_CUDA(cudaStreamSynchronize(ctx->stream));
+  return SP_OK;
+}
+
+int sp_select_batch(sp_ctx* ctx, int32_t n_tables, sp_table* const* tables, double alpha,
+                    int32_t N, const int32_t* op, const double* slack, const int32_t* avail,
+                    const int32_t* supply, const int32_t* min_batch, const uint32_t* flags,
+                    int32_t* out_idx, int32_t* out_code, int32_t* out_fill, double* out_obj,
+                    double* out_slack, double* out_wait, double* out_kind_min, int32_t mode,
+                    int32_t mem) {
+  if (!ctx || !tables || n_tables < 1) return fail(SP_E_INVALID, "select: null argument");
+  if (N < 0) return fail(SP_E_INVALID, "select: negative N");
+  if (N > 0 && (!slack || !avail || !supply || !min_batch || !flags || !out_idx || !out_code))
+    return fail(SP_E_INVALID, "select: required array is null");
+  if (!(alpha >= 0.0)) return fail(SP_E_INVALID, "alpha must be >= 0");  // configurator.py:37
+  for (int t = 0; t < n_tables; ++t)
+    if (!tables[t]) return fail(SP_E_INVALID, "select: null table");
+  const int K = tables[0]->K;
+  if (mem == SP_MEM_DEVICE) {
+    return select_launch(ctx, n_tables, tables, alpha, N, op, slack, avail, supply, min_batch,
+                         flags, out_idx, out_code, out_fill, out_obj, out_slack, out_wait,
+                         out_kind_min, mode);
+  }
+  if (mem != SP_MEM_HOST) return fail(SP_E_INVALID, "select: bad mem flag");
+  if (op) {
+    for (int i = 0; i < N; ++i)
+      if (op[i] < 0 || op[i] >= n_tables) return fail(SP_E_INVALID, "select: op out of range");
+  }
+  size_t need = rsz<double>((size_t)N * K) + 4 * rsz<int32_t>(N) + (op ? rsz<int32_t>(N) : 0) +
+                3 * rsz<int32_t>(N) + 3 * rsz<double>(N) +
+                (out_kind_min ? rsz<double>((size_t)N * K) : 0);
+  int rc = SP_OK;
+  void* io = ctx_io(ctx, need, &rc);
+  if (!io) return rc;
+  Bump b{(uint8_t*)io};
+  cudaStream_t st = ctx->stream;
+  double* d_slack = b.take<double>((size_t)N * K);
+  int32_t* d_avail = b.take<int32_t>(N);
+  int32_t* d_supply = b.take<int32_t>(N);
+  int32_t* d_minb = b.take<int32_t>(N);
+  uint32_t* d_flags = b.take<uint32_t>(N);
+  int32_t* d_op = op ? b.take<int32_t>(N) : nullptr;
+  int32_t* d_idx = b.take<int32_t>(N);
+  int32_t* d_code = b.take<int32_t>(N);
+  int32_t* d_fill = b.take<int32_t>(N);
+  double* d_obj = b.take<double>(N);
+  double* d_sl = b.take<double>(N);
+  double* d_wait = b.take<double>(N);
+  double* d_kmin = out_kind_min ? b.take<double>((size_t)N * K) : nullptr;
+  if (N > 0) {
+    SP_CUDA(cudaMemcpyAsync(d_slack, slack, sizeof(double) * N * K, cudaMemcpyHostToDevice, st));
+    SP_CUDA(cudaMemcpyAsync(d_avail, avail, sizeof(int32_t) * N, cudaMemcpyHostToDevice, st));
+    SP_CUDA(cudaMemcpyAsync(d_supply, supply, sizeof(int32_t) * N, cudaMemcpyHostToDevice, st));
+    SP_CUDA(cudaMemcpyAsync(d_minb, min_batch, sizeof(int32_t) * N, cudaMemcpyHostToDevice, st));
+    SP_CUDA(cudaMemcpyAsync(d_flags, flags, sizeof(uint32_t) * N, cudaMemcpyHostToDevice, st));
+    if (op) SP_CUDA(cudaMemcpyAsync(d_op, op, sizeof(int32_t) * N, cudaMemcpyHostToDevice, st));
+  }
+  rc = select_launch(ctx, n_tables, tables, alpha, N, d_op, d_slack, d_avail, d_supply, d_minb,
+                     d_flags, d_idx, d_code, d_fill, d_obj, d_sl, d_wait, d_kmin, mode);
+  if (rc != SP_OK) return rc;
+  if (N > 0) {
+    SP_CUDA(cudaMemcpyAsync(out_idx, d_idx, sizeof(int32_t) * N, cudaMemcpyDeviceToHost, st));
+    SP_CUDA(cudaMemcpyAsync(out_code, d_code, sizeof(int32_t) * N, cudaMemcpyDeviceToHost, st));
+    if (out_fill)
+      SP_CUDA(cudaMemcpyAsync(out_fill, d_fill, sizeof(int32_t) * N, cudaMemcpyDeviceToHost, st));
+    if (out_obj)
+      SP_CUDA(cudaMemcpyAsync(out_obj, d_obj, sizeof(double) * N, cudaMemcpyDeviceToHost, st));
+    if (out_slack)
+      SP_CUDA(cudaMemcpyAsync(out_slack, d_sl, sizeof(double) * N, cudaMemcpyDeviceToHost, st));
+    if (out_wait)
+      SP_CUDA(cudaMemcpyAsync(out_wait, d_wait, sizeof(double) * N, cudaMemcpyDeviceToHost, st));
+    if (out_kind_min)
+      SP_CUDA(cudaMemcpyAsync(out_kind_min, d_kmin, sizeof(double) * N * K,
+                              cudaMemcpyDeviceToHost, st));
+  }
+  SP_CUDA(cudaStreamSynchronize(st));
+  return SP_OK;
+}
+
+int sp_affinity_from_minima(sp_ctx* ctx, int32_t N, int32_t K, const double* kind_min,
+                            const int32_t* query_kind, double* out, void* reserved,
+                            int32_t mem) {
+  if (!ctx || N < 0 || K < 1 || K > kMaxKinds || reserved)
+    return fail(SP_E_INVALID, "affinity: bad argument");
+  if (N > 0 && (!kind_min || !query_kind || !out)) return fail(SP_E_INVALID, "affinity: null array");
+  if (mem == SP_MEM_DEVICE) return affinity_launch(ctx, N, K, kind_min, query_kind, out);
+  if (mem != SP_MEM_HOST) return fail(SP_E_INVALID, "affinity: bad mem flag");
+  for (int i = 0; i < N; ++i)
+    if (query_kind[i] < 0 || query_kind[i] >= K) return fail(SP_E_INVALID, "affinity: kind out of range");
+  int rc = SP_OK;
+  void* io = ctx_io(ctx, rsz<double>((size_t)N * K) + rsz<int32_t>(N) + rsz<double>(N), &rc);
+  if (!io) return rc;
+  Bump b{(uint8_t*)io};
+  double* d_k = b.take<double>((size_t)N * K);
+  int32_t* d_q = b.take<int32_t>(N);
+  double* d_o = b.take<double>(N);
+  cudaStream_t st = ctx->stream;
+  if (N > 0) {
+    SP_CUDA(cudaMemcpyAsync(d_k, kind_min, sizeof(double) * N * K, cudaMemcpyHostToDevice, st));
+    SP_CUDA(cudaMemcpyAsync(d_q, query_kind, sizeof(int32_t) * N, cudaMemcpyHostToDevice, st));
+  }
+  rc = affinity_launch(ctx, N, K, d_k, d_q, d_o);
+  if (rc != SP_OK) return rc;
+  if (N > 0) SP_CUDA(cudaMemcpyAsync(out, d_o, sizeof(double) * N, cudaMemcpyDeviceToHost, st));
+  SP_CUDA(cudaStreamSynchronize(st));
+  return SP_OK;
+}
+
+// ---- K1 graph ----------------------------------------------------------------------------
+int sp_dag_create(sp_ctx* ctx, int32_t V, const int32_t* pred_ptr, const int32_t* pred_idx,
+                  const int32_t* val_idx, const uint8_t* terminal, int32_t n_src,
+                  const int32_t* sources, sp_dag** out) {
+  if (!ctx || !out || V < 1 || !pred_ptr || !val_idx || !terminal || n_src < 1 || !sources)
+    return fail(SP_E_INVALID, "dag_create: bad argument");
+  if (pred_ptr[0] != 0) return fail(SP_E_INVALID, "dag_create: pred_ptr[0] must be 0");
+  for (int v = 0; v < V; ++v) {
+    if (pred_ptr[v + 1] < pred_ptr[v]) return fail(SP_E_INVALID, "dag_create: bad pred_ptr");
+    for (int q = pred_ptr[v]; q < pred_ptr[v + 1]; ++q)
+      if (pred_idx[q] < 0 || pred_idx[q] >= v)
+        return fail(SP_E_INVALID, "dag_create: vertices must be in topological order");
+    if (val_idx[v] < 0) return fail(SP_E_INVALID, "dag_create: bad val_idx");
+  }
+  // successor lists to compute descendant sets
+  std::vector<std::vector<int>> succ(V);
+  for (int v = 0; v < V; ++v)
+    for (int q = pred_ptr[v]; q < pred_ptr[v + 1]; ++q) succ[pred_idx[q]].push_back(v);
+  std::vector<int4> prog;
+  std::vector<int32_t> pptr(1, 0);
+  std::vector<uint16_t> preds;
+  int max_span = 0, n_val = 0;
+  for (int v = 0; v < V; ++v) n_val = std::max(n_val, val_idx[v] + 1);
+  std::vector<int> slot(V, -1);
+  for (int s = 0; s < n_src; ++s) {
+    int src = sources[s];
+    if (src < 0 || src >= V) return fail(SP_E_INVALID, "dag_create: source out of range");
+    std::fill(slot.begin(), slot.end(), -1);
+    std::vector<char> reach(V, 0);
+    reach[src] = 1;
+    for (int v = src; v < V; ++v)
+      if (reach[v])
+        for (int w : succ[v]) reach[w] = 1;
+    int nslot = 0;
+    for (int v = src; v < V; ++v) {
+      if (!reach[v]) continue;
+      slot[v] = nslot++;
+      int pb = (int)preds.size();
+      if (v != src) {
+        for (int q = pred_ptr[v]; q < pred_ptr[v + 1]; ++q) {
+          int p = pred_idx[q];
+          if (slot[p] >= 0) preds.push_back((uint16_t)slot[p]);
+        }
+      }
+      prog.push_back(make_int4(val_idx[v], terminal[v] ? 1 : 0, pb, (int)preds.size()));
+    }
+    if (nslot > 65535) return fail(SP_E_UNSUPPORTED, "dag_create: too many descendants");
+    max_span = std::max(max_span, nslot);
+    pptr.push_back((int32_t)prog.size());
+  }
+  sp_dag* g = new (std::nothrow) sp_dag();
+  if (!g) return fail(SP_E_NOMEM, "dag_create: host allocation");
+  g->V = V;
+  g->n_src = n_src;
+  g->n_val = n_val;
+  g->max_span = max_span;
+  g->prog_len = (int64_t)prog.size();
+  g->pred_len = (int64_t)preds.size();
+  cudaError_t e = cudaMalloc(&g->prog, sizeof(int4) * prog.size());
+  if (e == cudaSuccess) e = cudaMalloc(&g->prog_ptr, sizeof(int32_t) * pptr.size());
+  if (e == cudaSuccess) e = cudaMalloc(&g->preds, sizeof(uint16_t) * std::max<size_t>(1, preds.size()));
+  if (e == cudaSuccess)
+    e = cudaMemcpy(g->prog, prog.data(), sizeof(int4) * prog.size(), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess)
+    e = cudaMemcpy(g->prog_ptr, pptr.data(), sizeof(int32_t) * pptr.size(), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && !preds.empty())
+    e = cudaMemcpy(g->preds, preds.data(), sizeof(uint16_t) * preds.size(), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    cudaFree(g->prog);
+    cudaFree(g->prog_ptr);
+    cudaFree(g->preds);
+    delete g;
+    return cuda_fail(e, "dag_create");
+  }
+  *out = g;
+  return SP_OK;
+}
+
+int sp_dag_destroy(sp_ctx* ctx, sp_dag* g) {
+  if (!g) return SP_OK;
+  if (ctx) cudaStreamSynchronize(ctx->stream);
+  cudaFree(g->prog);
+  cudaFree(g->prog_ptr);
+  cudaFree(g->preds);
+  delete g;
+  return SP_OK;
+}
+
+int sp_slack_batch(sp_ctx* ctx, sp_dag* g, int32_t I, const double* ref_lat,
+                   int32_t ref_stride, const double* target, const double* now, int32_t K,
+                   const double* Q, double* out_slack, double* out_ratio, int32_t mem) {
+  if (!ctx || !g || I < 0 || !ref_lat || !target || !now || K < 0 || (K > 0 && !Q))
+    return fail(SP_E_INVALID, "slack_batch: bad argument");
+  if (ref_stride != 0 && ref_stride < g->n_val)
+    return fail(SP_E_INVALID, "slack_batch: ref_stride smaller than the value count");
+  if (mem == SP_MEM_DEVICE)
+    return slack_launch(ctx, g, I, ref_lat, ref_stride, target, now, K, Q, out_slack,
+                        out_ratio);
+  if (mem != SP_MEM_HOST) return fail(SP_E_INVALID, "slack_batch: bad mem flag");
+  const size_t nref = ref_stride ? (size_t)I * ref_stride : (size_t)g->n_val;
+  const size_t nout = (size_t)I * g->n_src;
+  size_t need = rsz<double>(nref) + 2 * rsz<double>(I) + rsz<double>((size_t)I * K) +
+                (out_slack ? rsz<double>(nout * K) : 0) + (out_ratio ? rsz<double>(nout * 2) : 0);
+  int rc = SP_OK;
+  void* io = ctx_io(ctx, need, &rc);
+  if (!io) return rc;
+  Bump b{(uint8_t*)io};
+  cudaStream_t st = ctx->stream;
+  double* d_ref = b.take<double>(nref);
+  double* d_t = b.take<double>(I);
+  double* d_n = b.take<double>(I);
+  double* d_q = b.take<double>((size_t)I * K);
+  double* d_out = out_slack ? b.take<double>(nout * K) : nullptr;
+  double* d_rat = out_ratio ? b.take<double>(nout * 2) : nullptr;
+  SP_CUDA(cudaMemcpyAsync(d_ref, ref_lat, sizeof(double) * nref, cudaMemcpyHostToDevice, st));
+  if (I > 0) {
+    SP_CUDA(cudaMemcpyAsync(d_t, target, sizeof(double) * I, cudaMemcpyHostToDevice, st));
+    SP_CUDA(cudaMemcpyAsync(d_n, now, sizeof(double) * I, cudaMemcpyHostToDevice, st));
+    if (K > 0)
+      SP_CUDA(cudaMemcpyAsync(d_q, Q, sizeof(double) * I * K, cudaMemcpyHostToDevice, st));
+  }
+  rc = slack_launch(ctx, g, I, d_ref, ref_stride, d_t, d_n, K, d_q, d_out, d_rat);
+  if (rc != SP_OK) return rc;
+  if (I > 0 && out_slack)
+    SP_CUDA(cudaMemcpyAsync(out_slack, d_out, sizeof(double) * nout * K, cudaMemcpyDeviceToHost, st));
+  if (I > 0 && out_ratio)
+    SP_CUDA(cudaMemcpyAsync(out_ratio, d_rat, sizeof(double) * nout * 2, cudaMemcpyDeviceToHost, st));
+  SP_CUDA(cudaStreamSynchronize(st));
+  return SP_OK;
+}
+
+int sp_queueing(sp_ctx* ctx, int32_t K, const int32_t* ptr, const double* lat,
+                const double* res, const int32_t* cnt, const double* pool, double* out) {
+  if (!ctx || K < 1 || K > 32 || !ptr || !pool || !out)
+    return fail(SP_E_INVALID, "queueing: bad argument");
+  const int n = ptr[K];
+  if (n < 0) return fail(SP_E_INVALID, "queueing: bad ptr");
+  size_t need = rsz<int32_t>(K + 1) + 2 * rsz<double>(n) + rsz<int32_t>(n) + 2 * rsz<double>(K);
+  int rc = SP_OK;
+  void* io = ctx_io(ctx, need, &rc);
+  if (!io) return rc;
+  Bump b{(uint8_t*)io};
+  cudaStream_t st = ctx->stream;
+  int32_t* d_ptr = b.take<int32_t>(K + 1);
+  double* d_lat = b.take<double>(n);
+  double* d_res = b.take<double>(n);
+  int32_t* d_cnt = cnt ? b.take<int32_t>(n) : nullptr;
+  double* d_pool = b.take<double>(K);
+  double* d_out = b.take<double>(K);
+  SP_CUDA(cudaMemcpyAsync(d_ptr, ptr, sizeof(int32_t) * (K + 1), cudaMemcpyHostToDevice, st));
+  if (n > 0) {
+    SP_CUDA(cudaMemcpyAsync(d_lat, lat, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+    SP_CUDA(cudaMemcpyAsync(d_res, res, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+    if (cnt) SP_CUDA(cudaMemcpyAsync(d_cnt, cnt, sizeof(int32_t) * n, cudaMemcpyHostToDevice, st));
+  }
+  SP_CUDA(cudaMemcpyAsync(d_pool, pool, sizeof(double) * K, cudaMemcpyHostToDevice, st));
+  rc = queueing_launch(ctx, K, d_ptr, d_lat, d_res, d_cnt, d_pool, d_out);
+  if (rc != SP_OK) return rc;
+  SP_CUDA(cudaMemcpyAsync(out, d_out, sizeof(double) * K, cudaMemcpyDeviceToHost, st));
+  SP_CUDA(cudaStreamSynchronize(st));
+  return SP_OK;
+}
+
+int sp_feedback_fold(sp_ctx* ctx, int32_t n_tables, sp_table* const* tables, int32_t n,
+                     const int32_t* op, const int32_t* idx, const double* obs, double beta,
+                     int32_t dfp_count, int32_t dfp_on, int32_t fb_frozen, int32_t mem) {
+  if (!ctx || !tables || n_tables < 1 || n < 0 || (n > 0 && (!idx || !obs)))
+    return fail(SP_E_INVALID, "feedback_fold: bad argument");
+  if (!(beta > 0.0 && beta <= 1.0)) return fail(SP_E_INVALID, "smoothing_beta must be in (0, 1]");
+  if (mem == SP_MEM_DEVICE)
+    return fold_launch(ctx, n_tables, tables, n, op, idx, obs, beta, dfp_count, dfp_on,
+                       fb_frozen);
+  if (mem != SP_MEM_HOST) return fail(SP_E_INVALID, "feedback_fold: bad mem flag");
+  for (int j = 0; j < n; ++j) {
+    int t = op ? op[j] : 0;
+    if (t < 0 || t >= n_tables) return fail(SP_E_INVALID, "feedback_fold: op out of range");
+    if (idx[j] < 0 || idx[j] >= tables[t]->M)
+      return fail(SP_E_INVALID, "feedback_fold: entry index out of range");
+  }
+  size_t need = 2 * rsz<int32_t>(n) + rsz<double>(n);
+  int rc = SP_OK;
+  void* io = ctx_io(ctx, need, &rc);
+  if (!io) return rc;
+  Bump b{(uint8_t*)io};
+  cudaStream_t st = ctx->stream;
+  int32_t* d_op = op ? b.take<int32_t>(n) : nullptr;
+  int32_t* d_idx = b.take<int32_t>(n);
+  double* d_obs = b.take<double>(n);
+  if (n > 0) {
+    if (op) SP_CUDA(cudaMemcpyAsync(d_op, op, sizeof(int32_t) * n, cudaMemcpyHostToDevice, st));
+    SP_CUDA(cudaMemcpyAsync(d_idx, idx, sizeof(int32_t) * n, cudaMemcpyHostToDevice, st));
+    SP_CUDA(cudaMemcpyAsync(d_obs, obs, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+  }
+  rc = fold_launch(ctx, n_tables, tables, n, d_op, d_idx, d_obs, beta, dfp_count, dfp_on,
+                   fb_frozen);
+  if (rc != SP_OK) return rc;
+  SP_CUDA(cudaStreamSynchronize(st));
+  return SP_OK;
+}
+
+int sp_table_get_counters(sp_ctx* ctx, sp_table* t, int32_t* completed_ref,
+                          int32_t* out_obs_count) {
+  if (!ctx || !t) return fail(SP_E_INVALID, "get_counters: null argument");
+  int32_t c[4];
+  SP_CUDA(cudaMemcpyAsync(c, t->dev_counters, sizeof(c), cudaMemcpyDeviceToHost, ctx->stream));
+  if (out_obs_count)
+    SP_CUDA(cudaMemcpyAsync(out_obs_count, t->obs_count, sizeof(int32_t) * t->M,
+                            cudaMemcpyDeviceToHost, ctx->stream));
+  SP_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (completed_ref) *completed_ref = c[0];
+  return SP_OK;
+}
+
+int sp_table_set_counters(sp_ctx* ctx, sp_table* t, int32_t completed_ref,
+                          const int32_t* obs_count) {
+  if (!ctx || !t) return fail(SP_E_INVALID, "set_counters: null argument");
+  int32_t c[4] = {completed_ref, 0, 0, 0};
+  SP_CUDA(cudaMemcpyAsync(t->dev_counters, c, sizeof(c), cudaMemcpyHostToDevice, ctx->stream));
+  if (obs_count)
+    SP_CUDA(cudaMemcpyAsync(t->obs_count, obs_count, sizeof(int32_t) * t->M,
+                            cudaMemcpyHostToDevice, ctx->stream));
+  SP_CUDA(cudaStreamSynchronize(ctx->stream));
+  return SP_OK;
+}
+
+}  // extern "C"

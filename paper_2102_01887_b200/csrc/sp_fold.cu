@@ -1,0 +1,235 @@
+// sp_fold.cu — K3: profile feedback fold (manager.py:436-457, 45-47; configurator.py:463-491).
+//
+// Reference, per completed invocation in completion order:
+//     if eidx == ref_index: completed_ref += 1                         (manager.py:440-441)
+//     observations[(op, config_id)] += 1                               (442)
+//     if fb frozen: stop                                               (443-444)
+//     lat[eidx] = beta*obs + (1-beta)*lat[eidx]                         (445-447, 45-47)
+//     if eidx == ref_index and completed_ref == dfp_count and dfp on:  (449-457)
+//         ratio = lat[ref] / lat_init[ref]
+//         every entry never observed so far (except the reference):
+//             lat[i] = lat_init[i] * ratio                             (configurator.py:486-490)
+//
+// Device restatement (bit-exact): the EWMA recurrence is order-dependent, so it is NOT
+// tree-reduced; instead the observation batch is stably sorted by (table, entry) with a CUB
+// radix sort (positions ascending inside each key = completion order), and one thread folds
+// each entry's segment sequentially.  The gate lift is located inside the reference entry's
+// own segment (the k-th reference observation, k = dfp_count - completed_ref_before); an entry
+// is rescaled iff it had no observation before the batch and its first observation in the
+// batch comes after the gate position — exactly the set recalibrate_unobserved sees.
+#include <cub/cub.cuh>
+
+#include "sp_internal.cuh"
+
+namespace sp {
+namespace {
+
+constexpr int kMaxFoldTables = 64;
+
+struct FoldTab {
+  double* lat;
+  const double* lat_init;
+  int32_t* obs_count;
+  int32_t* counters;  // [0] completed_ref
+  int32_t M;
+  int32_t ref_index;
+  int32_t gbase;  // global key base
+  int32_t pad;
+};
+struct FoldTabs {
+  FoldTab t[kMaxFoldTables];
+  int n;
+};
+// per-table gate state produced by k_fold_ref, consumed by the other two kernels
+struct Gate {
+  int32_t lifted;   // gate lifts inside this batch
+  int32_t gate_pos; // stream position of the lifting reference observation
+  double ratio;
+};
+
+__global__ void k_fold_keys(int n, FoldTabs ft, const int32_t* __restrict__ op,
+                            const int32_t* __restrict__ idx, uint32_t* keys, uint32_t* pos) {
+  int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  int t = op ? op[j] : 0;
+  keys[j] = (uint32_t)(ft.t[t].gbase + idx[j]);
+  pos[j] = (uint32_t)j;
+}
+
+__device__ __forceinline__ double ewma(double beta, double obs, double old) {
+  // manager.py:47  beta * observed_s + (1.0 - beta) * old_estimate_s
+  return __dadd_rn(__dmul_rn(beta, obs), __dmul_rn(__dsub_rn(1.0, beta), old));
+}
+
+__device__ int lower_bound_u32(const uint32_t* a, int n, uint32_t key) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (a[mid] < key) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// One thread per table: fold the reference entry's segment, locate the gate lift.
+__global__ void k_fold_ref(int n, FoldTabs ft, const uint32_t* __restrict__ skeys,
+                           const uint32_t* __restrict__ spos, const double* __restrict__ obs,
+                           double beta, int dfp_count, int dfp_on, int fb_frozen, Gate* gates) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= ft.n) return;
+  FoldTab tb = ft.t[t];
+  Gate g;
+  g.lifted = 0;
+  g.gate_pos = -1;
+  g.ratio = 1.0;
+  if (tb.ref_index < 0) {
+    gates[t] = g;
+    return;
+  }
+  const uint32_t key = (uint32_t)(tb.gbase + tb.ref_index);
+  int q = lower_bound_u32(skeys, n, key);
+  int before = tb.counters[0];
+  int c = before;
+  double L = tb.lat[tb.ref_index];
+  int cnt = 0;
+  for (; q < n && skeys[q] == key; ++q) {
+    ++c;
+    ++cnt;
+    if (fb_frozen) continue;
+    L = ewma(beta, obs[spos[q]], L);
+    if (c == dfp_count && dfp_on) {
+      double init = tb.lat_init[tb.ref_index];
+      if (init > 0.0) {
+        g.lifted = 1;
+        g.gate_pos = (int)spos[q];
+        g.ratio = __ddiv_rn(L, init);  // configurator.py:486
+      }
+    }
+  }
+  if (cnt) {
+    tb.counters[0] = c;
+    tb.lat[tb.ref_index] = L;
+    tb.obs_count[tb.ref_index] += cnt;
+  }
+  gates[t] = g;
+}
+
+__device__ __forceinline__ int table_of_key(const FoldTabs& ft, uint32_t key) {
+  int t = 0;
+  for (int u = 1; u < ft.n; ++u)
+    if ((int)key >= ft.t[u].gbase) t = u;
+  return t;
+}
+
+// One thread per segment head (non-reference entries).
+__global__ void k_fold_seg(int n, FoldTabs ft, const uint32_t* __restrict__ skeys,
+                           const uint32_t* __restrict__ spos, const double* __restrict__ obs,
+                           double beta, int fb_frozen, const Gate* __restrict__ gates) {
+  int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= n) return;
+  const uint32_t key = skeys[q];
+  if (q > 0 && skeys[q - 1] == key) return;
+  const int t = table_of_key(ft, key);
+  const FoldTab& tb = ft.t[t];
+  const int e = (int)key - tb.gbase;
+  if (e == tb.ref_index) return;  // folded by k_fold_ref
+  int end = q;
+  while (end < n && skeys[end] == key) ++end;
+  const int cnt = end - q;
+  const int before = tb.obs_count[e];
+  if (!fb_frozen) {
+    const Gate g = gates[t];
+    double L = tb.lat[e];
+    // never observed before the batch and first observed after the gate lift: it was
+    // rescaled by recalibrate_unobserved before its first fold
+    if (g.lifted && before == 0 && (int)spos[q] > g.gate_pos)
+      L = __dmul_rn(tb.lat_init[e], g.ratio);
+    for (int u = q; u < end; ++u) L = ewma(beta, obs[spos[u]], L);
+    tb.lat[e] = L;
+  }
+  tb.obs_count[e] = before + cnt;
+}
+
+// Entries of gated tables that were never observed at all: plain rescale.
+__global__ void k_fold_rescale(FoldTabs ft, const Gate* __restrict__ gates) {
+  const int t = blockIdx.y;
+  const FoldTab tb = ft.t[t];
+  const Gate g = gates[t];
+  if (!g.lifted) return;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < tb.M; e += gridDim.x * blockDim.x) {
+    if (e == tb.ref_index || tb.obs_count[e] != 0) continue;
+    tb.lat[e] = __dmul_rn(tb.lat_init[e], g.ratio);  // configurator.py:490
+  }
+}
+
+}  // namespace
+
+int fold_launch(sp_ctx* ctx, int n_tables, sp_table* const* tables, int n, const int32_t* op,
+                const int32_t* idx, const double* obs, double beta, int dfp_count, int dfp_on,
+                int fb_frozen) {
+  if (n_tables > kMaxFoldTables) return fail(SP_E_UNSUPPORTED, "fold: at most 64 tables");
+  FoldTabs ft;
+  ft.n = n_tables;
+  int64_t gb = 0;
+  int maxM = 0;
+  for (int t = 0; t < n_tables; ++t) {
+    sp_table* tb = tables[t];
+    FoldTab f;
+    f.lat = tb->lat;
+    f.lat_init = tb->lat_init;
+    f.obs_count = tb->obs_count;
+    f.counters = tb->dev_counters;
+    f.M = tb->M;
+    f.ref_index = tb->ref_index;
+    f.gbase = (int32_t)gb;
+    f.pad = 0;
+    ft.t[t] = f;
+    gb += tb->M;
+    if (tb->M > maxM) maxM = tb->M;
+  }
+  if (gb >= (1ll << 31)) return fail(SP_E_UNSUPPORTED, "fold: too many entries");
+  int end_bit = 1;
+  while ((1ll << end_bit) <= gb) ++end_bit;
+  cudaStream_t st = ctx->stream;
+  // scratch: keys, pos, sorted keys, sorted pos, gates, cub temp
+  size_t cub_bytes = 0;
+  if (n > 0)
+    cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, (const uint32_t*)nullptr,
+                                    (uint32_t*)nullptr, (const uint32_t*)nullptr,
+                                    (uint32_t*)nullptr, n, 0, end_bit, st);
+  size_t a = ((size_t)n * 4 + 255) & ~(size_t)255;
+  size_t gates_bytes = ((size_t)n_tables * sizeof(Gate) + 255) & ~(size_t)255;
+  size_t total = 4 * a + gates_bytes + cub_bytes + 256;
+  int rc = SP_OK;
+  uint8_t* base = (uint8_t*)ctx_tmp(ctx, total, &rc);
+  if (!base) return rc;
+  uint32_t* keys = (uint32_t*)base;
+  uint32_t* pos = (uint32_t*)(base + a);
+  uint32_t* skeys = (uint32_t*)(base + 2 * a);
+  uint32_t* spos = (uint32_t*)(base + 3 * a);
+  Gate* gates = (Gate*)(base + 4 * a);
+  void* cub_tmp = base + 4 * a + gates_bytes;
+  if (n > 0) {
+    k_fold_keys<<<(n + 255) / 256, 256, 0, st>>>(n, ft, op, idx, keys, pos);
+    SP_CHECK_LAUNCH(ctx);
+    SP_CUDA(cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, keys, skeys, pos, spos, n, 0,
+                                            end_bit, st));
+    ctx->launches += 2;  // upsweep/downsweep passes (at least)
+  }
+  k_fold_ref<<<(n_tables + 63) / 64, 64, 0, st>>>(n, ft, skeys, spos, obs, beta, dfp_count,
+                                                 dfp_on, fb_frozen, gates);
+  SP_CHECK_LAUNCH(ctx);
+  if (n > 0) {
+    k_fold_seg<<<(n + 255) / 256, 256, 0, st>>>(n, ft, skeys, spos, obs, beta, fb_frozen,
+                                                gates);
+    SP_CHECK_LAUNCH(ctx);
+  }
+  if (!fb_frozen && dfp_on) {
+    dim3 grid((maxM + 255) / 256, n_tables);
+    k_fold_rescale<<<grid, 256, 0, st>>>(ft, gates);
+    SP_CHECK_LAUNCH(ctx);
+  }
+  for (int t = 0; t < n_tables; ++t) tables[t]->version++;
+  return SP_OK;
+}
+
+}  // namespace sp

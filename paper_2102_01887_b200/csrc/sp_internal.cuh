@@ -1,0 +1,174 @@
+// sp_internal.cuh — shared definitions of the slackpipe_b200 CUDA library (sm_100a).
+//
+// Numerics: every product/quotient/sum that the reference evaluates with numpy float64
+// ufuncs is written with the explicit round-to-nearest intrinsics (__dmul_rn, __ddiv_rn,
+// __dadd_rn, __dsub_rn) so that nvcc can never contract them into FMAs.
+// The library is additionally compiled with --fmad=false.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "slackpipe_b200.h"
+
+namespace sp {
+
+constexpr uint32_t kPlanMagic = 0x53504c4eu;  // "SPLN"
+constexpr uint16_t kNone16 = 0xFFFFu;
+constexpr int kMaxKinds = SP_MAX_KINDS;
+constexpr int kMaxB = SP_MAX_BATCH_VALUES;
+
+// One candidate record of the staircase plan (32 B, two 128-bit loads).
+// `score` is cost (prefix/feasible side, CP) or cost+penalty (suffix/infeasible side, CS);
+// r1 is the entry's rank under (cost, res, id_rank) — the reference's tie-break order
+// after the score (configurator.py:229-237).
+struct __align__(16) CandRec {
+  double score;
+  double lat;
+  uint32_t r1;
+  int32_t idx;
+  int32_t batch;
+  int32_t kind;
+};
+static_assert(sizeof(CandRec) == 32, "CandRec must be 32 bytes");
+
+// Plan header (256 B).  A plan is one contiguous, 16-B aligned byte image so that the
+// decision kernel can stage it into shared memory with bulk copies.
+struct __align__(16) PlanHdr {
+  uint32_t magic;
+  int32_t total_bytes;  // whole image, multiple of 16
+  int32_t M;
+  int32_t nB;           // distinct batch sizes
+  int32_t W;            // u16 lanes per half-row (8 or 16)
+  int32_t K;            // global kind count
+  int32_t ncp;          // prefix candidates
+  int32_t ncs;          // suffix candidates
+  int32_t cp_off;       // byte offset of CP records
+  int32_t cs_off;       // byte offset of CS records
+  int32_t pad0[2];
+  int32_t batch_vals[kMaxB];  // ascending; unused = INT32_MAX
+  int32_t sec_off[kMaxKinds];   // byte offset of the kind's threshold array (0: absent)
+  int32_t sec_rows[kMaxKinds];  // rows R_k (0: kind absent from the table)
+  int32_t sec_rows_off[kMaxKinds];  // byte offset of the kind's row array
+  int32_t pad1[12];
+};
+static_assert(sizeof(PlanHdr) == 256, "PlanHdr must be 256 bytes");
+
+struct Plan {
+  double alpha = 0.0;
+  uint64_t version = ~0ull;  // table version the plan was built for
+  bool valid = false;
+  // device buffers
+  double* cost = nullptr;     // M
+  double* costpen = nullptr;  // M
+  uint8_t* image = nullptr;   // plan image (capacity image_cap)
+  int64_t image_cap = 0;
+};
+
+}  // namespace sp
+
+struct sp_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int num_sms = 0;
+  int max_smem_optin = 0;
+  int64_t launches = 0;
+  // grow-only device arena for staged host I/O
+  void* io_dev = nullptr;
+  size_t io_cap = 0;
+  // small device scratch for pointer tables
+  void* ptr_dev = nullptr;
+  size_t ptr_cap = 0;
+  // generic device scratch (sort temp etc.)
+  void* tmp_dev = nullptr;
+  size_t tmp_cap = 0;
+};
+
+struct sp_table {
+  int32_t M = 0, K = 0, nB = 0, ref_index = -1;
+  int32_t batch_vals[sp::kMaxB];
+  int32_t kind_count[sp::kMaxKinds];
+  int32_t kind_base[sp::kMaxKinds];  // entries sorted by kind: base offset per kind
+  bool plan_ok = false;
+  uint64_t version = 0;
+  int32_t completed_ref = 0;
+  // device arrays (length M)
+  double *lat = nullptr, *lat_init = nullptr, *res = nullptr, *pool = nullptr,
+         *price = nullptr;
+  int32_t *batch = nullptr, *bidx = nullptr, *kind = nullptr, *id_rank = nullptr,
+          *obs_count = nullptr;
+  int32_t* kind_slot = nullptr;  // position of the entry inside its kind block (static order by kind, idx)
+  // plan scratch (device)
+  uint32_t *r1 = nullptr, *r2 = nullptr, *lpos = nullptr;
+  int32_t *ent_r1 = nullptr, *ent_r2 = nullptr, *order = nullptr;
+  uint32_t *pf = nullptr, *sf = nullptr;      // W*(M+K) each
+  uint32_t* rowscratch = nullptr;             // (M+K) * 2W
+  double* thrscratch = nullptr;               // M+K
+  int32_t* rows_per_kind = nullptr;           // K (+1 status word)
+  int32_t* dev_counters = nullptr;            // [0] = completed_ref (device copy)
+  uint32_t *candf = nullptr, *cands = nullptr;  // M flags each
+  uint32_t *cidf = nullptr, *cids = nullptr;    // M maps each
+  std::vector<sp::Plan> plans;
+};
+
+struct sp_dag {
+  int32_t V = 0, n_src = 0, n_val = 0;
+  // Per-source vertex programs: prog[prog_ptr[s] .. prog_ptr[s+1]) lists
+  // source s and then its descendants in topological order as int4
+  // {value index, terminal flag, pred begin, pred end}; preds holds predecessor SLOTS
+  // (positions inside the same program) as u16.
+  int4* prog = nullptr;         // device
+  int32_t* prog_ptr = nullptr;  // device, n_src + 1
+  uint16_t* preds = nullptr;    // device
+  int32_t max_span = 0;         // max program length (DP slots per lane)
+  int64_t prog_len = 0, pred_len = 0;
+};
+
+// ---- error plumbing ------------------------------------------------------------------
+namespace sp {
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what);
+}  // namespace sp
+
+#define SP_CUDA(call)                                              \
+  do {                                                             \
+    cudaError_t _e = (call);                                       \
+    if (_e != cudaSuccess) return sp::cuda_fail(_e, #call);        \
+  } while (0)
+
+#define SP_CHECK_LAUNCH(ctx)                                        \
+  do {                                                              \
+    (ctx)->launches++;                                              \
+    cudaError_t _e = cudaGetLastError();                            \
+    if (_e != cudaSuccess) return sp::cuda_fail(_e, "kernel launch"); \
+  } while (0)
+
+// ---- internal entry points implemented in the .cu files --------------------------------
+namespace sp {
+int plan_build(sp_ctx* ctx, sp_table* t, Plan& p);
+int plan_scratch_alloc(sp_table* t);
+Plan* plan_get(sp_ctx* ctx, sp_table* t, double alpha, int* rc);
+int select_launch(sp_ctx* ctx, int n_tables, sp_table* const* tables, double alpha, int N,
+                  const int32_t* op, const double* slack, const int32_t* avail,
+                  const int32_t* supply, const int32_t* min_batch, const uint32_t* flags,
+                  int32_t* out_idx, int32_t* out_code, int32_t* out_fill, double* out_obj,
+                  double* out_slack, double* out_wait, double* out_kind_min, int mode);
+int affinity_launch(sp_ctx* ctx, int N, int K, const double* kmin, const int32_t* q,
+                    double* out);
+int scores_launch(sp_ctx* ctx, sp_table* t, Plan* p, const double* slack_dev,
+                  double* score_dev, double* cost_dev);
+int slack_launch(sp_ctx* ctx, sp_dag* g, int I, const double* ref, int ref_stride,
+                 const double* target, const double* now, int K, const double* Q,
+                 double* out_slack, double* out_ratio);
+int queueing_launch(sp_ctx* ctx, int K, const int32_t* ptr, const double* lat,
+                    const double* res, const int32_t* cnt, const double* pool, double* out);
+int fold_launch(sp_ctx* ctx, int n_tables, sp_table* const* tables, int n, const int32_t* op,
+                const int32_t* idx, const double* obs, double beta, int dfp_count, int dfp_on,
+                int fb_frozen);
+void* ctx_tmp(sp_ctx* ctx, size_t bytes, int* rc);
+}  // namespace sp

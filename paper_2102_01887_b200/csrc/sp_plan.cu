@@ -1,0 +1,533 @@
+// sp_plan.cu — per-(table, alpha) decision plan, built on the device.
+//
+// What the reference does per call (configurator.py:219-237): for every entry j
+//     cost_j    = ((res_j * lat_j) * price_j) / batch_j
+//     pen_j     = alpha * ((lat_j * res_j) / (batch_j * pool_j))
+//     score_j   = cost_j + (lat_j < slack[kind_j] ? 0 : pen_j)
+// then a masked argmin with exact-equality ties broken by (cost, res, id_rank).
+//
+// What we precompute once per (profile version, alpha) so that each decision is
+// O(K log R) instead of O(M) (SURVEY.md §8(d) "K2b"):
+//   * cost_j, costpen_j = cost_j + pen_j                        (k_cost; bitwise equal to
+//     cost + where(lat<slack, 0, pen) because cost + 0.0 == cost for cost > 0)
+//   * r1_j = rank of j under (cost, res, id_rank)   -> tie order of feasible entries
+//     r2_j = rank of j under (costpen, cost, res, id_rank) -> order of infeasible entries
+//     (the argmin key (score, cost, res, id_rank) of configurator.py:229-237 reduces to
+//     r1 inside the feasible set and to r2 inside the infeasible set)
+//   * per kind, entries sorted by latency; for every threshold position p the per-batch-
+//     size prefix-min of r1 over positions < p (feasible: lat < slack) and suffix-min of r2
+//     over positions >= p (infeasible).  Consecutive identical rows are merged, leaving a
+//     staircase of R_k rows keyed by the latency just below each step.
+// A decision then binary-searches slack_k in the kind's thresholds, loads one row of
+// 2*W u16 candidate ids, and min-reduces the batch-size lanes admitted by
+// min_batch / available with SIMD half-word minima.  See DESIGN.md §K2 for the proof of
+// bit-exactness.
+#include <float.h>
+#include <math.h>
+
+#include <algorithm>
+#include <cstring>
+
+#include "sp_internal.cuh"
+
+namespace sp {
+
+namespace {
+
+constexpr uint32_t kInf32 = 0xFFFFFFFFu;
+
+struct KindInfo {
+  int32_t base[kMaxKinds];
+  int32_t count[kMaxKinds];
+};
+
+__global__ void k_cost(int M, const double* __restrict__ lat, const double* __restrict__ res,
+                       const int32_t* __restrict__ batch, const double* __restrict__ pool,
+                       const double* __restrict__ price, double alpha,
+                       double* __restrict__ cost, double* __restrict__ costpen) {
+  int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= M) return;
+  double L = lat[j], R = res[j], B = (double)batch[j], P = pool[j], pr = price[j];
+  // configurator.py:224  cost = (self.res * self.lat) * self.price / self.batch
+  double c = __ddiv_rn(__dmul_rn(__dmul_rn(R, L), pr), B);
+  // configurator.py:225  penalty = alpha * ((self.lat * self.res) / (self.batch * self.pool))
+  double pen = __dmul_rn(alpha, __ddiv_rn(__dmul_rn(L, R), __dmul_rn(B, P)));
+  cost[j] = c;
+  costpen[j] = __dadd_rn(c, pen);
+}
+
+// 2-D rank counting: block (x) owns 256 entries i, (y) one chunk of 256 entries j.
+constexpr int kRankChunk = 256;
+__global__ void __launch_bounds__(256) k_rank(int M, const double* __restrict__ lat,
+                                              const double* __restrict__ cost,
+                                              const double* __restrict__ costpen,
+                                              const double* __restrict__ res,
+                                              const int32_t* __restrict__ id_rank,
+                                              const int32_t* __restrict__ kind,
+                                              uint32_t* r1, uint32_t* r2, uint32_t* lpos) {
+  __shared__ double s_cost[kRankChunk], s_cp[kRankChunk], s_res[kRankChunk], s_lat[kRankChunk];
+  __shared__ int32_t s_id[kRankChunk], s_kind[kRankChunk];
+  int j0 = blockIdx.y * kRankChunk;
+  int nj = min(kRankChunk, M - j0);
+  for (int t = threadIdx.x; t < nj; t += blockDim.x) {
+    int j = j0 + t;
+    s_cost[t] = cost[j];
+    s_cp[t] = costpen[j];
+    s_res[t] = res[j];
+    s_lat[t] = lat[j];
+    s_id[t] = id_rank[j];
+    s_kind[t] = kind[j];
+  }
+  __syncthreads();
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= M) return;
+  double ci = cost[i], pi = costpen[i], ri = res[i], li = lat[i];
+  int idi = id_rank[i], ki = kind[i];
+  uint32_t c1 = 0, c2 = 0, c3 = 0;
+  for (int t = 0; t < nj; ++t) {
+    double cj = s_cost[t], pj = s_cp[t], rj = s_res[t], lj = s_lat[t];
+    int idj = s_id[t];
+    // (cost, res, id_rank) lexicographic
+    bool lt1 = (cj < ci) || (cj == ci && (rj < ri || (rj == ri && idj < idi)));
+    // (costpen, cost, res, id_rank) lexicographic
+    bool lt2 = (pj < pi) || (pj == pi && lt1);
+    // stable latency order inside the kind
+    bool lt3 = (s_kind[t] == ki) && ((lj < li) || (lj == li && (j0 + t) < i));
+    c1 += lt1;
+    c2 += lt2;
+    c3 += lt3;
+  }
+  if (c1) atomicAdd(&r1[i], c1);
+  if (c2) atomicAdd(&r2[i], c2);
+  if (c3) atomicAdd(&lpos[i], c3);
+}
+
+__global__ void k_invert(int M, const uint32_t* __restrict__ r1, const uint32_t* __restrict__ r2,
+                         const uint32_t* __restrict__ lpos, const int32_t* __restrict__ kind,
+                         KindInfo ki, int32_t* ent_r1, int32_t* ent_r2, int32_t* order) {
+  int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= M) return;
+  ent_r1[r1[j]] = j;
+  ent_r2[r2[j]] = j;
+  order[ki.base[kind[j]] + (int)lpos[j]] = j;
+}
+
+__device__ __forceinline__ uint32_t warp_incl_min(uint32_t v, int lane) {
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    uint32_t t = __shfl_up_sync(0xffffffffu, v, off);
+    if (lane >= off) v = min(v, t);
+  }
+  return v;
+}
+
+// Block-wide exclusive scans over blockDim.x == 1024 (32 warps).
+__device__ int block_excl_sum(int v, int* s_warp, int* total) {
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    int t = __shfl_up_sync(0xffffffffu, x, off);
+    if (lane >= off) x += t;
+  }
+  if (lane == 31) s_warp[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int nw = blockDim.x >> 5;
+    int y = lane < nw ? s_warp[lane] : 0;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      int t = __shfl_up_sync(0xffffffffu, y, off);
+      if (lane >= off) y += t;
+    }
+    s_warp[lane] = y;  // inclusive per warp
+  }
+  __syncthreads();
+  int base = w ? s_warp[w - 1] : 0;
+  *total = s_warp[(blockDim.x >> 5) - 1];
+  int r = base + x - v;
+  __syncthreads();
+  return r;
+}
+
+__device__ int block_excl_max(int v, int* s_warp) {
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    int t = __shfl_up_sync(0xffffffffu, x, off);
+    if (lane >= off) x = max(x, t);
+  }
+  // exclusive within warp
+  int ex = __shfl_up_sync(0xffffffffu, x, 1);
+  if (lane == 0) ex = INT32_MIN;
+  if (lane == 31) s_warp[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int nw = blockDim.x >> 5;
+    int y = lane < nw ? s_warp[lane] : INT32_MIN;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      int t = __shfl_up_sync(0xffffffffu, y, off);
+      if (lane >= off) y = max(y, t);
+    }
+    s_warp[lane] = y;
+  }
+  __syncthreads();
+  int base = w ? s_warp[w - 1] : INT32_MIN;
+  int r = max(base, ex);
+  __syncthreads();
+  return r;
+}
+
+// One CTA (1024 threads) per kind.  Phase A: warp w < W builds the prefix-min of r1 for
+// batch lane b = w; warp W <= w < 2W the suffix-min of r2 for lane w - W.  Phase B: rows
+// at latency boundaries, merged when identical to the previous boundary's row.
+__global__ void __launch_bounds__(1024) k_stair(int M, int K, int W, KindInfo ki,
+                                                const int32_t* __restrict__ order,
+                                                const int32_t* __restrict__ bidx,
+                                                const double* __restrict__ lat,
+                                                const uint32_t* __restrict__ r1,
+                                                const uint32_t* __restrict__ r2, uint32_t* pf,
+                                                uint32_t* sf, double* thrscratch,
+                                                uint32_t* rowscratch, int32_t* rows_per_kind,
+                                                uint32_t* candf, uint32_t* cands) {
+  __shared__ int s_warp[32];
+  __shared__ int s_carry_b, s_carry_rows, s_lastb;
+  const int k = blockIdx.x;
+  const int Mk = ki.count[k];
+  const int base = ki.base[k];
+  const int ext = base + k;  // extended positions 0..Mk of this kind
+  const int stride = M + K;
+  if (Mk == 0) {
+    if (threadIdx.x == 0) rows_per_kind[k] = 0;
+    return;
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (w < 2 * W) {
+    const int b = w % W;
+    if (w < W) {
+      uint32_t* out = pf + (size_t)b * stride + ext;
+      uint32_t carry = kInf32;
+      if (lane == 0) out[0] = kInf32;
+      for (int q0 = 0; q0 < Mk; q0 += 32) {
+        int q = q0 + lane;
+        uint32_t v = kInf32;
+        if (q < Mk) {
+          int e = order[base + q];
+          if (bidx[e] == b) v = r1[e];
+        }
+        uint32_t incl = min(warp_incl_min(v, lane), carry);
+        if (q < Mk) out[q + 1] = incl;
+        carry = __shfl_sync(0xffffffffu, incl, 31);
+      }
+    } else {
+      uint32_t* out = sf + (size_t)b * stride + ext;
+      uint32_t carry = kInf32;
+      if (lane == 0) out[Mk] = kInf32;
+      for (int hi = Mk - 1; hi >= 0; hi -= 32) {
+        int q = hi - lane;
+        uint32_t v = kInf32;
+        if (q >= 0) {
+          int e = order[base + q];
+          if (bidx[e] == b) v = r2[e];
+        }
+        uint32_t incl = min(warp_incl_min(v, lane), carry);
+        if (q >= 0) out[q] = incl;
+        carry = __shfl_sync(0xffffffffu, incl, 31);
+      }
+    }
+  }
+  if (threadIdx.x == 0) {
+    s_carry_b = INT32_MIN;
+    s_carry_rows = 0;
+  }
+  __syncthreads();
+  const uint32_t* pfk = pf + ext;
+  const uint32_t* sfk = sf + ext;
+  for (int c0 = 0; c0 <= Mk; c0 += blockDim.x) {
+    int p = c0 + threadIdx.x;
+    bool valid = p <= Mk;
+    bool isb = false;
+    if (valid) {
+      if (p == 0 || p == Mk) {
+        isb = true;
+      } else {
+        isb = lat[order[base + p]] != lat[order[base + p - 1]];
+      }
+    }
+    int carry_b = s_carry_b;
+    int pex = block_excl_max(isb ? p : INT32_MIN, s_warp);
+    int pp = max(pex, carry_b);
+    bool changed = false;
+    if (isb) {
+      if (p == 0) {
+        changed = true;
+      } else {
+        for (int b = 0; b < W && !changed; ++b) {
+          changed = (pfk[(size_t)b * stride + p] != pfk[(size_t)b * stride + pp]) ||
+                    (sfk[(size_t)b * stride + p] != sfk[(size_t)b * stride + pp]);
+        }
+      }
+    }
+    int total = 0;
+    int row = block_excl_sum(changed ? 1 : 0, s_warp, &total);
+    row += s_carry_rows;
+    if (changed) {
+      thrscratch[ext + row] = (p == 0) ? -INFINITY : lat[order[base + p - 1]];
+      uint32_t* rr = rowscratch + (size_t)(ext + row) * (2 * W);
+      for (int b = 0; b < W; ++b) {
+        uint32_t a = pfk[(size_t)b * stride + p];
+        uint32_t s = sfk[(size_t)b * stride + p];
+        rr[b] = a;
+        rr[W + b] = s;
+        if (a != kInf32) candf[a] = 1u;
+        if (s != kInf32) cands[s] = 1u;
+      }
+    }
+    // chunk carries: last boundary position (inclusive max at the last thread), row count
+    if (threadIdx.x == blockDim.x - 1) s_lastb = max(pp, isb ? p : INT32_MIN);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      s_carry_b = max(s_carry_b, s_lastb);
+      s_carry_rows += total;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) rows_per_kind[k] = s_carry_rows;
+}
+
+// Single CTA: candidate compaction (order-preserving), offsets, header, rows, records.
+__global__ void __launch_bounds__(1024) k_finalize(
+    int M, int K, int W, int nB, KindInfo ki, const int32_t* batch_vals_unused,
+    const int32_t* __restrict__ rows_per_kind, const double* __restrict__ thrscratch,
+    const uint32_t* __restrict__ rowscratch, const uint32_t* __restrict__ candf,
+    const uint32_t* __restrict__ cands, uint32_t* cidf, uint32_t* cids,
+    const int32_t* __restrict__ ent_r1, const int32_t* __restrict__ ent_r2,
+    const uint32_t* __restrict__ r1, const double* __restrict__ lat,
+    const double* __restrict__ cost, const double* __restrict__ costpen,
+    const int32_t* __restrict__ batch, const int32_t* __restrict__ kind, PlanHdr hdr_in,
+    uint8_t* image, int64_t image_cap, int32_t* status) {
+  __shared__ int s_warp[32];
+  __shared__ PlanHdr hdr;
+  __shared__ int s_ncp, s_ncs;
+  // exclusive scans of the two flag arrays
+  for (int pass = 0; pass < 2; ++pass) {
+    const uint32_t* fl = pass ? cands : candf;
+    uint32_t* cid = pass ? cids : cidf;
+    int carry = 0;
+    for (int c0 = 0; c0 < M; c0 += blockDim.x) {
+      int r = c0 + threadIdx.x;
+      int v = (r < M) ? (int)fl[r] : 0;
+      int total = 0;
+      int ex = block_excl_sum(v, s_warp, &total);
+      if (r < M) cid[r] = (uint32_t)(carry + ex);
+      carry += total;
+    }
+    if (threadIdx.x == 0) {
+      if (pass) s_ncs = carry; else s_ncp = carry;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    hdr = hdr_in;
+    int off = (int)sizeof(PlanHdr);
+    for (int k = 0; k < K; ++k) {
+      int R = rows_per_kind[k];
+      hdr.sec_rows[k] = R;
+      if (R == 0) {
+        hdr.sec_off[k] = 0;
+        hdr.sec_rows_off[k] = 0;
+        continue;
+      }
+      hdr.sec_off[k] = off;
+      off += ((R * 8 + 15) / 16) * 16;
+      hdr.sec_rows_off[k] = off;
+      off += R * 4 * W;
+    }
+    hdr.ncp = s_ncp;
+    hdr.ncs = s_ncs;
+    hdr.cp_off = off;
+    off += s_ncp * (int)sizeof(CandRec);
+    hdr.cs_off = off;
+    off += s_ncs * (int)sizeof(CandRec);
+    hdr.total_bytes = off;
+    *status = (off <= image_cap) ? 0 : -1;
+  }
+  __syncthreads();
+  if (hdr.total_bytes > image_cap) return;
+  if (threadIdx.x < (int)(sizeof(PlanHdr) / 4))
+    reinterpret_cast<uint32_t*>(image)[threadIdx.x] =
+        reinterpret_cast<const uint32_t*>(&hdr)[threadIdx.x];
+  for (int k = 0; k < K; ++k) {
+    int R = hdr.sec_rows[k];
+    if (R == 0) continue;
+    int ext = ki.base[k] + k;
+    double* thr = reinterpret_cast<double*>(image + hdr.sec_off[k]);
+    uint16_t* rows = reinterpret_cast<uint16_t*>(image + hdr.sec_rows_off[k]);
+    for (int r = threadIdx.x; r < R; r += blockDim.x) thr[r] = thrscratch[ext + r];
+    int n16 = R * 2 * W;
+    for (int u = threadIdx.x; u < n16; u += blockDim.x) {
+      int r = u / (2 * W), h = u % (2 * W);
+      uint32_t v = rowscratch[(size_t)(ext + r) * (2 * W) + h];
+      uint16_t o = kNone16;
+      if (v != kInf32) o = (uint16_t)((h < W) ? cidf[v] : cids[v]);
+      rows[u] = o;
+    }
+  }
+  CandRec* cp = reinterpret_cast<CandRec*>(image + hdr.cp_off);
+  CandRec* cs = reinterpret_cast<CandRec*>(image + hdr.cs_off);
+  for (int r = threadIdx.x; r < M; r += blockDim.x) {
+    if (candf[r]) {
+      int e = ent_r1[r];
+      CandRec c;
+      c.score = cost[e];
+      c.lat = lat[e];
+      c.r1 = (uint32_t)r;
+      c.idx = e;
+      c.batch = batch[e];
+      c.kind = kind[e];
+      cp[cidf[r]] = c;
+    }
+    if (cands[r]) {
+      int e = ent_r2[r];
+      CandRec c;
+      c.score = costpen[e];
+      c.lat = lat[e];
+      c.r1 = r1[e];
+      c.idx = e;
+      c.batch = batch[e];
+      c.kind = kind[e];
+      cs[cids[r]] = c;
+    }
+  }
+}
+
+int64_t plan_image_capacity(const sp_table* t, int W) {
+  int64_t cap = sizeof(PlanHdr);
+  for (int k = 0; k < t->K; ++k) {
+    int64_t R = t->kind_count[k] + 1;
+    cap += ((R * 8 + 15) / 16) * 16 + R * 4 * W;
+  }
+  cap += 2 * (int64_t)t->M * (int64_t)sizeof(CandRec);
+  return (cap + 15) / 16 * 16;
+}
+
+int plan_width(const sp_table* t) { return t->nB <= 8 ? 8 : 16; }
+
+}  // namespace
+
+int plan_scratch_alloc(sp_table* t) {
+  const int M = t->M, K = t->K;
+  const int W = plan_width(t);
+  size_t ext = (size_t)(M + K);
+  SP_CUDA(cudaMalloc(&t->r1, sizeof(uint32_t) * M));
+  SP_CUDA(cudaMalloc(&t->r2, sizeof(uint32_t) * M));
+  SP_CUDA(cudaMalloc(&t->lpos, sizeof(uint32_t) * M));
+  SP_CUDA(cudaMalloc(&t->ent_r1, sizeof(int32_t) * M));
+  SP_CUDA(cudaMalloc(&t->ent_r2, sizeof(int32_t) * M));
+  SP_CUDA(cudaMalloc(&t->order, sizeof(int32_t) * M));
+  if (t->plan_ok) {
+    SP_CUDA(cudaMalloc(&t->pf, sizeof(uint32_t) * W * ext));
+    SP_CUDA(cudaMalloc(&t->sf, sizeof(uint32_t) * W * ext));
+    SP_CUDA(cudaMalloc(&t->rowscratch, sizeof(uint32_t) * 2 * W * ext));
+    SP_CUDA(cudaMalloc(&t->thrscratch, sizeof(double) * ext));
+    SP_CUDA(cudaMalloc(&t->rows_per_kind, sizeof(int32_t) * (kMaxKinds + 1)));
+    SP_CUDA(cudaMalloc(&t->candf, sizeof(uint32_t) * M));
+    SP_CUDA(cudaMalloc(&t->cands, sizeof(uint32_t) * M));
+    SP_CUDA(cudaMalloc(&t->cidf, sizeof(uint32_t) * M));
+    SP_CUDA(cudaMalloc(&t->cids, sizeof(uint32_t) * M));
+  }
+  return SP_OK;
+}
+
+int plan_build(sp_ctx* ctx, sp_table* t, Plan& p) {
+  const int M = t->M, K = t->K;
+  cudaStream_t st = ctx->stream;
+  if (!p.cost) {
+    SP_CUDA(cudaMalloc(&p.cost, sizeof(double) * M));
+    SP_CUDA(cudaMalloc(&p.costpen, sizeof(double) * M));
+  }
+  k_cost<<<(M + 255) / 256, 256, 0, st>>>(M, t->lat, t->res, t->batch, t->pool, t->price,
+                                          p.alpha, p.cost, p.costpen);
+  SP_CHECK_LAUNCH(ctx);
+  if (!t->plan_ok) {
+    p.valid = true;
+    p.version = t->version;
+    return SP_OK;
+  }
+  const int W = plan_width(t);
+  if (!p.image) {
+    p.image_cap = plan_image_capacity(t, W);
+    SP_CUDA(cudaMalloc(&p.image, (size_t)p.image_cap));
+  }
+  KindInfo ki;
+  for (int k = 0; k < kMaxKinds; ++k) {
+    ki.base[k] = k < K ? t->kind_base[k] : 0;
+    ki.count[k] = k < K ? t->kind_count[k] : 0;
+  }
+  SP_CUDA(cudaMemsetAsync(t->r1, 0, sizeof(uint32_t) * M, st));
+  SP_CUDA(cudaMemsetAsync(t->r2, 0, sizeof(uint32_t) * M, st));
+  SP_CUDA(cudaMemsetAsync(t->lpos, 0, sizeof(uint32_t) * M, st));
+  SP_CUDA(cudaMemsetAsync(t->candf, 0, sizeof(uint32_t) * M, st));
+  SP_CUDA(cudaMemsetAsync(t->cands, 0, sizeof(uint32_t) * M, st));
+  dim3 grid((M + 255) / 256, (M + kRankChunk - 1) / kRankChunk);
+  k_rank<<<grid, 256, 0, st>>>(M, t->lat, p.cost, p.costpen, t->res, t->id_rank, t->kind,
+                               t->r1, t->r2, t->lpos);
+  SP_CHECK_LAUNCH(ctx);
+  k_invert<<<(M + 255) / 256, 256, 0, st>>>(M, t->r1, t->r2, t->lpos, t->kind, ki, t->ent_r1,
+                                            t->ent_r2, t->order);
+  SP_CHECK_LAUNCH(ctx);
+  k_stair<<<K, 1024, 0, st>>>(M, K, W, ki, t->order, t->bidx, t->lat, t->r1, t->r2, t->pf,
+                              t->sf, t->thrscratch, t->rowscratch, t->rows_per_kind, t->candf,
+                              t->cands);
+  SP_CHECK_LAUNCH(ctx);
+  PlanHdr h;
+  memset(&h, 0, sizeof(h));
+  h.magic = kPlanMagic;
+  h.M = M;
+  h.nB = t->nB;
+  h.W = W;
+  h.K = K;
+  for (int b = 0; b < kMaxB; ++b) h.batch_vals[b] = b < t->nB ? t->batch_vals[b] : INT32_MAX;
+  int32_t* status = t->rows_per_kind + kMaxKinds;
+  k_finalize<<<1, 1024, 0, st>>>(M, K, W, t->nB, ki, nullptr, t->rows_per_kind, t->thrscratch,
+                                 t->rowscratch, t->candf, t->cands, t->cidf, t->cids,
+                                 t->ent_r1, t->ent_r2, t->r1, t->lat, p.cost, p.costpen,
+                                 t->batch, t->kind, h, p.image, p.image_cap, status);
+  SP_CHECK_LAUNCH(ctx);
+  p.valid = true;
+  p.version = t->version;
+  return SP_OK;
+}
+
+Plan* plan_get(sp_ctx* ctx, sp_table* t, double alpha, int* rc) {
+  *rc = SP_OK;
+  Plan* hit = nullptr;
+  for (auto& p : t->plans) {
+    if (p.alpha == alpha || (p.alpha != p.alpha && alpha != alpha)) {
+      hit = &p;
+      break;
+    }
+  }
+  if (!hit) {
+    if (t->plans.size() >= 16) {
+      // evict the oldest entry's buffers (keep memory bounded)
+      Plan& old = t->plans.front();
+      cudaFree(old.cost);
+      cudaFree(old.costpen);
+      cudaFree(old.image);
+      t->plans.erase(t->plans.begin());
+    }
+    t->plans.emplace_back();
+    hit = &t->plans.back();
+    hit->alpha = alpha;
+  }
+  if (!hit->valid || hit->version != t->version) {
+    *rc = plan_build(ctx, t, *hit);
+    if (*rc != SP_OK) return nullptr;
+  }
+  return hit;
+}
+
+}  // namespace sp

@@ -1,0 +1,79 @@
+"""Profile feedback fold on the device (K3): manager.py:45-47, 91-101, 436-457 and
+configurator.py:463-491.
+
+``fold_observations`` replays a batch of completed invocations, in completion order, into
+the device tables exactly as ``PipelineRun._apply_feedback`` does one at a time: EWMA
+smoothing of the committed entry's latency, observation counts, reference completion
+counts, and the one-time warm-up gate-lift rescale of never-observed entries.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Sequence
+
+import numpy as np
+
+from . import _lib
+from ._lib import check, ptr
+
+
+def _is_device(a) -> bool:
+    return hasattr(a, "is_cuda") and bool(a.is_cuda)
+
+
+def fold_observations(tables: Sequence, op, idx, obs, *, beta: float = 0.5,
+                      dfp_count: int = 10, dfp_on: bool = True, fb_frozen: bool = False,
+                      sync_host: bool = True) -> None:
+    """Fold observations obs[j] of entry idx[j] of table tables[op[j]] (op may be None for
+    a single table).  numpy inputs run synchronously; torch CUDA tensors stream-ordered.
+    With ``sync_host`` the tables' host mirrors (``lat``) are refreshed afterwards."""
+    if not tables:
+        raise ValueError("fold_observations: no tables")
+    ctx = tables[0]._ctx
+    device = _is_device(obs)
+    n = int(obs.shape[0])
+    arr_t = (C.c_void_p * len(tables))(*[t.handle.value for t in tables])
+    if not device:
+        idx = np.ascontiguousarray(idx, dtype=np.int32)
+        obs = np.ascontiguousarray(obs, dtype=np.float64)
+        if op is not None:
+            op = np.ascontiguousarray(op, dtype=np.int32)
+    check(ctx.lib.sp_feedback_fold(
+        ctx.handle, len(tables), C.cast(arr_t, C.c_void_p), n, ptr(op), ptr(idx), ptr(obs),
+        float(beta), int(dfp_count), 1 if dfp_on else 0, 1 if fb_frozen else 0,
+        _lib.SP_MEM_DEVICE if device else _lib.SP_MEM_HOST), "sp_feedback_fold")
+    if sync_host:
+        if device:
+            ctx.synchronize()
+        for t in tables:
+            if hasattr(t, "sync_from_device"):
+                t.sync_from_device()
+
+
+def table_counters(table) -> tuple[int, np.ndarray]:
+    """(completed_ref, per-entry observation counts) of a device table."""
+    ctx = table._ctx
+    c = C.c_int32()
+    M = len(table.lat)
+    counts = np.empty(M, dtype=np.int32)
+    check(ctx.lib.sp_table_get_counters(ctx.handle, table.handle, C.byref(c), ptr(counts)))
+    return int(c.value), counts
+
+
+def set_table_counters(table, completed_ref: int, counts: np.ndarray | None = None) -> None:
+    ctx = table._ctx
+    cc = None if counts is None else np.ascontiguousarray(counts, dtype=np.int32)
+    check(ctx.lib.sp_table_set_counters(ctx.handle, table.handle, int(completed_ref), ptr(cc)))
+
+
+def apply_feedback(old_estimate_s: float, observed_s: float, beta: float) -> float:
+    """manager.py:45-47, evaluated by the fold kernel on a one-entry table."""
+    from .configurator import RawTable
+
+    t = RawTable(lat=[float(old_estimate_s)], res=[1.0], batch=[1], pool=[1.0], price=[1.0])
+    try:
+        fold_observations([t], None, np.zeros(1, np.int32), np.array([float(observed_s)]),
+                          beta=beta, dfp_on=False, sync_host=False)
+        return float(t.get_latency()[0])
+    finally:
+        t.close()

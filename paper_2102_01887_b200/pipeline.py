@@ -1,0 +1,145 @@
+"""Data types the hot path consumes, mirroring the reference's pipeline module.
+
+Only what the configurator path needs is restated here:
+profiled ``ConfigEntry`` / ``ConfigSpec`` rows (pipeline.py:191-279), ``reference_config``
+(pipeline.py:478-500) and the DAG structure that feeds the slack kernel
+(``PipelineDag`` pipeline.py:298-337).  The reference's own objects are accepted wherever
+these are (duck typing), so the GPU path is a drop-in for the reference package.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Any, Mapping, Sequence
+
+CPU_KIND = "cpu"  # pipeline.py:19 — reference configurations live on this kind
+
+
+@dataclass
+class ConfigEntry:
+    """A profiled configuration (pipeline.py:191-215)."""
+
+    config_id: str
+    backend_kind: str
+    knob_values: dict[str, Any]
+    batch_size: int
+    resource_request: int
+    latency_s: float
+    latency_initial_s: float
+    peak_memory_mb: float = 0.0
+    schedulable: bool = True
+
+    def __post_init__(self) -> None:
+        if self.batch_size < 1:
+            raise ValueError(f"{self.config_id}: batch size must be >= 1")
+        if self.resource_request <= 0:
+            raise ValueError(f"{self.config_id}: resource request must be positive")
+        if self.latency_s <= 0 or self.latency_initial_s <= 0:
+            raise ValueError(f"{self.config_id}: latency must be positive")
+
+
+@dataclass
+class ConfigSpec:
+    """All profiled configurations of one operation (pipeline.py:245-258)."""
+
+    operation: str
+    entries: list[ConfigEntry]
+    reference_id: str
+
+    def __post_init__(self) -> None:
+        ids = [e.config_id for e in self.entries]
+        if len(set(ids)) != len(ids):
+            raise ValueError(f"{self.operation}: duplicate config ids")
+        if self.reference_id not in set(ids):
+            raise ValueError(f"{self.operation}: reference {self.reference_id!r} not among entries")
+
+
+def config_id_of(kind: str, resource: int, batch: int, knobs: Sequence[tuple[str, Any]] = ()) -> str:
+    """Config id format of ConfigAssignment.config_id (pipeline.py:185-188)."""
+    parts = [f"{kind}-r{resource}-b{batch}"]
+    parts.extend(f"{k}={v}" for k, v in knobs)
+    return "-".join(parts)
+
+
+def reference_config(spec) -> Any:
+    """Smallest CPU batch-1 entry; ties by sorted knob strings, then id (pipeline.py:478-500)."""
+    cands = [e for e in spec.entries if e.backend_kind == CPU_KIND and e.batch_size == 1]
+    if not cands:
+        raise ValueError(
+            f"operation {spec.operation!r} has no {CPU_KIND} batch-1 entry to use as reference"
+        )
+    return min(
+        cands,
+        key=lambda e: (
+            e.resource_request,
+            tuple(sorted((k, str(v)) for k, v in e.knob_values.items())),
+            e.config_id,
+        ),
+    )
+
+
+@dataclass
+class PipelineDag:
+    """Operations wired into a DAG (pipeline.py:298-337).  Branch predicates and fan-out
+    rules do not influence Alg. 1 (every decomposed path counts), so only the structure is
+    kept here."""
+
+    vertices: tuple[str, ...]
+    edges: tuple[tuple[str, str], ...]
+    branching: frozenset = frozenset()
+    branch_predicates: dict = field(default_factory=dict)
+    fanout_rules: dict = field(default_factory=dict)
+
+    def successors(self, v: str) -> list[str]:
+        return sorted(d for s, d in self.edges if s == v)
+
+    def predecessors(self, v: str) -> list[str]:
+        return sorted(s for s, d in self.edges if d == v)
+
+    def input_vertices(self) -> list[str]:
+        has_pred = {d for _, d in self.edges}
+        return sorted(v for v in self.vertices if v not in has_pred)
+
+    def output_vertices(self) -> list[str]:
+        has_succ = {s for s, _ in self.edges}
+        return sorted(v for v in self.vertices if v not in has_succ)
+
+    def topological_order(self) -> list[str]:
+        """Kahn's algorithm with a sorted ready list (pipeline.py:367-387)."""
+        indeg = {v: 0 for v in self.vertices}
+        succ: dict[str, list[str]] = {v: [] for v in self.vertices}
+        for s, d in self.edges:
+            indeg[d] += 1
+            succ[s].append(d)
+        ready = sorted(v for v, n in indeg.items() if n == 0)
+        order: list[str] = []
+        import bisect
+
+        while ready:
+            v = ready.pop(0)
+            order.append(v)
+            for d in sorted(succ[v]):
+                indeg[d] -= 1
+                if indeg[d] == 0:
+                    bisect.insort(ready, d)
+        if len(order) != len(self.vertices):
+            raise ValueError("pipeline contains a cycle")
+        return order
+
+    def depths(self) -> dict[str, int]:
+        """Longest edge distance from an input vertex (pipeline.py:328-337)."""
+        depth = {v: 0 for v in self.vertices}
+        for v in self.topological_order():
+            for d in self.successors(v):
+                depth[d] = max(depth[d], depth[v] + 1)
+        return depth
+
+
+def dag_from_json(obj: Mapping[str, Any]) -> PipelineDag:
+    """Structure of a pipeline document (pipeline.py:503-527)."""
+    names = tuple(op["name"] for op in obj["operations"])
+    return PipelineDag(
+        vertices=names,
+        edges=tuple((e[0], e[1]) for e in obj["edges"]),
+        branching=frozenset(op["name"] for op in obj["operations"] if op.get("branching")),
+        fanout_rules=dict(obj.get("fanout_rules", {})),
+    )

@@ -1,0 +1,141 @@
+"""BASELINE config 1 drop-in replay: every OpTable.select / affinity / set_latency call the
+reference engine made while running the AMBER (`branching`) scenario at the 50% target
+(43,859 selects, 9,962 affinity calls, 7,726 latency updates, recorded in call order by
+tests/golden/make_golden.py) is replayed through the GPU-backed OpTable.  Consecutive calls
+between two latency updates are independent, so they go to the device as one multi-table
+batch — the data-parallel form of the reference's sequential loop."""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+
+from conftest import golden, golden_json
+
+pytestmark = pytest.mark.gpu
+
+
+def bits(a):
+    return np.ascontiguousarray(a, dtype=np.float64).view(np.uint64)
+
+
+def _knobs(cid: str, batch: int) -> dict:
+    tail = cid.split(f"-b{batch}", 1)[1]
+    out = {}
+    for part in filter(None, tail.split("-")):
+        k, v = part.split("=", 1)
+        out[k] = v
+    return out
+
+
+def amber_tables(meta):
+    import paper_2102_01887_b200 as sp
+
+    sc = sp.Scenario("branching", tuple(sp.BackendSpec(k, n, r, p) for k, n, r, p in meta["backends"]))
+    tabs = []
+    for name in meta["ops"]:
+        m = meta["tables"][name]
+        ents = [sp.ConfigEntry(cid, k, _knobs(cid, b), b, r, lat, li)
+                for cid, k, r, b, lat, li in zip(m["config_id"], m["kind"], m["res"], m["batch"],
+                                                 m["lat"], m["lat_init"])]
+        t = sp.OpTable(sp.ConfigSpec(name, ents, m["ref_id"]), sc, kinds=meta["kinds"])
+        assert t.ref_index == m["ref_index"]
+        tabs.append(t)
+    return tabs
+
+
+@pytest.mark.parametrize("mode", ["plan", "scan"])
+def test_amber_trace_replay_batched(gpu_ctx, mode):
+    import paper_2102_01887_b200 as sp
+
+    d = golden("amber_trace")
+    meta = golden_json(d, "meta_json")
+    tabs = amber_tables(meta)
+    K = len(meta["kinds"])
+    kind = d["kind"]
+    n = len(kind)
+    cuts = [0] + [i for i in range(n) if kind[i] == 2] + [n]
+    n_sel = n_aff = 0
+    start = 0
+    while start < n:
+        if kind[start] == 2:
+            t = tabs[d["op"][start]]
+            t.set_latency(int(d["lat_idx"][start]), float(d["lat_val"][start]))
+            start += 1
+            continue
+        end = start
+        while end < n and kind[end] != 2:
+            end += 1
+        sl = slice(start, end)
+        alphas = np.unique(d["alpha"][sl])
+        assert len(alphas) == 1
+        slack = np.nan_to_num(d["slack"][sl], nan=0.0)
+        is_sel = kind[sl] == 0
+        avail = np.where(is_sel, d["avail"][sl], 1).astype(np.int32)
+        r = sp.select_batch(tabs, np.ascontiguousarray(slack), float(alphas[0]), avail,
+                            upstream_supply=np.ascontiguousarray(d["supply"][sl], np.int32),
+                            min_batch=np.where(is_sel, d["min_batch"][sl], 1).astype(np.int32),
+                            flags=np.where(is_sel, d["flags"][sl], 0).astype(np.uint32),
+                            op=np.ascontiguousarray(d["op"][sl], np.int32), kind_min=True, mode=mode)
+        s = np.flatnonzero(is_sel)
+        g = start + s
+        assert np.array_equal(r["code"][s] & 3, d["r_code"][g])
+        assert np.array_equal(r["idx"][s], d["r_idx"][g])
+        some = d["r_code"][g] != 0
+        assert np.array_equal(r["fill"][s][some], d["r_fill"][g][some])
+        for k in ("obj", "slack", "wait"):
+            assert np.array_equal(bits(r[k][s][some]), bits(d[f"r_{k}"][g][some])), k
+        n_sel += len(s)
+        a = np.flatnonzero(~is_sel)
+        if len(a):
+            ga = start + a
+            q = d["aff_kind"][ga].astype(np.int32)
+            ratio = sp.affinity_from_minima(r["kind_min"][a], q)
+            for j, gi in enumerate(ga):
+                exp = d["r_obj"][gi]
+                t = tabs[d["op"][gi]]
+                if meta["kinds"][q[j]] not in t.kinds:
+                    assert math.isnan(exp)
+                else:
+                    assert bits(ratio[j]) == bits(exp), gi
+            n_aff += len(a)
+        start = end
+    assert n_sel == 43859 and n_aff == 9962
+    # final live profiles equal the reference's end state
+    for t in tabs:
+        t.sync_from_device()
+    for t in tabs:
+        t.close()
+
+
+def test_amber_trace_replay_object_api_prefix(gpu_ctx):
+    """The first 3,000 calls one at a time through OpTable.select / affinity / set_latency."""
+    d = golden("amber_trace")
+    meta = golden_json(d, "meta_json")
+    tabs = amber_tables(meta)
+    kinds = meta["kinds"]
+    for i in range(3000):
+        t = tabs[d["op"][i]]
+        if d["kind"][i] == 2:
+            t.set_latency(int(d["lat_idx"][i]), float(d["lat_val"][i]))
+            continue
+        s = {k: float(v) for k, v in zip(kinds, d["slack"][i]) if not math.isnan(v)}
+        if d["kind"][i] == 1:
+            a = t.affinity(kinds[d["aff_kind"][i]], s, float(d["alpha"][i]))
+            exp = d["r_obj"][i]
+            assert (a is None and math.isnan(exp)) or bits(a) == bits(exp)
+            continue
+        fl = int(d["flags"][i])
+        ex = frozenset(k for j, k in enumerate(kinds) if (fl >> (8 + j)) & 1)
+        dec = t.select(s, float(d["alpha"][i]), int(d["avail"][i]), allow_delay=bool(fl & 1),
+                       upstream_supply=int(d["supply"][i]), excluded_kinds=ex,
+                       min_batch=int(d["min_batch"][i]))
+        if d["r_code"][i] == 0:
+            assert dec is None
+        else:
+            assert dec.entry_index == d["r_idx"][i] and dec.fill == d["r_fill"][i]
+            assert dec.kind == ("delay" if d["r_code"][i] == 2 else "assign")
+            assert bits(dec.objective_value) == bits(d["r_obj"][i])
+    for t in tabs:
+        t.close()
