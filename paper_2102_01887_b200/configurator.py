@@ -163,12 +163,14 @@ class OpTable:
         self.gkind = np.array([gpos[e.backend_kind] for e in entries], dtype=np.int32)
         self._ctx = get_context(device)
         lat_init = np.array([e.latency_initial_s for e in entries], dtype=np.float64)
+        batch32 = self.batch_int.astype(np.int32)  # kept alive across the call
+        rank32 = self.id_rank.astype(np.int32)
         h = C.c_void_p()
         check(
             self._ctx.lib.sp_table_create(
                 self._ctx.handle, n, ptr(self.lat), ptr(lat_init), ptr(self.res),
-                ptr(self.batch_int.astype(np.int32)), ptr(self.pool), ptr(self.price),
-                ptr(self.gkind), ptr(self.id_rank.astype(np.int32)), len(self.global_kinds),
+                ptr(batch32), ptr(self.pool), ptr(self.price),
+                ptr(self.gkind), ptr(rank32), len(self.global_kinds),
                 self.ref_index, C.byref(h)),
             "sp_table_create",
         )

@@ -39,6 +39,12 @@ def amber_tables(meta):
         ents = [sp.ConfigEntry(cid, k, _knobs(cid, b), b, r, lat, li)
                 for cid, k, r, b, lat, li in zip(m["config_id"], m["kind"], m["res"], m["batch"],
                                                  m["lat"], m["lat_init"])]
+        if m["ref_index"] < 0:
+            # reference sized beyond every instance (configurator.py:205-208): it anchors slack
+            # only; restore it as an unschedulable entry so reference_config finds it
+            res = int(m["ref_id"].split("-r", 1)[1].split("-", 1)[0])
+            ents.append(sp.ConfigEntry(m["ref_id"], "cpu", _knobs(m["ref_id"], 1), 1, res, 1.0, 1.0,
+                                       schedulable=False))
         t = sp.OpTable(sp.ConfigSpec(name, ents, m["ref_id"]), sc, kinds=meta["kinds"])
         assert t.ref_index == m["ref_index"]
         tabs.append(t)
