@@ -57,7 +57,8 @@ def workload_config(n_inv: int, M: int, mode: str, world: int) -> dict:
         "workload": "config2: 2^20 invocations x 4,096 configs per GPU "
                     "(sampling x variant x batch x cores/GPU-mem x {cpu,gpu}); SURVEY.md §8(d)",
         "invocations_per_gpu": n_inv, "configs": M, "kinds": K_KINDS, "alphas": list(ALPHAS),
-        "kernel": "k_select_plan (K2b staircase)" if mode == "plan" else "k_select_scan (K2a)",
+        "kernel": {"plan": "k_select_plan (K2b staircase)", "scan": "k_select_scan (K2a)",
+                   "auto": "k_select_plan (K2b staircase)"}.get(mode, "CPU: oracle restatement of OpTable.select"),
         "l2": "flushed between timed steps (256 MB write, outside the events)",
         "parallelism": f"replicated tables, invocations sharded, {world} GPU(s), no data-path collective",
     }
@@ -134,7 +135,7 @@ def cpu_baseline(target_s: float = 12.0) -> dict:
     t = optable.from_spec(spec, synth.synth_scenario(), ["cpu", "gpu"])
     M = len(t.lat)
     cores = os.cpu_count() or 1
-    inv = synth.synth_invocations(1 << 16, t.lat, t.gkind)
+    inv = synth.synth_invocations(1 << 20, t.lat, t.gkind)
     # calibrate on one core, then size the all-core sample for ~target_s
     t0 = time.perf_counter()
     optable.select_many([t], inv.slack, 100.0, inv.avail, inv.supply, inv.min_batch, inv.flags, None, 0, 200)

@@ -96,7 +96,7 @@ int sp_table_get_latency(sp_ctx* ctx, sp_table* t, double* out_lat);
 /* Build (or reuse) the per-alpha decision plan: cost/costpen precompute + staircase
  * index.  Called implicitly by the select entry points. */
 int sp_table_prepare(sp_ctx* ctx, sp_table* t, double alpha);
-/* 1 when the table's staircase plan is available (<= 16 distinct batch sizes, M < 65535). */
+/* 1 when the table's staircase plan is available (<= 16 distinct batch sizes, M < 32767). */
 int sp_table_plan_supported(const sp_table* t);
 /* Plan byte size for alpha after sp_table_prepare (synchronises); for DESIGN/bench. */
 int sp_table_plan_bytes(sp_ctx* ctx, sp_table* t, double alpha, int64_t* out_bytes);

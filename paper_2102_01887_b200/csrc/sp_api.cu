@@ -93,7 +93,9 @@ static void free_table(sp_table* t) {
   int32_t* ii[] = {t->batch, t->bidx, t->kind, t->id_rank, t->obs_count, t->kind_slot,
                    t->ent_r1, t->ent_r2, t->order, t->rows_per_kind, t->dev_counters};
   for (int32_t* p : ii) cudaFree(p);
-  uint32_t* uu[] = {t->r1, t->r2, t->lpos, t->pf, t->sf, t->rowscratch,
+  cudaFree(t->ukey);
+  cudaFree(t->uent);
+  uint32_t* uu[] = {t->ukr, t->umap, t->r1, t->r2, t->lpos, t->pf, t->sf, t->rowscratch,
                     t->candf, t->cands, t->cidf, t->cids};
   for (uint32_t* p : uu) cudaFree(p);
   for (auto& p : t->plans) {
@@ -191,7 +193,8 @@ int sp_table_create(sp_ctx* ctx, int32_t M, const double* lat, const double* lat
   t->K = K;
   t->ref_index = ref_index;
   t->nB = (int)bv.size();
-  t->plan_ok = t->nB <= kMaxB && M < 65535;
+  // unified candidate ids are u16: at most 2M - 1 < 65535 candidates
+  t->plan_ok = t->nB <= kMaxB && M < 32767;
   for (int b = 0; b < kMaxB; ++b) t->batch_vals[b] = b < t->nB ? bv[b] : INT32_MAX;
   std::vector<int32_t> bidx(M), kslot(M);
   for (int j = 0; j < M; ++j)

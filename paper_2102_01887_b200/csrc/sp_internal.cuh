@@ -21,41 +21,62 @@ constexpr uint16_t kNone16 = 0xFFFFu;
 constexpr int kMaxKinds = SP_MAX_KINDS;
 constexpr int kMaxB = SP_MAX_BATCH_VALUES;
 
-// One candidate record of the staircase plan (32 B, two 128-bit loads).
-// `score` is cost (prefix/feasible side, CP) or cost+penalty (suffix/infeasible side, CS);
-// r1 is the entry's rank under (cost, res, id_rank) — the reference's tie-break order
-// after the score (configurator.py:229-237).
+// One candidate record of the staircase plan (32 B).  Candidates live in ONE id space
+// ordered by the reference's argmin key (score, cost, res, id_rank) = (score, r1): the
+// feasible side of an entry carries score = cost, the infeasible side cost + penalty
+// (configurator.py:224-237).  The first 16 B hold what the decision always needs, the
+// second 16 B the winner's payload.
 struct __align__(16) CandRec {
   double score;
-  double lat;
-  uint32_t r1;
   int32_t idx;
+  int32_t feas;   // 1: feasible side (lat < slack), 0: penalized side
+  double lat;
   int32_t batch;
   int32_t kind;
 };
 static_assert(sizeof(CandRec) == 32, "CandRec must be 32 bytes");
 
-// Plan header (256 B).  A plan is one contiguous, 16-B aligned byte image so that the
-// decision kernel can stage it into shared memory with bulk copies.
+constexpr int kMaxBuckets = 4096;   // per-kind threshold buckets
+constexpr int kMaxLut = 4097;       // batch-lane lookup covers values 0..4096
+
+// Per-kind section descriptor (32 B, two broadcast 128-bit loads).
+struct __align__(16) KindDesc {
+  uint64_t kmin;       // order key of the smallest real threshold
+  int32_t thr_off;     // byte offset of the threshold array (R doubles, thr[0] = -inf)
+  int32_t rows_off;    // byte offset of the staircase rows (R x W u16)
+  int32_t bkt_off;     // byte offset of the bucket table (u32: lo | cnt << 16)
+  uint32_t nb1_shift;  // (buckets - 1) | shift << 16
+  int32_t R;           // rows (0: kind absent from the table)
+  int32_t pad;
+};
+static_assert(sizeof(KindDesc) == 32, "KindDesc must be 32 bytes");
+
+// Plan header (512 B).  A plan is one contiguous, 16-B aligned byte image so that the
+// decision kernel can stage it into shared memory with one bulk copy.
 struct __align__(16) PlanHdr {
   uint32_t magic;
   int32_t total_bytes;  // whole image, multiple of 16
   int32_t M;
   int32_t nB;           // distinct batch sizes
-  int32_t W;            // u16 lanes per half-row (8 or 16)
+  int32_t W;            // u16 lanes per row (8 or 16)
   int32_t K;            // global kind count
-  int32_t ncp;          // prefix candidates
-  int32_t ncs;          // suffix candidates
-  int32_t cp_off;       // byte offset of CP records
-  int32_t cs_off;       // byte offset of CS records
-  int32_t pad0[2];
+  int32_t ncp;          // feasible-side candidates
+  int32_t ncs;          // penalized-side candidates
+  int32_t rec_off;      // byte offset of the unified candidate records (ncp + ncs)
+  int32_t lut_off;      // u16 lut[v] = (#batch < v) | (#batch <= v) << 8, v in [0, lut_n)
+  int32_t lut_n;        // max batch + 1, or 0 when the lookup table is not built
+  int32_t pad0[5];
   int32_t batch_vals[kMaxB];  // ascending; unused = INT32_MAX
-  int32_t sec_off[kMaxKinds];   // byte offset of the kind's threshold array (0: absent)
-  int32_t sec_rows[kMaxKinds];  // rows R_k (0: kind absent from the table)
-  int32_t sec_rows_off[kMaxKinds];  // byte offset of the kind's row array
-  int32_t pad1[12];
+  KindDesc kd[kMaxKinds];
+  int32_t pad1[32];
 };
-static_assert(sizeof(PlanHdr) == 256, "PlanHdr must be 256 bytes");
+static_assert(sizeof(PlanHdr) == 512, "PlanHdr must be 512 bytes");
+
+// Monotone u64 order key of a non-NaN double (x < y  <=>  key(x) < key(y), except that
+// -0.0 orders below +0.0; thresholds are positive latencies so this never matters).
+__host__ __device__ __forceinline__ uint64_t order_key(uint64_t u) {
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
 
 struct Plan {
   double alpha = 0.0;
@@ -112,6 +133,10 @@ struct sp_table {
   int32_t* dev_counters = nullptr;            // [0] = completed_ref (device copy)
   uint32_t *candf = nullptr, *cands = nullptr;  // M flags each
   uint32_t *cidf = nullptr, *cids = nullptr;    // M maps each
+  double* ukey = nullptr;                       // 2M: unified candidate scores (CP then CS)
+  uint32_t* ukr = nullptr;                      // 2M: unified candidate r1 ranks
+  int32_t* uent = nullptr;                      // 2M: unified candidate entry index
+  uint32_t* umap = nullptr;                     // 2M: candidate -> unified id
   std::vector<sp::Plan> plans;
 };
 

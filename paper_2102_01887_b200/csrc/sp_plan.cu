@@ -7,21 +7,21 @@
 // then a masked argmin with exact-equality ties broken by (cost, res, id_rank).
 //
 // What we precompute once per (profile version, alpha) so that each decision is
-// O(K log R) instead of O(M) (SURVEY.md §8(d) "K2b"):
+// O(K) shared-memory lookups instead of O(M) (SURVEY.md §8(d) "K2b"):
 //   * cost_j, costpen_j = cost_j + pen_j                        (k_cost; bitwise equal to
 //     cost + where(lat<slack, 0, pen) because cost + 0.0 == cost for cost > 0)
 //   * r1_j = rank of j under (cost, res, id_rank)   -> tie order of feasible entries
-//     r2_j = rank of j under (costpen, cost, res, id_rank) -> order of infeasible entries
-//     (the argmin key (score, cost, res, id_rank) of configurator.py:229-237 reduces to
-//     r1 inside the feasible set and to r2 inside the infeasible set)
+//     r2_j = rank of j under (costpen, cost, res, id_rank) -> order of penalized entries
 //   * per kind, entries sorted by latency; for every threshold position p the per-batch-
 //     size prefix-min of r1 over positions < p (feasible: lat < slack) and suffix-min of r2
-//     over positions >= p (infeasible).  Consecutive identical rows are merged, leaving a
+//     over positions >= p (penalized).  Consecutive identical rows are merged, leaving a
 //     staircase of R_k rows keyed by the latency just below each step.
-// A decision then binary-searches slack_k in the kind's thresholds, loads one row of
-// 2*W u16 candidate ids, and min-reduces the batch-size lanes admitted by
-// min_batch / available with SIMD half-word minima.  See DESIGN.md §K2 for the proof of
-// bit-exactness.
+//   * every surviving candidate (entry, side) gets a unified id in (score, r1) order — the
+//     reference's argmin key — so a row lane stores min(id of best feasible, id of best
+//     penalized) and the whole decision reduces to a u16 minimum over admitted lanes.
+//   * per kind, an order-key bucket table over the thresholds (radix-accelerated search)
+//     and a batch-value lookup table for min_batch / available.
+// See DESIGN.md §K2 for the proof of bit-exactness.
 #include <float.h>
 #include <math.h>
 
@@ -158,7 +158,6 @@ __device__ int block_excl_max(int v, int* s_warp) {
     int t = __shfl_up_sync(0xffffffffu, x, off);
     if (lane >= off) x = max(x, t);
   }
-  // exclusive within warp
   int ex = __shfl_up_sync(0xffffffffu, x, 1);
   if (lane == 0) ex = INT32_MIN;
   if (lane == 31) s_warp[w] = x;
@@ -285,7 +284,6 @@ __global__ void __launch_bounds__(1024) k_stair(int M, int K, int W, KindInfo ki
         if (s != kInf32) cands[s] = 1u;
       }
     }
-    // chunk carries: last boundary position (inclusive max at the last thread), row count
     if (threadIdx.x == blockDim.x - 1) s_lastb = max(pp, isb ? p : INT32_MIN);
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -297,21 +295,27 @@ __global__ void __launch_bounds__(1024) k_stair(int M, int K, int W, KindInfo ki
   if (threadIdx.x == 0) rows_per_kind[k] = s_carry_rows;
 }
 
-// Single CTA: candidate compaction (order-preserving), offsets, header, rows, records.
+// (score, r1) strict order of unified candidates
+__device__ __forceinline__ bool key_lt(double sa, uint32_t ra, double sb, uint32_t rb) {
+  return sa < sb || (sa == sb && ra < rb);
+}
+
+// Single CTA: candidate compaction, unified (score, r1) ids, offsets, header, thresholds,
+// buckets, rows, records, batch lookup table.
 __global__ void __launch_bounds__(1024) k_finalize(
-    int M, int K, int W, int nB, KindInfo ki, const int32_t* batch_vals_unused,
-    const int32_t* __restrict__ rows_per_kind, const double* __restrict__ thrscratch,
-    const uint32_t* __restrict__ rowscratch, const uint32_t* __restrict__ candf,
-    const uint32_t* __restrict__ cands, uint32_t* cidf, uint32_t* cids,
-    const int32_t* __restrict__ ent_r1, const int32_t* __restrict__ ent_r2,
+    int M, int K, int W, int nB, KindInfo ki, const int32_t* __restrict__ rows_per_kind,
+    const double* __restrict__ thrscratch, const uint32_t* __restrict__ rowscratch,
+    const uint32_t* __restrict__ candf, const uint32_t* __restrict__ cands, uint32_t* cidf,
+    uint32_t* cids, const int32_t* __restrict__ ent_r1, const int32_t* __restrict__ ent_r2,
     const uint32_t* __restrict__ r1, const double* __restrict__ lat,
     const double* __restrict__ cost, const double* __restrict__ costpen,
-    const int32_t* __restrict__ batch, const int32_t* __restrict__ kind, PlanHdr hdr_in,
-    uint8_t* image, int64_t image_cap, int32_t* status) {
+    const int32_t* __restrict__ batch, const int32_t* __restrict__ kind, double* ukey,
+    uint32_t* ukr, int32_t* uent, uint32_t* umap, PlanHdr hdr_in, uint8_t* image,
+    int64_t image_cap, int32_t* status) {
   __shared__ int s_warp[32];
   __shared__ PlanHdr hdr;
   __shared__ int s_ncp, s_ncs;
-  // exclusive scans of the two flag arrays
+  // 1. order-preserving compaction of the two candidate sets
   for (int pass = 0; pass < 2; ++pass) {
     const uint32_t* fl = pass ? cands : candf;
     uint32_t* cid = pass ? cids : cidf;
@@ -329,85 +333,159 @@ __global__ void __launch_bounds__(1024) k_finalize(
     }
     __syncthreads();
   }
+  const int ncp = s_ncp, ncs = s_ncs;
+  // 2. candidate keys: CP[c] (feasible side) sorted by r1, CS[c] (penalized) sorted by r2;
+  //    both lists are ascending in their (score, r1) key.
+  for (int r = threadIdx.x; r < M; r += blockDim.x) {
+    if (candf[r]) {
+      const int c = (int)cidf[r], e = ent_r1[r];
+      ukey[c] = cost[e];
+      ukr[c] = (uint32_t)r;
+      uent[c] = e;
+    }
+    if (cands[r]) {
+      const int c = ncp + (int)cids[r], e = ent_r2[r];
+      ukey[c] = costpen[e];
+      ukr[c] = r1[e];
+      uent[c] = e;
+    }
+  }
+  __syncthreads();
+  // 3. merge ranks: uid = own position + #keys of the other list before it (ties, which
+  //    only occur for the two sides of one entry when the penalty is 0, put CP first)
+  for (int c = threadIdx.x; c < ncp + ncs; c += blockDim.x) {
+    const bool is_cp = c < ncp;
+    const double s = ukey[c];
+    const uint32_t rr = ukr[c];
+    int lo = is_cp ? ncp : 0, hi = is_cp ? ncp + ncs : ncp;
+    const int base = lo;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      const bool before = is_cp ? key_lt(ukey[mid], ukr[mid], s, rr)
+                                : !key_lt(s, rr, ukey[mid], ukr[mid]);
+      if (before) lo = mid + 1; else hi = mid;
+    }
+    const int own = is_cp ? c : c - ncp;
+    umap[c] = (uint32_t)(own + (lo - base));
+  }
   if (threadIdx.x == 0) {
     hdr = hdr_in;
     int off = (int)sizeof(PlanHdr);
-    for (int k = 0; k < K; ++k) {
-      int R = rows_per_kind[k];
-      hdr.sec_rows[k] = R;
-      if (R == 0) {
-        hdr.sec_off[k] = 0;
-        hdr.sec_rows_off[k] = 0;
-        continue;
+    int maxB = 0;
+    for (int b = 0; b < nB; ++b) maxB = max(maxB, hdr.batch_vals[b]);
+    hdr.lut_n = (maxB + 1 <= kMaxLut) ? maxB + 1 : 0;
+    hdr.lut_off = off;
+    off += ((hdr.lut_n * 2 + 15) / 16) * 16;
+    for (int k = 0; k < kMaxKinds; ++k) {
+      KindDesc d;
+      memset(&d, 0, sizeof(d));
+      const int R = k < K ? rows_per_kind[k] : 0;
+      d.R = R;
+      if (R > 0) {
+        const int ext = ki.base[k] + k;
+        d.thr_off = off;
+        off += ((R * 8 + 15) / 16) * 16;
+        d.rows_off = off;
+        off += ((R * 2 * W + 15) / 16) * 16;
+        int nbk = 1, shift = 0;
+        uint64_t kmin = 0;
+        if (R >= 2) {
+          kmin = order_key((uint64_t)__double_as_longlong(thrscratch[ext + 1]));
+          const uint64_t kmax = order_key((uint64_t)__double_as_longlong(thrscratch[ext + R - 1]));
+          while (nbk < 4 * (R - 1) && nbk < kMaxBuckets) nbk <<= 1;
+          while (((kmax - kmin) >> shift) >= (uint64_t)nbk) ++shift;
+        }
+        d.kmin = kmin;
+        d.bkt_off = off;
+        d.nb1_shift = (uint32_t)(nbk - 1) | ((uint32_t)shift << 16);
+        off += ((nbk * 4 + 15) / 16) * 16;
       }
-      hdr.sec_off[k] = off;
-      off += ((R * 8 + 15) / 16) * 16;
-      hdr.sec_rows_off[k] = off;
-      off += R * 4 * W;
+      hdr.kd[k] = d;
     }
-    hdr.ncp = s_ncp;
-    hdr.ncs = s_ncs;
-    hdr.cp_off = off;
-    off += s_ncp * (int)sizeof(CandRec);
-    hdr.cs_off = off;
-    off += s_ncs * (int)sizeof(CandRec);
+    hdr.ncp = ncp;
+    hdr.ncs = ncs;
+    hdr.rec_off = off;
+    off += (ncp + ncs) * (int)sizeof(CandRec);
     hdr.total_bytes = off;
-    *status = (off <= image_cap) ? 0 : -1;
+    *status = (off <= image_cap && ncp + ncs < (int)kNone16) ? 0 : -1;
   }
   __syncthreads();
-  if (hdr.total_bytes > image_cap) return;
+  if (hdr.total_bytes > image_cap || ncp + ncs >= (int)kNone16) {
+    if (threadIdx.x == 0) reinterpret_cast<uint32_t*>(image)[0] = 0;  // invalid magic
+    return;
+  }
   if (threadIdx.x < (int)(sizeof(PlanHdr) / 4))
     reinterpret_cast<uint32_t*>(image)[threadIdx.x] =
         reinterpret_cast<const uint32_t*>(&hdr)[threadIdx.x];
-  for (int k = 0; k < K; ++k) {
-    int R = hdr.sec_rows[k];
-    if (R == 0) continue;
-    int ext = ki.base[k] + k;
-    double* thr = reinterpret_cast<double*>(image + hdr.sec_off[k]);
-    uint16_t* rows = reinterpret_cast<uint16_t*>(image + hdr.sec_rows_off[k]);
-    for (int r = threadIdx.x; r < R; r += blockDim.x) thr[r] = thrscratch[ext + r];
-    int n16 = R * 2 * W;
-    for (int u = threadIdx.x; u < n16; u += blockDim.x) {
-      int r = u / (2 * W), h = u % (2 * W);
-      uint32_t v = rowscratch[(size_t)(ext + r) * (2 * W) + h];
-      uint16_t o = kNone16;
-      if (v != kInf32) o = (uint16_t)((h < W) ? cidf[v] : cids[v]);
-      rows[u] = o;
+  {
+    uint16_t* lut = reinterpret_cast<uint16_t*>(image + hdr.lut_off);
+    for (int v = threadIdx.x; v < hdr.lut_n; v += blockDim.x) {
+      int lo = 0, le = 0;
+      for (int b = 0; b < nB; ++b) {
+        lo += hdr.batch_vals[b] < v;
+        le += hdr.batch_vals[b] <= v;
+      }
+      lut[v] = (uint16_t)(lo | (le << 8));
     }
   }
-  CandRec* cp = reinterpret_cast<CandRec*>(image + hdr.cp_off);
-  CandRec* cs = reinterpret_cast<CandRec*>(image + hdr.cs_off);
-  for (int r = threadIdx.x; r < M; r += blockDim.x) {
-    if (candf[r]) {
-      int e = ent_r1[r];
-      CandRec c;
-      c.score = cost[e];
-      c.lat = lat[e];
-      c.r1 = (uint32_t)r;
-      c.idx = e;
-      c.batch = batch[e];
-      c.kind = kind[e];
-      cp[cidf[r]] = c;
+  for (int k = 0; k < K; ++k) {
+    const KindDesc d = hdr.kd[k];
+    const int R = d.R;
+    if (R == 0) continue;
+    const int ext = ki.base[k] + k;
+    double* thr = reinterpret_cast<double*>(image + d.thr_off);
+    uint16_t* rows = reinterpret_cast<uint16_t*>(image + d.rows_off);
+    for (int r = threadIdx.x; r < R; r += blockDim.x) thr[r] = thrscratch[ext + r];
+    for (int u = threadIdx.x; u < R * W; u += blockDim.x) {
+      const int r = u / W, b = u % W;
+      const uint32_t a = rowscratch[(size_t)(ext + r) * (2 * W) + b];
+      const uint32_t s = rowscratch[(size_t)(ext + r) * (2 * W) + W + b];
+      const uint32_t ua = a != kInf32 ? umap[cidf[a]] : kInf32;
+      const uint32_t us = s != kInf32 ? umap[ncp + cids[s]] : kInf32;
+      const uint32_t m = min(ua, us);
+      rows[u] = m == kInf32 ? kNone16 : (uint16_t)m;
     }
-    if (cands[r]) {
-      int e = ent_r2[r];
-      CandRec c;
-      c.score = costpen[e];
-      c.lat = lat[e];
-      c.r1 = r1[e];
-      c.idx = e;
-      c.batch = batch[e];
-      c.kind = kind[e];
-      cs[cids[r]] = c;
+    // bucket b holds thresholds j in [1, R) with (key_j - kmin) >> shift == b:
+    // entry = (#thresholds in lower buckets) | (#thresholds in b) << 16
+    uint32_t* bkt = reinterpret_cast<uint32_t*>(image + d.bkt_off);
+    const int nbk = (int)(d.nb1_shift & 0xFFFFu) + 1, shift = (int)(d.nb1_shift >> 16);
+    const uint64_t kmin = d.kmin;
+    for (int b = threadIdx.x; b < nbk; b += blockDim.x) {
+      int below[2] = {0, 0};
+      if (R >= 2) {
+        for (int q = 0; q < 2; ++q) {
+          const uint64_t bb = (uint64_t)b + q;
+          int lo = 1, hi = R;
+          while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            const uint64_t kk = order_key((uint64_t)__double_as_longlong(thrscratch[ext + mid]));
+            if (((kk - kmin) >> shift) < bb) lo = mid + 1; else hi = mid;
+          }
+          below[q] = lo - 1;
+        }
+      }
+      bkt[b] = (uint32_t)below[0] | ((uint32_t)(below[1] - below[0]) << 16);
     }
+  }
+  CandRec* rec = reinterpret_cast<CandRec*>(image + hdr.rec_off);
+  for (int c = threadIdx.x; c < ncp + ncs; c += blockDim.x) {
+    const int e = uent[c];
+    CandRec o;
+    o.score = ukey[c];
+    o.idx = e;
+    o.feas = c < ncp ? 1 : 0;
+    o.lat = lat[e];
+    o.batch = batch[e];
+    o.kind = kind[e];
+    rec[umap[c]] = o;
   }
 }
 
 int64_t plan_image_capacity(const sp_table* t, int W) {
-  int64_t cap = sizeof(PlanHdr);
+  int64_t cap = sizeof(PlanHdr) + ((kMaxLut * 2 + 15) / 16) * 16;
   for (int k = 0; k < t->K; ++k) {
     int64_t R = t->kind_count[k] + 1;
-    cap += ((R * 8 + 15) / 16) * 16 + R * 4 * W;
+    cap += ((R * 8 + 15) / 16) * 16 + ((R * 2 * W + 15) / 16) * 16 + kMaxBuckets * 4;
   }
   cap += 2 * (int64_t)t->M * (int64_t)sizeof(CandRec);
   return (cap + 15) / 16 * 16;
@@ -437,6 +515,10 @@ int plan_scratch_alloc(sp_table* t) {
     SP_CUDA(cudaMalloc(&t->cands, sizeof(uint32_t) * M));
     SP_CUDA(cudaMalloc(&t->cidf, sizeof(uint32_t) * M));
     SP_CUDA(cudaMalloc(&t->cids, sizeof(uint32_t) * M));
+    SP_CUDA(cudaMalloc(&t->ukey, sizeof(double) * 2 * M));
+    SP_CUDA(cudaMalloc(&t->ukr, sizeof(uint32_t) * 2 * M));
+    SP_CUDA(cudaMalloc(&t->uent, sizeof(int32_t) * 2 * M));
+    SP_CUDA(cudaMalloc(&t->umap, sizeof(uint32_t) * 2 * M));
   }
   return SP_OK;
 }
@@ -491,10 +573,11 @@ int plan_build(sp_ctx* ctx, sp_table* t, Plan& p) {
   h.K = K;
   for (int b = 0; b < kMaxB; ++b) h.batch_vals[b] = b < t->nB ? t->batch_vals[b] : INT32_MAX;
   int32_t* status = t->rows_per_kind + kMaxKinds;
-  k_finalize<<<1, 1024, 0, st>>>(M, K, W, t->nB, ki, nullptr, t->rows_per_kind, t->thrscratch,
+  k_finalize<<<1, 1024, 0, st>>>(M, K, W, t->nB, ki, t->rows_per_kind, t->thrscratch,
                                  t->rowscratch, t->candf, t->cands, t->cidf, t->cids,
                                  t->ent_r1, t->ent_r2, t->r1, t->lat, p.cost, p.costpen,
-                                 t->batch, t->kind, h, p.image, p.image_cap, status);
+                                 t->batch, t->kind, t->ukey, t->ukr, t->uent, t->umap, h,
+                                 p.image, p.image_cap, status);
   SP_CHECK_LAUNCH(ctx);
   p.valid = true;
   p.version = t->version;
