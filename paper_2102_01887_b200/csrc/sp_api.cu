@@ -183,6 +183,9 @@ int sp_table_create(sp_ctx* ctx, int32_t M, const double* lat, const double* lat
   for (int j = 0; j < M; ++j) {
     if (kind[j] < 0 || kind[j] >= K) return fail(SP_E_INVALID, "table_create: kind out of range");
     if (batch[j] < 1) return fail(SP_E_INVALID, "table_create: batch size must be >= 1");
+    // finite latencies keep every score finite; with an infinite score the reference's
+    // masked argmin (configurator.py:230-233) would tie masked-out entries too
+    if (!isfinite(lat[j])) return fail(SP_E_INVALID, "table_create: latency must be finite");
     bv.push_back(batch[j]);
   }
   std::sort(bv.begin(), bv.end());
@@ -271,6 +274,7 @@ int sp_table_set_latency(sp_ctx* ctx, sp_table* t, int32_t n, const int32_t* idx
   std::map<int32_t, double> last;
   for (int i = 0; i < n; ++i) {
     if (idx[i] < 0 || idx[i] >= t->M) return fail(SP_E_INVALID, "set_latency: index out of range");
+    if (!isfinite(val[i])) return fail(SP_E_INVALID, "set_latency: latency must be finite");
     last[idx[i]] = val[i];
   }
   if (last.empty()) return SP_OK;

@@ -5,9 +5,11 @@
 //                               ids; acc = vmin(acc, row) (two u16 lanes per instruction)
 //   lanes outside [min_batch, available] are masked once (min(a|m, b|m) = min(a, b)|m);
 //   the overall argmin is the smallest unified id (ids are ordered by the reference's
-//   argmin key (score, cost, res, id_rank)); its 32-byte record gives the decision.
-// Shared-memory plan addresses are formed from the extern array so that every plan access
-// compiles to LDS (STAGED); plans too big for the budget are read from global memory.
+//   argmin key (score, cost, res, id_rank)); its records give the decision.
+// One 1024-thread CTA per SM stages the plan(s) with TMA bulk copies while its threads
+// already fetch their first two invocations; shared-memory plan addresses are formed from
+// the extern array so every plan access is an LDS (plans over the budget are read from
+// global memory by a second instantiation of the loop).
 
 template <bool STAGED>
 __device__ __forceinline__ const uint8_t* plan_base(const uint8_t* smem, const uint8_t* const* gptr,
@@ -17,39 +19,41 @@ __device__ __forceinline__ const uint8_t* plan_base(const uint8_t* smem, const u
 }
 
 // Row of the threshold staircase for slack s: #{j in [1, R) : thr[j] < s}.
+//   q0 = {kmin_hi, nb1 | shift << 16, thr_off, rows_off},  q1 = {bkt_off, R, nonpos, -}
 __device__ __forceinline__ int stair_row(const uint8_t* base, const uint4& q0, const uint4& q1,
                                          double s) {
-  if (s != s) return 0;  // NaN: nothing is feasible (lat < NaN is false)
   const double* thr = reinterpret_cast<const double*>(base + (int)q0.z);
-  const uint32_t* bkt = reinterpret_cast<const uint32_t*>(base + (int)q1.x);
-  const uint64_t kmin = ((uint64_t)q0.y << 32) | q0.x;
-  const uint32_t nb1 = q1.y & 0xFFFFu, shift = q1.y >> 16;
-  const uint64_t key = order_key((uint64_t)__double_as_longlong(s));
-  uint64_t b = key < kmin ? 0ull : ((key - kmin) >> shift);
-  b = b < nb1 ? b : nb1;
-  const uint32_t e = bkt[b];
-  int r = (int)(e & 0xFFFFu);
-  int n = (int)(e >> 16);
-  while (n > 0) {  // thresholds of this bucket: thr[r+1 .. r+n], ascending
+  const bool nonpos = q1.z != 0;
+  int r = 0, n = nonpos ? (int)q1.y - 1 : 0;  // generic: search every real threshold
+  if (!nonpos && s > 0.0) {
+    // positive thresholds: bucket on the high word of the IEEE encoding
+    const uint32_t* bkt = reinterpret_cast<const uint32_t*>(base + (int)q1.x);
+    const int d = __double2hiint(s) - (int)q0.x;
+    const uint32_t nb1 = q0.y & 0xFFFFu;
+    uint32_t b = d < 0 ? 0u : ((uint32_t)d >> (q0.y >> 16));
+    b = b < nb1 ? b : nb1;
+    const uint32_t e = bkt[b];
+    r = (int)(e & 0xFFFFu);
+    n = (int)(e >> 16);
+  }  // else (s <= 0 or NaN, all thresholds positive): r = 0
+  while (n > 0) {  // candidate thresholds thr[r+1 .. r+n], ascending
     const int hh = n >> 1;
-    if (thr[r + hh + 1] < s) {
-      r += hh + 1;
-      n -= hh + 1;
-    } else {
-      n = hh;
-    }
+    const bool lt = thr[r + hh + 1] < s;
+    r = lt ? r + hh + 1 : r;
+    n = lt ? n - hh - 1 : hh;
   }
   return r;
 }
 
-template <int KT, int WW>
+template <int KT, int WW, bool KMIN>
 __device__ __forceinline__ void decide_plan(const uint8_t* base, const SelectIO& io, int i,
                                             const In<KT>& x, const uint32_t* s_mlo,
-                                            const uint32_t* s_mhi, bool want_kmin) {
+                                            const uint32_t* s_mhi) {
   constexpr int NW = WW / 2;  // 32-bit words per row
   const PlanHdr* h = reinterpret_cast<const PlanHdr*>(base);
   const int pw = h->W;        // this plan's row width (8 or 16 lanes)
-  const CandRec* rec = reinterpret_cast<const CandRec*>(base + h->rec_off);
+  const CandA* reca = reinterpret_cast<const CandA*>(base + h->rec_off);
+  const CandB* recb = reinterpret_cast<const CandB*>(base + h->recb_off);
 
   uint32_t acc[NW];
 #pragma unroll
@@ -60,10 +64,10 @@ __device__ __forceinline__ void decide_plan(const uint8_t* base, const SelectIO&
     if (k >= io.K) break;
     const uint4* kd = reinterpret_cast<const uint4*>(&h->kd[k]);
     const uint4 q1 = kd[1];
-    const int R = (int)q1.z;
-    const bool ex = (x.fl >> (SP_FLAG_EXCL_SHIFT + k)) & 1u;
-    if (R == 0 || (ex && !want_kmin)) {
-      if (want_kmin) io.out_kind_min[(size_t)i * io.K + k] = INFINITY;
+    const int R = (int)q1.y;
+    const uint32_t exm = ((x.fl >> (SP_FLAG_EXCL_SHIFT + k)) & 1u) ? 0xFFFFFFFFu : 0u;
+    if (R == 0 || (!KMIN && exm)) {
+      if (KMIN) io.out_kind_min[(size_t)i * io.K + k] = INFINITY;
       continue;
     }
     const uint4 q0 = kd[0];
@@ -82,24 +86,23 @@ __device__ __forceinline__ void decide_plan(const uint8_t* base, const SelectIO&
         U[4 * q + 0] = a.x; U[4 * q + 1] = a.y; U[4 * q + 2] = a.z; U[4 * q + 3] = a.w;
       }
     }
-    if (!ex) {
 #pragma unroll
-      for (int w = 0; w < NW; ++w) acc[w] = __vminu2(acc[w], U[w]);
-    }
-    if (want_kmin) {  // Eq. 3 operand: unmasked min score of the kind
+    for (int w = 0; w < NW; ++w) acc[w] = __vminu2(acc[w], U[w] | exm);
+    if (KMIN) {  // Eq. 3 operand: unmasked min score of the kind
       const uint32_t u = hmin_all<NW>(U);
-      io.out_kind_min[(size_t)i * io.K + k] = (u != kNone16) ? rec[u].score : INFINITY;
+      io.out_kind_min[(size_t)i * io.K + k] = (u != kNone16) ? reca[u].score : INFINITY;
     }
   }
 
   // batch lanes admitted by min_batch (configurator.py:264-265) and available (288)
   int lo, le;
   const int lut_n = h->lut_n;
-  if (lut_n > 0) {
+  if (lut_n > 0) {  // lut[0] = (0, 0); lut[lut_n - 1] saturates at (nB, nB)
     const uint16_t* lut = reinterpret_cast<const uint16_t*>(base + h->lut_off);
-    const int nB = h->nB;
-    lo = x.mb <= 0 ? 0 : (x.mb >= lut_n ? nB : (int)(lut[x.mb] & 0xFFu));
-    le = x.av <= 0 ? 0 : (x.av >= lut_n ? nB : (int)(lut[x.av] >> 8));
+    const uint32_t a = lut[min(max(x.mb, 0), lut_n - 1)];
+    const uint32_t b = lut[min(max(x.av, 0), lut_n - 1)];
+    lo = (int)(a & 0xFFu);
+    le = (int)(b >> 8);
   } else {
     lo = le = 0;
 #pragma unroll
@@ -119,80 +122,65 @@ __device__ __forceinline__ void decide_plan(const uint8_t* base, const SelectIO&
     }
   }
   Out o;
-  uint32_t u = hmin_or<NW>(acc, m1);
-  if (u == kNone16) {  // configurator.py:266-267
-    o.idx = -1; o.code = SP_DEC_NONE; o.fill = 0;
-    o.obj = 0.0; o.slack = 0.0; o.wait = 0.0;
-    store_out(io, i, o);
-    return;
-  }
-  uint4 a = *reinterpret_cast<const uint4*>(rec + u);
-  uint4 b = *(reinterpret_cast<const uint4*>(rec + u) + 1);
-  double sk = pick_kind<KT>(x.s, (int)b.w);
-  int B = (int)b.z;
-  // safe delayed batching (configurator.py:271-286)
-  if ((x.fl & SP_FLAG_ALLOW_DELAY) && B > x.av &&
-      (long long)x.sup >= (long long)B - (long long)x.av) {
-    const double wait = __dsub_rn(sk, __hiloint2double((int)b.y, (int)b.x));
-    if (wait > 0.0) {
-      o.idx = (int)a.z;
-      o.code = SP_DEC_DELAY | (a.w ? SP_DEC_FEASIBLE : 0);
-      o.fill = x.av;
-      o.obj = __hiloint2double((int)a.y, (int)a.x);
-      o.slack = sk;
-      o.wait = wait;
-      store_out(io, i, o);
-      return;
-    }
-  }
-  // downgrade to a batch size that fits what is available (configurator.py:287-291)
-  if (B > x.av) {
-    uint32_t m2[NW];
-    const uint4* q = reinterpret_cast<const uint4*>(s_mhi + le * NW);
+  o.idx = -1; o.code = SP_DEC_NONE; o.fill = 0;
+  o.obj = 0.0; o.slack = 0.0; o.wait = 0.0;
+  const uint32_t u = hmin_or<NW>(acc, m1);
+  if (u != kNone16) {
+    CandA ca = reca[u];
+    CandB cb = recb[u];
+    double sk = pick_kind<KT>(x.s, (int)(cb.meta >> 17));
+    // safe delayed batching (configurator.py:271-286)
+    const bool big = cb.batch > x.av;
+    const double wait = __dsub_rn(sk, ca.lat);
+    const bool delay = (x.fl & SP_FLAG_ALLOW_DELAY) && big &&
+                       (long long)x.sup >= (long long)cb.batch - (long long)x.av && wait > 0.0;
+    // downgrade to a batch size that fits what is available (configurator.py:287-291)
+    if (!delay && big) {
+      uint32_t m2[NW];
+      const uint4* q = reinterpret_cast<const uint4*>(s_mhi + le * NW);
 #pragma unroll
-    for (int v4 = 0; v4 < NW / 4; ++v4) {
-      const uint4 v = q[v4];
-      m2[4 * v4] = m1[4 * v4] | v.x; m2[4 * v4 + 1] = m1[4 * v4 + 1] | v.y;
-      m2[4 * v4 + 2] = m1[4 * v4 + 2] | v.z; m2[4 * v4 + 3] = m1[4 * v4 + 3] | v.w;
+      for (int v4 = 0; v4 < NW / 4; ++v4) {
+        const uint4 v = q[v4];
+        m2[4 * v4] = m1[4 * v4] | v.x; m2[4 * v4 + 1] = m1[4 * v4 + 1] | v.y;
+        m2[4 * v4 + 2] = m1[4 * v4 + 2] | v.z; m2[4 * v4 + 3] = m1[4 * v4 + 3] | v.w;
+      }
+      const uint32_t u2 = hmin_or<NW>(acc, m2);
+      if (u2 != kNone16) {
+        ca = reca[u2];
+        cb = recb[u2];
+        sk = pick_kind<KT>(x.s, (int)(cb.meta >> 17));
+      }
     }
-    const uint32_t u2 = hmin_or<NW>(acc, m2);
-    if (u2 != kNone16) {
-      u = u2;
-      a = *reinterpret_cast<const uint4*>(rec + u);
-      b = *(reinterpret_cast<const uint4*>(rec + u) + 1);
-      sk = pick_kind<KT>(x.s, (int)b.w);
-      B = (int)b.z;
-    }
+    const int feas = (cb.meta >> 16) & 1u;
+    o.idx = (int)(cb.meta & 0xFFFFu);
+    o.code = (delay ? SP_DEC_DELAY : SP_DEC_ASSIGN) | (feas ? SP_DEC_FEASIBLE : 0);
+    o.fill = delay ? x.av : min(cb.batch, x.av);
+    o.obj = ca.score;
+    o.slack = sk;
+    o.wait = delay ? wait : 0.0;
   }
-  o.idx = (int)a.z;
-  o.code = SP_DEC_ASSIGN | (a.w ? SP_DEC_FEASIBLE : 0);
-  o.fill = min(B, x.av);
-  o.obj = __hiloint2double((int)a.y, (int)a.x);
-  o.slack = sk;
-  o.wait = 0.0;
   store_out(io, i, o);
 }
 
-template <int KT, int WW, bool STAGED>
+template <int KT, int WW, bool STAGED, bool KMIN>
 __device__ __forceinline__ void plan_loop(const uint8_t* smem, const PlanPtrs& pp, const int* s_off,
                                           const SelectIO& io, const uint32_t* s_mlo,
-                                          const uint32_t* s_mhi) {
-  const bool want_kmin = io.out_kind_min != nullptr;
+                                          const uint32_t* s_mhi, int i, In<KT>& cur,
+                                          In<KT>& nxt) {
   const int stride = gridDim.x * blockDim.x;
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  In<KT> cur, nxt;
-  if (i < io.N) load_in<KT>(io, i, cur);
   for (; i < io.N; i += stride) {
-    const int j = i + stride;
-    if (j < io.N) load_in<KT>(io, j, nxt);  // prefetch the next invocation
-    decide_plan<KT, WW>(plan_base<STAGED>(smem, pp.p, s_off, cur.t), io, i, cur, s_mlo, s_mhi,
-                        want_kmin);
+    const int j = i + 2 * stride;
+    In<KT> nn;
+    if (j < io.N) load_in<KT>(io, j, nn);  // prefetch two invocations ahead
+    decide_plan<KT, WW, KMIN>(plan_base<STAGED>(smem, pp.p, s_off, cur.t), io, i, cur, s_mlo,
+                              s_mhi);
     cur = nxt;
+    nxt = nn;
   }
 }
 
 template <int KT, int WW>
-__global__ void __launch_bounds__(512, 2) k_select_plan(PlanPtrs pp, int smem_budget, SelectIO io) {
+__global__ void __launch_bounds__(1024, 1) k_select_plan(PlanPtrs pp, int smem_budget, SelectIO io) {
   constexpr int NW = WW / 2;
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ int s_off[kMaxPlanTables];
@@ -217,6 +205,12 @@ __global__ void __launch_bounds__(512, 2) k_select_plan(PlanPtrs pp, int smem_bu
       }
     }
   }
+  // the first two invocations are fetched while the plan copy is in flight
+  const int stride = gridDim.x * blockDim.x;
+  const int i = blockIdx.x * blockDim.x + tid;
+  In<KT> cur, nxt;
+  if (i < io.N) load_in<KT>(io, i, cur);
+  if (i + stride < io.N) load_in<KT>(io, i + stride, nxt);
   for (int u = tid; u < (WW + 1) * NW; u += blockDim.x) {
     const int row = u / NW, w = u % NW;
     const int b0 = 2 * w, b1 = 2 * w + 1;
@@ -224,10 +218,13 @@ __global__ void __launch_bounds__(512, 2) k_select_plan(PlanPtrs pp, int smem_bu
     s_mhi[u] = (b0 >= row ? 0xFFFFu : 0u) | (b1 >= row ? 0xFFFF0000u : 0u);
   }
   __syncthreads();
+  const bool kmin = io.out_kind_min != nullptr;
   if (s_fit) {
     mbar_wait(&s_bar, 0);
-    plan_loop<KT, WW, true>(smem, pp, s_off, io, s_mlo, s_mhi);
+    if (kmin) plan_loop<KT, WW, true, true>(smem, pp, s_off, io, s_mlo, s_mhi, i, cur, nxt);
+    else plan_loop<KT, WW, true, false>(smem, pp, s_off, io, s_mlo, s_mhi, i, cur, nxt);
   } else {
-    plan_loop<KT, WW, false>(smem, pp, s_off, io, s_mlo, s_mhi);
+    if (kmin) plan_loop<KT, WW, false, true>(smem, pp, s_off, io, s_mlo, s_mhi, i, cur, nxt);
+    else plan_loop<KT, WW, false, false>(smem, pp, s_off, io, s_mlo, s_mhi, i, cur, nxt);
   }
 }

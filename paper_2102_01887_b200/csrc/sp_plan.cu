@@ -373,7 +373,8 @@ __global__ void __launch_bounds__(1024) k_finalize(
     int off = (int)sizeof(PlanHdr);
     int maxB = 0;
     for (int b = 0; b < nB; ++b) maxB = max(maxB, hdr.batch_vals[b]);
-    hdr.lut_n = (maxB + 1 <= kMaxLut) ? maxB + 1 : 0;
+    // entries 0..maxB plus one saturating entry for every value above maxB
+    hdr.lut_n = (maxB + 2 <= kMaxLut) ? maxB + 2 : 0;
     hdr.lut_off = off;
     off += ((hdr.lut_n * 2 + 15) / 16) * 16;
     for (int k = 0; k < kMaxKinds; ++k) {
@@ -388,14 +389,16 @@ __global__ void __launch_bounds__(1024) k_finalize(
         d.rows_off = off;
         off += ((R * 2 * W + 15) / 16) * 16;
         int nbk = 1, shift = 0;
-        uint64_t kmin = 0;
+        uint32_t kmin = 0;
         if (R >= 2) {
-          kmin = order_key((uint64_t)__double_as_longlong(thrscratch[ext + 1]));
-          const uint64_t kmax = order_key((uint64_t)__double_as_longlong(thrscratch[ext + R - 1]));
+          // positive thresholds: the high word of the encoding is monotone
+          kmin = (uint32_t)__double2hiint(thrscratch[ext + 1]);
+          const uint32_t kmax = (uint32_t)__double2hiint(thrscratch[ext + R - 1]);
           while (nbk < 4 * (R - 1) && nbk < kMaxBuckets) nbk <<= 1;
-          while (((kmax - kmin) >> shift) >= (uint64_t)nbk) ++shift;
+          while (((kmax - kmin) >> shift) >= (uint32_t)nbk) ++shift;
+          d.pad[0] = !(thrscratch[ext + 1] > 0.0);  // non-positive latency: generic search
         }
-        d.kmin = kmin;
+        d.kmin_hi = kmin;
         d.bkt_off = off;
         d.nb1_shift = (uint32_t)(nbk - 1) | ((uint32_t)shift << 16);
         off += ((nbk * 4 + 15) / 16) * 16;
@@ -405,7 +408,9 @@ __global__ void __launch_bounds__(1024) k_finalize(
     hdr.ncp = ncp;
     hdr.ncs = ncs;
     hdr.rec_off = off;
-    off += (ncp + ncs) * (int)sizeof(CandRec);
+    off += (ncp + ncs) * (int)sizeof(CandA);
+    hdr.recb_off = off;
+    off += (((ncp + ncs) * (int)sizeof(CandB) + 15) / 16) * 16;
     hdr.total_bytes = off;
     *status = (off <= image_cap && ncp + ncs < (int)kNone16) ? 0 : -1;
   }
@@ -449,16 +454,16 @@ __global__ void __launch_bounds__(1024) k_finalize(
     // entry = (#thresholds in lower buckets) | (#thresholds in b) << 16
     uint32_t* bkt = reinterpret_cast<uint32_t*>(image + d.bkt_off);
     const int nbk = (int)(d.nb1_shift & 0xFFFFu) + 1, shift = (int)(d.nb1_shift >> 16);
-    const uint64_t kmin = d.kmin;
+    const uint32_t kmin = d.kmin_hi;
     for (int b = threadIdx.x; b < nbk; b += blockDim.x) {
       int below[2] = {0, 0};
       if (R >= 2) {
         for (int q = 0; q < 2; ++q) {
-          const uint64_t bb = (uint64_t)b + q;
+          const uint32_t bb = (uint32_t)b + q;
           int lo = 1, hi = R;
           while (lo < hi) {
             const int mid = (lo + hi) >> 1;
-            const uint64_t kk = order_key((uint64_t)__double_as_longlong(thrscratch[ext + mid]));
+            const uint32_t kk = (uint32_t)__double2hiint(thrscratch[ext + mid]);
             if (((kk - kmin) >> shift) < bb) lo = mid + 1; else hi = mid;
           }
           below[q] = lo - 1;
@@ -467,17 +472,19 @@ __global__ void __launch_bounds__(1024) k_finalize(
       bkt[b] = (uint32_t)below[0] | ((uint32_t)(below[1] - below[0]) << 16);
     }
   }
-  CandRec* rec = reinterpret_cast<CandRec*>(image + hdr.rec_off);
+  CandA* reca = reinterpret_cast<CandA*>(image + hdr.rec_off);
+  CandB* recb = reinterpret_cast<CandB*>(image + hdr.recb_off);
   for (int c = threadIdx.x; c < ncp + ncs; c += blockDim.x) {
     const int e = uent[c];
-    CandRec o;
-    o.score = ukey[c];
-    o.idx = e;
-    o.feas = c < ncp ? 1 : 0;
-    o.lat = lat[e];
-    o.batch = batch[e];
-    o.kind = kind[e];
-    rec[umap[c]] = o;
+    const uint32_t u = umap[c];
+    CandA a;
+    a.score = ukey[c];
+    a.lat = lat[e];
+    reca[u] = a;
+    CandB b;
+    b.meta = (uint32_t)e | ((c < ncp ? 1u : 0u) << 16) | ((uint32_t)kind[e] << 17);
+    b.batch = batch[e];
+    recb[u] = b;
   }
 }
 

@@ -327,7 +327,10 @@ __global__ void k_affinity(int N, int K, const double* __restrict__ kmin,
   out[i] = __ddiv_rn(other, kmin[(size_t)i * K + c]);
 }
 
-constexpr int kPlanSmemBudget = 96 * 1024;
+// one persistent 1024-thread CTA per SM with one staged copy of the plan(s)
+constexpr int kPlanThreads = 1024;
+constexpr int kPlanCtasPerSm = 1;
+constexpr int kPlanSmemBudget = 200 * 1024;
 
 template <int KT, int WW>
 int launch_plan_t(sp_ctx* ctx, const PlanPtrs& pp, const SelectIO& io) {
@@ -337,10 +340,10 @@ int launch_plan_t(sp_ctx* ctx, const PlanPtrs& pp, const SelectIO& io) {
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kPlanSmemBudget));
     attr_done = true;
   }
-  int blocks = ctx->num_sms * 2;
-  int need = (io.N + 511) / 512;
+  int blocks = ctx->num_sms * kPlanCtasPerSm;
+  int need = (io.N + kPlanThreads - 1) / kPlanThreads;
   if (need < blocks) blocks = need > 0 ? need : 1;
-  k_select_plan<KT, WW><<<blocks, 512, kPlanSmemBudget, ctx->stream>>>(pp, kPlanSmemBudget, io);
+  k_select_plan<KT, WW><<<blocks, kPlanThreads, kPlanSmemBudget, ctx->stream>>>(pp, kPlanSmemBudget, io);
   SP_CHECK_LAUNCH(ctx);
   return SP_OK;
 }

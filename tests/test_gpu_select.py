@@ -172,10 +172,13 @@ def test_config2_full_size_vs_c_oracle(c2_table, alpha):
     assert 0.05 < exp["feasible"][exp["code"] > 0].mean() < 0.95
 
 
-def _random_table(rng, M, nB, K):
+def _random_table(rng, M, nB, K, nonpos=False):
     batch_vals = np.sort(rng.choice(np.arange(1, 300), size=nB, replace=False))
     lat_pool = rng.uniform(0.01, 5.0, size=max(3, M // 8))
     lat = np.where(rng.random(M) < 0.5, rng.choice(lat_pool, size=M), rng.uniform(0.01, 5.0, size=M))
+    if nonpos:  # latencies set to <= 0 through set_latency (the reference does not forbid it)
+        lat[rng.random(M) < 0.1] = 0.0
+        lat[rng.random(M) < 0.1] = -rng.uniform(0.0, 2.0)
     res = rng.choice([1.0, 2.0, 4.0, 8.0], size=M)
     gk = rng.integers(0, K, size=M)
     gk[0] = 0
@@ -186,15 +189,17 @@ def _random_table(rng, M, nB, K):
                                 id_rank=rng.permutation(M), n_kinds=K)
 
 
-@pytest.mark.parametrize("seed,M,nB,K", [(1, 3000, 8, 2), (2, 2000, 16, 4), (3, 700, 13, 3),
-                                         (4, 5000, 5, 8), (5, 1, 1, 1), (6, 64, 2, 2)])
-def test_random_tables_plan_scan_oracle(gpu_ctx, seed, M, nB, K):
+@pytest.mark.parametrize("seed,M,nB,K,nonpos", [(1, 3000, 8, 2, False), (2, 2000, 16, 4, False),
+                                                (3, 700, 13, 3, False), (4, 5000, 5, 8, False),
+                                                (5, 1, 1, 1, False), (6, 64, 2, 2, False),
+                                                (7, 900, 8, 2, True), (8, 300, 11, 3, True)])
+def test_random_tables_plan_scan_oracle(gpu_ctx, seed, M, nB, K, nonpos):
     """Heavily tied random tables (repeated latencies, equal scores), every kind count and
-    both plan widths (W = 8 / 16): plan == scan == C oracle."""
+    both plan widths (W = 8 / 16), also zero / negative latencies: plan == scan == C oracle."""
     import paper_2102_01887_b200 as sp
 
     rng = np.random.default_rng(seed)
-    t = _random_table(rng, M, nB, K)
+    t = _random_table(rng, M, nB, K, nonpos)
     N = 20000
     slack = rng.uniform(-2, 6, size=(N, K))
     slack[rng.random((N, K)) < 0.05] = np.inf
