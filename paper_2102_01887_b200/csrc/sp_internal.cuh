@@ -35,12 +35,8 @@ struct __align__(16) CandRec {
   int32_t kind;
 };
 static_assert(sizeof(CandRec) == 32, "CandRec must be 32 bytes");
-// In the plan image candidates are stored as two arrays indexed by unified id:
-//   CandA (16 B) {score, lat}   and   CandB (8 B) {idx | feas << 16 | kind << 17, batch}
-struct __align__(16) CandA {
-  double score;
-  double lat;
-};
+// In the plan image candidates are stored as three arrays indexed by unified id:
+//   score[] (f64), lat[] (f64) and CandB (8 B) {idx | feas << 16 | kind << 17, batch}
 struct __align__(8) CandB {
   uint32_t meta;   // entry index (15 bits) | feasible (bit 16) | kind (bits 17..19)
   int32_t batch;
@@ -56,7 +52,7 @@ struct __align__(16) KindDesc {
   uint32_t kmin_hi;    // high word of the smallest real threshold
   uint32_t nb1_shift;  // (buckets - 1) | shift << 16
   int32_t thr_off;     // byte offset of the threshold array (R doubles, thr[0] = -inf)
-  int32_t rows_off;    // byte offset of the staircase rows (R x W u16)
+  int32_t rows_off;    // byte offset of the staircase rows (R x row_stride bytes)
   int32_t bkt_off;     // byte offset of the bucket table (u32: lo | cnt << 16)
   int32_t R;           // rows (0: kind absent from the table)
   int32_t pad[2];
@@ -74,11 +70,14 @@ struct __align__(16) PlanHdr {
   int32_t K;            // global kind count
   int32_t ncp;          // feasible-side candidates
   int32_t ncs;          // penalized-side candidates
-  int32_t rec_off;      // byte offset of CandA[ncp + ncs]; CandB[] follows at recb_off
-  int32_t recb_off;
+  int32_t score_off;    // byte offset of score[ncp + ncs] (f64)
+  int32_t lat_off;      // byte offset of lat[ncp + ncs] (f64)
+  int32_t recb_off;     // byte offset of CandB[ncp + ncs]
+  int32_t row_stride;   // bytes per staircase row: u16 range minima for every batch-lane
+                        // interval [lo, hi], at tri(lo) + hi - lo, tri(lo) = lo*nB - lo(lo-1)/2
   int32_t lut_off;      // u16 lut[v] = (#batch < v) | (#batch <= v) << 8, v in [0, lut_n)
-  int32_t lut_n;        // max batch + 1, or 0 when the lookup table is not built
-  int32_t pad0[4];
+  int32_t lut_n;        // max batch + 2, or 0 when the lookup table is not built
+  int32_t pad0[2];
   int32_t batch_vals[kMaxB];  // ascending; unused = INT32_MAX
   KindDesc kd[kMaxKinds];
   int32_t pad1[32];

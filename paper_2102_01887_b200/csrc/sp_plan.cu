@@ -370,6 +370,7 @@ __global__ void __launch_bounds__(1024) k_finalize(
   }
   if (threadIdx.x == 0) {
     hdr = hdr_in;
+    hdr.row_stride = ((nB * (nB + 1) + 3) / 4) * 4;  // nB(nB+1)/2 u16, 4-byte aligned
     int off = (int)sizeof(PlanHdr);
     int maxB = 0;
     for (int b = 0; b < nB; ++b) maxB = max(maxB, hdr.batch_vals[b]);
@@ -387,7 +388,7 @@ __global__ void __launch_bounds__(1024) k_finalize(
         d.thr_off = off;
         off += ((R * 8 + 15) / 16) * 16;
         d.rows_off = off;
-        off += ((R * 2 * W + 15) / 16) * 16;
+        off += ((R * hdr.row_stride + 15) / 16) * 16;
         int nbk = 1, shift = 0;
         uint32_t kmin = 0;
         if (R >= 2) {
@@ -407,8 +408,10 @@ __global__ void __launch_bounds__(1024) k_finalize(
     }
     hdr.ncp = ncp;
     hdr.ncs = ncs;
-    hdr.rec_off = off;
-    off += (ncp + ncs) * (int)sizeof(CandA);
+    hdr.score_off = off;
+    off += (ncp + ncs) * 8;
+    hdr.lat_off = off;
+    off += (ncp + ncs) * 8;
     hdr.recb_off = off;
     off += (((ncp + ncs) * (int)sizeof(CandB) + 15) / 16) * 16;
     hdr.total_bytes = off;
@@ -441,14 +444,27 @@ __global__ void __launch_bounds__(1024) k_finalize(
     double* thr = reinterpret_cast<double*>(image + d.thr_off);
     uint16_t* rows = reinterpret_cast<uint16_t*>(image + d.rows_off);
     for (int r = threadIdx.x; r < R; r += blockDim.x) thr[r] = thrscratch[ext + r];
-    for (int u = threadIdx.x; u < R * W; u += blockDim.x) {
-      const int r = u / W, b = u % W;
-      const uint32_t a = rowscratch[(size_t)(ext + r) * (2 * W) + b];
-      const uint32_t s = rowscratch[(size_t)(ext + r) * (2 * W) + W + b];
-      const uint32_t ua = a != kInf32 ? umap[cidf[a]] : kInf32;
-      const uint32_t us = s != kInf32 ? umap[ncp + cids[s]] : kInf32;
-      const uint32_t m = min(ua, us);
-      rows[u] = m == kInf32 ? kNone16 : (uint16_t)m;
+    // row r: lane b = min(unified id of the best feasible, of the best penalized entry with
+    // batch size batch_vals[b]); stored as the minimum over every lane interval [lo, hi]
+    for (int r = threadIdx.x; r < R; r += blockDim.x) {
+      uint32_t lane[kMaxB];
+      for (int b = 0; b < nB; ++b) {
+        const uint32_t a = rowscratch[(size_t)(ext + r) * (2 * W) + b];
+        const uint32_t s = rowscratch[(size_t)(ext + r) * (2 * W) + W + b];
+        const uint32_t ua = a != kInf32 ? umap[cidf[a]] : kInf32;
+        const uint32_t us = s != kInf32 ? umap[ncp + cids[s]] : kInf32;
+        lane[b] = min(ua, us);
+      }
+      uint16_t* out = reinterpret_cast<uint16_t*>(reinterpret_cast<uint8_t*>(rows) +
+                                                  (size_t)r * hdr.row_stride);
+      int q = 0;
+      for (int lo = 0; lo < nB; ++lo) {
+        uint32_t m = kInf32;
+        for (int hi = lo; hi < nB; ++hi) {
+          m = min(m, lane[hi]);
+          out[q++] = m == kInf32 ? kNone16 : (uint16_t)m;
+        }
+      }
     }
     // bucket b holds thresholds j in [1, R) with (key_j - kmin) >> shift == b:
     // entry = (#thresholds in lower buckets) | (#thresholds in b) << 16
@@ -472,15 +488,14 @@ __global__ void __launch_bounds__(1024) k_finalize(
       bkt[b] = (uint32_t)below[0] | ((uint32_t)(below[1] - below[0]) << 16);
     }
   }
-  CandA* reca = reinterpret_cast<CandA*>(image + hdr.rec_off);
+  double* rscore = reinterpret_cast<double*>(image + hdr.score_off);
+  double* rlat = reinterpret_cast<double*>(image + hdr.lat_off);
   CandB* recb = reinterpret_cast<CandB*>(image + hdr.recb_off);
   for (int c = threadIdx.x; c < ncp + ncs; c += blockDim.x) {
     const int e = uent[c];
     const uint32_t u = umap[c];
-    CandA a;
-    a.score = ukey[c];
-    a.lat = lat[e];
-    reca[u] = a;
+    rscore[u] = ukey[c];
+    rlat[u] = lat[e];
     CandB b;
     b.meta = (uint32_t)e | ((c < ncp ? 1u : 0u) << 16) | ((uint32_t)kind[e] << 17);
     b.batch = batch[e];
@@ -492,7 +507,8 @@ int64_t plan_image_capacity(const sp_table* t, int W) {
   int64_t cap = sizeof(PlanHdr) + ((kMaxLut * 2 + 15) / 16) * 16;
   for (int k = 0; k < t->K; ++k) {
     int64_t R = t->kind_count[k] + 1;
-    cap += ((R * 8 + 15) / 16) * 16 + ((R * 2 * W + 15) / 16) * 16 + kMaxBuckets * 4;
+    const int64_t stride = ((t->nB * (t->nB + 1) + 3) / 4) * 4;
+    cap += ((R * 8 + 15) / 16) * 16 + ((R * stride + 15) / 16) * 16 + kMaxBuckets * 4;
   }
   cap += 2 * (int64_t)t->M * (int64_t)sizeof(CandRec);
   return (cap + 15) / 16 * 16;

@@ -332,18 +332,18 @@ constexpr int kPlanThreads = 1024;
 constexpr int kPlanCtasPerSm = 1;
 constexpr int kPlanSmemBudget = 200 * 1024;
 
-template <int KT, int WW>
+template <int KT>
 int launch_plan_t(sp_ctx* ctx, const PlanPtrs& pp, const SelectIO& io) {
   static bool attr_done = false;
   if (!attr_done) {
-    SP_CUDA(cudaFuncSetAttribute(k_select_plan<KT, WW>,
+    SP_CUDA(cudaFuncSetAttribute(k_select_plan<KT>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kPlanSmemBudget));
     attr_done = true;
   }
   int blocks = ctx->num_sms * kPlanCtasPerSm;
   int need = (io.N + kPlanThreads - 1) / kPlanThreads;
   if (need < blocks) blocks = need > 0 ? need : 1;
-  k_select_plan<KT, WW><<<blocks, kPlanThreads, kPlanSmemBudget, ctx->stream>>>(pp, kPlanSmemBudget, io);
+  k_select_plan<KT><<<blocks, kPlanThreads, kPlanSmemBudget, ctx->stream>>>(pp, kPlanSmemBudget, io);
   SP_CHECK_LAUNCH(ctx);
   return SP_OK;
 }
@@ -380,11 +380,11 @@ int select_launch(sp_ctx* ctx, int n_tables, sp_table* const* tables, double alp
   if (n_tables < 1) return fail(SP_E_INVALID, "select: no tables");
   const int K = tables[0]->K;
   bool plan_ok = true;
-  int maxW = 8;
+
   for (int t = 0; t < n_tables; ++t) {
     if (tables[t]->K != K) return fail(SP_E_INVALID, "select: tables disagree on kind count");
     plan_ok = plan_ok && tables[t]->plan_ok;
-    if (tables[t]->nB > 8) maxW = 16;
+
   }
   if (mode == SP_MODE_PLAN && !plan_ok)
     return fail(SP_E_UNSUPPORTED, "select: staircase plan unsupported for this table");
@@ -411,14 +411,9 @@ int select_launch(sp_ctx* ctx, int n_tables, sp_table* const* tables, double alp
       if (!p) return rc;
       pp.p[t] = p->image;
     }
-    if (maxW == 16) {
-      if (KT == 2) return launch_plan_t<2, 16>(ctx, pp, io);
-      if (KT == 4) return launch_plan_t<4, 16>(ctx, pp, io);
-      return launch_plan_t<8, 16>(ctx, pp, io);
-    }
-    if (KT == 2) return launch_plan_t<2, 8>(ctx, pp, io);
-    if (KT == 4) return launch_plan_t<4, 8>(ctx, pp, io);
-    return launch_plan_t<8, 8>(ctx, pp, io);
+    if (KT == 2) return launch_plan_t<2>(ctx, pp, io);
+    if (KT == 4) return launch_plan_t<4>(ctx, pp, io);
+    return launch_plan_t<8>(ctx, pp, io);
   }
   ScanPtrs sp_;
   sp_.n = n_tables;
