@@ -352,7 +352,8 @@ def our_arm(args) -> None:
         "gpu_launches": launches,
         "step_ms": {"min": min(step_ms), "median": statistics.median(step_ms), "max": max(step_ms),
                     "by_alpha": {str(a): statistics.median(step_ms[j::len(ALPHAS)]) for j, a in
-                                 enumerate(ALPHAS[(args.warmup + k) % len(ALPHAS)] for k in range(len(ALPHAS)))}},
+                                 enumerate(ALPHAS[(args.warmup + k) % len(ALPHAS)] for k in range(len(ALPHAS)))
+                                 if step_ms[j::len(ALPHAS)]}},
         "plan": {"build_ms_per_alpha": plan_ms, "bytes": plan_bytes,
                  "note": "staircase plan built once per (profile version, alpha); table static in config 2"},
         "clocks": clk.summary(),

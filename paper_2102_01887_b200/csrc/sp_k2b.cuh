@@ -147,17 +147,31 @@ __device__ __forceinline__ void decide_plan(const uint8_t* base, const SelectIO&
   store_out(io, i, o);
 }
 
+// Ping-pong over two register buffers (unrolled by two so no buffer is ever copied): while
+// invocation i is decided from buffer A, invocation i + stride is already in flight into B.
 template <int KT, bool STAGED, bool KMIN>
 __device__ __forceinline__ void plan_loop(const uint8_t* smem, const PlanPtrs& pp, const int* s_off,
-                                          const SelectIO& io, int i, In<KT>& cur, In<KT>& nxt) {
+                                          const SelectIO& io, int i, In<KT>& a, In<KT>& b) {
+  const int stride = gridDim.x * blockDim.x;
+  for (; i < io.N; i += 2 * stride) {
+    decide_plan<KT, KMIN>(plan_base<STAGED>(smem, pp.p, s_off, a.t), io, i, a);
+    const int j = i + stride;
+    if (j >= io.N) break;
+    if (j + stride < io.N) load_in<KT>(io, j + stride, a);
+    decide_plan<KT, KMIN>(plan_base<STAGED>(smem, pp.p, s_off, b.t), io, j, b);
+    if (j + 2 * stride < io.N) load_in<KT>(io, j + 2 * stride, b);
+  }
+}
+
+// Variants off the hot path (Eq. 3 minima requested, or plans read from global memory).
+template <int KT, bool STAGED, bool KMIN>
+__device__ __forceinline__ void plan_loop_simple(const uint8_t* smem, const PlanPtrs& pp,
+                                              const int* s_off, const SelectIO& io, int i) {
   const int stride = gridDim.x * blockDim.x;
   for (; i < io.N; i += stride) {
-    const int j = i + 2 * stride;
-    In<KT> nn;
-    if (j < io.N) load_in<KT>(io, j, nn);  // prefetch two invocations ahead
-    decide_plan<KT, KMIN>(plan_base<STAGED>(smem, pp.p, s_off, cur.t), io, i, cur);
-    cur = nxt;
-    nxt = nn;
+    In<KT> x;
+    load_in<KT>(io, i, x);
+    decide_plan<KT, KMIN>(plan_base<STAGED>(smem, pp.p, s_off, x.t), io, i, x);
   }
 }
 
@@ -194,10 +208,10 @@ __global__ void __launch_bounds__(1024, 1) k_select_plan(PlanPtrs pp, int smem_b
   const bool kmin = io.out_kind_min != nullptr;
   if (s_fit) {
     mbar_wait(&s_bar, 0);
-    if (kmin) plan_loop<KT, true, true>(smem, pp, s_off, io, i, cur, nxt);
+    if (kmin) plan_loop_simple<KT, true, true>(smem, pp, s_off, io, i);
     else plan_loop<KT, true, false>(smem, pp, s_off, io, i, cur, nxt);
   } else {
-    if (kmin) plan_loop<KT, false, true>(smem, pp, s_off, io, i, cur, nxt);
-    else plan_loop<KT, false, false>(smem, pp, s_off, io, i, cur, nxt);
+    if (kmin) plan_loop_simple<KT, false, true>(smem, pp, s_off, io, i);
+    else plan_loop_simple<KT, false, false>(smem, pp, s_off, io, i);
   }
 }
