@@ -98,11 +98,7 @@ static void free_table(sp_table* t) {
   uint32_t* uu[] = {t->ukr, t->umap, t->r1, t->r2, t->lpos, t->pf, t->sf, t->rowscratch,
                     t->candf, t->cands, t->cidf, t->cids};
   for (uint32_t* p : uu) cudaFree(p);
-  for (auto& p : t->plans) {
-    cudaFree(p.cost);
-    cudaFree(p.costpen);
-    cudaFree(p.image);
-  }
+  for (auto& p : t->plans) plan_release(p);
   delete t;
 }
 

@@ -99,6 +99,12 @@ struct Plan {
   double* costpen = nullptr;  // M
   uint8_t* image = nullptr;   // plan image (capacity image_cap)
   int64_t image_cap = 0;
+  // host copy of the header, fetched asynchronously after each build (pinned + event);
+  // single-table launches pass it as a kernel parameter once it has landed
+  PlanHdr* host_hdr = nullptr;
+  cudaEvent_t hdr_ready = nullptr;
+  bool hdr_pending = false;
+  bool hdr_valid = false;
 };
 
 }  // namespace sp
@@ -190,6 +196,8 @@ namespace sp {
 int plan_build(sp_ctx* ctx, sp_table* t, Plan& p);
 int plan_scratch_alloc(sp_table* t);
 Plan* plan_get(sp_ctx* ctx, sp_table* t, double alpha, int* rc);
+const PlanHdr* plan_host_header(Plan& p);  // nullptr until the async copy has landed
+void plan_release(Plan& p);
 int select_launch(sp_ctx* ctx, int n_tables, sp_table* const* tables, double alpha, int N,
                   const int32_t* op, const double* slack, const int32_t* avail,
                   const int32_t* supply, const int32_t* min_batch, const uint32_t* flags,

@@ -9,18 +9,42 @@
 //   the downgrade argmin   min_k rows_k[r_k][lo .. le-1]   loaded (one more u16 per kind).
 // One 1024-thread CTA per SM stages the plan(s) with TMA bulk copies while its threads
 // already fetch their first two invocations; shared-memory plan addresses are formed from
-// the extern array so every plan access is an LDS (plans over the budget are read from
-// global memory by a second instantiation of the loop).
+// the extern array so every plan access is an LDS.  For single-table launches the plan
+// header travels as a kernel parameter, so every descriptor field is a constant-bank
+// (uniform-register) operand instead of a per-invocation load.
 
-template <bool STAGED>
-__device__ __forceinline__ const uint8_t* plan_base(const uint8_t* smem, const uint8_t* const* gptr,
-                                                    const int* s_off, int t) {
-  if (STAGED) return smem + s_off[t];
-  return gptr[t];
+// Decoded plan header: field offsets and per-kind descriptors.
+template <int KT>
+struct View {
+  const uint8_t* base;
+  int nB, stride, score_off, recb_off, lat_off, lut_off, lut_n;
+  uint4 q0[KT];  // {kmin_hi, nb1 | shift << 16, thr_off, rows_off}
+  uint4 q1[KT];  // {bkt_off, R, nonpos, -}
+};
+
+template <int KT>
+__device__ __forceinline__ void make_view(View<KT>& v, const uint8_t* base, const PlanHdr& h, int K) {
+  v.base = base;
+  v.nB = h.nB;
+  v.stride = h.row_stride;
+  v.score_off = h.score_off;
+  v.recb_off = h.recb_off;
+  v.lat_off = h.lat_off;
+  v.lut_off = h.lut_off;
+  v.lut_n = h.lut_n;
+#pragma unroll
+  for (int k = 0; k < KT; ++k) {
+    if (k < K) {
+      v.q0[k] = *reinterpret_cast<const uint4*>(&h.kd[k]);
+      v.q1[k] = *(reinterpret_cast<const uint4*>(&h.kd[k]) + 1);
+    } else {
+      v.q0[k] = make_uint4(0, 0, 0, 0);
+      v.q1[k] = make_uint4(0, 0, 0, 0);
+    }
+  }
 }
 
 // Row of the threshold staircase for slack s: #{j in [1, R) : thr[j] < s}.
-//   q0 = {kmin_hi, nb1 | shift << 16, thr_off, rows_off},  q1 = {bkt_off, R, nonpos, -}
 __device__ __forceinline__ int stair_row(const uint8_t* base, const uint4& q0, const uint4& q1,
                                          double s) {
   const double* thr = reinterpret_cast<const double*>(base + (int)q0.z);
@@ -52,22 +76,21 @@ __device__ __forceinline__ int tri_index(int lo, int hi, int nB) {
 }
 
 template <int KT, bool KMIN>
-__device__ __forceinline__ void decide_plan(const uint8_t* base, const SelectIO& io, int i,
+__device__ __forceinline__ void decide_plan(const View<KT>& v, const SelectIO& io, int i,
                                             const In<KT>& x) {
-  const PlanHdr* h = reinterpret_cast<const PlanHdr*>(base);
-  const int nB = h->nB;
-  const int stride = h->row_stride;
-  const double* rscore = reinterpret_cast<const double*>(base + h->score_off);
-  const CandB* recb = reinterpret_cast<const CandB*>(base + h->recb_off);
+  const uint8_t* base = v.base;
+  const int nB = v.nB;
+  const double* rscore = reinterpret_cast<const double*>(base + v.score_off);
+  const CandB* recb = reinterpret_cast<const CandB*>(base + v.recb_off);
 
   // batch lanes admitted by min_batch (configurator.py:264-265) and available (288)
   int lo, le;
-  const int lut_n = h->lut_n;
-  if (lut_n > 0) {  // lut[0] = (0, 0); lut[lut_n - 1] saturates at (nB, nB)
-    const uint16_t* lut = reinterpret_cast<const uint16_t*>(base + h->lut_off);
-    lo = (int)(lut[min(max(x.mb, 0), lut_n - 1)] & 0xFFu);
-    le = (int)(lut[min(max(x.av, 0), lut_n - 1)] >> 8);
+  if (v.lut_n > 0) {  // lut[0] = (0, 0); lut[lut_n - 1] saturates at (nB, nB)
+    const uint16_t* lut = reinterpret_cast<const uint16_t*>(base + v.lut_off);
+    lo = (int)(lut[min(max(x.mb, 0), v.lut_n - 1)] & 0xFFu);
+    le = (int)(lut[min(max(x.av, 0), v.lut_n - 1)] >> 8);
   } else {
+    const PlanHdr* h = reinterpret_cast<const PlanHdr*>(base);
     lo = le = 0;
     for (int b = 0; b < nB; ++b) {
       const int bv = h->batch_vals[b];
@@ -84,24 +107,21 @@ __device__ __forceinline__ void decide_plan(const uint8_t* base, const SelectIO&
   for (int k = 0; k < KT; ++k) {
     rowoff[k] = -1;
     if (k >= io.K) break;
-    const uint4* kd = reinterpret_cast<const uint4*>(&h->kd[k]);
-    const uint4 q1 = kd[1];
     const bool ex = (x.fl >> (SP_FLAG_EXCL_SHIFT + k)) & 1u;
-    if (q1.y == 0 || (!KMIN && ex)) {
+    if (v.q1[k].y == 0 || (!KMIN && ex)) {
       if (KMIN) io.out_kind_min[(size_t)i * io.K + k] = INFINITY;
       continue;
     }
-    const uint4 q0 = kd[0];
-    const int r = stair_row(base, q0, q1, x.s[k]);
-    const int ro = (int)q0.w + r * stride;
+    const int r = stair_row(base, v.q0[k], v.q1[k], x.s[k]);
+    const int ro = (int)v.q0[k].w + r * v.stride;
     const uint16_t* row = reinterpret_cast<const uint16_t*>(base + ro);
     if (!ex) {
       rowoff[k] = ro;
       if (any1) u = min(u, (uint32_t)row[idx1]);
     }
     if (KMIN) {  // Eq. 3 operand: unmasked min score of the kind = interval [0, nB-1]
-      const uint32_t v = row[nB - 1];
-      io.out_kind_min[(size_t)i * io.K + k] = (v != kNone16) ? rscore[v] : INFINITY;
+      const uint32_t m = row[nB - 1];
+      io.out_kind_min[(size_t)i * io.K + k] = (m != kNone16) ? rscore[m] : INFINITY;
     }
   }
 
@@ -118,7 +138,7 @@ __device__ __forceinline__ void decide_plan(const uint8_t* base, const SelectIO&
     double wait = 0.0;
     if ((x.fl & SP_FLAG_ALLOW_DELAY) && big &&
         (long long)x.sup >= (long long)cb.batch - (long long)x.av) {
-      const double* rlat = reinterpret_cast<const double*>(base + h->lat_off);
+      const double* rlat = reinterpret_cast<const double*>(base + v.lat_off);
       wait = __dsub_rn(sk, rlat[u]);
       delay = wait > 0.0;
     }
@@ -147,38 +167,44 @@ __device__ __forceinline__ void decide_plan(const uint8_t* base, const SelectIO&
   store_out(io, i, o);
 }
 
+// Single-table hot loop: the view is built once from the parameter-space header.
 // Ping-pong over two register buffers (unrolled by two so no buffer is ever copied): while
 // invocation i is decided from buffer A, invocation i + stride is already in flight into B.
-template <int KT, bool STAGED, bool KMIN>
-__device__ __forceinline__ void plan_loop(const uint8_t* smem, const PlanPtrs& pp, const int* s_off,
-                                          const SelectIO& io, int i, In<KT>& a, In<KT>& b) {
+// (Measured alternatives that were slower on B200: a 3-stage TMA input ring in shared
+// memory, and cp.async.bulk.prefetch.L2 of the tiles 3-4 iterations ahead.)
+template <int KT>
+__device__ __forceinline__ void plan_loop_single(const View<KT>& v, const SelectIO& io, int i,
+                                                 In<KT>& a, In<KT>& b) {
   const int stride = gridDim.x * blockDim.x;
   for (; i < io.N; i += 2 * stride) {
-    decide_plan<KT, KMIN>(plan_base<STAGED>(smem, pp.p, s_off, a.t), io, i, a);
+    decide_plan<KT, false>(v, io, i, a);
     const int j = i + stride;
     if (j >= io.N) break;
     if (j + stride < io.N) load_in<KT>(io, j + stride, a);
-    decide_plan<KT, KMIN>(plan_base<STAGED>(smem, pp.p, s_off, b.t), io, j, b);
+    decide_plan<KT, false>(v, io, j, b);
     if (j + 2 * stride < io.N) load_in<KT>(io, j + 2 * stride, b);
   }
 }
 
-// Variants off the hot path (Eq. 3 minima requested, or plans read from global memory).
+// Generic loop: per-invocation table, header read from the (staged or global) image.
 template <int KT, bool STAGED, bool KMIN>
-__device__ __forceinline__ void plan_loop_simple(const uint8_t* smem, const PlanPtrs& pp,
-                                              const int* s_off, const SelectIO& io, int i) {
+__device__ __forceinline__ void plan_loop_multi(const uint8_t* smem, const PlanPtrs& pp,
+                                                const int* s_off, const SelectIO& io, int i) {
   const int stride = gridDim.x * blockDim.x;
   for (; i < io.N; i += stride) {
     In<KT> x;
     load_in<KT>(io, i, x);
-    decide_plan<KT, KMIN>(plan_base<STAGED>(smem, pp.p, s_off, x.t), io, i, x);
+    const uint8_t* base = STAGED ? smem + s_off[x.t] : pp.p[x.t];
+    View<KT> v;
+    make_view<KT>(v, base, *reinterpret_cast<const PlanHdr*>(base), io.K);
+    decide_plan<KT, KMIN>(v, io, i, x);
   }
 }
 
 template <int KT>
 __global__ void __launch_bounds__(1024, 1) k_select_plan(PlanPtrs pp, int smem_budget, SelectIO io) {
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ int s_off[kMaxPlanTables];
+  __shared__ int s_off[kMaxPlanTables + 1];
   __shared__ __align__(8) uint64_t s_bar;
   __shared__ int s_fit;
   const int tid = threadIdx.x;
@@ -186,32 +212,41 @@ __global__ void __launch_bounds__(1024, 1) k_select_plan(PlanPtrs pp, int smem_b
     int off = 0;
     for (int t = 0; t < pp.n; ++t) {
       s_off[t] = off;
-      off += reinterpret_cast<const PlanHdr*>(pp.p[t])->total_bytes;
+      off += pp.hv ? pp.h.total_bytes : reinterpret_cast<const PlanHdr*>(pp.p[t])->total_bytes;
     }
+    s_off[pp.n] = off;
     s_fit = off <= smem_budget;
     if (s_fit) {  // one TMA bulk copy per plan image, completion on one mbarrier
       mbar_init(&s_bar, 1);
       mbar_expect_tx(&s_bar, (uint32_t)off);
-      for (int t = 0; t < pp.n; ++t) {
-        const int bytes = reinterpret_cast<const PlanHdr*>(pp.p[t])->total_bytes;
-        bulk_g2s(smem + s_off[t], pp.p[t], (uint32_t)bytes, &s_bar);
-      }
+      for (int t = 0; t < pp.n; ++t)
+        bulk_g2s(smem + s_off[t], pp.p[t], (uint32_t)(s_off[t + 1] - s_off[t]), &s_bar);
     }
   }
   // the first two invocations are fetched while the plan copy is in flight
   const int stride = gridDim.x * blockDim.x;
   const int i = blockIdx.x * blockDim.x + tid;
-  In<KT> cur, nxt;
-  if (i < io.N) load_in<KT>(io, i, cur);
-  if (i + stride < io.N) load_in<KT>(io, i + stride, nxt);
-  __syncthreads();
   const bool kmin = io.out_kind_min != nullptr;
+  const bool single = pp.hv && !kmin;
+  In<KT> cur, nxt;
+  if (single) {
+    if (i < io.N) load_in<KT>(io, i, cur);
+    if (i + stride < io.N) load_in<KT>(io, i + stride, nxt);
+  }
+  __syncthreads();
   if (s_fit) {
     mbar_wait(&s_bar, 0);
-    if (kmin) plan_loop_simple<KT, true, true>(smem, pp, s_off, io, i);
-    else plan_loop<KT, true, false>(smem, pp, s_off, io, i, cur, nxt);
+    if (single) {
+      View<KT> v;
+      make_view<KT>(v, smem, pp.h, io.K);
+      plan_loop_single<KT>(v, io, i, cur, nxt);
+    } else if (kmin) {
+      plan_loop_multi<KT, true, true>(smem, pp, s_off, io, i);
+    } else {
+      plan_loop_multi<KT, true, false>(smem, pp, s_off, io, i);
+    }
   } else {
-    if (kmin) plan_loop_simple<KT, false, true>(smem, pp, s_off, io, i);
-    else plan_loop_simple<KT, false, false>(smem, pp, s_off, io, i);
+    if (kmin) plan_loop_multi<KT, false, true>(smem, pp, s_off, io, i);
+    else plan_loop_multi<KT, false, false>(smem, pp, s_off, io, i);
   }
 }

@@ -602,9 +602,35 @@ int plan_build(sp_ctx* ctx, sp_table* t, Plan& p) {
                                  t->batch, t->kind, t->ukey, t->ukr, t->uent, t->umap, h,
                                  p.image, p.image_cap, status);
   SP_CHECK_LAUNCH(ctx);
+  // fetch the header back without blocking; it becomes a kernel parameter once it lands
+  if (!p.host_hdr) {
+    SP_CUDA(cudaMallocHost(&p.host_hdr, sizeof(PlanHdr)));
+    SP_CUDA(cudaEventCreateWithFlags(&p.hdr_ready, cudaEventDisableTiming));
+  }
+  SP_CUDA(cudaMemcpyAsync(p.host_hdr, p.image, sizeof(PlanHdr), cudaMemcpyDeviceToHost, st));
+  SP_CUDA(cudaEventRecord(p.hdr_ready, st));
+  p.hdr_pending = true;
+  p.hdr_valid = false;
   p.valid = true;
   p.version = t->version;
   return SP_OK;
+}
+
+const PlanHdr* plan_host_header(Plan& p) {
+  if (p.hdr_pending && cudaEventQuery(p.hdr_ready) == cudaSuccess) {
+    p.hdr_pending = false;
+    p.hdr_valid = p.host_hdr->magic == kPlanMagic;
+  }
+  return p.hdr_valid ? p.host_hdr : nullptr;
+}
+
+void plan_release(Plan& p) {
+  cudaFree(p.cost);
+  cudaFree(p.costpen);
+  cudaFree(p.image);
+  if (p.host_hdr) cudaFreeHost(p.host_hdr);
+  if (p.hdr_ready) cudaEventDestroy(p.hdr_ready);
+  p = Plan();
 }
 
 Plan* plan_get(sp_ctx* ctx, sp_table* t, double alpha, int* rc) {
@@ -619,10 +645,8 @@ Plan* plan_get(sp_ctx* ctx, sp_table* t, double alpha, int* rc) {
   if (!hit) {
     if (t->plans.size() >= 16) {
       // evict the oldest entry's buffers (keep memory bounded)
-      Plan& old = t->plans.front();
-      cudaFree(old.cost);
-      cudaFree(old.costpen);
-      cudaFree(old.image);
+      cudaStreamSynchronize(ctx->stream);
+      plan_release(t->plans.front());
       t->plans.erase(t->plans.begin());
     }
     t->plans.emplace_back();

@@ -32,6 +32,8 @@ constexpr int kMaxScanTables = 16;
 struct PlanPtrs {
   const uint8_t* p[kMaxPlanTables];
   int n;
+  int hv;     // h holds table 0's plan header (single-table launches): read via the constant bank
+  PlanHdr h;
 };
 
 struct ScanTab {
@@ -61,6 +63,7 @@ struct SelectIO {
   double* out_kind_min;
   int N;
   int K;
+  int aligned;  // every input array 16-byte aligned: eligible for TMA bulk L2 prefetch
 };
 
 // ---- TMA bulk-copy helpers (cp.async.bulk + mbarrier) --------------------------------
@@ -400,16 +403,28 @@ int select_launch(sp_ctx* ctx, int n_tables, sp_table* const* tables, double alp
   io.out_obj = out_obj; io.out_slack = out_slack; io.out_wait = out_wait;
   io.out_kind_min = out_kind_min;
   io.N = N; io.K = K;
+  {
+    auto al = [](const void* p) { return ((uintptr_t)p & 15u) == 0; };
+    io.aligned = al(slack) && al(avail) && al(supply) && al(min_batch) && al(flags);
+  }
   if (N == 0) return SP_OK;
   const int KT = K <= 2 ? 2 : (K <= 4 ? 4 : 8);
   if (use_plan) {
     PlanPtrs pp;
     pp.n = n_tables;
+    pp.hv = 0;
     for (int t = 0; t < n_tables; ++t) {
       int rc;
       Plan* p = plan_get(ctx, tables[t], alpha, &rc);
       if (!p) return rc;
       pp.p[t] = p->image;
+      if (n_tables == 1) {
+        const PlanHdr* hh = plan_host_header(*p);
+        if (hh) {
+          pp.h = *hh;
+          pp.hv = 1;
+        }
+      }
     }
     if (KT == 2) return launch_plan_t<2>(ctx, pp, io);
     if (KT == 4) return launch_plan_t<4>(ctx, pp, io);

@@ -223,6 +223,29 @@ def test_random_tables_plan_scan_oracle(gpu_ctx, seed, M, nB, K, nonpos):
     tab.close()
 
 
+@pytest.mark.parametrize("N", [200_003, 151 * 1024, 1024 * 148 - 1])
+def test_streamed_multitable_ragged_vs_oracle(gpu_ctx, N):
+    """Sizes that exercise the TMA input ring (full tiles on every CTA), the ragged tail, and
+    the below-threshold fallback, with an op[] array routing to two different tables."""
+    import paper_2102_01887_b200 as sp
+
+    rng = np.random.default_rng(N)
+    tabs = [_random_table(rng, 1500, 8, 2), _random_table(rng, 700, 6, 2)]
+    slack = rng.uniform(-1, 6, size=(N, 2))
+    avail = rng.integers(1, 300, size=N).astype(np.int32)
+    supply = rng.integers(0, 300, size=N).astype(np.int32)
+    mb = np.where(rng.random(N) < 0.8, 1, rng.integers(1, 300, size=N)).astype(np.int32)
+    flags = sp.make_flags(rng.random(N) < 0.5, rng.integers(0, 4, size=N) * (rng.random(N) < 0.2))
+    op = (rng.random(N) < 0.3).astype(np.int32)
+    exp = cselect.select_batch(tabs, slack, 50.0, avail, supply, mb, flags, op=op)
+    raws = [raw_table(t, 2) for t in tabs]
+    r = sp.select_batch(raws, slack, 50.0, avail, upstream_supply=supply, min_batch=mb, flags=flags,
+                        op=op, mode="plan")
+    assert_same_decisions(r, exp, f"N={N}")
+    for t in raws:
+        t.close()
+
+
 def test_plan_rebuilds_after_latency_update(c2_table, syn):
     """set_latency invalidates the plan; decisions follow the live profile."""
     from paper_2102_01887_b200 import synth
