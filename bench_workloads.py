@@ -1,0 +1,283 @@
+"""BASELINE.json configs 3-5 on B200 (invoked as `python bench.py --workload c3|c4|c5`).
+
+c3  deep DAG: 64 ops, 845 edges (~3.3e9 decomposed paths, which the reference cannot
+    enumerate), 100,000 pipeline instances, 4 backend kinds: Alg. 1 slack for every
+    (instance, op, kind) through K1.  CPU baseline: the exact forward-DP restatement (oracle,
+    labelled "restatement, not reference") on all host cores over a 1,000-instance sample.
+c4  latency-target sweep x replicas on the AMBER pipeline: 10,000 replicas x 5 targets
+    (0.5x..10x the fast-anchor latency) x 64 snapshots; per snapshot K1 (7 ops x 4 kinds) feeds
+    K2 directly on the device (one decision per op) — 22.4M decisions per step.
+c5  online mode: 2^24 invocations x 16,384 configurations in 256 batches of 65,536; every batch is
+    decided against the batch-start profile snapshot, the chosen configurations produce noisy
+    latency observations, and K3 folds them back (the next batch's plan is rebuilt on device).
+All numbers are device time (CUDA events), inputs resident in HBM; one JSON line on stdout.
+"""
+from __future__ import annotations
+
+import json
+import math
+import os
+import statistics
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+
+def _events(torch, n):
+    return [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n)]
+
+
+def _flush_factory(torch, dev):
+    buf = torch.ones(256 << 20, dtype=torch.uint8, device=dev)
+    return lambda: buf.max()
+
+
+def _peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    return float(json.loads(p.read_text())["hbm_gbs"]) if p.exists() else 6650.0
+
+
+# ---- c3 -------------------------------------------------------------------------------------
+
+def _c3_cpu_worker(args):
+    from oracle import slack as osl
+
+    order, preds, term, vcol, ref, T, now, Q = args
+    out = []
+    for i in range(len(T)):
+        refo = ref[i][vcol]
+        for s in range(len(order)):
+            lo, hi = osl.dp_ratios(order, preds, term, refo, s)
+            for k in range(Q.shape[1]):
+                out.append(osl.dp_slack(lo, hi, (T[i] - now[i]) - Q[i, k]))
+    return len(out)
+
+
+def run_c3(args):
+    import torch
+
+    import paper_2102_01887_b200 as sp
+    from paper_2102_01887_b200 import synth
+
+    dev = torch.device("cuda", 0)
+    stream = torch.cuda.current_stream(dev)
+    ctx = sp.get_context(0)
+    ctx.set_stream(stream.cuda_stream)
+    dag = synth.deep_dag()
+    I, K = 100_000, 4
+    ref, T, now, Q = synth.deep_dag_instances(dag, I, K=K)
+    g = sp.SlackGraph.from_dag(dag)
+    V = len(dag.vertices)
+    d = {k: torch.from_numpy(np.ascontiguousarray(v)).to(dev) for k, v in
+         (("ref", ref), ("T", T), ("now", now), ("Q", Q))}
+    out = {"slack": torch.empty((I, V, K), dtype=torch.float64, device=dev)}
+    flush = _flush_factory(torch, dev)
+    for _ in range(args.warmup):
+        g.slack_batch(d["ref"], d["T"], d["now"], d["Q"], out=out)
+    torch.cuda.synchronize(dev)
+    evs = _events(torch, args.steps)
+    l0 = ctx.launch_count
+    for i in range(args.steps):
+        flush()
+        evs[i][0].record(stream)
+        g.slack_batch(d["ref"], d["T"], d["now"], d["Q"], out=out)
+        evs[i][1].record(stream)
+    torch.cuda.synchronize(dev)
+    ms = [a.elapsed_time(b) for a, b in evs]
+    t = sum(ms) / 1e3
+    vals = args.steps * I * V * K
+    bytes_inst = 8 * V + 16 + 8 * K + 8 * V * K
+    # CPU: the exact DP restatement on all host cores over a bounded sample
+    order = dag.topological_order()
+    pos = {v: j for j, v in enumerate(order)}
+    preds = [[pos[p] for p in dag.predecessors(v)] for v in order]
+    term = [not dag.successors(v) for v in order]
+    vcol = [dag.vertices.index(v) for v in order]
+    cores = os.cpu_count() or 1
+    S = args.c3_cpu_instances
+    import multiprocessing as mp
+
+    chunks = np.array_split(np.arange(S), cores)
+    work = [(order, preds, term, vcol, ref[c], T[c], now[c], Q[c]) for c in chunks if len(c)]
+    t0 = time.perf_counter()
+    with mp.get_context("fork").Pool(len(work)) as pool:
+        n_cpu = sum(pool.map(_c3_cpu_worker, work))
+    cpu_t = time.perf_counter() - t0
+    line = {
+        "workload": "c3", "metric": "Alg. 1 slack values (instance x op x kind) / s", "unit": "slack/s",
+        "value": vals / t, "ms_per_step": 1e3 * t / args.steps, "steps": args.steps, "n_gpus": 1,
+        "config": {"ops": V, "edges": len(dag.edges), "instances": I, "kinds": K,
+                   "decomposed_paths": "~3.3e9 (not enumerable by the reference)"},
+        "instances_per_s": args.steps * I / t,
+        "roofline": {"bound": "fp64/lds issue (exact forward DP, DESIGN.md §3)",
+                     "hbm_bytes_per_instance": bytes_inst,
+                     "hbm_frac": (args.steps * I * bytes_inst / t / 1e9) / _peaks()},
+        "gpu_launches": ctx.launch_count - l0,
+        "cpu_baseline": {"value": n_cpu / cpu_t, "unit": "slack/s", "cores": cores,
+                         "kind": "restatement (the reference cannot run this DAG)",
+                         "sample": f"{S} instances, oracle/slack.py dp_ratios on {cores} processes"},
+        "step_ms": {"median": statistics.median(ms), "min": min(ms), "max": max(ms)},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---- c4 -------------------------------------------------------------------------------------
+
+def _amber_tables(sp, meta):
+    sc = sp.Scenario("branching", tuple(sp.BackendSpec(k, n, r, p) for k, n, r, p in meta["backends"]))
+    tabs = []
+    for name in meta["ops"]:
+        m = meta["tables"][name]
+        ents = [sp.ConfigEntry(cid, k, {}, b, r, lat, li) for cid, k, r, b, lat, li in
+                zip(m["config_id"], m["kind"], m["res"], m["batch"], m["lat"], m["lat_init"])]
+        if m["ref_index"] < 0:
+            res = int(m["ref_id"].split("-r", 1)[1].split("-", 1)[0])
+            ents.append(sp.ConfigEntry(m["ref_id"], "cpu", {}, 1, res, 1.0, 1.0, schedulable=False))
+        tabs.append(sp.OpTable(sp.ConfigSpec(name, ents, m["ref_id"]), sc, kinds=meta["kinds"]))
+    return tabs
+
+
+def run_c4(args):
+    import torch
+
+    import paper_2102_01887_b200 as sp
+
+    with np.load(ROOT / "tests" / "golden" / "amber_trace.npz") as z:
+        meta = json.loads(bytes(z["meta_json"]).decode())
+    dev = torch.device("cuda", 0)
+    stream = torch.cuda.current_stream(dev)
+    ctx = sp.get_context(0)
+    ctx.set_stream(stream.cuda_stream)
+    tabs = _amber_tables(sp, meta)
+    ops = meta["ops"]
+    V, K = len(ops), len(meta["kinds"])
+    g = sp.SlackGraph.from_paths([tuple(p) for p in meta["paths"]], ops)
+    ref0 = np.array([meta["tables"][o]["lat"][meta["tables"][o]["ref_index"]]
+                     if meta["tables"][o]["ref_index"] >= 0 else 1.0 for o in ops])
+    # value order of the graph = names in path order; map
+    vpos = [ops.index(n) for n in g.value_names]
+    R, mults, S = args.c4_replicas, (0.5, 1.0, 2.0, 5.0, 10.0), 64
+    cp_min = 90.41885182994682
+    I = R * len(mults) * S
+    rng = np.random.default_rng(4)
+    target = np.repeat(np.array(mults) * cp_min, S)[None, :].repeat(R, 0).reshape(-1)
+    now = (np.tile(np.arange(S) / S, R * len(mults))) * target
+    Q = rng.exponential(1.0, size=(I, K)) * (0.02 * target)[:, None]
+    ref = (ref0[vpos][None, :] * np.exp(rng.normal(0.0, 0.2, size=(I, len(vpos)))))
+    N = I * V
+    avail = rng.integers(1, 65, size=N).astype(np.int32)
+    supply = rng.integers(0, 65, size=N).astype(np.int32)
+    flags = np.ones(N, np.uint32)
+    op = np.tile(np.arange(V, dtype=np.int32), I)
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    d = {"ref": T(ref), "target": T(target), "now": T(now), "Q": T(Q), "avail": T(avail),
+         "supply": T(supply), "mb": T(np.ones(N, np.int32)), "flags": T(flags.astype(np.int32)),
+         "op": T(op)}
+    slack = torch.empty((I, V, K), dtype=torch.float64, device=dev)
+    out = {k: torch.empty(N, dtype=dt, device=dev) for k, dt in
+           (("idx", torch.int32), ("code", torch.int32), ("fill", torch.int32),
+            ("obj", torch.float64), ("slack", torch.float64), ("wait", torch.float64))}
+    alpha = 100.0
+    for t in tabs:
+        t.prepare(alpha)
+    torch.cuda.synchronize(dev)
+
+    def step():
+        g.slack_batch(d["ref"], d["target"], d["now"], d["Q"], out={"slack": slack})
+        sp.select_batch(tabs, slack.view(N, K), alpha, d["avail"], upstream_supply=d["supply"],
+                        min_batch=d["mb"], flags=d["flags"], op=d["op"], out=out)
+
+    flush = _flush_factory(torch, dev)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    evs = _events(torch, args.steps)
+    l0 = ctx.launch_count
+    for i in range(args.steps):
+        flush()
+        evs[i][0].record(stream)
+        step()
+        evs[i][1].record(stream)
+    torch.cuda.synchronize(dev)
+    ms = [a.elapsed_time(b) for a, b in evs]
+    t = sum(ms) / 1e3
+    evals_per_inst = sum(len(x.entries) for x in tabs)
+    codes = torch.bincount(out["code"] & 3, minlength=3).cpu().tolist()
+    line = {
+        "workload": "c4", "metric": "config decisions/s (K1 slack -> K2 select, on device)",
+        "unit": "decisions/s", "value": args.steps * N / t, "ms_per_step": 1e3 * t / args.steps,
+        "steps": args.steps, "n_gpus": 1,
+        "evals_per_s": args.steps * I * evals_per_inst / t,
+        "config": {"replicas": R, "targets_x_cp_min": list(mults), "snapshots": S, "instances": I,
+                   "ops": V, "kinds": K, "decisions_per_step": N, "cp_min": cp_min},
+        "decision_mix": {"none": codes[0], "assign": codes[1], "delay": codes[2]},
+        "gpu_launches": ctx.launch_count - l0,
+        "step_ms": {"median": statistics.median(ms), "min": min(ms), "max": max(ms)},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---- c5 -------------------------------------------------------------------------------------
+
+def run_c5(args):
+    import torch
+
+    import paper_2102_01887_b200 as sp
+    from paper_2102_01887_b200 import synth
+
+    dev = torch.device("cuda", 0)
+    stream = torch.cuda.current_stream(dev)
+    ctx = sp.get_context(0)
+    ctx.set_stream(stream.cuda_stream)
+    spec = synth.synth_spec(True)
+    table = sp.OpTable(spec, synth.synth_scenario())
+    M = len(table.entries)
+    B, NB = 65536, args.c5_batches
+    N = B * NB
+    inv = synth.synth_invocations(N, table.lat, table.gkind, seed=5)
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    d = {"slack": T(inv.slack), "avail": T(inv.avail), "supply": T(inv.supply),
+         "mb": T(inv.min_batch), "flags": T(inv.flags.astype(np.int32))}
+    lat_init = T(np.array([e.latency_initial_s for e in table.entries]))
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(5)
+    noise = torch.exp(0.3 * torch.randn(N, dtype=torch.float64, device=dev, generator=gen))
+    out = {k: torch.empty(B, dtype=dt, device=dev) for k, dt in
+           (("idx", torch.int32), ("code", torch.int32), ("fill", torch.int32),
+            ("obj", torch.float64), ("slack", torch.float64), ("wait", torch.float64))}
+    obs_idx = torch.empty(B, dtype=torch.int32, device=dev)
+    alpha = 100.0
+    table.prepare(alpha)
+    torch.cuda.synchronize(dev)
+    l0 = ctx.launch_count
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for b in range(NB):
+        s = slice(b * B, (b + 1) * B)
+        table.select_batch(d["slack"][s], alpha, d["avail"][s], upstream_supply=d["supply"][s],
+                           min_batch=d["mb"][s], flags=d["flags"][s], out=out)
+        # the chosen configurations run: observation = truth(config) * lognormal noise;
+        # delayed / None decisions produce no observation (idx = -1)
+        torch.where((out["code"] & 3) == 1, out["idx"], torch.full_like(out["idx"], -1), out=obs_idx)
+        obs = lat_init[obs_idx.clamp(min=0).long()] * noise[s]
+        sp.fold_observations([table], None, obs_idx, obs, beta=0.5, dfp_count=10, sync_host=False)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    t = e0.elapsed_time(e1) / 1e3
+    line = {
+        "workload": "c5", "metric": "online config decisions/s incl. per-batch feedback fold and replanning",
+        "unit": "decisions/s", "value": N / t, "evals_per_s": N * M / t, "seconds": t, "n_gpus": 1,
+        "config": {"invocations": N, "configs": M, "batches": NB, "batch": B, "beta": 0.5, "dfp_count": 10},
+        "gpu_launches": ctx.launch_count - l0,
+        "per_batch_ms": 1e3 * t / NB,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main(args):
+    {"c3": run_c3, "c4": run_c4, "c5": run_c5}[args.workload](args)

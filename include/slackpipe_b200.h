@@ -162,7 +162,8 @@ int sp_queueing(sp_ctx* ctx, int32_t K, const int32_t* ptr, const double* lat,
 
 /* ---- K3: feedback fold (manager.py:436-457, configurator.py:463-491) ---------------- */
 /* Folds n observations (in completion order) into the tables: for observation j on table
- * tables[op[j]], entry idx[j], value obs[j]:
+ * tables[op[j]], entry idx[j], value obs[j] (idx[j] < 0 marks "no observation" and is skipped,
+ * so a decision batch's out_idx can be passed straight through):
  *   completed_ref += (idx == ref_index);  obs_count[idx] += 1;
  *   unless fb_frozen: lat[idx] = beta*obs + (1-beta)*lat[idx]            (manager.py:45-47)
  *   if idx == ref_index && completed_ref == dfp_count && dfp_on:        (manager.py:449-457)

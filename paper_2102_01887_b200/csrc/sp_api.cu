@@ -637,7 +637,7 @@ int sp_feedback_fold(sp_ctx* ctx, int32_t n_tables, sp_table* const* tables, int
   for (int j = 0; j < n; ++j) {
     int t = op ? op[j] : 0;
     if (t < 0 || t >= n_tables) return fail(SP_E_INVALID, "feedback_fold: op out of range");
-    if (idx[j] < 0 || idx[j] >= tables[t]->M)
+    if (idx[j] >= tables[t]->M)  // idx < 0: no observation (skipped)
       return fail(SP_E_INVALID, "feedback_fold: entry index out of range");
   }
   size_t need = 2 * rsz<int32_t>(n) + rsz<double>(n);

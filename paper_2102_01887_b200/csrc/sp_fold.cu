@@ -39,6 +39,7 @@ struct FoldTab {
 struct FoldTabs {
   FoldTab t[kMaxFoldTables];
   int n;
+  int total;  // entries over all tables; the sort key of a skipped observation (idx < 0)
 };
 // per-table gate state produced by k_fold_ref, consumed by the other two kernels
 struct Gate {
@@ -52,7 +53,7 @@ __global__ void k_fold_keys(int n, FoldTabs ft, const int32_t* __restrict__ op,
   int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n) return;
   int t = op ? op[j] : 0;
-  keys[j] = (uint32_t)(ft.t[t].gbase + idx[j]);
+  keys[j] = idx[j] < 0 ? (uint32_t)ft.total : (uint32_t)(ft.t[t].gbase + idx[j]);
   pos[j] = (uint32_t)j;
 }
 
@@ -128,6 +129,7 @@ __global__ void k_fold_seg(int n, FoldTabs ft, const uint32_t* __restrict__ skey
   if (q >= n) return;
   const uint32_t key = skeys[q];
   if (q > 0 && skeys[q - 1] == key) return;
+  if ((int)key >= ft.total) return;  // skipped observations (idx < 0) sort last
   const int t = table_of_key(ft, key);
   const FoldTab& tb = ft.t[t];
   const int e = (int)key - tb.gbase;
@@ -186,7 +188,8 @@ int fold_launch(sp_ctx* ctx, int n_tables, sp_table* const* tables, int n, const
     gb += tb->M;
     if (tb->M > maxM) maxM = tb->M;
   }
-  if (gb >= (1ll << 31)) return fail(SP_E_UNSUPPORTED, "fold: too many entries");
+  if (gb >= (1ll << 31) - 1) return fail(SP_E_UNSUPPORTED, "fold: too many entries");
+  ft.total = (int)gb;
   int end_bit = 1;
   while ((1ll << end_bit) <= gb) ++end_bit;
   cudaStream_t st = ctx->stream;

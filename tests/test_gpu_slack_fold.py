@@ -125,6 +125,28 @@ def test_feedback_fold_vs_reference(gpu_ctx, chunked):
             t.close()
 
 
+def test_feedback_fold_skips_negative_indices(gpu_ctx):
+    """idx < 0 marks 'no observation' (e.g. a None / delay decision passed straight through)."""
+    import paper_2102_01887_b200 as sp
+
+    rng = np.random.default_rng(12)
+    M = 300
+    lat0 = rng.uniform(0.1, 2.0, size=M)
+    idx = rng.integers(-1, M, size=5000).astype(np.int32)
+    idx[rng.random(5000) < 0.3] = -1
+    idx[::40] = 0
+    obs = rng.uniform(0.1, 3.0, size=5000)
+    tab = sp.RawTable(lat=lat0, res=np.ones(M), batch=np.ones(M, np.int32), pool=np.ones(M),
+                      price=np.ones(M), ref_index=0, lat_init=lat0)
+    sp.fold_observations([tab], None, idx, obs, beta=0.5, dfp_count=7, sync_host=False)
+    keep = idx >= 0
+    st = ofb.FoldState(lat0.copy(), lat0.copy(), 0)
+    ofb.fold([st], None, idx[keep], obs[keep], beta=0.5, dfp_count=7)
+    assert np.array_equal(bits(tab.get_latency()), bits(st.lat))
+    cref, cnt = sp.table_counters(tab)
+    assert cref == st.completed_ref and np.array_equal(cnt, st.obs_count)
+
+
 def test_feedback_fold_large_stream_vs_oracle(gpu_ctx):
     """A config-5-sized batch (65,536 observations over a 16,384-entry table, heavy skew)
     against the sequential oracle."""
