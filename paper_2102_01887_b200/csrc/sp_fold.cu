@@ -71,9 +71,33 @@ __device__ int lower_bound_u32(const uint32_t* a, int n, uint32_t key) {
   return lo;
 }
 
+// Observations in sorted (entry, completion) order: a parallel gather, so the sequential
+// recurrence below streams contiguous memory instead of chasing spos[] per step.
+__global__ void k_fold_gather(int n, const uint32_t* __restrict__ spos,
+                              const double* __restrict__ obs, double* __restrict__ sobs) {
+  int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < n) sobs[q] = obs[spos[q]];
+}
+
+// Sequential EWMA over sobs[q, end): loads are issued eight ahead of the dependent chain.
+__device__ __forceinline__ double fold_run(double L, const double* __restrict__ sobs, int q, int end,
+                                           double beta) {
+  const double ob = beta, ol = __dsub_rn(1.0, beta);
+  int u = q;
+  for (; u + 8 <= end; u += 8) {
+    double o[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) o[j] = __ldg(sobs + u + j);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) L = __dadd_rn(__dmul_rn(ob, o[j]), __dmul_rn(ol, L));
+  }
+  for (; u < end; ++u) L = __dadd_rn(__dmul_rn(ob, __ldg(sobs + u)), __dmul_rn(ol, L));
+  return L;
+}
+
 // One thread per table: fold the reference entry's segment, locate the gate lift.
 __global__ void k_fold_ref(int n, FoldTabs ft, const uint32_t* __restrict__ skeys,
-                           const uint32_t* __restrict__ spos, const double* __restrict__ obs,
+                           const uint32_t* __restrict__ spos, const double* __restrict__ sobs,
                            double beta, int dfp_count, int dfp_on, int fb_frozen, Gate* gates) {
   int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= ft.n) return;
@@ -87,28 +111,27 @@ __global__ void k_fold_ref(int n, FoldTabs ft, const uint32_t* __restrict__ skey
     return;
   }
   const uint32_t key = (uint32_t)(tb.gbase + tb.ref_index);
-  int q = lower_bound_u32(skeys, n, key);
-  int before = tb.counters[0];
-  int c = before;
-  double L = tb.lat[tb.ref_index];
-  int cnt = 0;
-  for (; q < n && skeys[q] == key; ++q) {
-    ++c;
-    ++cnt;
-    if (fb_frozen) continue;
-    L = ewma(beta, obs[spos[q]], L);
-    if (c == dfp_count && dfp_on) {
-      double init = tb.lat_init[tb.ref_index];
-      if (init > 0.0) {
-        g.lifted = 1;
-        g.gate_pos = (int)spos[q];
-        g.ratio = __ddiv_rn(L, init);  // configurator.py:486
-      }
-    }
-  }
+  const int q = lower_bound_u32(skeys, n, key);
+  const int end = lower_bound_u32(skeys, n, key + 1);
+  const int cnt = end - q;
+  const int before = tb.counters[0];
   if (cnt) {
-    tb.counters[0] = c;
-    tb.lat[tb.ref_index] = L;
+    if (!fb_frozen) {
+      double L = tb.lat[tb.ref_index];
+      // the k-th reference completion of this batch makes completed_ref == dfp_count
+      const int k = dfp_count - before;  // 1-based position inside the segment
+      if (dfp_on && k >= 1 && k <= cnt && tb.lat_init[tb.ref_index] > 0.0) {
+        L = fold_run(L, sobs, q, q + k, beta);
+        g.lifted = 1;
+        g.gate_pos = (int)spos[q + k - 1];
+        g.ratio = __ddiv_rn(L, tb.lat_init[tb.ref_index]);  // configurator.py:486
+        L = fold_run(L, sobs, q + k, end, beta);
+      } else {
+        L = fold_run(L, sobs, q, end, beta);
+      }
+      tb.lat[tb.ref_index] = L;
+    }
+    tb.counters[0] = before + cnt;
     tb.obs_count[tb.ref_index] += cnt;
   }
   gates[t] = g;
@@ -123,7 +146,7 @@ __device__ __forceinline__ int table_of_key(const FoldTabs& ft, uint32_t key) {
 
 // One thread per segment head (non-reference entries).
 __global__ void k_fold_seg(int n, FoldTabs ft, const uint32_t* __restrict__ skeys,
-                           const uint32_t* __restrict__ spos, const double* __restrict__ obs,
+                           const uint32_t* __restrict__ spos, const double* __restrict__ sobs,
                            double beta, int fb_frozen, const Gate* __restrict__ gates) {
   int q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= n) return;
@@ -134,8 +157,7 @@ __global__ void k_fold_seg(int n, FoldTabs ft, const uint32_t* __restrict__ skey
   const FoldTab& tb = ft.t[t];
   const int e = (int)key - tb.gbase;
   if (e == tb.ref_index) return;  // folded by k_fold_ref
-  int end = q;
-  while (end < n && skeys[end] == key) ++end;
+  const int end = lower_bound_u32(skeys, n, key + 1);
   const int cnt = end - q;
   const int before = tb.obs_count[e];
   if (!fb_frozen) {
@@ -145,8 +167,7 @@ __global__ void k_fold_seg(int n, FoldTabs ft, const uint32_t* __restrict__ skey
     // rescaled by recalibrate_unobserved before its first fold
     if (g.lifted && before == 0 && (int)spos[q] > g.gate_pos)
       L = __dmul_rn(tb.lat_init[e], g.ratio);
-    for (int u = q; u < end; ++u) L = ewma(beta, obs[spos[u]], L);
-    tb.lat[e] = L;
+    tb.lat[e] = fold_run(L, sobs, q, end, beta);
   }
   tb.obs_count[e] = before + cnt;
 }
@@ -201,7 +222,7 @@ int fold_launch(sp_ctx* ctx, int n_tables, sp_table* const* tables, int n, const
                                     (uint32_t*)nullptr, n, 0, end_bit, st);
   size_t a = ((size_t)n * 4 + 255) & ~(size_t)255;
   size_t gates_bytes = ((size_t)n_tables * sizeof(Gate) + 255) & ~(size_t)255;
-  size_t total = 4 * a + gates_bytes + cub_bytes + 256;
+  size_t total = 4 * a + gates_bytes + cub_bytes + 256 + (((size_t)n * 8 + 255) & ~(size_t)255);
   int rc = SP_OK;
   uint8_t* base = (uint8_t*)ctx_tmp(ctx, total, &rc);
   if (!base) return rc;
@@ -211,18 +232,21 @@ int fold_launch(sp_ctx* ctx, int n_tables, sp_table* const* tables, int n, const
   uint32_t* spos = (uint32_t*)(base + 3 * a);
   Gate* gates = (Gate*)(base + 4 * a);
   void* cub_tmp = base + 4 * a + gates_bytes;
+  double* sobs = (double*)(base + 4 * a + gates_bytes + ((cub_bytes + 255) & ~(size_t)255));
   if (n > 0) {
     k_fold_keys<<<(n + 255) / 256, 256, 0, st>>>(n, ft, op, idx, keys, pos);
     SP_CHECK_LAUNCH(ctx);
     SP_CUDA(cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, keys, skeys, pos, spos, n, 0,
                                             end_bit, st));
     ctx->launches += 2;  // upsweep/downsweep passes (at least)
+    k_fold_gather<<<(n + 255) / 256, 256, 0, st>>>(n, spos, obs, sobs);
+    SP_CHECK_LAUNCH(ctx);
   }
-  k_fold_ref<<<(n_tables + 63) / 64, 64, 0, st>>>(n, ft, skeys, spos, obs, beta, dfp_count,
+  k_fold_ref<<<(n_tables + 63) / 64, 64, 0, st>>>(n, ft, skeys, spos, sobs, beta, dfp_count,
                                                  dfp_on, fb_frozen, gates);
   SP_CHECK_LAUNCH(ctx);
   if (n > 0) {
-    k_fold_seg<<<(n + 255) / 256, 256, 0, st>>>(n, ft, skeys, spos, obs, beta, fb_frozen,
+    k_fold_seg<<<(n + 255) / 256, 256, 0, st>>>(n, ft, skeys, spos, sobs, beta, fb_frozen,
                                                 gates);
     SP_CHECK_LAUNCH(ctx);
   }
