@@ -5,6 +5,7 @@
 // kernels of sp_plan.cu / sp_select.cu / sp_slack.cu / sp_fold.cu.  No decision, score or
 // slack is ever computed on the host.
 #include <algorithm>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -144,6 +145,17 @@ int sp_ctx_destroy(sp_ctx* ctx) {
   cudaFree(ctx->io_dev);
   cudaFree(ctx->ptr_dev);
   cudaFree(ctx->tmp_dev);
+  if (ctx->h2d) {
+    cudaStreamSynchronize(ctx->h2d);
+    cudaStreamSynchronize(ctx->d2h);
+    cudaStreamDestroy(ctx->h2d);
+    cudaStreamDestroy(ctx->d2h);
+    for (int c = 0; c < sp_ctx::kPipeChunks; ++c) {
+      cudaEventDestroy(ctx->ev_in[c]);
+      cudaEventDestroy(ctx->ev_comp[c]);
+      cudaEventDestroy(ctx->ev_out[c]);
+    }
+  }
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
   return SP_OK;
@@ -402,32 +414,67 @@ int sp_select_batch(sp_ctx* ctx, int32_t n_tables, sp_table* const* tables, doub
   double* d_sl = b.take<double>(N);
   double* d_wait = b.take<double>(N);
   double* d_kmin = out_kind_min ? b.take<double>((size_t)N * K) : nullptr;
-  if (N > 0) {
-    SP_CUDA(cudaMemcpyAsync(d_slack, slack, sizeof(double) * N * K, cudaMemcpyHostToDevice, st));
-    SP_CUDA(cudaMemcpyAsync(d_avail, avail, sizeof(int32_t) * N, cudaMemcpyHostToDevice, st));
-    SP_CUDA(cudaMemcpyAsync(d_supply, supply, sizeof(int32_t) * N, cudaMemcpyHostToDevice, st));
-    SP_CUDA(cudaMemcpyAsync(d_minb, min_batch, sizeof(int32_t) * N, cudaMemcpyHostToDevice, st));
-    SP_CUDA(cudaMemcpyAsync(d_flags, flags, sizeof(uint32_t) * N, cudaMemcpyHostToDevice, st));
-    if (op) SP_CUDA(cudaMemcpyAsync(d_op, op, sizeof(int32_t) * N, cudaMemcpyHostToDevice, st));
+  // Pipeline over chunks: H2D of chunk c+1 and D2H of chunk c-1 (separate copy streams, both
+  // PCIe directions at once) overlap the decision kernel of chunk c.
+  constexpr int kChunkMin = 1 << 18;  // 4 chunks for 2^20 invocations (measured best on B200)
+  int nchunk = N >= 2 * kChunkMin
+                   ? std::min(sp_ctx::kPipeChunks, (N + kChunkMin - 1) / kChunkMin)
+                   : 1;
+  if (const char* e = getenv("SP_PIPE_CHUNKS")) nchunk = std::max(1, std::min(sp_ctx::kPipeChunks, atoi(e)));
+  if (nchunk > 1 && !ctx->h2d) {
+    SP_CUDA(cudaStreamCreateWithFlags(&ctx->h2d, cudaStreamNonBlocking));
+    SP_CUDA(cudaStreamCreateWithFlags(&ctx->d2h, cudaStreamNonBlocking));
+    for (int c = 0; c < sp_ctx::kPipeChunks; ++c) {
+      SP_CUDA(cudaEventCreateWithFlags(&ctx->ev_in[c], cudaEventDisableTiming));
+      SP_CUDA(cudaEventCreateWithFlags(&ctx->ev_comp[c], cudaEventDisableTiming));
+      SP_CUDA(cudaEventCreateWithFlags(&ctx->ev_out[c], cudaEventDisableTiming));
+    }
   }
-  rc = select_launch(ctx, n_tables, tables, alpha, N, d_op, d_slack, d_avail, d_supply, d_minb,
-                     d_flags, d_idx, d_code, d_fill, d_obj, d_sl, d_wait, d_kmin, mode);
-  if (rc != SP_OK) return rc;
-  if (N > 0) {
-    SP_CUDA(cudaMemcpyAsync(out_idx, d_idx, sizeof(int32_t) * N, cudaMemcpyDeviceToHost, st));
-    SP_CUDA(cudaMemcpyAsync(out_code, d_code, sizeof(int32_t) * N, cudaMemcpyDeviceToHost, st));
-    if (out_fill)
-      SP_CUDA(cudaMemcpyAsync(out_fill, d_fill, sizeof(int32_t) * N, cudaMemcpyDeviceToHost, st));
-    if (out_obj)
-      SP_CUDA(cudaMemcpyAsync(out_obj, d_obj, sizeof(double) * N, cudaMemcpyDeviceToHost, st));
-    if (out_slack)
-      SP_CUDA(cudaMemcpyAsync(out_slack, d_sl, sizeof(double) * N, cudaMemcpyDeviceToHost, st));
-    if (out_wait)
-      SP_CUDA(cudaMemcpyAsync(out_wait, d_wait, sizeof(double) * N, cudaMemcpyDeviceToHost, st));
+  cudaStream_t sin = nchunk > 1 ? ctx->h2d : st;
+  cudaStream_t sout = nchunk > 1 ? ctx->d2h : st;
+  if (nchunk > 1) {  // copy streams must not overtake earlier work on the compute stream
+    SP_CUDA(cudaEventRecord(ctx->ev_out[0], st));
+    SP_CUDA(cudaStreamWaitEvent(sin, ctx->ev_out[0], 0));
+    SP_CUDA(cudaStreamWaitEvent(sout, ctx->ev_out[0], 0));
+  }
+  const auto h2d = cudaMemcpyHostToDevice;
+  const auto d2h = cudaMemcpyDeviceToHost;
+  for (int c = 0; c < nchunk; ++c) {
+    const size_t a = (size_t)N * c / nchunk, n = (size_t)N * (c + 1) / nchunk - a;
+    if (n == 0) continue;
+    SP_CUDA(cudaMemcpyAsync(d_slack + a * K, slack + a * K, sizeof(double) * n * K, h2d, sin));
+    SP_CUDA(cudaMemcpyAsync(d_avail + a, avail + a, sizeof(int32_t) * n, h2d, sin));
+    SP_CUDA(cudaMemcpyAsync(d_supply + a, supply + a, sizeof(int32_t) * n, h2d, sin));
+    SP_CUDA(cudaMemcpyAsync(d_minb + a, min_batch + a, sizeof(int32_t) * n, h2d, sin));
+    SP_CUDA(cudaMemcpyAsync(d_flags + a, flags + a, sizeof(uint32_t) * n, h2d, sin));
+    if (op) SP_CUDA(cudaMemcpyAsync(d_op + a, op + a, sizeof(int32_t) * n, h2d, sin));
+    if (nchunk > 1) {
+      SP_CUDA(cudaEventRecord(ctx->ev_in[c], sin));
+      SP_CUDA(cudaStreamWaitEvent(st, ctx->ev_in[c], 0));
+    }
+    rc = select_launch(ctx, n_tables, tables, alpha, (int)n, d_op ? d_op + a : nullptr,
+                       d_slack + a * K, d_avail + a, d_supply + a, d_minb + a, d_flags + a,
+                       d_idx + a, d_code + a, d_fill + a, d_obj + a, d_sl + a, d_wait + a,
+                       d_kmin ? d_kmin + a * K : nullptr, mode);
+    if (rc != SP_OK) return rc;
+    if (nchunk > 1) {
+      SP_CUDA(cudaEventRecord(ctx->ev_comp[c], st));
+      SP_CUDA(cudaStreamWaitEvent(sout, ctx->ev_comp[c], 0));
+    }
+    SP_CUDA(cudaMemcpyAsync(out_idx + a, d_idx + a, sizeof(int32_t) * n, d2h, sout));
+    SP_CUDA(cudaMemcpyAsync(out_code + a, d_code + a, sizeof(int32_t) * n, d2h, sout));
+    if (out_fill) SP_CUDA(cudaMemcpyAsync(out_fill + a, d_fill + a, sizeof(int32_t) * n, d2h, sout));
+    if (out_obj) SP_CUDA(cudaMemcpyAsync(out_obj + a, d_obj + a, sizeof(double) * n, d2h, sout));
+    if (out_slack) SP_CUDA(cudaMemcpyAsync(out_slack + a, d_sl + a, sizeof(double) * n, d2h, sout));
+    if (out_wait) SP_CUDA(cudaMemcpyAsync(out_wait + a, d_wait + a, sizeof(double) * n, d2h, sout));
     if (out_kind_min)
-      SP_CUDA(cudaMemcpyAsync(out_kind_min, d_kmin, sizeof(double) * N * K,
-                              cudaMemcpyDeviceToHost, st));
+      SP_CUDA(cudaMemcpyAsync(out_kind_min + a * K, d_kmin + a * K, sizeof(double) * n * K, d2h, sout));
   }
+  if (nchunk > 1) {  // the compute stream's later work must see the completed outputs
+    SP_CUDA(cudaEventRecord(ctx->ev_out[0], sout));
+    SP_CUDA(cudaStreamWaitEvent(st, ctx->ev_out[0], 0));
+  }
+  SP_CUDA(cudaStreamSynchronize(sout));
   SP_CUDA(cudaStreamSynchronize(st));
   return SP_OK;
 }

@@ -125,6 +125,10 @@ struct sp_ctx {
   // generic device scratch (sort temp etc.)
   void* tmp_dev = nullptr;
   size_t tmp_cap = 0;
+  // host-buffer pipeline: H2D and D2H copy streams (full-duplex PCIe) + per-chunk events
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  static constexpr int kPipeChunks = 8;
+  cudaEvent_t ev_in[kPipeChunks] = {}, ev_comp[kPipeChunks] = {}, ev_out[kPipeChunks] = {};
 };
 
 struct sp_table {

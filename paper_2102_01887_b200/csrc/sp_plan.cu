@@ -395,7 +395,7 @@ __global__ void __launch_bounds__(1024) k_finalize(
           // positive thresholds: the high word of the encoding is monotone
           kmin = (uint32_t)__double2hiint(thrscratch[ext + 1]);
           const uint32_t kmax = (uint32_t)__double2hiint(thrscratch[ext + R - 1]);
-          while (nbk < 4 * (R - 1) && nbk < kMaxBuckets) nbk <<= 1;
+          while (nbk < 2 * (R - 1) && nbk < kMaxBuckets) nbk <<= 1;
           while (((kmax - kmin) >> shift) >= (uint32_t)nbk) ++shift;
           d.pad[0] = !(thrscratch[ext + 1] > 0.0);  // non-positive latency: generic search
         }

@@ -20,6 +20,10 @@
 // Both then apply the safe-delayed-batching rule and the downgrade argmin
 // (configurator.py:271-300).
 #include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <algorithm>
 
 #include "sp_internal.cuh"
 
@@ -341,12 +345,38 @@ int launch_plan_t(sp_ctx* ctx, const PlanPtrs& pp, const SelectIO& io) {
   if (!attr_done) {
     SP_CUDA(cudaFuncSetAttribute(k_select_plan<KT>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kPlanSmemBudget));
+    SP_CUDA(cudaFuncSetAttribute(k_select_pair<KT>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, kPlanSmemBudget));
+    SP_CUDA(cudaFuncSetAttribute(k_select_lean<KT>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
     attr_done = true;
+  }
+  const char* variant = getenv("SP_K2_VARIANT");
+  const bool single = pp.hv && pp.n == 1 && !io.out_kind_min;
+  if (single && variant && !strcmp(variant, "lean")) {
+    int blocks = ctx->num_sms * 2;
+    int need = (io.N + 767) / 768;
+    if (need < blocks) blocks = need > 0 ? need : 1;
+    k_select_lean<KT><<<blocks, 768, 100 * 1024, ctx->stream>>>(pp, 100 * 1024, io);
+    SP_CHECK_LAUNCH(ctx);
+    return SP_OK;
+  }
+  if (single && variant && !strcmp(variant, "pair")) {
+    int blocks = ctx->num_sms;
+    int need = (io.N + 511) / 512;
+    if (need < blocks) blocks = need > 0 ? need : 1;
+    k_select_pair<KT><<<blocks, 512, kPlanSmemBudget, ctx->stream>>>(pp, kPlanSmemBudget, io);
+    SP_CHECK_LAUNCH(ctx);
+    return SP_OK;
   }
   int blocks = ctx->num_sms * kPlanCtasPerSm;
   int need = (io.N + kPlanThreads - 1) / kPlanThreads;
   if (need < blocks) blocks = need > 0 ? need : 1;
-  k_select_plan<KT><<<blocks, kPlanThreads, kPlanSmemBudget, ctx->stream>>>(pp, kPlanSmemBudget, io);
+  // request only the shared memory the staged plan needs when its size is known on the host
+  int smem = kPlanSmemBudget;
+  if (pp.hv && pp.n == 1 && !getenv("SP_FULL_SMEM"))
+    smem = std::min(kPlanSmemBudget, ((pp.h.total_bytes + 1023) / 1024) * 1024);
+  k_select_plan<KT><<<blocks, kPlanThreads, smem, ctx->stream>>>(pp, smem, io);
   SP_CHECK_LAUNCH(ctx);
   return SP_OK;
 }
