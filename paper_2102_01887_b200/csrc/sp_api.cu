@@ -527,11 +527,12 @@ int sp_dag_create(sp_ctx* ctx, int32_t V, const int32_t* pred_ptr, const int32_t
   for (int v = 0; v < V; ++v)
     for (int q = pred_ptr[v]; q < pred_ptr[v + 1]; ++q) succ[pred_idx[q]].push_back(v);
   std::vector<int4> prog;
-  std::vector<int32_t> pptr(1, 0);
-  std::vector<uint16_t> preds;
-  int max_span = 0, n_val = 0;
+  std::vector<int32_t> pptr(1, 0), qptr(1, 0);
+  std::vector<uint32_t> preds;
+  int max_span = 0, max_slots = 0, max_preds = 0, n_val = 0;
   for (int v = 0; v < V; ++v) n_val = std::max(n_val, val_idx[v] + 1);
-  std::vector<int> slot(V, -1);
+  std::vector<int> slot(V, -1), last(V, -1);
+  std::vector<int> free_slots;
   for (int s = 0; s < n_src; ++s) {
     int src = sources[s];
     if (src < 0 || src >= V) return fail(SP_E_INVALID, "dag_create: source out of range");
@@ -541,22 +542,59 @@ int sp_dag_create(sp_ctx* ctx, int32_t V, const int32_t* pred_ptr, const int32_t
     for (int v = src; v < V; ++v)
       if (reach[v])
         for (int w : succ[v]) reach[w] = 1;
-    int nslot = 0;
+    // last reader of each reachable value (vertices are in topological order, so the
+    // largest reachable successor id); a value without readers dies where it is made
     for (int v = src; v < V; ++v) {
       if (!reach[v]) continue;
-      slot[v] = nslot++;
-      int pb = (int)preds.size();
+      last[v] = v;
+      for (int w : succ[v]) last[v] = std::max(last[v], w);
+    }
+    free_slots.clear();
+    int nslot = 0, nprog = 0;
+    const int qbase = (int)preds.size();
+    for (int v = src; v < V; ++v) {
+      if (!reach[v]) continue;
+      ++nprog;
+      const int pb = (int)preds.size() - qbase;
       if (v != src) {
         for (int q = pred_ptr[v]; q < pred_ptr[v + 1]; ++q) {
           int p = pred_idx[q];
-          if (slot[p] >= 0) preds.push_back((uint16_t)slot[p]);
+          if (reach[p]) preds.push_back((uint32_t)slot[p]);
+        }
+        if (((int)preds.size() - qbase - pb) & 1) preds.push_back(preds.back());
+        // predecessors read for the last time here release their slots; the kernel reads
+        // every predecessor before it writes the new value, so v may take one of them
+        for (int q = pred_ptr[v]; q < pred_ptr[v + 1]; ++q) {
+          int p = pred_idx[q];
+          if (reach[p] && last[p] == v && slot[p] >= 0) {
+            free_slots.push_back(slot[p]);
+            slot[p] = -2;  // released (a predecessor may be listed twice)
+          }
         }
       }
-      prog.push_back(make_int4(val_idx[v], terminal[v] ? 1 : 0, pb, (int)preds.size()));
+      int sl;
+      if (!free_slots.empty()) {
+        sl = free_slots.back();
+        free_slots.pop_back();
+      } else {
+        sl = nslot++;
+      }
+      if (last[v] == v) {
+        free_slots.push_back(sl);  // only the terminal fold reads it
+        slot[v] = -2;
+      } else {
+        slot[v] = sl;
+      }
+      const int npairs = ((int)preds.size() - qbase - pb) >> 1;
+      prog.push_back(make_int4(val_idx[v], sl | (terminal[v] ? 1 << 16 : 0), pb, npairs));
     }
-    if (nslot > 65535) return fail(SP_E_UNSUPPORTED, "dag_create: too many descendants");
-    max_span = std::max(max_span, nslot);
+    if (nslot > 65535 || (int)preds.size() - qbase > (1 << 24))
+      return fail(SP_E_UNSUPPORTED, "dag_create: too many descendants");
+    max_span = std::max(max_span, nprog);
+    max_slots = std::max(max_slots, nslot);
+    max_preds = std::max(max_preds, (int)preds.size() - qbase);
     pptr.push_back((int32_t)prog.size());
+    qptr.push_back((int32_t)preds.size());
   }
   sp_dag* g = new (std::nothrow) sp_dag();
   if (!g) return fail(SP_E_NOMEM, "dag_create: host allocation");
@@ -564,20 +602,26 @@ int sp_dag_create(sp_ctx* ctx, int32_t V, const int32_t* pred_ptr, const int32_t
   g->n_src = n_src;
   g->n_val = n_val;
   g->max_span = max_span;
+  g->max_slots = max_slots;
+  g->max_preds = max_preds;
   g->prog_len = (int64_t)prog.size();
   g->pred_len = (int64_t)preds.size();
   cudaError_t e = cudaMalloc(&g->prog, sizeof(int4) * prog.size());
   if (e == cudaSuccess) e = cudaMalloc(&g->prog_ptr, sizeof(int32_t) * pptr.size());
-  if (e == cudaSuccess) e = cudaMalloc(&g->preds, sizeof(uint16_t) * std::max<size_t>(1, preds.size()));
+  if (e == cudaSuccess) e = cudaMalloc(&g->pred_ptr, sizeof(int32_t) * qptr.size());
+  if (e == cudaSuccess) e = cudaMalloc(&g->preds, sizeof(uint32_t) * std::max<size_t>(4, preds.size()));
   if (e == cudaSuccess)
     e = cudaMemcpy(g->prog, prog.data(), sizeof(int4) * prog.size(), cudaMemcpyHostToDevice);
   if (e == cudaSuccess)
     e = cudaMemcpy(g->prog_ptr, pptr.data(), sizeof(int32_t) * pptr.size(), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess)
+    e = cudaMemcpy(g->pred_ptr, qptr.data(), sizeof(int32_t) * qptr.size(), cudaMemcpyHostToDevice);
   if (e == cudaSuccess && !preds.empty())
-    e = cudaMemcpy(g->preds, preds.data(), sizeof(uint16_t) * preds.size(), cudaMemcpyHostToDevice);
+    e = cudaMemcpy(g->preds, preds.data(), sizeof(uint32_t) * preds.size(), cudaMemcpyHostToDevice);
   if (e != cudaSuccess) {
     cudaFree(g->prog);
     cudaFree(g->prog_ptr);
+    cudaFree(g->pred_ptr);
     cudaFree(g->preds);
     delete g;
     return cuda_fail(e, "dag_create");
@@ -591,6 +635,7 @@ int sp_dag_destroy(sp_ctx* ctx, sp_dag* g) {
   if (ctx) cudaStreamSynchronize(ctx->stream);
   cudaFree(g->prog);
   cudaFree(g->prog_ptr);
+  cudaFree(g->pred_ptr);
   cudaFree(g->preds);
   delete g;
   return SP_OK;

@@ -166,12 +166,19 @@ struct sp_dag {
   int32_t V = 0, n_src = 0, n_val = 0;
   // Per-source vertex programs: prog[prog_ptr[s] .. prog_ptr[s+1]) lists
   // source s and then its descendants in topological order as int4
-  // {value index, terminal flag, pred begin, pred end}; preds holds predecessor SLOTS
-  // (positions inside the same program) as u16.
+  //   {value index, out slot | terminal << 16, pred offset, pred groups}.
+  // Slots are DP registers reused once every reader of a value has run (liveness), so a
+  // lane needs max_slots of them.  preds[pred_ptr[s] ..] holds the source's predecessor
+  // slots, each vertex's list padded to an even length by repeating its last entry
+  // (max / min are idempotent); the pred offset is relative to pred_ptr[s].  The kernel
+  // turns slots into shared-memory byte offsets when it stages the program.
   int4* prog = nullptr;         // device
   int32_t* prog_ptr = nullptr;  // device, n_src + 1
-  uint16_t* preds = nullptr;    // device
-  int32_t max_span = 0;         // max program length (DP slots per lane)
+  uint32_t* preds = nullptr;    // device
+  int32_t* pred_ptr = nullptr;  // device, n_src + 1
+  int32_t max_span = 0;         // max program length
+  int32_t max_slots = 0;        // max live DP values per lane
+  int32_t max_preds = 0;        // max padded pred entries of one source
   int64_t prog_len = 0, pred_len = 0;
 };
 
