@@ -12,11 +12,24 @@
 //
 // Device restatement (bit-exact): the EWMA recurrence is order-dependent, so it is NOT
 // tree-reduced; instead the observation batch is stably sorted by (table, entry) with a CUB
-// radix sort (positions ascending inside each key = completion order), and one thread folds
-// each entry's segment sequentially.  The gate lift is located inside the reference entry's
-// own segment (the k-th reference observation, k = dfp_count - completed_ref_before); an entry
-// is rescaled iff it had no observation before the batch and its first observation in the
-// batch comes after the gate position — exactly the set recalibrate_unobserved sees.
+// radix sort (positions ascending inside each key = completion order), and each entry's
+// segment is folded in completion order.  The gate lift is located inside the reference
+// entry's own segment (the k-th reference observation, k = dfp_count - completed_ref_before);
+// an entry is rescaled iff it had no observation before the batch and its first observation
+// in the batch comes after the gate position — exactly the set recalibrate_unobserved sees.
+//
+// Long segments (a hot configuration can receive most of a batch) use a coalescing window
+// instead of a sequential chain tens of thousands of steps long.  One step
+// x -> fl(fl(beta*o) + fl((1-beta)*x)) is monotone non-decreasing in x (beta in (0, 1]), so the
+// fold of a window is a monotone function of the window's input.  Every chain value lies in
+// [lo, hi] (the range of the start value and the segment's observations, widened by a
+// rounding margin, see fold_bounds); if the chains started at lo and at hi over the last W
+// observations end on the same bits, every input in [lo, hi] — the true one included — gives
+// exactly that value.  Otherwise the segment is folded sequentially.  W is sized so that a
+// gap of 2^80 ulps decays below one ulp (80 / -log2(1 - beta) steps).
+#include <algorithm>
+#include <math.h>
+
 #include <cub/cub.cuh>
 
 #include "sp_internal.cuh"
@@ -95,39 +108,131 @@ __device__ __forceinline__ double fold_run(double L, const double* __restrict__ 
   return L;
 }
 
-// One thread per table: fold the reference entry's segment, locate the gate lift.
+// The chains from lo and from hi over sobs[w0, end), interleaved (two independent chains).
+__device__ __forceinline__ bool fold_window(const double* __restrict__ sobs, int w0, int end,
+                                            double beta, double lo, double hi, double* out) {
+  const double ob = beta, ol = __dsub_rn(1.0, beta);
+  double a = lo, b = hi;
+  int u = w0;
+  for (; u + 4 <= end; u += 4) {
+    double o[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) o[j] = __ldg(sobs + u + j);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const double t = __dmul_rn(ob, o[j]);
+      a = __dadd_rn(t, __dmul_rn(ol, a));
+      b = __dadd_rn(t, __dmul_rn(ol, b));
+    }
+  }
+  for (; u < end; ++u) {
+    const double t = __dmul_rn(ob, __ldg(sobs + u));
+    a = __dadd_rn(t, __dmul_rn(ol, a));
+    b = __dadd_rn(t, __dmul_rn(ol, b));
+  }
+  *out = a;
+  return __double_as_longlong(a) == __double_as_longlong(b);
+}
+
+// Exact fold of sobs[q, end) from L; bounds (lo, hi) must hold every chain value.
+__device__ __forceinline__ double fold_exact(double L, const double* __restrict__ sobs, int q,
+                                             int end, double beta, int win, bool bounded,
+                                             double lo, double hi) {
+  if (bounded && end - q > win) {
+    double v;
+    if (fold_window(sobs, end - win, end, beta, lo, hi, &v)) return v;
+  }
+  return fold_run(L, sobs, q, end, beta);
+}
+
+// Block-wide bounds of every chain value of a fold of sobs[q, end) started at L.  With
+// ob = beta, ol = fl(1 - beta) >= 0, ob + ol <= 1 + u, a step from values in [m, M] stays in
+// [m (1 - u)^4, M (1 + u)^4] (u = 2^-53) up to subnormal absolute error; over fewer than 2^31
+// steps the relative drift is below 2^-20, so [m - |m| 2^-20 - 2^-1000, M + |M| 2^-20 +
+// 2^-1000] holds the whole chain.  Non-finite values disable the window.  Result in
+// bnd[0..1], finite flag in *ok (valid after the trailing barrier).
+__device__ void fold_bounds(const double* __restrict__ sobs, int q, int end, double L,
+                            double* bnd, int* ok) {
+  __shared__ double smin[32], smax[32];
+  __shared__ int sbad[32];
+  double m = L, M = L;
+  int bad = isfinite(L) ? 0 : 1;
+  for (int u = q + threadIdx.x; u < end; u += blockDim.x) {
+    const double o = __ldg(sobs + u);
+    bad |= isfinite(o) ? 0 : 1;
+    m = o < m ? o : m;
+    M = o > M ? o : M;
+  }
+  for (int d = 16; d; d >>= 1) {
+    const double om = __shfl_xor_sync(0xffffffffu, m, d), oM = __shfl_xor_sync(0xffffffffu, M, d);
+    m = om < m ? om : m;
+    M = oM > M ? oM : M;
+    bad |= __shfl_xor_sync(0xffffffffu, bad, d);
+  }
+  const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    smin[w] = m;
+    smax[w] = M;
+    sbad[w] = bad;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int j = 1; j < nw; ++j) {
+      m = smin[j] < m ? smin[j] : m;
+      M = smax[j] > M ? smax[j] : M;
+      bad |= sbad[j];
+    }
+    bnd[0] = m - fabs(m) * 0x1p-20 - 0x1p-1000;
+    bnd[1] = M + fabs(M) * 0x1p-20 + 0x1p-1000;
+    *ok = !bad;
+  }
+  __syncthreads();
+}
+
+// One block per table: fold the reference entry's segment, locate the gate lift.  Block 0
+// also resets the long-segment queue filled by k_fold_seg.
 __global__ void k_fold_ref(int n, FoldTabs ft, const uint32_t* __restrict__ skeys,
                            const uint32_t* __restrict__ spos, const double* __restrict__ sobs,
-                           double beta, int dfp_count, int dfp_on, int fb_frozen, Gate* gates) {
-  int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= ft.n) return;
+                           double beta, int win, int dfp_count, int dfp_on, int fb_frozen,
+                           Gate* gates, int* long_count) {
+  __shared__ int seg[2];
+  __shared__ double bnd[2];
+  __shared__ int bnd_ok;
+  const int t = blockIdx.x;
+  if (t == 0 && threadIdx.x == 0) *long_count = 0;
   FoldTab tb = ft.t[t];
-  Gate g;
-  g.lifted = 0;
-  g.gate_pos = -1;
-  g.ratio = 1.0;
   if (tb.ref_index < 0) {
-    gates[t] = g;
+    if (threadIdx.x == 0) gates[t] = Gate{0, -1, 1.0};
     return;
   }
   const uint32_t key = (uint32_t)(tb.gbase + tb.ref_index);
-  const int q = lower_bound_u32(skeys, n, key);
-  const int end = lower_bound_u32(skeys, n, key + 1);
-  const int cnt = end - q;
+  if (threadIdx.x == 0) {
+    seg[0] = lower_bound_u32(skeys, n, key);
+    seg[1] = lower_bound_u32(skeys, n, key + 1);
+  }
+  __syncthreads();
+  const int q = seg[0], end = seg[1], cnt = end - q;
+  const double L0 = tb.lat[tb.ref_index];
+  const bool bounded = !fb_frozen && cnt > win;
+  if (bounded) fold_bounds(sobs, q, end, L0, bnd, &bnd_ok);
+  if (threadIdx.x != 0) return;
+  Gate g{0, -1, 1.0};
   const int before = tb.counters[0];
   if (cnt) {
     if (!fb_frozen) {
-      double L = tb.lat[tb.ref_index];
+      const bool bd = bounded && bnd_ok;
+      const double lo = bounded ? bnd[0] : 0.0, hi = bounded ? bnd[1] : 0.0;
+      double L = L0;
       // the k-th reference completion of this batch makes completed_ref == dfp_count
       const int k = dfp_count - before;  // 1-based position inside the segment
       if (dfp_on && k >= 1 && k <= cnt && tb.lat_init[tb.ref_index] > 0.0) {
-        L = fold_run(L, sobs, q, q + k, beta);
+        L = fold_exact(L, sobs, q, q + k, beta, win, bd, lo, hi);
         g.lifted = 1;
         g.gate_pos = (int)spos[q + k - 1];
         g.ratio = __ddiv_rn(L, tb.lat_init[tb.ref_index]);  // configurator.py:486
-        L = fold_run(L, sobs, q + k, end, beta);
+        L = fold_exact(L, sobs, q + k, end, beta, win, bd, lo, hi);
       } else {
-        L = fold_run(L, sobs, q, end, beta);
+        L = fold_exact(L, sobs, q, end, beta, win, bd, lo, hi);
       }
       tb.lat[tb.ref_index] = L;
     }
@@ -144,10 +249,19 @@ __device__ __forceinline__ int table_of_key(const FoldTabs& ft, uint32_t key) {
   return t;
 }
 
-// One thread per segment head (non-reference entries).
+struct LongSeg {
+  int32_t q, end;
+  double* dst;
+  double L0;
+  int64_t pad;
+};
+
+// One thread per segment head (non-reference entries); segments longer than long_min are
+// queued for k_fold_long.
 __global__ void k_fold_seg(int n, FoldTabs ft, const uint32_t* __restrict__ skeys,
                            const uint32_t* __restrict__ spos, const double* __restrict__ sobs,
-                           double beta, int fb_frozen, const Gate* __restrict__ gates) {
+                           double beta, int fb_frozen, const Gate* __restrict__ gates,
+                           int long_min, LongSeg* long_q, int* long_count) {
   int q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= n) return;
   const uint32_t key = skeys[q];
@@ -167,9 +281,29 @@ __global__ void k_fold_seg(int n, FoldTabs ft, const uint32_t* __restrict__ skey
     // rescaled by recalibrate_unobserved before its first fold
     if (g.lifted && before == 0 && (int)spos[q] > g.gate_pos)
       L = __dmul_rn(tb.lat_init[e], g.ratio);
-    tb.lat[e] = fold_run(L, sobs, q, end, beta);
+    if (cnt > long_min) {
+      const int j = atomicAdd(long_count, 1);
+      long_q[j] = LongSeg{q, end, tb.lat + e, L, 0};
+    } else {
+      tb.lat[e] = fold_run(L, sobs, q, end, beta);
+    }
   }
   tb.obs_count[e] = before + cnt;
+}
+
+// One block per queued long segment: bounds, then the coalescing window (or the chain).
+__global__ void k_fold_long(const double* __restrict__ sobs, double beta, int win,
+                            const LongSeg* __restrict__ long_q, const int* __restrict__ long_count) {
+  __shared__ double bnd[2];
+  __shared__ int bnd_ok;
+  const int nl = *long_count;
+  for (int j = blockIdx.x; j < nl; j += gridDim.x) {
+    const LongSeg sg = long_q[j];
+    fold_bounds(sobs, sg.q, sg.end, sg.L0, bnd, &bnd_ok);
+    if (threadIdx.x == 0)
+      *sg.dst = fold_exact(sg.L0, sobs, sg.q, sg.end, beta, win, bnd_ok, bnd[0], bnd[1]);
+    __syncthreads();
+  }
 }
 
 // Entries of gated tables that were never observed at all: plain rescale.
@@ -220,9 +354,20 @@ int fold_launch(sp_ctx* ctx, int n_tables, sp_table* const* tables, int n, const
     cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, (const uint32_t*)nullptr,
                                     (uint32_t*)nullptr, (const uint32_t*)nullptr,
                                     (uint32_t*)nullptr, n, 0, end_bit, st);
+  // coalescing window: ol^win * 2^80 < 1 ulp  (ol = 1 - beta); disabled when it would be long
+  const double ol = 1.0 - beta;
+  int win = 8;
+  if (ol > 0.0) {
+    const double w = ceil(80.0 / -log2(ol));
+    win = w > 4096.0 ? (1 << 30) : (w < 8.0 ? 8 : (int)w);
+  }
+  const int long_min = win >= (1 << 30) ? (1 << 30) : std::max(2 * win, 512);
+  const int long_cap = n / (long_min + 1) + 1;
   size_t a = ((size_t)n * 4 + 255) & ~(size_t)255;
   size_t gates_bytes = ((size_t)n_tables * sizeof(Gate) + 255) & ~(size_t)255;
-  size_t total = 4 * a + gates_bytes + cub_bytes + 256 + (((size_t)n * 8 + 255) & ~(size_t)255);
+  size_t long_bytes = ((size_t)long_cap * sizeof(LongSeg) + 256 + 255) & ~(size_t)255;
+  size_t total = 4 * a + gates_bytes + long_bytes + cub_bytes + 256 +
+                 (((size_t)n * 8 + 255) & ~(size_t)255);
   int rc = SP_OK;
   uint8_t* base = (uint8_t*)ctx_tmp(ctx, total, &rc);
   if (!base) return rc;
@@ -231,8 +376,11 @@ int fold_launch(sp_ctx* ctx, int n_tables, sp_table* const* tables, int n, const
   uint32_t* skeys = (uint32_t*)(base + 2 * a);
   uint32_t* spos = (uint32_t*)(base + 3 * a);
   Gate* gates = (Gate*)(base + 4 * a);
-  void* cub_tmp = base + 4 * a + gates_bytes;
-  double* sobs = (double*)(base + 4 * a + gates_bytes + ((cub_bytes + 255) & ~(size_t)255));
+  int* long_count = (int*)(base + 4 * a + gates_bytes);
+  LongSeg* long_q = (LongSeg*)(base + 4 * a + gates_bytes + 256);
+  void* cub_tmp = base + 4 * a + gates_bytes + long_bytes;
+  double* sobs = (double*)(base + 4 * a + gates_bytes + long_bytes +
+                           ((cub_bytes + 255) & ~(size_t)255));
   if (n > 0) {
     k_fold_keys<<<(n + 255) / 256, 256, 0, st>>>(n, ft, op, idx, keys, pos);
     SP_CHECK_LAUNCH(ctx);
@@ -242,13 +390,18 @@ int fold_launch(sp_ctx* ctx, int n_tables, sp_table* const* tables, int n, const
     k_fold_gather<<<(n + 255) / 256, 256, 0, st>>>(n, spos, obs, sobs);
     SP_CHECK_LAUNCH(ctx);
   }
-  k_fold_ref<<<(n_tables + 63) / 64, 64, 0, st>>>(n, ft, skeys, spos, sobs, beta, dfp_count,
-                                                 dfp_on, fb_frozen, gates);
+  k_fold_ref<<<n_tables, 256, 0, st>>>(n, ft, skeys, spos, sobs, beta, win, dfp_count, dfp_on,
+                                       fb_frozen, gates, long_count);
   SP_CHECK_LAUNCH(ctx);
   if (n > 0) {
     k_fold_seg<<<(n + 255) / 256, 256, 0, st>>>(n, ft, skeys, spos, sobs, beta, fb_frozen,
-                                                gates);
+                                                gates, long_min, long_q, long_count);
     SP_CHECK_LAUNCH(ctx);
+    if (!fb_frozen && long_min < n) {
+      k_fold_long<<<std::min(long_cap, 2 * ctx->num_sms), 256, 0, st>>>(sobs, beta, win, long_q,
+                                                                        long_count);
+      SP_CHECK_LAUNCH(ctx);
+    }
   }
   if (!fb_frozen && dfp_on) {
     dim3 grid((maxM + 255) / 256, n_tables);

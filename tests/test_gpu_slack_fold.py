@@ -172,3 +172,37 @@ def test_feedback_fold_large_stream_vs_oracle(gpu_ctx):
     assert np.array_equal(bits(tab.get_latency()), bits(st.lat))
     cref, cnt = sp.table_counters(tab)
     assert cref == st.completed_ref and np.array_equal(cnt, st.obs_count)
+
+
+@pytest.mark.parametrize("beta", [0.5, 0.3, 0.1, 0.9, 1.0, 0.01])
+def test_feedback_fold_long_segments_vs_oracle(gpu_ctx, beta):
+    """Hot entries with tens of thousands of observations in one batch take the coalescing
+    window path (sp_fold.cu): the result must still equal the sequential fold bit for bit,
+    including the gate inside a long reference segment, a segment whose range is too wide to
+    coalesce (1e300 in its prefix: sequential fallback) and a non-finite observation."""
+    import paper_2102_01887_b200 as sp
+
+    rng = np.random.default_rng(int(beta * 1000) + 7)
+    M, n = 4096, 60000
+    lat0 = np.exp(rng.uniform(np.log(1e-3), np.log(1.0), size=M))
+    ref_index = 0
+    u = rng.random(n)
+    idx = np.where(u < 0.55, 7, np.where(u < 0.75, ref_index, np.where(
+        u < 0.8, 9, np.where(u < 0.85, 11, rng.integers(0, M, size=n))))).astype(np.int32)
+    obs = lat0[idx] * np.exp(rng.normal(0, 0.5, size=n))
+    nine = np.flatnonzero(idx == 9)
+    obs[nine[50]] = 1e300          # range too wide for the window: sequential fallback
+    if beta < 1.0:                 # (beta = 1 would turn inf into 0 * inf = nan)
+        eleven = np.flatnonzero(idx == 11)
+        obs[eleven[40]] = np.inf   # non-finite prefix: window disabled, result stays inf
+    tab = sp.RawTable(lat=lat0 * 0.7, res=np.ones(M), batch=np.ones(M, np.int32), pool=np.ones(M),
+                      price=np.ones(M), ref_index=ref_index, lat_init=lat0 * 0.7)
+    st = ofb.FoldState(lat0 * 0.7, lat0 * 0.7, ref_index)
+    for a, b in ((0, 1000), (1000, n)):   # the gate (5000th reference completion) lies in batch 2
+        sp.fold_observations([tab], None, idx[a:b], obs[a:b], beta=beta, dfp_count=5000,
+                             sync_host=False)
+        ofb.fold([st], None, idx[a:b], obs[a:b], beta=beta, dfp_count=5000)
+    got = tab.get_latency()
+    assert np.array_equal(bits(got), bits(st.lat))
+    cref, cnt = sp.table_counters(tab)
+    assert cref == st.completed_ref and np.array_equal(cnt, st.obs_count)
