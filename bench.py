@@ -354,7 +354,7 @@ def our_arm(args) -> None:
         "decisions_per_s": args.steps * N * world / t_max,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "decisions_per_s": args.steps * N * world / t_e2e,
-                "path": "OpTable.select_batch(numpy pinned) -> sp_select_batch(SP_MEM_HOST)"},
+                "path": "OpTable.select_batch(numpy pinned) -> sp_select_batch(SP_MEM_HOST): pinned buffers are read and written over PCIe by the decision kernel itself (zero-copy, one launch)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                      "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
                      "algorithmic_bytes_per_launch": alg_bytes,

@@ -479,6 +479,9 @@ class _RawTable:
                                                 C.byref(out)))
         return int(out.value)
 
+    def prepare(self, alpha: float) -> None:
+        check(self._ctx.lib.sp_table_prepare(self._ctx.handle, self._handle, float(alpha)))
+
     def close(self) -> None:
         if getattr(self, "_handle", None):
             self._ctx.lib.sp_table_destroy(self._ctx.handle, self._handle)

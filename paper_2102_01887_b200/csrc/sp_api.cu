@@ -82,6 +82,30 @@ static size_t rsz(size_t n) {
   return (n * sizeof(T) + 255) & ~(size_t)255;
 }
 
+// Device address of a pinned, mapped host range [h, h + bytes), or false (pageable memory,
+// or a range that leaves the registered allocation).
+static bool mapped_host(const void* h, size_t bytes, void** dev) {
+  if (!h || bytes == 0) return false;
+  cudaPointerAttributes a0, a1;
+  if (cudaPointerGetAttributes(&a0, h) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  const void* last = static_cast<const uint8_t*>(h) + bytes - 1;
+  if (cudaPointerGetAttributes(&a1, last) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  if (a0.type != cudaMemoryTypeHost || a1.type != cudaMemoryTypeHost || !a0.devicePointer ||
+      !a1.devicePointer)
+    return false;
+  if (static_cast<uint8_t*>(a1.devicePointer) - static_cast<uint8_t*>(a0.devicePointer) !=
+      (ptrdiff_t)(bytes - 1))
+    return false;
+  *dev = a0.devicePointer;
+  return true;
+}
+
 __global__ void k_scatter(int m, const int32_t* __restrict__ idx, const double* __restrict__ val,
                           double* __restrict__ dst) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -392,6 +416,40 @@ int sp_select_batch(sp_ctx* ctx, int32_t n_tables, sp_table* const* tables, doub
   if (op) {
     for (int i = 0; i < N; ++i)
       if (op[i] < 0 || op[i] >= n_tables) return fail(SP_E_INVALID, "select: op out of range");
+  }
+  // Zero-copy: when every caller buffer is pinned, mapped host memory, the decision kernel
+  // reads its inputs and writes its outputs over PCIe itself — one launch, both link
+  // directions busy at once, no copy-engine operations.
+  {
+    const bool want = !getenv("SP_ZERO_COPY") || atoi(getenv("SP_ZERO_COPY")) != 0;
+    struct Buf {
+      const void* h;
+      size_t bytes;
+      void* d;
+    } bufs[] = {{slack, sizeof(double) * N * K, nullptr},  {avail, 4u * N, nullptr},
+                {supply, 4u * N, nullptr},                  {min_batch, 4u * N, nullptr},
+                {flags, 4u * N, nullptr},                   {op, 4u * N, nullptr},
+                {out_idx, 4u * N, nullptr},                 {out_code, 4u * N, nullptr},
+                {out_fill, 4u * N, nullptr},                {out_obj, 8u * N, nullptr},
+                {out_slack, 8u * N, nullptr},               {out_wait, 8u * N, nullptr},
+                {out_kind_min, sizeof(double) * N * K, nullptr}};
+    bool ok = want && N > 0;
+    for (auto& bf : bufs) {
+      if (!ok) break;
+      if (!bf.h) continue;
+      ok = mapped_host(bf.h, bf.bytes, &bf.d);
+    }
+    if (ok) {
+      int rc = select_launch(ctx, n_tables, tables, alpha, N, (const int32_t*)bufs[5].d,
+                             (const double*)bufs[0].d, (const int32_t*)bufs[1].d,
+                             (const int32_t*)bufs[2].d, (const int32_t*)bufs[3].d,
+                             (const uint32_t*)bufs[4].d, (int32_t*)bufs[6].d, (int32_t*)bufs[7].d,
+                             (int32_t*)bufs[8].d, (double*)bufs[9].d, (double*)bufs[10].d,
+                             (double*)bufs[11].d, (double*)bufs[12].d, mode);
+      if (rc != SP_OK) return rc;
+      SP_CUDA(cudaStreamSynchronize(ctx->stream));
+      return SP_OK;
+    }
   }
   size_t need = rsz<double>((size_t)N * K) + 4 * rsz<int32_t>(N) + (op ? rsz<int32_t>(N) : 0) +
                 3 * rsz<int32_t>(N) + 3 * rsz<double>(N) +

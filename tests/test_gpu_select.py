@@ -293,3 +293,41 @@ def test_empty_batch_and_errors(c2_table):
         c2_table.select({"cpu": 1.0, "gpu": 1.0}, -1.0, 1, allow_delay=False)
     with pytest.raises(KeyError):
         c2_table.select({"cpu": 1.0}, 1.0, 1, allow_delay=False)
+
+
+@pytest.mark.parametrize("N", [1 << 20, 200_003])
+def test_pinned_host_buffers_zero_copy(gpu_ctx, N):
+    """Pinned (mapped) host buffers take the zero-copy path (the kernel reads and writes host
+    memory over PCIe in a single launch) and give the same decisions as the oracle; pageable
+    buffers of the same call take the staged-copy path."""
+    import torch
+
+    import paper_2102_01887_b200 as sp
+
+    rng = np.random.default_rng(N + 1)
+    tabs = [_random_table(rng, 1500, 8, 2), _random_table(rng, 700, 6, 2)]
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+    slack = rng.uniform(-1, 6, size=(N, 2))
+    avail = rng.integers(1, 300, size=N).astype(np.int32)
+    supply = rng.integers(0, 300, size=N).astype(np.int32)
+    mb = np.where(rng.random(N) < 0.8, 1, rng.integers(1, 300, size=N)).astype(np.int32)
+    flags = sp.make_flags(rng.random(N) < 0.5, rng.integers(0, 4, size=N) * (rng.random(N) < 0.2))
+    op = (rng.random(N) < 0.3).astype(np.int32)
+    exp = cselect.select_batch(tabs, slack, 50.0, avail, supply, mb, flags, op=op)
+    raws = [raw_table(t, 2) for t in tabs]
+    for t in raws:
+        t.prepare(50.0)
+    out = {"idx": pin(np.full(N, -7, np.int32)), "code": pin(np.full(N, -7, np.int32)),
+           "fill": pin(np.zeros(N, np.int32)), "obj": pin(np.zeros(N)), "slack": pin(np.zeros(N)),
+           "wait": pin(np.zeros(N))}
+    ctx = sp.get_context(0)
+    l0 = ctx.launch_count
+    r = sp.select_batch(raws, pin(slack), 50.0, pin(avail), upstream_supply=pin(supply),
+                        min_batch=pin(mb), flags=pin(flags), op=pin(op), mode="plan", out=out)
+    assert ctx.launch_count - l0 == 1  # one decision launch, no chunked copies
+    assert_same_decisions(r, exp, f"pinned N={N}")
+    r2 = sp.select_batch(raws, slack, 50.0, avail, upstream_supply=supply, min_batch=mb,
+                         flags=flags, op=op, mode="plan")
+    assert_same_decisions(r2, exp, f"pageable N={N}")
+    for t in raws:
+        t.close()
