@@ -170,6 +170,7 @@ __device__ __forceinline__ void store_out(const SelectIO& io, int i, const Out& 
 
 // ---- K2b: staircase plan kernel ----------------------------------------------------------
 #include "sp_k2b.cuh"
+#include "sp_k2f.cuh"
 
 // ---- K2a: literal scan kernel -------------------------------------------------------------
 struct Best {
@@ -353,6 +354,33 @@ int launch_plan_t(sp_ctx* ctx, const PlanPtrs& pp, const SelectIO& io) {
   }
   const char* variant = getenv("SP_K2_VARIANT");
   const bool single = pp.hv && pp.n == 1 && !io.out_kind_min;
+  // specialised kernel (sp_k2f.cuh) for the common shape; SP_K2_VARIANT=plan forces K2b
+  if (single && io.K == KT && !(variant && strcmp(variant, "fast"))) {
+    bool ok = pp.h.lut_n > 0 && io.out_idx && io.out_code && io.out_fill && io.out_obj &&
+              io.out_slack && io.out_wait;
+    for (int k = 0; k < KT && ok; ++k) ok = pp.h.kd[k].pad[0] == 0;  // positive thresholds
+    const int lut_off = (pp.h.total_bytes + 15) & ~15;
+    const int smem = ((lut_off + 4 * pp.h.lut_n + 1023) / 1024) * 1024;
+    if (ok && smem <= kPlanSmemBudget) {
+      static bool fast_attr = false;
+      if (!fast_attr) {
+        SP_CUDA(cudaFuncSetAttribute(k_select_fast<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     kPlanSmemBudget));
+        fast_attr = true;
+      }
+      FastIO<KT> f;
+      f.slack = io.slack; f.avail = io.avail; f.supply = io.supply; f.min_batch = io.min_batch;
+      f.flags = io.flags; f.out_idx = io.out_idx; f.out_code = io.out_code; f.out_fill = io.out_fill;
+      f.out_obj = io.out_obj; f.out_slack = io.out_slack; f.out_wait = io.out_wait;
+      f.N = (uint32_t)io.N; f.lut_bytes_off = lut_off;
+      int blocks = ctx->num_sms;
+      int need = (io.N + kPlanThreads - 1) / kPlanThreads;
+      if (need < blocks) blocks = need > 0 ? need : 1;
+      k_select_fast<KT><<<blocks, kPlanThreads, smem, ctx->stream>>>(pp.p[0], pp.h, f);
+      SP_CHECK_LAUNCH(ctx);
+      return SP_OK;
+    }
+  }
   if (single && variant && !strcmp(variant, "lean")) {
     int blocks = ctx->num_sms * 2;
     int need = (io.N + 767) / 768;
