@@ -8,9 +8,11 @@ invocations (K2, staircase kernel) with alpha rotating over {0, 1, 100, 1000} by
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 One JSON line on rank 0:
-  value     invocation x configuration evaluations / s, inputs resident in HBM, L2 flushed
-            between steps (256 MB read sweep), device time (CUDA events on the launching stream),
-            max over ranks; decisions_per_s alongside.
+  value     invocation x configuration evaluations / s, inputs resident in HBM and larger than
+            L2: K steps back to back over 4 rotating invocation sets (4 x 71.5 MB > 126 MB L2),
+            one CUDA-event pair on the launching stream around the K steps, max over ranks;
+            decisions_per_s alongside.  The per-step time with an L2 flush (256 MB read sweep)
+            and an event pair around every step is reported beside it (step_ms_l2_flushed).
   e2e       the same metric through the reference-facing call with HOST (pinned) buffers:
             H2D of the step's inputs, kernel, D2H of every decision, inside the timed region.
   roofline  K2 kernel: algorithmic bytes per launch / mean launch time
@@ -39,6 +41,7 @@ sys.path.insert(0, str(ROOT))
 METRIC = "config decisions/sec (invocation x config evals/s) at 1/2/4/8 B200; % HBM roofline"
 UNIT = "evals/s"
 ALPHAS = (0.0, 1.0, 100.0, 1000.0)
+SETS = 4                     # rotating invocation sets per GPU (together larger than L2)
 K_KINDS = 2
 B_IN = 8 * K_KINDS + 16      # slack[K] f64 + avail, supply, min_batch i32 + flags u32
 B_OUT = 4 + 4 + 4 + 8 + 8 + 8  # idx, code, fill i32 + objective, slack, wait f64
@@ -57,9 +60,13 @@ def workload_config(n_inv: int, M: int, mode: str, world: int) -> dict:
         "workload": "config2: 2^20 invocations x 4,096 configs per GPU "
                     "(sampling x variant x batch x cores/GPU-mem x {cpu,gpu}); SURVEY.md §8(d)",
         "invocations_per_gpu": n_inv, "configs": M, "kinds": K_KINDS, "alphas": list(ALPHAS),
-        "kernel": {"plan": "k_select_plan (K2b staircase)", "scan": "k_select_scan (K2a)",
-                   "auto": "k_select_plan (K2b staircase)"}.get(mode, "CPU: oracle restatement of OpTable.select"),
-        "l2": "flushed between timed steps: a 256 MB read (evicts every line, leaves L2 clean), outside the events",
+        "kernel": {"plan": "k_select_fast (K2f: specialised K2b staircase, PDL launch)",
+                   "scan": "k_select_scan (K2a)",
+                   "auto": "k_select_fast (K2f: specialised K2b staircase, PDL launch)"}.get(mode, "CPU: oracle restatement of OpTable.select"),
+        "l2": ("inputs larger than L2: steps rotate over 4 invocation sets (4 x 71.5 MB = 286 MB "
+               "> 126 MB L2), K steps back to back in one event pair; step_ms_l2_flushed = the same "
+               "step with a 256 MB read sweep before it and an event pair around it"),
+        "sets": SETS,
         "parallelism": f"replicated tables, invocations sharded, {world} GPU(s), no data-path collective",
     }
 
@@ -127,7 +134,7 @@ def load_peaks() -> dict:
 
 
 def ncu_traffic() -> tuple[float | None, str | None]:
-    p = ROOT / "profiles" / "ncu_k2_summary.json"
+    p = ROOT / "profiles" / "ncu_k2f_summary.json"
     if p.exists():
         d = json.loads(p.read_text())
         return d.get("dram_bytes_per_launch"), d.get("source")
@@ -237,16 +244,22 @@ def our_arm(args) -> None:
     N = args.n
     gk = table.gkind
     inv = synth.synth_invocations(N, table.lat, gk, seed=20261017 + rank)
-    d_in = {
-        "slack": torch.from_numpy(inv.slack).to(dev), "avail": torch.from_numpy(inv.avail).to(dev),
-        "supply": torch.from_numpy(inv.supply).to(dev), "min_batch": torch.from_numpy(inv.min_batch).to(dev),
-        "flags": torch.from_numpy(inv.flags.astype(np.int32)).to(dev),
-    }
-    out = {
-        "idx": torch.empty(N, dtype=torch.int32, device=dev), "code": torch.empty(N, dtype=torch.int32, device=dev),
-        "fill": torch.empty(N, dtype=torch.int32, device=dev), "obj": torch.empty(N, dtype=torch.float64, device=dev),
-        "slack": torch.empty(N, dtype=torch.float64, device=dev), "wait": torch.empty(N, dtype=torch.float64, device=dev),
-    }
+
+    def dev_set(v):
+        d = {"slack": torch.from_numpy(v.slack).to(dev), "avail": torch.from_numpy(v.avail).to(dev),
+             "supply": torch.from_numpy(v.supply).to(dev), "min_batch": torch.from_numpy(v.min_batch).to(dev),
+             "flags": torch.from_numpy(v.flags.astype(np.int32)).to(dev)}
+        o = {"idx": torch.empty(N, dtype=torch.int32, device=dev),
+             "code": torch.empty(N, dtype=torch.int32, device=dev),
+             "fill": torch.empty(N, dtype=torch.int32, device=dev),
+             "obj": torch.empty(N, dtype=torch.float64, device=dev),
+             "slack": torch.empty(N, dtype=torch.float64, device=dev),
+             "wait": torch.empty(N, dtype=torch.float64, device=dev)}
+        return d, o
+
+    sets = [dev_set(inv)] + [
+        dev_set(synth.synth_invocations(N, table.lat, gk, seed=20261017 + 1000 * s + rank))
+        for s in range(1, SETS)]
 
     # plan build for every alpha (table is static: plans are reused across steps) — timed once
     plan_ms = {}
@@ -266,42 +279,43 @@ def our_arm(args) -> None:
         # written back here, outside the timed region, and L2 is left holding clean data
         flush.max()
 
+    def alpha_of(i):
+        return ALPHAS[(i + i // SETS) % len(ALPHAS)]
+
     def step(i, host=None):
-        a = ALPHAS[i % len(ALPHAS)]
+        a = alpha_of(i)
         if host is None:
-            table.select_batch(d_in["slack"], a, d_in["avail"], upstream_supply=d_in["supply"],
-                               min_batch=d_in["min_batch"], flags=d_in["flags"], mode=args.mode, out=out)
+            d, o = sets[i % SETS]
+            table.select_batch(d["slack"], a, d["avail"], upstream_supply=d["supply"],
+                               min_batch=d["min_batch"], flags=d["flags"], mode=args.mode, out=o)
         else:
             table.select_batch(host["slack"], a, host["avail"], upstream_supply=host["supply"],
                                min_batch=host["min_batch"], flags=host["flags"], mode=args.mode,
                                out=host["out"])
 
     for i in range(args.warmup):
-        flush_l2()
         step(i)
     torch.cuda.synchronize(dev)
 
-    # ---- timed: device-resident ----
+    # ---- timed: device-resident, K steps back to back over rotating sets ----
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize(dev)
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = ctx.launch_count
     with ClockSampler(local) as clk:
         # hold the GPU while the host enqueues every timed step, so that host-side launch
-        # jitter can never land between a step's start and end events
+        # jitter can never land inside the timed region
         torch.cuda._sleep(int(2e6 + 4e5 * args.steps))
+        e0.record(stream)
         for i in range(args.steps):
-            flush_l2()
-            evs[i][0].record(stream)
             step(args.warmup + i)
-            evs[i][1].record(stream)
+        e1.record(stream)
         torch.cuda.synchronize(dev)
     launches = ctx.launch_count - launches0
     if world > 1:
         torch.distributed.barrier()
-    step_ms = [a.elapsed_time(b) for a, b in evs]
-    t_local = sum(step_ms) / 1e3
+    t_local = e0.elapsed_time(e1) / 1e3
     t_max = t_local
     if world > 1:
         tt = torch.tensor([t_local], dtype=torch.float64, device=dev)
@@ -309,6 +323,18 @@ def our_arm(args) -> None:
         t_max = float(tt.item())
     evals = args.steps * N * M * world
     value = evals / t_max
+
+    # ---- the same steps, one at a time: L2 flushed before, an event pair around each ----
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    torch.cuda.synchronize(dev)
+    torch.cuda._sleep(int(2e6 + 4e5 * args.steps))
+    for i in range(args.steps):
+        flush_l2()
+        evs[i][0].record(stream)
+        step(args.warmup + i)
+        evs[i][1].record(stream)
+    torch.cuda.synchronize(dev)
+    step_ms = [a.elapsed_time(b) for a, b in evs]
 
     # ---- e2e: host pinned buffers through the reference-facing call ----
     pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
@@ -362,10 +388,12 @@ def our_arm(args) -> None:
                      "kernel_ms": kernel_s * 1e3, "peak_source": peaks["source"],
                      "traffic_source": traffic_src},
         "gpu_launches": launches,
-        "step_ms": {"min": min(step_ms), "median": statistics.median(step_ms), "max": max(step_ms),
-                    "by_alpha": {str(a): statistics.median(step_ms[j::len(ALPHAS)]) for j, a in
-                                 enumerate(ALPHAS[(args.warmup + k) % len(ALPHAS)] for k in range(len(ALPHAS)))
-                                 if step_ms[j::len(ALPHAS)]}},
+        "step_ms_l2_flushed": {"min": min(step_ms), "median": statistics.median(step_ms), "max": max(step_ms),
+                               "by_alpha": {str(a): statistics.median([t for k, t in enumerate(step_ms)
+                                                                       if alpha_of(args.warmup + k) == a])
+                                            for a in ALPHAS
+                                            if any(alpha_of(args.warmup + k) == a for k in range(args.steps))},
+                               "evals_per_s": N * M * world / (statistics.median(step_ms) / 1e3)},
         "plan": {"build_ms_per_alpha": plan_ms, "bytes": plan_bytes,
                  "note": "staircase plan built once per (profile version, alpha); table static in config 2"},
         "clocks": clk.summary(),

@@ -193,12 +193,10 @@ __global__ void __launch_bounds__(1024, 1) k_select_fast(const uint8_t* __restri
   __shared__ __align__(8) uint64_t s_bar;
   const int tid = threadIdx.x;
   const int bytes = h.total_bytes;
-  if (tid == 0) {  // TMA bulk copies of the plan image, completion on one mbarrier
-    mbar_init(&s_bar, 1);
-    mbar_expect_tx(&s_bar, (uint32_t)bytes);
-    for (int c = 0; c < bytes; c += kStageChunk)
-      bulk_g2s(smem + c, plan + c, (uint32_t)min(kStageChunk, bytes - c), &s_bar);
-  }
+  // Programmatic dependent launch: everything above griddepcontrol.wait touches only
+  // parameters and this CTA's shared memory, so it overlaps the previous kernel's tail; no
+  // global memory is read or written before the predecessor grid has completed.
+  if (tid == 0) mbar_init(&s_bar, 1);
   // CTA lookup table v -> (#batch < v) | (#batch <= v) << 8 | (tri_base(lo) - lo) << 16
   {
     uint32_t* lut = reinterpret_cast<uint32_t*>(smem + io.lut_bytes_off);
@@ -212,6 +210,14 @@ __global__ void __launch_bounds__(1024, 1) k_select_fast(const uint8_t* __restri
       const int tb = lo * nB - ((lo * (lo - 1)) >> 1) - lo;
       lut[v] = (uint32_t)lo | ((uint32_t)le << 8) | ((uint32_t)tb << 16);
     }
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  // the next launch in the stream may start its prologue as this grid's CTAs retire
+  asm volatile("griddepcontrol.launch_dependents;");
+  if (tid == 0) {  // TMA bulk copies of the plan image, completion on one mbarrier
+    mbar_expect_tx(&s_bar, (uint32_t)bytes);
+    for (int c = 0; c < bytes; c += kStageChunk)
+      bulk_g2s(smem + c, plan + c, (uint32_t)min(kStageChunk, bytes - c), &s_bar);
   }
   const uint32_t stride = gridDim.x * blockDim.x;
   uint32_t i = blockIdx.x * blockDim.x + tid;

@@ -376,7 +376,17 @@ int launch_plan_t(sp_ctx* ctx, const PlanPtrs& pp, const SelectIO& io) {
       int blocks = ctx->num_sms;
       int need = (io.N + kPlanThreads - 1) / kPlanThreads;
       if (need < blocks) blocks = need > 0 ? need : 1;
-      k_select_fast<KT><<<blocks, kPlanThreads, smem, ctx->stream>>>(pp.p[0], pp.h, f);
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(blocks);
+      cfg.blockDim = dim3(kPlanThreads);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = ctx->stream;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = getenv("SP_NO_PDL") ? 0 : 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      SP_CUDA(cudaLaunchKernelEx(&cfg, k_select_fast<KT>, (const uint8_t*)pp.p[0], pp.h, f));
       SP_CHECK_LAUNCH(ctx);
       return SP_OK;
     }
