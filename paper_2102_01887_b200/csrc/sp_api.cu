@@ -190,6 +190,7 @@ int sp_ctx_set_stream(sp_ctx* ctx, void* stream) {
   SP_CUDA(cudaStreamSynchronize(ctx->stream));
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
   ctx->stream = (cudaStream_t)stream;
+  ctx->plan_dirty = true;
   ctx->own_stream = false;
   return SP_OK;
 }

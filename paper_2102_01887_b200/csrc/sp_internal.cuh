@@ -116,6 +116,9 @@ struct sp_ctx {
   int num_sms = 0;
   int max_smem_optin = 0;
   int64_t launches = 0;
+  // a plan image was (re)written by a kernel that no select launch has waited on yet: the
+  // next K2f launch must not read any plan before its griddepcontrol.wait
+  bool plan_dirty = true;
   // grow-only device arena for staged host I/O
   void* io_dev = nullptr;
   size_t io_cap = 0;

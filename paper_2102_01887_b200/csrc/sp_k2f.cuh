@@ -32,6 +32,8 @@ struct FastIO {
   double* out_wait;
   uint32_t N;
   int lut_bytes_off;  // byte offset of the CTA lookup table in dynamic shared memory
+  int prestage;       // 1: the plan was completed by a kernel an earlier select launch waited
+                      // on, so it may be staged before griddepcontrol.wait
 };
 
 template <int K>
@@ -194,9 +196,18 @@ __global__ void __launch_bounds__(1024, 1) k_select_fast(const uint8_t* __restri
   const int tid = threadIdx.x;
   const int bytes = h.total_bytes;
   // Programmatic dependent launch: everything above griddepcontrol.wait touches only
-  // parameters and this CTA's shared memory, so it overlaps the previous kernel's tail; no
-  // global memory is read or written before the predecessor grid has completed.
-  if (tid == 0) mbar_init(&s_bar, 1);
+  // parameters, this CTA's shared memory and (when io.prestage) a plan image that an earlier
+  // select launch has already waited on, so it overlaps the previous kernel's tail; the
+  // invocation stream is neither read nor written before the predecessor grid has completed.
+  const bool pre = io.prestage != 0;
+  if (tid == 0) {
+    mbar_init(&s_bar, 1);
+    if (pre) {  // TMA bulk copies of the plan image, completion on one mbarrier
+      mbar_expect_tx(&s_bar, (uint32_t)bytes);
+      for (int c = 0; c < bytes; c += kStageChunk)
+        bulk_g2s(smem + c, plan + c, (uint32_t)min(kStageChunk, bytes - c), &s_bar);
+    }
+  }
   // CTA lookup table v -> (#batch < v) | (#batch <= v) << 8 | (tri_base(lo) - lo) << 16
   {
     uint32_t* lut = reinterpret_cast<uint32_t*>(smem + io.lut_bytes_off);
@@ -214,7 +225,7 @@ __global__ void __launch_bounds__(1024, 1) k_select_fast(const uint8_t* __restri
   asm volatile("griddepcontrol.wait;" ::: "memory");
   // the next launch in the stream may start its prologue as this grid's CTAs retire
   asm volatile("griddepcontrol.launch_dependents;");
-  if (tid == 0) {  // TMA bulk copies of the plan image, completion on one mbarrier
+  if (tid == 0 && !pre) {
     mbar_expect_tx(&s_bar, (uint32_t)bytes);
     for (int c = 0; c < bytes; c += kStageChunk)
       bulk_g2s(smem + c, plan + c, (uint32_t)min(kStageChunk, bytes - c), &s_bar);

@@ -602,6 +602,7 @@ int plan_build(sp_ctx* ctx, sp_table* t, Plan& p) {
                                  t->batch, t->kind, t->ukey, t->ukr, t->uent, t->umap, h,
                                  p.image, p.image_cap, status);
   SP_CHECK_LAUNCH(ctx);
+  ctx->plan_dirty = true;
   // fetch the header back without blocking; it becomes a kernel parameter once it lands
   if (!p.host_hdr) {
     SP_CUDA(cudaMallocHost(&p.host_hdr, sizeof(PlanHdr)));

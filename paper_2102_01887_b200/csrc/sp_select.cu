@@ -373,6 +373,7 @@ int launch_plan_t(sp_ctx* ctx, const PlanPtrs& pp, const SelectIO& io) {
       f.flags = io.flags; f.out_idx = io.out_idx; f.out_code = io.out_code; f.out_fill = io.out_fill;
       f.out_obj = io.out_obj; f.out_slack = io.out_slack; f.out_wait = io.out_wait;
       f.N = (uint32_t)io.N; f.lut_bytes_off = lut_off;
+      f.prestage = ctx->plan_dirty ? 0 : 1;
       int blocks = ctx->num_sms;
       int need = (io.N + kPlanThreads - 1) / kPlanThreads;
       if (need < blocks) blocks = need > 0 ? need : 1;
@@ -388,6 +389,7 @@ int launch_plan_t(sp_ctx* ctx, const PlanPtrs& pp, const SelectIO& io) {
       cfg.numAttrs = 1;
       SP_CUDA(cudaLaunchKernelEx(&cfg, k_select_fast<KT>, (const uint8_t*)pp.p[0], pp.h, f));
       SP_CHECK_LAUNCH(ctx);
+      ctx->plan_dirty = false;
       return SP_OK;
     }
   }
