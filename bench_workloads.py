@@ -37,6 +37,31 @@ def _flush_factory(torch, dev):
     return lambda: buf.max()
 
 
+def _dist(torch):
+    """(rank, world, local) — NCCL process group when launched under torchrun (one rank per GPU)."""
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1 and not torch.distributed.is_initialized():
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return rank, world, local
+
+
+def _tmax(torch, t: float, dev) -> float:
+    """Device time of the slowest rank."""
+    if not (torch.distributed.is_available() and torch.distributed.is_initialized()):
+        return t
+    tt = torch.tensor([t], dtype=torch.float64, device=dev)
+    torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+    return float(tt.item())
+
+
+def _barrier(torch):
+    if torch.distributed.is_available() and torch.distributed.is_initialized():
+        torch.distributed.barrier()
+
+
 def _peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     return float(json.loads(p.read_text())["hbm_gbs"]) if p.exists() else 6650.0
@@ -64,13 +89,18 @@ def run_c3(args):
     import paper_2102_01887_b200 as sp
     from paper_2102_01887_b200 import synth
 
-    dev = torch.device("cuda", 0)
+    from paper_2102_01887_b200.shard import shard_range
+
+    rank, world, local = _dist(torch)
+    dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream(dev)
-    ctx = sp.get_context(0)
+    ctx = sp.get_context(local)
     ctx.set_stream(stream.cuda_stream)
     dag = synth.deep_dag()
-    I, K = 100_000, 4
-    ref, T, now, Q = synth.deep_dag_instances(dag, I, K=K)
+    I, K = 100_000, 4  # instances per GPU (weak scaling): rank r owns instance rows [r*I, (r+1)*I)
+    ref_all, T_all, now_all, Q_all = synth.deep_dag_instances(dag, I * world, K=K)
+    a, b = shard_range(I * world, rank, world)
+    ref, T, now, Q = ref_all[a:b], T_all[a:b], now_all[a:b], Q_all[a:b]
     g = sp.SlackGraph.from_dag(dag)
     V = len(dag.vertices)
     d = {k: torch.from_numpy(np.ascontiguousarray(v)).to(dev) for k, v in
@@ -80,6 +110,7 @@ def run_c3(args):
     for _ in range(args.warmup):
         g.slack_batch(d["ref"], d["T"], d["now"], d["Q"], out=out)
     torch.cuda.synchronize(dev)
+    _barrier(torch)
     evs = _events(torch, args.steps)
     l0 = ctx.launch_count
     for i in range(args.steps):
@@ -88,9 +119,11 @@ def run_c3(args):
         g.slack_batch(d["ref"], d["T"], d["now"], d["Q"], out=out)
         evs[i][1].record(stream)
     torch.cuda.synchronize(dev)
-    ms = [a.elapsed_time(b) for a, b in evs]
-    t = sum(ms) / 1e3
-    vals = args.steps * I * V * K
+    ms = [x.elapsed_time(y) for x, y in evs]
+    t = _tmax(torch, sum(ms) / 1e3, dev)
+    vals = args.steps * I * V * K * world
+    if rank != 0:
+        return
     bytes_inst = 8 * V + 16 + 8 * K + 8 * V * K
     # CPU: the exact DP restatement on all host cores over a bounded sample
     order = dag.topological_order()
@@ -100,25 +133,29 @@ def run_c3(args):
     vcol = [dag.vertices.index(v) for v in order]
     cores = os.cpu_count() or 1
     S = args.c3_cpu_instances
-    import multiprocessing as mp
+    n_cpu, cpu_t = 0, 1.0
+    if world == 1:  # the CPU baseline runs on rank 0 at N=1 only
+        import multiprocessing as mp
 
-    chunks = np.array_split(np.arange(S), cores)
-    work = [(order, preds, term, vcol, ref[c], T[c], now[c], Q[c]) for c in chunks if len(c)]
-    t0 = time.perf_counter()
-    with mp.get_context("fork").Pool(len(work)) as pool:
-        n_cpu = sum(pool.map(_c3_cpu_worker, work))
-    cpu_t = time.perf_counter() - t0
+        chunks = np.array_split(np.arange(S), cores)
+        work = [(order, preds, term, vcol, ref[c], T[c], now[c], Q[c]) for c in chunks if len(c)]
+        t0 = time.perf_counter()
+        with mp.get_context("fork").Pool(len(work)) as pool:
+            n_cpu = sum(pool.map(_c3_cpu_worker, work))
+        cpu_t = time.perf_counter() - t0
     line = {
         "workload": "c3", "metric": "Alg. 1 slack values (instance x op x kind) / s", "unit": "slack/s",
-        "value": vals / t, "ms_per_step": 1e3 * t / args.steps, "steps": args.steps, "n_gpus": 1,
-        "config": {"ops": V, "edges": len(dag.edges), "instances": I, "kinds": K,
-                   "decomposed_paths": "~3.3e9 (not enumerable by the reference)"},
-        "instances_per_s": args.steps * I / t,
+        "value": vals / t, "ms_per_step": 1e3 * t / args.steps, "steps": args.steps, "n_gpus": world,
+        "scaling": "weak",
+        "config": {"ops": V, "edges": len(dag.edges), "instances_per_gpu": I, "kinds": K,
+                   "decomposed_paths": "~3.3e9 (not enumerable by the reference)",
+                   "parallelism": f"instances sharded over {world} GPU(s), no collective"},
+        "instances_per_s": args.steps * I * world / t,
         "roofline": {"bound": "fp64/lds issue (exact forward DP, DESIGN.md §3)",
                      "hbm_bytes_per_instance": bytes_inst,
-                     "hbm_frac": (args.steps * I * bytes_inst / t / 1e9) / _peaks()},
+                     "hbm_frac": (args.steps * I * world * bytes_inst / t / 1e9) / (world * _peaks())},
         "gpu_launches": ctx.launch_count - l0,
-        "cpu_baseline": {"value": n_cpu / cpu_t, "unit": "slack/s", "cores": cores,
+        "cpu_baseline": None if world > 1 else {"value": n_cpu / cpu_t, "unit": "slack/s", "cores": cores,
                          "kind": "restatement (the reference cannot run this DAG)",
                          "sample": f"{S} instances, oracle/slack.py dp_ratios on {cores} processes"},
         "step_ms": {"median": statistics.median(ms), "min": min(ms), "max": max(ms)},
@@ -149,9 +186,10 @@ def run_c4(args):
 
     with np.load(ROOT / "tests" / "golden" / "amber_trace.npz") as z:
         meta = json.loads(bytes(z["meta_json"]).decode())
-    dev = torch.device("cuda", 0)
+    rank, world, local = _dist(torch)
+    dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream(dev)
-    ctx = sp.get_context(0)
+    ctx = sp.get_context(local)
     ctx.set_stream(stream.cuda_stream)
     tabs = _amber_tables(sp, meta)
     ops = meta["ops"]
@@ -164,7 +202,7 @@ def run_c4(args):
     R, mults, S = args.c4_replicas, (0.5, 1.0, 2.0, 5.0, 10.0), 64
     cp_min = 90.41885182994682
     I = R * len(mults) * S
-    rng = np.random.default_rng(4)
+    rng = np.random.default_rng(4 + 1000 * rank)  # rank r owns replicas [r*R, (r+1)*R)
     target = np.repeat(np.array(mults) * cp_min, S)[None, :].repeat(R, 0).reshape(-1)
     now = (np.tile(np.arange(S) / S, R * len(mults))) * target
     Q = rng.exponential(1.0, size=(I, K)) * (0.02 * target)[:, None]
@@ -196,6 +234,7 @@ def run_c4(args):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize(dev)
+    _barrier(torch)
     evs = _events(torch, args.steps)
     l0 = ctx.launch_count
     for i in range(args.steps):
@@ -205,16 +244,23 @@ def run_c4(args):
         evs[i][1].record(stream)
     torch.cuda.synchronize(dev)
     ms = [a.elapsed_time(b) for a, b in evs]
-    t = sum(ms) / 1e3
+    t = _tmax(torch, sum(ms) / 1e3, dev)
+    codes = torch.bincount(out["code"] & 3, minlength=3)
+    if world > 1:
+        torch.distributed.all_reduce(codes)
+    codes = codes.cpu().tolist()
+    if rank != 0:
+        return
     evals_per_inst = sum(len(x.entries) for x in tabs)
-    codes = torch.bincount(out["code"] & 3, minlength=3).cpu().tolist()
     line = {
         "workload": "c4", "metric": "config decisions/s (K1 slack -> K2 select, on device)",
-        "unit": "decisions/s", "value": args.steps * N / t, "ms_per_step": 1e3 * t / args.steps,
-        "steps": args.steps, "n_gpus": 1,
-        "evals_per_s": args.steps * I * evals_per_inst / t,
-        "config": {"replicas": R, "targets_x_cp_min": list(mults), "snapshots": S, "instances": I,
-                   "ops": V, "kinds": K, "decisions_per_step": N, "cp_min": cp_min},
+        "unit": "decisions/s", "value": args.steps * N * world / t, "ms_per_step": 1e3 * t / args.steps,
+        "steps": args.steps, "n_gpus": world, "scaling": "weak",
+        "evals_per_s": args.steps * I * world * evals_per_inst / t,
+        "config": {"replicas_per_gpu": R, "targets_x_cp_min": list(mults), "snapshots": S,
+                   "instances_per_gpu": I, "ops": V, "kinds": K, "decisions_per_step_per_gpu": N,
+                   "cp_min": cp_min,
+                   "parallelism": f"replicas sharded over {world} GPU(s); decision counters all-reduced"},
         "decision_mix": {"none": codes[0], "assign": codes[1], "delay": codes[2]},
         "gpu_launches": ctx.launch_count - l0,
         "step_ms": {"median": statistics.median(ms), "min": min(ms), "max": max(ms)},
@@ -230,9 +276,12 @@ def run_c5(args):
     import paper_2102_01887_b200 as sp
     from paper_2102_01887_b200 import synth
 
-    dev = torch.device("cuda", 0)
+    from paper_2102_01887_b200.shard import gather_observations, shard_range
+
+    rank, world, local = _dist(torch)
+    dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream(dev)
-    ctx = sp.get_context(0)
+    ctx = sp.get_context(local)
     ctx.set_stream(stream.cuda_stream)
     spec = synth.synth_spec(True)
     table = sp.OpTable(spec, synth.synth_scenario())
@@ -247,32 +296,54 @@ def run_c5(args):
     gen = torch.Generator(device=dev)
     gen.manual_seed(5)
     noise = torch.exp(0.3 * torch.randn(N, dtype=torch.float64, device=dev, generator=gen))
-    out = {k: torch.empty(B, dtype=dt, device=dev) for k, dt in
+    # every batch is split contiguously over the ranks (decisions), then the observation records
+    # are all-gathered so that each rank folds the whole batch in global order
+    a, b = shard_range(B, rank, world)
+    Bl = b - a
+    out = {k: torch.empty(Bl, dtype=dt, device=dev) for k, dt in
            (("idx", torch.int32), ("code", torch.int32), ("fill", torch.int32),
             ("obj", torch.float64), ("slack", torch.float64), ("wait", torch.float64))}
-    obs_idx = torch.empty(B, dtype=torch.int32, device=dev)
+    obs_idx = torch.empty(Bl, dtype=torch.int32, device=dev)
     alpha = 100.0
     table.prepare(alpha)
     torch.cuda.synchronize(dev)
+    _barrier(torch)
     l0 = ctx.launch_count
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    for b in range(NB):
-        s = slice(b * B, (b + 1) * B)
+    for bt in range(NB):
+        s = slice(bt * B + a, bt * B + b)
         table.select_batch(d["slack"][s], alpha, d["avail"][s], upstream_supply=d["supply"][s],
                            min_batch=d["mb"][s], flags=d["flags"][s], out=out)
         # the chosen configurations run: observation = truth(config) * lognormal noise;
         # delayed / None decisions produce no observation (idx = -1)
         torch.where((out["code"] & 3) == 1, out["idx"], torch.full_like(out["idx"], -1), out=obs_idx)
         obs = lat_init[obs_idx.clamp(min=0).long()] * noise[s]
-        sp.fold_observations([table], None, obs_idx, obs, beta=0.5, dfp_count=10, sync_host=False)
+        f_idx, f_obs = gather_observations(obs_idx, obs, B) if world > 1 else (obs_idx, obs)
+        sp.fold_observations([table], None, f_idx, f_obs, beta=0.5, dfp_count=10, sync_host=False)
     e1.record(stream)
     torch.cuda.synchronize(dev)
-    t = e0.elapsed_time(e1) / 1e3
+    t = _tmax(torch, e0.elapsed_time(e1) / 1e3, dev)
+    # replicas must stay bit-identical: compare a checksum of the final latency table
+    table.sync_from_device()
+    lat_now = torch.from_numpy(table.lat.copy()).to(dev)
+    chk = lat_now.view(torch.int64).sum().view(1)
+    identical = True
+    if world > 1:
+        lo, hi = chk.clone(), chk.clone()
+        torch.distributed.all_reduce(lo, op=torch.distributed.ReduceOp.MIN)
+        torch.distributed.all_reduce(hi, op=torch.distributed.ReduceOp.MAX)
+        identical = bool(lo.item() == hi.item())
+    if rank != 0:
+        return
     line = {
         "workload": "c5", "metric": "online config decisions/s incl. per-batch feedback fold and replanning",
-        "unit": "decisions/s", "value": N / t, "evals_per_s": N * M / t, "seconds": t, "n_gpus": 1,
-        "config": {"invocations": N, "configs": M, "batches": NB, "batch": B, "beta": 0.5, "dfp_count": 10},
+        "unit": "decisions/s", "value": N / t, "evals_per_s": N * M / t, "seconds": t, "n_gpus": world,
+        "scaling": "strong",
+        "config": {"invocations": N, "configs": M, "batches": NB, "batch": B, "beta": 0.5, "dfp_count": 10,
+                   "parallelism": (f"each batch split over {world} GPU(s); per batch one all-gather of the "
+                                   "16-B observation records, replicated fold" if world > 1 else "1 GPU")},
+        "tables_bit_identical_across_ranks": identical,
         "gpu_launches": ctx.launch_count - l0,
         "per_batch_ms": 1e3 * t / NB,
     }

@@ -9,6 +9,10 @@ exchange steps, used when a caller wants whole-job results:
 * ``gather_partials``   per-rank FP partial sums, all-gathered and summed on every rank in
                         rank order (deterministic for a fixed world size)
 * ``gather_decisions``  the decision records of every shard, in global invocation order
+* ``gather_observations``  online mode (config 5): the 16-byte observation records (table
+                        entry, observed latency) of every shard of a batch, in global invocation
+                        order, so every rank folds the identical ordered stream and the replicated
+                        profile tables stay bit-identical without a broadcast
 
 They take torch tensors and work with NCCL (CUDA tensors, B200 / NVLink) and gloo (CPU tensors,
 the multi-process CPU tests).
@@ -80,3 +84,21 @@ def gather_decisions(arrays: Mapping[str, "object"], n_total: int, group=None) -
         dist.all_gather(parts, pad, group=group)
         out[name] = torch.cat([p[: b - a] for p, (a, b) in zip(parts, sizes)])
     return out
+
+
+def gather_observations(idx, obs, n_total: int, group=None):
+    """All-gather one batch's observation records from every shard (``shard_range`` layout).
+
+    ``idx`` (int32, entry index or -1 for "no observation") and ``obs`` (float64) are this rank's
+    shard; returns the whole batch ``(idx, obs)`` in global invocation order on every rank.  The
+    records travel as one (n, 2) float64 tensor (16 B per observation, the index is exact in f64),
+    i.e. one collective per batch.
+    """
+    import torch
+    import torch.distributed as dist
+
+    if not (dist.is_available() and dist.is_initialized()):
+        return idx.clone(), obs.clone()
+    rec = torch.stack([idx.to(torch.float64), obs.to(torch.float64)], dim=1)
+    full = gather_decisions({"rec": rec}, n_total, group=group)["rec"]
+    return full[:, 0].to(torch.int32), full[:, 1].contiguous()

@@ -84,3 +84,68 @@ def test_two_rank_gloo_matches_single_process(tmp_path):
     a, b = shard_range(inv.N, 0, 2)
     expect_total = float(np.sum(r["obj"][a:b])) + float(np.sum(r["obj"][b:]))
     assert got["total"].item() == expect_total
+
+
+# ---- online mode (config 5): per-batch all-gather of observation records ---------------------
+
+def _online_batches():
+    from oracle import optable
+    from paper_2102_01887_b200 import synth
+
+    t = optable.from_spec(synth.synth_spec(False), synth.synth_scenario(), ["cpu", "gpu"])
+    inv = synth.synth_invocations(3 * 400, t.lat, t.gkind, seed=505)
+    noise = np.exp(np.random.default_rng(9).normal(0.0, 0.3, size=inv.N))
+    return t, inv, noise, 400
+
+
+def _online_run(t, inv, noise, B, lo_hi, gather):
+    """Decide each batch (this rank's shard) against the batch-start table, turn assigns into
+    observations, gather the whole batch's records, fold them in global order."""
+    from oracle import feedback, optable
+
+    lat_init = t.lat.copy()
+    st = feedback.FoldState(t.lat.copy(), lat_init, t.ref_index)
+    for bt in range(inv.N // B):
+        t.lat = st.lat.copy()  # batch-start snapshot
+        a, b = lo_hi
+        r = optable.select_many([t], inv.slack, 100.0, inv.avail, inv.supply, inv.min_batch, inv.flags,
+                                None, bt * B + a, bt * B + b)
+        idx = np.where(r["code"] == optable.ASSIGN, r["idx"], -1).astype(np.int32)
+        obs = lat_init[np.maximum(idx, 0)] * noise[bt * B + a: bt * B + b]
+        f_idx, f_obs = gather(idx, obs)
+        keep = f_idx >= 0
+        feedback.fold([st], None, f_idx[keep], f_obs[keep], beta=0.5, dfp_count=10)
+    return st.lat
+
+
+def _online_rank_main(rank, world, port, out_path):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2102_01887_b200.shard import gather_observations
+
+    t, inv, noise, B = _online_batches()
+
+    def gather(idx, obs):
+        gi, go = gather_observations(torch.from_numpy(idx), torch.from_numpy(obs), B)
+        return gi.numpy(), go.numpy()
+
+    lat = _online_run(t, inv, noise, B, shard_range(B, rank, world), gather)
+    torch.save(torch.from_numpy(lat), f"{out_path}.{rank}")
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_online_fold_keeps_replicas_identical(tmp_path):
+    """Config 5 semantics at world_size 2: every rank folds the gathered, globally ordered
+    observation stream, so the replicated tables end bit-identical to each other and to the
+    single-process run."""
+    out = tmp_path / "lat"
+    mp.start_processes(_online_rank_main, args=(2, _free_port(), str(out)), nprocs=2, join=True,
+                       start_method="spawn")
+    l0 = torch.load(f"{out}.0").numpy()
+    l1 = torch.load(f"{out}.1").numpy()
+    t, inv, noise, B = _online_batches()
+    single = _online_run(t, inv, noise, B, (0, B), lambda i, o: (i, o))
+    assert np.array_equal(l0.view(np.uint64), l1.view(np.uint64))
+    assert np.array_equal(l0.view(np.uint64), single.view(np.uint64))
+    assert not np.array_equal(single, _online_batches()[0].lat)  # the fold did change the table
