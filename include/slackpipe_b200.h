@@ -180,6 +180,32 @@ int sp_table_get_counters(sp_ctx* ctx, sp_table* t, int32_t* completed_ref,
 int sp_table_set_counters(sp_ctx* ctx, sp_table* t, int32_t completed_ref,
                           const int32_t* obs_count /* M, may be NULL */);
 
+/* ---- batched commit step: Configurator.pump_commits rounds (configurator.py:657-756) ---- */
+/* head_flags bits and policy bits */
+#define SP_HEAD_PRESENT 1u  /* the op's speculative queue has a head (configurator.py:708-711) */
+#define SP_HEAD_FORCED 2u   /* the head is a warm-up (DFP) invocation: head.forced            */
+#define SP_COMMIT_FIFO 1    /* "pbc" ablation: key = (invocation_id,)   (configurator.py:716)  */
+#define SP_COMMIT_ESLC 2    /* "eslc" ablation: commit the speculated entry (676-680)          */
+/* R independent rounds over the same n_ops operations (tables[j] = op j, n_ops <= 64, the
+ * reference's `for op in self.tables` order).  Per (round r, op j), i = r*n_ops + j:
+ *   slack[i*K + k]  Configurator.slack_by_kind(op)[kind k]     head_fill[i]  head.fill
+ *   buffered[i]     buffered_count(op)                          head_id[i]    invocation_id
+ *   head_flags[i]   SP_HEAD_*                                   spec_idx/spec_slack/spec_obj[i]
+ *                   head.spec_eidx / spec_slack_s / spec_objective (read under SP_COMMIT_ESLC)
+ * depth[j] = PipelineDag.depths()[op]; full_mask[r] = kinds whose commit queue is saturated.
+ * Outputs per (r, j): the _commit_candidate result (configurator.py:657-691) — out_idx entry
+ * (-1 = None), out_fill fill target, out_slack, out_obj (NaN for forced heads) — and
+ * out_aff the Eq. 3 affinity of the candidate's kind (NaN when not part of the key); per
+ * round out_best[r] = index j of the op whose head the round commits (the minimum priority
+ * key, configurator.py:713-728), or -1 when no op has a candidate. */
+int sp_commit_round(sp_ctx* ctx, int32_t R, int32_t n_ops, sp_table* const* tables, double alpha,
+                    const double* slack, const int32_t* head_fill, const int32_t* buffered,
+                    const int64_t* head_id, const int32_t* depth, const uint32_t* head_flags,
+                    const int32_t* spec_idx, const double* spec_slack, const double* spec_obj,
+                    const uint32_t* full_mask, int32_t policy, int32_t* out_idx,
+                    int32_t* out_fill, double* out_slack, double* out_obj, double* out_aff,
+                    int32_t* out_best, int32_t mem);
+
 #ifdef __cplusplus
 }
 #endif

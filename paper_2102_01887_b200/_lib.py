@@ -38,6 +38,11 @@ SP_MODE_PLAN = 1
 SP_MODE_SCAN = 2
 MODES = {"auto": SP_MODE_AUTO, "plan": SP_MODE_PLAN, "scan": SP_MODE_SCAN}
 
+SP_HEAD_PRESENT = 1
+SP_HEAD_FORCED = 2
+SP_COMMIT_FIFO = 1
+SP_COMMIT_ESLC = 2
+
 MAX_KINDS = 8
 
 # (name, restype, argtypes) for every exported symbol; the CPU test suite checks that
@@ -73,6 +78,7 @@ SIGNATURES = {
     "sp_feedback_fold": (C.c_int, [_p, _i32, _p, _i32, _p, _p, _p, _d, _i32, _i32, _i32, _i32]),
     "sp_table_get_counters": (C.c_int, [_p, _p, _p, _p]),
     "sp_table_set_counters": (C.c_int, [_p, _p, _i32, _p]),
+    "sp_commit_round": (C.c_int, [_p, _i32, _i32, _p, _d] + [_p] * 10 + [_i32] + [_p] * 6 + [_i32]),
 }
 
 

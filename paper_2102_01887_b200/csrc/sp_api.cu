@@ -838,3 +838,97 @@ int sp_table_set_counters(sp_ctx* ctx, sp_table* t, int32_t completed_ref,
 }
 
 }  // extern "C"
+
+// ---- batched commit step (configurator.py:657-756) ----------------------------------------
+extern "C" int sp_commit_round(sp_ctx* ctx, int32_t R, int32_t n_ops, sp_table* const* tables,
+                               double alpha, const double* slack, const int32_t* head_fill,
+                               const int32_t* buffered, const int64_t* head_id,
+                               const int32_t* depth, const uint32_t* head_flags,
+                               const int32_t* spec_idx, const double* spec_slack,
+                               const double* spec_obj, const uint32_t* full_mask, int32_t policy,
+                               int32_t* out_idx, int32_t* out_fill, double* out_slack,
+                               double* out_obj, double* out_aff, int32_t* out_best,
+                               int32_t mem) {
+  if (!ctx || !tables) return fail(SP_E_INVALID, "commit: null argument");
+  if (n_ops < 1 || n_ops > 64) return fail(SP_E_INVALID, "commit: n_ops must be in [1, 64]");
+  if (R < 0) return fail(SP_E_INVALID, "commit: negative round count");
+  if (!(alpha >= 0.0)) return fail(SP_E_INVALID, "alpha must be >= 0");  // configurator.py:37
+  for (int j = 0; j < n_ops; ++j)
+    if (!tables[j]) return fail(SP_E_INVALID, "commit: null table");
+  const int K = tables[0]->K;
+  for (int j = 0; j < n_ops; ++j)
+    if (tables[j]->K != K) return fail(SP_E_INVALID, "commit: tables disagree on kind count");
+  if (R == 0) return SP_OK;
+  if (!slack || !head_fill || !buffered || !head_id || !depth || !head_flags || !spec_idx ||
+      !spec_slack || !spec_obj || !full_mask || !out_idx || !out_fill || !out_slack || !out_obj ||
+      !out_aff || !out_best)
+    return fail(SP_E_INVALID, "commit: required array is null");
+  const size_t N = (size_t)R * n_ops;
+  int rc = SP_OK;
+  void* scratch = ctx_tmp(ctx, commit_scratch_bytes(R, n_ops, K), &rc);
+  if (!scratch) return rc;
+  if (mem == SP_MEM_DEVICE)
+    return commit_launch(ctx, R, n_ops, tables, alpha, slack, head_fill, buffered,
+                         reinterpret_cast<const long long*>(head_id), depth, head_flags, spec_idx,
+                         spec_slack, spec_obj, full_mask, policy, scratch, out_idx, out_fill,
+                         out_slack, out_obj, out_aff, out_best);
+  if (mem != SP_MEM_HOST) return fail(SP_E_INVALID, "commit: bad mem flag");
+  for (size_t i = 0; i < N; ++i) {  // host-side validation of what the kernel will index
+    const int j = (int)(i % n_ops);
+    if ((head_flags[i] & SP_HEAD_PRESENT) && !(head_flags[i] & SP_HEAD_FORCED) &&
+        (policy & SP_COMMIT_ESLC) && (spec_idx[i] < 0 || spec_idx[i] >= tables[j]->M))
+      return fail(SP_E_INVALID, "commit: speculated entry index out of range");
+    if (head_fill[i] < 0 || buffered[i] < 0) return fail(SP_E_INVALID, "commit: negative fill");
+  }
+  const size_t need = rsz<double>(N * K) + 5 * rsz<int32_t>(N) + rsz<int64_t>(N) +
+                      rsz<int32_t>(n_ops) + 2 * rsz<double>(N) + rsz<uint32_t>(R) +
+                      2 * rsz<int32_t>(N) + 3 * rsz<double>(N) + rsz<int32_t>(R);
+  void* io = ctx_io(ctx, need, &rc);
+  if (!io) return rc;
+  Bump b{(uint8_t*)io};
+  cudaStream_t st = ctx->stream;
+  auto up = [&](auto* dst, const void* src, size_t bytes) {
+    return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st);
+  };
+  double* d_slack = b.take<double>(N * K);
+  int32_t* d_fill = b.take<int32_t>(N);
+  int32_t* d_buf = b.take<int32_t>(N);
+  long long* d_id = b.take<long long>(N);
+  int32_t* d_depth = b.take<int32_t>(n_ops);
+  uint32_t* d_hf = b.take<uint32_t>(N);
+  int32_t* d_sidx = b.take<int32_t>(N);
+  double* d_ssl = b.take<double>(N);
+  double* d_sob = b.take<double>(N);
+  uint32_t* d_full = b.take<uint32_t>(R);
+  int32_t* o_idx = b.take<int32_t>(N);
+  int32_t* o_fill = b.take<int32_t>(N);
+  double* o_sl = b.take<double>(N);
+  double* o_ob = b.take<double>(N);
+  double* o_aff = b.take<double>(N);
+  int32_t* o_best = b.take<int32_t>(R);
+  SP_CUDA(up(d_slack, slack, sizeof(double) * N * K));
+  SP_CUDA(up(d_fill, head_fill, 4 * N));
+  SP_CUDA(up(d_buf, buffered, 4 * N));
+  SP_CUDA(up(d_id, head_id, 8 * N));
+  SP_CUDA(up(d_depth, depth, 4 * (size_t)n_ops));
+  SP_CUDA(up(d_hf, head_flags, 4 * N));
+  SP_CUDA(up(d_sidx, spec_idx, 4 * N));
+  SP_CUDA(up(d_ssl, spec_slack, 8 * N));
+  SP_CUDA(up(d_sob, spec_obj, 8 * N));
+  SP_CUDA(up(d_full, full_mask, 4 * (size_t)R));
+  rc = commit_launch(ctx, R, n_ops, tables, alpha, d_slack, d_fill, d_buf, d_id, d_depth, d_hf,
+                     d_sidx, d_ssl, d_sob, d_full, policy, scratch, o_idx, o_fill, o_sl, o_ob,
+                     o_aff, o_best);
+  if (rc != SP_OK) return rc;
+  auto down = [&](void* dst, const void* src, size_t bytes) {
+    return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st);
+  };
+  SP_CUDA(down(out_idx, o_idx, 4 * N));
+  SP_CUDA(down(out_fill, o_fill, 4 * N));
+  SP_CUDA(down(out_slack, o_sl, 8 * N));
+  SP_CUDA(down(out_obj, o_ob, 8 * N));
+  SP_CUDA(down(out_aff, o_aff, 8 * N));
+  SP_CUDA(down(out_best, o_best, 4 * (size_t)R));
+  SP_CUDA(cudaStreamSynchronize(st));
+  return SP_OK;
+}

@@ -219,6 +219,14 @@ int select_launch(sp_ctx* ctx, int n_tables, sp_table* const* tables, double alp
                   double* out_slack, double* out_wait, double* out_kind_min, int mode);
 int affinity_launch(sp_ctx* ctx, int N, int K, const double* kmin, const int32_t* q,
                     double* out);
+int commit_launch(sp_ctx* ctx, int R, int n_ops, sp_table* const* tables, double alpha,
+                  const double* slack, const int32_t* fill, const int32_t* buffered,
+                  const long long* head_id, const int32_t* depth, const uint32_t* hflags,
+                  const int32_t* spec_idx, const double* spec_slack, const double* spec_obj,
+                  const uint32_t* full_mask, int policy, void* scratch, int32_t* out_idx,
+                  int32_t* out_fill, double* out_slack, double* out_obj, double* out_aff,
+                  int32_t* out_best);
+size_t commit_scratch_bytes(int R, int n_ops, int K);
 int scores_launch(sp_ctx* ctx, sp_table* t, Plan* p, const double* slack_dev,
                   double* score_dev, double* cost_dev);
 int slack_launch(sp_ctx* ctx, sp_dag* g, int I, const double* ref, int ref_stride,

@@ -15,6 +15,10 @@ where /root/reference does not exist.  Files:
   queue_cases.npz    estimate_queueing on random lists (+ the reference's 20 fixtures)
   amber_trace.npz    every OpTable.select / affinity / set_latency call of the reference
                      AMBER (`branching`) run at the 50% target, in call order, with results
+  commit_rounds.npz  every Configurator.pump_commits round (one _commit_candidate per op with a
+                     speculated head, then the winner) of AMBER runs at the 50% and fast
+                     targets and under the pbc / eslc ablations, interleaved in order with the
+                     set_latency calls that change the tables between rounds
 """
 from __future__ import annotations
 
@@ -479,6 +483,131 @@ def gen_amber(R, ref_root: Path, target=142.20064921472454):
     return out
 
 
+
+# ---- 7. commit rounds (Configurator.pump_commits) -----------------------
+
+def gen_commit_rounds(R, ref_root: Path, max_rounds=6000):
+    """Record, for AMBER runs of the reference engine, each pump_commits round: per op with a
+    speculated head the inputs of _commit_candidate (head fill / forced / id / speculated entry,
+    buffered items, saturated kinds, the op's slack per kind) and its result, plus the winner
+    (the invocation the round committed).  set_latency calls are recorded in the same order so a
+    replay can keep the tables identical.  Everything is captured by wrapping the reference's own
+    methods; no reference logic is restated here."""
+    conf, man, pipe, prof, scen = R
+    from slackpipe import workload
+
+    bundle = ref_root / "scenarios" / "branching"
+    dag, ops = pipe.load_pipeline(json.loads((bundle / "pipeline.json").read_text()))
+    sc = scen.load_scenario(bundle / "scenario.json")
+    frames = workload.load_trace(bundle / "trace.jsonl")
+    profiles = {n: prof.profile_operation(o, sc, sc.tuning.samples_per_config) for n, o in ops.items()}
+    kinds = sc.backend_kinds()
+    op_names = sorted(dag.vertices)
+    paths = pipe.decompose_paths(dag)
+    runs = [(142.20064921472454, ()), (0.0, ()), (142.20064921472454, ("pbc",)),
+            (142.20064921472454, ("eslc",))]
+    C = {k: [] for k in ("round", "op", "fill", "forced", "inv", "spec_idx", "spec_kind", "spec_slack",
+                         "spec_obj", "buffered", "full_mask", "slack", "r_idx", "r_fill", "r_slack",
+                         "r_obj")}
+    Rd = {k: [] for k in ("run", "seq", "winner_op", "winner_inv", "first_cand", "n_cand")}
+    S = {k: [] for k in ("run", "seq", "op", "idx", "val")}
+    run_meta = []
+    orig_cc, orig_pump, orig_set = conf.Configurator._commit_candidate, conf.Configurator.pump_commits, \
+        conf.OpTable.set_latency
+    state = {"run": 0, "seq": 0, "open": None, "rounds": 0}
+
+    def close(winner_inv=None, winner_op=-1):
+        o = state["open"]
+        if o is not None and o["n"] > 0:
+            Rd["run"].append(state["run"])
+            Rd["seq"].append(state["seq"])
+            Rd["winner_op"].append(winner_op)
+            Rd["winner_inv"].append(-1 if winner_inv is None else winner_inv)
+            Rd["first_cand"].append(o["first"])
+            Rd["n_cand"].append(o["n"])
+            state["seq"] += 1
+            state["rounds"] += 1
+        state["open"] = None
+
+    def cc(self, op, head, full_kinds, buffered):
+        r = orig_cc(self, op, head, full_kinds, buffered)
+        if state["rounds"] >= max_rounds:
+            return r
+        if state["open"] is None:
+            state["open"] = {"first": len(C["op"]), "n": 0}
+        sl = self.slack_by_kind(op)
+        C["round"].append(len(Rd["run"]))
+        C["op"].append(op_names.index(op))
+        C["fill"].append(head.fill)
+        C["forced"].append(int(head.forced))
+        C["inv"].append(head.invocation_id)
+        C["spec_idx"].append(head.spec_eidx)
+        C["spec_kind"].append(kinds.index(head.spec_entry.backend_kind) if head.spec_entry is not None else -1)
+        C["spec_slack"].append(float(head.spec_slack_s))
+        C["spec_obj"].append(float(head.spec_objective))
+        C["buffered"].append(int(buffered))
+        C["full_mask"].append(sum(1 << kinds.index(k) for k in full_kinds))
+        C["slack"].append([float(sl.get(k, math.nan)) for k in kinds])
+        if r is None:
+            C["r_idx"].append(-1); C["r_fill"].append(0); C["r_slack"].append(0.0); C["r_obj"].append(0.0)
+        else:
+            C["r_idx"].append(r[1]); C["r_fill"].append(r[2]); C["r_slack"].append(float(r[3]))
+            C["r_obj"].append(float(r[4]))
+        state["open"]["n"] += 1
+        return r
+
+    def pump(self, buffered_count, topup):
+        close()
+        return orig_pump(self, buffered_count, topup)
+
+    def setl(self, index, latency_s):
+        orig_set(self, index, latency_s)
+        if state["rounds"] >= max_rounds:
+            return
+        close()
+        S["run"].append(state["run"])
+        S["seq"].append(state["seq"])
+        S["op"].append(op_names.index(self.operation))
+        S["idx"].append(index)
+        S["val"].append(float(self.lat[index]))
+        state["seq"] += 1
+
+    class Log(list):
+        def append(self, e):
+            super().append(e)
+            if e[1] == "commit" and state["open"] is not None and state["rounds"] < max_rounds:
+                close(winner_inv=e[2], winner_op=op_names.index(e[3]))
+
+    conf.Configurator._commit_candidate, conf.Configurator.pump_commits = cc, pump
+    conf.OpTable.set_latency = setl
+    try:
+        for ri, (target, abl) in enumerate(runs):
+            state.update(run=ri, open=None, rounds=0)
+            run = man.PipelineRun(dag, ops, profiles, frames, sc, target, conf.TuningParams(
+                alpha=sc.tuning.alpha, smoothing_beta=sc.tuning.smoothing_beta,
+                dfp_count=sc.tuning.dfp_count, straggler_timeout_factor=sc.tuning.straggler_timeout_factor,
+                cq_capacity=sc.tuning.cq_capacity), ablations=abl, paths=paths,
+                pipeline_name="video_branching")
+            run.configurator.decision_log = Log()
+            run_meta.append({"target": target, "ablations": list(abl), "alpha": run.params.alpha,
+                             "depths": [run.depths[o] for o in op_names],
+                             "tables": {n: {"lat": [e.latency_s for e in run.tables[n].entries],
+                                            "ref_index": run.tables[n].ref_index}
+                                        for n in op_names}})
+            run.run_to_completion()
+            close()
+    finally:
+        conf.Configurator._commit_candidate, conf.Configurator.pump_commits = orig_cc, orig_pump
+        conf.OpTable.set_latency = orig_set
+    out = {f"c_{k}": np.array(v) for k, v in C.items()}
+    out["c_slack"] = np.array(C["slack"], dtype=np.float64)
+    out.update({f"r_{k}": np.array(v, dtype=np.int64) for k, v in Rd.items()})
+    out.update({f"s_{k}": np.array(v) for k, v in S.items()})
+    out["s_val"] = np.array(S["val"], dtype=np.float64)
+    meta = {"kinds": kinds, "ops": op_names, "runs": run_meta, "max_rounds": max_rounds}
+    out["meta_json"] = np.frombuffer(json.dumps(meta).encode(), np.uint8)
+    return out
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--ref", default="/root/reference/pkg/src")
@@ -493,6 +622,7 @@ def main() -> None:
         "feedback_cases": lambda: gen_feedback(R),
         "queue_cases": lambda: gen_queue(R),
         "amber_trace": lambda: gen_amber(R, ref_root),
+        "commit_rounds": lambda: gen_commit_rounds(R, ref_root),
     }
     for name, fn in jobs.items():
         if a.only and name not in a.only.split(","):

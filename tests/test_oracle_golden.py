@@ -269,3 +269,67 @@ def test_oracle_against_live_reference_random(ref):
         else:
             assert r[:3] == (2 if d.kind == "delay" else 1, d.entry_index, d.fill)
             assert _same(r[3], d.objective_value) and _same(r[5], d.wait_budget_s)
+
+
+# ---- commit rounds (Configurator.pump_commits) --------------------------------------------------
+
+def _commit_replay(max_rounds_per_run=None):
+    """Yield (tables, round index, per-op inputs) in the recorded order, applying the recorded
+    set_latency calls to the oracle tables in between."""
+    from oracle import commit as oc
+
+    d = golden("commit_rounds")
+    meta = golden_json(d, "meta_json")
+    amb = golden_json(golden("amber_trace"), "meta_json")
+    runs = d["r_run"]
+    for ri, rm in enumerate(meta["runs"]):
+        tabs = oc.amber_tables(amb)
+        for t, name in zip(tabs, meta["ops"]):
+            t.lat[:] = rm["tables"][name]["lat"]
+        ev = [(int(s), 0, i) for i, s in enumerate(d["s_seq"]) if d["s_run"][i] == ri]
+        ev += [(int(s), 1, i) for i, s in enumerate(d["r_seq"]) if runs[i] == ri]
+        ev.sort()
+        seen = 0
+        for _, typ, i in ev:
+            if typ == 0:
+                tabs[d["s_op"][i]].lat[d["s_idx"][i]] = d["s_val"][i]
+                continue
+            seen += 1
+            if max_rounds_per_run and seen > max_rounds_per_run:
+                break
+            yield ri, rm, tabs, i
+
+
+def test_commit_round_oracle_matches_reference_rounds():
+    """oracle/commit.py reproduces every recorded round: each _commit_candidate result and the
+    committed op (4 runs: 50% target, fast target, pbc and eslc ablations)."""
+    from oracle import commit as oc
+
+    d = golden("commit_rounds")
+    n_rounds = n_cands = 0
+    for ri, rm, tabs, i in _commit_replay(max_rounds_per_run=700):
+        a, n = int(d["r_first_cand"][i]), int(d["r_n_cand"][i])
+        heads, slacks, buffered = [None] * len(tabs), [None] * len(tabs), [0] * len(tabs)
+        full = None
+        for c in range(a, a + n):
+            j = int(d["c_op"][c])
+            heads[j] = oc.Head(int(d["c_fill"][c]), bool(d["c_forced"][c]), int(d["c_inv"][c]),
+                               int(d["c_spec_idx"][c]), float(d["c_spec_slack"][c]),
+                               float(d["c_spec_obj"][c]))
+            slacks[j] = np.nan_to_num(d["c_slack"][c], nan=0.0)
+            buffered[j] = int(d["c_buffered"][c])
+            full = int(d["c_full_mask"][c])
+            cand = oc.commit_candidate(tabs[j], slacks[j], heads[j], full, buffered[j], rm["alpha"],
+                                       "eslc" in rm["ablations"])
+            if d["c_r_idx"][c] < 0:
+                assert cand is None
+            else:
+                assert cand[0] == d["c_r_idx"][c] and cand[1] == d["c_r_fill"][c]
+                assert cand[2] == d["c_r_slack"][c]
+                assert (math.isnan(cand[3]) and math.isnan(d["c_r_obj"][c])) or cand[3] == d["c_r_obj"][c]
+            n_cands += 1
+        w = oc.round_winner(tabs, slacks, heads, full, buffered, rm["depths"], rm["alpha"],
+                            fifo="pbc" in rm["ablations"], eslc="eslc" in rm["ablations"])
+        assert (w[0] if w else -1) == d["r_winner_op"][i]
+        n_rounds += 1
+    assert n_rounds == 4 * 700 and n_cands > 4000
