@@ -7,6 +7,9 @@ c3  deep DAG: 64 ops, 845 edges (~3.3e9 decomposed paths, which the reference ca
 c4  latency-target sweep x replicas on the AMBER pipeline: 10,000 replicas x 5 targets
     (0.5x..10x the fast-anchor latency) x 64 snapshots; per snapshot K1 (7 ops x 4 kinds) feeds
     K2 directly on the device (one decision per op) — 22.4M decisions per step.
+commit  batched commit step: 65,536 independent Configurator.pump_commits
+    rounds over the 7 AMBER operations per call (one K2 re-selection of every head + a warp
+    key reduction per round); CPU baseline: oracle/commit.py round_winner on all host cores.
 c5  online mode: 2^24 invocations x 16,384 configurations in 256 batches of 65,536; every batch is
     decided against the batch-start profile snapshot, the chosen configurations produce noisy
     latency observations, and K3 folds them back (the next batch's plan is rebuilt on device).
@@ -350,5 +353,122 @@ def run_c5(args):
     print(json.dumps(line), flush=True)
 
 
+
+# ---- commit rounds --------------------------------------------------------------------------
+
+def _commit_inputs(meta, R, seed=8):
+    rng = np.random.default_rng(seed)
+    n_ops, K = len(meta["ops"]), len(meta["kinds"])
+    refs = np.array([meta["tables"][o]["ref_index"] for o in meta["ops"]])
+    present = rng.random((R, n_ops)) < 0.8
+    forced = present & (rng.random((R, n_ops)) < 0.1) & (refs[None, :] >= 0)
+    return {
+        "slack": rng.uniform(-2.0, 20.0, size=(R, n_ops, K)),
+        "fill": rng.integers(1, 5, size=(R, n_ops)).astype(np.int32),
+        "buffered": rng.integers(0, 9, size=(R, n_ops)).astype(np.int32),
+        "head_id": np.arange(R * n_ops, dtype=np.int64).reshape(R, n_ops)[:, rng.permutation(n_ops)],
+        "flags": (present.astype(np.uint32) | (forced.astype(np.uint32) << 1)),
+        "full": (rng.random((R, K)) < 0.2).astype(np.uint32) @ (1 << np.arange(K, dtype=np.uint32)),
+        # PipelineDag.depths (pipeline.py:328-337): longest edge distance from a source
+        "depth": np.array([max(p.index(o) for p in meta["paths"] if o in p) for o in meta["ops"]],
+                          dtype=np.int32),
+    }
+
+
+def _commit_cpu_worker(args):
+    from oracle import commit as oc
+
+    meta, x, lo, hi, alpha = args
+    tabs = oc.amber_tables(meta)
+    won = 0
+    for r in range(lo, hi):
+        heads = [oc.Head(int(x["fill"][r, j]), bool(x["flags"][r, j] & 2), int(x["head_id"][r, j]))
+                 if x["flags"][r, j] & 1 else None for j in range(len(tabs))]
+        w = oc.round_winner(tabs, x["slack"][r], heads, int(x["full"][r]), x["buffered"][r],
+                            x["depth"], alpha)
+        won += w is not None
+    return hi - lo
+
+
+def run_commit(args):
+    import torch
+
+    import paper_2102_01887_b200 as sp
+
+    with np.load(ROOT / "tests" / "golden" / "amber_trace.npz") as z:
+        meta = json.loads(bytes(z["meta_json"]).decode())
+    rank, world, local = _dist(torch)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    ctx = sp.get_context(local)
+    ctx.set_stream(stream.cuda_stream)
+    tabs = _amber_tables(sp, meta)
+    R = 65536
+    x = _commit_inputs(meta, R, seed=8 + rank)
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    d = {k: T(v) for k, v in x.items()}
+    alpha = 100.0
+
+    def step():
+        return sp.commit_round(tabs, d["slack"], d["fill"], d["buffered"], d["head_id"], d["depth"],
+                               d["flags"], alpha=alpha, full_mask=d["full"])
+
+    for _ in range(args.warmup):
+        out = step()
+    torch.cuda.synchronize(dev)
+    # parity spot check against the oracle on the first rounds (checker only)
+    from oracle import commit as oc
+
+    otabs = oc.amber_tables(meta)
+    best = out["best"][:64].cpu().numpy()
+    for r in range(64):
+        heads = [oc.Head(int(x["fill"][r, j]), bool(x["flags"][r, j] & 2), int(x["head_id"][r, j]))
+                 if x["flags"][r, j] & 1 else None for j in range(len(otabs))]
+        w = oc.round_winner(otabs, x["slack"][r], heads, int(x["full"][r]), x["buffered"][r],
+                            x["depth"], alpha)
+        assert (w[0] if w else -1) == best[r], f"commit round {r} disagrees with the oracle"
+    _barrier(torch)
+    evs = _events(torch, args.steps)
+    l0 = ctx.launch_count
+    for i in range(args.steps):
+        evs[i][0].record(stream)
+        step()
+        evs[i][1].record(stream)
+    torch.cuda.synchronize(dev)
+    ms = [a.elapsed_time(b) for a, b in evs]
+    t = _tmax(torch, sum(ms) / 1e3, dev)
+    if rank != 0:
+        return
+    cpu = None
+    if world == 1:
+        import multiprocessing as mp
+
+        cores = os.cpu_count() or 1
+        S = 3000 * cores
+        xs = {k: v for k, v in x.items()}
+        work = [(meta, xs, int(a[0]), int(a[-1]) + 1, alpha)
+                for a in np.array_split(np.arange(S), cores) if len(a)]
+        t0 = time.perf_counter()
+        with mp.get_context("fork").Pool(len(work)) as pool:
+            n = sum(pool.map(_commit_cpu_worker, work))
+        dt = time.perf_counter() - t0
+        cpu = {"value": n / dt, "unit": "rounds/s", "cores": cores, "kind": "port",
+               "sample": f"{S} rounds, oracle/commit.py round_winner (configurator.py:657-728) on "
+                         f"{cores} processes"}
+    heads = int((x["flags"] & 1).sum())
+    line = {
+        "workload": "commit", "metric": "Configurator.pump_commits rounds / s (batched commit step)",
+        "unit": "rounds/s", "value": args.steps * R * world / t, "ms_per_step": 1e3 * t / args.steps,
+        "steps": args.steps, "n_gpus": world, "scaling": "weak",
+        "heads_per_s": args.steps * heads * world / t,
+        "config": {"rounds_per_call": R, "ops": len(tabs), "kinds": len(meta["kinds"]),
+                   "heads_per_call": heads, "alpha": alpha,
+                   "inputs": "synthetic heads (80% present, 10% forced), slack U(-2, 20), 20% kinds saturated"},
+        "gpu_launches": ctx.launch_count - l0,
+        "cpu_baseline": cpu,
+        "step_ms": {"median": statistics.median(ms), "min": min(ms), "max": max(ms)},
+    }
+    print(json.dumps(line), flush=True)
+
 def main(args):
-    {"c3": run_c3, "c4": run_c4, "c5": run_c5}[args.workload](args)
+    {"c3": run_c3, "c4": run_c4, "c5": run_c5, "commit": run_commit}[args.workload](args)
