@@ -120,9 +120,10 @@ static void free_table(sp_table* t) {
   for (int32_t* p : ii) cudaFree(p);
   cudaFree(t->ukey);
   cudaFree(t->uent);
-  uint32_t* uu[] = {t->ukr, t->umap, t->r1, t->r2, t->lpos, t->pf, t->sf, t->rowscratch,
+  uint32_t* uu[] = {t->ukr, t->umap, t->r1, t->r2, t->pf, t->sf, t->rowscratch,
                     t->candf, t->cands, t->cidf, t->cids};
   for (uint32_t* p : uu) cudaFree(p);
+  cudaFree(t->sort_tmp);
   for (auto& p : t->plans) plan_release(p);
   delete t;
 }

@@ -149,7 +149,10 @@ struct sp_table {
           *obs_count = nullptr;
   int32_t* kind_slot = nullptr;  // position of the entry inside its kind block (static order by kind, idx)
   // plan scratch (device)
-  uint32_t *r1 = nullptr, *r2 = nullptr, *lpos = nullptr;
+  uint32_t *r1 = nullptr, *r2 = nullptr;
+  // scratch of the plan's three entry-order sorts (tile + merged item buffers)
+  void* sort_tmp = nullptr;
+  size_t sort_tmp_bytes = 0;
   int32_t *ent_r1 = nullptr, *ent_r2 = nullptr, *order = nullptr;
   uint32_t *pf = nullptr, *sf = nullptr;      // W*(M+K) each
   uint32_t* rowscratch = nullptr;             // (M+K) * 2W

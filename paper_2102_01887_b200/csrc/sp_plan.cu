@@ -28,6 +28,8 @@
 #include <algorithm>
 #include <cstring>
 
+#include <cub/cub.cuh>
+
 #include "sp_internal.cuh"
 
 namespace sp {
@@ -56,60 +58,169 @@ __global__ void k_cost(int M, const double* __restrict__ lat, const double* __re
   costpen[j] = __dadd_rn(c, pen);
 }
 
-// 2-D rank counting: block (x) owns 256 entries i, (y) one chunk of 256 entries j.
-constexpr int kRankChunk = 256;
-__global__ void __launch_bounds__(256) k_rank(int M, const double* __restrict__ lat,
-                                              const double* __restrict__ cost,
-                                              const double* __restrict__ costpen,
-                                              const double* __restrict__ res,
-                                              const int32_t* __restrict__ id_rank,
-                                              const int32_t* __restrict__ kind,
-                                              uint32_t* r1, uint32_t* r2, uint32_t* lpos) {
-  __shared__ double s_cost[kRankChunk], s_cp[kRankChunk], s_res[kRankChunk], s_lat[kRankChunk];
-  __shared__ int32_t s_id[kRankChunk], s_kind[kRankChunk];
-  int j0 = blockIdx.y * kRankChunk;
-  int nj = min(kRankChunk, M - j0);
-  for (int t = threadIdx.x; t < nj; t += blockDim.x) {
-    int j = j0 + t;
-    s_cost[t] = cost[j];
-    s_cp[t] = costpen[j];
-    s_res[t] = res[j];
-    s_lat[t] = lat[j];
-    s_id[t] = id_rank[j];
-    s_kind[t] = kind[j];
-  }
-  __syncthreads();
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= M) return;
-  double ci = cost[i], pi = costpen[i], ri = res[i], li = lat[i];
-  int idi = id_rank[i], ki = kind[i];
-  uint32_t c1 = 0, c2 = 0, c3 = 0;
-  for (int t = 0; t < nj; ++t) {
-    double cj = s_cost[t], pj = s_cp[t], rj = s_res[t], lj = s_lat[t];
-    int idj = s_id[t];
-    // (cost, res, id_rank) lexicographic
-    bool lt1 = (cj < ci) || (cj == ci && (rj < ri || (rj == ri && idj < idi)));
-    // (costpen, cost, res, id_rank) lexicographic
-    bool lt2 = (pj < pi) || (pj == pi && lt1);
-    // stable latency order inside the kind
-    bool lt3 = (s_kind[t] == ki) && ((lj < li) || (lj == li && (j0 + t) < i));
-    c1 += lt1;
-    c2 += lt2;
-    c3 += lt3;
-  }
-  if (c1) atomicAdd(&r1[i], c1);
-  if (c2) atomicAdd(&r2[i], c2);
-  if (c3) atomicAdd(&lpos[i], c3);
+// ---- the plan's three entry orders ---------------------------------------------------------
+//   r1     rank under (cost, res, id_rank)            -> tie order of feasible entries
+//   r2     rank under (costpen, cost, res, id_rank)   =  (costpen, r1)
+//   order  entries by (kind, lat, index)              -> latency order inside each kind
+// Each is a sort of M unique (u64 key, u32 tag) items: CTA tiles of 2048 items are sorted with
+// a block merge sort (k_tile_sort), then every item's final position is its rank inside its
+// tile plus, per other tile, the number of smaller items there (binary search, k_merge_rank).
+// r1 sorts by (cost, index) and then resolves exact-equality cost ties by (res, id_rank)
+// inside each (short) tie run (k_rank_r1).
+
+__device__ __forceinline__ uint64_t dkey(double x) {
+  return order_key(static_cast<uint64_t>(__double_as_longlong(x)));
 }
 
-__global__ void k_invert(int M, const uint32_t* __restrict__ r1, const uint32_t* __restrict__ r2,
-                         const uint32_t* __restrict__ lpos, const int32_t* __restrict__ kind,
-                         KindInfo ki, int32_t* ent_r1, int32_t* ent_r2, int32_t* order) {
-  int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= M) return;
-  ent_r1[r1[j]] = j;
-  ent_r2[r2[j]] = j;
-  order[ki.base[kind[j]] + (int)lpos[j]] = j;
+struct __align__(16) SItem {
+  uint64_t k;
+  uint32_t t;
+  uint32_t pad;
+};
+constexpr int kSortThreads = 512, kSortIpt = 4, kSortTile = kSortThreads * kSortIpt;
+constexpr int kSortR1 = 0, kSortR2 = 1, kSortOrder = 2;
+
+template <int KIND>
+struct SLess {
+  __device__ __forceinline__ bool operator()(const SItem& a, const SItem& b) const {
+    if (KIND == kSortOrder) {  // (kind, lat, index): kind in the tag's top byte
+      const uint32_t ka = a.t >> 24, kb = b.t >> 24;
+      if (ka != kb) return ka < kb;
+      if (a.k != b.k) return a.k < b.k;
+      return (a.t & 0xFFFFFFu) < (b.t & 0xFFFFFFu);
+    }
+    return a.k < b.k || (a.k == b.k && a.t < b.t);
+  }
+};
+
+__device__ __forceinline__ SItem sentinel() {
+  SItem x;
+  x.k = ~0ull;
+  x.t = 0xFFFFFFFFu;
+  x.pad = 0;
+  return x;
+}
+
+// item of entry / position j for sort KIND (j >= M: sentinel)
+template <int KIND>
+__device__ __forceinline__ SItem make_item(int j, int M, const double* __restrict__ a,
+                                           const int32_t* __restrict__ b) {
+  if (j >= M) return sentinel();
+  SItem x;
+  x.pad = 0;
+  if (KIND == kSortR1) {        // a = cost
+    x.k = dkey(a[j]);
+    x.t = (uint32_t)j;
+  } else if (KIND == kSortR2) {  // position j of the r1 order: a = costpen, b = ent_r1
+    x.k = dkey(a[b[j]]);
+    x.t = (uint32_t)j;           // r1 rank
+  } else {                       // a = lat, b = kind
+    x.k = dkey(a[j]);
+    x.t = ((uint32_t)b[j] << 24) | (uint32_t)j;
+  }
+  return x;
+}
+
+template <int KIND>
+__device__ void tile_sort(int M, int tile, const double* a, const int32_t* b, SItem* out,
+                          void* temp) {
+  using Sort = cub::BlockMergeSort<SItem, kSortThreads, kSortIpt>;
+  SItem it[kSortIpt];
+  const int base = tile * kSortTile + threadIdx.x * kSortIpt;
+#pragma unroll
+  for (int q = 0; q < kSortIpt; ++q) it[q] = make_item<KIND>(base + q, M, a, b);
+  Sort(*reinterpret_cast<typename Sort::TempStorage*>(temp)).Sort(it, SLess<KIND>());
+#pragma unroll
+  for (int q = 0; q < kSortIpt; ++q) out[base + q] = it[q];
+}
+
+// blockIdx.x < ntiles: sort A (KA) tile; otherwise sort B (KB) tile (B may be absent)
+template <int KA, int KB>
+__global__ void __launch_bounds__(kSortThreads) k_tile_sort(int M, int ntiles, const double* aA,
+                                                            const int32_t* bA, SItem* outA,
+                                                            const double* aB, const int32_t* bB,
+                                                            SItem* outB) {
+  __shared__ typename cub::BlockMergeSort<SItem, kSortThreads, kSortIpt>::TempStorage temp;
+  if ((int)blockIdx.x < ntiles)
+    tile_sort<KA>(M, blockIdx.x, aA, bA, outA, &temp);
+  else
+    tile_sort<KB>(M, blockIdx.x - ntiles, aB, bB, outB, &temp);
+}
+
+template <int KIND>
+__device__ __forceinline__ int merged_rank(const SItem* __restrict__ tiles, int ntiles, int p) {
+  const SItem x = tiles[p];
+  const int a = p / kSortTile;
+  int r = p - a * kSortTile;
+  SLess<KIND> less;
+  for (int bt = 0; bt < ntiles; ++bt) {
+    if (bt == a) continue;
+    const SItem* t = tiles + (size_t)bt * kSortTile;
+    int lo = 0, hi = kSortTile;  // # items of tile bt smaller than x (items are unique)
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (less(t[mid], x)) lo = mid + 1; else hi = mid;
+    }
+    r += lo;
+  }
+  return r;
+}
+
+// final positions of both sorts' items; only real items (position < M) are written
+template <int KA, int KB>
+__global__ void k_merge_rank(int M, int ntiles, const SItem* __restrict__ tA, SItem* outA,
+                             const SItem* __restrict__ tB, SItem* outB) {
+  const int n = ntiles * kSortTile;
+  int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < n) {
+    const int r = merged_rank<KA>(tA, ntiles, p);
+    if (r < M) outA[r] = tA[p];
+  } else if (tB && p < 2 * n) {
+    p -= n;
+    const int r = merged_rank<KB>(tB, ntiles, p);
+    if (r < M) outB[r] = tB[p];
+  }
+}
+
+// position p of the (cost, index) order -> r1 (ties by (res, id_rank), configurator.py:235-237)
+__global__ void k_rank_r1(int M, const SItem* __restrict__ srt, const double* __restrict__ res,
+                          const int32_t* __restrict__ id_rank, uint32_t* r1, int32_t* ent_r1) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= M) return;
+  const uint64_t k = srt[p].k;
+  const int e = (int)srt[p].t;
+  int r = p;
+  const bool tl = p > 0 && srt[p - 1].k == k, tr = p + 1 < M && srt[p + 1].k == k;
+  if (tl || tr) {
+    int a = p, b = p + 1;
+    while (a > 0 && srt[a - 1].k == k) --a;
+    while (b < M && srt[b].k == k) ++b;
+    const double re = res[e];
+    const int ie = id_rank[e];
+    int c = 0;
+    for (int q = a; q < b; ++q) {
+      const int f = (int)srt[q].t;
+      const double rf = res[f];
+      c += (rf < re) || (rf == re && id_rank[f] < ie);
+    }
+    r = a + c;
+  }
+  r1[e] = (uint32_t)r;
+  ent_r1[r] = e;
+}
+
+// sorted (costpen, r1) items -> ent_r2 / r2;  sorted (kind, lat, index) items -> order
+__global__ void k_orders_out(int M, const SItem* __restrict__ s2, const int32_t* __restrict__ ent_r1,
+                             int32_t* ent_r2, uint32_t* r2, const SItem* __restrict__ s3,
+                             int32_t* order) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= M) return;
+  if (s2) {
+    const int e = ent_r1[s2[q].t];
+    ent_r2[q] = e;
+    r2[e] = (uint32_t)q;
+  }
+  if (s3) order[q] = (int32_t)(s3[q].t & 0xFFFFFFu);
 }
 
 __device__ __forceinline__ uint32_t warp_incl_min(uint32_t v, int lane) {
@@ -179,9 +290,13 @@ __device__ int block_excl_max(int v, int* s_warp) {
   return r;
 }
 
-// One CTA (1024 threads) per kind.  Phase A: warp w < W builds the prefix-min of r1 for
-// batch lane b = w; warp W <= w < 2W the suffix-min of r2 for lane w - W.  Phase B: rows
-// at latency boundaries, merged when identical to the previous boundary's row.
+// One CTA (1024 threads) per kind.  Phase A: per batch lane b the prefix-min of r1 (feasible
+// side, positions < p) and the suffix-min of r2 (penalized side, positions >= p) over the
+// kind's latency order — every thread owns a contiguous chunk of positions, the per-chunk
+// lane minima are scanned across chunks in shared memory (one warp per lane and direction),
+// then each thread writes its chunk with the carried minima.  Phase B: rows at latency
+// boundaries, merged when identical to the previous boundary's row.
+constexpr int kStairMaxW = 16;
 __global__ void __launch_bounds__(1024) k_stair(int M, int K, int W, KindInfo ki,
                                                 const int32_t* __restrict__ order,
                                                 const int32_t* __restrict__ bidx,
@@ -191,6 +306,7 @@ __global__ void __launch_bounds__(1024) k_stair(int M, int K, int W, KindInfo ki
                                                 uint32_t* sf, double* thrscratch,
                                                 uint32_t* rowscratch, int32_t* rows_per_kind,
                                                 uint32_t* candf, uint32_t* cands) {
+  extern __shared__ uint32_t s_lane[];  // [2][W][blockDim.x]: chunk minima -> carries
   __shared__ int s_warp[32];
   __shared__ int s_carry_b, s_carry_rows, s_lastb;
   const int k = blockIdx.x;
@@ -202,41 +318,81 @@ __global__ void __launch_bounds__(1024) k_stair(int M, int K, int W, KindInfo ki
     if (threadIdx.x == 0) rows_per_kind[k] = 0;
     return;
   }
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  if (w < 2 * W) {
-    const int b = w % W;
-    if (w < W) {
-      uint32_t* out = pf + (size_t)b * stride + ext;
-      uint32_t carry = kInf32;
-      if (lane == 0) out[0] = kInf32;
-      for (int q0 = 0; q0 < Mk; q0 += 32) {
-        int q = q0 + lane;
-        uint32_t v = kInf32;
-        if (q < Mk) {
-          int e = order[base + q];
-          if (bidx[e] == b) v = r1[e];
-        }
-        uint32_t incl = min(warp_incl_min(v, lane), carry);
-        if (q < Mk) out[q + 1] = incl;
-        carry = __shfl_sync(0xffffffffu, incl, 31);
+  const int T = blockDim.x, t = threadIdx.x;
+  uint32_t* A = s_lane;          // prefix side
+  uint32_t* B = s_lane + W * T;  // suffix side
+  const int P = (Mk + T - 1) / T;
+  const int q0 = min(t * P, Mk), q1 = min(q0 + P, Mk);
+  for (int b = 0; b < W; ++b) {
+    A[b * T + t] = kInf32;
+    B[b * T + t] = kInf32;
+  }
+  for (int q = q0; q < q1; ++q) {
+    const int e = order[base + q];
+    const int b = bidx[e];
+    A[b * T + t] = min(A[b * T + t], r1[e]);
+    B[b * T + t] = min(B[b * T + t], r2[e]);
+  }
+  __syncthreads();
+  {  // warp w: lane b = w % W, direction w / W; exclusive scan over the T chunk minima
+    const int w = t >> 5, l = t & 31;
+    if (w < 2 * W) {
+      const bool suf = w >= W;
+      uint32_t* v = (suf ? B : A) + (w % W) * T;
+      const int per = T / 32;
+      uint32_t m = kInf32;
+      for (int c = 0; c < per; ++c) {
+        const int idx = suf ? T - 1 - (l * per + c) : l * per + c;
+        m = min(m, v[idx]);
       }
-    } else {
-      uint32_t* out = sf + (size_t)b * stride + ext;
-      uint32_t carry = kInf32;
-      if (lane == 0) out[Mk] = kInf32;
-      for (int hi = Mk - 1; hi >= 0; hi -= 32) {
-        int q = hi - lane;
-        uint32_t v = kInf32;
-        if (q >= 0) {
-          int e = order[base + q];
-          if (bidx[e] == b) v = r2[e];
-        }
-        uint32_t incl = min(warp_incl_min(v, lane), carry);
-        if (q >= 0) out[q] = incl;
-        carry = __shfl_sync(0xffffffffu, incl, 31);
+      uint32_t incl = warp_incl_min(m, l);
+      uint32_t carry = __shfl_up_sync(0xffffffffu, incl, 1);
+      if (l == 0) carry = kInf32;
+      for (int c = 0; c < per; ++c) {
+        const int idx = suf ? T - 1 - (l * per + c) : l * per + c;
+        const uint32_t x = v[idx];
+        v[idx] = carry;  // minimum over the chunks before (prefix) / after (suffix) this one
+        carry = min(carry, x);
       }
     }
   }
+  __syncthreads();
+  {
+    uint32_t run[kStairMaxW];
+#pragma unroll
+    for (int b = 0; b < kStairMaxW; ++b) run[b] = b < W ? A[b * T + t] : kInf32;
+    for (int q = q0; q < q1; ++q) {  // pf[b][ext + q] = min r1 over positions < q
+#pragma unroll
+      for (int b = 0; b < kStairMaxW; ++b)
+        if (b < W) pf[(size_t)b * stride + ext + q] = run[b];
+      const int e = order[base + q];
+      const int bq = bidx[e];
+      const uint32_t v = r1[e];
+#pragma unroll
+      for (int b = 0; b < kStairMaxW; ++b) run[b] = (b == bq) ? min(run[b], v) : run[b];
+    }
+    if (q1 == Mk && q0 < q1) {
+#pragma unroll
+      for (int b = 0; b < kStairMaxW; ++b)
+        if (b < W) pf[(size_t)b * stride + ext + Mk] = run[b];
+    }
+#pragma unroll
+    for (int b = 0; b < kStairMaxW; ++b) run[b] = b < W ? B[b * T + t] : kInf32;
+    for (int q = q1 - 1; q >= q0; --q) {  // sf[b][ext + q] = min r2 over positions >= q
+      const int e = order[base + q];
+      const int bq = bidx[e];
+      const uint32_t v = r2[e];
+#pragma unroll
+      for (int b = 0; b < kStairMaxW; ++b) {
+        run[b] = (b == bq) ? min(run[b], v) : run[b];
+        if (b < W) sf[(size_t)b * stride + ext + q] = run[b];
+      }
+    }
+    if (t == 0) {
+      for (int b = 0; b < W; ++b) sf[(size_t)b * stride + ext + Mk] = kInf32;
+    }
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
     s_carry_b = INT32_MIN;
     s_carry_rows = 0;
@@ -524,10 +680,14 @@ int plan_scratch_alloc(sp_table* t) {
   size_t ext = (size_t)(M + K);
   SP_CUDA(cudaMalloc(&t->r1, sizeof(uint32_t) * M));
   SP_CUDA(cudaMalloc(&t->r2, sizeof(uint32_t) * M));
-  SP_CUDA(cudaMalloc(&t->lpos, sizeof(uint32_t) * M));
   SP_CUDA(cudaMalloc(&t->ent_r1, sizeof(int32_t) * M));
   SP_CUDA(cudaMalloc(&t->ent_r2, sizeof(int32_t) * M));
   SP_CUDA(cudaMalloc(&t->order, sizeof(int32_t) * M));
+  {  // sort scratch: two tile buffers + two merged buffers of SItem
+    const size_t n = (size_t)((M + kSortTile - 1) / kSortTile) * kSortTile;
+    t->sort_tmp_bytes = 4 * n * sizeof(SItem);
+    SP_CUDA(cudaMalloc(&t->sort_tmp, t->sort_tmp_bytes));
+  }
   if (t->plan_ok) {
     SP_CUDA(cudaMalloc(&t->pf, sizeof(uint32_t) * W * ext));
     SP_CUDA(cudaMalloc(&t->sf, sizeof(uint32_t) * W * ext));
@@ -571,19 +731,39 @@ int plan_build(sp_ctx* ctx, sp_table* t, Plan& p) {
     ki.base[k] = k < K ? t->kind_base[k] : 0;
     ki.count[k] = k < K ? t->kind_count[k] : 0;
   }
-  SP_CUDA(cudaMemsetAsync(t->r1, 0, sizeof(uint32_t) * M, st));
-  SP_CUDA(cudaMemsetAsync(t->r2, 0, sizeof(uint32_t) * M, st));
-  SP_CUDA(cudaMemsetAsync(t->lpos, 0, sizeof(uint32_t) * M, st));
   SP_CUDA(cudaMemsetAsync(t->candf, 0, sizeof(uint32_t) * M, st));
   SP_CUDA(cudaMemsetAsync(t->cands, 0, sizeof(uint32_t) * M, st));
-  dim3 grid((M + 255) / 256, (M + kRankChunk - 1) / kRankChunk);
-  k_rank<<<grid, 256, 0, st>>>(M, t->lat, p.cost, p.costpen, t->res, t->id_rank, t->kind,
-                               t->r1, t->r2, t->lpos);
+  const int nb = (M + 255) / 256;
+  const int ntiles = (M + kSortTile - 1) / kSortTile;
+  const int nmerge = (2 * ntiles * kSortTile + 255) / 256;
+  SItem* tA = reinterpret_cast<SItem*>(t->sort_tmp);           // tiles of sort A
+  SItem* tB = tA + (size_t)ntiles * kSortTile;                  // tiles of sort B
+  SItem* oA = tB + (size_t)ntiles * kSortTile;                  // merged A
+  SItem* oB = oA + (size_t)ntiles * kSortTile;                  // merged B
+  // (cost, index) and (kind, lat, index) tile sorts + merges
+  k_tile_sort<kSortR1, kSortOrder><<<2 * ntiles, kSortThreads, 0, st>>>(
+      M, ntiles, p.cost, nullptr, tA, t->lat, t->kind, tB);
   SP_CHECK_LAUNCH(ctx);
-  k_invert<<<(M + 255) / 256, 256, 0, st>>>(M, t->r1, t->r2, t->lpos, t->kind, ki, t->ent_r1,
-                                            t->ent_r2, t->order);
+  k_merge_rank<kSortR1, kSortOrder><<<nmerge, 256, 0, st>>>(M, ntiles, tA, oA, tB, oB);
   SP_CHECK_LAUNCH(ctx);
-  k_stair<<<K, 1024, 0, st>>>(M, K, W, ki, t->order, t->bidx, t->lat, t->r1, t->r2, t->pf,
+  k_rank_r1<<<nb, 256, 0, st>>>(M, oA, t->res, t->id_rank, t->r1, t->ent_r1);
+  SP_CHECK_LAUNCH(ctx);
+  // (costpen, r1): items at r1 positions
+  k_tile_sort<kSortR2, kSortR2><<<ntiles, kSortThreads, 0, st>>>(M, ntiles, p.costpen, t->ent_r1,
+                                                                 tA, nullptr, nullptr, nullptr);
+  SP_CHECK_LAUNCH(ctx);
+  k_merge_rank<kSortR2, kSortR2><<<(ntiles * kSortTile + 255) / 256, 256, 0, st>>>(
+      M, ntiles, tA, oA, nullptr, nullptr);
+  SP_CHECK_LAUNCH(ctx);
+  k_orders_out<<<nb, 256, 0, st>>>(M, oA, t->ent_r1, t->ent_r2, t->r2, oB, t->order);
+  SP_CHECK_LAUNCH(ctx);
+  static bool stair_attr = false;
+  if (!stair_attr) {
+    SP_CUDA(cudaFuncSetAttribute(k_stair, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 2 * kStairMaxW * 1024 * (int)sizeof(uint32_t)));
+    stair_attr = true;
+  }
+  k_stair<<<K, 1024, 2 * W * 1024 * sizeof(uint32_t), st>>>(M, K, W, ki, t->order, t->bidx, t->lat, t->r1, t->r2, t->pf,
                               t->sf, t->thrscratch, t->rowscratch, t->rows_per_kind, t->candf,
                               t->cands);
   SP_CHECK_LAUNCH(ctx);
