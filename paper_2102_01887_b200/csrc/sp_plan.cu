@@ -24,6 +24,7 @@
 // See DESIGN.md §K2 for the proof of bit-exactness.
 #include <float.h>
 #include <math.h>
+#include <stdlib.h>
 
 #include <algorithm>
 #include <cstring>
@@ -451,6 +452,213 @@ __global__ void __launch_bounds__(1024) k_stair(int M, int K, int W, KindInfo ki
   if (threadIdx.x == 0) rows_per_kind[k] = s_carry_rows;
 }
 
+// Shared-memory variant of k_stair for kinds of at most kStairSmemMax entries (same output).
+// The kind's positions are staged once — lane, r1, r2 and the latency-boundary flag, all loads
+// in flight together — so the sequential scans run on shared memory instead of chains of
+// dependent global loads:
+//   phase A  warp w < 2W: lane b = w % W, direction w / W; each of its 32 threads owns a
+//            contiguous run of positions (local minimum, warp exclusive scan, rewrite with the
+//            carry), writing pf / sf for every position;
+//   phase B  every thread owns a contiguous run of positions p in [0, Mk]: previous boundary
+//            (block max-scan carry), "row changed" test against it, row numbers (block sum-scan
+//            carry), row / threshold / candidate-flag writes.
+constexpr int kStairSmemMax = 16384;
+// Per-position arrays are laid out in 32 runs of S positions (S a power of two >= 128, one run
+// per thread of a scanning warp) with one pad word after every run, so the 32 threads of a
+// warp — each walking its own run — hit 32 different banks for 32-, 16- and 8-bit arrays.
+__device__ __forceinline__ int i32(int q, int sh) { return q + (q >> sh); }
+__device__ __forceinline__ int i16(int q, int sh) { return q + ((q >> sh) << 1); }
+__device__ __forceinline__ int i8(int q, int sh) { return q + ((q >> sh) << 2); }
+constexpr int kStairCap = kStairSmemMax + 160;  // positions 0..Mk plus the run pads
+constexpr int kStairSmemBytes = 2 * kStairCap * 4 + kStairCap * 2 + 3 * kStairCap;
+// Consecutive latency boundaries pp < p carry different rows iff some position of the group
+// [pp, p) strictly improves its lane's running prefix minimum of r1 (scanning forward) or its
+// running suffix minimum of r2 (scanning backward).  So: scan once to flag those positions,
+// number the changed boundaries (= rows) with block scans, then scan again and write each
+// lane's running minimum only where a row starts — no per-position pf / sf arrays.
+__global__ void __launch_bounds__(1024) k_stair_smem(int M, int K, int W, KindInfo ki,
+                                                     const int32_t* __restrict__ order,
+                                                     const int32_t* __restrict__ bidx,
+                                                     const double* __restrict__ lat,
+                                                     const uint32_t* __restrict__ r1,
+                                                     const uint32_t* __restrict__ r2,
+                                                     double* thrscratch, uint32_t* rowscratch,
+                                                     int32_t* rows_per_kind, uint32_t* candf,
+                                                     uint32_t* cands) {
+  extern __shared__ __align__(16) uint8_t s_st[];
+  __shared__ int s_warp[32];
+  const int k = blockIdx.x;
+  const int Mk = ki.count[k];
+  const int base = ki.base[k];
+  const int ext = base + k;
+  if (Mk == 0) {
+    if (threadIdx.x == 0) rows_per_kind[k] = 0;
+    return;
+  }
+  const int T = blockDim.x, t = threadIdx.x;
+  int sh = 7;  // runs of S = 2^sh >= 128 positions, 32 runs cover Mk
+  while ((32 << sh) < Mk + 1) ++sh;
+  // rank | lane << 16 (ranks < 2^15 for plan tables)
+  uint32_t* sr1 = reinterpret_cast<uint32_t*>(s_st);
+  uint32_t* sr2 = sr1 + kStairCap;
+  uint16_t* scnt = reinterpret_cast<uint16_t*>(sr2 + kStairCap);  // #flags before p
+  uint16_t* srow = scnt;  // then: row starting at boundary p, or 0xFFFF
+  uint8_t* sisb = reinterpret_cast<uint8_t*>(scnt + kStairCap);  // lat[q] != lat[q - 1]
+  uint8_t* simpP = sisb + kStairCap;   // q improves its lane's prefix min of r1
+  uint8_t* simpS = simpP + kStairCap;  // q improves its lane's suffix min of r2
+  // ---- stage (several independent loads per thread in flight) ----
+  for (int q0 = t; q0 < Mk; q0 += 4 * T) {
+    int e[4], e1[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int q = q0 + u * T;
+      e[u] = q < Mk ? order[base + q] : 0;
+      e1[u] = (q < Mk && q > 0) ? order[base + q - 1] : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int q = q0 + u * T;
+      if (q < Mk) {
+        const uint32_t ln = (uint32_t)bidx[e[u]] << 16;
+        sr1[i32(q, sh)] = r1[e[u]] | ln;
+        sr2[i32(q, sh)] = r2[e[u]] | ln;
+        sisb[i8(q, sh)] = q > 0 && lat[e[u]] != lat[e1[u]];
+      }
+    }
+  }
+  __syncthreads();
+  const int w = t >> 5, l = t & 31;
+  const int a0 = min(l << sh, Mk), a1 = min(a0 + (1 << sh), Mk);
+  // inside a run, position q sits at q + l (32-bit), q + 2l (16-bit), q + 4l (8-bit)
+  // lane carries of warp w < 2W (lane b = w % W, forward for w < W, backward otherwise)
+  uint32_t carry = kInf32;
+  // ---- phase A: flag improving positions ----
+  if (w < 2 * W) {
+    const uint32_t b = (uint32_t)(w % W);
+    const bool suf = w >= W;
+    const uint32_t* v = suf ? sr2 : sr1;
+    uint32_t m = kInf32;
+    for (int q = a0; q < a1; ++q) {
+      const uint32_t x = v[q + l];
+      m = ((x >> 16) == b) ? min(m, x & 0xFFFFu) : m;
+    }
+    if (!suf) {
+      const uint32_t incl = warp_incl_min(m, l);
+      carry = __shfl_up_sync(0xffffffffu, incl, 1);
+      if (l == 0) carry = kInf32;
+      uint32_t run = carry;
+      for (int q = a0; q < a1; ++q) {
+        const uint32_t x = v[q + l];
+        if ((x >> 16) == b) {
+          const uint32_t r = x & 0xFFFFu;
+          simpP[q + 4 * l] = r < run;
+          run = min(run, r);
+        }
+      }
+    } else {
+      uint32_t x = m;  // exclusive over the lanes after l
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t y = __shfl_down_sync(0xffffffffu, x, off);
+        if (l + off < 32) x = min(x, y);
+      }
+      carry = __shfl_down_sync(0xffffffffu, x, 1);
+      if (l == 31) carry = kInf32;
+      uint32_t run = carry;
+      for (int q = a1 - 1; q >= a0; --q) {
+        const uint32_t y = v[q + l];
+        if ((y >> 16) == b) {
+          const uint32_t r = y & 0xFFFFu;
+          simpS[q + 4 * l] = r < run;
+          run = min(run, r);
+        }
+      }
+    }
+  }
+  __syncthreads();
+  // ---- phase B: boundaries p in [0, Mk] (each thread a contiguous run) -> rows ----
+  const int n = Mk + 1;
+  const int P = (n + T - 1) / T;
+  const int p0 = min(t * P, n), p1 = min(p0 + P, n);
+  int lastb = INT32_MIN, nf = 0;
+  for (int p = p0; p < p1; ++p) {
+    if (p == 0 || p == Mk || sisb[i8(p, sh)]) lastb = p;
+    if (p < Mk) nf += (simpP[i8(p, sh)] | simpS[i8(p, sh)]) != 0;
+  }
+  int tot_f = 0;
+  int cf = block_excl_sum(nf, s_warp, &tot_f);
+  const int prevb = block_excl_max(lastb, s_warp);  // last boundary before this run
+  for (int p = p0; p < p1; ++p) {
+    scnt[i16(p, sh)] = (uint16_t)cf;
+    if (p < Mk) cf += (simpP[i8(p, sh)] | simpS[i8(p, sh)]) != 0;
+  }
+  __syncthreads();
+  uint32_t chmask = 0;  // changed boundaries of this run (P <= 17 for Mk <= 16384)
+  int cnt = 0;
+  {
+    int pp = prevb;
+    for (int p = p0; p < p1; ++p) {
+      if (!(p == 0 || p == Mk || sisb[i8(p, sh)])) continue;
+      if ((p == 0) || scnt[i16(p, sh)] > scnt[i16(pp, sh)]) {
+        chmask |= 1u << (p - p0);
+        ++cnt;
+      }
+      pp = p;
+    }
+  }
+  int total = 0;
+  int row = block_excl_sum(cnt, s_warp, &total);
+  for (int p = p0; p < p1; ++p) {
+    const bool ch = (chmask >> (p - p0)) & 1u;
+    srow[i16(p, sh)] = ch ? (uint16_t)row : (uint16_t)0xFFFFu;
+    if (ch) {
+      thrscratch[ext + row] = (p == 0) ? -INFINITY : lat[order[base + p - 1]];
+      ++row;
+    }
+  }
+  __syncthreads();
+  // ---- phase A again: each lane's running minimum where a row starts ----
+  if (w < 2 * W) {
+    const uint32_t b = (uint32_t)(w % W);
+    const bool suf = w >= W;
+    const uint32_t* v = suf ? sr2 : sr1;
+    uint32_t run = carry;
+    if (!suf) {
+      for (int q = a0; q < a1; ++q) {  // row at boundary q: min r1 over positions < q
+        const uint32_t rw = srow[q + 2 * l];
+        if (rw != 0xFFFFu) {
+          rowscratch[(size_t)(ext + rw) * (2 * W) + b] = run;
+          if (run != kInf32) candf[run] = 1u;
+        }
+        const uint32_t x = v[q + l];
+        run = ((x >> 16) == b) ? min(run, x & 0xFFFFu) : run;
+      }
+      if (a1 == Mk && a0 < a1) {  // boundary Mk: the whole-kind minimum
+        const uint32_t rw = srow[i16(Mk, sh)];
+        if (rw != 0xFFFFu) {
+          rowscratch[(size_t)(ext + rw) * (2 * W) + b] = run;
+          if (run != kInf32) candf[run] = 1u;
+        }
+      }
+    } else {
+      for (int q = a1 - 1; q >= a0; --q) {  // row at boundary q: min r2 over positions >= q
+        const uint32_t y = v[q + l];
+        run = ((y >> 16) == b) ? min(run, y & 0xFFFFu) : run;
+        const uint32_t rw = srow[q + 2 * l];
+        if (rw != 0xFFFFu) {
+          rowscratch[(size_t)(ext + rw) * (2 * W) + W + b] = run;
+          if (run != kInf32) cands[run] = 1u;
+        }
+      }
+      if (l == 0) {
+        const uint32_t rw = srow[i16(Mk, sh)];
+        if (rw != 0xFFFFu) rowscratch[(size_t)(ext + rw) * (2 * W) + W + b] = kInf32;
+      }
+    }
+  }
+  if (t == 0) rows_per_kind[k] = total;
+}
+
 // (score, r1) strict order of unified candidates
 __device__ __forceinline__ bool key_lt(double sa, uint32_t ra, double sb, uint32_t rb) {
   return sa < sb || (sa == sb && ra < rb);
@@ -761,8 +969,17 @@ int plan_build(sp_ctx* ctx, sp_table* t, Plan& p) {
   if (!stair_attr) {
     SP_CUDA(cudaFuncSetAttribute(k_stair, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  2 * kStairMaxW * 1024 * (int)sizeof(uint32_t)));
+    SP_CUDA(cudaFuncSetAttribute(k_stair_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kStairSmemBytes));
     stair_attr = true;
   }
+  int max_mk = 0;
+  for (int k = 0; k < K; ++k) max_mk = std::max(max_mk, t->kind_count[k]);
+  if (max_mk <= kStairSmemMax && !getenv("SP_STAIR_GLOBAL"))
+    k_stair_smem<<<K, 1024, kStairSmemBytes, st>>>(M, K, W, ki, t->order, t->bidx, t->lat, t->r1,
+                                                   t->r2, t->thrscratch, t->rowscratch,
+                                                   t->rows_per_kind, t->candf, t->cands);
+  else
   k_stair<<<K, 1024, 2 * W * 1024 * sizeof(uint32_t), st>>>(M, K, W, ki, t->order, t->bidx, t->lat, t->r1, t->r2, t->pf,
                               t->sf, t->thrscratch, t->rowscratch, t->rows_per_kind, t->candf,
                               t->cands);
