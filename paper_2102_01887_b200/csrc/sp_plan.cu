@@ -680,57 +680,102 @@ __global__ void __launch_bounds__(1024) k_finalize(
   __shared__ PlanHdr hdr;
   __shared__ int s_ncp, s_ncs;
   // 1. order-preserving compaction of the two candidate sets
-  for (int pass = 0; pass < 2; ++pass) {
-    const uint32_t* fl = pass ? cands : candf;
-    uint32_t* cid = pass ? cids : cidf;
-    int carry = 0;
-    for (int c0 = 0; c0 < M; c0 += blockDim.x) {
-      int r = c0 + threadIdx.x;
-      int v = (r < M) ? (int)fl[r] : 0;
-      int total = 0;
-      int ex = block_excl_sum(v, s_warp, &total);
-      if (r < M) cid[r] = (uint32_t)(carry + ex);
-      carry += total;
+  //    (each thread a contiguous run of flags, all loads in flight, one block scan per set)
+  {
+    const int T = blockDim.x;
+    const int P = (M + T - 1) / T;
+    const int r0 = min((int)threadIdx.x * P, M), r1e = min(r0 + P, M);
+    int nf = 0, ns = 0;
+    for (int r = r0; r < r1e; ++r) {
+      nf += candf[r] != 0;
+      ns += cands[r] != 0;
+    }
+    int tf = 0, ts = 0;
+    int cf = block_excl_sum(nf, s_warp, &tf);
+    int cs = block_excl_sum(ns, s_warp, &ts);
+    for (int r = r0; r < r1e; ++r) {
+      cidf[r] = (uint32_t)cf;
+      cids[r] = (uint32_t)cs;
+      cf += candf[r] != 0;
+      cs += cands[r] != 0;
     }
     if (threadIdx.x == 0) {
-      if (pass) s_ncs = carry; else s_ncp = carry;
+      s_ncp = tf;
+      s_ncs = ts;
     }
     __syncthreads();
   }
   const int ncp = s_ncp, ncs = s_ncs;
   // 2. candidate keys: CP[c] (feasible side) sorted by r1, CS[c] (penalized) sorted by r2;
   //    both lists are ascending in their (score, r1) key.
-  for (int r = threadIdx.x; r < M; r += blockDim.x) {
-    if (candf[r]) {
-      const int c = (int)cidf[r], e = ent_r1[r];
-      ukey[c] = cost[e];
-      ukr[c] = (uint32_t)r;
-      uent[c] = e;
+  //    (four rows per thread per step so the dependent loads of different rows overlap)
+  for (int r0 = threadIdx.x; r0 < M; r0 += 4 * blockDim.x) {
+    uint32_t fa[4], fs[4];
+    int ea[4], es[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int r = r0 + u * blockDim.x;
+      fa[u] = r < M ? candf[r] : 0u;
+      fs[u] = r < M ? cands[r] : 0u;
+      ea[u] = (r < M && fa[u]) ? ent_r1[r] : 0;
+      es[u] = (r < M && fs[u]) ? ent_r2[r] : 0;
     }
-    if (cands[r]) {
-      const int c = ncp + (int)cids[r], e = ent_r2[r];
-      ukey[c] = costpen[e];
-      ukr[c] = r1[e];
-      uent[c] = e;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int r = r0 + u * blockDim.x;
+      if (fa[u]) {
+        const int c = (int)cidf[r];
+        ukey[c] = cost[ea[u]];
+        ukr[c] = (uint32_t)r;
+        uent[c] = ea[u];
+      }
+      if (fs[u]) {
+        const int c = ncp + (int)cids[r];
+        ukey[c] = costpen[es[u]];
+        ukr[c] = r1[es[u]];
+        uent[c] = es[u];
+      }
     }
   }
   __syncthreads();
   // 3. merge ranks: uid = own position + #keys of the other list before it (ties, which
-  //    only occur for the two sides of one entry when the penalty is 0, put CP first)
-  for (int c = threadIdx.x; c < ncp + ncs; c += blockDim.x) {
-    const bool is_cp = c < ncp;
-    const double s = ukey[c];
-    const uint32_t rr = ukr[c];
-    int lo = is_cp ? ncp : 0, hi = is_cp ? ncp + ncs : ncp;
-    const int base = lo;
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      const bool before = is_cp ? key_lt(ukey[mid], ukr[mid], s, rr)
-                                : !key_lt(s, rr, ukey[mid], ukr[mid]);
-      if (before) lo = mid + 1; else hi = mid;
+  //    only occur for the two sides of one entry when the penalty is 0, put CP first);
+  //    four binary searches per thread advance in lockstep
+  for (int c0 = threadIdx.x; c0 < ncp + ncs; c0 += 4 * blockDim.x) {
+    int lo[4], hi[4], bse[4];
+    double sk[4];
+    uint32_t rk[4];
+    bool cp[4], ok[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int c = c0 + u * blockDim.x;
+      ok[u] = c < ncp + ncs;
+      cp[u] = c < ncp;
+      sk[u] = ok[u] ? ukey[c] : 0.0;
+      rk[u] = ok[u] ? ukr[c] : 0u;
+      lo[u] = cp[u] ? ncp : 0;
+      hi[u] = ok[u] ? (cp[u] ? ncp + ncs : ncp) : 0;
+      bse[u] = lo[u];
     }
-    const int own = is_cp ? c : c - ncp;
-    umap[c] = (uint32_t)(own + (lo - base));
+    for (;;) {
+      bool any = false;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (lo[u] < hi[u]) {
+          any = true;
+          const int mid = (lo[u] + hi[u]) >> 1;
+          const bool before = cp[u] ? key_lt(ukey[mid], ukr[mid], sk[u], rk[u])
+                                    : !key_lt(sk[u], rk[u], ukey[mid], ukr[mid]);
+          if (before) lo[u] = mid + 1; else hi[u] = mid;
+        }
+      }
+      if (!any) break;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int c = c0 + u * blockDim.x;
+      if (ok[u]) umap[c] = (uint32_t)((cp[u] ? c : c - ncp) + (lo[u] - bse[u]));
+    }
   }
   if (threadIdx.x == 0) {
     hdr = hdr_in;
