@@ -308,22 +308,33 @@ def run_c5(args):
             ("obj", torch.float64), ("slack", torch.float64), ("wait", torch.float64))}
     obs_idx = torch.empty(Bl, dtype=torch.int32, device=dev)
     alpha = 100.0
+
+    def online_batch(tab, bt):
+        # decide this rank's shard of batch bt against the batch-start table; the chosen
+        # configurations run: observation = truth(config) * lognormal noise (delayed / None
+        # decisions produce no observation, idx = -1); every rank folds the whole batch
+        s = slice(bt * B + a, bt * B + b)
+        tab.select_batch(d["slack"][s], alpha, d["avail"][s], upstream_supply=d["supply"][s],
+                         min_batch=d["mb"][s], flags=d["flags"][s], out=out)
+        torch.where((out["code"] & 3) == 1, out["idx"], torch.full_like(out["idx"], -1), out=obs_idx)
+        obs = lat_init[obs_idx.clamp(min=0).long()] * noise[s]
+        f_idx, f_obs = gather_observations(obs_idx, obs, B) if world > 1 else (obs_idx, obs)
+        sp.fold_observations([tab], None, f_idx, f_obs, beta=0.5, dfp_count=10, sync_host=False)
+
+    # warm-up on a throw-away copy of the table (module loading, scratch allocation, plan-build
+    # graph capture); the timed run starts from the untouched table
+    wtab = sp.OpTable(spec, synth.synth_scenario())
+    for bt in range(max(3, args.warmup)):
+        online_batch(wtab, bt)
     table.prepare(alpha)
     torch.cuda.synchronize(dev)
+    del wtab
     _barrier(torch)
     l0 = ctx.launch_count
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for bt in range(NB):
-        s = slice(bt * B + a, bt * B + b)
-        table.select_batch(d["slack"][s], alpha, d["avail"][s], upstream_supply=d["supply"][s],
-                           min_batch=d["mb"][s], flags=d["flags"][s], out=out)
-        # the chosen configurations run: observation = truth(config) * lognormal noise;
-        # delayed / None decisions produce no observation (idx = -1)
-        torch.where((out["code"] & 3) == 1, out["idx"], torch.full_like(out["idx"], -1), out=obs_idx)
-        obs = lat_init[obs_idx.clamp(min=0).long()] * noise[s]
-        f_idx, f_obs = gather_observations(obs_idx, obs, B) if world > 1 else (obs_idx, obs)
-        sp.fold_observations([table], None, f_idx, f_obs, beta=0.5, dfp_count=10, sync_host=False)
+        online_batch(table, bt)
     e1.record(stream)
     torch.cuda.synchronize(dev)
     t = _tmax(torch, e0.elapsed_time(e1) / 1e3, dev)

@@ -164,6 +164,11 @@ int sp_ctx_create(int device, sp_ctx** out) {
 }
 
 int sp_ctx_destroy(sp_ctx* ctx) {
+  if (ctx && ctx->capture) {
+    cudaStreamSynchronize(ctx->stream);
+    cudaStreamDestroy(ctx->capture);
+    ctx->capture = nullptr;
+  }
   if (!ctx) return SP_OK;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);

@@ -105,6 +105,11 @@ struct Plan {
   cudaEvent_t hdr_ready = nullptr;
   bool hdr_pending = false;
   bool hdr_valid = false;
+  // rebuilds after the first are replayed from a CUDA graph of the whole build (one launch
+  // instead of ~12 kernel launches + 3 memory operations)
+  int builds = 0;
+  cudaGraphExec_t graph = nullptr;
+  int64_t graph_kernels = 0;
 };
 
 }  // namespace sp
@@ -132,6 +137,7 @@ struct sp_ctx {
   cudaStream_t h2d = nullptr, d2h = nullptr;
   static constexpr int kPipeChunks = 8;
   cudaEvent_t ev_in[kPipeChunks] = {}, ev_comp[kPipeChunks] = {}, ev_out[kPipeChunks] = {};
+  cudaStream_t capture = nullptr;  // private stream for CUDA-graph captures
 };
 
 struct sp_table {
@@ -201,11 +207,14 @@ int cuda_fail(cudaError_t e, const char* what);
     if (_e != cudaSuccess) return sp::cuda_fail(_e, #call);        \
   } while (0)
 
-#define SP_CHECK_LAUNCH(ctx)                                        \
-  do {                                                              \
-    (ctx)->launches++;                                              \
-    cudaError_t _e = cudaGetLastError();                            \
-    if (_e != cudaSuccess) return sp::cuda_fail(_e, "kernel launch"); \
+#define SP_STR2(x) #x
+#define SP_STR(x) SP_STR2(x)
+#define SP_CHECK_LAUNCH(ctx)                                                              \
+  do {                                                                                    \
+    (ctx)->launches++;                                                                    \
+    cudaError_t _e = cudaGetLastError();                                                  \
+    if (_e != cudaSuccess)                                                                \
+      return sp::cuda_fail(_e, "kernel launch (" __FILE__ ":" SP_STR(__LINE__) ")");     \
   } while (0)
 
 // ---- internal entry points implemented in the .cu files --------------------------------

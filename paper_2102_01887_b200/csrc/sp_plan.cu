@@ -959,7 +959,7 @@ int plan_scratch_alloc(sp_table* t) {
   return SP_OK;
 }
 
-int plan_build(sp_ctx* ctx, sp_table* t, Plan& p) {
+static int plan_enqueue(sp_ctx* ctx, sp_table* t, Plan& p) {
   const int M = t->M, K = t->K;
   cudaStream_t st = ctx->stream;
   if (!p.cost) {
@@ -1051,12 +1051,58 @@ int plan_build(sp_ctx* ctx, sp_table* t, Plan& p) {
     SP_CUDA(cudaEventCreateWithFlags(&p.hdr_ready, cudaEventDisableTiming));
   }
   SP_CUDA(cudaMemcpyAsync(p.host_hdr, p.image, sizeof(PlanHdr), cudaMemcpyDeviceToHost, st));
-  SP_CUDA(cudaEventRecord(p.hdr_ready, st));
+  // (the header-ready event is recorded by plan_build, outside any graph capture)
   p.hdr_pending = true;
   p.hdr_valid = false;
   p.valid = true;
   p.version = t->version;
   return SP_OK;
+}
+
+int plan_build(sp_ctx* ctx, sp_table* t, Plan& p) {
+  if (p.graph && !getenv("SP_NO_PLAN_GRAPH")) {
+    SP_CUDA(cudaGraphLaunch(p.graph, ctx->stream));
+    if (t->plan_ok) SP_CUDA(cudaEventRecord(p.hdr_ready, ctx->stream));
+    ctx->launches += p.graph_kernels;
+    ctx->plan_dirty = true;
+    p.hdr_pending = t->plan_ok;
+    p.hdr_valid = false;
+    p.valid = true;
+    p.version = t->version;
+    return SP_OK;
+  }
+  if (p.builds == 0 || getenv("SP_NO_PLAN_GRAPH")) {  // first build: allocations happen here
+    ++p.builds;
+    const int rc = plan_enqueue(ctx, t, p);
+    if (rc == SP_OK && t->plan_ok) SP_CUDA(cudaEventRecord(p.hdr_ready, ctx->stream));
+    return rc;
+  }
+  // second build: capture the whole build once on a private stream, then replay it
+  if (!ctx->capture) SP_CUDA(cudaStreamCreateWithFlags(&ctx->capture, cudaStreamNonBlocking));
+  cudaStream_t user = ctx->stream;
+  const int64_t l0 = ctx->launches;
+  ctx->stream = ctx->capture;
+  cudaError_t e = cudaStreamBeginCapture(ctx->capture, cudaStreamCaptureModeThreadLocal);
+  int rc = e == cudaSuccess ? plan_enqueue(ctx, t, p) : cuda_fail(e, "cudaStreamBeginCapture");
+  cudaGraph_t g = nullptr;
+  cudaError_t e2 = cudaStreamEndCapture(ctx->capture, &g);
+  ctx->stream = user;
+  const int64_t nk = ctx->launches - l0;
+  ctx->launches = l0;
+  if (rc != SP_OK) {
+    if (g) cudaGraphDestroy(g);
+    return rc;
+  }
+  if (e2 != cudaSuccess) return cuda_fail(e2, "cudaStreamEndCapture");
+  e = cudaGraphInstantiate(&p.graph, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) {
+    p.graph = nullptr;
+    return cuda_fail(e, "cudaGraphInstantiate(plan)");
+  }
+  p.graph_kernels = nk;
+  ++p.builds;
+  return plan_build(ctx, t, p);  // replay
 }
 
 const PlanHdr* plan_host_header(Plan& p) {
@@ -1068,6 +1114,7 @@ const PlanHdr* plan_host_header(Plan& p) {
 }
 
 void plan_release(Plan& p) {
+  if (p.graph) cudaGraphExecDestroy(p.graph);
   cudaFree(p.cost);
   cudaFree(p.costpen);
   cudaFree(p.image);
