@@ -228,10 +228,15 @@ def run_c4(args):
         t.prepare(alpha)
     torch.cuda.synchronize(dev)
 
-    def step():
+    def step_two_kernels():  # K1 writes slack[I][V][K], K2 reads it back
         g.slack_batch(d["ref"], d["target"], d["now"], d["Q"], out={"slack": slack})
         sp.select_batch(tabs, slack.view(N, K), alpha, d["avail"], upstream_supply=d["supply"],
                         min_batch=d["mb"], flags=d["flags"], op=d["op"], out=out)
+
+    def step():  # K1 -> K2 fused: the slack never leaves registers
+        g.slack_select_batch(tabs, alpha, d["ref"], d["target"], d["now"], d["Q"], d["avail"],
+                             upstream_supply=d["supply"], min_batch=d["mb"], flags=d["flags"],
+                             out=out)
 
     flush = _flush_factory(torch, dev)
     for _ in range(args.warmup):
@@ -249,6 +254,18 @@ def run_c4(args):
     ms = [a.elapsed_time(b) for a, b in evs]
     t = _tmax(torch, sum(ms) / 1e3, dev)
     codes = torch.bincount(out["code"] & 3, minlength=3)
+    launches = ctx.launch_count - l0
+    # the unfused K1 + K2 pair on the same inputs, for comparison
+    for _ in range(2):
+        step_two_kernels()
+    ev2 = _events(torch, args.steps)
+    for i in range(args.steps):
+        flush()
+        ev2[i][0].record(stream)
+        step_two_kernels()
+        ev2[i][1].record(stream)
+    torch.cuda.synchronize(dev)
+    ms2 = [a.elapsed_time(b) for a, b in ev2]
     if world > 1:
         torch.distributed.all_reduce(codes)
     codes = codes.cpu().tolist()
@@ -256,7 +273,7 @@ def run_c4(args):
         return
     evals_per_inst = sum(len(x.entries) for x in tabs)
     line = {
-        "workload": "c4", "metric": "config decisions/s (K1 slack -> K2 select, on device)",
+        "workload": "c4", "metric": "config decisions/s (K1 slack -> K2 select fused on device)",
         "unit": "decisions/s", "value": args.steps * N * world / t, "ms_per_step": 1e3 * t / args.steps,
         "steps": args.steps, "n_gpus": world, "scaling": "weak",
         "evals_per_s": args.steps * I * world * evals_per_inst / t,
@@ -265,8 +282,11 @@ def run_c4(args):
                    "cp_min": cp_min,
                    "parallelism": f"replicas sharded over {world} GPU(s); decision counters all-reduced"},
         "decision_mix": {"none": codes[0], "assign": codes[1], "delay": codes[2]},
-        "gpu_launches": ctx.launch_count - l0,
+        "gpu_launches": launches,
         "step_ms": {"median": statistics.median(ms), "min": min(ms), "max": max(ms)},
+        "kernel": "k_slack_select (K1 -> K2 fused, sp_slack_select_batch)",
+        "two_kernel_step_ms": {"median": statistics.median(ms2), "min": min(ms2),
+                               "note": "k_slack then k_select_plan, slack through HBM"},
     }
     print(json.dumps(line), flush=True)
 

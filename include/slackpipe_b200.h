@@ -153,6 +153,22 @@ int sp_slack_batch(sp_ctx* ctx, sp_dag* g, int32_t I, const double* ref_lat,
                    int32_t ref_stride, const double* target, const double* now, int32_t K,
                    const double* Q, double* out_slack, double* out_ratio, int32_t mem);
 
+/* ---- K1 -> K2 fused: slack of every source operation straight into its decision ----- */
+/* For pipeline instance i and source s of g (tables[s] = that operation's table, n_tables =
+ * n_src): the slack of sp_slack_batch (slack_k = (b_k >= 0 ? own/Tmax : own/Tmin) * b_k,
+ * b_k = (target[i] - now[i]) - Q[i*K + k], configurator.py:526-543) is used as the
+ * slack_by_kind of invocation d = i*n_src + s, decided exactly as sp_select_batch does with
+ * avail[d], supply[d], min_batch[d], flags[d] (configurator.py:239-300).  Outputs per d as
+ * in sp_select_batch; out_kslack (optional, N*K) receives the slack values.  One kernel when
+ * every plan fits in shared memory with the vertex programs, else K1 then K2. */
+int sp_slack_select_batch(sp_ctx* ctx, sp_dag* g, int32_t n_tables, sp_table* const* tables,
+                          double alpha, int32_t I, const double* ref_lat, int32_t ref_stride,
+                          const double* target, const double* now, int32_t K, const double* Q,
+                          const int32_t* avail, const int32_t* supply, const int32_t* min_batch,
+                          const uint32_t* flags, int32_t* out_idx, int32_t* out_code,
+                          int32_t* out_fill, double* out_obj, double* out_slack,
+                          double* out_wait, double* out_kslack, int32_t mem);
+
 /* ---- Eq. 2: queueing_by_kind / estimate_queueing (configurator.py:109-119, 511-524) --- */
 /* Ordered sequential sum per kind: out[k] = (sum_{j in [ptr[k],ptr[k+1])} cnt[j]*(lat[j]*res[j]))
  * / pool[k] when cnt != NULL (queueing_by_kind order), else sum of lat[j]*res[j]/pool[k]

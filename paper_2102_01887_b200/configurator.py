@@ -468,6 +468,15 @@ class _RawTable:
                                       ptr(score), ptr(cost)), "sp_scores")
         return score, cost
 
+    def set_latency(self, index, latency_s) -> None:
+        """Batched configurator.py:211-213: lat[index[j]] = latency_s[j] (host mirror + device)."""
+        i = np.ascontiguousarray(np.atleast_1d(index), dtype=np.int32)
+        v = np.ascontiguousarray(np.atleast_1d(latency_s), dtype=np.float64)
+        if i.shape != v.shape:
+            raise ValueError("set_latency: index and latency_s differ in length")
+        self.lat[i] = v
+        check(self._ctx.lib.sp_table_set_latency(self._ctx.handle, self._handle, len(i), ptr(i), ptr(v)))
+
     def get_latency(self) -> np.ndarray:
         out = np.empty(self.M, np.float64)
         check(self._ctx.lib.sp_table_get_latency(self._ctx.handle, self._handle, ptr(out)))

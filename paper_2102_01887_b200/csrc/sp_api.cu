@@ -938,3 +938,83 @@ extern "C" int sp_commit_round(sp_ctx* ctx, int32_t R, int32_t n_ops, sp_table* 
   SP_CUDA(cudaStreamSynchronize(st));
   return SP_OK;
 }
+
+// ---- K1 -> K2 fused (sp_k12.cuh) ------------------------------------------------------------
+extern "C" int sp_slack_select_batch(sp_ctx* ctx, sp_dag* g, int32_t n_tables,
+                                     sp_table* const* tables, double alpha, int32_t I,
+                                     const double* ref_lat, int32_t ref_stride,
+                                     const double* target, const double* now, int32_t K,
+                                     const double* Q, const int32_t* avail,
+                                     const int32_t* supply, const int32_t* min_batch,
+                                     const uint32_t* flags, int32_t* out_idx, int32_t* out_code,
+                                     int32_t* out_fill, double* out_obj, double* out_slack,
+                                     double* out_wait, double* out_kslack, int32_t mem) {
+  if (!ctx || !g || !tables || I < 0 || K < 1 || K > SP_MAX_KINDS)
+    return fail(SP_E_INVALID, "slack_select: bad argument");
+  for (int t = 0; t < n_tables; ++t)
+    if (!tables[t]) return fail(SP_E_INVALID, "slack_select: null table");
+  if (!(alpha >= 0.0)) return fail(SP_E_INVALID, "alpha must be >= 0");  // configurator.py:37
+  if (ref_stride != 0 && ref_stride < g->n_val)
+    return fail(SP_E_INVALID, "slack_select: ref_stride smaller than the value count");
+  if (I > 0 && (!ref_lat || !target || !now || !Q || !avail || !supply || !min_batch || !flags ||
+                !out_idx || !out_code))
+    return fail(SP_E_INVALID, "slack_select: required array is null");
+  if (mem == SP_MEM_DEVICE)
+    return slack_select_launch(ctx, g, n_tables, tables, alpha, I, ref_lat, ref_stride, target,
+                               now, K, Q, avail, supply, min_batch, flags, out_idx, out_code,
+                               out_fill, out_obj, out_slack, out_wait, out_kslack);
+  if (mem != SP_MEM_HOST) return fail(SP_E_INVALID, "slack_select: bad mem flag");
+  if (I == 0) return SP_OK;
+  const size_t N = (size_t)I * n_tables;
+  const size_t nref = ref_stride ? (size_t)I * ref_stride : (size_t)g->n_val;
+  const size_t need = rsz<double>(nref) + 2 * rsz<double>(I) + rsz<double>((size_t)I * K) +
+                      4 * rsz<int32_t>(N) + 3 * rsz<int32_t>(N) + 3 * rsz<double>(N) +
+                      (out_kslack ? rsz<double>(N * K) : 0);
+  int rc = SP_OK;
+  void* io = ctx_io(ctx, need, &rc);
+  if (!io) return rc;
+  Bump b{(uint8_t*)io};
+  cudaStream_t st = ctx->stream;
+  double* d_ref = b.take<double>(nref);
+  double* d_t = b.take<double>(I);
+  double* d_n = b.take<double>(I);
+  double* d_q = b.take<double>((size_t)I * K);
+  int32_t* d_av = b.take<int32_t>(N);
+  int32_t* d_sup = b.take<int32_t>(N);
+  int32_t* d_mb = b.take<int32_t>(N);
+  uint32_t* d_fl = b.take<uint32_t>(N);
+  int32_t* o_idx = b.take<int32_t>(N);
+  int32_t* o_code = b.take<int32_t>(N);
+  int32_t* o_fill = b.take<int32_t>(N);
+  double* o_obj = b.take<double>(N);
+  double* o_sl = b.take<double>(N);
+  double* o_wait = b.take<double>(N);
+  double* o_ks = out_kslack ? b.take<double>(N * K) : nullptr;
+  auto up = [&](void* dst, const void* src, size_t bytes) {
+    return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st);
+  };
+  SP_CUDA(up(d_ref, ref_lat, sizeof(double) * nref));
+  SP_CUDA(up(d_t, target, sizeof(double) * I));
+  SP_CUDA(up(d_n, now, sizeof(double) * I));
+  SP_CUDA(up(d_q, Q, sizeof(double) * I * K));
+  SP_CUDA(up(d_av, avail, 4 * N));
+  SP_CUDA(up(d_sup, supply, 4 * N));
+  SP_CUDA(up(d_mb, min_batch, 4 * N));
+  SP_CUDA(up(d_fl, flags, 4 * N));
+  rc = slack_select_launch(ctx, g, n_tables, tables, alpha, I, d_ref, ref_stride, d_t, d_n, K,
+                           d_q, d_av, d_sup, d_mb, d_fl, o_idx, o_code, o_fill, o_obj, o_sl,
+                           o_wait, o_ks);
+  if (rc != SP_OK) return rc;
+  auto down = [&](void* dst, const void* src, size_t bytes) {
+    return dst ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st) : cudaSuccess;
+  };
+  SP_CUDA(down(out_idx, o_idx, 4 * N));
+  SP_CUDA(down(out_code, o_code, 4 * N));
+  SP_CUDA(down(out_fill, o_fill, 4 * N));
+  SP_CUDA(down(out_obj, o_obj, 8 * N));
+  SP_CUDA(down(out_slack, o_sl, 8 * N));
+  SP_CUDA(down(out_wait, o_wait, 8 * N));
+  if (out_kslack) SP_CUDA(down(out_kslack, o_ks, 8 * N * K));
+  SP_CUDA(cudaStreamSynchronize(st));
+  return SP_OK;
+}

@@ -231,6 +231,13 @@ int select_launch(sp_ctx* ctx, int n_tables, sp_table* const* tables, double alp
                   double* out_slack, double* out_wait, double* out_kind_min, int mode);
 int affinity_launch(sp_ctx* ctx, int N, int K, const double* kmin, const int32_t* q,
                     double* out);
+int slack_select_launch(sp_ctx* ctx, sp_dag* g, int n_tables, sp_table* const* tables,
+                        double alpha, int I, const double* ref, int ref_stride,
+                        const double* target, const double* now, int K, const double* Q,
+                        const int32_t* avail, const int32_t* supply, const int32_t* min_batch,
+                        const uint32_t* flags, int32_t* out_idx, int32_t* out_code,
+                        int32_t* out_fill, double* out_obj, double* out_slack, double* out_wait,
+                        double* out_kslack);
 int commit_launch(sp_ctx* ctx, int R, int n_ops, sp_table* const* tables, double alpha,
                   const double* slack, const int32_t* fill, const int32_t* buffered,
                   const long long* head_id, const int32_t* depth, const uint32_t* hflags,

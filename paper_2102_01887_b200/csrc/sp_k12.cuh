@@ -1,0 +1,140 @@
+// sp_k12.cuh — K1 -> K2 fused: Alg. 1 slack straight into the staircase decision
+// (included by sp_select.cu after sp_k2b.cuh).
+//
+// The snapshot workloads (BASELINE config 4: target sweep x replicas) decide one invocation of
+// every operation per pipeline instance right after computing that instance's slack.  Run as
+// two kernels, K1 writes slack[I][n_src][K] to HBM and K2 reads it back (2 x 8*n_src*K bytes
+// per instance, 448 B for AMBER).  Here one thread owns one instance end to end: for every
+// source operation s it runs the forward DP of K1 (sp_slack.cu; same program, same shared-
+// memory DP slots, same bit-exact arithmetic), forms slack_k = (b_k >= 0 ? own/Tmax :
+// own/Tmin) * b_k with b_k = (target - now) - Q_k (configurator.py:526-543), and decides
+// invocation (i, s) against operation s's staircase plan (configurator.py:239-300) — the
+// slack never leaves registers.  Persistent grid; every CTA stages all vertex programs and all
+// plans once.
+
+constexpr int kK12Warps = 8;
+constexpr int kK12MaxSrc = kMaxPlanTables;
+
+struct K12Dag {
+  const int4* prog;
+  const int32_t* prog_ptr;   // n_src + 1
+  const uint32_t* preds;
+  const int32_t* pred_ptr;   // n_src + 1
+  int n_src, nslots, prog_len, pred_len;
+};
+
+struct K12In {
+  const double* ref;
+  int ref_stride;
+  const double* target;
+  const double* now;
+  const double* Q;  // I x K
+  int I;
+  double* out_kslack;  // optional I x n_src x K
+};
+
+template <int KT>
+__global__ void __launch_bounds__(32 * kK12Warps) k_slack_select(K12Dag g, K12In in, PlanPtrs pp,
+                                                                 int plan_off, SelectIO io) {
+  extern __shared__ __align__(16) uint8_t sm12[];
+  __shared__ int s_pb[kK12MaxSrc + 1], s_qb[kK12MaxSrc + 1], s_off[kK12MaxSrc + 1];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  double2* Dall = reinterpret_cast<double2*>(sm12);
+  int4* P = reinterpret_cast<int4*>(Dall + (size_t)kK12Warps * g.nslots * 32);
+  uint32_t* G = reinterpret_cast<uint32_t*>(P + g.prog_len);
+  uint8_t* plans = sm12 + plan_off;
+  // ---- stage programs, predecessor byte offsets and every plan image ----
+  if (tid <= g.n_src) {
+    s_pb[tid] = g.prog_ptr[tid];
+    s_qb[tid] = g.pred_ptr[tid];
+  }
+  if (tid == 0) {
+    int off = 0;
+    for (int t = 0; t < pp.n; ++t) {
+      s_off[t] = off;
+      off += reinterpret_cast<const PlanHdr*>(pp.p[t])->total_bytes;
+    }
+    s_off[pp.n] = off;
+  }
+  for (int t = tid; t < g.prog_len; t += blockDim.x) P[t] = g.prog[t];
+  for (int t = tid; t < g.pred_len; t += blockDim.x) G[t] = g.preds[t] * (32 * sizeof(double2));
+  __syncthreads();
+  for (int t = 0; t < pp.n; ++t) {
+    const uint4* src = reinterpret_cast<const uint4*>(pp.p[t]);
+    uint4* dst = reinterpret_cast<uint4*>(plans + s_off[t]);
+    const int n16 = (s_off[t + 1] - s_off[t]) / 16;
+    for (int c = tid; c < n16; c += blockDim.x) dst[c] = src[c];
+  }
+  __syncthreads();
+  double2* D = Dall + (size_t)warp * g.nslots * 32 + lane;
+  const char* Db = reinterpret_cast<const char*>(D);
+  const int K = io.K;
+  // ---- one instance per thread, grid-stride over warps of instances ----
+  const int nwarps_total = gridDim.x * kK12Warps;
+  for (int i0 = (blockIdx.x * kK12Warps + warp) * 32; i0 < in.I; i0 += nwarps_total * 32) {
+    const int i = i0 + lane;
+    const bool live = i < in.I;
+    const int ii = live ? i : i0;
+    const double* r = in.ref + (size_t)ii * in.ref_stride;
+    // configurator.py:535  budget = self.target_s - now - queueing[k]
+    const double base = __dsub_rn(__ldg(in.target + ii), __ldg(in.now + ii));
+    double bud[KT];
+#pragma unroll
+    for (int k = 0; k < KT; ++k)
+      bud[k] = k < K ? __dsub_rn(base, __ldg(in.Q + (size_t)ii * K + k)) : 0.0;
+    for (int s = 0; s < g.n_src; ++s) {
+      // K1: forward DP over the source's descendants (sp_slack.cu)
+      const int4* Ps = P + s_pb[s];
+      const int n = s_pb[s + 1] - s_pb[s];
+      const uint32_t* Gs = G + s_qb[s];
+      const int4 head = Ps[0];
+      const double own = __dadd_rn(0.0, __ldg(r + head.x));  // total = 0.0; total += ref[op]
+      D[(head.y & 0xffff) * 32] = make_double2(own, own);
+      double tmax = (head.y >> 16) ? own : -INFINITY;
+      double tmin = (head.y >> 16) ? own : INFINITY;
+      for (int e = 1; e < n; ++e) {
+        const int4 pr = Ps[e];
+        const double rv = __ldg(r + pr.x);
+        const uint2* gp = reinterpret_cast<const uint2*>(Gs + pr.z);
+        double hm = -INFINITY, lm = INFINITY;
+        for (int t = 0; t < pr.w; ++t) {
+          const uint2 w0 = gp[t];
+          const double2 a = *reinterpret_cast<const double2*>(Db + w0.x);
+          const double2 b = *reinterpret_cast<const double2*>(Db + w0.y);
+          hm = hm > a.x ? hm : a.x;
+          hm = hm > b.x ? hm : b.x;
+          lm = lm < a.y ? lm : a.y;
+          lm = lm < b.y ? lm : b.y;
+        }
+        const double h = __dadd_rn(hm, rv), l = __dadd_rn(lm, rv);
+        D[(pr.y & 0xffff) * 32] = make_double2(h, l);
+        if (pr.y >> 16) {
+          tmax = h > tmax ? h : tmax;
+          tmin = l < tmin ? l : tmin;
+        }
+      }
+      const double lo = __ddiv_rn(own, tmax);  // min over suffixes of own/total
+      const double hi = __ddiv_rn(own, tmin);  // max over suffixes of own/total
+      if (!live) continue;
+      // K2: decide invocation (i, s) against operation s's plan
+      const int d = i * g.n_src + s;
+      In<KT> x;
+#pragma unroll
+      for (int k = 0; k < KT; ++k) x.s[k] = k < K ? __dmul_rn(bud[k] >= 0.0 ? lo : hi, bud[k]) : 0.0;
+      if (in.out_kslack) {
+#pragma unroll
+        for (int k = 0; k < KT; ++k)
+          if (k < K) in.out_kslack[(size_t)d * K + k] = x.s[k];
+      }
+      x.av = __ldg(io.avail + d);
+      x.sup = __ldg(io.supply + d);
+      x.mb = __ldg(io.min_batch + d);
+      x.fl = __ldg(io.flags + d);
+      x.t = s;
+      const uint8_t* bp = plans + s_off[s];
+      View<KT> v;
+      make_view<KT>(v, bp, *reinterpret_cast<const PlanHdr*>(bp), K);
+      decide_plan<KT, false>(v, io, d, x);
+    }
+  }
+}

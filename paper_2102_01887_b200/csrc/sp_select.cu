@@ -171,6 +171,7 @@ __device__ __forceinline__ void store_out(const SelectIO& io, int i, const Out& 
 // ---- K2b: staircase plan kernel ----------------------------------------------------------
 #include "sp_k2b.cuh"
 #include "sp_k2f.cuh"
+#include "sp_k12.cuh"
 
 // ---- K2a: literal scan kernel -------------------------------------------------------------
 struct Best {
@@ -444,6 +445,102 @@ int launch_scan_t(sp_ctx* ctx, const ScanPtrs& sp_, size_t stage_bytes, const Se
 }
 
 }  // namespace
+
+static __global__ void k_op_index(int N, int n_src, int32_t* op) {
+  const int d = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d < N) op[d] = d % n_src;
+}
+
+int slack_select_launch(sp_ctx* ctx, sp_dag* g, int n_tables, sp_table* const* tables,
+                        double alpha, int I, const double* ref, int ref_stride,
+                        const double* target, const double* now, int K, const double* Q,
+                        const int32_t* avail, const int32_t* supply, const int32_t* min_batch,
+                        const uint32_t* flags, int32_t* out_idx, int32_t* out_code,
+                        int32_t* out_fill, double* out_obj, double* out_slack, double* out_wait,
+                        double* out_kslack) {
+  if (n_tables != g->n_src) return fail(SP_E_INVALID, "slack_select: one table per DAG source");
+  if (n_tables > kK12MaxSrc) return fail(SP_E_UNSUPPORTED, "slack_select: more than 64 sources");
+  for (int t = 0; t < n_tables; ++t)
+    if (tables[t]->K != K) return fail(SP_E_INVALID, "slack_select: tables disagree with K");
+  if (I == 0) return SP_OK;
+  const int N = I * n_tables;
+  const int KT = K <= 2 ? 2 : (K <= 4 ? 4 : 8);
+  // plans and their sizes (a freshly rebuilt plan's header is waited for once)
+  PlanPtrs pp;
+  pp.n = n_tables;
+  pp.hv = 0;
+  size_t plan_bytes = 0;
+  bool fused = !getenv("SP_NO_K12");
+  for (int t = 0; t < n_tables; ++t) {
+    int rc;
+    Plan* p = plan_get(ctx, tables[t], alpha, &rc);
+    if (!p) return rc;
+    pp.p[t] = p->image;
+    if (!tables[t]->plan_ok) {
+      fused = false;
+      continue;
+    }
+    const PlanHdr* h = plan_host_header(*p);
+    if (!h) {
+      SP_CUDA(cudaEventSynchronize(p->hdr_ready));
+      h = plan_host_header(*p);
+    }
+    if (!h) return fail(SP_E_RUNTIME, "slack_select: plan header unavailable");
+    plan_bytes += (size_t)h->total_bytes;
+  }
+  const size_t dp = (size_t)kK12Warps * g->max_slots * 32 * sizeof(double2);
+  const size_t progb = (size_t)g->prog_len * sizeof(int4) + (((size_t)g->pred_len * 4 + 15) / 16) * 16;
+  const size_t smem = dp + progb + plan_bytes;
+  if (fused && smem <= (size_t)kPlanSmemBudget) {
+    SelectIO io;
+    memset(&io, 0, sizeof(io));
+    io.avail = avail; io.supply = supply; io.min_batch = min_batch; io.flags = flags;
+    io.out_idx = out_idx; io.out_code = out_code; io.out_fill = out_fill;
+    io.out_obj = out_obj; io.out_slack = out_slack; io.out_wait = out_wait;
+    io.N = N; io.K = K;
+    K12Dag kg{g->prog, g->prog_ptr, g->preds, g->pred_ptr, g->n_src, g->max_slots,
+              (int)g->prog_len, (int)g->pred_len};
+    K12In ki{ref, ref_stride, target, now, Q, I, out_kslack};
+    auto launch = [&](auto kern) -> int {
+      static bool attr = false;
+      if (!attr) {
+        SP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     kPlanSmemBudget));
+        attr = true;
+      }
+      int per_sm = 0;
+      SP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * kK12Warps, smem));
+      if (per_sm < 1) return fail(SP_E_UNSUPPORTED, "slack_select: no resident CTA");
+      int blocks = ctx->num_sms * per_sm;
+      const int need = (I + 32 * kK12Warps - 1) / (32 * kK12Warps);
+      if (need < blocks) blocks = need;
+      kern<<<blocks, 32 * kK12Warps, smem, ctx->stream>>>(kg, ki, pp, (int)(dp + progb), io);
+      SP_CHECK_LAUNCH(ctx);
+      return SP_OK;
+    };
+    if (KT == 2) return launch(k_slack_select<2>);
+    if (KT == 4) return launch(k_slack_select<4>);
+    return launch(k_slack_select<8>);
+  }
+  // two-kernel fallback: K1 slack into scratch, then the multi-table K2 launch
+  int rc = SP_OK;
+  const size_t sl_bytes = ((sizeof(double) * (size_t)N * K + 255) / 256) * 256;
+  void* tmp = ctx_tmp(ctx, sl_bytes + sizeof(int32_t) * (size_t)N, &rc);
+  if (!tmp) return rc;
+  double* sl = static_cast<double*>(tmp);
+  int32_t* op = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(tmp) + sl_bytes);
+  rc = slack_launch(ctx, g, I, ref, ref_stride, target, now, K, Q, sl, nullptr);
+  if (rc != SP_OK) return rc;
+  k_op_index<<<(N + 255) / 256, 256, 0, ctx->stream>>>(N, n_tables, op);
+  SP_CHECK_LAUNCH(ctx);
+  rc = select_launch(ctx, n_tables, tables, alpha, N, op, sl, avail, supply, min_batch, flags,
+                     out_idx, out_code, out_fill, out_obj, out_slack, out_wait, nullptr,
+                     SP_MODE_AUTO);
+  if (rc != SP_OK || !out_kslack) return rc;
+  SP_CUDA(cudaMemcpyAsync(out_kslack, sl, sizeof(double) * (size_t)N * K, cudaMemcpyDeviceToDevice,
+                          ctx->stream));
+  return SP_OK;
+}
 
 int select_launch(sp_ctx* ctx, int n_tables, sp_table* const* tables, double alpha, int N,
                   const int32_t* op, const double* slack, const int32_t* avail,

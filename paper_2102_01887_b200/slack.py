@@ -151,6 +151,45 @@ class SlackGraph:
             _lib.SP_MEM_DEVICE if device else _lib.SP_MEM_HOST), "sp_slack_batch")
         return out
 
+    def slack_select_batch(self, tables: Sequence, alpha: float, ref, target, now, Q, available,
+                           *, upstream_supply, min_batch, flags, out=None, kslack: bool = False):
+        """K1 -> K2 fused (sp_slack_select_batch): for every instance i and source s, the Alg. 1
+        slack of s is the slack_by_kind of invocation d = i * n_src + s, decided against
+        ``tables[s]`` (one table per source, in ``source_names`` order).
+
+        ``available``, ``upstream_supply``, ``min_batch``, ``flags``: (I * n_src,).  Returns the
+        decision arrays of ``select_batch`` (flattened over d) and, with ``kslack``, the slack
+        values (I * n_src, K).  numpy -> synchronous; torch CUDA tensors -> stream-ordered.
+        """
+        if len(tables) != len(self.source_names):
+            raise ValueError("slack_select_batch: one table per source operation")
+        device = hasattr(target, "is_cuda") and bool(target.is_cuda)
+        I = int(target.shape[0])
+        K = int(Q.shape[1])
+        N = I * len(tables)
+        stride = 0 if ref.ndim == 1 else int(ref.shape[1])
+        if out is None:
+            if device:
+                import torch
+
+                z = lambda shape, dt: torch.empty(shape, dtype=dt, device=target.device)
+                i32, f64 = torch.int32, torch.float64
+            else:
+                z = lambda shape, dt: np.empty(shape, dtype=dt)
+                i32, f64 = np.int32, np.float64
+            out = {"idx": z(N, i32), "code": z(N, i32), "fill": z(N, i32), "obj": z(N, f64),
+                   "slack": z(N, f64), "wait": z(N, f64)}
+            if kslack:
+                out["kslack"] = z((N, K), f64)
+        arr_t = (C.c_void_p * len(tables))(*[t.handle.value for t in tables])
+        check(self._ctx.lib.sp_slack_select_batch(
+            self._ctx.handle, self._handle, len(tables), C.cast(arr_t, C.c_void_p), float(alpha), I,
+            ptr(ref), stride, ptr(target), ptr(now), K, ptr(Q), ptr(available), ptr(upstream_supply),
+            ptr(min_batch), ptr(flags), ptr(out["idx"]), ptr(out["code"]), ptr(out.get("fill")),
+            ptr(out.get("obj")), ptr(out.get("slack")), ptr(out.get("wait")), ptr(out.get("kslack")),
+            _lib.SP_MEM_DEVICE if device else _lib.SP_MEM_HOST), "sp_slack_select_batch")
+        return out
+
     def slack_by_kind(self, op: str, kinds: Sequence[str], *, target_s: float, now: float,
                       queueing: Mapping[str, float], ref_latency: Mapping[str, float]) -> dict:
         """Configurator.slack_by_kind for one op (configurator.py:526-543)."""

@@ -223,6 +223,50 @@ def test_random_tables_plan_scan_oracle(gpu_ctx, seed, M, nB, K, nonpos):
     tab.close()
 
 
+@pytest.mark.parametrize("seed,M,nB,K,nonpos", [(11, 3000, 8, 2, False), (12, 2000, 16, 4, False),
+                                                (13, 5000, 5, 8, False), (14, 900, 8, 2, True),
+                                                (15, 64, 2, 2, False), (16, 700, 13, 3, False)])
+def test_single_table_fast_kernel_vs_oracle(gpu_ctx, seed, M, nB, K, nonpos):
+    """Once a plan's header has reached the host, single-table calls without kind minima run
+    the specialised K2f kernel (K == 2, 4, 8 with positive thresholds; otherwise K2b): every
+    such call must equal the C oracle, including repeated calls (plan pre-staged before the
+    programmatic-dependent-launch wait) and a call right after a latency update."""
+    import paper_2102_01887_b200 as sp
+
+    rng = np.random.default_rng(seed)
+    t = _random_table(rng, M, nB, K, nonpos)
+    N = 30011
+    slack = rng.uniform(-2, 6, size=(N, K))
+    slack[rng.random((N, K)) < 0.05] = np.inf
+    pick = rng.random((N, K)) < 0.1
+    slack[pick] = rng.choice(t.lat, size=int(pick.sum()))
+    avail = rng.integers(0, 320, size=N).astype(np.int32)
+    supply = rng.integers(0, 320, size=N).astype(np.int32)
+    mb = np.where(rng.random(N) < 0.7, 1, rng.integers(-1, 300, size=N)).astype(np.int32)
+    flags = sp.make_flags(rng.random(N) < 0.5, rng.integers(0, 1 << K, size=N) * (rng.random(N) < 0.3))
+    tab = raw_table(t, K)
+    for alpha in (0.0, 7.5):
+        exp = cselect.select_batch([t], slack, alpha, avail, supply, mb, flags)
+        tab.prepare(alpha)
+        gpu_ctx.synchronize()
+        for rep in range(3):
+            r = sp.select_batch([tab], slack, alpha, avail, upstream_supply=supply, min_batch=mb,
+                                flags=flags, mode="plan")
+            assert_same_decisions(r, exp, f"alpha={alpha} rep={rep}")
+    # latency update -> rebuilt plan (captured into a CUDA graph, then replayed)
+    for step in range(3):
+        j = int(rng.integers(0, M))
+        v = float(t.lat[j] * (0.5 + step))
+        t.lat[j] = v
+        tab.set_latency(np.array([j], np.int32), np.array([v]))
+        exp = cselect.select_batch([t], slack, 7.5, avail, supply, mb, flags)
+        for rep in range(2):
+            r = sp.select_batch([tab], slack, 7.5, avail, upstream_supply=supply, min_batch=mb,
+                                flags=flags, mode="plan")
+            assert_same_decisions(r, exp, f"after update {step} rep={rep}")
+    tab.close()
+
+
 @pytest.mark.parametrize("N", [200_003, 151 * 1024, 1024 * 148 - 1])
 def test_streamed_multitable_ragged_vs_oracle(gpu_ctx, N):
     """Sizes that exercise the TMA input ring (full tiles on every CTA), the ragged tail, and

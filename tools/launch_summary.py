@@ -9,8 +9,11 @@ txt = [l for l in open(sys.argv[1]).read().splitlines() if l.startswith('"')]
 rows = list(csv.reader(txt))
 h = rows[0]
 iK, iV, iU = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+iM = h.index("Metric Name")
 c = collections.defaultdict(list)
 for r in rows[1:]:
+    if r[iM] != "gpu__time_duration.sum":
+        continue
     v = float(r[iV].replace(",", ""))
     v = v / 1e3 if r[iU] == "ns" else (v * 1e3 if r[iU] == "ms" else v)
     c[r[iK][:80]].append(v)
