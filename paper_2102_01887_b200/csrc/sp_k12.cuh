@@ -12,7 +12,10 @@
 // slack never leaves registers.  Persistent grid; every CTA stages all vertex programs and all
 // plans once.
 
-constexpr int kK12Warps = 8;
+constexpr int kK12Warps = 4;
+// per-warp staging of the group's 32 * n_src decisions: 4 input words + 36 output bytes each,
+// so every global access of the per-decision streams is a coalesced, contiguous warp access
+constexpr int kK12StageBytesPerDecision = 16 + 36;
 constexpr int kK12MaxSrc = kMaxPlanTables;
 
 struct K12Dag {
@@ -33,11 +36,16 @@ struct K12In {
   double* out_kslack;  // optional I x n_src x K
 };
 
-template <int KT>
+// FAST: every table has exactly KT kinds, positive thresholds and a batch lookup table, so the
+// decision is K2f's decide_fast (per-table lane lookup table built next to each staged plan);
+// otherwise the generic K2b decide_plan.
+template <int KT, bool FAST>
 __global__ void __launch_bounds__(32 * kK12Warps) k_slack_select(K12Dag g, K12In in, PlanPtrs pp,
-                                                                 int plan_off, SelectIO io) {
+                                                                 int plan_off, int stage_off,
+                                                                 SelectIO io) {
   extern __shared__ __align__(16) uint8_t sm12[];
   __shared__ int s_pb[kK12MaxSrc + 1], s_qb[kK12MaxSrc + 1], s_off[kK12MaxSrc + 1];
+  __shared__ int s_lut[kK12MaxSrc];  // lane lookup table of plan t, relative to its image
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   double2* Dall = reinterpret_cast<double2*>(sm12);
   int4* P = reinterpret_cast<int4*>(Dall + (size_t)kK12Warps * g.nslots * 32);
@@ -51,8 +59,13 @@ __global__ void __launch_bounds__(32 * kK12Warps) k_slack_select(K12Dag g, K12In
   if (tid == 0) {
     int off = 0;
     for (int t = 0; t < pp.n; ++t) {
+      const PlanHdr* hg = reinterpret_cast<const PlanHdr*>(pp.p[t]);
       s_off[t] = off;
-      off += reinterpret_cast<const PlanHdr*>(pp.p[t])->total_bytes;
+      off += hg->total_bytes;
+      if (FAST) {
+        s_lut[t] = hg->total_bytes;  // images are multiples of 16 bytes
+        off += ((hg->lut_n * 4 + 15) / 16) * 16;
+      }
     }
     s_off[pp.n] = off;
   }
@@ -62,16 +75,58 @@ __global__ void __launch_bounds__(32 * kK12Warps) k_slack_select(K12Dag g, K12In
   for (int t = 0; t < pp.n; ++t) {
     const uint4* src = reinterpret_cast<const uint4*>(pp.p[t]);
     uint4* dst = reinterpret_cast<uint4*>(plans + s_off[t]);
-    const int n16 = (s_off[t + 1] - s_off[t]) / 16;
+    const int n16 = reinterpret_cast<const PlanHdr*>(pp.p[t])->total_bytes / 16;
     for (int c = tid; c < n16; c += blockDim.x) dst[c] = src[c];
   }
   __syncthreads();
+  if (FAST) {
+    for (int t = 0; t < pp.n; ++t)
+      build_lane_lut(*reinterpret_cast<const PlanHdr*>(plans + s_off[t]),
+                     reinterpret_cast<uint32_t*>(plans + s_off[t] + s_lut[t]));
+    __syncthreads();
+  }
+  const uint32_t plans_sb = smem_u32(plans);
+  // this warp's staging area: inputs avail, supply, min_batch, flags; outputs idx, code, fill,
+  // obj, slack, wait — decisions d0 + c of the current group at index c
+  const int Dw = 32 * g.n_src;
+  uint8_t* wst = sm12 + stage_off + (size_t)warp * Dw * kK12StageBytesPerDecision;
+  int32_t* s_av = reinterpret_cast<int32_t*>(wst);
+  int32_t* s_sup = s_av + Dw;
+  int32_t* s_mb = s_sup + Dw;
+  uint32_t* s_fl = reinterpret_cast<uint32_t*>(s_mb + Dw);
+  int32_t* o_idx = reinterpret_cast<int32_t*>(s_fl + Dw);
+  int32_t* o_code = o_idx + Dw;
+  int32_t* o_fill = o_code + Dw;
+  double* o_obj = reinterpret_cast<double*>(o_fill + Dw);  // 28 * Dw bytes in: 8-aligned
+  double* o_sl = o_obj + Dw;
+  double* o_wait = o_sl + Dw;
+  SelectIO sio = io;  // decisions land in the staging area
+  sio.out_idx = o_idx; sio.out_code = o_code; sio.out_fill = o_fill;
+  sio.out_obj = o_obj; sio.out_slack = o_sl; sio.out_wait = o_wait;
+  FastIO<KT> fio;
+  if (FAST) {
+    fio.slack = nullptr; fio.avail = nullptr; fio.supply = nullptr;
+    fio.min_batch = nullptr; fio.flags = nullptr; fio.out_idx = o_idx;
+    fio.out_code = o_code; fio.out_fill = o_fill; fio.out_obj = o_obj;
+    fio.out_slack = o_sl; fio.out_wait = o_wait; fio.N = (uint32_t)io.N;
+    fio.lut_bytes_off = 0; fio.prestage = 0;
+  }
   double2* D = Dall + (size_t)warp * g.nslots * 32 + lane;
   const char* Db = reinterpret_cast<const char*>(D);
   const int K = io.K;
   // ---- one instance per thread, grid-stride over warps of instances ----
   const int nwarps_total = gridDim.x * kK12Warps;
   for (int i0 = (blockIdx.x * kK12Warps + warp) * 32; i0 < in.I; i0 += nwarps_total * 32) {
+    const int d0 = i0 * g.n_src;
+    const int nd = min(Dw, io.N - d0);
+    __syncwarp();
+    for (int c = lane; c < nd; c += 32) {  // coalesced loads of the group's decision inputs
+      s_av[c] = __ldg(io.avail + d0 + c);
+      s_sup[c] = __ldg(io.supply + d0 + c);
+      s_mb[c] = __ldg(io.min_batch + d0 + c);
+      s_fl[c] = __ldg(io.flags + d0 + c);
+    }
+    __syncwarp();
     const int i = i0 + lane;
     const bool live = i < in.I;
     const int ii = live ? i : i0;
@@ -126,15 +181,34 @@ __global__ void __launch_bounds__(32 * kK12Warps) k_slack_select(K12Dag g, K12In
         for (int k = 0; k < KT; ++k)
           if (k < K) in.out_kslack[(size_t)d * K + k] = x.s[k];
       }
-      x.av = __ldg(io.avail + d);
-      x.sup = __ldg(io.supply + d);
-      x.mb = __ldg(io.min_batch + d);
-      x.fl = __ldg(io.flags + d);
+      const int dl = lane * g.n_src + s;  // index inside the group's staging area
+      x.av = s_av[dl];
+      x.sup = s_sup[dl];
+      x.mb = s_mb[dl];
+      x.fl = s_fl[dl];
       x.t = s;
       const uint8_t* bp = plans + s_off[s];
-      View<KT> v;
-      make_view<KT>(v, bp, *reinterpret_cast<const PlanHdr*>(bp), K);
-      decide_plan<KT, false>(v, io, d, x);
+      if (FAST) {
+        InF<KT> xf;
+#pragma unroll
+        for (int k = 0; k < KT; ++k) xf.s[k] = x.s[k];
+        xf.av = x.av; xf.sup = x.sup; xf.mb = x.mb; xf.fl = x.fl;
+        decide_fast<KT>(*reinterpret_cast<const PlanHdr*>(bp), plans_sb + (uint32_t)s_off[s],
+                        (uint32_t)s_lut[s], fio, (uint32_t)dl, xf);
+      } else {
+        View<KT> v;
+        make_view<KT>(v, bp, *reinterpret_cast<const PlanHdr*>(bp), K);
+        decide_plan<KT, false>(v, sio, dl, x);
+      }
+    }
+    __syncwarp();
+    for (int c = lane; c < nd; c += 32) {  // coalesced stores of the group's decisions
+      io.out_idx[d0 + c] = o_idx[c];
+      io.out_code[d0 + c] = o_code[c];
+      if (io.out_fill) io.out_fill[d0 + c] = o_fill[c];
+      if (io.out_obj) io.out_obj[d0 + c] = o_obj[c];
+      if (io.out_slack) io.out_slack[d0 + c] = o_sl[c];
+      if (io.out_wait) io.out_wait[d0 + c] = o_wait[c];
     }
   }
 }

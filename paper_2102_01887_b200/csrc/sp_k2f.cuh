@@ -120,11 +120,10 @@ __device__ __forceinline__ int fast_row(uint32_t sm, const KindDesc& d, double s
 }
 
 template <int K>
-__device__ __forceinline__ void decide_fast(const PlanHdr& h, uint32_t sm, const FastIO<K>& io,
-                                            uint32_t i, const InF<K>& x) {
+__device__ __forceinline__ void decide_fast(const PlanHdr& h, uint32_t sm, uint32_t lut,
+                                            const FastIO<K>& io, uint32_t i, const InF<K>& x) {
   const int nB = h.nB;
   const int lmax = h.lut_n - 1;
-  const uint32_t lut = (uint32_t)io.lut_bytes_off;
   // batch lanes admitted by min_batch (configurator.py:264-265) and by available (288)
   const uint32_t A = lds_u32(sm + lut + 4u * (uint32_t)min(max(x.mb, 0), lmax));
   const uint32_t B = lds_u32(sm + lut + 4u * (uint32_t)min(max(x.av, 0), lmax));
@@ -188,6 +187,20 @@ __device__ __forceinline__ void decide_fast(const PlanHdr& h, uint32_t sm, const
   io.out_wait[i] = (some && delay) ? wait : 0.0;
 }
 
+// CTA lookup table v -> (#batch < v) | (#batch <= v) << 8 | (tri_base(lo) - lo) << 16
+__device__ __forceinline__ void build_lane_lut(const PlanHdr& h, uint32_t* lut) {
+  const int nB = h.nB;
+  for (int v = threadIdx.x; v < h.lut_n; v += blockDim.x) {
+    int lo = 0, le = 0;
+    for (int b = 0; b < nB; ++b) {
+      lo += h.batch_vals[b] < v;
+      le += h.batch_vals[b] <= v;
+    }
+    const int tb = lo * nB - ((lo * (lo - 1)) >> 1) - lo;
+    lut[v] = (uint32_t)lo | ((uint32_t)le << 8) | ((uint32_t)tb << 16);
+  }
+}
+
 template <int K>
 __global__ void __launch_bounds__(1024, 1) k_select_fast(const uint8_t* __restrict__ plan,
                                                          PlanHdr h, FastIO<K> io) {
@@ -208,20 +221,7 @@ __global__ void __launch_bounds__(1024, 1) k_select_fast(const uint8_t* __restri
         bulk_g2s(smem + c, plan + c, (uint32_t)min(kStageChunk, bytes - c), &s_bar);
     }
   }
-  // CTA lookup table v -> (#batch < v) | (#batch <= v) << 8 | (tri_base(lo) - lo) << 16
-  {
-    uint32_t* lut = reinterpret_cast<uint32_t*>(smem + io.lut_bytes_off);
-    const int nB = h.nB;
-    for (int v = tid; v < h.lut_n; v += blockDim.x) {
-      int lo = 0, le = 0;
-      for (int b = 0; b < nB; ++b) {
-        lo += h.batch_vals[b] < v;
-        le += h.batch_vals[b] <= v;
-      }
-      const int tb = lo * nB - ((lo * (lo - 1)) >> 1) - lo;
-      lut[v] = (uint32_t)lo | ((uint32_t)le << 8) | ((uint32_t)tb << 16);
-    }
-  }
+  build_lane_lut(h, reinterpret_cast<uint32_t*>(smem + io.lut_bytes_off));
   asm volatile("griddepcontrol.wait;" ::: "memory");
   // the next launch in the stream may start its prologue as this grid's CTAs retire
   asm volatile("griddepcontrol.launch_dependents;");
@@ -241,11 +241,11 @@ __global__ void __launch_bounds__(1024, 1) k_select_fast(const uint8_t* __restri
   asm volatile("mov.u32 %0, %1;" : "=r"(sb) : "r"(smem_u32(smem)) : "memory");
   // ping-pong over two register buffers: invocation i + stride is in flight while i is decided
   for (; i < io.N; i += 2 * stride) {
-    decide_fast<K>(h, sb, io, i, a);
+    decide_fast<K>(h, sb, (uint32_t)io.lut_bytes_off, io, i, a);
     const uint32_t j = i + stride;
     if (j >= io.N) break;
     if (j + stride < io.N) load_fast<K>(io, j + stride, a);
-    decide_fast<K>(h, sb, io, j, b);
+    decide_fast<K>(h, sb, (uint32_t)io.lut_bytes_off, io, j, b);
     if (j + 2 * stride < io.N) load_fast<K>(io, j + 2 * stride, b);
   }
 }

@@ -469,8 +469,9 @@ int slack_select_launch(sp_ctx* ctx, sp_dag* g, int n_tables, sp_table* const* t
   PlanPtrs pp;
   pp.n = n_tables;
   pp.hv = 0;
-  size_t plan_bytes = 0;
+  size_t plan_bytes = 0, lut_bytes = 0;
   bool fused = !getenv("SP_NO_K12");
+  bool fast_ok = !getenv("SP_K12_GENERIC");
   for (int t = 0; t < n_tables; ++t) {
     int rc;
     Plan* p = plan_get(ctx, tables[t], alpha, &rc);
@@ -487,10 +488,16 @@ int slack_select_launch(sp_ctx* ctx, sp_dag* g, int n_tables, sp_table* const* t
     }
     if (!h) return fail(SP_E_RUNTIME, "slack_select: plan header unavailable");
     plan_bytes += (size_t)h->total_bytes;
+    lut_bytes += (size_t)((h->lut_n * 4 + 15) / 16) * 16;
+    for (int k = 0; k < K; ++k) fast_ok = fast_ok && h->kd[k].pad[0] == 0;
+    fast_ok = fast_ok && h->lut_n > 0 && K == KT;
   }
   const size_t dp = (size_t)kK12Warps * g->max_slots * 32 * sizeof(double2);
   const size_t progb = (size_t)g->prog_len * sizeof(int4) + (((size_t)g->pred_len * 4 + 15) / 16) * 16;
-  const size_t smem = dp + progb + plan_bytes;
+  if (!fused) fast_ok = false;
+  const size_t plans_all = plan_bytes + (fast_ok ? lut_bytes : 0);
+  const size_t stage = (size_t)kK12Warps * 32 * n_tables * kK12StageBytesPerDecision;
+  const size_t smem = dp + progb + plans_all + stage;
   if (fused && smem <= (size_t)kPlanSmemBudget) {
     SelectIO io;
     memset(&io, 0, sizeof(io));
@@ -502,11 +509,17 @@ int slack_select_launch(sp_ctx* ctx, sp_dag* g, int n_tables, sp_table* const* t
               (int)g->prog_len, (int)g->pred_len};
     K12In ki{ref, ref_stride, target, now, Q, I, out_kslack};
     auto launch = [&](auto kern) -> int {
-      static bool attr = false;
-      if (!attr) {
+      static const void* attr_done[6] = {};  // one entry per k_slack_select instantiation
+      bool done = false;
+      for (const void* f : attr_done) done = done || f == reinterpret_cast<const void*>(kern);
+      if (!done) {
         SP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      kPlanSmemBudget));
-        attr = true;
+        for (const void*& f : attr_done)
+          if (!f) {
+            f = reinterpret_cast<const void*>(kern);
+            break;
+          }
       }
       int per_sm = 0;
       SP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * kK12Warps, smem));
@@ -514,13 +527,19 @@ int slack_select_launch(sp_ctx* ctx, sp_dag* g, int n_tables, sp_table* const* t
       int blocks = ctx->num_sms * per_sm;
       const int need = (I + 32 * kK12Warps - 1) / (32 * kK12Warps);
       if (need < blocks) blocks = need;
-      kern<<<blocks, 32 * kK12Warps, smem, ctx->stream>>>(kg, ki, pp, (int)(dp + progb), io);
+      kern<<<blocks, 32 * kK12Warps, smem, ctx->stream>>>(kg, ki, pp, (int)(dp + progb),
+                                                          (int)(dp + progb + plans_all), io);
       SP_CHECK_LAUNCH(ctx);
       return SP_OK;
     };
-    if (KT == 2) return launch(k_slack_select<2>);
-    if (KT == 4) return launch(k_slack_select<4>);
-    return launch(k_slack_select<8>);
+    if (fast_ok) {
+      if (KT == 2) return launch(k_slack_select<2, true>);
+      if (KT == 4) return launch(k_slack_select<4, true>);
+      return launch(k_slack_select<8, true>);
+    }
+    if (KT == 2) return launch(k_slack_select<2, false>);
+    if (KT == 4) return launch(k_slack_select<4, false>);
+    return launch(k_slack_select<8, false>);
   }
   // two-kernel fallback: K1 slack into scratch, then the multi-table K2 launch
   int rc = SP_OK;

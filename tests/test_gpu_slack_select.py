@@ -64,15 +64,18 @@ def test_fused_matches_two_kernels(gpu_ctx, alpha):
     some = (two["code"] & 3) != 0
     for k in ("obj", "slack", "wait"):
         assert np.array_equal(bits(fused[k][some]), bits(two[k][some])), k
-    # the two-kernel fallback inside the library gives the same
-    os.environ["SP_NO_K12"] = "1"
-    try:
-        fb = g.slack_select_batch(tabs, alpha, refv, target, now, Q, avail, upstream_supply=supply,
-                                  min_batch=mb, flags=flags)
-    finally:
-        del os.environ["SP_NO_K12"]
-    assert np.array_equal(fb["idx"], fused["idx"]) and np.array_equal(fb["code"], fused["code"])
-    assert np.array_equal(bits(fb["obj"][some]), bits(fused["obj"][some]))
+    # the generic-decision fused kernel and the two-kernel fallback inside the library agree
+    for env in ("SP_K12_GENERIC", "SP_NO_K12"):
+        os.environ[env] = "1"
+        try:
+            fb = g.slack_select_batch(tabs, alpha, refv, target, now, Q, avail, upstream_supply=supply,
+                                      min_batch=mb, flags=flags)
+        finally:
+            del os.environ[env]
+        assert np.array_equal(fb["idx"], fused["idx"]) and np.array_equal(fb["code"], fused["code"]), env
+        assert np.array_equal(fb["fill"], fused["fill"]), env
+        for k in ("obj", "slack", "wait"):
+            assert np.array_equal(bits(fb[k][some]), bits(fused[k][some])), (env, k)
 
 
 def test_fused_matches_oracle_sample(gpu_ctx):
