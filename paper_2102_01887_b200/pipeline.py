@@ -37,6 +37,36 @@ class ConfigEntry:
             raise ValueError(f"{self.config_id}: latency must be positive")
 
 
+    def to_json(self) -> dict[str, Any]:
+        """pipeline.py:217-228 (same keys, knob values sorted by name)."""
+        return {
+            "config_id": self.config_id,
+            "backend_kind": self.backend_kind,
+            "knob_values": dict(sorted(self.knob_values.items())),
+            "batch_size": self.batch_size,
+            "resource_request": self.resource_request,
+            "latency_s": self.latency_s,
+            "latency_initial_s": self.latency_initial_s,
+            "peak_memory_mb": self.peak_memory_mb,
+            "schedulable": self.schedulable,
+        }
+
+    @staticmethod
+    def from_json(obj: Mapping[str, Any]) -> "ConfigEntry":
+        """pipeline.py:230-242."""
+        return ConfigEntry(
+            config_id=obj["config_id"],
+            backend_kind=obj["backend_kind"],
+            knob_values=dict(obj["knob_values"]),
+            batch_size=int(obj["batch_size"]),
+            resource_request=int(obj["resource_request"]),
+            latency_s=float(obj["latency_s"]),
+            latency_initial_s=float(obj["latency_initial_s"]),
+            peak_memory_mb=float(obj.get("peak_memory_mb", 0.0)),
+            schedulable=bool(obj.get("schedulable", True)),
+        )
+
+
 @dataclass
 class ConfigSpec:
     """All profiled configurations of one operation (pipeline.py:245-258)."""
@@ -51,6 +81,18 @@ class ConfigSpec:
             raise ValueError(f"{self.operation}: duplicate config ids")
         if self.reference_id not in set(ids):
             raise ValueError(f"{self.operation}: reference {self.reference_id!r} not among entries")
+
+    def to_json(self) -> dict[str, Any]:
+        """pipeline.py:266-271."""
+        return {"operation": self.operation, "reference_id": self.reference_id,
+                "entries": [e.to_json() for e in self.entries]}
+
+    @staticmethod
+    def from_json(obj: Mapping[str, Any]) -> "ConfigSpec":
+        """pipeline.py:273-279."""
+        return ConfigSpec(operation=obj["operation"],
+                          entries=[ConfigEntry.from_json(e) for e in obj["entries"]],
+                          reference_id=obj["reference_id"])
 
 
 def config_id_of(kind: str, resource: int, batch: int, knobs: Sequence[tuple[str, Any]] = ()) -> str:

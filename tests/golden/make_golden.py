@@ -608,6 +608,28 @@ def gen_commit_rounds(R, ref_root: Path, max_rounds=6000):
     out["meta_json"] = np.frombuffer(json.dumps(meta).encode(), np.uint8)
     return out
 
+
+# ---- 8. metadata directory (profile ingest) ---------------------------
+
+def gen_metadata_amber(R, ref_root: Path):
+    """The reference's own MetadataStore files for the AMBER pipeline: one configspec JSON per
+    operation (profile_operation of the bundled scenario) and the decomposed path set."""
+    conf, man, pipe, prof, scen = R
+    import shutil
+
+    bundle = ref_root / "scenarios" / "branching"
+    doc = json.loads((bundle / "pipeline.json").read_text())
+    dag, ops = pipe.load_pipeline(doc)
+    sc = scen.load_scenario(bundle / "scenario.json")
+    out_dir = HERE / "metadata_amber"
+    if out_dir.exists():
+        shutil.rmtree(out_dir)
+    store = prof.MetadataStore(out_dir)
+    for name, op in sorted(ops.items()):
+        store.ensure_profile(op, sc, sc.tuning.samples_per_config)
+    store.store_paths(pipe.pipeline_content_hash(doc), pipe.decompose_paths(dag))
+    return None
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--ref", default="/root/reference/pkg/src")
@@ -623,11 +645,15 @@ def main() -> None:
         "queue_cases": lambda: gen_queue(R),
         "amber_trace": lambda: gen_amber(R, ref_root),
         "commit_rounds": lambda: gen_commit_rounds(R, ref_root),
+        "metadata_amber": lambda: gen_metadata_amber(R, ref_root),
     }
     for name, fn in jobs.items():
         if a.only and name not in a.only.split(","):
             continue
         out = fn()
+        if out is None:  # job wrote its own files
+            print(name, "written")
+            continue
         np.savez_compressed(HERE / f"{name}.npz", **out)
         print(name, {k: v.shape for k, v in list(out.items())[:6]}, "...")
 
