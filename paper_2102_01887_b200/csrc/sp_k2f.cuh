@@ -201,9 +201,9 @@ __device__ __forceinline__ void build_lane_lut(const PlanHdr& h, uint32_t* lut) 
   }
 }
 
-template <int K>
-__global__ void __launch_bounds__(1024, 1) k_select_fast(const uint8_t* __restrict__ plan,
-                                                         PlanHdr h, FastIO<K> io) {
+template <int K, int THREADS = 1024>
+__global__ void __launch_bounds__(THREADS, 1024 / THREADS) k_select_fast(
+    const uint8_t* __restrict__ plan, PlanHdr h, FastIO<K> io) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t s_bar;
   const int tid = threadIdx.x;
