@@ -169,171 +169,6 @@ __device__ __forceinline__ void decide_plan(const View<KT>& v, const SelectIO& i
   store_out(io, i, o);
 }
 
-// ---- paired decision (single-table hot path) -------------------------------------------
-// Two invocations per thread, written phase by phase without data-dependent branches so the
-// compiler interleaves the two dependency chains (shared-memory load latency is the limiter).
-
-// Two predicated steps of the in-bucket binary search; exact for buckets of <= 3 thresholds,
-// the rare larger bucket finishes in stair_tail.
-__device__ __forceinline__ void stair_step(const double* thr, int rmax, double s, int& r, int& n) {
-  const int hh = n >> 1;
-  const int at = min(r + hh + 1, rmax);
-  const bool lt = n > 0 && thr[at] < s;
-  r = lt ? r + hh + 1 : r;
-  n = n > 0 ? (lt ? n - hh - 1 : hh) : 0;
-}
-__device__ __forceinline__ void stair_tail(const double* thr, double s, int& r, int& n) {
-  while (n > 0) {
-    const int hh = n >> 1;
-    const bool lt = thr[r + hh + 1] < s;
-    r = lt ? r + hh + 1 : r;
-    n = lt ? n - hh - 1 : hh;
-  }
-}
-__device__ __forceinline__ void stair_begin(const uint8_t* base, const uint4& q0, const uint4& q1,
-                                            double s, int& r, int& n) {
-  const bool nonpos = q1.z != 0;
-  r = 0;
-  n = nonpos ? (int)q1.y - 1 : 0;
-  if (!nonpos) {
-    const uint32_t* bkt = reinterpret_cast<const uint32_t*>(base + (int)q1.x);
-    const int d = __double2hiint(s) - (int)q0.x;
-    const uint32_t nb1 = q0.y & 0xFFFFu;
-    uint32_t b = d < 0 ? 0u : ((uint32_t)d >> (q0.y >> 16));
-    b = b < nb1 ? b : nb1;
-    const uint32_t e = bkt[b];
-    const bool pos = s > 0.0;  // s <= 0 or NaN: below every (positive) threshold
-    r = pos ? (int)(e & 0xFFFFu) : 0;
-    n = pos ? (int)(e >> 16) : 0;
-  }
-}
-
-template <int KT>
-__device__ __forceinline__ void decide_pair(const View<KT>& v, const SelectIO& io, int i0, int i1,
-                                            const In<KT>& x0, const In<KT>& x1) {
-  const uint8_t* base = v.base;
-  const int nB = v.nB;
-  const double* rscore = reinterpret_cast<const double*>(base + v.score_off);
-  const double* rlat = reinterpret_cast<const double*>(base + v.lat_off);
-  const CandB* recb = reinterpret_cast<const CandB*>(base + v.recb_off);
-  const In<KT>* X[2] = {&x0, &x1};
-  const bool live[2] = {true, i1 < io.N};
-
-  int lo[2], le[2], idx1[2];
-#pragma unroll
-  for (int j = 0; j < 2; ++j) {
-    if (v.lut_n > 0) {
-      const uint16_t* lut = reinterpret_cast<const uint16_t*>(base + v.lut_off);
-      lo[j] = (int)(lut[min(max(X[j]->mb, 0), v.lut_n - 1)] & 0xFFu);
-      le[j] = (int)(lut[min(max(X[j]->av, 0), v.lut_n - 1)] >> 8);
-    } else {
-      const PlanHdr* h = reinterpret_cast<const PlanHdr*>(base);
-      lo[j] = le[j] = 0;
-      for (int b = 0; b < nB; ++b) {
-        const int bv = h->batch_vals[b];
-        lo[j] += (bv < X[j]->mb);
-        le[j] += (bv <= X[j]->av);
-      }
-    }
-    idx1[j] = lo[j] < nB ? tri_index(lo[j], nB - 1, nB) : 0;
-  }
-
-  uint32_t u[2] = {kNone16, kNone16};
-  int rowoff[2][KT];
-#pragma unroll
-  for (int k = 0; k < KT; ++k) {
-    rowoff[0][k] = rowoff[1][k] = -1;
-    if (k >= io.K || v.q1[k].y == 0) continue;  // uniform
-    const double* thr = reinterpret_cast<const double*>(base + (int)v.q0[k].z);
-    const int rmax = (int)v.q1[k].y - 1;
-    int r[2], n[2];
-#pragma unroll
-    for (int j = 0; j < 2; ++j) stair_begin(base, v.q0[k], v.q1[k], X[j]->s[k], r[j], n[j]);
-#pragma unroll
-    for (int j = 0; j < 2; ++j) stair_step(thr, rmax, X[j]->s[k], r[j], n[j]);
-#pragma unroll
-    for (int j = 0; j < 2; ++j) stair_step(thr, rmax, X[j]->s[k], r[j], n[j]);
-#pragma unroll
-    for (int j = 0; j < 2; ++j) stair_tail(thr, X[j]->s[k], r[j], n[j]);
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const bool ex = (X[j]->fl >> (SP_FLAG_EXCL_SHIFT + k)) & 1u;
-      const int ro = (int)v.q0[k].w + r[j] * v.stride;
-      const uint32_t m = reinterpret_cast<const uint16_t*>(base + ro)[idx1[j]];
-      u[j] = (ex || lo[j] >= nB) ? u[j] : min(u[j], m);
-      rowoff[j][k] = ex ? -1 : ro;
-    }
-  }
-
-  Out o[2];
-  CandB cb[2];
-  double score[2], sk[2], wait[2];
-  bool delay[2], down[2];
-#pragma unroll
-  for (int j = 0; j < 2; ++j) {
-    const uint32_t uu = u[j] == kNone16 ? 0u : u[j];
-    cb[j] = recb[uu];
-    score[j] = rscore[uu];
-    sk[j] = pick_kind<KT>(X[j]->s, (int)(cb[j].meta >> 17));
-    const bool big = cb[j].batch > X[j]->av;
-    const bool cand = (X[j]->fl & SP_FLAG_ALLOW_DELAY) && big &&
-                      (long long)X[j]->sup >= (long long)cb[j].batch - (long long)X[j]->av;
-    wait[j] = __dsub_rn(sk[j], rlat[uu]);
-    delay[j] = cand && wait[j] > 0.0;
-    down[j] = !delay[j] && big && lo[j] < le[j];
-  }
-#pragma unroll
-  for (int j = 0; j < 2; ++j) {
-    if (down[j]) {  // configurator.py:287-291
-      const int idx2 = tri_index(lo[j], le[j] - 1, nB);
-      uint32_t u2 = kNone16;
-#pragma unroll
-      for (int k = 0; k < KT; ++k)
-        if (rowoff[j][k] >= 0)
-          u2 = min(u2, (uint32_t)reinterpret_cast<const uint16_t*>(base + rowoff[j][k])[idx2]);
-      if (u2 != kNone16) {
-        cb[j] = recb[u2];
-        score[j] = rscore[u2];
-        sk[j] = pick_kind<KT>(X[j]->s, (int)(cb[j].meta >> 17));
-      }
-    }
-  }
-#pragma unroll
-  for (int j = 0; j < 2; ++j) {
-    const bool some = u[j] != kNone16;
-    const int feas = (cb[j].meta >> 16) & 1u;
-    o[j].idx = some ? (int)(cb[j].meta & 0xFFFFu) : -1;
-    o[j].code = some ? ((delay[j] ? SP_DEC_DELAY : SP_DEC_ASSIGN) | (feas ? SP_DEC_FEASIBLE : 0))
-                     : SP_DEC_NONE;
-    o[j].fill = some ? (delay[j] ? X[j]->av : min(cb[j].batch, X[j]->av)) : 0;
-    o[j].obj = some ? score[j] : 0.0;
-    o[j].slack = some ? sk[j] : 0.0;
-    o[j].wait = (some && delay[j]) ? wait[j] : 0.0;
-  }
-  store_out(io, i0, o[0]);
-  if (live[1]) store_out(io, i1, o[1]);
-}
-
-// Paired single-table loop: thread handles invocations (i, i + stride) per iteration while the
-// next pair is prefetched into registers.
-template <int KT>
-__device__ __forceinline__ void plan_loop_pair(const View<KT>& v, const SelectIO& io, int i) {
-  const int stride = gridDim.x * blockDim.x;
-  In<KT> a0, a1, b0, b1;
-  if (i < io.N) load_in<KT>(io, i, a0);
-  if (i + stride < io.N) load_in<KT>(io, i + stride, a1);
-  for (; i < io.N; i += 4 * stride) {
-    if (i + 2 * stride < io.N) load_in<KT>(io, i + 2 * stride, b0);
-    if (i + 3 * stride < io.N) load_in<KT>(io, i + 3 * stride, b1);
-    decide_pair<KT>(v, io, i, i + stride, a0, a1);
-    const int j = i + 2 * stride;
-    if (j >= io.N) break;
-    if (j + 2 * stride < io.N) load_in<KT>(io, j + 2 * stride, a0);
-    if (j + 3 * stride < io.N) load_in<KT>(io, j + 3 * stride, a1);
-    decide_pair<KT>(v, io, j, j + stride, b0, b1);
-  }
-}
-
 // Single-table hot loop: the view is built once from the parameter-space header.
 // Ping-pong over two register buffers (unrolled by two so no buffer is ever copied): while
 // invocation i is decided from buffer A, invocation i + stride is already in flight into B.
@@ -366,63 +201,6 @@ __device__ __forceinline__ void plan_loop_multi(const uint8_t* smem, const PlanP
     make_view<KT>(v, base, *reinterpret_cast<const PlanHdr*>(base), io.K);
     decide_plan<KT, KMIN>(v, io, i, x);
   }
-}
-
-// Lean variant: 2 CTAs x 768 threads per SM (<= 42 registers), one invocation per thread per
-// step and no register prefetch — more warps in flight instead of deeper per-thread queues.
-template <int KT>
-__global__ void __launch_bounds__(768, 2) k_select_lean(PlanPtrs pp, int smem_budget, SelectIO io) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ __align__(8) uint64_t s_bar;
-  const int tid = threadIdx.x;
-  const int bytes = pp.h.total_bytes;
-  const bool fit = bytes <= smem_budget;
-  if (tid == 0 && fit) {
-    mbar_init(&s_bar, 1);
-    mbar_expect_tx(&s_bar, (uint32_t)bytes);
-    bulk_g2s(smem, pp.p[0], (uint32_t)bytes, &s_bar);
-  }
-  const int stride = gridDim.x * blockDim.x;
-  int i = blockIdx.x * blockDim.x + tid;
-  In<KT> x;
-  if (i < io.N) load_in<KT>(io, i, x);
-  __syncthreads();
-  View<KT> v;
-  if (fit) {
-    mbar_wait(&s_bar, 0);
-    make_view<KT>(v, smem, pp.h, io.K);
-  } else {
-    make_view<KT>(v, pp.p[0], pp.h, io.K);
-  }
-  for (; i < io.N; i += stride) {
-    decide_plan<KT, false>(v, io, i, x);
-    if (i + stride < io.N) load_in<KT>(io, i + stride, x);
-  }
-}
-
-// Paired variant for single-table launches whose header is a kernel parameter: 512 threads
-// per SM (128-register budget), two invocations per thread per step.
-template <int KT>
-__global__ void __launch_bounds__(512, 1) k_select_pair(PlanPtrs pp, int smem_budget, SelectIO io) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ __align__(8) uint64_t s_bar;
-  const int tid = threadIdx.x;
-  const int bytes = pp.h.total_bytes;
-  const bool fit = bytes <= smem_budget;
-  if (tid == 0 && fit) {
-    mbar_init(&s_bar, 1);
-    mbar_expect_tx(&s_bar, (uint32_t)bytes);
-    bulk_g2s(smem, pp.p[0], (uint32_t)bytes, &s_bar);
-  }
-  __syncthreads();
-  View<KT> v;
-  if (fit) {
-    mbar_wait(&s_bar, 0);
-    make_view<KT>(v, smem, pp.h, io.K);
-  } else {
-    make_view<KT>(v, pp.p[0], pp.h, io.K);
-  }
-  plan_loop_pair<KT>(v, io, blockIdx.x * blockDim.x + tid);
 }
 
 template <int KT>

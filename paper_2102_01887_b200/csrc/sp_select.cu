@@ -347,10 +347,6 @@ int launch_plan_t(sp_ctx* ctx, const PlanPtrs& pp, const SelectIO& io) {
   if (!attr_done) {
     SP_CUDA(cudaFuncSetAttribute(k_select_plan<KT>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kPlanSmemBudget));
-    SP_CUDA(cudaFuncSetAttribute(k_select_pair<KT>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, kPlanSmemBudget));
-    SP_CUDA(cudaFuncSetAttribute(k_select_lean<KT>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
     attr_done = true;
   }
   const char* variant = getenv("SP_K2_VARIANT");
@@ -404,22 +400,6 @@ int launch_plan_t(sp_ctx* ctx, const PlanPtrs& pp, const SelectIO& io) {
       ctx->plan_dirty = false;
       return SP_OK;
     }
-  }
-  if (single && variant && !strcmp(variant, "lean")) {
-    int blocks = ctx->num_sms * 2;
-    int need = (io.N + 767) / 768;
-    if (need < blocks) blocks = need > 0 ? need : 1;
-    k_select_lean<KT><<<blocks, 768, 100 * 1024, ctx->stream>>>(pp, 100 * 1024, io);
-    SP_CHECK_LAUNCH(ctx);
-    return SP_OK;
-  }
-  if (single && variant && !strcmp(variant, "pair")) {
-    int blocks = ctx->num_sms;
-    int need = (io.N + 511) / 512;
-    if (need < blocks) blocks = need > 0 ? need : 1;
-    k_select_pair<KT><<<blocks, 512, kPlanSmemBudget, ctx->stream>>>(pp, kPlanSmemBudget, io);
-    SP_CHECK_LAUNCH(ctx);
-    return SP_OK;
   }
   int blocks = ctx->num_sms * kPlanCtasPerSm;
   int need = (io.N + kPlanThreads - 1) / kPlanThreads;
