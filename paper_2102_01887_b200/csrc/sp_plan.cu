@@ -65,7 +65,8 @@ __global__ void k_cost(int M, const double* __restrict__ lat, const double* __re
 //   order  entries by (kind, lat, index)              -> latency order inside each kind
 // Each is a sort of M unique (u64 key, u32 tag) items: CTA tiles of 2048 items are sorted with
 // a block merge sort (k_tile_sort), then every item's final position is its rank inside its
-// tile plus, per other tile, the number of smaller items there (binary search, k_merge_rank).
+// tile plus, per other tile, the number of smaller items there (k_merge_pairs: one CTA per
+// (tile, other tile) pair, the other tile staged in shared memory, binary searches there).
 // r1 sorts by (cost, index) and then resolves exact-equality cost ties by (res, id_rank)
 // inside each (short) tie run (k_rank_r1).
 
@@ -78,7 +79,7 @@ struct __align__(16) SItem {
   uint32_t t;
   uint32_t pad;
 };
-constexpr int kSortThreads = 512, kSortIpt = 4, kSortTile = kSortThreads * kSortIpt;
+constexpr int kSortThreads = 128, kSortIpt = 4, kSortTile = kSortThreads * kSortIpt;
 constexpr int kSortR1 = 0, kSortR2 = 1, kSortOrder = 2;
 
 template <int KIND>
@@ -124,7 +125,7 @@ __device__ __forceinline__ SItem make_item(int j, int M, const double* __restric
 
 template <int KIND>
 __device__ void tile_sort(int M, int tile, const double* a, const int32_t* b, SItem* out,
-                          void* temp) {
+                          int32_t* rank, void* temp) {
   using Sort = cub::BlockMergeSort<SItem, kSortThreads, kSortIpt>;
   SItem it[kSortIpt];
   const int base = tile * kSortTile + threadIdx.x * kSortIpt;
@@ -132,53 +133,71 @@ __device__ void tile_sort(int M, int tile, const double* a, const int32_t* b, SI
   for (int q = 0; q < kSortIpt; ++q) it[q] = make_item<KIND>(base + q, M, a, b);
   Sort(*reinterpret_cast<typename Sort::TempStorage*>(temp)).Sort(it, SLess<KIND>());
 #pragma unroll
-  for (int q = 0; q < kSortIpt; ++q) out[base + q] = it[q];
+  for (int q = 0; q < kSortIpt; ++q) {
+    out[base + q] = it[q];
+    rank[base + q] = threadIdx.x * kSortIpt + q;  // rank inside the tile; k_merge_pairs adds
+  }
 }
 
 // blockIdx.x < ntiles: sort A (KA) tile; otherwise sort B (KB) tile (B may be absent)
 template <int KA, int KB>
 __global__ void __launch_bounds__(kSortThreads) k_tile_sort(int M, int ntiles, const double* aA,
                                                             const int32_t* bA, SItem* outA,
-                                                            const double* aB, const int32_t* bB,
-                                                            SItem* outB) {
+                                                            int32_t* rkA, const double* aB,
+                                                            const int32_t* bB, SItem* outB,
+                                                            int32_t* rkB) {
   __shared__ typename cub::BlockMergeSort<SItem, kSortThreads, kSortIpt>::TempStorage temp;
   if ((int)blockIdx.x < ntiles)
-    tile_sort<KA>(M, blockIdx.x, aA, bA, outA, &temp);
+    tile_sort<KA>(M, blockIdx.x, aA, bA, outA, rkA, &temp);
   else
-    tile_sort<KB>(M, blockIdx.x - ntiles, aB, bB, outB, &temp);
+    tile_sort<KB>(M, blockIdx.x - ntiles, aB, bB, outB, rkB, &temp);
 }
 
+// CTA (x, y): items of tile a (x < ntiles: sort A, else sort B, tile x - ntiles) against tile
+// b = y of the same sort, staged in shared memory; every item adds the number of smaller items
+// of tile b to its rank (items are unique, so the ranks form a permutation).
 template <int KIND>
-__device__ __forceinline__ int merged_rank(const SItem* __restrict__ tiles, int ntiles, int p) {
-  const SItem x = tiles[p];
-  const int a = p / kSortTile;
-  int r = p - a * kSortTile;
+__device__ __forceinline__ void merge_pair(const SItem* __restrict__ tiles, int32_t* rank, int a,
+                                           int b, SItem* sb) {
+  for (int c = threadIdx.x; c < kSortTile; c += blockDim.x) sb[c] = tiles[(size_t)b * kSortTile + c];
+  __syncthreads();
   SLess<KIND> less;
-  for (int bt = 0; bt < ntiles; ++bt) {
-    if (bt == a) continue;
-    const SItem* t = tiles + (size_t)bt * kSortTile;
-    int lo = 0, hi = kSortTile;  // # items of tile bt smaller than x (items are unique)
+  for (int e = threadIdx.x; e < kSortTile; e += blockDim.x) {
+    const SItem x = tiles[(size_t)a * kSortTile + e];
+    int lo = 0, hi = kSortTile;
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
-      if (less(t[mid], x)) lo = mid + 1; else hi = mid;
+      if (less(sb[mid], x)) lo = mid + 1; else hi = mid;
     }
-    r += lo;
+    if (lo) atomicAdd(&rank[(size_t)a * kSortTile + e], lo);
   }
-  return r;
 }
 
-// final positions of both sorts' items; only real items (position < M) are written
 template <int KA, int KB>
-__global__ void k_merge_rank(int M, int ntiles, const SItem* __restrict__ tA, SItem* outA,
-                             const SItem* __restrict__ tB, SItem* outB) {
-  const int n = ntiles * kSortTile;
+__global__ void __launch_bounds__(256) k_merge_pairs(int ntiles, const SItem* __restrict__ tA,
+                                                     int32_t* rkA, const SItem* __restrict__ tB,
+                                                     int32_t* rkB) {
+  __shared__ SItem sb[kSortTile];
+  const int x = blockIdx.x, b = blockIdx.y;
+  if (x < ntiles) {
+    if (x != b) merge_pair<KA>(tA, rkA, x, b, sb);
+  } else if (x - ntiles != b) {
+    merge_pair<KB>(tB, rkB, x - ntiles, b, sb);
+  }
+}
+
+// final positions of both sorts' items; only real items (rank < M) are written
+__global__ void k_scatter_items(int M, int n, const SItem* __restrict__ tA,
+                                const int32_t* __restrict__ rkA, SItem* outA,
+                                const SItem* __restrict__ tB, const int32_t* __restrict__ rkB,
+                                SItem* outB) {
   int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p < n) {
-    const int r = merged_rank<KA>(tA, ntiles, p);
+    const int r = rkA[p];
     if (r < M) outA[r] = tA[p];
   } else if (tB && p < 2 * n) {
     p -= n;
-    const int r = merged_rank<KB>(tB, ntiles, p);
+    const int r = rkB[p];
     if (r < M) outB[r] = tB[p];
   }
 }
@@ -938,7 +957,7 @@ int plan_scratch_alloc(sp_table* t) {
   SP_CUDA(cudaMalloc(&t->order, sizeof(int32_t) * M));
   {  // sort scratch: two tile buffers + two merged buffers of SItem
     const size_t n = (size_t)((M + kSortTile - 1) / kSortTile) * kSortTile;
-    t->sort_tmp_bytes = 4 * n * sizeof(SItem);
+    t->sort_tmp_bytes = 4 * n * sizeof(SItem) + 2 * n * sizeof(int32_t);
     SP_CUDA(cudaMalloc(&t->sort_tmp, t->sort_tmp_bytes));
   }
   if (t->plan_ok) {
@@ -988,25 +1007,37 @@ static int plan_enqueue(sp_ctx* ctx, sp_table* t, Plan& p) {
   SP_CUDA(cudaMemsetAsync(t->cands, 0, sizeof(uint32_t) * M, st));
   const int nb = (M + 255) / 256;
   const int ntiles = (M + kSortTile - 1) / kSortTile;
-  const int nmerge = (2 * ntiles * kSortTile + 255) / 256;
+  const int nall = ntiles * kSortTile;
   SItem* tA = reinterpret_cast<SItem*>(t->sort_tmp);           // tiles of sort A
-  SItem* tB = tA + (size_t)ntiles * kSortTile;                  // tiles of sort B
-  SItem* oA = tB + (size_t)ntiles * kSortTile;                  // merged A
-  SItem* oB = oA + (size_t)ntiles * kSortTile;                  // merged B
-  // (cost, index) and (kind, lat, index) tile sorts + merges
+  SItem* tB = tA + (size_t)nall;                                // tiles of sort B
+  SItem* oA = tB + (size_t)nall;                                // merged A
+  SItem* oB = oA + (size_t)nall;                                // merged B
+  int32_t* rkA = reinterpret_cast<int32_t*>(oB + (size_t)nall);  // ranks A / B
+  int32_t* rkB = rkA + nall;
+  // (cost, index) and (kind, lat, index) tile sorts + pairwise merges
   k_tile_sort<kSortR1, kSortOrder><<<2 * ntiles, kSortThreads, 0, st>>>(
-      M, ntiles, p.cost, nullptr, tA, t->lat, t->kind, tB);
+      M, ntiles, p.cost, nullptr, tA, rkA, t->lat, t->kind, tB, rkB);
   SP_CHECK_LAUNCH(ctx);
-  k_merge_rank<kSortR1, kSortOrder><<<nmerge, 256, 0, st>>>(M, ntiles, tA, oA, tB, oB);
+  if (ntiles > 1) {
+    k_merge_pairs<kSortR1, kSortOrder><<<dim3(2 * ntiles, ntiles), 256, 0, st>>>(ntiles, tA, rkA,
+                                                                             tB, rkB);
+    SP_CHECK_LAUNCH(ctx);
+  }
+  k_scatter_items<<<(2 * nall + 255) / 256, 256, 0, st>>>(M, nall, tA, rkA, oA, tB, rkB, oB);
   SP_CHECK_LAUNCH(ctx);
   k_rank_r1<<<nb, 256, 0, st>>>(M, oA, t->res, t->id_rank, t->r1, t->ent_r1);
   SP_CHECK_LAUNCH(ctx);
   // (costpen, r1): items at r1 positions
-  k_tile_sort<kSortR2, kSortR2><<<ntiles, kSortThreads, 0, st>>>(M, ntiles, p.costpen, t->ent_r1,
-                                                                 tA, nullptr, nullptr, nullptr);
+  k_tile_sort<kSortR2, kSortR2><<<ntiles, kSortThreads, 0, st>>>(
+      M, ntiles, p.costpen, t->ent_r1, tA, rkA, nullptr, nullptr, nullptr, nullptr);
   SP_CHECK_LAUNCH(ctx);
-  k_merge_rank<kSortR2, kSortR2><<<(ntiles * kSortTile + 255) / 256, 256, 0, st>>>(
-      M, ntiles, tA, oA, nullptr, nullptr);
+  if (ntiles > 1) {
+    k_merge_pairs<kSortR2, kSortR2><<<dim3(ntiles, ntiles), 256, 0, st>>>(ntiles, tA, rkA,
+                                                                         nullptr, nullptr);
+    SP_CHECK_LAUNCH(ctx);
+  }
+  k_scatter_items<<<(nall + 255) / 256, 256, 0, st>>>(M, nall, tA, rkA, oA, nullptr, nullptr,
+                                                       nullptr);
   SP_CHECK_LAUNCH(ctx);
   k_orders_out<<<nb, 256, 0, st>>>(M, oA, t->ent_r1, t->ent_r2, t->r2, oB, t->order);
   SP_CHECK_LAUNCH(ctx);
