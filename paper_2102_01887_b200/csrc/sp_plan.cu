@@ -683,119 +683,87 @@ __device__ __forceinline__ bool key_lt(double sa, uint32_t ra, double sb, uint32
   return sa < sb || (sa == sb && ra < rb);
 }
 
-// Single CTA: candidate compaction, unified (score, r1) ids, offsets, header, thresholds,
-// buckets, rows, records, batch lookup table.
-__global__ void __launch_bounds__(1024) k_finalize(
-    int M, int K, int W, int nB, KindInfo ki, const int32_t* __restrict__ rows_per_kind,
-    const double* __restrict__ thrscratch, const uint32_t* __restrict__ rowscratch,
-    const uint32_t* __restrict__ candf, const uint32_t* __restrict__ cands, uint32_t* cidf,
-    uint32_t* cids, const int32_t* __restrict__ ent_r1, const int32_t* __restrict__ ent_r2,
-    const uint32_t* __restrict__ r1, const double* __restrict__ lat,
-    const double* __restrict__ cost, const double* __restrict__ costpen,
-    const int32_t* __restrict__ batch, const int32_t* __restrict__ kind, double* ukey,
-    uint32_t* ukr, int32_t* uent, uint32_t* umap, PlanHdr hdr_in, uint8_t* image,
-    int64_t image_cap, int32_t* status) {
+// Plan finalisation, four kernels (multi-CTA where the work is parallel):
+//   k_fin_head   one CTA: order-preserving compaction of the two candidate sets (cidf / cids),
+//                then the header (section offsets, per-kind bucket geometry) written to the
+//                image — or an invalid magic when the image would not fit
+//   k_fin_keys   per candidate its (score, r1) key: CP[c] (feasible side) in r1 order, CS[c]
+//                (penalized side) in r2 order; both lists ascend in (score, r1)
+//   k_fin_merge  unified ids: own position + #keys of the other list before it
+//   k_fin_fill   lane lookup table, thresholds, staircase rows, buckets, candidate records
+__global__ void __launch_bounds__(1024) k_fin_head(
+    int M, int K, int nB, KindInfo ki, const int32_t* __restrict__ rows_per_kind,
+    const double* __restrict__ thrscratch, const uint32_t* __restrict__ candf,
+    const uint32_t* __restrict__ cands, uint32_t* cidf, uint32_t* cids, PlanHdr hdr_in,
+    uint8_t* image, int64_t image_cap, int32_t* status) {
   __shared__ int s_warp[32];
   __shared__ PlanHdr hdr;
   __shared__ int s_ncp, s_ncs;
-  // 1. order-preserving compaction of the two candidate sets
-  //    (each thread a contiguous run of flags, all loads in flight, one block scan per set)
   {
+    // flags staged into shared memory with coalesced loads, then each thread scans a contiguous
+    // run of them (one block scan per set); ids written back coalesced from shared memory
+    extern __shared__ uint8_t s_fl[];  // [M] feasible flags, [M] penalized flags
+    uint16_t* s_id = reinterpret_cast<uint16_t*>(s_fl + ((2 * M + 15) & ~15));  // [2][M] ids
+    for (int r = threadIdx.x; r < M; r += blockDim.x) {
+      s_fl[r] = candf[r] != 0;
+      s_fl[M + r] = cands[r] != 0;
+    }
+    __syncthreads();
     const int T = blockDim.x;
     const int P = (M + T - 1) / T;
     const int r0 = min((int)threadIdx.x * P, M), r1e = min(r0 + P, M);
     int nf = 0, ns = 0;
     for (int r = r0; r < r1e; ++r) {
-      nf += candf[r] != 0;
-      ns += cands[r] != 0;
+      nf += s_fl[r];
+      ns += s_fl[M + r];
     }
     int tf = 0, ts = 0;
     int cf = block_excl_sum(nf, s_warp, &tf);
     int cs = block_excl_sum(ns, s_warp, &ts);
     for (int r = r0; r < r1e; ++r) {
-      cidf[r] = (uint32_t)cf;
-      cids[r] = (uint32_t)cs;
-      cf += candf[r] != 0;
-      cs += cands[r] != 0;
+      s_id[r] = (uint16_t)cf;
+      s_id[M + r] = (uint16_t)cs;
+      cf += s_fl[r];
+      cs += s_fl[M + r];
     }
     if (threadIdx.x == 0) {
       s_ncp = tf;
       s_ncs = ts;
     }
     __syncthreads();
+    for (int r = threadIdx.x; r < M; r += blockDim.x) {
+      cidf[r] = s_id[r];
+      cids[r] = s_id[M + r];
+    }
   }
   const int ncp = s_ncp, ncs = s_ncs;
-  // 2. candidate keys: CP[c] (feasible side) sorted by r1, CS[c] (penalized) sorted by r2;
-  //    both lists are ascending in their (score, r1) key.
-  //    (four rows per thread per step so the dependent loads of different rows overlap)
-  for (int r0 = threadIdx.x; r0 < M; r0 += 4 * blockDim.x) {
-    uint32_t fa[4], fs[4];
-    int ea[4], es[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int r = r0 + u * blockDim.x;
-      fa[u] = r < M ? candf[r] : 0u;
-      fs[u] = r < M ? cands[r] : 0u;
-      ea[u] = (r < M && fa[u]) ? ent_r1[r] : 0;
-      es[u] = (r < M && fs[u]) ? ent_r2[r] : 0;
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int r = r0 + u * blockDim.x;
-      if (fa[u]) {
-        const int c = (int)cidf[r];
-        ukey[c] = cost[ea[u]];
-        ukr[c] = (uint32_t)r;
-        uent[c] = ea[u];
+  // per-kind bucket geometry in parallel (one thread per kind), offsets by thread 0
+  __shared__ KindDesc s_kd[kMaxKinds];
+  if (threadIdx.x < kMaxKinds) {
+    const int k = threadIdx.x;
+    KindDesc d;
+    memset(&d, 0, sizeof(d));
+    const int R = k < K ? rows_per_kind[k] : 0;
+    d.R = R;
+    if (R > 0) {
+      const int ext = ki.base[k] + k;
+      int nbk = 1, shift = 0;
+      uint32_t kmin = 0;
+      if (R >= 2) {
+        // positive thresholds: the high word of the encoding is monotone
+        const double t1 = thrscratch[ext + 1];
+        kmin = (uint32_t)__double2hiint(t1);
+        const uint32_t kmax = (uint32_t)__double2hiint(thrscratch[ext + R - 1]);
+        while (nbk < 2 * (R - 1) && nbk < kMaxBuckets) nbk <<= 1;
+        while (((kmax - kmin) >> shift) >= (uint32_t)nbk) ++shift;
+        d.pad[0] = !(t1 > 0.0);  // non-positive latency: generic search
       }
-      if (fs[u]) {
-        const int c = ncp + (int)cids[r];
-        ukey[c] = costpen[es[u]];
-        ukr[c] = r1[es[u]];
-        uent[c] = es[u];
-      }
+      d.kmin_hi = kmin;
+      d.nb1_shift = (uint32_t)(nbk - 1) | ((uint32_t)shift << 16);
     }
+    s_kd[k] = d;
   }
   __syncthreads();
-  // 3. merge ranks: uid = own position + #keys of the other list before it (ties, which
-  //    only occur for the two sides of one entry when the penalty is 0, put CP first);
-  //    four binary searches per thread advance in lockstep
-  for (int c0 = threadIdx.x; c0 < ncp + ncs; c0 += 4 * blockDim.x) {
-    int lo[4], hi[4], bse[4];
-    double sk[4];
-    uint32_t rk[4];
-    bool cp[4], ok[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int c = c0 + u * blockDim.x;
-      ok[u] = c < ncp + ncs;
-      cp[u] = c < ncp;
-      sk[u] = ok[u] ? ukey[c] : 0.0;
-      rk[u] = ok[u] ? ukr[c] : 0u;
-      lo[u] = cp[u] ? ncp : 0;
-      hi[u] = ok[u] ? (cp[u] ? ncp + ncs : ncp) : 0;
-      bse[u] = lo[u];
-    }
-    for (;;) {
-      bool any = false;
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        if (lo[u] < hi[u]) {
-          any = true;
-          const int mid = (lo[u] + hi[u]) >> 1;
-          const bool before = cp[u] ? key_lt(ukey[mid], ukr[mid], sk[u], rk[u])
-                                    : !key_lt(sk[u], rk[u], ukey[mid], ukr[mid]);
-          if (before) lo[u] = mid + 1; else hi[u] = mid;
-        }
-      }
-      if (!any) break;
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int c = c0 + u * blockDim.x;
-      if (ok[u]) umap[c] = (uint32_t)((cp[u] ? c : c - ncp) + (lo[u] - bse[u]));
-    }
-  }
   if (threadIdx.x == 0) {
     hdr = hdr_in;
     hdr.row_stride = ((nB * (nB + 1) + 3) / 4) * 4;  // nB(nB+1)/2 u16, 4-byte aligned
@@ -807,30 +775,15 @@ __global__ void __launch_bounds__(1024) k_finalize(
     hdr.lut_off = off;
     off += ((hdr.lut_n * 2 + 15) / 16) * 16;
     for (int k = 0; k < kMaxKinds; ++k) {
-      KindDesc d;
-      memset(&d, 0, sizeof(d));
-      const int R = k < K ? rows_per_kind[k] : 0;
-      d.R = R;
+      KindDesc d = s_kd[k];
+      const int R = d.R;
       if (R > 0) {
-        const int ext = ki.base[k] + k;
         d.thr_off = off;
         off += ((R * 8 + 15) / 16) * 16;
         d.rows_off = off;
         off += ((R * hdr.row_stride + 15) / 16) * 16;
-        int nbk = 1, shift = 0;
-        uint32_t kmin = 0;
-        if (R >= 2) {
-          // positive thresholds: the high word of the encoding is monotone
-          kmin = (uint32_t)__double2hiint(thrscratch[ext + 1]);
-          const uint32_t kmax = (uint32_t)__double2hiint(thrscratch[ext + R - 1]);
-          while (nbk < 2 * (R - 1) && nbk < kMaxBuckets) nbk <<= 1;
-          while (((kmax - kmin) >> shift) >= (uint32_t)nbk) ++shift;
-          d.pad[0] = !(thrscratch[ext + 1] > 0.0);  // non-positive latency: generic search
-        }
-        d.kmin_hi = kmin;
         d.bkt_off = off;
-        d.nb1_shift = (uint32_t)(nbk - 1) | ((uint32_t)shift << 16);
-        off += ((nbk * 4 + 15) / 16) * 16;
+        off += (((int)(d.nb1_shift & 0xFFFFu) + 1) * 4 + 15) / 16 * 16;
       }
       hdr.kd[k] = d;
     }
@@ -843,38 +796,96 @@ __global__ void __launch_bounds__(1024) k_finalize(
     hdr.recb_off = off;
     off += (((ncp + ncs) * (int)sizeof(CandB) + 15) / 16) * 16;
     hdr.total_bytes = off;
-    *status = (off <= image_cap && ncp + ncs < (int)kNone16) ? 0 : -1;
+    const bool ok = off <= image_cap && ncp + ncs < (int)kNone16;
+    *status = ok ? 0 : -1;
+    if (!ok) hdr.magic = 0;  // invalid image: every later stage and every reader stops
   }
   __syncthreads();
-  if (hdr.total_bytes > image_cap || ncp + ncs >= (int)kNone16) {
-    if (threadIdx.x == 0) reinterpret_cast<uint32_t*>(image)[0] = 0;  // invalid magic
-    return;
-  }
   if (threadIdx.x < (int)(sizeof(PlanHdr) / 4))
     reinterpret_cast<uint32_t*>(image)[threadIdx.x] =
         reinterpret_cast<const uint32_t*>(&hdr)[threadIdx.x];
-  {
-    uint16_t* lut = reinterpret_cast<uint16_t*>(image + hdr.lut_off);
-    for (int v = threadIdx.x; v < hdr.lut_n; v += blockDim.x) {
+}
+
+__global__ void k_fin_keys(int M, const uint8_t* __restrict__ image,
+                           const uint32_t* __restrict__ candf, const uint32_t* __restrict__ cands,
+                           const uint32_t* __restrict__ cidf, const uint32_t* __restrict__ cids,
+                           const int32_t* __restrict__ ent_r1, const int32_t* __restrict__ ent_r2,
+                           const uint32_t* __restrict__ r1, const double* __restrict__ cost,
+                           const double* __restrict__ costpen, double* ukey, uint32_t* ukr,
+                           int32_t* uent) {
+  const PlanHdr* H = reinterpret_cast<const PlanHdr*>(image);
+  if (H->magic != kPlanMagic) return;
+  const int ncp = H->ncp;
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= M) return;
+  if (candf[r]) {
+    const int c = (int)cidf[r], e = ent_r1[r];
+    ukey[c] = cost[e];
+    ukr[c] = (uint32_t)r;
+    uent[c] = e;
+  }
+  if (cands[r]) {
+    const int c = ncp + (int)cids[r], e = ent_r2[r];
+    ukey[c] = costpen[e];
+    ukr[c] = r1[e];
+    uent[c] = e;
+  }
+}
+
+// ties (which only occur for the two sides of one entry when the penalty is 0) put CP first
+__global__ void k_fin_merge(const uint8_t* __restrict__ image, const double* __restrict__ ukey,
+                            const uint32_t* __restrict__ ukr, uint32_t* umap) {
+  const PlanHdr* H = reinterpret_cast<const PlanHdr*>(image);
+  if (H->magic != kPlanMagic) return;
+  const int ncp = H->ncp, ncs = H->ncs;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ncp + ncs) return;
+  const bool is_cp = c < ncp;
+  const double s = ukey[c];
+  const uint32_t rr = ukr[c];
+  int lo = is_cp ? ncp : 0, hi = is_cp ? ncp + ncs : ncp;
+  const int base = lo;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    const bool before = is_cp ? key_lt(ukey[mid], ukr[mid], s, rr)
+                              : !key_lt(s, rr, ukey[mid], ukr[mid]);
+    if (before) lo = mid + 1; else hi = mid;
+  }
+  umap[c] = (uint32_t)((is_cp ? c : c - ncp) + (lo - base));
+}
+
+__global__ void k_fin_fill(int K, int W, KindInfo ki, const double* __restrict__ thrscratch,
+                           const uint32_t* __restrict__ rowscratch,
+                           const uint32_t* __restrict__ cidf, const uint32_t* __restrict__ cids,
+                           const double* __restrict__ ukey, const int32_t* __restrict__ uent,
+                           const uint32_t* __restrict__ umap, const double* __restrict__ lat,
+                           const int32_t* __restrict__ batch, const int32_t* __restrict__ kind,
+                           uint8_t* image) {
+  const PlanHdr* H = reinterpret_cast<const PlanHdr*>(image);
+  if (H->magic != kPlanMagic) return;
+  const int g = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
+  const int nB = H->nB, ncp = H->ncp, ncand = H->ncp + H->ncs;
+  {  // batch lookup table of the generic kernels
+    uint16_t* lut = reinterpret_cast<uint16_t*>(image + H->lut_off);
+    for (int v = g; v < H->lut_n; v += gs) {
       int lo = 0, le = 0;
       for (int b = 0; b < nB; ++b) {
-        lo += hdr.batch_vals[b] < v;
-        le += hdr.batch_vals[b] <= v;
+        lo += H->batch_vals[b] < v;
+        le += H->batch_vals[b] <= v;
       }
       lut[v] = (uint16_t)(lo | (le << 8));
     }
   }
   for (int k = 0; k < K; ++k) {
-    const KindDesc d = hdr.kd[k];
+    const KindDesc d = H->kd[k];
     const int R = d.R;
     if (R == 0) continue;
     const int ext = ki.base[k] + k;
     double* thr = reinterpret_cast<double*>(image + d.thr_off);
-    uint16_t* rows = reinterpret_cast<uint16_t*>(image + d.rows_off);
-    for (int r = threadIdx.x; r < R; r += blockDim.x) thr[r] = thrscratch[ext + r];
+    for (int r = g; r < R; r += gs) thr[r] = thrscratch[ext + r];
     // row r: lane b = min(unified id of the best feasible, of the best penalized entry with
     // batch size batch_vals[b]); stored as the minimum over every lane interval [lo, hi]
-    for (int r = threadIdx.x; r < R; r += blockDim.x) {
+    for (int r = g; r < R; r += gs) {
       uint32_t lane[kMaxB];
       for (int b = 0; b < nB; ++b) {
         const uint32_t a = rowscratch[(size_t)(ext + r) * (2 * W) + b];
@@ -883,8 +894,7 @@ __global__ void __launch_bounds__(1024) k_finalize(
         const uint32_t us = s != kInf32 ? umap[ncp + cids[s]] : kInf32;
         lane[b] = min(ua, us);
       }
-      uint16_t* out = reinterpret_cast<uint16_t*>(reinterpret_cast<uint8_t*>(rows) +
-                                                  (size_t)r * hdr.row_stride);
+      uint16_t* out = reinterpret_cast<uint16_t*>(image + d.rows_off + (size_t)r * H->row_stride);
       int q = 0;
       for (int lo = 0; lo < nB; ++lo) {
         uint32_t m = kInf32;
@@ -895,31 +905,37 @@ __global__ void __launch_bounds__(1024) k_finalize(
       }
     }
     // bucket b holds thresholds j in [1, R) with (key_j - kmin) >> shift == b:
-    // entry = (#thresholds in lower buckets) | (#thresholds in b) << 16
+    // entry = (#thresholds in lower buckets) | (#thresholds in b) << 16.  Thresholds ascend, so
+    // threshold j (or the end sentinel j = R) fills every bucket from just after the previous
+    // threshold's bucket up to its own: no search per bucket.
     uint32_t* bkt = reinterpret_cast<uint32_t*>(image + d.bkt_off);
     const int nbk = (int)(d.nb1_shift & 0xFFFFu) + 1, shift = (int)(d.nb1_shift >> 16);
     const uint32_t kmin = d.kmin_hi;
-    for (int b = threadIdx.x; b < nbk; b += blockDim.x) {
-      int below[2] = {0, 0};
-      if (R >= 2) {
-        for (int q = 0; q < 2; ++q) {
-          const uint32_t bb = (uint32_t)b + q;
-          int lo = 1, hi = R;
-          while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            const uint32_t kk = (uint32_t)__double2hiint(thrscratch[ext + mid]);
-            if (((kk - kmin) >> shift) < bb) lo = mid + 1; else hi = mid;
-          }
-          below[q] = lo - 1;
-        }
+    if (R < 2) {
+      for (int b = g; b < nbk; b += gs) bkt[b] = 0u;
+      continue;
+    }
+    auto bucket_of = [&](int j) -> int {
+      const uint32_t kk = (uint32_t)__double2hiint(thrscratch[ext + j]);
+      return (int)min((kk - kmin) >> shift, (uint32_t)(nbk - 1));
+    };
+    for (int j = 1 + g; j <= R; j += gs) {
+      const int bp = j == 1 ? -1 : bucket_of(j - 1);
+      const int bj = j == R ? nbk : bucket_of(j);
+      if (bj == bp) continue;  // j shares its bucket with j - 1
+      int cnt = 0;            // thresholds in bucket bj, starting at j
+      if (j < R) {
+        cnt = 1;
+        while (j + cnt < R && bucket_of(j + cnt) == bj) ++cnt;
       }
-      bkt[b] = (uint32_t)below[0] | ((uint32_t)(below[1] - below[0]) << 16);
+      for (int b = bp + 1; b < bj && b < nbk; ++b) bkt[b] = (uint32_t)(j - 1);  // empty buckets
+      if (bj < nbk) bkt[bj] = (uint32_t)(j - 1) | ((uint32_t)cnt << 16);
     }
   }
-  double* rscore = reinterpret_cast<double*>(image + hdr.score_off);
-  double* rlat = reinterpret_cast<double*>(image + hdr.lat_off);
-  CandB* recb = reinterpret_cast<CandB*>(image + hdr.recb_off);
-  for (int c = threadIdx.x; c < ncp + ncs; c += blockDim.x) {
+  double* rscore = reinterpret_cast<double*>(image + H->score_off);
+  double* rlat = reinterpret_cast<double*>(image + H->lat_off);
+  CandB* recb = reinterpret_cast<CandB*>(image + H->recb_off);
+  for (int c = g; c < ncand; c += gs) {
     const int e = uent[c];
     const uint32_t u = umap[c];
     rscore[u] = ukey[c];
@@ -1069,11 +1085,23 @@ static int plan_enqueue(sp_ctx* ctx, sp_table* t, Plan& p) {
   h.K = K;
   for (int b = 0; b < kMaxB; ++b) h.batch_vals[b] = b < t->nB ? t->batch_vals[b] : INT32_MAX;
   int32_t* status = t->rows_per_kind + kMaxKinds;
-  k_finalize<<<1, 1024, 0, st>>>(M, K, W, t->nB, ki, t->rows_per_kind, t->thrscratch,
-                                 t->rowscratch, t->candf, t->cands, t->cidf, t->cids,
-                                 t->ent_r1, t->ent_r2, t->r1, t->lat, p.cost, p.costpen,
-                                 t->batch, t->kind, t->ukey, t->ukr, t->uent, t->umap, h,
-                                 p.image, p.image_cap, status);
+  static bool fin_attr = false;
+  if (!fin_attr) {
+    SP_CUDA(cudaFuncSetAttribute(k_fin_head, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 6 * 32768 + 16));
+    fin_attr = true;
+  }
+  k_fin_head<<<1, 1024, ((2 * M + 15) & ~15) + 4 * M, st>>>(M, K, t->nB, ki, t->rows_per_kind, t->thrscratch, t->candf,
+                                 t->cands, t->cidf, t->cids, h, p.image, p.image_cap, status);
+  SP_CHECK_LAUNCH(ctx);
+  k_fin_keys<<<nb, 256, 0, st>>>(M, p.image, t->candf, t->cands, t->cidf, t->cids, t->ent_r1,
+                                 t->ent_r2, t->r1, p.cost, p.costpen, t->ukey, t->ukr, t->uent);
+  SP_CHECK_LAUNCH(ctx);
+  k_fin_merge<<<(2 * M + 255) / 256, 256, 0, st>>>(p.image, t->ukey, t->ukr, t->umap);
+  SP_CHECK_LAUNCH(ctx);
+  k_fin_fill<<<std::min(ctx->num_sms * 4, std::max(1, (2 * M + 255) / 256)), 256, 0, st>>>(
+      K, W, ki, t->thrscratch, t->rowscratch, t->cidf, t->cids, t->ukey, t->uent, t->umap, t->lat,
+      t->batch, t->kind, p.image);
   SP_CHECK_LAUNCH(ctx);
   ctx->plan_dirty = true;
   // fetch the header back without blocking; it becomes a kernel parameter once it lands
