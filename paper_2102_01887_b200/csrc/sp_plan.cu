@@ -678,6 +678,346 @@ __global__ void __launch_bounds__(1024) k_stair_smem(int M, int K, int W, KindIn
   if (t == 0) rows_per_kind[k] = total;
 }
 
+// ---- k_stair_lanes: the staircase by per-lane segmented scans (kinds of <= 8192 entries) ---
+// Same output as k_stair.  The kind's positions are bucketed by batch lane (a stable counting
+// sort inside the CTA), so each lane's prefix minimum of r1 and suffix minimum of r2 is a
+// segmented scan over that lane's own positions only — one block-wide scan per direction for
+// all lanes together instead of one scan of every position per lane.  "Improving" positions
+// (strictly below their lane's running minimum) flag the latency groups whose boundary starts
+// a new row (see k_stair_smem); a row's lane values are read from the scanned lane lists at
+// (#lane positions before the boundary).
+constexpr int kStairLanesMax = 8192;
+
+// exclusive block scan of NW packed u32 words (two 16-bit counters each)
+template <int NW>
+__device__ __forceinline__ void block_excl_sum_vec(uint32_t (&v)[NW], uint32_t (&tot)[NW],
+                                                   uint32_t* s_w /* 32 * NW */) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  uint32_t x[NW];
+#pragma unroll
+  for (int q = 0; q < NW; ++q) {
+    x[q] = v[q];
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x[q], off);
+      if (lane >= off) x[q] += y;
+    }
+    if (lane == 31) s_w[w * NW + q] = x[q];
+  }
+  __syncthreads();
+  if (w == 0) {
+#pragma unroll
+    for (int q = 0; q < NW; ++q) {
+      uint32_t y = lane < nw ? s_w[lane * NW + q] : 0u;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t z = __shfl_up_sync(0xffffffffu, y, off);
+        if (lane >= off) y += z;
+      }
+      s_w[lane * NW + q] = y;  // inclusive over warps
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < NW; ++q) {
+    const uint32_t base = w ? s_w[(w - 1) * NW + q] : 0u;
+    tot[q] = s_w[(nw - 1) * NW + q];
+    v[q] = base + x[q] - v[q];
+  }
+  __syncthreads();
+}
+
+// segmented scan operator on (segment, value): the running minimum restarts at a new segment
+struct SegMin {
+  uint32_t seg, val;
+};
+__device__ __forceinline__ SegMin seg_combine(SegMin a, SegMin b) {
+  SegMin r;
+  r.seg = b.seg;
+  r.val = a.seg == b.seg ? min(a.val, b.val) : b.val;
+  return r;
+}
+// exclusive block scan with SegMin; threads in order of `rank` (0..T-1)
+__device__ __forceinline__ SegMin block_excl_segmin(SegMin v, int rank, uint32_t* s_seg,
+                                                    uint32_t* s_val) {
+  const int lane = rank & 31, w = rank >> 5, nw = blockDim.x >> 5;
+  // warp shuffles follow the hardware lane order; `rank` is threadIdx.x or its mirror, so
+  // warp membership is preserved and the lane order inside a warp is either kept or reversed
+  const bool mirror = rank != (int)threadIdx.x;
+  SegMin x = v;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    SegMin y;
+    y.seg = mirror ? __shfl_down_sync(0xffffffffu, x.seg, off) : __shfl_up_sync(0xffffffffu, x.seg, off);
+    y.val = mirror ? __shfl_down_sync(0xffffffffu, x.val, off) : __shfl_up_sync(0xffffffffu, x.val, off);
+    if (lane >= off) x = seg_combine(y, x);
+  }
+  if (lane == 31) {
+    s_seg[w] = x.seg;
+    s_val[w] = x.val;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int l = threadIdx.x;
+    SegMin y;
+    y.seg = l < nw ? s_seg[l] : 0xFFFFFFFFu;
+    y.val = l < nw ? s_val[l] : kInf32;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      SegMin z;
+      z.seg = __shfl_up_sync(0xffffffffu, y.seg, off);
+      z.val = __shfl_up_sync(0xffffffffu, y.val, off);
+      if (l >= off) y = seg_combine(z, y);
+    }
+    __syncwarp();
+    s_seg[32 + l] = y.seg;  // inclusive over warps (in rank order)
+    s_val[32 + l] = y.val;
+  }
+  __syncthreads();
+  // exclusive: the inclusive value of the previous rank
+  SegMin prev;
+  SegMin xin;
+  xin.seg = mirror ? __shfl_down_sync(0xffffffffu, x.seg, 1) : __shfl_up_sync(0xffffffffu, x.seg, 1);
+  xin.val = mirror ? __shfl_down_sync(0xffffffffu, x.val, 1) : __shfl_up_sync(0xffffffffu, x.val, 1);
+  if (lane == 0) {
+    if (w == 0) {
+      prev.seg = 0xFFFFFFFFu;
+      prev.val = kInf32;
+    } else {
+      prev.seg = s_seg[32 + w - 1];
+      prev.val = s_val[32 + w - 1];
+    }
+  } else {
+    prev = xin;
+    if (w > 0) {
+      SegMin carry;
+      carry.seg = s_seg[32 + w - 1];
+      carry.val = s_val[32 + w - 1];
+      prev = seg_combine(carry, prev);
+    }
+  }
+  __syncthreads();
+  return prev;
+}
+
+template <int NWW>  // NWW = W / 2 packed words (W = 8 -> 4, W = 16 -> 8)
+__global__ void __launch_bounds__(1024) k_stair_lanes(int M, int K, int W, KindInfo ki,
+                                                      const int32_t* __restrict__ order,
+                                                      const int32_t* __restrict__ bidx,
+                                                      const double* __restrict__ lat,
+                                                      const uint32_t* __restrict__ r1,
+                                                      const uint32_t* __restrict__ r2,
+                                                      double* thrscratch, uint32_t* rowscratch,
+                                                      int32_t* rows_per_kind, uint32_t* candf,
+                                                      uint32_t* cands) {
+  constexpr int WM = 2 * NWW;  // lanes held in registers
+  extern __shared__ __align__(16) uint8_t s_l[];
+  __shared__ int s_warp[32];
+  __shared__ uint32_t s_w[32 * NWW], s_seg[64], s_val[64];
+  __shared__ int s_start[WM + 1];
+  const int k = blockIdx.x;
+  const int Mk = ki.count[k];
+  const int base = ki.base[k];
+  const int ext = base + k;
+  if (Mk == 0) {
+    if (threadIdx.x == 0) rows_per_kind[k] = 0;
+    return;
+  }
+  const int T = blockDim.x, t = threadIdx.x;
+  constexpr int C = kStairLanesMax;
+  uint32_t* pr1 = reinterpret_cast<uint32_t*>(s_l);  // position order (reused as scnt later)
+  uint32_t* pr2 = pr1 + C;
+  uint32_t* L1 = pr2 + C;       // lane order: r1, then the inclusive prefix minimum
+  uint32_t* L2 = L1 + C;        // lane order: r2, then the inclusive suffix minimum
+  uint16_t* Lpos = reinterpret_cast<uint16_t*>(L2 + C);
+  uint8_t* plane = reinterpret_cast<uint8_t*>(Lpos + C);
+  uint8_t* Llane = plane + C;
+  uint8_t* sisb = Llane + C;    // lat[q] != lat[q - 1]
+  uint8_t* impP = sisb + C;
+  uint8_t* impS = impP + C;
+  uint16_t* scnt = reinterpret_cast<uint16_t*>(pr1);  // #flags before p (after the scatter)
+  // ---- 1. stage (coalesced) ----
+  for (int q0 = t; q0 < Mk; q0 += 4 * T) {
+    int e[4], e1[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int q = q0 + u * T;
+      e[u] = q < Mk ? order[base + q] : 0;
+      e1[u] = (q < Mk && q > 0) ? order[base + q - 1] : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int q = q0 + u * T;
+      if (q < Mk) {
+        plane[q] = (uint8_t)bidx[e[u]];
+        pr1[q] = r1[e[u]];
+        pr2[q] = r2[e[u]];
+        sisb[q] = q > 0 && lat[e[u]] != lat[e1[u]];
+      }
+    }
+  }
+  __syncthreads();
+  // ---- 2. per-thread chunk lane counts, block scan -> lane list offsets ----
+  const int n = Mk + 1;  // boundaries 0..Mk; positions 0..Mk-1
+  const int P = (n + T - 1) / T;
+  const int p0 = min(t * P, n), p1 = min(p0 + P, n);
+  uint32_t cw[NWW], tw[NWW];
+#pragma unroll
+  for (int q = 0; q < NWW; ++q) cw[q] = 0u;
+  for (int p = p0; p < min(p1, Mk); ++p) {
+    const int l = plane[p];
+#pragma unroll
+    for (int q = 0; q < NWW; ++q) cw[q] += (l == 2 * q ? 1u : 0u) | (l == 2 * q + 1 ? 0x10000u : 0u);
+  }
+  block_excl_sum_vec<NWW>(cw, tw, s_w);
+  if (t == 0) {
+    int acc = 0;
+    for (int b = 0; b < WM; ++b) {
+      s_start[b] = acc;
+      acc += (int)((tw[b >> 1] >> (16 * (b & 1))) & 0xFFFFu);
+    }
+    s_start[WM] = acc;
+  }
+  __syncthreads();
+  uint32_t before[WM];  // #lane-b positions before this thread's chunk
+#pragma unroll
+  for (int b = 0; b < WM; ++b) before[b] = (cw[b >> 1] >> (16 * (b & 1))) & 0xFFFFu;
+  {  // ---- 3. stable scatter into lane order ----
+    uint32_t run[WM];
+#pragma unroll
+    for (int b = 0; b < WM; ++b) run[b] = before[b];
+    for (int p = p0; p < min(p1, Mk); ++p) {
+      const int l = plane[p];
+      uint32_t at = 0;
+#pragma unroll
+      for (int b = 0; b < WM; ++b) {
+        at = (l == b) ? (uint32_t)s_start[b] + run[b] : at;
+        run[b] += (l == b);
+      }
+      L1[at] = pr1[p];
+      L2[at] = pr2[p];
+      Lpos[at] = (uint16_t)p;
+      Llane[at] = (uint8_t)l;
+    }
+  }
+  __syncthreads();
+  // ---- 4. segmented prefix minimum of r1 (forward) and suffix minimum of r2 (backward) ----
+  const int E = (Mk + T - 1) / T;  // list elements per thread
+  const int j0 = min(t * E, Mk), j1 = min(j0 + E, Mk);
+  {
+    SegMin a;
+    a.seg = 0xFFFFFFFFu;
+    a.val = kInf32;
+    for (int j = j0; j < j1; ++j) {
+      SegMin x;
+      x.seg = Llane[j];
+      x.val = L1[j];
+      a = (a.seg == 0xFFFFFFFFu) ? x : seg_combine(a, x);
+    }
+    if (j0 >= j1) a.seg = 0xFFFFFFFEu;  // empty chunk: passes nothing on
+    SegMin c = block_excl_segmin(a, t, s_seg, s_val);
+    uint32_t rn = kInf32;
+    uint32_t sg = 0xFFFFFFFFu;
+    if (j0 < j1 && c.seg == Llane[j0]) rn = c.val;
+    for (int j = j0; j < j1; ++j) {
+      const uint32_t l = Llane[j];
+      if (l != sg && j != j0) rn = kInf32;
+      sg = l;
+      const uint32_t v = L1[j];
+      impP[Lpos[j]] = v < rn;
+      rn = min(rn, v);
+      L1[j] = rn;  // inclusive prefix minimum inside the lane
+    }
+  }
+  {
+    const int tm = T - 1 - t;  // mirrored rank: the scan runs from the end of the list
+    const int k0 = j0, k1 = j1;  // same chunk, processed backwards: k1 - 1, ..., k0
+    SegMin a;
+    a.seg = 0xFFFFFFFFu;
+    a.val = kInf32;
+    for (int j = k1 - 1; j >= k0; --j) {
+      SegMin x;
+      x.seg = Llane[j];
+      x.val = L2[j];
+      a = (a.seg == 0xFFFFFFFFu) ? x : seg_combine(a, x);
+    }
+    if (k0 >= k1) a.seg = 0xFFFFFFFEu;
+    SegMin c = block_excl_segmin(a, tm, s_seg, s_val);
+    uint32_t rn = kInf32;
+    uint32_t sg = 0xFFFFFFFFu;
+    if (k0 < k1 && c.seg == Llane[k1 - 1]) rn = c.val;
+    for (int j = k1 - 1; j >= k0; --j) {
+      const uint32_t l = Llane[j];
+      if (l != sg && j != k1 - 1) rn = kInf32;
+      sg = l;
+      const uint32_t v = L2[j];
+      impS[Lpos[j]] = v < rn;
+      rn = min(rn, v);
+      L2[j] = rn;  // inclusive suffix minimum inside the lane
+    }
+  }
+  __syncthreads();
+  // ---- 5. boundaries -> rows ----
+  int lastb = INT32_MIN, nf = 0;
+  for (int p = p0; p < p1; ++p) {
+    if (p == 0 || p == Mk || sisb[p]) lastb = p;
+    if (p < Mk) nf += (impP[p] | impS[p]) != 0;
+  }
+  int tot_f = 0;
+  int cf = block_excl_sum(nf, s_warp, &tot_f);
+  const int prevb = block_excl_max(lastb, s_warp);
+  for (int p = p0; p < p1; ++p) {
+    scnt[p] = (uint16_t)cf;
+    if (p < Mk) cf += (impP[p] | impS[p]) != 0;
+  }
+  __syncthreads();
+  uint32_t chmask = 0;
+  int cnt = 0;
+  {
+    int pp = prevb;
+    for (int p = p0; p < p1; ++p) {
+      if (!(p == 0 || p == Mk || sisb[p])) continue;
+      if ((p == 0) || scnt[p] > scnt[pp]) {
+        chmask |= 1u << (p - p0);
+        ++cnt;
+      }
+      pp = p;
+    }
+  }
+  int total = 0;
+  int row = block_excl_sum(cnt, s_warp, &total);
+  {
+    uint32_t c_b[WM];  // #lane-b positions before boundary p
+#pragma unroll
+    for (int b = 0; b < WM; ++b) c_b[b] = before[b];
+    for (int p = p0; p < p1; ++p) {
+      if ((chmask >> (p - p0)) & 1u) {
+        thrscratch[ext + row] = (p == 0) ? -INFINITY : lat[order[base + p - 1]];
+        uint32_t* rr = rowscratch + (size_t)(ext + row) * (2 * W);
+#pragma unroll
+        for (int b = 0; b < WM; ++b) {
+          if (b >= W) break;
+          const int st = s_start[b], nb = s_start[b + 1] - st;
+          const uint32_t a = c_b[b] > 0 ? L1[st + c_b[b] - 1] : kInf32;
+          const uint32_t c = (int)c_b[b] < nb ? L2[st + c_b[b]] : kInf32;
+          rr[b] = a;
+          rr[W + b] = c;
+          if (a != kInf32) candf[a] = 1u;
+          if (c != kInf32) cands[c] = 1u;
+        }
+        ++row;
+      }
+      if (p < Mk) {
+        const int l = plane[p];
+#pragma unroll
+        for (int b = 0; b < WM; ++b) c_b[b] += (l == b);
+      }
+    }
+  }
+  if (t == 0) rows_per_kind[k] = total;
+}
+constexpr int kStairLanesSmem = kStairLanesMax * (4 * 4 + 2 + 5);
+
 // (score, r1) strict order of unified candidates
 __device__ __forceinline__ bool key_lt(double sa, uint32_t ra, double sb, uint32_t rb) {
   return sa < sb || (sa == sb && ra < rb);
@@ -1067,7 +1407,26 @@ static int plan_enqueue(sp_ctx* ctx, sp_table* t, Plan& p) {
   }
   int max_mk = 0;
   for (int k = 0; k < K; ++k) max_mk = std::max(max_mk, t->kind_count[k]);
-  if (max_mk <= kStairSmemMax && !getenv("SP_STAIR_GLOBAL"))
+  static bool lanes_attr = false;
+  if (!lanes_attr) {
+    SP_CUDA(cudaFuncSetAttribute(k_stair_lanes<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kStairLanesSmem));
+    SP_CUDA(cudaFuncSetAttribute(k_stair_lanes<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kStairLanesSmem));
+    lanes_attr = true;
+  }
+  if (max_mk <= kStairLanesMax && !getenv("SP_STAIR_SMEM") && !getenv("SP_STAIR_GLOBAL")) {
+    if (W <= 8)
+      k_stair_lanes<4><<<K, 1024, kStairLanesSmem, st>>>(M, K, W, ki, t->order, t->bidx, t->lat,
+                                                         t->r1, t->r2, t->thrscratch,
+                                                         t->rowscratch, t->rows_per_kind,
+                                                         t->candf, t->cands);
+    else
+      k_stair_lanes<8><<<K, 1024, kStairLanesSmem, st>>>(M, K, W, ki, t->order, t->bidx, t->lat,
+                                                         t->r1, t->r2, t->thrscratch,
+                                                         t->rowscratch, t->rows_per_kind,
+                                                         t->candf, t->cands);
+  } else if (max_mk <= kStairSmemMax && !getenv("SP_STAIR_GLOBAL"))
     k_stair_smem<<<K, 1024, kStairSmemBytes, st>>>(M, K, W, ki, t->order, t->bidx, t->lat, t->r1,
                                                    t->r2, t->thrscratch, t->rowscratch,
                                                    t->rows_per_kind, t->candf, t->cands);
