@@ -1244,32 +1244,39 @@ __global__ void k_fin_fill(int K, int W, KindInfo ki, const double* __restrict__
         }
       }
     }
-    // bucket b holds thresholds j in [1, R) with (key_j - kmin) >> shift == b:
-    // entry = (#thresholds in lower buckets) | (#thresholds in b) << 16.  Thresholds ascend, so
-    // threshold j (or the end sentinel j = R) fills every bucket from just after the previous
-    // threshold's bucket up to its own: no search per bucket.
-    uint32_t* bkt = reinterpret_cast<uint32_t*>(image + d.bkt_off);
-    const int nbk = (int)(d.nb1_shift & 0xFFFFu) + 1, shift = (int)(d.nb1_shift >> 16);
-    const uint32_t kmin = d.kmin_hi;
-    if (R < 2) {
-      for (int b = g; b < nbk; b += gs) bkt[b] = 0u;
-      continue;
-    }
-    auto bucket_of = [&](int j) -> int {
-      const uint32_t kk = (uint32_t)__double2hiint(thrscratch[ext + j]);
-      return (int)min((kk - kmin) >> shift, (uint32_t)(nbk - 1));
-    };
-    for (int j = 1 + g; j <= R; j += gs) {
-      const int bp = j == 1 ? -1 : bucket_of(j - 1);
-      const int bj = j == R ? nbk : bucket_of(j);
-      if (bj == bp) continue;  // j shares its bucket with j - 1
-      int cnt = 0;            // thresholds in bucket bj, starting at j
-      if (j < R) {
-        cnt = 1;
-        while (j + cnt < R && bucket_of(j + cnt) == bj) ++cnt;
+  }
+  // bucket b holds thresholds j in [1, R) with (key_j - kmin) >> shift == b:
+  // entry = (#thresholds in lower buckets) | (#thresholds in b) << 16 — CTA k builds kind k's
+  // table from a shared-memory histogram and one block scan (no per-bucket searches)
+  if ((int)blockIdx.x < K) {
+    __shared__ uint32_t s_h[kMaxBuckets];
+    __shared__ int s_warp[32];
+    const int k = blockIdx.x;
+    const KindDesc d = H->kd[k];
+    const int R = d.R;
+    if (R > 0) {
+      const int ext = ki.base[k] + k;
+      uint32_t* bkt = reinterpret_cast<uint32_t*>(image + d.bkt_off);
+      const int nbk = (int)(d.nb1_shift & 0xFFFFu) + 1, shift = (int)(d.nb1_shift >> 16);
+      const uint32_t kmin = d.kmin_hi;
+      for (int b = threadIdx.x; b < nbk; b += blockDim.x) s_h[b] = 0u;
+      __syncthreads();
+      for (int j = 1 + (int)threadIdx.x; j < R; j += blockDim.x) {
+        const uint32_t kk = (uint32_t)__double2hiint(thrscratch[ext + j]);
+        atomicAdd(&s_h[min((kk - kmin) >> shift, (uint32_t)(nbk - 1))], 1u);
       }
-      for (int b = bp + 1; b < bj && b < nbk; ++b) bkt[b] = (uint32_t)(j - 1);  // empty buckets
-      if (bj < nbk) bkt[bj] = (uint32_t)(j - 1) | ((uint32_t)cnt << 16);
+      __syncthreads();
+      const int per = (nbk + blockDim.x - 1) / blockDim.x;
+      const int b0 = min((int)threadIdx.x * per, nbk), b1 = min(b0 + per, nbk);
+      int loc = 0;
+      for (int b = b0; b < b1; ++b) loc += (int)s_h[b];
+      int tot = 0;
+      int below = block_excl_sum(loc, s_warp, &tot);
+      for (int b = b0; b < b1; ++b) {
+        const uint32_t c = s_h[b];
+        bkt[b] = (uint32_t)below | (c << 16);
+        below += (int)c;
+      }
     }
   }
   double* rscore = reinterpret_cast<double*>(image + H->score_off);
@@ -1458,7 +1465,8 @@ static int plan_enqueue(sp_ctx* ctx, sp_table* t, Plan& p) {
   SP_CHECK_LAUNCH(ctx);
   k_fin_merge<<<(2 * M + 255) / 256, 256, 0, st>>>(p.image, t->ukey, t->ukr, t->umap);
   SP_CHECK_LAUNCH(ctx);
-  k_fin_fill<<<std::min(ctx->num_sms * 4, std::max(1, (2 * M + 255) / 256)), 256, 0, st>>>(
+  k_fin_fill<<<std::max(K, std::min(ctx->num_sms * 4, std::max(1, (2 * M + 255) / 256))), 256, 0,
+               st>>>(
       K, W, ki, t->thrscratch, t->rowscratch, t->cidf, t->cids, t->ukey, t->uent, t->umap, t->lat,
       t->batch, t->kind, p.image);
   SP_CHECK_LAUNCH(ctx);
