@@ -375,3 +375,34 @@ def test_pinned_host_buffers_zero_copy(gpu_ctx, N):
     assert_same_decisions(r2, exp, f"pageable N={N}")
     for t in raws:
         t.close()
+
+
+@pytest.mark.parametrize("variant", ["SP_STAIR_SMEM", "SP_STAIR_GLOBAL", "SP_NO_PLAN_GRAPH"])
+def test_staircase_builder_variants_vs_oracle(gpu_ctx, variant, monkeypatch):
+    """The fallback staircase builders (shared-memory run scans for kinds of 8,193-16,384
+    entries, the global-memory builder above that) and the un-graphed rebuild path give the same
+    plans as the default lane-scan builder: forced on ordinary tables, plus a 20,000-entry kind
+    that takes the global builder on its own."""
+    import paper_2102_01887_b200 as sp
+
+    monkeypatch.setenv(variant, "1")
+    rng = np.random.default_rng(hash(variant) & 0xFFFF)
+    for M, nB, K in ((3000, 8, 2), (1500, 16, 4), (20000, 8, 1)):
+        t = _random_table(rng, M, nB, K)
+        N = 20000
+        slack = rng.uniform(-2, 6, size=(N, K))
+        pick = rng.random((N, K)) < 0.1
+        slack[pick] = rng.choice(t.lat, size=int(pick.sum()))
+        avail = rng.integers(0, 320, size=N).astype(np.int32)
+        supply = rng.integers(0, 320, size=N).astype(np.int32)
+        mb = np.where(rng.random(N) < 0.7, 1, rng.integers(-1, 300, size=N)).astype(np.int32)
+        flags = sp.make_flags(rng.random(N) < 0.5, rng.integers(0, 1 << K, size=N) * (rng.random(N) < 0.3))
+        tab = raw_table(t, K)
+        for step in range(3):  # first build, captured rebuild, replayed rebuild
+            exp = cselect.select_batch([t], slack, 7.5, avail, supply, mb, flags)
+            r = sp.select_batch([tab], slack, 7.5, avail, upstream_supply=supply, min_batch=mb,
+                                flags=flags, mode="plan")
+            assert_same_decisions(r, exp, f"{variant} M={M} step={step}")
+            j = int(rng.integers(0, M))
+            tab.set_latency(np.array([j], np.int32), np.array([float(t.lat[j] * 1.7)]))
+        tab.close()
