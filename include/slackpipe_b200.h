@@ -190,6 +190,16 @@ int sp_queueing(sp_ctx* ctx, int32_t K, const int32_t* ptr, const double* lat,
 int sp_feedback_fold(sp_ctx* ctx, int32_t n_tables, sp_table* const* tables, int32_t n,
                      const int32_t* op, const int32_t* idx, const double* obs, double beta,
                      int32_t dfp_count, int32_t dfp_on, int32_t fb_frozen, int32_t mem);
+/* Percentile estimate of an observation batch (extension: the reference has no percentile,
+ * SURVEY.md §8(c); pinned to numpy).  Entries are numbered across the tables (table t's entry e
+ * is tables[0..t-1] sizes + e).  out[e] = np.quantile(observations of e, q,
+ * method="inverted_cdf") (NaN when e has none), out_count[e] = #observations; out_smooth
+ * (optional, in/out) <- beta * out[e] + (1 - beta) * out_smooth[e] for observed entries
+ * (initialised to out[e] where it holds NaN).  idx[j] < 0 = no observation.  0 <= q <= 1. */
+int sp_observation_quantiles(sp_ctx* ctx, int32_t n_tables, sp_table* const* tables, int32_t n,
+                             const int32_t* op, const int32_t* idx, const double* obs, double q,
+                             double beta, double* out, int32_t* out_count, double* out_smooth,
+                             int32_t mem);
 /* Per-table counters maintained by sp_feedback_fold (host out). */
 int sp_table_get_counters(sp_ctx* ctx, sp_table* t, int32_t* completed_ref,
                           int32_t* out_obs_count /* M, may be NULL */);

@@ -27,7 +27,7 @@ from .configurator import (
 )
 from . import metadata
 from .commit import commit_candidates, commit_round
-from .feedback import apply_feedback, fold_observations, set_table_counters, table_counters
+from .feedback import apply_feedback, fold_observations, observation_quantiles, set_table_counters, table_counters
 from .pipeline import ConfigEntry, ConfigSpec, PipelineDag, reference_config
 from .scenario import BackendSpec, Scenario
 from .slack import SlackGraph, compute_slack
@@ -39,6 +39,6 @@ __all__ = [
     "OpTable", "PipelineDag", "RawTable", "Scenario", "SelectResult", "Slack", "SlackGraph",
     "SlackpipeError", "TuningParams", "affinity", "affinity_from_minima", "apply_feedback",
     "commit_candidates", "commit_round", "compute_slack", "estimate_queueing", "fold_observations", "get_context", "load_library",
-    "make_flags", "metadata", "objective", "reference_config", "remaining_path_latency", "select_batch",
+    "make_flags", "metadata", "objective", "observation_quantiles", "reference_config", "remaining_path_latency", "select_batch",
     "select_config", "set_table_counters", "table_counters",
 ]

@@ -79,6 +79,7 @@ SIGNATURES = {
     "sp_table_get_counters": (C.c_int, [_p, _p, _p, _p]),
     "sp_table_set_counters": (C.c_int, [_p, _p, _i32, _p]),
     "sp_commit_round": (C.c_int, [_p, _i32, _i32, _p, _d] + [_p] * 10 + [_i32] + [_p] * 6 + [_i32]),
+    "sp_observation_quantiles": (C.c_int, [_p, _i32, _p, _i32, _p, _p, _p, _d, _d, _p, _p, _p, _i32]),
     "sp_slack_select_batch": (C.c_int, [_p, _p, _i32, _p, _d, _i32, _p, _i32, _p, _p, _i32, _p]
                               + [_p] * 11 + [_i32]),
 }

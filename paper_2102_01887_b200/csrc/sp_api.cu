@@ -1018,3 +1018,56 @@ extern "C" int sp_slack_select_batch(sp_ctx* ctx, sp_dag* g, int32_t n_tables,
   SP_CUDA(cudaStreamSynchronize(st));
   return SP_OK;
 }
+
+// ---- percentile estimate of an observation batch (sp_quantile.cu) ---------------------------
+extern "C" int sp_observation_quantiles(sp_ctx* ctx, int32_t n_tables, sp_table* const* tables,
+                                        int32_t n, const int32_t* op, const int32_t* idx,
+                                        const double* obs, double q, double beta, double* out,
+                                        int32_t* out_count, double* out_smooth, int32_t mem) {
+  if (!ctx || !tables || n_tables < 1 || n < 0) return fail(SP_E_INVALID, "quantiles: bad argument");
+  if (!(q >= 0.0 && q <= 1.0)) return fail(SP_E_INVALID, "quantiles: q must be in [0, 1]");
+  if (out_smooth && !(beta >= 0.0 && beta <= 1.0))
+    return fail(SP_E_INVALID, "quantiles: beta must be in [0, 1]");
+  if (n > 0 && (!idx || !obs)) return fail(SP_E_INVALID, "quantiles: required array is null");
+  size_t total = 0;
+  for (int t = 0; t < n_tables; ++t) {
+    if (!tables[t]) return fail(SP_E_INVALID, "quantiles: null table");
+    total += (size_t)tables[t]->M;
+  }
+  if (mem == SP_MEM_DEVICE)
+    return quantile_launch(ctx, n_tables, tables, n, op, idx, obs, q, beta, out, out_count,
+                           out_smooth);
+  if (mem != SP_MEM_HOST) return fail(SP_E_INVALID, "quantiles: bad mem flag");
+  for (int j = 0; j < n; ++j) {
+    const int t = op ? op[j] : 0;
+    if (t < 0 || t >= n_tables) return fail(SP_E_INVALID, "quantiles: op out of range");
+    if (idx[j] >= tables[t]->M) return fail(SP_E_INVALID, "quantiles: entry index out of range");
+  }
+  const size_t need = rsz<int32_t>(n) * 2 + rsz<double>(n) + rsz<double>(total) * 2 +
+                      rsz<int32_t>(total);
+  int rc = SP_OK;
+  void* io = ctx_io(ctx, need, &rc);
+  if (!io) return rc;
+  Bump b{(uint8_t*)io};
+  cudaStream_t st = ctx->stream;
+  int32_t* d_op = op ? b.take<int32_t>(n) : nullptr;
+  int32_t* d_idx = b.take<int32_t>(n);
+  double* d_obs = b.take<double>(n);
+  double* d_out = b.take<double>(total);
+  int32_t* d_cnt = b.take<int32_t>(total);
+  double* d_sm = out_smooth ? b.take<double>(total) : nullptr;
+  if (n > 0) {
+    if (op) SP_CUDA(cudaMemcpyAsync(d_op, op, 4 * (size_t)n, cudaMemcpyHostToDevice, st));
+    SP_CUDA(cudaMemcpyAsync(d_idx, idx, 4 * (size_t)n, cudaMemcpyHostToDevice, st));
+    SP_CUDA(cudaMemcpyAsync(d_obs, obs, 8 * (size_t)n, cudaMemcpyHostToDevice, st));
+  }
+  if (out_smooth)
+    SP_CUDA(cudaMemcpyAsync(d_sm, out_smooth, 8 * total, cudaMemcpyHostToDevice, st));
+  rc = quantile_launch(ctx, n_tables, tables, n, d_op, d_idx, d_obs, q, beta, d_out, d_cnt, d_sm);
+  if (rc != SP_OK) return rc;
+  if (out) SP_CUDA(cudaMemcpyAsync(out, d_out, 8 * total, cudaMemcpyDeviceToHost, st));
+  if (out_count) SP_CUDA(cudaMemcpyAsync(out_count, d_cnt, 4 * total, cudaMemcpyDeviceToHost, st));
+  if (out_smooth) SP_CUDA(cudaMemcpyAsync(out_smooth, d_sm, 8 * total, cudaMemcpyDeviceToHost, st));
+  SP_CUDA(cudaStreamSynchronize(st));
+  return SP_OK;
+}

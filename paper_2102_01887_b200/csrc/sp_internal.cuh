@@ -246,6 +246,9 @@ int commit_launch(sp_ctx* ctx, int R, int n_ops, sp_table* const* tables, double
                   int32_t* out_fill, double* out_slack, double* out_obj, double* out_aff,
                   int32_t* out_best);
 size_t commit_scratch_bytes(int R, int n_ops, int K);
+int quantile_launch(sp_ctx* ctx, int n_tables, sp_table* const* tables, int n, const int32_t* op,
+                    const int32_t* idx, const double* obs, double q, double beta, double* out,
+                    int32_t* out_count, double* out_smooth);
 int scores_launch(sp_ctx* ctx, sp_table* t, Plan* p, const double* slack_dev,
                   double* score_dev, double* cost_dev);
 int slack_launch(sp_ctx* ctx, sp_dag* g, int I, const double* ref, int ref_stride,

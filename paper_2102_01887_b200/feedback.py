@@ -77,3 +77,37 @@ def apply_feedback(old_estimate_s: float, observed_s: float, beta: float) -> flo
         return float(t.get_latency()[0])
     finally:
         t.close()
+
+
+def observation_quantiles(tables: Sequence, op, idx, obs, q: float, *, smooth=None,
+                          beta: float = 0.5) -> dict:
+    """Per-entry latency percentile of an observation batch (extension of K3; the reference has
+    no percentile — parity is pinned to numpy): ``quantile[e] = np.quantile(obs of entry e, q,
+    method="inverted_cdf")`` (NaN without observations) and ``count[e]``, entries numbered
+    across ``tables`` in order.  ``smooth`` (optional array, updated in place) receives
+    ``beta * quantile + (1 - beta) * smooth`` for observed entries — the EWMA of
+    manager.py:45-47 applied to the batch percentile.  numpy in -> synchronous; torch CUDA
+    tensors in -> stream-ordered."""
+    if not tables:
+        raise ValueError("observation_quantiles: no tables")
+    ctx = tables[0]._ctx
+    device = _is_device(obs)
+    n = int(obs.shape[0])
+    total = sum(len(t.lat) for t in tables)
+    arr_t = (C.c_void_p * len(tables))(*[t.handle.value for t in tables])
+    if device:
+        import torch
+
+        out = {"quantile": torch.empty(total, dtype=torch.float64, device=obs.device),
+               "count": torch.empty(total, dtype=torch.int32, device=obs.device)}
+    else:
+        idx = np.ascontiguousarray(idx, dtype=np.int32)
+        obs = np.ascontiguousarray(obs, dtype=np.float64)
+        if op is not None:
+            op = np.ascontiguousarray(op, dtype=np.int32)
+        out = {"quantile": np.empty(total, np.float64), "count": np.empty(total, np.int32)}
+    check(ctx.lib.sp_observation_quantiles(
+        ctx.handle, len(tables), C.cast(arr_t, C.c_void_p), n, ptr(op), ptr(idx), ptr(obs),
+        float(q), float(beta), ptr(out["quantile"]), ptr(out["count"]), ptr(smooth),
+        _lib.SP_MEM_DEVICE if device else _lib.SP_MEM_HOST), "sp_observation_quantiles")
+    return out
