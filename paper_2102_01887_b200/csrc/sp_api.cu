@@ -683,11 +683,43 @@ int sp_dag_create(sp_ctx* ctx, int32_t V, const int32_t* pred_ptr, const int32_t
     e = cudaMemcpy(g->pred_ptr, qptr.data(), sizeof(int32_t) * qptr.size(), cudaMemcpyHostToDevice);
   if (e == cudaSuccess && !preds.empty())
     e = cudaMemcpy(g->preds, preds.data(), sizeof(uint32_t) * preds.size(), cudaMemcpyHostToDevice);
+  // certified backward form (k_slack_cert): worth it when the per-source forward programs
+  // relax many more edges than one backward pass over the graph does
+  // (SP_K1_CERT=force builds it for every eligible graph — the parity tests use that)
+  int E = pred_ptr[V];
+  const char* cf = getenv("SP_K1_CERT");
+  const bool force = cf && !strcmp(cf, "force");
+  const bool off = cf && !strcmp(cf, "0");
+  if (e == cudaSuccess && !off && V <= kCertMaxV && n_val < 65536 &&
+      (force || (int64_t)preds.size() >= 4 * (int64_t)(E + V))) {
+    auto a16 = [](int x) { return (x + 15) & ~15; };
+    g->E = E;
+    g->off_vidx = a16(2 * (V + 1));
+    g->off_term = g->off_vidx + a16(2 * V);
+    g->off_src = g->off_term + a16(V);
+    g->off_succ = g->off_src + a16(n_src);
+    g->cert_bytes = g->off_succ + a16(std::max(E, 1));
+    std::vector<uint8_t> img(g->cert_bytes, 0);
+    uint16_t* sp = reinterpret_cast<uint16_t*>(img.data());
+    uint16_t* vi = reinterpret_cast<uint16_t*>(img.data() + g->off_vidx);
+    int c = 0;
+    for (int v = 0; v < V; ++v) {
+      sp[v] = (uint16_t)c;
+      for (int w : succ[v]) img[g->off_succ + c++] = (uint8_t)w;
+      vi[v] = (uint16_t)val_idx[v];
+      img[g->off_term + v] = terminal[v] ? 1 : 0;
+    }
+    sp[V] = (uint16_t)c;
+    for (int s = 0; s < n_src; ++s) img[g->off_src + s] = (uint8_t)sources[s];
+    e = cudaMalloc(&g->cert, img.size());
+    if (e == cudaSuccess) e = cudaMemcpy(g->cert, img.data(), img.size(), cudaMemcpyHostToDevice);
+  }
   if (e != cudaSuccess) {
     cudaFree(g->prog);
     cudaFree(g->prog_ptr);
     cudaFree(g->pred_ptr);
     cudaFree(g->preds);
+    cudaFree(g->cert);
     delete g;
     return cuda_fail(e, "dag_create");
   }
@@ -702,6 +734,7 @@ int sp_dag_destroy(sp_ctx* ctx, sp_dag* g) {
   cudaFree(g->prog_ptr);
   cudaFree(g->pred_ptr);
   cudaFree(g->preds);
+  cudaFree(g->cert);
   delete g;
   return SP_OK;
 }

@@ -25,6 +25,10 @@
 // memory run four vertices ahead in a register shift ring, so the per-vertex dependency
 // chain is program broadcast -> DP loads -> compare tree -> add -> store.
 #include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <cmath>
 
 #include "sp_internal.cuh"
 
@@ -124,6 +128,246 @@ __global__ void __launch_bounds__(32 * kSlackWarps) k_slack(
   }
 }
 
+__device__ __forceinline__ void store_slack(int i, int s, int n_src, double own, double tmax,
+                                            double tmin, double base, int K,
+                                            const double* __restrict__ Q,
+                                            double* __restrict__ out_slack,
+                                            double* __restrict__ out_ratio) {
+  const double ratio_lo = __ddiv_rn(own, tmax);  // min over suffixes of own/total
+  const double ratio_hi = __ddiv_rn(own, tmin);  // max over suffixes of own/total
+  const size_t o = (size_t)i * n_src + s;
+  if (out_ratio) {
+    out_ratio[2 * o] = ratio_lo;
+    out_ratio[2 * o + 1] = ratio_hi;
+  }
+  if (out_slack) {
+    for (int k = 0; k < K; ++k) {
+      const double b = __dsub_rn(base, __ldg(Q + (size_t)i * K + k));
+      out_slack[o * K + k] = __dmul_rn(b >= 0.0 ? ratio_lo : ratio_hi, b);
+    }
+  }
+}
+
+// ---- K1c: certified backward pass -------------------------------------------------------
+// The forward DP above relaxes every edge of every source's descendant set (19,227 edge
+// relaxations per instance on config 3's 64-op DAG).  K1c finds each source's extremal path
+// with ONE backward pass over the graph (845 edges) and then proves, per source, that the
+// path it found is the one the reference's left-to-right sums make extremal:
+//   backward:  Hb[v] = fl(ref[v] + max(end_v ? 0 : -inf, max_u Hb[u]))   (u: successors)
+//              argmax[v] = the option taken, gap[v] = its value minus the runner-up option's,
+//              rounded down to float (+inf without a runner-up);  min side alike.
+//   Monotone rounding makes Hb[v] = max over paths of the right-nested rounded path sums R, so
+//   following argmax from s gives a path p^ with R(p^) = Hb[s]; the walk recomputes its forward
+//   sum  Tmax = ((0 + r_s) + r_1) + ...  exactly as configurator.py:500-506 does.
+//   Certificate: any other path p leaves p^ at some node v_j through a runner-up option, whose
+//   best continuation has R <= Y_j - gap_j (Y_j = the chosen option's value, R of p^'s tail).
+//   With recursive-summation bounds for non-negative terms (|fl - exact| <= g * exact,
+//   g = V u / (1 - V u), u = 2^-53) on the forward sums of p and p^ and on R, p's forward sum
+//   cannot exceed Tmax once gap_j >= 2g A_j + 4.01g Y_j, which min_j gap_j >= theta * Tmax
+//   (theta = 5g + 8u) implies.  So Tmax IS the reference's maximum; the min side mirrors it
+//   (max orientation on negated values, the same gap test against Tmin).
+// Sources whose certificate fails (near-ties within ~1e-13 relative, exact ties, refs that are
+// negative / non-finite / > 1e300) fall back to the exact forward DP of that source, so the
+// output is bit-identical to k_slack in every case.
+// Layout: TWO lanes per instance — the even lane runs the max side, the odd lane the min side
+// (in max orientation on negated values, so both run the same code) — which halves the shared
+// memory per lane and doubles the resident warps; the walks are then shared out by source
+// parity, two sources per lane in flight.  Per instance and node 26 bytes of shared memory:
+// {Hb, -Lb} (later the walk record {ref, gap_max | gap_min}), the two float gaps, the two args.
+constexpr uint32_t kArgNone = 0xFE, kArgEnd = 0xFF;
+constexpr int kCertWarps = 4;  // 64 instances per block
+
+// one walk step along an extremal path: w = {ref, gap_max | gap_min} of node v; the chain adds
+// ref to its forward sum and keeps the smallest margin seen
+struct Walk {
+  uint32_t v;
+  bool on;
+  double acc;  // forward sum ((0 + r_s) + r_1) + ... along the path
+  float gap;   // smallest margin of a chosen option over its runner-up on the path
+};
+
+template <bool MAX>
+__device__ __forceinline__ void walk_step(Walk& c, const double2* __restrict__ W,
+                                          const uint16_t* __restrict__ R, bool& none) {
+  if (!c.on) return;
+  const double2 w = W[c.v * 16];
+  const uint32_t rr = R[c.v * 16];
+  const uint32_t nx = MAX ? (rr & 0xFFu) : (rr >> 8);
+  c.acc = __dadd_rn(c.acc, w.x);
+  const float g = __int_as_float(MAX ? __double2loint(w.y) : __double2hiint(w.y));
+  c.gap = g < c.gap ? g : c.gap;
+  none |= nx == kArgNone;
+  c.on = nx < kArgNone;
+  c.v = nx;
+}
+
+__global__ void __launch_bounds__(32 * kCertWarps) k_slack_cert(
+    const uint8_t* __restrict__ cert, int cert_bytes, int V, int n_src, int off_vidx,
+    int off_term, int off_src, int off_succ, const int4* __restrict__ prog,
+    const int32_t* __restrict__ prog_ptr, const uint32_t* __restrict__ preds,
+    const int32_t* __restrict__ pred_ptr, int I, const double* __restrict__ ref, int ref_stride,
+    const double* __restrict__ target, const double* __restrict__ now, int K,
+    const double* __restrict__ Q, double theta, double* __restrict__ out_slack,
+    double* __restrict__ out_ratio) {
+  extern __shared__ __align__(16) uint8_t smc[];
+  for (int t = threadIdx.x; t < cert_bytes / 16; t += blockDim.x)
+    reinterpret_cast<uint4*>(smc)[t] = __ldg(reinterpret_cast<const uint4*>(cert) + t);
+  __syncthreads();
+  const uint16_t* SP = reinterpret_cast<const uint16_t*>(smc);
+  const uint16_t* VI = reinterpret_cast<const uint16_t*>(smc + off_vidx);
+  const uint8_t* TE = smc + off_term;
+  const uint8_t* SRC = smc + off_src;
+  const uint8_t* SU = smc + off_succ;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int k = lane >> 1, side = lane & 1;  // instance in the warp, 0 = max / 1 = min side
+  const int nfw = (n_src + 31) >> 5;
+  uint8_t* wb = smc + cert_bytes + (size_t)warp * ((size_t)V * 416 + (size_t)nfw * 128);
+  // element (v, k, side) of each [V][16][2] array sits at v * 32 + 2k + side
+  double* A = reinterpret_cast<double*>(wb) + 2 * k;
+  float* Cf = reinterpret_cast<float*>(wb + (size_t)V * 256) + 2 * k;
+  uint8_t* Rb = wb + (size_t)V * 384 + 2 * k;
+  uint32_t* Fw = reinterpret_cast<uint32_t*>(wb + (size_t)V * 416) + lane;
+  const double2* W = reinterpret_cast<const double2*>(A);  // walk record (v, k) at v * 16
+  const uint16_t* R = reinterpret_cast<const uint16_t*>(Rb);
+  const int i0 = (blockIdx.x * kCertWarps + warp) * 16;
+  if (i0 >= I) return;
+  const int i = i0 + k;
+  const bool live = i < I;
+  const double* r = ref + (size_t)(live ? i : i0) * ref_stride;
+
+  // ---- backward pass in max orientation (the min side negates), reverse topological order ----
+  bool bad = false;
+  double rn = __ldg(r + VI[V - 1]);
+  for (int v = V - 1; v >= 0; --v) {
+    const double rv = rn;
+    if (v > 0) rn = __ldg(r + VI[v - 1]);
+    bad |= !(rv >= 0.0 && rv <= 1e300);
+    const bool te = TE[v] != 0;
+    double h1 = te ? 0.0 : -INFINITY, h2 = -INFINITY;
+    uint32_t a1 = te ? kArgEnd : kArgNone;
+    const int e1 = SP[v + 1];
+    int e = SP[v];
+    for (; e + 4 <= e1; e += 4) {
+      const uint32_t u0 = SU[e], u1 = SU[e + 1], u2 = SU[e + 2], u3 = SU[e + 3];
+      const double x0 = A[u0 * 32 + side], x1 = A[u1 * 32 + side];
+      const double x2 = A[u2 * 32 + side], x3 = A[u3 * 32 + side];
+      // top two of the four (and the arg of the best), merged into the running pair; an exact
+      // tie leaves the runner-up equal to the best, which fails the certificate as it must
+      const bool g01 = x1 > x0, g23 = x3 > x2;
+      const double m01 = g01 ? x1 : x0, s01 = g01 ? x0 : x1;
+      const double m23 = g23 ? x3 : x2, s23 = g23 ? x2 : x3;
+      const uint32_t i01 = g01 ? u1 : u0, i23 = g23 ? u3 : u2;
+      const bool gq = m23 > m01;
+      const double M = gq ? m23 : m01;
+      const double lo = gq ? m01 : m23;
+      const double sm = s01 > s23 ? s01 : s23;
+      const double S = lo > sm ? lo : sm;
+      const uint32_t iq = gq ? i23 : i01;
+      const bool gt = M > h1;
+      const double l2 = gt ? h1 : M;
+      const double s2 = S > h2 ? S : h2;
+      h2 = l2 > s2 ? l2 : s2;
+      h1 = gt ? M : h1;
+      a1 = gt ? iq : a1;
+    }
+    for (; e < e1; ++e) {
+      const uint32_t u0 = SU[e];
+      const double x0 = A[u0 * 32 + side];
+      const bool gt = x0 > h1;
+      h2 = gt ? h1 : (x0 > h2 ? x0 : h2);
+      h1 = gt ? x0 : h1;
+      a1 = gt ? u0 : a1;
+    }
+    A[v * 32 + side] = __dadd_rn(side ? -rv : rv, h1);
+    Cf[v * 32 + side] = __double2float_rd(__dsub_rd(h1, h2));  // margin of the chosen option
+    Rb[v * 32 + side] = (uint8_t)a1;
+  }
+  bad |= __shfl_xor_sync(0xffffffffu, bad, 1);
+  __syncwarp();
+  // walk records {ref, gap_max | gap_min}: the even lane brings the ref, the odd lane the gaps
+  for (int v = 0; v < V; ++v)
+    A[v * 32 + side] = side ? *reinterpret_cast<const double*>(Cf + v * 32) : __ldg(r + VI[v]);
+  for (int w = 0; w < nfw; ++w) Fw[w * 32] = 0u;
+  __syncwarp();
+
+  // configurator.py:535  budget = self.target_s - now - queueing[k]
+  const double base = live ? __dsub_rn(__ldg(target + i), __ldg(now + i)) : 0.0;
+  // ---- per source: walk both extremal paths, certify, emit (sources by parity, 2 at once) ----
+  for (int g = side; g < n_src; g += 4) {
+    const int sa = g, sb = g + 2 < n_src ? g + 2 : -1;
+    const uint32_t va = SRC[sa], vb = sb >= 0 ? SRC[sb] : 0u;
+    Walk ha{va, true, 0.0, INFINITY}, la{va, true, 0.0, INFINITY};
+    Walk hb{vb, sb >= 0, 0.0, INFINITY}, lb{vb, sb >= 0, 0.0, INFINITY};
+    bool none_a = false, none_b = false;
+    while (ha.on || la.on || hb.on || lb.on) {
+      walk_step<true>(ha, W, R, none_a);
+      walk_step<false>(la, W, R, none_a);
+      walk_step<true>(hb, W, R, none_b);
+      walk_step<false>(lb, W, R, none_b);
+    }
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int si = q ? sb : sa;
+      if (si < 0) continue;
+      const Walk& h = q ? hb : ha;
+      const Walk& l = q ? lb : la;
+      const bool ok = !bad && !(q ? none_b : none_a) &&
+                      (double)h.gap >= __dmul_ru(theta, h.acc) &&
+                      (double)l.gap >= __dmul_ru(theta, l.acc);
+      if (ok) {
+        if (live) {
+          const double own = __dadd_rn(0.0, W[SRC[si] * 16].x);
+          store_slack(i, si, n_src, own, h.acc, l.acc, base, K, Q, out_slack, out_ratio);
+        }
+      } else {
+        Fw[(si >> 5) * 32] |= 1u << (si & 31);
+      }
+    }
+  }
+  __syncwarp();
+
+  // ---- uncertified sources: the exact forward DP (k_slack's program, read from global), one
+  // side at a time, slots in the instance's [V] x 16-byte column ----
+  double2* D = reinterpret_cast<double2*>(A);
+  for (int sd = 0; sd < 2; ++sd) {
+    if (side == sd) {
+      for (int w = 0; w < nfw; ++w) {
+        uint32_t bits = Fw[w * 32];
+        while (bits) {
+          const int si = w * 32 + __ffs(bits) - 1;
+          bits &= bits - 1;
+          const int4* Ps = prog + prog_ptr[si];
+          const int n = prog_ptr[si + 1] - prog_ptr[si];
+          const uint32_t* Gs = preds + pred_ptr[si];
+          const int4 head = Ps[0];
+          const double own = __dadd_rn(0.0, __ldg(r + head.x));
+          D[(head.y & 0xffff) * 16] = make_double2(own, own);
+          double tmax = (head.y >> 16) ? own : -INFINITY;
+          double tmin = (head.y >> 16) ? own : INFINITY;
+          for (int e = 1; e < n; ++e) {
+            const int4 pr = Ps[e];
+            const double rv = __ldg(r + pr.x);
+            double hm = -INFINITY, lm = INFINITY;
+            for (int t = 0; t < 2 * pr.w; ++t) {
+              const double2 a = D[Gs[pr.z + t] * 16];
+              hm = hm > a.x ? hm : a.x;
+              lm = lm < a.y ? lm : a.y;
+            }
+            const double h = __dadd_rn(hm, rv), l = __dadd_rn(lm, rv);
+            D[(pr.y & 0xffff) * 16] = make_double2(h, l);
+            if (pr.y >> 16) {
+              tmax = h > tmax ? h : tmax;
+              tmin = l < tmin ? l : tmin;
+            }
+          }
+          if (live) store_slack(i, si, n_src, own, tmax, tmin, base, K, Q, out_slack, out_ratio);
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
 // Eq. 2 ordered sum, one thread per kind (configurator.py:516-523 / 116-119).
 __global__ void k_queueing(int K, const int32_t* __restrict__ ptr, const double* __restrict__ lat,
                            const double* __restrict__ res, const int32_t* __restrict__ cnt,
@@ -150,6 +394,29 @@ int slack_launch(sp_ctx* ctx, sp_dag* g, int I, const double* ref, int ref_strid
                  const double* target, const double* now, int K, const double* Q,
                  double* out_slack, double* out_ratio) {
   if (I == 0) return SP_OK;
+  const char* ce = getenv("SP_K1_CERT");
+  if (g->cert && !(ce && !strcmp(ce, "0"))) {
+    const int nfw = (g->n_src + 31) / 32;
+    const size_t smem = (size_t)g->cert_bytes +
+                        (size_t)kCertWarps * ((size_t)g->V * 416 + (size_t)nfw * 128);
+    if (smem <= 227 * 1024) {
+      static size_t cert_attr = 0;
+      if (smem > 48 * 1024 && smem > cert_attr) {
+        SP_CUDA(cudaFuncSetAttribute(k_slack_cert, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+        cert_attr = smem;
+      }
+      const double u = std::ldexp(1.0, -53);
+      const double gam = g->V * u / (1.0 - g->V * u);
+      const int per_block = 16 * kCertWarps;
+      k_slack_cert<<<(I + per_block - 1) / per_block, 32 * kCertWarps, smem, ctx->stream>>>(
+          g->cert, g->cert_bytes, g->V, g->n_src, g->off_vidx, g->off_term, g->off_src,
+          g->off_succ, g->prog, g->prog_ptr, g->preds, g->pred_ptr, I, ref, ref_stride, target,
+          now, K, Q, 5.0 * gam + 8.0 * u, out_slack, out_ratio);
+      SP_CHECK_LAUNCH(ctx);
+      return SP_OK;
+    }
+  }
   const size_t smem = (size_t)kSlackWarps * g->max_slots * 32 * sizeof(double2) +
                       (size_t)g->max_span * sizeof(int4) +
                       (size_t)g->max_preds * sizeof(uint32_t);

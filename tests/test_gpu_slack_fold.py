@@ -78,6 +78,41 @@ def test_deep_dag_config3_vs_dp_oracle(gpu_ctx):
     assert np.isfinite(r["slack"]).all()
 
 
+def test_deep_dag_certified_pass_equals_forward_dp(gpu_ctx, monkeypatch):
+    """K1c (certified backward pass, the default for config 3) against K1's forward DP on the
+    full 100k-instance launch: every slack and ratio bit-identical.  A second batch with
+    quantised refs (exact ties between paths), zeros, and a few negative / inf / NaN refs
+    forces the per-source fallbacks."""
+    from paper_2102_01887_b200 import SlackGraph
+    from paper_2102_01887_b200 import synth
+
+    dag = synth.deep_dag()
+    ref, T, now, Q = synth.deep_dag_instances(dag, 100_000)
+    rng = np.random.default_rng(11)
+    tie = np.round(ref[:4000] * 4) / 4
+    tie[rng.random(tie.shape) < 0.01] = 0.0
+    tie[5, 3] = -1.0
+    tie[17, 40] = np.inf
+    tie[23, 12] = np.nan
+    tie[29, :] = 0.0
+    for refs, t, n, q in ((ref, T, now, Q), (tie, T[:4000], now[:4000], Q[:4000])):
+        g = SlackGraph.from_dag(dag)
+        got = g.slack_batch(refs, t, n, q, ratios=True)
+        monkeypatch.setenv("SP_K1_CERT", "0")
+        exp = g.slack_batch(refs, t, n, q, ratios=True)
+        monkeypatch.delenv("SP_K1_CERT")
+        g.close()
+        for key in ("slack", "ratio"):
+            assert np.array_equal(bits(got[key]), bits(exp[key])), key
+
+
+def test_dag_slack_certified_forced_vs_reference(gpu_ctx, monkeypatch):
+    """The 400 reference DAG cases with K1c forced on every graph (SP_K1_CERT=force), small
+    integer-valued refs included: bit-identical to the reference's compute_slack."""
+    monkeypatch.setenv("SP_K1_CERT", "force")
+    test_dag_slack_vs_reference_compute_slack(gpu_ctx)
+
+
 def _fold_tables(d, m, lo):
     import paper_2102_01887_b200 as sp
 
