@@ -123,8 +123,22 @@ def run_c3(args):
         evs[i][1].record(stream)
     torch.cuda.synchronize(dev)
     ms = [x.elapsed_time(y) for x, y in evs]
+    launches = ctx.launch_count - l0
     t = _tmax(torch, sum(ms) / 1e3, dev)
     vals = args.steps * I * V * K * world
+    # the same step through K1's per-source forward DP (SP_K1_CERT=0), reported beside it
+    os.environ["SP_K1_CERT"] = "0"
+    try:
+        evf = _events(torch, args.steps)
+        for i in range(args.steps):
+            flush()
+            evf[i][0].record(stream)
+            g.slack_batch(d["ref"], d["T"], d["now"], d["Q"], out=out)
+            evf[i][1].record(stream)
+        torch.cuda.synchronize(dev)
+    finally:
+        del os.environ["SP_K1_CERT"]
+    fwd_ms = statistics.median([x.elapsed_time(y) for x, y in evf])
     if rank != 0:
         return
     bytes_inst = 8 * V + 16 + 8 * K + 8 * V * K
@@ -154,10 +168,12 @@ def run_c3(args):
                    "decomposed_paths": "~3.3e9 (not enumerable by the reference)",
                    "parallelism": f"instances sharded over {world} GPU(s), no collective"},
         "instances_per_s": args.steps * I * world / t,
-        "roofline": {"bound": "fp64/lds issue (exact forward DP, DESIGN.md §3)",
+        "roofline": {"bound": "issue / shared-memory latency (K1c: one backward pass + per-source "
+                              "extremal-path walks, DESIGN.md §5)",
                      "hbm_bytes_per_instance": bytes_inst,
                      "hbm_frac": (args.steps * I * world * bytes_inst / t / 1e9) / (world * _peaks())},
-        "gpu_launches": ctx.launch_count - l0,
+        "forward_dp_step_ms": fwd_ms,
+        "gpu_launches": launches,
         "cpu_baseline": None if world > 1 else {"value": n_cpu / cpu_t, "unit": "slack/s", "cores": cores,
                          "kind": "restatement (the reference cannot run this DAG)",
                          "sample": f"{S} instances, oracle/slack.py dp_ratios on {cores} processes"},

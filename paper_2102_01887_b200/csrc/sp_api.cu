@@ -693,23 +693,30 @@ int sp_dag_create(sp_ctx* ctx, int32_t V, const int32_t* pred_ptr, const int32_t
   if (e == cudaSuccess && !off && V <= kCertMaxV && n_val < 65536 &&
       (force || (int64_t)preds.size() >= 4 * (int64_t)(E + V))) {
     auto a16 = [](int x) { return (x + 15) & ~15; };
+    // successor lists as u16 byte offsets (node * 256, the stride of a node's row in the
+    // kernel's [node][lane] arrays), padded to groups of four with the sentinel row V
+    int groups = 0;
+    for (int v = 0; v < V; ++v) groups += ((int)succ[v].size() + 3) / 4;
     g->E = E;
     g->off_vidx = a16(2 * (V + 1));
     g->off_term = g->off_vidx + a16(2 * V);
     g->off_src = g->off_term + a16(V);
     g->off_succ = g->off_src + a16(n_src);
-    g->cert_bytes = g->off_succ + a16(std::max(E, 1));
+    g->cert_bytes = g->off_succ + a16(8 * std::max(groups, 1));
     std::vector<uint8_t> img(g->cert_bytes, 0);
-    uint16_t* sp = reinterpret_cast<uint16_t*>(img.data());
+    uint16_t* sp = reinterpret_cast<uint16_t*>(img.data());  // group index of each node's list
     uint16_t* vi = reinterpret_cast<uint16_t*>(img.data() + g->off_vidx);
-    int c = 0;
+    uint16_t* so = reinterpret_cast<uint16_t*>(img.data() + g->off_succ);
+    int q = 0;
     for (int v = 0; v < V; ++v) {
-      sp[v] = (uint16_t)c;
-      for (int w : succ[v]) img[g->off_succ + c++] = (uint8_t)w;
+      sp[v] = (uint16_t)q;
+      const int n = (int)succ[v].size(), ng = (n + 3) / 4;
+      for (int j = 0; j < 4 * ng; ++j) so[4 * q + j] = (uint16_t)((j < n ? succ[v][j] : V) * 256);
+      q += ng;
       vi[v] = (uint16_t)val_idx[v];
       img[g->off_term + v] = terminal[v] ? 1 : 0;
     }
-    sp[V] = (uint16_t)c;
+    sp[V] = (uint16_t)q;
     for (int s = 0; s < n_src; ++s) img[g->off_src + s] = (uint8_t)sources[s];
     e = cudaMalloc(&g->cert, img.size());
     if (e == cudaSuccess) e = cudaMemcpy(g->cert, img.data(), img.size(), cudaMemcpyHostToDevice);

@@ -193,8 +193,9 @@ struct sp_dag {
   int32_t max_preds = 0;        // max padded pred entries of one source
   int64_t prog_len = 0, pred_len = 0;
   // Certified backward form (sp_slack.cu, k_slack_cert): one byte image, staged whole into
-  // shared memory — succ_ptr u16[V+1] | vidx u16[V] | term u8[V] | src u8[n_src] | succ u8[E],
-  // 16-byte aligned sections.  Present when V <= kCertMaxV and the per-source programs are
+  // shared memory — group_ptr u16[V+1] | vidx u16[V] | term u8[V] | src u8[n_src] |
+  // succ u16[4 * groups] (successor byte offsets node * 256, each list padded to a multiple of
+  // four with the sentinel node V), 16-byte aligned sections.  Present when V <= kCertMaxV and the per-source programs are
   // long enough (Σ_s |E(desc s)|) for the backward pass to pay.
   uint8_t* cert = nullptr;  // device
   int32_t cert_bytes = 0, E = 0;

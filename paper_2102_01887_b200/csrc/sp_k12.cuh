@@ -23,7 +23,7 @@ struct K12Dag {
   const int32_t* prog_ptr;   // n_src + 1
   const uint32_t* preds;
   const int32_t* pred_ptr;   // n_src + 1
-  int n_src, nslots, prog_len, pred_len;
+  int n_src, nslots, prog_len, pred_len, n_val;
 };
 
 struct K12In {
@@ -42,7 +42,7 @@ struct K12In {
 template <int KT, bool FAST>
 __global__ void __launch_bounds__(32 * kK12Warps) k_slack_select(K12Dag g, K12In in, PlanPtrs pp,
                                                                  int plan_off, int stage_off,
-                                                                 SelectIO io) {
+                                                                 int out_stage, SelectIO io) {
   extern __shared__ __align__(16) uint8_t sm12[];
   __shared__ int s_pb[kK12MaxSrc + 1], s_qb[kK12MaxSrc + 1], s_off[kK12MaxSrc + 1];
   __shared__ int s_lut[kK12MaxSrc];  // lane lookup table of plan t, relative to its image
@@ -86,10 +86,16 @@ __global__ void __launch_bounds__(32 * kK12Warps) k_slack_select(K12Dag g, K12In
     __syncthreads();
   }
   const uint32_t plans_sb = smem_u32(plans);
-  // this warp's staging area: inputs avail, supply, min_batch, flags; outputs idx, code, fill,
-  // obj, slack, wait — decisions d0 + c of the current group at index c
+  // this warp's staging area: inputs avail, supply, min_batch, flags; with out_stage also the
+  // outputs idx, code, fill, obj, slack, wait — decisions d0 + c of the current group at index c
+  // (without it the decisions are stored straight to global memory and L2 merges the strided
+  // partial-sector writes)
   const int Dw = 32 * g.n_src;
-  uint8_t* wst = sm12 + stage_off + (size_t)warp * Dw * kK12StageBytesPerDecision;
+  const int bpd = out_stage ? kK12StageBytesPerDecision : 16;
+  uint8_t* wst = sm12 + stage_off + (size_t)warp * Dw * bpd;
+  // this lane's reference latencies, staged once per instance: [value][lane]
+  double* Rs = reinterpret_cast<double*>(sm12 + stage_off + (size_t)kK12Warps * Dw * bpd) +
+               (size_t)warp * g.n_val * 32 + lane;
   int32_t* s_av = reinterpret_cast<int32_t*>(wst);
   int32_t* s_sup = s_av + Dw;
   int32_t* s_mb = s_sup + Dw;
@@ -119,6 +125,15 @@ __global__ void __launch_bounds__(32 * kK12Warps) k_slack_select(K12Dag g, K12In
   for (int i0 = (blockIdx.x * kK12Warps + warp) * 32; i0 < in.I; i0 += nwarps_total * 32) {
     const int d0 = i0 * g.n_src;
     const int nd = min(Dw, io.N - d0);
+    if (!out_stage) {
+      sio.out_idx = io.out_idx + d0; sio.out_code = io.out_code + d0;
+      sio.out_fill = io.out_fill ? io.out_fill + d0 : nullptr;
+      sio.out_obj = io.out_obj ? io.out_obj + d0 : nullptr;
+      sio.out_slack = io.out_slack ? io.out_slack + d0 : nullptr;
+      sio.out_wait = io.out_wait ? io.out_wait + d0 : nullptr;
+      fio.out_idx = sio.out_idx; fio.out_code = sio.out_code; fio.out_fill = sio.out_fill;
+      fio.out_obj = sio.out_obj; fio.out_slack = sio.out_slack; fio.out_wait = sio.out_wait;
+    }
     __syncwarp();
     for (int c = lane; c < nd; c += 32) {  // coalesced loads of the group's decision inputs
       s_av[c] = __ldg(io.avail + d0 + c);
@@ -131,25 +146,32 @@ __global__ void __launch_bounds__(32 * kK12Warps) k_slack_select(K12Dag g, K12In
     const bool live = i < in.I;
     const int ii = live ? i : i0;
     const double* r = in.ref + (size_t)ii * in.ref_stride;
+    for (int v = 0; v < g.n_val; ++v) Rs[v * 32] = __ldg(r + v);  // all loads in flight at once
     // configurator.py:535  budget = self.target_s - now - queueing[k]
     const double base = __dsub_rn(__ldg(in.target + ii), __ldg(in.now + ii));
     double bud[KT];
+    bool need_lo = false, need_hi = false;  // which of own/Tmax, own/Tmin the kinds use
 #pragma unroll
-    for (int k = 0; k < KT; ++k)
+    for (int k = 0; k < KT; ++k) {
       bud[k] = k < K ? __dsub_rn(base, __ldg(in.Q + (size_t)ii * K + k)) : 0.0;
+      if (k < K) {
+        need_lo |= bud[k] >= 0.0;
+        need_hi |= !(bud[k] >= 0.0);
+      }
+    }
     for (int s = 0; s < g.n_src; ++s) {
       // K1: forward DP over the source's descendants (sp_slack.cu)
       const int4* Ps = P + s_pb[s];
       const int n = s_pb[s + 1] - s_pb[s];
       const uint32_t* Gs = G + s_qb[s];
       const int4 head = Ps[0];
-      const double own = __dadd_rn(0.0, __ldg(r + head.x));  // total = 0.0; total += ref[op]
+      const double own = __dadd_rn(0.0, Rs[head.x * 32]);  // total = 0.0; total += ref[op]
       D[(head.y & 0xffff) * 32] = make_double2(own, own);
       double tmax = (head.y >> 16) ? own : -INFINITY;
       double tmin = (head.y >> 16) ? own : INFINITY;
       for (int e = 1; e < n; ++e) {
         const int4 pr = Ps[e];
-        const double rv = __ldg(r + pr.x);
+        const double rv = Rs[pr.x * 32];
         const uint2* gp = reinterpret_cast<const uint2*>(Gs + pr.z);
         double hm = -INFINITY, lm = INFINITY;
         for (int t = 0; t < pr.w; ++t) {
@@ -168,8 +190,9 @@ __global__ void __launch_bounds__(32 * kK12Warps) k_slack_select(K12Dag g, K12In
           tmin = l < tmin ? l : tmin;
         }
       }
-      const double lo = __ddiv_rn(own, tmax);  // min over suffixes of own/total
-      const double hi = __ddiv_rn(own, tmin);  // max over suffixes of own/total
+      // min / max over suffixes of own/total, each divided out only if some kind uses it
+      const double lo = need_lo ? __ddiv_rn(own, tmax) : 0.0;
+      const double hi = need_hi ? __ddiv_rn(own, tmin) : 0.0;
       if (!live) continue;
       // K2: decide invocation (i, s) against operation s's plan
       const int d = i * g.n_src + s;
@@ -201,6 +224,7 @@ __global__ void __launch_bounds__(32 * kK12Warps) k_slack_select(K12Dag g, K12In
         decide_plan<KT, false>(v, sio, dl, x);
       }
     }
+    if (!out_stage) continue;
     __syncwarp();
     for (int c = lane; c < nd; c += 32) {  // coalesced stores of the group's decisions
       io.out_idx[d0 + c] = o_idx[c];

@@ -487,8 +487,13 @@ int slack_select_launch(sp_ctx* ctx, sp_dag* g, int n_tables, sp_table* const* t
   const size_t progb = (size_t)g->prog_len * sizeof(int4) + (((size_t)g->pred_len * 4 + 15) / 16) * 16;
   if (!fused) fast_ok = false;
   const size_t plans_all = plan_bytes + (fast_ok ? lut_bytes : 0);
-  const size_t stage = (size_t)kK12Warps * 32 * n_tables * kK12StageBytesPerDecision;
-  const size_t smem = dp + progb + plans_all + stage;
+  // decisions staged for coalesced stores only on request (SP_K12_OUTSTAGE=1): without it the
+  // per-warp area holds just the 16 input bytes per decision and more CTAs stay resident
+  const int out_stage = (getenv("SP_K12_OUTSTAGE") || !out_fill || !out_obj || !out_slack ||
+                         !out_wait) ? 1 : 0;
+  const size_t stage = (size_t)kK12Warps * 32 * n_tables * (out_stage ? kK12StageBytesPerDecision : 16);
+  const size_t refs = (size_t)kK12Warps * g->n_val * 32 * sizeof(double);
+  const size_t smem = dp + progb + plans_all + stage + refs;
   if (fused && smem <= (size_t)kPlanSmemBudget) {
     SelectIO io;
     memset(&io, 0, sizeof(io));
@@ -497,7 +502,7 @@ int slack_select_launch(sp_ctx* ctx, sp_dag* g, int n_tables, sp_table* const* t
     io.out_obj = out_obj; io.out_slack = out_slack; io.out_wait = out_wait;
     io.N = N; io.K = K;
     K12Dag kg{g->prog, g->prog_ptr, g->preds, g->pred_ptr, g->n_src, g->max_slots,
-              (int)g->prog_len, (int)g->pred_len};
+              (int)g->prog_len, (int)g->pred_len, g->n_val};
     K12In ki{ref, ref_stride, target, now, Q, I, out_kslack};
     auto launch = [&](auto kern) -> int {
       static const void* attr_done[6] = {};  // one entry per k_slack_select instantiation
@@ -519,7 +524,7 @@ int slack_select_launch(sp_ctx* ctx, sp_dag* g, int n_tables, sp_table* const* t
       const int need = (I + 32 * kK12Warps - 1) / (32 * kK12Warps);
       if (need < blocks) blocks = need;
       kern<<<blocks, 32 * kK12Warps, smem, ctx->stream>>>(kg, ki, pp, (int)(dp + progb),
-                                                          (int)(dp + progb + plans_all), io);
+                                                          (int)(dp + progb + plans_all), out_stage, io);
       SP_CHECK_LAUNCH(ctx);
       return SP_OK;
     };

@@ -155,7 +155,8 @@ __device__ __forceinline__ void store_slack(int i, int s, int n_src, double own,
 // path it found is the one the reference's left-to-right sums make extremal:
 //   backward:  Hb[v] = fl(ref[v] + max(end_v ? 0 : -inf, max_u Hb[u]))   (u: successors)
 //              argmax[v] = the option taken, gap[v] = its value minus the runner-up option's,
-//              rounded down to float (+inf without a runner-up);  min side alike.
+//              rounded down to float (+inf without a runner-up), G[v] = min(gap[v],
+//              G[argmax[v]]) the smallest margin along the path;  min side alike.
 //   Monotone rounding makes Hb[v] = max over paths of the right-nested rounded path sums R, so
 //   following argmax from s gives a path p^ with R(p^) = Hb[s]; the walk recomputes its forward
 //   sum  Tmax = ((0 + r_s) + r_1) + ...  exactly as configurator.py:500-506 does.
@@ -164,7 +165,7 @@ __device__ __forceinline__ void store_slack(int i, int s, int n_src, double own,
 //   With recursive-summation bounds for non-negative terms (|fl - exact| <= g * exact,
 //   g = V u / (1 - V u), u = 2^-53) on the forward sums of p and p^ and on R, p's forward sum
 //   cannot exceed Tmax once gap_j >= 2g A_j + 4.01g Y_j, which min_j gap_j >= theta * Tmax
-//   (theta = 5g + 8u) implies.  So Tmax IS the reference's maximum; the min side mirrors it
+//   (theta = 5g + 8u), i.e. G[s] >= theta * Tmax, implies.  So Tmax IS the reference's maximum; the min side mirrors it
 //   (max orientation on negated values, the same gap test against Tmin).
 // Sources whose certificate fails (near-ties within ~1e-13 relative, exact ties, refs that are
 // negative / non-finite / > 1e300) fall back to the exact forward DP of that source, so the
@@ -173,32 +174,27 @@ __device__ __forceinline__ void store_slack(int i, int s, int n_src, double own,
 // (in max orientation on negated values, so both run the same code) — which halves the shared
 // memory per lane and doubles the resident warps; the walks are then shared out by source
 // parity, two sources per lane in flight.  Per instance and node 26 bytes of shared memory:
-// {Hb, -Lb} (later the walk record {ref, gap_max | gap_min}), the two float gaps, the two args.
+// {Hb, -Lb} (later the walk record {ref, G_max | G_min}), the two float margins, the two args.
 constexpr uint32_t kArgNone = 0xFE, kArgEnd = 0xFF;
 constexpr int kCertWarps = 4;  // 64 instances per block
 
-// one walk step along an extremal path: w = {ref, gap_max | gap_min} of node v; the chain adds
-// ref to its forward sum and keeps the smallest margin seen
+// one walk step along an extremal path: add the node's ref to the forward sum, follow the arg
 struct Walk {
-  uint32_t v;
-  bool on;
+  uint32_t v;  // current node; kArgEnd / kArgNone once the path has ended
   double acc;  // forward sum ((0 + r_s) + r_1) + ... along the path
-  float gap;   // smallest margin of a chosen option over its runner-up on the path
 };
 
 template <bool MAX>
 __device__ __forceinline__ void walk_step(Walk& c, const double2* __restrict__ W,
-                                          const uint16_t* __restrict__ R, bool& none) {
-  if (!c.on) return;
-  const double2 w = W[c.v * 16];
-  const uint32_t rr = R[c.v * 16];
-  const uint32_t nx = MAX ? (rr & 0xFFu) : (rr >> 8);
-  c.acc = __dadd_rn(c.acc, w.x);
-  const float g = __int_as_float(MAX ? __double2loint(w.y) : __double2hiint(w.y));
-  c.gap = g < c.gap ? g : c.gap;
-  none |= nx == kArgNone;
-  c.on = nx < kArgNone;
-  c.v = nx;
+                                          const uint16_t* __restrict__ R) {
+  // branch-free: a finished chain re-reads node 0 and keeps its state
+  const bool on = c.v < kArgNone;
+  const uint32_t v = on ? c.v : 0u;
+  const double rv = W[v * 16].x;
+  const uint32_t rr = R[v * 16];
+  const double acc = __dadd_rn(c.acc, rv);
+  c.acc = on ? acc : c.acc;
+  c.v = on ? (MAX ? (rr & 0xFFu) : (rr >> 8)) : c.v;
 }
 
 __global__ void __launch_bounds__(32 * kCertWarps) k_slack_cert(
@@ -217,16 +213,18 @@ __global__ void __launch_bounds__(32 * kCertWarps) k_slack_cert(
   const uint16_t* VI = reinterpret_cast<const uint16_t*>(smc + off_vidx);
   const uint8_t* TE = smc + off_term;
   const uint8_t* SRC = smc + off_src;
-  const uint8_t* SU = smc + off_succ;
+  const uint16_t* SU = reinterpret_cast<const uint16_t*>(smc + off_succ);  // groups of 4 offsets
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int k = lane >> 1, side = lane & 1;  // instance in the warp, 0 = max / 1 = min side
   const int nfw = (n_src + 31) >> 5;
-  uint8_t* wb = smc + cert_bytes + (size_t)warp * ((size_t)V * 416 + (size_t)nfw * 128);
+  const size_t arow = (size_t)(V + 1) * 256;  // A has a sentinel row V (-inf on both sides)
+  uint8_t* wb = smc + cert_bytes + (size_t)warp * (arow + (size_t)V * 160 + (size_t)nfw * 128);
   // element (v, k, side) of each [V][16][2] array sits at v * 32 + 2k + side
   double* A = reinterpret_cast<double*>(wb) + 2 * k;
-  float* Cf = reinterpret_cast<float*>(wb + (size_t)V * 256) + 2 * k;
-  uint8_t* Rb = wb + (size_t)V * 384 + 2 * k;
-  uint32_t* Fw = reinterpret_cast<uint32_t*>(wb + (size_t)V * 416) + lane;
+  float* Cf = reinterpret_cast<float*>(wb + arow) + 2 * k;
+  uint8_t* Rb = wb + arow + (size_t)V * 128 + 2 * k;
+  uint32_t* Fw = reinterpret_cast<uint32_t*>(wb + arow + (size_t)V * 160) + lane;
+  const char* As = reinterpret_cast<const char*>(A + side);  // + node * 256: this lane's value
   const double2* W = reinterpret_cast<const double2*>(A);  // walk record (v, k) at v * 16
   const uint16_t* R = reinterpret_cast<const uint16_t*>(Rb);
   const int i0 = (blockIdx.x * kCertWarps + warp) * 16;
@@ -236,6 +234,7 @@ __global__ void __launch_bounds__(32 * kCertWarps) k_slack_cert(
   const double* r = ref + (size_t)(live ? i : i0) * ref_stride;
 
   // ---- backward pass in max orientation (the min side negates), reverse topological order ----
+  A[V * 32 + side] = -INFINITY;
   bool bad = false;
   double rn = __ldg(r + VI[V - 1]);
   for (int v = V - 1; v >= 0; --v) {
@@ -244,13 +243,14 @@ __global__ void __launch_bounds__(32 * kCertWarps) k_slack_cert(
     bad |= !(rv >= 0.0 && rv <= 1e300);
     const bool te = TE[v] != 0;
     double h1 = te ? 0.0 : -INFINITY, h2 = -INFINITY;
-    uint32_t a1 = te ? kArgEnd : kArgNone;
-    const int e1 = SP[v + 1];
-    int e = SP[v];
-    for (; e + 4 <= e1; e += 4) {
-      const uint32_t u0 = SU[e], u1 = SU[e + 1], u2 = SU[e + 2], u3 = SU[e + 3];
-      const double x0 = A[u0 * 32 + side], x1 = A[u1 * 32 + side];
-      const double x2 = A[u2 * 32 + side], x3 = A[u3 * 32 + side];
+    uint32_t a1 = te ? (kArgEnd << 8) : (kArgNone << 8);  // chosen option as a byte offset
+    for (int q = SP[v]; q < SP[v + 1]; ++q) {
+      const uint2 w = *reinterpret_cast<const uint2*>(SU + 4 * q);
+      const uint32_t u0 = w.x & 0xFFFFu, u1 = w.x >> 16, u2 = w.y & 0xFFFFu, u3 = w.y >> 16;
+      const double x0 = *reinterpret_cast<const double*>(As + u0);
+      const double x1 = *reinterpret_cast<const double*>(As + u1);
+      const double x2 = *reinterpret_cast<const double*>(As + u2);
+      const double x3 = *reinterpret_cast<const double*>(As + u3);
       // top two of the four (and the arg of the best), merged into the running pair; an exact
       // tie leaves the runner-up equal to the best, which fails the certificate as it must
       const bool g01 = x1 > x0, g23 = x3 > x2;
@@ -270,21 +270,23 @@ __global__ void __launch_bounds__(32 * kCertWarps) k_slack_cert(
       h1 = gt ? M : h1;
       a1 = gt ? iq : a1;
     }
-    for (; e < e1; ++e) {
-      const uint32_t u0 = SU[e];
-      const double x0 = A[u0 * 32 + side];
-      const bool gt = x0 > h1;
-      h2 = gt ? h1 : (x0 > h2 ? x0 : h2);
-      h1 = gt ? x0 : h1;
-      a1 = gt ? u0 : a1;
-    }
+    a1 >>= 8;  // node id, or kArgEnd / kArgNone
     A[v * 32 + side] = __dadd_rn(side ? -rv : rv, h1);
-    Cf[v * 32 + side] = __double2float_rd(__dsub_rd(h1, h2));  // margin of the chosen option
+    // smallest margin along the extremal path from v: this node's chosen option over its
+    // runner-up, then the successor's path (-inf when no path: the certificate fails)
+    float gm = __double2float_rd(__dsub_rd(h1, h2));
+    if (a1 < kArgNone) {
+      const float gn = Cf[a1 * 32 + side];
+      gm = gn < gm ? gn : gm;
+    } else if (a1 == kArgNone) {
+      gm = -INFINITY;
+    }
+    Cf[v * 32 + side] = gm;
     Rb[v * 32 + side] = (uint8_t)a1;
   }
   bad |= __shfl_xor_sync(0xffffffffu, bad, 1);
   __syncwarp();
-  // walk records {ref, gap_max | gap_min}: the even lane brings the ref, the odd lane the gaps
+  // walk records {ref, G_max | G_min}: the even lane brings the ref, the odd lane the margins
   for (int v = 0; v < V; ++v)
     A[v * 32 + side] = side ? *reinterpret_cast<const double*>(Cf + v * 32) : __ldg(r + VI[v]);
   for (int w = 0; w < nfw; ++w) Fw[w * 32] = 0u;
@@ -296,14 +298,13 @@ __global__ void __launch_bounds__(32 * kCertWarps) k_slack_cert(
   for (int g = side; g < n_src; g += 4) {
     const int sa = g, sb = g + 2 < n_src ? g + 2 : -1;
     const uint32_t va = SRC[sa], vb = sb >= 0 ? SRC[sb] : 0u;
-    Walk ha{va, true, 0.0, INFINITY}, la{va, true, 0.0, INFINITY};
-    Walk hb{vb, sb >= 0, 0.0, INFINITY}, lb{vb, sb >= 0, 0.0, INFINITY};
-    bool none_a = false, none_b = false;
-    while (ha.on || la.on || hb.on || lb.on) {
-      walk_step<true>(ha, W, R, none_a);
-      walk_step<false>(la, W, R, none_a);
-      walk_step<true>(hb, W, R, none_b);
-      walk_step<false>(lb, W, R, none_b);
+    Walk ha{va, 0.0}, la{va, 0.0};
+    Walk hb{sb >= 0 ? vb : kArgEnd, 0.0}, lb{sb >= 0 ? vb : kArgEnd, 0.0};
+    while (ha.v < kArgNone || la.v < kArgNone || hb.v < kArgNone || lb.v < kArgNone) {
+      walk_step<true>(ha, W, R);
+      walk_step<false>(la, W, R);
+      walk_step<true>(hb, W, R);
+      walk_step<false>(lb, W, R);
     }
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
@@ -311,12 +312,14 @@ __global__ void __launch_bounds__(32 * kCertWarps) k_slack_cert(
       if (si < 0) continue;
       const Walk& h = q ? hb : ha;
       const Walk& l = q ? lb : la;
-      const bool ok = !bad && !(q ? none_b : none_a) &&
-                      (double)h.gap >= __dmul_ru(theta, h.acc) &&
-                      (double)l.gap >= __dmul_ru(theta, l.acc);
+      const double2 ws = W[SRC[si] * 16];
+      const float gh = __int_as_float(__double2loint(ws.y));
+      const float gl = __int_as_float(__double2hiint(ws.y));
+      const bool ok = !bad && (double)gh >= __dmul_ru(theta, h.acc) &&
+                      (double)gl >= __dmul_ru(theta, l.acc);
       if (ok) {
         if (live) {
-          const double own = __dadd_rn(0.0, W[SRC[si] * 16].x);
+          const double own = __dadd_rn(0.0, ws.x);
           store_slack(i, si, n_src, own, h.acc, l.acc, base, K, Q, out_slack, out_ratio);
         }
       } else {
@@ -398,7 +401,8 @@ int slack_launch(sp_ctx* ctx, sp_dag* g, int I, const double* ref, int ref_strid
   if (g->cert && !(ce && !strcmp(ce, "0"))) {
     const int nfw = (g->n_src + 31) / 32;
     const size_t smem = (size_t)g->cert_bytes +
-                        (size_t)kCertWarps * ((size_t)g->V * 416 + (size_t)nfw * 128);
+                        (size_t)kCertWarps * ((size_t)(g->V + 1) * 256 + (size_t)g->V * 160 +
+                                              (size_t)nfw * 128);
     if (smem <= 227 * 1024) {
       static size_t cert_attr = 0;
       if (smem > 48 * 1024 && smem > cert_attr) {
