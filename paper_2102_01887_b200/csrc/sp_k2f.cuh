@@ -201,6 +201,8 @@ __device__ __forceinline__ void build_lane_lut(const PlanHdr& h, uint32_t* lut) 
   }
 }
 
+constexpr int kK2fDepth = 3;
+
 template <int K, int THREADS = 1024>
 __global__ void __launch_bounds__(THREADS, 1024 / THREADS) k_select_fast(
     const uint8_t* __restrict__ plan, PlanHdr h, FastIO<K> io) {
@@ -232,20 +234,23 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS) k_select_fast(
   }
   const uint32_t stride = gridDim.x * blockDim.x;
   uint32_t i = blockIdx.x * blockDim.x + tid;
-  InF<K> a, b;
-  if (i < io.N) load_fast<K>(io, i, a);
-  if (i + stride < io.N) load_fast<K>(io, i + stride, b);
+  // kK2fDepth register buffers: the next kK2fDepth - 1 invocations of this thread are in
+  // flight while one is decided
+  InF<K> buf[kK2fDepth];
+#pragma unroll
+  for (int q = 0; q < kK2fDepth; ++q)
+    if (i + q * stride < io.N) load_fast<K>(io, i + q * stride, buf[q]);
   __syncthreads();
   mbar_wait(&s_bar, 0);
   uint32_t sb;  // shared-window base of the staged plan, ordered after the wait
   asm volatile("mov.u32 %0, %1;" : "=r"(sb) : "r"(smem_u32(smem)) : "memory");
-  // ping-pong over two register buffers: invocation i + stride is in flight while i is decided
-  for (; i < io.N; i += 2 * stride) {
-    decide_fast<K>(h, sb, (uint32_t)io.lut_bytes_off, io, i, a);
-    const uint32_t j = i + stride;
-    if (j >= io.N) break;
-    if (j + stride < io.N) load_fast<K>(io, j + stride, a);
-    decide_fast<K>(h, sb, (uint32_t)io.lut_bytes_off, io, j, b);
-    if (j + 2 * stride < io.N) load_fast<K>(io, j + 2 * stride, b);
+  for (; i < io.N; i += kK2fDepth * stride) {
+#pragma unroll
+    for (int q = 0; q < kK2fDepth; ++q) {
+      const uint32_t j = i + q * stride;
+      if (j >= io.N) break;
+      decide_fast<K>(h, sb, (uint32_t)io.lut_bytes_off, io, j, buf[q]);
+      if (j + kK2fDepth * stride < io.N) load_fast<K>(io, j + kK2fDepth * stride, buf[q]);
+    }
   }
 }
