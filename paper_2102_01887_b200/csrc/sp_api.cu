@@ -124,6 +124,7 @@ static void free_table(sp_table* t) {
                     t->candf, t->cands, t->cidf, t->cids};
   for (uint32_t* p : uu) cudaFree(p);
   cudaFree(t->sort_tmp);
+  cudaFree(t->fin_chunk);
   for (auto& p : t->plans) plan_release(p);
   delete t;
 }

@@ -167,6 +167,7 @@ struct sp_table {
   int32_t* dev_counters = nullptr;            // [0] = completed_ref (device copy)
   uint32_t *candf = nullptr, *cands = nullptr;  // M flags each
   uint32_t *cidf = nullptr, *cids = nullptr;    // M maps each
+  int2* fin_chunk = nullptr;  // 2 x ceil(M / 256): per-chunk candidate counts, then bases
   double* ukey = nullptr;                       // 2M: unified candidate scores (CP then CS)
   uint32_t* ukr = nullptr;                      // 2M: unified candidate r1 ranks
   int32_t* uent = nullptr;                      // 2M: unified candidate entry index

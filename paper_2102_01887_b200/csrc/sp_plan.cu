@@ -687,6 +687,8 @@ __global__ void __launch_bounds__(1024) k_stair_smem(int M, int K, int W, KindIn
 // a new row (see k_stair_smem); a row's lane values are read from the scanned lane lists at
 // (#lane positions before the boundary).
 constexpr int kStairLanesMax = 8192;
+constexpr int kFinChunk = 256;  // entries per compaction chunk (<= 1024 chunks: M <= 262,144)
+constexpr int kStairLanesPer = (kStairLanesMax + 1 + 1023) / 1024;  // boundaries per thread
 
 // exclusive block scan of NW packed u32 words (two 16-bit counters each)
 template <int NW>
@@ -986,13 +988,29 @@ __global__ void __launch_bounds__(1024) k_stair_lanes(int M, int K, int W, KindI
   }
   int total = 0;
   int row = block_excl_sum(cnt, s_warp, &total);
+  // the row thresholds (latency of the position before each boundary), all loads in flight
+  // together: p1 - p0 <= kStairLanesPer for the kinds this kernel takes
+  double thv[kStairLanesPer];
+  {
+    int ev[kStairLanesPer];
+#pragma unroll
+    for (int u = 0; u < kStairLanesPer; ++u) {
+      const int p = p0 + u;
+      ev[u] = (p < p1 && p > 0 && ((chmask >> u) & 1u)) ? order[base + p - 1] : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < kStairLanesPer; ++u) thv[u] = ev[u] >= 0 ? lat[ev[u]] : -INFINITY;
+  }
   {
     uint32_t c_b[WM];  // #lane-b positions before boundary p
 #pragma unroll
     for (int b = 0; b < WM; ++b) c_b[b] = before[b];
-    for (int p = p0; p < p1; ++p) {
-      if ((chmask >> (p - p0)) & 1u) {
-        thrscratch[ext + row] = (p == 0) ? -INFINITY : lat[order[base + p - 1]];
+#pragma unroll
+    for (int u = 0; u < kStairLanesPer; ++u) {
+      const int p = p0 + u;
+      if (p >= p1) break;
+      if ((chmask >> u) & 1u) {
+        thrscratch[ext + row] = thv[u];
         uint32_t* rr = rowscratch + (size_t)(ext + row) * (2 * W);
 #pragma unroll
         for (int b = 0; b < WM; ++b) {
@@ -1031,50 +1049,36 @@ __device__ __forceinline__ bool key_lt(double sa, uint32_t ra, double sb, uint32
 //                (penalized side) in r2 order; both lists ascend in (score, r1)
 //   k_fin_merge  unified ids: own position + #keys of the other list before it
 //   k_fin_fill   lane lookup table, thresholds, staircase rows, buckets, candidate records
+// candidate counts of every 256-entry chunk (the compaction of the two candidate sets runs over
+// many CTAs: counts here, one scan of the chunk counts in k_fin_head, the in-chunk scan and the
+// ids in k_fin_keys)
+__global__ void __launch_bounds__(kFinChunk) k_fin_count(int M, const uint32_t* __restrict__ candf,
+                                                        const uint32_t* __restrict__ cands,
+                                                        int2* chunk_cnt) {
+  const int r = blockIdx.x * kFinChunk + threadIdx.x;
+  const int nf = __syncthreads_count(r < M && candf[r] != 0);
+  const int ns = __syncthreads_count(r < M && cands[r] != 0);
+  if (threadIdx.x == 0) chunk_cnt[blockIdx.x] = make_int2(nf, ns);
+}
+
 __global__ void __launch_bounds__(1024) k_fin_head(
     int M, int K, int nB, KindInfo ki, const int32_t* __restrict__ rows_per_kind,
-    const double* __restrict__ thrscratch, const uint32_t* __restrict__ candf,
-    const uint32_t* __restrict__ cands, uint32_t* cidf, uint32_t* cids, PlanHdr hdr_in,
-    uint8_t* image, int64_t image_cap, int32_t* status) {
+    const double* __restrict__ thrscratch, int nchunks, const int2* __restrict__ chunk_cnt,
+    int2* chunk_base, PlanHdr hdr_in, uint8_t* image, int64_t image_cap, int32_t* status) {
   __shared__ int s_warp[32];
   __shared__ PlanHdr hdr;
   __shared__ int s_ncp, s_ncs;
-  {
-    // flags staged into shared memory with coalesced loads, then each thread scans a contiguous
-    // run of them (one block scan per set); ids written back coalesced from shared memory
-    extern __shared__ uint8_t s_fl[];  // [M] feasible flags, [M] penalized flags
-    uint16_t* s_id = reinterpret_cast<uint16_t*>(s_fl + ((2 * M + 15) & ~15));  // [2][M] ids
-    for (int r = threadIdx.x; r < M; r += blockDim.x) {
-      s_fl[r] = candf[r] != 0;
-      s_fl[M + r] = cands[r] != 0;
-    }
-    __syncthreads();
-    const int T = blockDim.x;
-    const int P = (M + T - 1) / T;
-    const int r0 = min((int)threadIdx.x * P, M), r1e = min(r0 + P, M);
-    int nf = 0, ns = 0;
-    for (int r = r0; r < r1e; ++r) {
-      nf += s_fl[r];
-      ns += s_fl[M + r];
-    }
+  {  // exclusive scan of the per-chunk counts (nchunks <= blockDim.x)
+    const int2 c = (int)threadIdx.x < nchunks ? chunk_cnt[threadIdx.x] : make_int2(0, 0);
     int tf = 0, ts = 0;
-    int cf = block_excl_sum(nf, s_warp, &tf);
-    int cs = block_excl_sum(ns, s_warp, &ts);
-    for (int r = r0; r < r1e; ++r) {
-      s_id[r] = (uint16_t)cf;
-      s_id[M + r] = (uint16_t)cs;
-      cf += s_fl[r];
-      cs += s_fl[M + r];
-    }
+    const int bf = block_excl_sum(c.x, s_warp, &tf);
+    const int bs = block_excl_sum(c.y, s_warp, &ts);
+    if ((int)threadIdx.x < nchunks) chunk_base[threadIdx.x] = make_int2(bf, bs);
     if (threadIdx.x == 0) {
       s_ncp = tf;
       s_ncs = ts;
     }
     __syncthreads();
-    for (int r = threadIdx.x; r < M; r += blockDim.x) {
-      cidf[r] = s_id[r];
-      cids[r] = s_id[M + r];
-    }
   }
   const int ncp = s_ncp, ncs = s_ncs;
   // per-kind bucket geometry in parallel (one thread per kind), offsets by thread 0
@@ -1146,26 +1150,44 @@ __global__ void __launch_bounds__(1024) k_fin_head(
         reinterpret_cast<const uint32_t*>(&hdr)[threadIdx.x];
 }
 
-__global__ void k_fin_keys(int M, const uint8_t* __restrict__ image,
-                           const uint32_t* __restrict__ candf, const uint32_t* __restrict__ cands,
-                           const uint32_t* __restrict__ cidf, const uint32_t* __restrict__ cids,
-                           const int32_t* __restrict__ ent_r1, const int32_t* __restrict__ ent_r2,
-                           const uint32_t* __restrict__ r1, const double* __restrict__ cost,
-                           const double* __restrict__ costpen, double* ukey, uint32_t* ukr,
-                           int32_t* uent) {
+__global__ void __launch_bounds__(kFinChunk) k_fin_keys(
+    int M, const uint8_t* __restrict__ image, const uint32_t* __restrict__ candf,
+    const uint32_t* __restrict__ cands, const int2* __restrict__ chunk_base, uint32_t* cidf,
+    uint32_t* cids, const int32_t* __restrict__ ent_r1, const int32_t* __restrict__ ent_r2,
+    const uint32_t* __restrict__ r1, const double* __restrict__ cost,
+    const double* __restrict__ costpen, double* ukey, uint32_t* ukr, int32_t* uent) {
   const PlanHdr* H = reinterpret_cast<const PlanHdr*>(image);
   if (H->magic != kPlanMagic) return;
   const int ncp = H->ncp;
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  const int r = blockIdx.x * kFinChunk + threadIdx.x;
+  // compaction ids: chunk base + exclusive count inside the chunk (order-preserving)
+  __shared__ int s_wf[kFinChunk / 32], s_ws[kFinChunk / 32];
+  const bool f = r < M && candf[r] != 0, sflag = r < M && cands[r] != 0;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t bf = __ballot_sync(0xffffffffu, f), bs = __ballot_sync(0xffffffffu, sflag);
+  const uint32_t below = (1u << lane) - 1u;
+  if (lane == 0) {
+    s_wf[w] = __popc(bf);
+    s_ws[w] = __popc(bs);
+  }
+  __syncthreads();
+  int of = __popc(bf & below), os = __popc(bs & below);
+  for (int q = 0; q < w; ++q) {
+    of += s_wf[q];
+    os += s_ws[q];
+  }
+  const int2 base = chunk_base[blockIdx.x];
   if (r >= M) return;
-  if (candf[r]) {
-    const int c = (int)cidf[r], e = ent_r1[r];
+  cidf[r] = (uint32_t)(base.x + of);
+  cids[r] = (uint32_t)(base.y + os);
+  if (f) {
+    const int c = base.x + of, e = ent_r1[r];
     ukey[c] = cost[e];
     ukr[c] = (uint32_t)r;
     uent[c] = e;
   }
-  if (cands[r]) {
-    const int c = ncp + (int)cids[r], e = ent_r2[r];
+  if (sflag) {
+    const int c = ncp + base.y + os, e = ent_r2[r];
     ukey[c] = costpen[e];
     ukr[c] = r1[e];
     uent[c] = e;
@@ -1226,12 +1248,24 @@ __global__ void k_fin_fill(int K, int W, KindInfo ki, const double* __restrict__
     // row r: lane b = min(unified id of the best feasible, of the best penalized entry with
     // batch size batch_vals[b]); stored as the minimum over every lane interval [lo, hi]
     for (int r = g; r < R; r += gs) {
-      uint32_t lane[kMaxB];
-      for (int b = 0; b < nB; ++b) {
-        const uint32_t a = rowscratch[(size_t)(ext + r) * (2 * W) + b];
-        const uint32_t s = rowscratch[(size_t)(ext + r) * (2 * W) + W + b];
-        const uint32_t ua = a != kInf32 ? umap[cidf[a]] : kInf32;
-        const uint32_t us = s != kInf32 ? umap[ncp + cids[s]] : kInf32;
+      // three rounds of independent loads (row words, candidate ids, unified ids) instead of
+      // one dependent chain per lane
+      uint32_t lane[kMaxB], ia[kMaxB], is[kMaxB];
+      const uint32_t* rw = rowscratch + (size_t)(ext + r) * (2 * W);
+#pragma unroll
+      for (int b = 0; b < kMaxB; ++b) {
+        ia[b] = b < nB ? rw[b] : kInf32;
+        is[b] = b < nB ? rw[W + b] : kInf32;
+      }
+#pragma unroll
+      for (int b = 0; b < kMaxB; ++b) {
+        ia[b] = ia[b] != kInf32 ? cidf[ia[b]] : kInf32;
+        is[b] = is[b] != kInf32 ? ncp + cids[is[b]] : kInf32;
+      }
+#pragma unroll
+      for (int b = 0; b < kMaxB; ++b) {
+        const uint32_t ua = ia[b] != kInf32 ? umap[ia[b]] : kInf32;
+        const uint32_t us = is[b] != kInf32 ? umap[is[b]] : kInf32;
         lane[b] = min(ua, us);
       }
       uint16_t* out = reinterpret_cast<uint16_t*>(image + d.rows_off + (size_t)r * H->row_stride);
@@ -1261,9 +1295,19 @@ __global__ void k_fin_fill(int K, int W, KindInfo ki, const double* __restrict__
       const uint32_t kmin = d.kmin_hi;
       for (int b = threadIdx.x; b < nbk; b += blockDim.x) s_h[b] = 0u;
       __syncthreads();
-      for (int j = 1 + (int)threadIdx.x; j < R; j += blockDim.x) {
-        const uint32_t kk = (uint32_t)__double2hiint(thrscratch[ext + j]);
-        atomicAdd(&s_h[min((kk - kmin) >> shift, (uint32_t)(nbk - 1))], 1u);
+      for (int j0 = 1 + (int)threadIdx.x; j0 < R; j0 += 8 * blockDim.x) {
+        double tv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int j = j0 + u * blockDim.x;
+          tv[u] = j < R ? thrscratch[ext + j] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (j0 + u * (int)blockDim.x >= R) break;
+          const uint32_t kk = (uint32_t)__double2hiint(tv[u]);
+          atomicAdd(&s_h[min((kk - kmin) >> shift, (uint32_t)(nbk - 1))], 1u);
+        }
       }
       __syncthreads();
       const int per = (nbk + blockDim.x - 1) / blockDim.x;
@@ -1333,6 +1377,7 @@ int plan_scratch_alloc(sp_table* t) {
     SP_CUDA(cudaMalloc(&t->cands, sizeof(uint32_t) * M));
     SP_CUDA(cudaMalloc(&t->cidf, sizeof(uint32_t) * M));
     SP_CUDA(cudaMalloc(&t->cids, sizeof(uint32_t) * M));
+    SP_CUDA(cudaMalloc(&t->fin_chunk, sizeof(int2) * 2 * ((M + kFinChunk - 1) / kFinChunk)));
     SP_CUDA(cudaMalloc(&t->ukey, sizeof(double) * 2 * M));
     SP_CUDA(cudaMalloc(&t->ukr, sizeof(uint32_t) * 2 * M));
     SP_CUDA(cudaMalloc(&t->uent, sizeof(int32_t) * 2 * M));
@@ -1451,17 +1496,17 @@ static int plan_enqueue(sp_ctx* ctx, sp_table* t, Plan& p) {
   h.K = K;
   for (int b = 0; b < kMaxB; ++b) h.batch_vals[b] = b < t->nB ? t->batch_vals[b] : INT32_MAX;
   int32_t* status = t->rows_per_kind + kMaxKinds;
-  static bool fin_attr = false;
-  if (!fin_attr) {
-    SP_CUDA(cudaFuncSetAttribute(k_fin_head, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 6 * 32768 + 16));
-    fin_attr = true;
-  }
-  k_fin_head<<<1, 1024, ((2 * M + 15) & ~15) + 4 * M, st>>>(M, K, t->nB, ki, t->rows_per_kind, t->thrscratch, t->candf,
-                                 t->cands, t->cidf, t->cids, h, p.image, p.image_cap, status);
+  const int nfc = (M + kFinChunk - 1) / kFinChunk;
+  int2* chunk_cnt = t->fin_chunk;
+  int2* chunk_base = t->fin_chunk + nfc;
+  k_fin_count<<<nfc, kFinChunk, 0, st>>>(M, t->candf, t->cands, chunk_cnt);
   SP_CHECK_LAUNCH(ctx);
-  k_fin_keys<<<nb, 256, 0, st>>>(M, p.image, t->candf, t->cands, t->cidf, t->cids, t->ent_r1,
-                                 t->ent_r2, t->r1, p.cost, p.costpen, t->ukey, t->ukr, t->uent);
+  k_fin_head<<<1, 1024, 0, st>>>(M, K, t->nB, ki, t->rows_per_kind, t->thrscratch, nfc, chunk_cnt,
+                                 chunk_base, h, p.image, p.image_cap, status);
+  SP_CHECK_LAUNCH(ctx);
+  k_fin_keys<<<nfc, kFinChunk, 0, st>>>(M, p.image, t->candf, t->cands, chunk_base, t->cidf,
+                                        t->cids, t->ent_r1, t->ent_r2, t->r1, p.cost, p.costpen,
+                                        t->ukey, t->ukr, t->uent);
   SP_CHECK_LAUNCH(ctx);
   k_fin_merge<<<(2 * M + 255) / 256, 256, 0, st>>>(p.image, t->ukey, t->ukr, t->umap);
   SP_CHECK_LAUNCH(ctx);
