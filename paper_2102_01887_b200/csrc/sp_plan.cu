@@ -1216,73 +1216,15 @@ __global__ void k_fin_merge(const uint8_t* __restrict__ image, const double* __r
   umap[c] = (uint32_t)((is_cp ? c : c - ncp) + (lo - base));
 }
 
-__global__ void k_fin_fill(int K, int W, KindInfo ki, const double* __restrict__ thrscratch,
-                           const uint32_t* __restrict__ rowscratch,
-                           const uint32_t* __restrict__ cidf, const uint32_t* __restrict__ cids,
-                           const double* __restrict__ ukey, const int32_t* __restrict__ uent,
-                           const uint32_t* __restrict__ umap, const double* __restrict__ lat,
-                           const int32_t* __restrict__ batch, const int32_t* __restrict__ kind,
-                           uint8_t* image) {
+// bucket tables, one CTA per kind (runs beside the row / record fill)
+__global__ void __launch_bounds__(1024) k_fin_buckets(KindInfo ki, const double* __restrict__ thrscratch,
+                                                      uint8_t* image) {
   const PlanHdr* H = reinterpret_cast<const PlanHdr*>(image);
   if (H->magic != kPlanMagic) return;
-  const int g = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
-  const int nB = H->nB, ncp = H->ncp, ncand = H->ncp + H->ncs;
-  {  // batch lookup table of the generic kernels
-    uint16_t* lut = reinterpret_cast<uint16_t*>(image + H->lut_off);
-    for (int v = g; v < H->lut_n; v += gs) {
-      int lo = 0, le = 0;
-      for (int b = 0; b < nB; ++b) {
-        lo += H->batch_vals[b] < v;
-        le += H->batch_vals[b] <= v;
-      }
-      lut[v] = (uint16_t)(lo | (le << 8));
-    }
-  }
-  for (int k = 0; k < K; ++k) {
-    const KindDesc d = H->kd[k];
-    const int R = d.R;
-    if (R == 0) continue;
-    const int ext = ki.base[k] + k;
-    double* thr = reinterpret_cast<double*>(image + d.thr_off);
-    for (int r = g; r < R; r += gs) thr[r] = thrscratch[ext + r];
-    // row r: lane b = min(unified id of the best feasible, of the best penalized entry with
-    // batch size batch_vals[b]); stored as the minimum over every lane interval [lo, hi]
-    for (int r = g; r < R; r += gs) {
-      // three rounds of independent loads (row words, candidate ids, unified ids) instead of
-      // one dependent chain per lane
-      uint32_t lane[kMaxB], ia[kMaxB], is[kMaxB];
-      const uint32_t* rw = rowscratch + (size_t)(ext + r) * (2 * W);
-#pragma unroll
-      for (int b = 0; b < kMaxB; ++b) {
-        ia[b] = b < nB ? rw[b] : kInf32;
-        is[b] = b < nB ? rw[W + b] : kInf32;
-      }
-#pragma unroll
-      for (int b = 0; b < kMaxB; ++b) {
-        ia[b] = ia[b] != kInf32 ? cidf[ia[b]] : kInf32;
-        is[b] = is[b] != kInf32 ? ncp + cids[is[b]] : kInf32;
-      }
-#pragma unroll
-      for (int b = 0; b < kMaxB; ++b) {
-        const uint32_t ua = ia[b] != kInf32 ? umap[ia[b]] : kInf32;
-        const uint32_t us = is[b] != kInf32 ? umap[is[b]] : kInf32;
-        lane[b] = min(ua, us);
-      }
-      uint16_t* out = reinterpret_cast<uint16_t*>(image + d.rows_off + (size_t)r * H->row_stride);
-      int q = 0;
-      for (int lo = 0; lo < nB; ++lo) {
-        uint32_t m = kInf32;
-        for (int hi = lo; hi < nB; ++hi) {
-          m = min(m, lane[hi]);
-          out[q++] = m == kInf32 ? kNone16 : (uint16_t)m;
-        }
-      }
-    }
-  }
   // bucket b holds thresholds j in [1, R) with (key_j - kmin) >> shift == b:
   // entry = (#thresholds in lower buckets) | (#thresholds in b) << 16 — CTA k builds kind k's
   // table from a shared-memory histogram and one block scan (no per-bucket searches)
-  if ((int)blockIdx.x < K) {
+  {
     __shared__ uint32_t s_h[kMaxBuckets];
     __shared__ int s_warp[32];
     const int k = blockIdx.x;
@@ -1320,6 +1262,76 @@ __global__ void k_fin_fill(int K, int W, KindInfo ki, const double* __restrict__
         const uint32_t c = s_h[b];
         bkt[b] = (uint32_t)below | (c << 16);
         below += (int)c;
+      }
+    }
+  }
+}
+
+__global__ void k_fin_fill(int K, int W, const __grid_constant__ KindInfo ki,
+                           const double* __restrict__ thrscratch,
+                           const uint32_t* __restrict__ rowscratch,
+                           const uint32_t* __restrict__ cidf, const uint32_t* __restrict__ cids,
+                           const double* __restrict__ ukey, const int32_t* __restrict__ uent,
+                           const uint32_t* __restrict__ umap, const double* __restrict__ lat,
+                           const int32_t* __restrict__ batch, const int32_t* __restrict__ kind,
+                           uint8_t* image) {
+  const PlanHdr* H = reinterpret_cast<const PlanHdr*>(image);
+  if (H->magic != kPlanMagic) return;
+  const int g = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
+  const int nB = H->nB, ncp = H->ncp, ncand = H->ncp + H->ncs;
+  {  // batch lookup table of the generic kernels
+    uint16_t* lut = reinterpret_cast<uint16_t*>(image + H->lut_off);
+    for (int v = g; v < H->lut_n; v += gs) {
+      int lo = 0, le = 0;
+      for (int b = 0; b < nB; ++b) {
+        lo += H->batch_vals[b] < v;
+        le += H->batch_vals[b] <= v;
+      }
+      lut[v] = (uint16_t)(lo | (le << 8));
+    }
+  }
+  for (int k = 0; k < K; ++k) {
+    const KindDesc d = H->kd[k];
+    const int R = d.R;
+    if (R == 0) continue;
+    const int ext = ki.base[k] + k;
+    double* thr = reinterpret_cast<double*>(image + d.thr_off);
+    for (int r = g; r < R; r += gs) thr[r] = thrscratch[ext + r];
+    // row r: lane b = min(unified id of the best feasible, of the best penalized entry with
+    // batch size batch_vals[b]); stored as the minimum over every lane interval [lo, hi] at
+    // tri(lo) + hi - lo.  One warp per row: lane b resolves batch lane b (three independent
+    // loads), every lane then folds one or more intervals from the shuffled lane values and the
+    // row's nB(nB+1)/2 u16 are stored contiguously (thread-per-row stores were one sector per
+    // lane and queued for ~20 us on the few SMs holding the rows)
+    const int wg = g >> 5, nwg = gs >> 5, ln = threadIdx.x & 31;
+    const int nq = nB * (nB + 1) / 2;
+    for (int r = wg; r < R; r += nwg) {
+      const uint32_t* rw = rowscratch + (size_t)(ext + r) * (2 * W);
+      uint32_t v = kInf32;
+      if (ln < nB) {
+        const uint32_t a = rw[ln], c = rw[W + ln];
+        const uint32_t ua = a != kInf32 ? umap[cidf[a]] : kInf32;
+        const uint32_t us = c != kInf32 ? umap[ncp + cids[c]] : kInf32;
+        v = min(ua, us);
+      }
+      uint16_t* out = reinterpret_cast<uint16_t*>(image + d.rows_off + (size_t)r * H->row_stride);
+      for (int q0 = 0; q0 < nq; q0 += 32) {
+        const int q = q0 + ln;
+        int lo = 0, hi = -1;
+        if (q < nq) {  // decode q -> (lo, hi)
+          int rem = q;
+          while (rem >= nB - lo) {
+            rem -= nB - lo;
+            ++lo;
+          }
+          hi = lo + rem;
+        }
+        uint32_t m = kInf32;
+        for (int bb = 0; bb < nB; ++bb) {
+          const uint32_t vb = __shfl_sync(0xffffffffu, v, bb);
+          if (bb >= lo && bb <= hi) m = min(m, vb);
+        }
+        if (q < nq) out[q] = m == kInf32 ? kNone16 : (uint16_t)m;
       }
     }
   }
@@ -1509,6 +1521,8 @@ static int plan_enqueue(sp_ctx* ctx, sp_table* t, Plan& p) {
                                         t->ukey, t->ukr, t->uent);
   SP_CHECK_LAUNCH(ctx);
   k_fin_merge<<<(2 * M + 255) / 256, 256, 0, st>>>(p.image, t->ukey, t->ukr, t->umap);
+  SP_CHECK_LAUNCH(ctx);
+  k_fin_buckets<<<K, 1024, 0, st>>>(ki, t->thrscratch, p.image);
   SP_CHECK_LAUNCH(ctx);
   k_fin_fill<<<std::max(K, std::min(ctx->num_sms * 4, std::max(1, (2 * M + 255) / 256))), 256, 0,
                st>>>(
