@@ -125,6 +125,9 @@ static void free_table(sp_table* t) {
   for (uint32_t* p : uu) cudaFree(p);
   cudaFree(t->sort_tmp);
   cudaFree(t->fin_chunk);
+  cudaFree(t->pos_r12);
+  cudaFree(t->pos_meta);
+  cudaFree(t->pos_lat);
   for (auto& p : t->plans) plan_release(p);
   delete t;
 }

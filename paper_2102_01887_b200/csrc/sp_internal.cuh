@@ -168,6 +168,11 @@ struct sp_table {
   uint32_t *candf = nullptr, *cands = nullptr;  // M flags each
   uint32_t *cidf = nullptr, *cids = nullptr;    // M maps each
   int2* fin_chunk = nullptr;  // 2 x ceil(M / 256): per-chunk candidate counts, then bases
+  // per position of the kind-major latency order: {r1, r2}, lane | new-latency << 7, latency
+  // (gathered by a wide kernel so the one-CTA-per-kind staircase reads them coalesced)
+  uint2* pos_r12 = nullptr;
+  uint8_t* pos_meta = nullptr;
+  double* pos_lat = nullptr;
   double* ukey = nullptr;                       // 2M: unified candidate scores (CP then CS)
   uint32_t* ukr = nullptr;                      // 2M: unified candidate r1 ranks
   int32_t* uent = nullptr;                      // 2M: unified candidate entry index

@@ -802,6 +802,26 @@ __device__ __forceinline__ SegMin block_excl_segmin(SegMin v, int rank, uint32_t
   return prev;
 }
 
+// Per position q of the kind-major latency order (entry e = order[q]): {r1[e], r2[e]},
+// lane | (latency differs from the previous position of the kind) << 7, and lat[e] — the
+// gathers of k_stair_lanes' staging spread over every SM instead of one CTA per kind.
+__global__ void k_stair_stage(int M, int K, const __grid_constant__ KindInfo ki,
+                              const int32_t* __restrict__ order, const int32_t* __restrict__ bidx,
+                              const double* __restrict__ lat, const uint32_t* __restrict__ r1,
+                              const uint32_t* __restrict__ r2, uint2* pos_r12, uint8_t* pos_meta,
+                              double* pos_lat) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= M) return;
+  bool first = false;
+  for (int k = 0; k < K; ++k) first |= q == ki.base[k];
+  const int e = order[q];
+  const double l = lat[e];
+  const bool sisb = !first && q > 0 && l != lat[order[q - 1]];
+  pos_r12[q] = make_uint2(r1[e], r2[e]);
+  pos_meta[q] = (uint8_t)(bidx[e] | (sisb ? 0x80 : 0));
+  pos_lat[q] = l;
+}
+
 template <int NWW>  // NWW = W / 2 packed words (W = 8 -> 4, W = 16 -> 8)
 __global__ void __launch_bounds__(1024) k_stair_lanes(int M, int K, int W, KindInfo ki,
                                                       const int32_t* __restrict__ order,
@@ -811,7 +831,10 @@ __global__ void __launch_bounds__(1024) k_stair_lanes(int M, int K, int W, KindI
                                                       const uint32_t* __restrict__ r2,
                                                       double* thrscratch, uint32_t* rowscratch,
                                                       int32_t* rows_per_kind, uint32_t* candf,
-                                                      uint32_t* cands) {
+                                                      uint32_t* cands,
+                                                      const uint2* __restrict__ pos_r12,
+                                                      const uint8_t* __restrict__ pos_meta,
+                                                      const double* __restrict__ pos_lat) {
   constexpr int WM = 2 * NWW;  // lanes held in registers
   extern __shared__ __align__(16) uint8_t s_l[];
   __shared__ int s_warp[32];
@@ -838,23 +861,24 @@ __global__ void __launch_bounds__(1024) k_stair_lanes(int M, int K, int W, KindI
   uint8_t* impP = sisb + C;
   uint8_t* impS = impP + C;
   uint16_t* scnt = reinterpret_cast<uint16_t*>(pr1);  // #flags before p (after the scatter)
-  // ---- 1. stage (coalesced) ----
+  // ---- 1. stage (coalesced: k_stair_stage gathered the per-position records) ----
   for (int q0 = t; q0 < Mk; q0 += 4 * T) {
-    int e[4], e1[4];
+    uint2 rr[4];
+    uint32_t mm[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int q = q0 + u * T;
-      e[u] = q < Mk ? order[base + q] : 0;
-      e1[u] = (q < Mk && q > 0) ? order[base + q - 1] : 0;
+      rr[u] = q < Mk ? pos_r12[base + q] : make_uint2(0u, 0u);
+      mm[u] = q < Mk ? pos_meta[base + q] : 0u;
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int q = q0 + u * T;
       if (q < Mk) {
-        plane[q] = (uint8_t)bidx[e[u]];
-        pr1[q] = r1[e[u]];
-        pr2[q] = r2[e[u]];
-        sisb[q] = q > 0 && lat[e[u]] != lat[e1[u]];
+        plane[q] = (uint8_t)(mm[u] & 0x7Fu);
+        pr1[q] = rr[u].x;
+        pr2[q] = rr[u].y;
+        sisb[q] = (uint8_t)(mm[u] >> 7);
       }
     }
   }
@@ -991,15 +1015,10 @@ __global__ void __launch_bounds__(1024) k_stair_lanes(int M, int K, int W, KindI
   // the row thresholds (latency of the position before each boundary), all loads in flight
   // together: p1 - p0 <= kStairLanesPer for the kinds this kernel takes
   double thv[kStairLanesPer];
-  {
-    int ev[kStairLanesPer];
 #pragma unroll
-    for (int u = 0; u < kStairLanesPer; ++u) {
-      const int p = p0 + u;
-      ev[u] = (p < p1 && p > 0 && ((chmask >> u) & 1u)) ? order[base + p - 1] : -1;
-    }
-#pragma unroll
-    for (int u = 0; u < kStairLanesPer; ++u) thv[u] = ev[u] >= 0 ? lat[ev[u]] : -INFINITY;
+  for (int u = 0; u < kStairLanesPer; ++u) {
+    const int p = p0 + u;
+    thv[u] = (p < p1 && p > 0 && ((chmask >> u) & 1u)) ? pos_lat[base + p - 1] : -INFINITY;
   }
   {
     uint32_t c_b[WM];  // #lane-b positions before boundary p
@@ -1390,6 +1409,9 @@ int plan_scratch_alloc(sp_table* t) {
     SP_CUDA(cudaMalloc(&t->cidf, sizeof(uint32_t) * M));
     SP_CUDA(cudaMalloc(&t->cids, sizeof(uint32_t) * M));
     SP_CUDA(cudaMalloc(&t->fin_chunk, sizeof(int2) * 2 * ((M + kFinChunk - 1) / kFinChunk)));
+    SP_CUDA(cudaMalloc(&t->pos_r12, sizeof(uint2) * M));
+    SP_CUDA(cudaMalloc(&t->pos_meta, M));
+    SP_CUDA(cudaMalloc(&t->pos_lat, sizeof(double) * M));
     SP_CUDA(cudaMalloc(&t->ukey, sizeof(double) * 2 * M));
     SP_CUDA(cudaMalloc(&t->ukr, sizeof(uint32_t) * 2 * M));
     SP_CUDA(cudaMalloc(&t->uent, sizeof(int32_t) * 2 * M));
@@ -1480,16 +1502,21 @@ static int plan_enqueue(sp_ctx* ctx, sp_table* t, Plan& p) {
     lanes_attr = true;
   }
   if (max_mk <= kStairLanesMax && !getenv("SP_STAIR_SMEM") && !getenv("SP_STAIR_GLOBAL")) {
+    k_stair_stage<<<(M + 255) / 256, 256, 0, st>>>(M, K, ki, t->order, t->bidx, t->lat, t->r1,
+                                                   t->r2, t->pos_r12, t->pos_meta, t->pos_lat);
+    SP_CHECK_LAUNCH(ctx);
     if (W <= 8)
       k_stair_lanes<4><<<K, 1024, kStairLanesSmem, st>>>(M, K, W, ki, t->order, t->bidx, t->lat,
                                                          t->r1, t->r2, t->thrscratch,
                                                          t->rowscratch, t->rows_per_kind,
-                                                         t->candf, t->cands);
+                                                         t->candf, t->cands, t->pos_r12,
+                                                         t->pos_meta, t->pos_lat);
     else
       k_stair_lanes<8><<<K, 1024, kStairLanesSmem, st>>>(M, K, W, ki, t->order, t->bidx, t->lat,
                                                          t->r1, t->r2, t->thrscratch,
                                                          t->rowscratch, t->rows_per_kind,
-                                                         t->candf, t->cands);
+                                                         t->candf, t->cands, t->pos_r12,
+                                                         t->pos_meta, t->pos_lat);
   } else if (max_mk <= kStairSmemMax && !getenv("SP_STAIR_GLOBAL"))
     k_stair_smem<<<K, 1024, kStairSmemBytes, st>>>(M, K, W, ki, t->order, t->bidx, t->lat, t->r1,
                                                    t->r2, t->thrscratch, t->rowscratch,
