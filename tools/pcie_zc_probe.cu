@@ -51,9 +51,11 @@ int main() {
   cudaStream_t s1, s2;
   cudaStreamCreate(&s1);
   cudaStreamCreate(&s2);
-  cudaEvent_t a, b;
+  cudaEvent_t a, b, c, d;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
+  cudaEventCreateWithFlags(&c, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&d, cudaEventDisableTiming);
   int sms;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   auto time = [&](auto fn, const char* name, double bytes) {
@@ -71,12 +73,12 @@ int main() {
   time([&] { cudaMemcpyAsync(din, hin, IN, cudaMemcpyHostToDevice, s1); }, "memcpy H2D 32MB", IN);
   time([&] { cudaMemcpyAsync(hout, dout, OUT, cudaMemcpyDeviceToHost, s1); }, "memcpy D2H 36MB", OUT);
   time([&] {
-    cudaEventRecord(a, s1);
-    cudaStreamWaitEvent(s2, a);
+    cudaEventRecord(c, s1);  // fork s2 off s1, join it back (the timing events stay on s1)
+    cudaStreamWaitEvent(s2, c);
     cudaMemcpyAsync(din, hin, IN, cudaMemcpyHostToDevice, s1);
     cudaMemcpyAsync(hout, dout, OUT, cudaMemcpyDeviceToHost, s2);
-    cudaEventRecord(b, s2);
-    cudaStreamWaitEvent(s1, b);
+    cudaEventRecord(d, s2);
+    cudaStreamWaitEvent(s1, d);
   }, "memcpy H2D||D2H", IN + OUT);
   for (int blocks : {sms, 4 * sms}) {
     char nm[64];
