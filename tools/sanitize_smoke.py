@@ -1,6 +1,6 @@
 """Small end-to-end exercise of every kernel family for compute-sanitizer runs (memcheck,
 racecheck, synccheck): K2f/K2b/K2a select, plan build (sorts, stair, finalize, graph replay),
-K1 slack, K3 fold, commit rounds."""
+K1 slack, K1c certified slack (with fallbacks), K3 fold, commit rounds, quantiles."""
 import sys
 
 import numpy as np
@@ -32,4 +32,21 @@ out = sp.commit_round(tabs, rng.uniform(-1, 10, (R, 2, 2)), np.ones((R, 2), np.i
                       np.zeros((R, 2), np.int32), np.arange(2 * R).reshape(R, 2),
                       np.array([0, 1], np.int32), np.ones((R, 2), np.uint32), alpha=100.0,
                       full_mask=np.zeros(R, np.uint32))
+# K1c: certified backward pass with ties / bad refs (per-source and whole-instance fallbacks)
+import os  # noqa: E402
+
+dag = synth.deep_dag()
+ref, T, now, Q = synth.deep_dag_instances(dag, 200, seed=9, K=2)
+ref = np.round(ref * 2) / 2
+ref[3, 5] = -1.0
+ref[7, :] = 0.0
+gd = sp.SlackGraph.from_dag(dag)
+a = gd.slack_batch(ref, T, now, Q, ratios=True)
+os.environ["SP_K1_CERT"] = "0"
+b = gd.slack_batch(ref, T, now, Q, ratios=True)
+del os.environ["SP_K1_CERT"]
+assert np.array_equal(a["slack"].view(np.uint64), b["slack"].view(np.uint64))
+# per-entry observation quantiles
+idx = rng.integers(0, len(table.lat), 4000).astype(np.int32)
+sp.observation_quantiles([table], None, idx, rng.uniform(0.1, 2.0, 4000), 0.9)
 print("sanitize smoke ok", int((out["best"] >= 0).sum()))
