@@ -609,6 +609,135 @@ def gen_commit_rounds(R, ref_root: Path, max_rounds=6000):
     return out
 
 
+# ---- 7b. speculate_from_buffer calls ---------------------------------
+
+def gen_speculate_calls(R, ref_root: Path, max_calls=5000):
+    """Record, for AMBER runs of the reference engine, each Configurator.speculate_from_buffer
+    call: its inputs (op, buffered items, upstream supply, clock, the op's path ratios, the
+    forced / batching-hold state, and the SQ / CQ weight dicts in their order) and what it did
+    (every invocation formed: entry, fill, slack, objective; the delay it stopped on).
+    set_latency calls are recorded in the same order so a replay can keep the tables identical.
+    Everything is captured by wrapping the reference's own methods."""
+    conf, man, pipe, prof, scen = R
+    from slackpipe import workload
+
+    bundle = ref_root / "scenarios" / "branching"
+    dag, ops = pipe.load_pipeline(json.loads((bundle / "pipeline.json").read_text()))
+    sc = scen.load_scenario(bundle / "scenario.json")
+    frames = workload.load_trace(bundle / "trace.jsonl")
+    profiles = {n: prof.profile_operation(o, sc, sc.tuning.samples_per_config) for n, o in ops.items()}
+    kinds = sc.backend_kinds()
+    op_names = sorted(dag.vertices)
+    paths = pipe.decompose_paths(dag)
+    runs = [(142.20064921472454, ()), (116.30975052233568, ()), (142.20064921472454, ("dfp",))]
+    C = {k: [] for k in ("run", "seq", "op", "n", "supply", "now", "target", "rmin", "rmax", "flags",
+                         "w_first", "w_n", "d_first", "d_n", "delay_idx", "delay_wait", "slack0")}
+    W = {k: [] for k in ("kind", "queue", "tab", "eidx", "count")}
+    D = {k: [] for k in ("idx", "fill", "slack", "obj")}
+    S = {k: [] for k in ("run", "seq", "op", "idx", "val")}
+    run_meta = []
+    orig_spec, orig_enq = conf.Configurator.speculate_from_buffer, conf.Configurator._enqueue_speculated
+    orig_sel, orig_set = conf.OpTable.select, conf.OpTable.set_latency
+    state = {"run": 0, "seq": 0, "calls": 0, "in": False, "last": None}
+
+    def spec(self, op, buffer):
+        if state["calls"] >= max_calls:
+            return orig_spec(self, op, buffer)
+        t = self.tables[op]
+        hold = self.holds.get(op)
+        now = self._clock()
+        forced = ("dfp" not in self.ablations and t.ref_index >= 0
+                  and self.completed_ref[op] < self.params.dfp_count)
+        flags = (1 if "sdb" not in self.ablations else 0) | (2 if forced else 0) | \
+                (4 if hold is not None and now >= hold.deadline_s else 0)
+        ratios = self._path_ratios(op)
+        # the first iteration's slack is whatever slack_by_kind returns now — its cache is keyed
+        # by the weight version only, so it may carry an earlier clock (configurator.py:526-529);
+        # later iterations recompute after every _weights_add bump with the current clock
+        sl0 = self.slack_by_kind(op)
+        C["slack0"].append([float(sl0[k]) for k in kinds])
+        C["run"].append(state["run"]); C["seq"].append(state["seq"])
+        C["op"].append(op_names.index(op)); C["n"].append(len(buffer))
+        C["supply"].append(int(self._supply(op))); C["now"].append(float(now))
+        C["target"].append(float(self.target_s)); C["rmin"].append(min(ratios))
+        C["rmax"].append(max(ratios)); C["flags"].append(flags)
+        C["w_first"].append(len(W["kind"]))
+        for q, table in enumerate((self._sq_weight, self._cq_weight)):
+            for k in kinds:
+                for (o, e), c in table[k].items():
+                    W["kind"].append(kinds.index(k)); W["queue"].append(q)
+                    W["tab"].append(op_names.index(o)); W["eidx"].append(e); W["count"].append(c)
+        C["w_n"].append(len(W["kind"]) - C["w_first"][-1])
+        C["d_first"].append(len(D["idx"]))
+        state["in"], state["last"] = True, None
+        try:
+            r = orig_spec(self, op, buffer)
+        finally:
+            state["in"] = False
+        C["d_n"].append(len(D["idx"]) - C["d_first"][-1])
+        last = state["last"]
+        if buffer and last is not None and last.kind == "delay":
+            C["delay_idx"].append(last.entry_index); C["delay_wait"].append(float(last.wait_budget_s))
+        else:
+            C["delay_idx"].append(-1); C["delay_wait"].append(0.0)
+        state["seq"] += 1
+        state["calls"] += 1
+        return r
+
+    def enq(self, inv, decision):
+        if state["in"]:
+            D["idx"].append(decision.entry_index); D["fill"].append(inv.fill)
+            D["slack"].append(float(decision.slack_s)); D["obj"].append(float(decision.objective_value))
+        return orig_enq(self, inv, decision)
+
+    def sel(self, *a, **kw):
+        d = orig_sel(self, *a, **kw)
+        if state["in"]:
+            state["last"] = d
+        return d
+
+    def setl(self, index, latency_s):
+        orig_set(self, index, latency_s)
+        if state["calls"] >= max_calls:
+            return
+        S["run"].append(state["run"]); S["seq"].append(state["seq"])
+        S["op"].append(op_names.index(self.operation)); S["idx"].append(index)
+        S["val"].append(float(self.lat[index]))
+        state["seq"] += 1
+
+    conf.Configurator.speculate_from_buffer, conf.Configurator._enqueue_speculated = spec, enq
+    conf.OpTable.select, conf.OpTable.set_latency = sel, setl
+    try:
+        for ri, (target, abl) in enumerate(runs):
+            state.update(run=ri, calls=0)
+            run = man.PipelineRun(dag, ops, profiles, frames, sc, target, conf.TuningParams(
+                alpha=sc.tuning.alpha, smoothing_beta=sc.tuning.smoothing_beta,
+                dfp_count=sc.tuning.dfp_count, straggler_timeout_factor=sc.tuning.straggler_timeout_factor,
+                cq_capacity=sc.tuning.cq_capacity), ablations=abl, paths=paths,
+                pipeline_name="video_branching")
+            run_meta.append({"target": target, "ablations": list(abl), "alpha": run.params.alpha,
+                             "pool": [run.configurator._pool[k] for k in kinds],
+                             "tables": {n: {"lat": [e.latency_s for e in run.tables[n].entries],
+                                            "ref_index": run.tables[n].ref_index}
+                                        for n in op_names}})
+            run.run_to_completion()
+    finally:
+        conf.Configurator.speculate_from_buffer, conf.Configurator._enqueue_speculated = orig_spec, orig_enq
+        conf.OpTable.select, conf.OpTable.set_latency = orig_sel, orig_set
+    out = {f"c_{k}": np.array(v) for k, v in C.items()}
+    for k in ("now", "target", "rmin", "rmax", "delay_wait", "slack0"):
+        out[f"c_{k}"] = np.array(C[k], dtype=np.float64)
+    out.update({f"w_{k}": np.array(v, dtype=np.int64) for k, v in W.items()})
+    out.update({f"d_{k}": np.array(v) for k, v in D.items()})
+    out["d_slack"] = np.array(D["slack"], dtype=np.float64)
+    out["d_obj"] = np.array(D["obj"], dtype=np.float64)
+    out.update({f"s_{k}": np.array(v) for k, v in S.items()})
+    out["s_val"] = np.array(S["val"], dtype=np.float64)
+    meta = {"kinds": kinds, "ops": op_names, "runs": run_meta, "max_calls": max_calls}
+    out["meta_json"] = np.frombuffer(json.dumps(meta).encode(), np.uint8)
+    return out
+
+
 # ---- 8. metadata directory (profile ingest, SURVEY.md §8(f) rank 3) ---------------------------
 
 def gen_metadata_amber(R, ref_root: Path):
@@ -645,6 +774,7 @@ def main() -> None:
         "queue_cases": lambda: gen_queue(R),
         "amber_trace": lambda: gen_amber(R, ref_root),
         "commit_rounds": lambda: gen_commit_rounds(R, ref_root),
+        "speculate_calls": lambda: gen_speculate_calls(R, ref_root),
         "metadata_amber": lambda: gen_metadata_amber(R, ref_root),
     }
     for name, fn in jobs.items():

@@ -333,3 +333,67 @@ def test_commit_round_oracle_matches_reference_rounds():
         assert (w[0] if w else -1) == d["r_winner_op"][i]
         n_rounds += 1
     assert n_rounds == 4 * 700 and n_cands > 4000
+
+
+def speculate_call_inputs(d, i, K):
+    """(sq, cq) weight lists of recorded speculate call i, per global kind in dict order."""
+    sq = [[] for _ in range(K)]
+    cq = [[] for _ in range(K)]
+    a, n = int(d["c_w_first"][i]), int(d["c_w_n"][i])
+    for w in range(a, a + n):
+        lst = sq if d["w_queue"][w] == 0 else cq
+        lst[int(d["w_kind"][w])].append([int(d["w_tab"][w]), int(d["w_eidx"][w]), int(d["w_count"][w])])
+    return sq, cq
+
+
+def speculate_replay():
+    """Yield (run meta, oracle tables, call index) in the recorded order, applying the recorded
+    set_latency calls to the oracle tables in between."""
+    from oracle import commit as oc
+
+    d = golden("speculate_calls")
+    meta = golden_json(d, "meta_json")
+    amb = golden_json(golden("amber_trace"), "meta_json")
+    for ri, rm in enumerate(meta["runs"]):
+        tabs = oc.amber_tables(amb)
+        for t, name in zip(tabs, meta["ops"]):
+            t.lat[:] = rm["tables"][name]["lat"]
+        ev = [(int(s), 0, i) for i, s in enumerate(d["s_seq"]) if d["s_run"][i] == ri]
+        ev += [(int(s), 1, i) for i, s in enumerate(d["c_seq"]) if d["c_run"][i] == ri]
+        ev.sort()
+        for _, typ, i in ev:
+            if typ == 0:
+                tabs[d["s_op"][i]].lat[d["s_idx"][i]] = d["s_val"][i]
+                continue
+            yield rm, tabs, i
+
+
+def test_speculate_oracle_matches_reference_calls():
+    """oracle/speculate.py reproduces every recorded Configurator.speculate_from_buffer call of
+    three AMBER runs (50 % and 25 % targets, dfp ablation): every invocation formed (entry,
+    fill, slack, objective) and the delay the loop stopped on."""
+    from oracle import speculate as osp
+
+    d = golden("speculate_calls")
+    meta = golden_json(d, "meta_json")
+    K = len(meta["kinds"])
+    calls = formed = 0
+    for rm, tabs, i in speculate_replay():
+        sq, cq = speculate_call_inputs(d, i, K)
+        dec, delay = osp.speculate(tabs, int(d["c_op"][i]), int(d["c_n"][i]), int(d["c_supply"][i]),
+                                   float(d["c_now"][i]), float(d["c_target"][i]), float(d["c_rmin"][i]),
+                                   float(d["c_rmax"][i]), rm["pool"], rm["alpha"], int(d["c_flags"][i]),
+                                   sq, cq, d["c_slack0"][i])
+        a, n = int(d["c_d_first"][i]), int(d["c_d_n"][i])
+        assert len(dec) == n, i
+        for j, (e, fill, s_k, obj) in enumerate(dec):
+            assert e == d["d_idx"][a + j] and fill == d["d_fill"][a + j], i
+            assert s_k == d["d_slack"][a + j], i
+            assert (math.isnan(obj) and math.isnan(d["d_obj"][a + j])) or obj == d["d_obj"][a + j], i
+        if d["c_delay_idx"][i] >= 0:
+            assert delay is not None and delay[0] == d["c_delay_idx"][i] and delay[1] == d["c_delay_wait"][i], i
+        else:
+            assert delay is None, i
+        calls += 1
+        formed += n
+    assert calls == 15000 and formed > 7000
