@@ -232,6 +232,38 @@ int sp_commit_round(sp_ctx* ctx, int32_t R, int32_t n_ops, sp_table* const* tabl
                     int32_t* out_fill, double* out_slack, double* out_obj, double* out_aff,
                     int32_t* out_best, int32_t mem);
 
+/* ---- speculation loop ------------------------------------------- */
+#define SP_SPEC_SDB 1           /* safe delayed batching on ("sdb" not ablated, 594)            */
+#define SP_SPEC_FORCED 2        /* dfp warm-up: every decision is the reference entry (571-589)  */
+#define SP_SPEC_HOLD_EXPIRED 4  /* a batching hold exists and its deadline has passed (597-599)  */
+
+/* Replaces Configurator.speculate_from_buffer (configurator.py:563-620) for R independent
+ * calls (one call = one operation's buffer).  Call r speculates operation op[r] (index into
+ * `tables`, the run's OpTables) holding n_buf[r] buffered items:
+ *   supply[r] = self._supply(op), now[r] = self._clock(), target[r] = self.target_s,
+ *   rmin/rmax[r] = min/max of self._path_ratios(op) (Alg. 1),
+ *   slack0[r*K + k] = self.slack_by_kind(op)[k] at entry (cached by weight version only, 526-529),
+ *   flags[r] = SP_SPEC_*, pool[k] = self._pool[kind k];
+ *   weights: the SQ (queue 0) and CQ (queue 1) dicts of every kind in their iteration order,
+ *   entries w_ptr[(r*2 + q)*K + k] .. w_ptr[(r*2 + q)*K + k + 1] of (w_tab, w_eidx, w_count)
+ *   = ((op, entry) key, count) — w_ptr has 2*K*R + 1 offsets.
+ * Every later iteration recomputes Eq. 2 (511-524) and Alg. 1's slack (526-543) on the device
+ * from the weights the call itself has updated (_weights_add, 553-561).  Outputs: the
+ * invocations formed, in order, at out_off[r] .. out_off[r] + out_n[r] (the caller reserves
+ * out_off[r+1] - out_off[r] >= n_buf[r] slots): out_idx entry, out_fill items, out_slack
+ * Decision.slack_s, out_obj objective (NaN when forced); out_delay_idx[r] / out_delay_wait[r]
+ * the delay decision that stopped the loop (-1 when the buffer emptied).  out_n[r] = -1 when a
+ * call touched more than 64 distinct weight keys (SP_E_UNSUPPORTED is returned). */
+int sp_speculate_batch(sp_ctx* ctx, int32_t n_tables, sp_table* const* tables, double alpha,
+                       int32_t K, const double* pool, int32_t R, const int32_t* op,
+                       const int32_t* n_buf, const int32_t* supply, const double* now,
+                       const double* target, const double* rmin, const double* rmax,
+                       const double* slack0, const uint32_t* flags, const int32_t* w_ptr,
+                       const int32_t* w_tab, const int32_t* w_eidx, const int32_t* w_count,
+                       const int32_t* out_off, int32_t* out_idx, int32_t* out_fill,
+                       double* out_slack, double* out_obj, int32_t* out_n, int32_t* out_delay_idx,
+                       double* out_delay_wait, int32_t mem);
+
 #ifdef __cplusplus
 }
 #endif

@@ -31,6 +31,7 @@ from .feedback import apply_feedback, fold_observations, observation_quantiles, 
 from .pipeline import ConfigEntry, ConfigSpec, PipelineDag, reference_config
 from .scenario import BackendSpec, Scenario
 from .slack import SlackGraph, compute_slack
+from .speculate import speculate_batch, speculate_from_buffer
 
 __version__ = "0.1.0"
 
@@ -40,5 +41,6 @@ __all__ = [
     "SlackpipeError", "TuningParams", "affinity", "affinity_from_minima", "apply_feedback",
     "commit_candidates", "commit_round", "compute_slack", "estimate_queueing", "fold_observations", "get_context", "load_library",
     "make_flags", "metadata", "objective", "observation_quantiles", "reference_config", "remaining_path_latency", "select_batch",
-    "select_config", "set_table_counters", "table_counters",
+    "select_config", "set_table_counters", "speculate_batch", "speculate_from_buffer",
+    "table_counters",
 ]

@@ -40,6 +40,9 @@ MODES = {"auto": SP_MODE_AUTO, "plan": SP_MODE_PLAN, "scan": SP_MODE_SCAN}
 
 SP_HEAD_PRESENT = 1
 SP_HEAD_FORCED = 2
+SP_SPEC_SDB = 1
+SP_SPEC_FORCED = 2
+SP_SPEC_HOLD_EXPIRED = 4
 SP_COMMIT_FIFO = 1
 SP_COMMIT_ESLC = 2
 
@@ -78,6 +81,7 @@ SIGNATURES = {
     "sp_feedback_fold": (C.c_int, [_p, _i32, _p, _i32, _p, _p, _p, _d, _i32, _i32, _i32, _i32]),
     "sp_table_get_counters": (C.c_int, [_p, _p, _p, _p]),
     "sp_table_set_counters": (C.c_int, [_p, _p, _i32, _p]),
+    "sp_speculate_batch": (C.c_int, [_p, _i32, _p, _d, _i32, _p, _i32] + [_p] * 21 + [_i32]),
     "sp_commit_round": (C.c_int, [_p, _i32, _i32, _p, _d] + [_p] * 10 + [_i32] + [_p] * 6 + [_i32]),
     "sp_observation_quantiles": (C.c_int, [_p, _i32, _p, _i32, _p, _p, _p, _d, _d, _p, _p, _p, _i32]),
     "sp_slack_select_batch": (C.c_int, [_p, _p, _i32, _p, _d, _i32, _p, _i32, _p, _p, _i32, _p]

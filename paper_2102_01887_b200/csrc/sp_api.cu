@@ -890,6 +890,122 @@ int sp_table_set_counters(sp_ctx* ctx, sp_table* t, int32_t completed_ref,
 }  // extern "C"
 
 // ---- batched commit step (configurator.py:657-756) ----------------------------------------
+extern "C" int sp_speculate_batch(sp_ctx* ctx, int32_t n_tables, sp_table* const* tables,
+                                  double alpha, int32_t K, const double* pool, int32_t R,
+                                  const int32_t* op, const int32_t* n_buf, const int32_t* supply,
+                                  const double* now, const double* target, const double* rmin,
+                                  const double* rmax, const double* slack0,
+                                  const uint32_t* flags, const int32_t* w_ptr,
+                                  const int32_t* w_tab, const int32_t* w_eidx,
+                                  const int32_t* w_count, const int32_t* out_off,
+                                  int32_t* out_idx, int32_t* out_fill, double* out_slack,
+                                  double* out_obj, int32_t* out_n, int32_t* out_delay_idx,
+                                  double* out_delay_wait, int32_t mem) {
+  if (!ctx || !tables || !pool) return fail(SP_E_INVALID, "speculate: null argument");
+  if (n_tables < 1 || n_tables > 64) return fail(SP_E_INVALID, "speculate: n_tables must be in [1, 64]");
+  if (!(alpha >= 0.0)) return fail(SP_E_INVALID, "alpha must be >= 0");  // configurator.py:37
+  if (R < 0) return fail(SP_E_INVALID, "speculate: negative call count");
+  for (int t = 0; t < n_tables; ++t) {
+    if (!tables[t]) return fail(SP_E_INVALID, "speculate: null table");
+    if (tables[t]->K != K) return fail(SP_E_INVALID, "speculate: tables disagree with K");
+  }
+  if (R == 0) return SP_OK;
+  if (!op || !n_buf || !supply || !now || !target || !rmin || !rmax || !slack0 || !flags ||
+      !w_ptr || !w_tab || !w_eidx || !w_count || !out_off || !out_idx || !out_fill ||
+      !out_slack || !out_obj || !out_n || !out_delay_idx || !out_delay_wait)
+    return fail(SP_E_INVALID, "speculate: required array is null");
+  if (mem == SP_MEM_DEVICE)
+    return speculate_launch(ctx, n_tables, tables, alpha, K, pool, R, op, n_buf, supply, now,
+                            target, rmin, rmax, slack0, flags, w_ptr, w_tab, w_eidx, w_count,
+                            out_off, out_idx, out_fill, out_slack, out_obj, out_n,
+                            out_delay_idx, out_delay_wait);
+  if (mem != SP_MEM_HOST) return fail(SP_E_INVALID, "speculate: bad mem flag");
+  // host-side validation of everything the kernel indexes
+  const size_t nw = (size_t)2 * K * R;
+  if (w_ptr[0] != 0) return fail(SP_E_INVALID, "speculate: w_ptr[0] must be 0");
+  for (size_t q = 0; q < nw; ++q)
+    if (w_ptr[q + 1] < w_ptr[q]) return fail(SP_E_INVALID, "speculate: w_ptr not ascending");
+  const int W = w_ptr[nw];
+  for (int w = 0; w < W; ++w)
+    if (w_tab[w] < 0 || w_tab[w] >= n_tables || w_eidx[w] < 0 || w_eidx[w] >= tables[w_tab[w]]->M)
+      return fail(SP_E_INVALID, "speculate: weight key out of range");
+  if (out_off[0] != 0) return fail(SP_E_INVALID, "speculate: out_off[0] must be 0");
+  for (int r = 0; r < R; ++r) {
+    if (op[r] < 0 || op[r] >= n_tables) return fail(SP_E_INVALID, "speculate: op out of range");
+    if (n_buf[r] < 0) return fail(SP_E_INVALID, "speculate: negative buffer");
+    if (out_off[r + 1] - out_off[r] < n_buf[r])
+      return fail(SP_E_INVALID, "speculate: output slots smaller than the buffer");
+    if ((flags[r] & SP_SPEC_FORCED) && tables[op[r]]->ref_index < 0)
+      return fail(SP_E_INVALID, "speculate: forced call on a table without a reference entry");
+  }
+  const int O = out_off[R];
+  const size_t need = 3 * rsz<int32_t>(R) + 4 * rsz<double>(R) + rsz<double>((size_t)R * K) +
+                      rsz<uint32_t>(R) + rsz<int32_t>(nw + 1) + 3 * rsz<int32_t>(std::max(W, 1)) +
+                      rsz<int32_t>(R + 1) + 2 * rsz<int32_t>(std::max(O, 1)) +
+                      2 * rsz<double>(std::max(O, 1)) + 2 * rsz<int32_t>(R) + rsz<double>(R);
+  int rc = SP_OK;
+  void* io = ctx_io(ctx, need, &rc);
+  if (!io) return rc;
+  Bump b{(uint8_t*)io};
+  cudaStream_t st = ctx->stream;
+  auto up = [&](auto* dst, const void* src, size_t bytes) {
+    return bytes ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st) : cudaSuccess;
+  };
+  int32_t* d_op = b.take<int32_t>(R);
+  int32_t* d_n = b.take<int32_t>(R);
+  int32_t* d_sup = b.take<int32_t>(R);
+  double* d_now = b.take<double>(R);
+  double* d_tgt = b.take<double>(R);
+  double* d_rmin = b.take<double>(R);
+  double* d_rmax = b.take<double>(R);
+  double* d_s0 = b.take<double>((size_t)R * K);
+  uint32_t* d_fl = b.take<uint32_t>(R);
+  int32_t* d_wp = b.take<int32_t>(nw + 1);
+  int32_t* d_wt = b.take<int32_t>(std::max(W, 1));
+  int32_t* d_we = b.take<int32_t>(std::max(W, 1));
+  int32_t* d_wc = b.take<int32_t>(std::max(W, 1));
+  int32_t* d_off = b.take<int32_t>(R + 1);
+  int32_t* o_idx = b.take<int32_t>(std::max(O, 1));
+  int32_t* o_fill = b.take<int32_t>(std::max(O, 1));
+  double* o_sl = b.take<double>(std::max(O, 1));
+  double* o_ob = b.take<double>(std::max(O, 1));
+  int32_t* o_n = b.take<int32_t>(R);
+  int32_t* o_di = b.take<int32_t>(R);
+  double* o_dw = b.take<double>(R);
+  SP_CUDA(up(d_op, op, 4 * (size_t)R));
+  SP_CUDA(up(d_n, n_buf, 4 * (size_t)R));
+  SP_CUDA(up(d_sup, supply, 4 * (size_t)R));
+  SP_CUDA(up(d_now, now, 8 * (size_t)R));
+  SP_CUDA(up(d_tgt, target, 8 * (size_t)R));
+  SP_CUDA(up(d_rmin, rmin, 8 * (size_t)R));
+  SP_CUDA(up(d_rmax, rmax, 8 * (size_t)R));
+  SP_CUDA(up(d_s0, slack0, 8 * (size_t)R * K));
+  SP_CUDA(up(d_fl, flags, 4 * (size_t)R));
+  SP_CUDA(up(d_wp, w_ptr, 4 * (nw + 1)));
+  SP_CUDA(up(d_wt, w_tab, 4 * (size_t)W));
+  SP_CUDA(up(d_we, w_eidx, 4 * (size_t)W));
+  SP_CUDA(up(d_wc, w_count, 4 * (size_t)W));
+  SP_CUDA(up(d_off, out_off, 4 * (size_t)(R + 1)));
+  rc = speculate_launch(ctx, n_tables, tables, alpha, K, pool, R, d_op, d_n, d_sup, d_now, d_tgt,
+                        d_rmin, d_rmax, d_s0, d_fl, d_wp, d_wt, d_we, d_wc, d_off, o_idx, o_fill,
+                        o_sl, o_ob, o_n, o_di, o_dw);
+  if (rc != SP_OK) return rc;
+  auto down = [&](void* dst, const void* src, size_t bytes) {
+    return bytes ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st) : cudaSuccess;
+  };
+  SP_CUDA(down(out_idx, o_idx, 4 * (size_t)O));
+  SP_CUDA(down(out_fill, o_fill, 4 * (size_t)O));
+  SP_CUDA(down(out_slack, o_sl, 8 * (size_t)O));
+  SP_CUDA(down(out_obj, o_ob, 8 * (size_t)O));
+  SP_CUDA(down(out_n, o_n, 4 * (size_t)R));
+  SP_CUDA(down(out_delay_idx, o_di, 4 * (size_t)R));
+  SP_CUDA(down(out_delay_wait, o_dw, 8 * (size_t)R));
+  SP_CUDA(cudaStreamSynchronize(st));
+  for (int r = 0; r < R; ++r)
+    if (out_n[r] < 0) return fail(SP_E_UNSUPPORTED, "speculate: a call touched more than 64 weight keys");
+  return SP_OK;
+}
+
 extern "C" int sp_commit_round(sp_ctx* ctx, int32_t R, int32_t n_ops, sp_table* const* tables,
                                double alpha, const double* slack, const int32_t* head_fill,
                                const int32_t* buffered, const int64_t* head_id,

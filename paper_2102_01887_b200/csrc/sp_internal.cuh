@@ -266,6 +266,14 @@ int quantile_launch(sp_ctx* ctx, int n_tables, sp_table* const* tables, int n, c
                     int32_t* out_count, double* out_smooth);
 int scores_launch(sp_ctx* ctx, sp_table* t, Plan* p, const double* slack_dev,
                   double* score_dev, double* cost_dev);
+int speculate_launch(sp_ctx* ctx, int n_tables, sp_table* const* tables, double alpha, int K,
+                     const double* pool, int R, const int32_t* op, const int32_t* n_buf,
+                     const int32_t* supply, const double* now, const double* target,
+                     const double* rmin, const double* rmax, const double* slack0,
+                     const uint32_t* flags, const int32_t* w_ptr, const int32_t* w_tab,
+                     const int32_t* w_eidx, const int32_t* w_count, const int32_t* out_off,
+                     int32_t* out_idx, int32_t* out_fill, double* out_slack, double* out_obj,
+                     int32_t* out_n, int32_t* out_delay_idx, double* out_delay_wait);
 int slack_launch(sp_ctx* ctx, sp_dag* g, int I, const double* ref, int ref_stride,
                  const double* target, const double* now, int K, const double* Q,
                  double* out_slack, double* out_ratio);

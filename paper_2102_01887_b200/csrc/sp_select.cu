@@ -172,6 +172,7 @@ __device__ __forceinline__ void store_out(const SelectIO& io, int i, const Out& 
 #include "sp_k2b.cuh"
 #include "sp_k2f.cuh"
 #include "sp_k12.cuh"
+#include "sp_spec.cuh"
 
 // ---- K2a: literal scan kernel -------------------------------------------------------------
 struct Best {

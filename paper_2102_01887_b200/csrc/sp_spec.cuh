@@ -1,0 +1,230 @@
+// sp_spec.cuh — Configurator.speculate_from_buffer on the device (
+// included by sp_select.cu after sp_k2b.cuh).
+//
+// One thread runs one call's sequential loop (configurator.py:563-620):
+//   slack  — the entry value the caller passes (slack_by_kind is cached by weight version only,
+//            configurator.py:526-529), then after every formed invocation Eq. 2 recomputed from
+//            the weights (queueing_by_kind, 511-524: SQ then CQ weights in dict order,
+//            total += count * (lat * res), / pool) and budget = (target - now) - Q,
+//            slack = (budget >= 0 ? rmin : rmax) * budget (526-543);
+//   decide — forced warm-up: the reference entry, fill 1, objective NaN (571-589); otherwise
+//            OpTable.select(slack, alpha, buffered, allow_delay, supply) on the op's staircase
+//            plan (K2b's decide_plan), allow_delay cleared on the first iteration when the
+//            batching hold has expired (597-599); a delay decision ends the loop (606-612);
+//   update — buffered -= fill; _weights_add(SQ, kind, op, entry, +1) (553-561): an existing key
+//            is incremented in place, a new key appended after the kind's list.
+// The input weight lists are read-only; the call's increments and new keys live in a small
+// per-thread list (kMaxSpecKeys), so the Eq. 2 order is: input SQ entries (count + increment),
+// then the call's new keys of the kind in append order, then the CQ entries.
+
+constexpr int kMaxSpecTables = 64;
+constexpr int kMaxSpecKeys = 64;
+
+struct SpecTabs {
+  const double* lat[kMaxSpecTables];
+  const double* res[kMaxSpecTables];
+  const int32_t* kind[kMaxSpecTables];
+  const uint8_t* plan[kMaxSpecTables];
+  int32_t ref_index[kMaxSpecTables];
+  double pool[kMaxKinds];
+};
+
+struct SpecIO {
+  const int32_t* op;
+  const int32_t* n_buf;
+  const int32_t* supply;
+  const double* now;
+  const double* target;
+  const double* rmin;
+  const double* rmax;
+  const double* slack0;  // R x K
+  const uint32_t* flags;
+  const int32_t* w_ptr;  // R * 2K + 1: (r, queue, kind) lists
+  const int32_t* w_tab;
+  const int32_t* w_eidx;
+  const int32_t* w_count;
+  const int32_t* out_off;  // R + 1
+  int32_t* out_idx;
+  int32_t* out_fill;
+  double* out_slack;
+  double* out_obj;
+  int32_t* out_n;  // -1: the call needed more than kMaxSpecKeys new / incremented keys
+  int32_t* out_delay_idx;
+  double* out_delay_wait;
+  int R;
+  int K;
+};
+
+struct SpecKey {
+  int32_t kind, tab, eidx, cnt, orig;  // orig: input SQ position incremented, -1 new key
+};
+
+template <int KT>
+__global__ void __launch_bounds__(128) k_speculate(SpecTabs tb, double alpha, SpecIO io,
+                                                   SelectIO sel) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= io.R) return;
+  const int K = io.K;
+  const int op = io.op[r];
+  int n = io.n_buf[r];
+  const int supply = io.supply[r];
+  const double span = __dsub_rn(io.target[r], io.now[r]);  // target - now
+  const double rmin = io.rmin[r], rmax = io.rmax[r];
+  const uint32_t fl = io.flags[r];
+  const int32_t* wp = io.w_ptr + (size_t)r * 2 * K;
+  View<KT> v;
+  make_view<KT>(v, tb.plan[op], *reinterpret_cast<const PlanHdr*>(tb.plan[op]), K);
+  SpecKey keys[kMaxSpecKeys];
+  int nk = 0;
+  const int o0 = io.out_off[r];
+  int nd = 0;
+  bool first = true, overflow = false;
+  io.out_delay_idx[r] = -1;
+  io.out_delay_wait[r] = 0.0;
+  In<KT> x;
+  while (n > 0) {
+#pragma unroll
+    for (int k = 0; k < KT; ++k) {
+      if (k >= K) {
+        x.s[k] = 0.0;
+        continue;
+      }
+      if (first) {
+        x.s[k] = io.slack0[(size_t)r * K + k];
+        continue;
+      }
+      double total = 0.0;  // configurator.py:516-522
+      for (int w = wp[k]; w < wp[k + 1]; ++w) {  // SQ, in dict order
+        int c = io.w_count[w];
+        for (int q = 0; q < nk; ++q) c += keys[q].orig == w ? keys[q].cnt : 0;
+        const int t = io.w_tab[w], e = io.w_eidx[w];
+        total = __dadd_rn(total, __dmul_rn((double)c, __dmul_rn(tb.lat[t][e], tb.res[t][e])));
+      }
+      for (int q = 0; q < nk; ++q) {  // keys this call appended to the kind's SQ dict
+        if (keys[q].orig >= 0 || keys[q].kind != k) continue;
+        const int t = keys[q].tab, e = keys[q].eidx;
+        total = __dadd_rn(total, __dmul_rn((double)keys[q].cnt, __dmul_rn(tb.lat[t][e], tb.res[t][e])));
+      }
+      for (int w = wp[K + k]; w < wp[K + k + 1]; ++w) {  // CQ
+        const int t = io.w_tab[w], e = io.w_eidx[w];
+        total = __dadd_rn(total,
+                          __dmul_rn((double)io.w_count[w], __dmul_rn(tb.lat[t][e], tb.res[t][e])));
+      }
+      const double budget = __dsub_rn(span, __ddiv_rn(total, tb.pool[k]));  // 535
+      x.s[k] = __dmul_rn(budget >= 0.0 ? rmin : rmax, budget);             // 536-540
+    }
+    int idx, fill, kd;
+    double s_k, obj;
+    if (fl & SP_SPEC_FORCED) {  // configurator.py:571-589
+      idx = tb.ref_index[op];
+      fill = 1;
+      kd = tb.kind[op][idx];
+      s_k = pick_kind<KT>(x.s, kd);
+      obj = NAN;
+    } else {
+      const bool allow = (fl & SP_SPEC_SDB) && !(first && (fl & SP_SPEC_HOLD_EXPIRED));
+      x.av = n;
+      x.sup = supply;
+      x.mb = 1;
+      x.fl = allow ? SP_FLAG_ALLOW_DELAY : 0u;
+      x.t = op;
+      decide_plan<KT, false>(v, sel, r, x);
+      const int code = sel.out_code[r];
+      idx = sel.out_idx[r];
+      if ((code & 3) == SP_DEC_DELAY) {  // configurator.py:606-612
+        io.out_delay_idx[r] = idx;
+        io.out_delay_wait[r] = sel.out_wait[r];
+        break;
+      }
+      if ((code & 3) != SP_DEC_ASSIGN) {  // cannot happen without exclusions (assert, 605)
+        overflow = true;
+        break;
+      }
+      fill = sel.out_fill[r];
+      s_k = sel.out_slack[r];
+      obj = sel.out_obj[r];
+      kd = tb.kind[op][idx];
+    }
+    first = false;
+    n -= fill;
+    // _weights_add(self._sq_weight, kind, op, idx, +1)
+    int hit = -1;
+    for (int q = 0; q < nk; ++q)
+      if (keys[q].kind == kd && keys[q].tab == op && keys[q].eidx == idx) hit = q;
+    if (hit < 0) {
+      int orig = -1;
+      for (int w = wp[kd]; w < wp[kd + 1]; ++w)
+        if (io.w_tab[w] == op && io.w_eidx[w] == idx) orig = w;
+      if (nk == kMaxSpecKeys) {
+        overflow = true;
+        break;
+      }
+      keys[nk] = SpecKey{kd, op, idx, 0, orig};
+      hit = nk++;
+    }
+    keys[hit].cnt += 1;
+    io.out_idx[o0 + nd] = idx;
+    io.out_fill[o0 + nd] = fill;
+    io.out_slack[o0 + nd] = s_k;
+    io.out_obj[o0 + nd] = obj;
+    ++nd;
+  }
+  io.out_n[r] = overflow ? -1 : nd;
+}
+
+}  // namespace
+
+int speculate_launch(sp_ctx* ctx, int n_tables, sp_table* const* tables, double alpha, int K,
+                     const double* pool, int R, const int32_t* op, const int32_t* n_buf,
+                     const int32_t* supply, const double* now, const double* target,
+                     const double* rmin, const double* rmax, const double* slack0,
+                     const uint32_t* flags, const int32_t* w_ptr, const int32_t* w_tab,
+                     const int32_t* w_eidx, const int32_t* w_count, const int32_t* out_off,
+                     int32_t* out_idx, int32_t* out_fill, double* out_slack, double* out_obj,
+                     int32_t* out_n, int32_t* out_delay_idx, double* out_delay_wait) {
+  if (n_tables > kMaxSpecTables) return fail(SP_E_UNSUPPORTED, "speculate: more than 64 tables");
+  if (K > 8) return fail(SP_E_UNSUPPORTED, "speculate: more than 8 kinds");
+  SpecTabs tb;
+  memset(&tb, 0, sizeof(tb));
+  for (int t = 0; t < n_tables; ++t) {
+    if (!tables[t]->plan_ok) return fail(SP_E_UNSUPPORTED, "speculate: table without a plan");
+    int rc;
+    Plan* p = plan_get(ctx, tables[t], alpha, &rc);
+    if (!p) return rc;
+    tb.lat[t] = tables[t]->lat;
+    tb.res[t] = tables[t]->res;
+    tb.kind[t] = tables[t]->kind;
+    tb.plan[t] = p->image;
+    tb.ref_index[t] = tables[t]->ref_index;
+  }
+  for (int k = 0; k < K; ++k) tb.pool[k] = pool[k];
+  // per-call decide_plan outputs (read back by the same thread)
+  int rc = SP_OK;
+  const size_t al = ((size_t)R * 8 + 255) & ~(size_t)255;
+  uint8_t* s = static_cast<uint8_t*>(ctx_tmp(ctx, 6 * al, &rc));
+  if (!s) return rc;
+  SelectIO sel;
+  memset(&sel, 0, sizeof(sel));
+  sel.out_idx = reinterpret_cast<int32_t*>(s);
+  sel.out_code = reinterpret_cast<int32_t*>(s + al);
+  sel.out_fill = reinterpret_cast<int32_t*>(s + 2 * al);
+  sel.out_obj = reinterpret_cast<double*>(s + 3 * al);
+  sel.out_slack = reinterpret_cast<double*>(s + 4 * al);
+  sel.out_wait = reinterpret_cast<double*>(s + 5 * al);
+  sel.N = R;
+  sel.K = K;
+  SpecIO io{op, n_buf, supply, now, target, rmin, rmax, slack0, flags, w_ptr, w_tab, w_eidx,
+            w_count, out_off, out_idx, out_fill, out_slack, out_obj, out_n, out_delay_idx,
+            out_delay_wait, R, K};
+  const int blocks = (R + 127) / 128;
+  if (K <= 2)
+    k_speculate<2><<<blocks, 128, 0, ctx->stream>>>(tb, alpha, io, sel);
+  else if (K <= 4)
+    k_speculate<4><<<blocks, 128, 0, ctx->stream>>>(tb, alpha, io, sel);
+  else
+    k_speculate<8><<<blocks, 128, 0, ctx->stream>>>(tb, alpha, io, sel);
+  SP_CHECK_LAUNCH(ctx);
+  return SP_OK;
+}
+
+namespace {
