@@ -517,5 +517,166 @@ def run_commit(args):
     }
     print(json.dumps(line), flush=True)
 
+# ---- speculate ----------------------------------------------------------
+
+def _spec_inputs(meta, R, seed):
+    """R synthetic speculate_from_buffer calls on the AMBER tables: buffers of 1-40 items, upstream
+    supply, clock / target spans from overdue to loose, path ratios, entry slack, 0-7 weight keys
+    per call (60 % speculative), sdb on 80 %, forced warm-up 10 %, expired holds 10 %."""
+    from oracle import commit as oc
+
+    otabs = oc.amber_tables(meta)
+    K = len(meta["kinds"])
+    rng = np.random.default_rng(seed)
+    ops = rng.integers(0, len(otabs), R)
+    x = {"op": ops, "n": rng.integers(1, 40, R), "supply": rng.integers(0, 60, R),
+         "now": rng.uniform(0, 100, R)}
+    x["target"] = x["now"] + rng.uniform(-5, 80, R)
+    x["rmin"] = rng.uniform(0.05, 0.5, R)
+    x["rmax"] = x["rmin"] + rng.uniform(0, 0.5, R)
+    ref_ok = np.array([otabs[o].ref_index >= 0 for o in ops])
+    x["flags"] = ((rng.random(R) < 0.8).astype(np.uint32)
+                  | np.where((rng.random(R) < 0.1) & ref_ok, 2, 0).astype(np.uint32)
+                  | np.where(rng.random(R) < 0.1, 4, 0).astype(np.uint32))
+    x["slack0"] = rng.uniform(-2, 60, (R, K))
+    calls = []
+    ptr, tab, eidx, cnt = [0], [], [], []
+    for _ in range(R):
+        sq = [[] for _ in range(K)]
+        cq = [[] for _ in range(K)]
+        for _ in range(rng.integers(0, 8)):
+            tb = int(rng.integers(0, len(otabs)))
+            e = int(rng.integers(0, len(otabs[tb].lat)))
+            k = int(otabs[tb].gkind[e])
+            lst = sq if rng.random() < 0.6 else cq
+            if not any(y[0] == tb and y[1] == e for y in lst[k]):
+                lst[k].append([tb, e, int(rng.integers(1, 5))])
+        calls.append((sq, cq))
+        for lists in (sq, cq):
+            for k in range(K):
+                for tb, e, c in lists[k]:
+                    tab.append(tb); eidx.append(e); cnt.append(c)
+                ptr.append(len(tab))
+    x["w_ptr"], x["w_tab"], x["w_eidx"], x["w_count"] = ptr, tab, eidx, cnt
+    pk = {k: float(n * r) for k, n, r, _ in meta["backends"]}
+    return x, calls, [pk[k] for k in meta["kinds"]]
+
+
+def _spec_cpu_worker(a):
+    meta, x, calls, pool, lo, hi, alpha = a
+    from oracle import commit as oc
+    from oracle import speculate as osp
+
+    otabs = oc.amber_tables(meta)
+    n = 0
+    for r in range(lo, hi):
+        sq = [[list(y) for y in lst] for lst in calls[r][0]]
+        osp.speculate(otabs, int(x["op"][r]), int(x["n"][r]), int(x["supply"][r]), float(x["now"][r]),
+                      float(x["target"][r]), float(x["rmin"][r]), float(x["rmax"][r]), pool, alpha,
+                      int(x["flags"][r]), sq, calls[r][1], x["slack0"][r])
+        n += 1
+    return n
+
+
+def run_speculate(args):
+    import torch
+
+    import paper_2102_01887_b200 as sp
+
+    with np.load(ROOT / "tests" / "golden" / "amber_trace.npz") as z:
+        meta = json.loads(bytes(z["meta_json"]).decode())
+    rank, world, local = _dist(torch)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    ctx = sp.get_context(local)
+    ctx.set_stream(stream.cuda_stream)
+    tabs = _amber_tables(sp, meta)
+    R = 65536
+    alpha = 100.0
+    x, calls, pool = _spec_inputs(meta, R, seed=21 + rank)
+    T = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(dev)
+    d = {k: T(x[k], np.int32) for k in ("op", "n", "supply", "w_ptr", "w_tab", "w_eidx", "w_count")}
+    d.update({k: T(x[k], np.float64) for k in ("now", "target", "rmin", "rmax", "slack0")})
+    d["flags"] = T(x["flags"].astype(np.int32), np.int32)
+
+    def step(out=None):
+        return sp.speculate_batch(tabs, alpha, pool, d["op"], d["n"], d["supply"], d["now"],
+                                  d["target"], d["rmin"], d["rmax"], d["slack0"], d["flags"],
+                                  d["w_ptr"], d["w_tab"], d["w_eidx"], d["w_count"], out=out)
+
+    out = step()
+    for _ in range(args.warmup):
+        step(out)
+    torch.cuda.synchronize(dev)
+    formed = int(out["n"].sum().item())
+    # parity spot check against the oracle on the first calls (checker only)
+    from oracle import commit as oc
+    from oracle import speculate as osp
+
+    otabs = oc.amber_tables(meta)
+    n_dev = out["n"][:64].cpu().numpy()
+    for r in range(64):
+        sq = [[list(y) for y in lst] for lst in calls[r][0]]
+        dec, _ = osp.speculate(otabs, int(x["op"][r]), int(x["n"][r]), int(x["supply"][r]),
+                               float(x["now"][r]), float(x["target"][r]), float(x["rmin"][r]),
+                               float(x["rmax"][r]), pool, alpha, int(x["flags"][r]), sq, calls[r][1],
+                               x["slack0"][r])
+        assert len(dec) == n_dev[r], f"speculate call {r} disagrees with the oracle"
+    _barrier(torch)
+    evs = _events(torch, args.steps)
+    l0 = ctx.launch_count
+    for i in range(args.steps):
+        evs[i][0].record(stream)
+        step(out)
+        evs[i][1].record(stream)
+    torch.cuda.synchronize(dev)
+    launches = ctx.launch_count - l0
+    ms = [a.elapsed_time(b) for a, b in evs]
+    t = _tmax(torch, sum(ms) / 1e3, dev)
+    # end to end: numpy inputs in host memory through the same public call (copies inside)
+    hx = {k: np.ascontiguousarray(x[k]) for k in x}
+    t0 = time.perf_counter()
+    reps = 5
+    for _ in range(reps):
+        sp.speculate_batch(tabs, alpha, pool, hx["op"], hx["n"], hx["supply"], hx["now"], hx["target"],
+                           hx["rmin"], hx["rmax"], hx["slack0"], hx["flags"], hx["w_ptr"], hx["w_tab"],
+                           hx["w_eidx"], hx["w_count"])
+    e2e_s = (time.perf_counter() - t0) / reps
+    if rank != 0:
+        return
+    cpu = None
+    if world == 1:
+        import multiprocessing as mp
+
+        cores = os.cpu_count() or 1
+        S = 400 * cores
+        work = [(meta, x, calls, pool, int(a[0]), int(a[-1]) + 1, alpha)
+                for a in np.array_split(np.arange(S), cores) if len(a)]
+        t0 = time.perf_counter()
+        with mp.get_context("fork").Pool(len(work)) as pool_:
+            n = sum(pool_.map(_spec_cpu_worker, work))
+        dt = time.perf_counter() - t0
+        cpu = {"value": n / dt, "unit": "calls/s", "cores": cores, "kind": "port",
+               "sample": f"{S} calls, oracle/speculate.py (configurator.py:563-620) on {cores} processes"}
+    line = {
+        "workload": "speculate",
+        "metric": "Configurator.speculate_from_buffer calls / s (replica-parallel speculation loop)",
+        "unit": "calls/s", "value": args.steps * R * world / t, "ms_per_step": 1e3 * t / args.steps,
+        "steps": args.steps, "n_gpus": world, "scaling": "weak",
+        "invocations_formed_per_s": args.steps * formed * world / t,
+        "config": {"calls_per_step": R, "ops": len(tabs), "kinds": len(meta["kinds"]), "alpha": alpha,
+                   "invocations_formed_per_step": formed,
+                   "inputs": "synthetic AMBER-table calls: buffers 1-40, 0-7 weight keys, sdb 80%, "
+                             "forced 10%, expired holds 10%"},
+        "e2e": {"value": R / e2e_s, "unit": "calls/s", "path": "speculate_batch(numpy) -> "
+                "sp_speculate_batch(SP_MEM_HOST)"},
+        "gpu_launches": launches,
+        "cpu_baseline": cpu,
+        "step_ms": {"median": statistics.median(ms), "min": min(ms), "max": max(ms)},
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main(args):
-    {"c3": run_c3, "c4": run_c4, "c5": run_c5, "commit": run_commit}[args.workload](args)
+    {"c3": run_c3, "c4": run_c4, "c5": run_c5, "commit": run_commit,
+     "speculate": run_speculate}[args.workload](args)

@@ -25,40 +25,61 @@ from ._lib import check, ptr
 
 
 def speculate_batch(tables: Sequence, alpha: float, pool, op, n_buf, supply, now, target, rmin,
-                    rmax, slack0, flags, w_ptr, w_tab, w_eidx, w_count, *, ctx=None) -> dict:
-    """R speculate_from_buffer calls (numpy, host memory; see sp_speculate_batch).
+                    rmax, slack0, flags, w_ptr, w_tab, w_eidx, w_count, *, ctx=None,
+                    out=None) -> dict:
+    """R speculate_from_buffer calls (see sp_speculate_batch).
 
     ``slack0`` (R, K); ``w_ptr`` (2*K*R + 1,) CSR over (call, queue, kind) of the weight keys
-    (``w_tab`` table index, ``w_eidx`` entry, ``w_count``).  Returns ``off`` (R + 1,) and, per
-    formed invocation, ``idx, fill, slack, obj``; per call ``n`` (invocations formed) and the
-    stopping delay ``delay_idx`` (-1: none) / ``delay_wait``.
+    (``w_tab`` table index, ``w_eidx`` entry, ``w_count``); ``pool`` (K,) host values.  numpy
+    arrays: host memory, the call copies in and out and synchronises; torch CUDA tensors
+    (int32 / float64 / uint32 as the C header says): stream-ordered device call.  Returns
+    ``off`` (R + 1,) and, per formed invocation, ``idx, fill, slack, obj``; per call ``n``
+    (invocations formed) and the stopping delay ``delay_idx`` (-1: none) / ``delay_wait``.
+    ``out`` (a previous result for the same n_buf) is reused without reallocating — for
+    device calls that keeps the call free of host synchronisation.
     """
     ctx = ctx or tables[0]._ctx
     K = int(tables[0].K)
-    i32 = lambda a: np.ascontiguousarray(a, dtype=np.int32)
-    f64 = lambda a: np.ascontiguousarray(a, dtype=np.float64)
-    op, n_buf, supply = i32(op), i32(n_buf), i32(supply)
-    R = len(op)
-    now, target, rmin, rmax = f64(now), f64(target), f64(rmin), f64(rmax)
-    slack0 = f64(slack0).reshape(R, K)
-    flags = np.ascontiguousarray(flags, dtype=np.uint32)
-    w_ptr, w_tab, w_eidx, w_count = i32(w_ptr), i32(w_tab), i32(w_eidx), i32(w_count)
-    if len(w_tab) == 0:
-        w_tab = w_eidx = w_count = np.zeros(1, np.int32)
-    off = np.zeros(R + 1, np.int32)
-    np.cumsum(n_buf, out=off[1:])
-    O = max(int(off[-1]), 1)
-    out = {"off": off, "idx": np.empty(O, np.int32), "fill": np.empty(O, np.int32),
-           "slack": np.empty(O), "obj": np.empty(O), "n": np.empty(R, np.int32),
-           "delay_idx": np.empty(R, np.int32), "delay_wait": np.empty(R)}
+    pool = np.ascontiguousarray(pool, dtype=np.float64)
     handles = (C.c_void_p * len(tables))(*[t.handle.value for t in tables])
-    pool = f64(pool)
+    if hasattr(op, "is_cuda") and op.is_cuda:
+        import torch
+
+        R = int(op.shape[0])
+        if out is None:
+            off = torch.zeros(R + 1, dtype=torch.int32, device=op.device)
+            off[1:] = torch.cumsum(n_buf, 0)
+            O = max(int(off[-1].item()), 1)
+        z = lambda n, dt: torch.empty(n, dtype=dt, device=op.device)
+        i32, f64 = torch.int32, torch.float64
+        mem = _lib.SP_MEM_DEVICE
+    else:
+        i32c = lambda a: np.ascontiguousarray(a, dtype=np.int32)
+        f64c = lambda a: np.ascontiguousarray(a, dtype=np.float64)
+        op, n_buf, supply = i32c(op), i32c(n_buf), i32c(supply)
+        R = len(op)
+        now, target, rmin, rmax = f64c(now), f64c(target), f64c(rmin), f64c(rmax)
+        slack0 = f64c(slack0).reshape(R, K)
+        flags = np.ascontiguousarray(flags, dtype=np.uint32)
+        w_ptr, w_tab, w_eidx, w_count = i32c(w_ptr), i32c(w_tab), i32c(w_eidx), i32c(w_count)
+        if len(w_tab) == 0:
+            w_tab = w_eidx = w_count = np.zeros(1, np.int32)
+        off = np.zeros(R + 1, np.int32)
+        np.cumsum(n_buf, out=off[1:])
+        O = max(int(off[-1]), 1)
+        z = lambda n, dt: np.empty(n, dtype=dt)
+        i32, f64 = np.int32, np.float64
+        mem = _lib.SP_MEM_HOST
+    if out is None:
+        out = {"off": off, "idx": z(O, i32), "fill": z(O, i32), "slack": z(O, f64),
+               "obj": z(O, f64), "n": z(R, i32), "delay_idx": z(R, i32), "delay_wait": z(R, f64)}
+    off = out["off"]
     check(ctx.lib.sp_speculate_batch(
         ctx.handle, len(tables), handles, float(alpha), K, ptr(pool), R, ptr(op), ptr(n_buf),
         ptr(supply), ptr(now), ptr(target), ptr(rmin), ptr(rmax), ptr(slack0), ptr(flags),
         ptr(w_ptr), ptr(w_tab), ptr(w_eidx), ptr(w_count), ptr(off), ptr(out["idx"]),
         ptr(out["fill"]), ptr(out["slack"]), ptr(out["obj"]), ptr(out["n"]),
-        ptr(out["delay_idx"]), ptr(out["delay_wait"]), _lib.SP_MEM_HOST), "sp_speculate_batch")
+        ptr(out["delay_idx"]), ptr(out["delay_wait"]), mem), "sp_speculate_batch")
     return out
 
 
