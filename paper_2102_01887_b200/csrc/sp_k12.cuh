@@ -216,13 +216,58 @@ __global__ void __launch_bounds__(32 * kK12Warps) k_slack_select(K12Dag g, K12In
 #pragma unroll
         for (int k = 0; k < KT; ++k) xf.s[k] = x.s[k];
         xf.av = x.av; xf.sup = x.sup; xf.mb = x.mb; xf.fl = x.fl;
-        decide_fast<KT>(*reinterpret_cast<const PlanHdr*>(bp), plans_sb + (uint32_t)s_off[s],
-                        (uint32_t)s_lut[s], fio, (uint32_t)dl, xf);
+        if (!out_stage) {
+          // compact decision into the 16 input bytes it has just consumed: {candidate | code,
+          // fill, slack}; the group's flush below expands it with coalesced stores
+          const FastDec r = decide_fast_core<KT>(*reinterpret_cast<const PlanHdr*>(bp),
+                                                 plans_sb + (uint32_t)s_off[s],
+                                                 (uint32_t)s_lut[s], xf);
+          s_av[dl] = (int32_t)(r.u | ((uint32_t)r.code << 16));
+          s_sup[dl] = r.fill;
+          s_mb[dl] = __double2loint(r.sk);
+          s_fl[dl] = (uint32_t)__double2hiint(r.sk);
+        } else {
+          decide_fast<KT>(*reinterpret_cast<const PlanHdr*>(bp), plans_sb + (uint32_t)s_off[s],
+                          (uint32_t)s_lut[s], fio, (uint32_t)dl, xf);
+        }
       } else {
         View<KT> v;
         make_view<KT>(v, bp, *reinterpret_cast<const PlanHdr*>(bp), K);
         decide_plan<KT, false>(v, sio, dl, x);
       }
+    }
+    if (FAST && !out_stage) {
+      // expand the compact decisions: one decision per lane, contiguous global stores (full
+      // sectors); objective, index and wait budget come from the decision's plan records
+      __syncwarp();
+      int s = lane % g.n_src;
+      const int r32 = 32 % g.n_src;
+      for (int c = lane; c < nd; c += 32) {
+        const uint32_t w0 = (uint32_t)s_av[c];
+        const uint32_t u = w0 & 0xFFFFu;
+        const int code = (int)(w0 >> 16);
+        const double sk = __hiloint2double((int)s_fl[c], s_mb[c]);
+        const uint8_t* bp = plans + s_off[s];
+        const PlanHdr* hp = reinterpret_cast<const PlanHdr*>(bp);
+        int idx = -1;
+        double obj = 0.0, wait = 0.0;
+        if (code != SP_DEC_NONE) {
+          idx = (int)(reinterpret_cast<const CandB*>(bp + hp->recb_off)[u].meta & 0xFFFFu);
+          obj = reinterpret_cast<const double*>(bp + hp->score_off)[u];
+          if ((code & 3) == SP_DEC_DELAY)  // configurator.py:275-278: slack - latency
+            wait = __dsub_rn(sk, reinterpret_cast<const double*>(bp + hp->lat_off)[u]);
+        }
+        const int d = d0 + c;
+        io.out_idx[d] = idx;
+        io.out_code[d] = code;
+        io.out_fill[d] = s_sup[c];
+        io.out_obj[d] = obj;
+        io.out_slack[d] = sk;
+        io.out_wait[d] = wait;
+        s += r32;
+        if (s >= g.n_src) s -= g.n_src;
+      }
+      continue;
     }
     if (!out_stage) continue;
     __syncwarp();

@@ -119,9 +119,17 @@ __device__ __forceinline__ int fast_row(uint32_t sm, const KindDesc& d, double s
   return r;
 }
 
+// the decision of one invocation: the final candidate id (kNone16 for None), its record, the
+// SP_DEC_* code, the fill, objective, slack and wait budget
+struct FastDec {
+  uint32_t u, meta;
+  int code, fill;
+  double score, sk, wait;
+};
+
 template <int K>
-__device__ __forceinline__ void decide_fast(const PlanHdr& h, uint32_t sm, uint32_t lut,
-                                            const FastIO<K>& io, uint32_t i, const InF<K>& x) {
+__device__ __forceinline__ FastDec decide_fast_core(const PlanHdr& h, uint32_t sm, uint32_t lut,
+                                                    const InF<K>& x) {
   const int nB = h.nB;
   const int lmax = h.lut_n - 1;
   // batch lanes admitted by min_batch (configurator.py:264-265) and by available (288)
@@ -176,15 +184,29 @@ __device__ __forceinline__ void decide_fast(const PlanHdr& h, uint32_t sm, uint3
     fb = (int)c2.y;
     sk = pick_kind<K>(x.s, (int)(c2.x >> 17));
   }
-  const int code = some ? ((delay ? SP_DEC_DELAY : SP_DEC_ASSIGN) |
-                           (((meta >> 16) & 1u) ? SP_DEC_FEASIBLE : 0))
-                        : SP_DEC_NONE;
-  io.out_idx[i] = some ? (int)(meta & 0xFFFFu) : -1;
-  io.out_code[i] = code;
-  io.out_fill[i] = some ? (delay ? x.av : min(fb, x.av)) : 0;
-  io.out_obj[i] = some ? score : 0.0;
-  io.out_slack[i] = some ? sk : 0.0;
-  io.out_wait[i] = (some && delay) ? wait : 0.0;
+  FastDec r;
+  r.u = some ? (down ? u2 : u) : kNone16;
+  r.meta = meta;
+  r.code = some ? ((delay ? SP_DEC_DELAY : SP_DEC_ASSIGN) |
+                   (((meta >> 16) & 1u) ? SP_DEC_FEASIBLE : 0))
+                : SP_DEC_NONE;
+  r.fill = some ? (delay ? x.av : min(fb, x.av)) : 0;
+  r.score = some ? score : 0.0;
+  r.sk = some ? sk : 0.0;
+  r.wait = (some && delay) ? wait : 0.0;
+  return r;
+}
+
+template <int K>
+__device__ __forceinline__ void decide_fast(const PlanHdr& h, uint32_t sm, uint32_t lut,
+                                            const FastIO<K>& io, uint32_t i, const InF<K>& x) {
+  const FastDec r = decide_fast_core<K>(h, sm, lut, x);
+  io.out_idx[i] = r.code != SP_DEC_NONE ? (int)(r.meta & 0xFFFFu) : -1;
+  io.out_code[i] = r.code;
+  io.out_fill[i] = r.fill;
+  io.out_obj[i] = r.score;
+  io.out_slack[i] = r.sk;
+  io.out_wait[i] = r.wait;
 }
 
 // CTA lookup table v -> (#batch < v) | (#batch <= v) << 8 | (tri_base(lo) - lo) << 16
