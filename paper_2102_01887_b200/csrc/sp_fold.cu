@@ -29,6 +29,7 @@
 // gap of 2^80 ulps decays below one ulp (80 / -log2(1 - beta) steps).
 #include <algorithm>
 #include <math.h>
+#include <stdlib.h>
 
 #include <cub/cub.cuh>
 
@@ -361,7 +362,10 @@ int fold_launch(sp_ctx* ctx, int n_tables, sp_table* const* tables, int n, const
     const double w = ceil(80.0 / -log2(ol));
     win = w > 4096.0 ? (1 << 30) : (w < 8.0 ? 8 : (int)w);
   }
-  const int long_min = win >= (1 << 30) ? (1 << 30) : std::max(2 * win, 512);
+  // segments longer than two windows take the block-parallel window path (measured on config 5:
+  // 2 * win = 160 beats 512 — a 512-step sequential chain in one thread is the longer pole)
+  int long_min = win >= (1 << 30) ? (1 << 30) : std::max(2 * win, 128);
+  if (const char* e = getenv("SP_FOLD_LONG_MIN")) long_min = std::max(2 * win, atoi(e));
   const int long_cap = n / (long_min + 1) + 1;
   size_t a = ((size_t)n * 4 + 255) & ~(size_t)255;
   size_t gates_bytes = ((size_t)n_tables * sizeof(Gate) + 255) & ~(size_t)255;
