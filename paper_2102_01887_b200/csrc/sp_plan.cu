@@ -1012,44 +1012,40 @@ __global__ void __launch_bounds__(1024) k_stair_lanes(int M, int K, int W, KindI
   }
   int total = 0;
   int row = block_excl_sum(cnt, s_warp, &total);
-  // the row thresholds (latency of the position before each boundary), all loads in flight
-  // together: p1 - p0 <= kStairLanesPer for the kinds this kernel takes
-  double thv[kStairLanesPer];
+  // Rows are written cooperatively: each boundary position goes to rowp[row] (pr2 is dead since
+  // the scatter), then the block writes the rows word by word — consecutive threads on
+  // consecutive words, so the row stores are coalesced and the candidate flags spread over the
+  // whole CTA; a word's lane count before the boundary is a lower bound in the lane's
+  // ascending position list.
+  uint16_t* rowp = reinterpret_cast<uint16_t*>(pr2);
 #pragma unroll
   for (int u = 0; u < kStairLanesPer; ++u) {
     const int p = p0 + u;
-    thv[u] = (p < p1 && p > 0 && ((chmask >> u) & 1u)) ? pos_lat[base + p - 1] : -INFINITY;
+    if (p >= p1) break;
+    if ((chmask >> u) & 1u) rowp[row++] = (uint16_t)p;
   }
-  {
-    uint32_t c_b[WM];  // #lane-b positions before boundary p
-#pragma unroll
-    for (int b = 0; b < WM; ++b) c_b[b] = before[b];
-#pragma unroll
-    for (int u = 0; u < kStairLanesPer; ++u) {
-      const int p = p0 + u;
-      if (p >= p1) break;
-      if ((chmask >> u) & 1u) {
-        thrscratch[ext + row] = thv[u];
-        uint32_t* rr = rowscratch + (size_t)(ext + row) * (2 * W);
-#pragma unroll
-        for (int b = 0; b < WM; ++b) {
-          if (b >= W) break;
-          const int st = s_start[b], nb = s_start[b + 1] - st;
-          const uint32_t a = c_b[b] > 0 ? L1[st + c_b[b] - 1] : kInf32;
-          const uint32_t c = (int)c_b[b] < nb ? L2[st + c_b[b]] : kInf32;
-          rr[b] = a;
-          rr[W + b] = c;
-          if (a != kInf32) candf[a] = 1u;
-          if (c != kInf32) cands[c] = 1u;
-        }
-        ++row;
-      }
-      if (p < Mk) {
-        const int l = plane[p];
-#pragma unroll
-        for (int b = 0; b < WM; ++b) c_b[b] += (l == b);
-      }
+  __syncthreads();
+  const int W2 = 2 * W;
+  for (int j = t; j < total * W2; j += T) {
+    const int rw = j / W2, b2 = j - rw * W2;
+    const int p = rowp[rw];
+    if (b2 == 0) thrscratch[ext + rw] = p > 0 ? pos_lat[base + p - 1] : -INFINITY;
+    const int b = b2 < W ? b2 : b2 - W;
+    const int st = s_start[b], nb = s_start[b + 1] - st;
+    int lo = 0, hi = nb;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if ((int)Lpos[st + mid] < p) lo = mid + 1; else hi = mid;
     }
+    uint32_t v;
+    if (b2 < W) {  // best feasible entry of lane b among positions before the boundary
+      v = lo > 0 ? L1[st + lo - 1] : kInf32;
+      if (v != kInf32) candf[v] = 1u;
+    } else {       // best penalized entry of lane b among positions from the boundary on
+      v = lo < nb ? L2[st + lo] : kInf32;
+      if (v != kInf32) cands[v] = 1u;
+    }
+    rowscratch[(size_t)(ext + rw) * W2 + b2] = v;
   }
   if (t == 0) rows_per_kind[k] = total;
 }
