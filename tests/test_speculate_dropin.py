@@ -1,0 +1,87 @@
+"""The speculation drop-in's host bookkeeping, end to end on the CPU (build container only).
+
+``speculate_from_buffer(conf, op, buffer)`` takes its decisions from one sp_speculate_batch call
+and replays the reference's bookkeeping (invocations, queues, holds, wake-ups, forced counts,
+decision log).  Here the unmodified reference engine runs the AMBER scenario with its
+``Configurator.speculate_from_buffer`` replaced by the drop-in, and the device call replaced by
+the oracle restatement (oracle/speculate.py, itself pinned to 15,000 recorded calls) over the
+engine's live tables — so the run's decision log and CSV row must equal the reference's own
+golden run (15,290 decision-log rows at the 50 % target).  The device side of
+the same call is covered bit-for-bit by tests/test_gpu_speculate.py.
+"""
+from __future__ import annotations
+
+import hashlib
+from pathlib import Path
+
+import numpy as np
+
+from oracle import optable
+from oracle import speculate as osp
+
+BUNDLE = Path("/root/reference/pkg/scenarios/branching")
+
+
+def _oracle_tables(conf):
+    kinds = list(conf.kinds)
+    out = []
+    for name, t in conf.tables.items():
+        gk = [kinds.index(e.backend_kind) for e in t.entries]
+        out.append(optable.from_columns(lat=np.array(t.lat, dtype=np.float64), res=t.res, batch=t.batch,
+                                        pool=t.pool, price=t.price, gkind=gk, id_rank=t.id_rank,
+                                        n_kinds=len(kinds), ref_index=t.ref_index))
+    return out
+
+
+def _fake_batch(conf_box):
+    """speculate_batch stand-in: the oracle over the live reference tables."""
+    def run(tables, alpha, pool, op, n_buf, supply, now, target, rmin, rmax, slack0, flags, w_ptr,
+            w_tab, w_eidx, w_count, **_):
+        conf = conf_box[0]
+        otabs = _oracle_tables(conf)
+        K = len(pool)
+        sq = [[] for _ in range(K)]
+        cq = [[] for _ in range(K)]
+        for q, lists in enumerate((sq, cq)):
+            for k in range(K):
+                for w in range(w_ptr[q * K + k], w_ptr[q * K + k + 1]):
+                    lists[k].append([int(w_tab[w]), int(w_eidx[w]), int(w_count[w])])
+        dec, delay = osp.speculate(otabs, int(op[0]), int(n_buf[0]), int(supply[0]), float(now[0]),
+                                   float(target[0]), float(rmin[0]), float(rmax[0]), pool, alpha,
+                                   int(flags[0]), sq, cq, slack0[0])
+        n = len(dec)
+        return {"off": np.array([0, n]), "idx": np.array([d[0] for d in dec], np.int64),
+                "fill": np.array([d[1] for d in dec], np.int64),
+                "slack": np.array([d[2] for d in dec]), "obj": np.array([d[3] for d in dec]),
+                "n": np.array([n]), "delay_idx": np.array([delay[0] if delay else -1]),
+                "delay_wait": np.array([delay[1] if delay else 0.0])}
+    return run
+
+
+def test_speculate_dropin_reproduces_the_reference_run(ref, monkeypatch, tmp_path):
+    from slackpipe import cli, configurator
+
+    import paper_2102_01887_b200.speculate as dropin
+
+    box = [None]
+    monkeypatch.setattr(dropin, "speculate_batch", _fake_batch(box))
+
+    def spec(self, op, buffer):
+        box[0] = self
+        return dropin.speculate_from_buffer(self, op, buffer)
+
+    monkeypatch.setattr(configurator.Configurator, "speculate_from_buffer", spec)
+    out = tmp_path / "run.csv"
+    log = tmp_path / "decisions.tsv"
+    rc = cli.main(["run", "--pipeline", str(BUNDLE / "pipeline.json"), "--scenario",
+                   str(BUNDLE / "scenario.json"), "--trace", str(BUNDLE / "trace.jsonl"),
+                   "--target", "142.20064921472454", "--metadata-dir", str(tmp_path / "md"),
+                   "--report", str(out), "--decision-log", str(log)])
+    assert rc == 0
+    row = out.read_text().strip().splitlines()[-1].split(",")
+    # golden CSV row of the reference's own run
+    assert row[1:] == ["142.20064921472454", "132.73451153109434", "0.9334311218977895",
+                       "0.16671542613566986", "1.0", "20", "0", "0"]
+    assert len(log.read_text().strip().splitlines()) == 1 + 15290  # header + decisions
+    digest = hashlib.sha256(log.read_bytes()).hexdigest()[:16]
+    assert digest == "4647eeb560b36a71"
