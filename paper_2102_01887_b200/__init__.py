@@ -26,7 +26,7 @@ from .configurator import (
     select_config,
 )
 from . import metadata
-from .commit import commit_candidates, commit_round
+from .commit import commit_candidates, commit_round, pump_commits
 from .feedback import apply_feedback, fold_observations, observation_quantiles, set_table_counters, table_counters
 from .pipeline import ConfigEntry, ConfigSpec, PipelineDag, reference_config
 from .scenario import BackendSpec, Scenario
@@ -40,7 +40,7 @@ __all__ = [
     "OpTable", "PipelineDag", "RawTable", "Scenario", "SelectResult", "Slack", "SlackGraph",
     "SlackpipeError", "TuningParams", "affinity", "affinity_from_minima", "apply_feedback",
     "commit_candidates", "commit_round", "compute_slack", "estimate_queueing", "fold_observations", "get_context", "load_library",
-    "make_flags", "metadata", "objective", "observation_quantiles", "reference_config", "remaining_path_latency", "select_batch",
+    "make_flags", "metadata", "objective", "pump_commits", "observation_quantiles", "reference_config", "remaining_path_latency", "select_batch",
     "select_config", "set_table_counters", "speculate_batch", "speculate_from_buffer",
     "table_counters",
 ]

@@ -131,3 +131,48 @@ def commit_candidates(tables: Sequence, slacks: Sequence[Mapping[str, float]],
     e = int(r["idx"][0, j])
     return (j, tables[j].entries[e], e, int(r["fill"][0, j]), float(r["slack"][0, j]),
             float(r["obj"][0, j]))
+
+
+def pump_commits(conf, buffered_count, topup) -> int:
+    """Drop-in for ``Configurator.pump_commits`` (configurator.py:693-756) on a reference-shaped
+    configurator whose ``tables`` are this package's ``OpTable``s.
+
+    Every round's candidate scan and priority key (657-728: re-selection of each op's head,
+    Eq. 3 affinity, the key order) is one ``commit_candidates`` call on the device; the commit
+    itself — popping the head, moving its weight from the speculative to the commit queue,
+    topping up, the decision log, submission (731-756) — is the reference's bookkeeping,
+    replayed in the same order.  Returns the number of commits.
+    """
+    import time
+
+    committed = 0
+    ops = list(conf.tables)
+    tabs = [conf.tables[o] for o in ops]
+    depths = [conf.depths[o] for o in ops]
+    while True:
+        t0 = time.perf_counter()
+        full = frozenset(k for k in conf.kinds if conf._cq_length(k) >= conf.cq_capacity[k])
+        heads = [conf.sq_by_op[o][0] if conf.sq_by_op[o] else None for o in ops]
+        slacks = [conf.slack_by_kind(o) if h is not None else None for o, h in zip(ops, heads)]
+        best = commit_candidates(tabs, slacks, heads, [buffered_count(o) if h is not None else 0
+                                                       for o, h in zip(ops, heads)],
+                                 depths, full, conf.params.alpha, conf.ablations)
+        if best is None:
+            return committed
+        j, entry, eidx, fill_target, slack_s, obj = best
+        op, inv = ops[j], heads[j]
+        conf.sq_by_op[op].popleft()
+        conf._weights_add(conf._sq_weight, inv.spec_entry.backend_kind, op, inv.spec_eidx, -1)
+        if fill_target > inv.fill:
+            topup(inv, fill_target - inv.fill)
+        inv.state = "committed"
+        inv.committed_entry = entry
+        inv.committed_eidx = eidx
+        inv.committed_slack_s = slack_s
+        inv.committed_at = conf._clock()
+        conf._weights_add(conf._cq_weight, entry.backend_kind, op, eidx, +1)
+        conf.decision_log.append((conf._clock(), "commit", inv.invocation_id, op,
+                                  entry.backend_kind, entry.config_id, slack_s, obj))
+        conf.commit_times.append(time.perf_counter() - t0)
+        committed += 1
+        conf._submit(inv, entry, inv.fill)
