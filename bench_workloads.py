@@ -492,9 +492,14 @@ def run_commit(args):
 
         cores = os.cpu_count() or 1
         S = 3000 * cores
-        xs = {k: v for k, v in x.items()}
-        work = [(meta, xs, int(a[0]), int(a[-1]) + 1, alpha)
-                for a in np.array_split(np.arange(S), cores) if len(a)]
+        # each worker gets only its slice of the rounds (pickling the whole batch would be
+        # timed as CPU work); `depth` is per op
+        work = []
+        for a in np.array_split(np.arange(S), cores):
+            if len(a):
+                lo, hi = int(a[0]), int(a[-1]) + 1
+                xs = {k: (v if k == "depth" else v[lo:hi]) for k, v in x.items()}
+                work.append((meta, xs, 0, hi - lo, alpha))
         t0 = time.perf_counter()
         with mp.get_context("fork").Pool(len(work)) as pool:
             n = sum(pool.map(_commit_cpu_worker, work))
@@ -591,7 +596,7 @@ def run_speculate(args):
     ctx = sp.get_context(local)
     ctx.set_stream(stream.cuda_stream)
     tabs = _amber_tables(sp, meta)
-    R = 65536
+    R = 262144  # one thread per call: enough calls to fill 148 SMs
     alpha = 100.0
     x, calls, pool = _spec_inputs(meta, R, seed=21 + rank)
     T = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(dev)
@@ -650,8 +655,14 @@ def run_speculate(args):
 
         cores = os.cpu_count() or 1
         S = 400 * cores
-        work = [(meta, x, calls, pool, int(a[0]), int(a[-1]) + 1, alpha)
-                for a in np.array_split(np.arange(S), cores) if len(a)]
+        # each worker gets only its slice (pickling the whole batch would be timed as CPU work)
+        keys = ("op", "n", "supply", "now", "target", "rmin", "rmax", "flags", "slack0")
+        work = []
+        for a in np.array_split(np.arange(S), cores):
+            if len(a):
+                lo, hi = int(a[0]), int(a[-1]) + 1
+                work.append((meta, {k: x[k][lo:hi] for k in keys}, calls[lo:hi], pool, 0, hi - lo,
+                             alpha))
         t0 = time.perf_counter()
         with mp.get_context("fork").Pool(len(work)) as pool_:
             n = sum(pool_.map(_spec_cpu_worker, work))
