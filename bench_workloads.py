@@ -373,6 +373,7 @@ def run_c5(args):
         online_batch(table, bt)
     e1.record(stream)
     torch.cuda.synchronize(dev)
+    launches = ctx.launch_count - l0
     t = _tmax(torch, e0.elapsed_time(e1) / 1e3, dev)
     # replicas must stay bit-identical: compare a checksum of the final latency table
     table.sync_from_device()
@@ -386,6 +387,54 @@ def run_c5(args):
         identical = bool(lo.item() == hi.item())
     if rank != 0:
         return
+    # Checker (world 1 only): the first two batches replayed on a fresh table, decisions against
+    # the C oracle (oracle/cselect.py) and the fold against the sequential oracle
+    # (oracle/feedback.py) — decisions and the latency table bit-identical after each batch; the
+    # CPU baseline is the numpy restatement of OpTable.select on all host cores plus the
+    # sequential fold for one batch (the reference's per-batch semantics).
+    parity, cpu = None, None
+    if world == 1:
+        from oracle import cselect, optable
+        from oracle import feedback as ofb
+
+        vtab = sp.OpTable(spec, synth.synth_scenario())
+        ot = optable.from_spec(spec, synth.synth_scenario(), ["cpu", "gpu"])
+        st = ofb.FoldState(ot.lat.copy(), np.array([e.latency_initial_s for e in spec.entries]),
+                           int(ot.ref_index))
+        checked = 0
+        for bt in range(2):
+            s = slice(bt * B, (bt + 1) * B)
+            ot.lat[:] = st.lat
+            exp = cselect.select_batch([ot], inv.slack[s], alpha, inv.avail[s], inv.supply[s],
+                                       inv.min_batch[s], inv.flags[s])
+            online_batch(vtab, bt)
+            torch.cuda.synchronize(dev)
+            got_idx = out["idx"].cpu().numpy()
+            got_code = out["code"].cpu().numpy()
+            assert np.array_equal(got_idx, exp["idx"]) and np.array_equal(got_code & 3, exp["code"] & 3), \
+                f"c5 batch {bt}: decisions disagree with the oracle"
+            oi = obs_idx.cpu().numpy()
+            ob = (lat_init[obs_idx.clamp(min=0).long()] * noise[s]).cpu().numpy()
+            keep = oi >= 0
+            ofb.fold([st], None, oi[keep], ob[keep], beta=0.5, dfp_count=10)
+            vtab.sync_from_device()
+            assert np.array_equal(np.asarray(vtab.lat).view(np.uint64), st.lat.view(np.uint64)), \
+                f"c5 batch {bt}: folded table disagrees with the oracle"
+            checked += B
+        parity = {"batches": 2, "decisions": checked, "result": "bit-identical decisions and tables"}
+        s = slice(0, B)
+        t0 = time.perf_counter()
+        optable.select_many_parallel([ot], inv.slack[s], alpha, inv.avail[s], inv.supply[s],
+                                     inv.min_batch[s], inv.flags[s])
+        t_sel = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        ofb.fold([ofb.FoldState(ot.lat.copy(), st.lat_init.copy(), int(ot.ref_index))], None,
+                 oi[keep], ob[keep], beta=0.5, dfp_count=10)
+        t_fold = time.perf_counter() - t0
+        cores = os.cpu_count() or 1
+        cpu = {"value": B / (t_sel + t_fold), "unit": "decisions/s", "cores": cores, "kind": "port",
+               "sample": f"one batch: {B} OpTable.select (oracle/optable.py numpy restatement, "
+                         f"{cores} processes) + the sequential fold of its observations"}
     line = {
         "workload": "c5", "metric": "online config decisions/s incl. per-batch feedback fold and replanning",
         "unit": "decisions/s", "value": N / t, "evals_per_s": N * M / t, "seconds": t, "n_gpus": world,
@@ -394,8 +443,10 @@ def run_c5(args):
                    "parallelism": (f"each batch split over {world} GPU(s); per batch one all-gather of the "
                                    "16-B observation records, replicated fold" if world > 1 else "1 GPU")},
         "tables_bit_identical_across_ranks": identical,
-        "gpu_launches": ctx.launch_count - l0,
+        "gpu_launches": launches,
         "per_batch_ms": 1e3 * t / NB,
+        "parity": parity,
+        "cpu_baseline": cpu,
     }
     print(json.dumps(line), flush=True)
 
