@@ -198,6 +198,30 @@ def _amber_tables(sp, meta):
     return tabs
 
 
+def _c4_cpu_worker(a):
+    """Oracle per decision: slack_by_kind (configurator.py:526-543 over the path list) of each op
+    of each instance, then OpTable.select (239-300).  Returns (instances, ops, 2) of (idx, code)."""
+    (meta, paths, value_names, alpha), inst, ref, target, now, Q, avail, supply = a
+    from oracle import commit as oc
+    from oracle import optable
+    from oracle import slack as osl
+
+    otabs = oc.amber_tables(meta)
+    kinds = meta["kinds"]
+    out = np.zeros((len(inst), len(meta["ops"]), 2), np.int64)
+    for r in range(len(inst)):
+        refmap = dict(zip(value_names, ref[r]))
+        q = dict(zip(kinds, Q[r]))
+        for j, op in enumerate(meta["ops"]):
+            sl = osl.slack_by_kind(op, kinds, target_s=float(target[r]), now=float(now[r]),
+                                   queueing=q, paths=paths, ref=refmap)
+            res = optable.select(otabs[j], np.array([sl[k] for k in kinds]), alpha,
+                                 int(avail[r, j]), allow_delay=True,
+                                 upstream_supply=int(supply[r, j]))
+            out[r, j] = (res[1], res[0])
+    return out
+
+
 def run_c4(args):
     import torch
 
@@ -271,6 +295,7 @@ def run_c4(args):
     t = _tmax(torch, sum(ms) / 1e3, dev)
     codes = torch.bincount(out["code"] & 3, minlength=3)
     launches = ctx.launch_count - l0
+    fused_out = {k: v.clone() for k, v in out.items() if k in ("idx", "code")}
     # the unfused K1 + K2 pair on the same inputs, for comparison
     for _ in range(2):
         step_two_kernels()
@@ -287,6 +312,35 @@ def run_c4(args):
     codes = codes.cpu().tolist()
     if rank != 0:
         return
+    # Checker (world 1): the fused decisions of a sample of instances against the oracle —
+    # configurator.slack_by_kind over the AMBER path list (oracle/slack.py) then OpTable.select
+    # (oracle/optable.py); the CPU baseline times exactly that per decision on all host cores
+    parity, cpu = None, None
+    if world == 1:
+        import multiprocessing as mp
+
+        fused_idx = fused_out["idx"].cpu().numpy()
+        fused_code = fused_out["code"].cpu().numpy()
+        work_meta = (meta, [tuple(p) for p in meta["paths"]], g.value_names, alpha)
+        samp = np.random.default_rng(99).choice(I, size=400, replace=False)
+        chk = _c4_cpu_worker((work_meta, samp, ref[samp], target[samp], now[samp], Q[samp],
+                              avail.reshape(I, V)[samp], supply.reshape(I, V)[samp]))
+        got = np.stack([fused_idx.reshape(I, V)[samp], fused_code.reshape(I, V)[samp] & 3], -1)
+        assert np.array_equal(chk, got), "c4: fused decisions disagree with the oracle"
+        parity = {"instances": len(samp), "decisions": len(samp) * V,
+                  "result": "bit-identical (index, kind) vs oracle slack_by_kind + OpTable.select"}
+        cores = os.cpu_count() or 1
+        S_cpu = 60 * cores
+        sl = np.array_split(np.arange(S_cpu), cores)
+        jobs = [(work_meta, a, ref[a], target[a], now[a], Q[a], avail.reshape(I, V)[a],
+                 supply.reshape(I, V)[a]) for a in sl if len(a)]
+        t0 = time.perf_counter()
+        with mp.get_context("fork").Pool(len(jobs)) as pool:
+            n = sum(len(r) * V for r in pool.map(_c4_cpu_worker, jobs))
+        dt = time.perf_counter() - t0
+        cpu = {"value": n / dt, "unit": "decisions/s", "cores": cores, "kind": "port",
+               "sample": f"{S_cpu} instances x {V} ops: oracle slack_by_kind over the path list + "
+                         f"OpTable.select per decision, {cores} processes"}
     evals_per_inst = sum(len(x.entries) for x in tabs)
     line = {
         "workload": "c4", "metric": "config decisions/s (K1 slack -> K2 select fused on device)",
@@ -303,6 +357,8 @@ def run_c4(args):
         "kernel": "k_slack_select (K1 -> K2 fused, sp_slack_select_batch)",
         "two_kernel_step_ms": {"median": statistics.median(ms2), "min": min(ms2),
                                "note": "k_slack then k_select_plan, slack through HBM"},
+        "parity": parity,
+        "cpu_baseline": cpu,
     }
     print(json.dumps(line), flush=True)
 
