@@ -599,6 +599,7 @@ int sp_dag_create(sp_ctx* ctx, int32_t V, const int32_t* pred_ptr, const int32_t
   std::vector<int32_t> pptr(1, 0), qptr(1, 0);
   std::vector<uint32_t> preds;
   int max_span = 0, max_slots = 0, max_preds = 0, n_val = 0;
+  bool single_pred = true;  // every descendant has exactly one reachable predecessor (a trie)
   for (int v = 0; v < V; ++v) n_val = std::max(n_val, val_idx[v] + 1);
   std::vector<int> slot(V, -1), last(V, -1);
   std::vector<int> free_slots;
@@ -630,6 +631,7 @@ int sp_dag_create(sp_ctx* ctx, int32_t V, const int32_t* pred_ptr, const int32_t
           int p = pred_idx[q];
           if (reach[p]) preds.push_back((uint32_t)slot[p]);
         }
+        if ((int)preds.size() - qbase - pb != 1) single_pred = false;
         if (((int)preds.size() - qbase - pb) & 1) preds.push_back(preds.back());
         // predecessors read for the last time here release their slots; the kernel reads
         // every predecessor before it writes the new value, so v may take one of them
@@ -673,6 +675,7 @@ int sp_dag_create(sp_ctx* ctx, int32_t V, const int32_t* pred_ptr, const int32_t
   g->max_span = max_span;
   g->max_slots = max_slots;
   g->max_preds = max_preds;
+  g->single_pred = single_pred ? 1 : 0;
   g->prog_len = (int64_t)prog.size();
   g->pred_len = (int64_t)preds.size();
   cudaError_t e = cudaMalloc(&g->prog, sizeof(int4) * prog.size());

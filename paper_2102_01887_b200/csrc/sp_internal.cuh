@@ -198,6 +198,9 @@ struct sp_dag {
   int32_t max_slots = 0;        // max live DP values per lane
   int32_t max_preds = 0;        // max padded pred entries of one source
   int64_t prog_len = 0, pred_len = 0;
+  // every program entry after a source has exactly one predecessor (path-list tries): the DP
+  // is a chain of sums (K12 takes a lean loop)
+  int32_t single_pred = 0;
   // Certified backward form (sp_slack.cu, k_slack_cert): one byte image, staged whole into
   // shared memory — group_ptr u16[V+1] | vidx u16[V] | term u8[V] | src u8[n_src] |
   // succ u16[4 * groups] (successor byte offsets node * 256, each list padded to a multiple of

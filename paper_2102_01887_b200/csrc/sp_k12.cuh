@@ -24,6 +24,7 @@ struct K12Dag {
   const uint32_t* preds;
   const int32_t* pred_ptr;   // n_src + 1
   int n_src, nslots, prog_len, pred_len, n_val;
+  int single_pred;  // every entry after the source has one predecessor: H = L along chains
 };
 
 struct K12In {
@@ -40,7 +41,7 @@ struct K12In {
 // decision is K2f's decide_fast (per-table lane lookup table built next to each staged plan);
 // otherwise the generic K2b decide_plan.
 template <int KT, bool FAST>
-__global__ void __launch_bounds__(32 * kK12Warps) k_slack_select(K12Dag g, K12In in, PlanPtrs pp,
+__global__ void __launch_bounds__(32 * kK12Warps, 7) k_slack_select(K12Dag g, K12In in, PlanPtrs pp,
                                                                  int plan_off, int stage_off,
                                                                  int out_stage, SelectIO io) {
   extern __shared__ __align__(16) uint8_t sm12[];
@@ -169,25 +170,41 @@ __global__ void __launch_bounds__(32 * kK12Warps) k_slack_select(K12Dag g, K12In
       D[(head.y & 0xffff) * 32] = make_double2(own, own);
       double tmax = (head.y >> 16) ? own : -INFINITY;
       double tmin = (head.y >> 16) ? own : INFINITY;
-      for (int e = 1; e < n; ++e) {
-        const int4 pr = Ps[e];
-        const double rv = Rs[pr.x * 32];
-        const uint2* gp = reinterpret_cast<const uint2*>(Gs + pr.z);
-        double hm = -INFINITY, lm = INFINITY;
-        for (int t = 0; t < pr.w; ++t) {
-          const uint2 w0 = gp[t];
-          const double2 a = *reinterpret_cast<const double2*>(Db + w0.x);
-          const double2 b = *reinterpret_cast<const double2*>(Db + w0.y);
-          hm = hm > a.x ? hm : a.x;
-          hm = hm > b.x ? hm : b.x;
-          lm = lm < a.y ? lm : a.y;
-          lm = lm < b.y ? lm : b.y;
+      if (g.single_pred) {
+        // trie programs (path lists): one predecessor each, so H and L stay equal along every
+        // chain — the DP is one add per entry (the generic loop's max / min over the padded
+        // predecessor pair would return the same value)
+        for (int e = 1; e < n; ++e) {
+          const int4 pr = Ps[e];
+          const double h = __dadd_rn(reinterpret_cast<const double2*>(Db + Gs[pr.z])->x,
+                                     Rs[pr.x * 32]);
+          D[(pr.y & 0xffff) * 32] = make_double2(h, h);
+          if (pr.y >> 16) {
+            tmax = h > tmax ? h : tmax;
+            tmin = h < tmin ? h : tmin;
+          }
         }
-        const double h = __dadd_rn(hm, rv), l = __dadd_rn(lm, rv);
-        D[(pr.y & 0xffff) * 32] = make_double2(h, l);
-        if (pr.y >> 16) {
-          tmax = h > tmax ? h : tmax;
-          tmin = l < tmin ? l : tmin;
+      } else {
+        for (int e = 1; e < n; ++e) {
+          const int4 pr = Ps[e];
+          const double rv = Rs[pr.x * 32];
+          const uint2* gp = reinterpret_cast<const uint2*>(Gs + pr.z);
+          double hm = -INFINITY, lm = INFINITY;
+          for (int t = 0; t < pr.w; ++t) {
+            const uint2 w0 = gp[t];
+            const double2 a = *reinterpret_cast<const double2*>(Db + w0.x);
+            const double2 b = *reinterpret_cast<const double2*>(Db + w0.y);
+            hm = hm > a.x ? hm : a.x;
+            hm = hm > b.x ? hm : b.x;
+            lm = lm < a.y ? lm : a.y;
+            lm = lm < b.y ? lm : b.y;
+          }
+          const double h = __dadd_rn(hm, rv), l = __dadd_rn(lm, rv);
+          D[(pr.y & 0xffff) * 32] = make_double2(h, l);
+          if (pr.y >> 16) {
+            tmax = h > tmax ? h : tmax;
+            tmin = l < tmin ? l : tmin;
+          }
         }
       }
       // min / max over suffixes of own/total, each divided out only if some kind uses it

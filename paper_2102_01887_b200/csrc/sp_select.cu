@@ -503,7 +503,8 @@ int slack_select_launch(sp_ctx* ctx, sp_dag* g, int n_tables, sp_table* const* t
     io.out_obj = out_obj; io.out_slack = out_slack; io.out_wait = out_wait;
     io.N = N; io.K = K;
     K12Dag kg{g->prog, g->prog_ptr, g->preds, g->pred_ptr, g->n_src, g->max_slots,
-              (int)g->prog_len, (int)g->pred_len, g->n_val};
+              (int)g->prog_len, (int)g->pred_len, g->n_val,
+              getenv("SP_K12_GENERIC_DP") ? 0 : g->single_pred};
     K12In ki{ref, ref_stride, target, now, Q, I, out_kslack};
     auto launch = [&](auto kern) -> int {
       static const void* attr_done[6] = {};  // one entry per k_slack_select instantiation
