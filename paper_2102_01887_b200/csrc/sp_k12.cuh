@@ -41,7 +41,7 @@ struct K12In {
 // decision is K2f's decide_fast (per-table lane lookup table built next to each staged plan);
 // otherwise the generic K2b decide_plan.
 template <int KT, bool FAST>
-__global__ void __launch_bounds__(32 * kK12Warps, 7) k_slack_select(K12Dag g, K12In in, PlanPtrs pp,
+__global__ void __launch_bounds__(32 * kK12Warps) k_slack_select(K12Dag g, K12In in, PlanPtrs pp,
                                                                  int plan_off, int stage_off,
                                                                  int out_stage, SelectIO io) {
   extern __shared__ __align__(16) uint8_t sm12[];
@@ -174,6 +174,7 @@ __global__ void __launch_bounds__(32 * kK12Warps, 7) k_slack_select(K12Dag g, K1
         // trie programs (path lists): one predecessor each, so H and L stay equal along every
         // chain — the DP is one add per entry (the generic loop's max / min over the padded
         // predecessor pair would return the same value)
+#pragma unroll 1
         for (int e = 1; e < n; ++e) {
           const int4 pr = Ps[e];
           const double h = __dadd_rn(reinterpret_cast<const double2*>(Db + Gs[pr.z])->x,
