@@ -399,6 +399,7 @@ def run_c5(args):
            (("idx", torch.int32), ("code", torch.int32), ("fill", torch.int32),
             ("obj", torch.float64), ("slack", torch.float64), ("wait", torch.float64))}
     obs_idx = torch.empty(Bl, dtype=torch.int32, device=dev)
+    neg1 = torch.full((Bl,), -1, dtype=torch.int32, device=dev)
     alpha = 100.0
 
     def online_batch(tab, bt):
@@ -408,8 +409,8 @@ def run_c5(args):
         s = slice(bt * B + a, bt * B + b)
         tab.select_batch(d["slack"][s], alpha, d["avail"][s], upstream_supply=d["supply"][s],
                          min_batch=d["mb"][s], flags=d["flags"][s], out=out)
-        torch.where((out["code"] & 3) == 1, out["idx"], torch.full_like(out["idx"], -1), out=obs_idx)
-        obs = lat_init[obs_idx.clamp(min=0).long()] * noise[s]
+        torch.where((out["code"] & 3) == 1, out["idx"], neg1, out=obs_idx)
+        obs = torch.index_select(lat_init, 0, obs_idx.clamp(min=0)) * noise[s]
         f_idx, f_obs = gather_observations(obs_idx, obs, B) if world > 1 else (obs_idx, obs)
         sp.fold_observations([tab], None, f_idx, f_obs, beta=0.5, dfp_count=10, sync_host=False)
 
