@@ -77,8 +77,9 @@ __device__ __forceinline__ Key shfl_key(const Key& k, int src) {
   return o;
 }
 
-// one warp per round; lane l handles ops l and l + 32
-__global__ void k_commit_round(int R, int n_ops, int K, CommitTabs tb,
+// LPR lanes per round (a power of two >= min(n_ops, 32)), 32 / LPR rounds per warp; lane l of a
+// round's group handles ops l, l + LPR, ...
+__global__ void k_commit_round(int R, int n_ops, int K, int lpr_log2, CommitTabs tb,
                                const double* __restrict__ slack,
                                const int32_t* __restrict__ fill,
                                const long long* __restrict__ head_id,
@@ -95,16 +96,19 @@ __global__ void k_commit_round(int R, int n_ops, int K, CommitTabs tb,
                                const double* __restrict__ kmin, int32_t* out_idx,
                                int32_t* out_fill, double* out_slack, double* out_obj,
                                double* out_aff, int32_t* out_best) {
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (warp >= R) return;
+  const int LPR = 1 << lpr_log2;
+  const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int warp = gid >> lpr_log2;  // the round this lane works on
+  const int lane = gid & (LPR - 1);
+  if (((gid >> 5) << 5) >= R * LPR) return;  // whole warp past the last round
+  const bool live = warp < R;
   const bool fifo = policy & SP_COMMIT_FIFO;
   const bool eslc = policy & SP_COMMIT_ESLC;
-  const uint32_t full = full_mask[warp];
+  const uint32_t full = live ? full_mask[warp] : 0u;
   Key best;
   best.op = -1;
   best.cls = 0; best.k1 = 0.0; best.k2 = 0.0; best.id = 0;
-  for (int j = lane; j < n_ops; j += 32) {
+  for (int j = lane; live && j < n_ops; j += LPR) {
     const int i = warp * n_ops + j;
     const uint32_t hf = hflags[i];
     int idx = -1, ft = 0;
@@ -159,12 +163,13 @@ __global__ void k_commit_round(int R, int n_ops, int K, CommitTabs tb,
     out_aff[i] = aff;
     if (key_less(k, best)) best = k;
   }
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    const Key o = shfl_key(best, lane ^ off);
+  // reduction inside each LPR-lane group (xor partners stay inside the group)
+  const int wl = threadIdx.x & 31;
+  for (int off = LPR >> 1; off > 0; off >>= 1) {
+    const Key o = shfl_key(best, wl ^ off);
     if (key_less(o, best)) best = o;
   }
-  if (lane == 0) out_best[warp] = best.op;
+  if (live && lane == 0) out_best[warp] = best.op;
 }
 
 }  // namespace
@@ -207,8 +212,10 @@ int commit_launch(sp_ctx* ctx, int R, int n_ops, sp_table* const* tables, double
                          d_code, d_fill, d_obj, d_sl, d_wait, d_kmin, SP_MODE_AUTO);
   if (rc != SP_OK) return rc;
   const int threads = 256;
-  k_commit_round<<<(R * 32 + threads - 1) / threads, threads, 0, ctx->stream>>>(
-      R, n_ops, K, tb, slack, fill, head_id, depth, hflags, spec_idx, spec_slack, spec_obj,
+  int lg = 0;
+  while ((1 << lg) < n_ops && lg < 5) ++lg;  // lanes per round: next power of two, <= 32
+  k_commit_round<<<(int)(((size_t)R * (1 << lg) + threads - 1) / threads), threads, 0, ctx->stream>>>(
+      R, n_ops, K, lg, tb, slack, fill, head_id, depth, hflags, spec_idx, spec_slack, spec_obj,
       full_mask, policy, d_idx, d_fill, d_obj, d_sl, d_kmin, out_idx, out_fill, out_slack,
       out_obj, out_aff, out_best);
   SP_CHECK_LAUNCH(ctx);
