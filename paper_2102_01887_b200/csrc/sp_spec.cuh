@@ -62,114 +62,142 @@ struct SpecKey {
 template <int KT>
 __global__ void __launch_bounds__(128) k_speculate(SpecTabs tb, double alpha, SpecIO io,
                                                    SelectIO sel) {
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= io.R) return;
+  // Persistent threads: each thread runs calls r, r + stride, ... one loop ITERATION per pass of
+  // the outer loop, taking its next call the moment the current one ends — the calls' loops
+  // have different lengths, so lanes stay converged on the iteration body instead of idling
+  // behind the longest call of the warp.
+  const int stride = gridDim.x * blockDim.x;
   const int K = io.K;
-  const int op = io.op[r];
-  int n = io.n_buf[r];
-  const int supply = io.supply[r];
-  const double span = __dsub_rn(io.target[r], io.now[r]);  // target - now
-  const double rmin = io.rmin[r], rmax = io.rmax[r];
-  const uint32_t fl = io.flags[r];
-  const int32_t* wp = io.w_ptr + (size_t)r * 2 * K;
-  View<KT> v;
-  make_view<KT>(v, tb.plan[op], *reinterpret_cast<const PlanHdr*>(tb.plan[op]), K);
-  SpecKey keys[kMaxSpecKeys];
-  int nk = 0;
-  const int o0 = io.out_off[r];
-  int nd = 0;
+  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  int op = 0, n = 0, supply = 0, nk = 0, o0 = 0, nd = 0;
+  double span = 0.0, rmin = 0.0, rmax = 0.0;
+  uint32_t fl = 0;
   bool first = true, overflow = false;
-  io.out_delay_idx[r] = -1;
-  io.out_delay_wait[r] = 0.0;
+  const int32_t* wp = io.w_ptr;
+  View<KT> v;
+  SpecKey keys[kMaxSpecKeys];
   In<KT> x;
-  while (n > 0) {
+  auto start = [&](int rr) {  // load call rr's state
+    op = io.op[rr];
+    n = io.n_buf[rr];
+    supply = io.supply[rr];
+    span = __dsub_rn(io.target[rr], io.now[rr]);  // target - now
+    rmin = io.rmin[rr];
+    rmax = io.rmax[rr];
+    fl = io.flags[rr];
+    wp = io.w_ptr + (size_t)rr * 2 * K;
+    make_view<KT>(v, tb.plan[op], *reinterpret_cast<const PlanHdr*>(tb.plan[op]), K);
+    nk = 0;
+    o0 = io.out_off[rr];
+    nd = 0;
+    first = true;
+    overflow = false;
+    io.out_delay_idx[rr] = -1;
+    io.out_delay_wait[rr] = 0.0;
+  };
+  if (r < io.R) start(r);
+  while (r < io.R) {
+    bool done = n <= 0;
+    if (!done) {
 #pragma unroll
-    for (int k = 0; k < KT; ++k) {
-      if (k >= K) {
-        x.s[k] = 0.0;
-        continue;
+      for (int k = 0; k < KT; ++k) {
+        if (k >= K) {
+          x.s[k] = 0.0;
+          continue;
+        }
+        if (first) {
+          x.s[k] = io.slack0[(size_t)r * K + k];
+          continue;
+        }
+        double total = 0.0;  // configurator.py:516-522
+        for (int w = wp[k]; w < wp[k + 1]; ++w) {  // SQ, in dict order
+          int c = io.w_count[w];
+          for (int q = 0; q < nk; ++q) c += keys[q].orig == w ? keys[q].cnt : 0;
+          const int t = io.w_tab[w], e = io.w_eidx[w];
+          total = __dadd_rn(total, __dmul_rn((double)c, __dmul_rn(tb.lat[t][e], tb.res[t][e])));
+        }
+        for (int q = 0; q < nk; ++q) {  // keys this call appended to the kind's SQ dict
+          if (keys[q].orig >= 0 || keys[q].kind != k) continue;
+          const int t = keys[q].tab, e = keys[q].eidx;
+          total = __dadd_rn(total,
+                            __dmul_rn((double)keys[q].cnt, __dmul_rn(tb.lat[t][e], tb.res[t][e])));
+        }
+        for (int w = wp[K + k]; w < wp[K + k + 1]; ++w) {  // CQ
+          const int t = io.w_tab[w], e = io.w_eidx[w];
+          total = __dadd_rn(total,
+                            __dmul_rn((double)io.w_count[w], __dmul_rn(tb.lat[t][e], tb.res[t][e])));
+        }
+        const double budget = __dsub_rn(span, __ddiv_rn(total, tb.pool[k]));  // 535
+        x.s[k] = __dmul_rn(budget >= 0.0 ? rmin : rmax, budget);             // 536-540
       }
-      if (first) {
-        x.s[k] = io.slack0[(size_t)r * K + k];
-        continue;
+      int idx = -1, fill = 0, kd = 0;
+      double s_k = 0.0, obj = 0.0;
+      if (fl & SP_SPEC_FORCED) {  // configurator.py:571-589
+        idx = tb.ref_index[op];
+        fill = 1;
+        kd = tb.kind[op][idx];
+        s_k = pick_kind<KT>(x.s, kd);
+        obj = NAN;
+      } else {
+        const bool allow = (fl & SP_SPEC_SDB) && !(first && (fl & SP_SPEC_HOLD_EXPIRED));
+        x.av = n;
+        x.sup = supply;
+        x.mb = 1;
+        x.fl = allow ? SP_FLAG_ALLOW_DELAY : 0u;
+        x.t = op;
+        decide_plan<KT, false>(v, sel, r, x);
+        const int code = sel.out_code[r];
+        idx = sel.out_idx[r];
+        if ((code & 3) == SP_DEC_DELAY) {  // configurator.py:606-612
+          io.out_delay_idx[r] = idx;
+          io.out_delay_wait[r] = sel.out_wait[r];
+          done = true;
+        } else if ((code & 3) != SP_DEC_ASSIGN) {  // cannot happen without exclusions (605)
+          overflow = true;
+          done = true;
+        } else {
+          fill = sel.out_fill[r];
+          s_k = sel.out_slack[r];
+          obj = sel.out_obj[r];
+          kd = tb.kind[op][idx];
+        }
       }
-      double total = 0.0;  // configurator.py:516-522
-      for (int w = wp[k]; w < wp[k + 1]; ++w) {  // SQ, in dict order
-        int c = io.w_count[w];
-        for (int q = 0; q < nk; ++q) c += keys[q].orig == w ? keys[q].cnt : 0;
-        const int t = io.w_tab[w], e = io.w_eidx[w];
-        total = __dadd_rn(total, __dmul_rn((double)c, __dmul_rn(tb.lat[t][e], tb.res[t][e])));
+      if (!done) {
+        first = false;
+        n -= fill;
+        // _weights_add(self._sq_weight, kind, op, idx, +1)
+        int hit = -1;
+        for (int q = 0; q < nk; ++q)
+          if (keys[q].kind == kd && keys[q].tab == op && keys[q].eidx == idx) hit = q;
+        if (hit < 0) {
+          int orig = -1;
+          for (int w = wp[kd]; w < wp[kd + 1]; ++w)
+            if (io.w_tab[w] == op && io.w_eidx[w] == idx) orig = w;
+          if (nk == kMaxSpecKeys) {
+            overflow = true;
+            done = true;
+          } else {
+            keys[nk] = SpecKey{kd, op, idx, 0, orig};
+            hit = nk++;
+          }
+        }
+        if (!done) {
+          keys[hit].cnt += 1;
+          io.out_idx[o0 + nd] = idx;
+          io.out_fill[o0 + nd] = fill;
+          io.out_slack[o0 + nd] = s_k;
+          io.out_obj[o0 + nd] = obj;
+          ++nd;
+          done = n <= 0;
+        }
       }
-      for (int q = 0; q < nk; ++q) {  // keys this call appended to the kind's SQ dict
-        if (keys[q].orig >= 0 || keys[q].kind != k) continue;
-        const int t = keys[q].tab, e = keys[q].eidx;
-        total = __dadd_rn(total, __dmul_rn((double)keys[q].cnt, __dmul_rn(tb.lat[t][e], tb.res[t][e])));
-      }
-      for (int w = wp[K + k]; w < wp[K + k + 1]; ++w) {  // CQ
-        const int t = io.w_tab[w], e = io.w_eidx[w];
-        total = __dadd_rn(total,
-                          __dmul_rn((double)io.w_count[w], __dmul_rn(tb.lat[t][e], tb.res[t][e])));
-      }
-      const double budget = __dsub_rn(span, __ddiv_rn(total, tb.pool[k]));  // 535
-      x.s[k] = __dmul_rn(budget >= 0.0 ? rmin : rmax, budget);             // 536-540
     }
-    int idx, fill, kd;
-    double s_k, obj;
-    if (fl & SP_SPEC_FORCED) {  // configurator.py:571-589
-      idx = tb.ref_index[op];
-      fill = 1;
-      kd = tb.kind[op][idx];
-      s_k = pick_kind<KT>(x.s, kd);
-      obj = NAN;
-    } else {
-      const bool allow = (fl & SP_SPEC_SDB) && !(first && (fl & SP_SPEC_HOLD_EXPIRED));
-      x.av = n;
-      x.sup = supply;
-      x.mb = 1;
-      x.fl = allow ? SP_FLAG_ALLOW_DELAY : 0u;
-      x.t = op;
-      decide_plan<KT, false>(v, sel, r, x);
-      const int code = sel.out_code[r];
-      idx = sel.out_idx[r];
-      if ((code & 3) == SP_DEC_DELAY) {  // configurator.py:606-612
-        io.out_delay_idx[r] = idx;
-        io.out_delay_wait[r] = sel.out_wait[r];
-        break;
-      }
-      if ((code & 3) != SP_DEC_ASSIGN) {  // cannot happen without exclusions (assert, 605)
-        overflow = true;
-        break;
-      }
-      fill = sel.out_fill[r];
-      s_k = sel.out_slack[r];
-      obj = sel.out_obj[r];
-      kd = tb.kind[op][idx];
+    if (done) {
+      io.out_n[r] = overflow ? -1 : nd;
+      r += stride;
+      if (r < io.R) start(r);
     }
-    first = false;
-    n -= fill;
-    // _weights_add(self._sq_weight, kind, op, idx, +1)
-    int hit = -1;
-    for (int q = 0; q < nk; ++q)
-      if (keys[q].kind == kd && keys[q].tab == op && keys[q].eidx == idx) hit = q;
-    if (hit < 0) {
-      int orig = -1;
-      for (int w = wp[kd]; w < wp[kd + 1]; ++w)
-        if (io.w_tab[w] == op && io.w_eidx[w] == idx) orig = w;
-      if (nk == kMaxSpecKeys) {
-        overflow = true;
-        break;
-      }
-      keys[nk] = SpecKey{kd, op, idx, 0, orig};
-      hit = nk++;
-    }
-    keys[hit].cnt += 1;
-    io.out_idx[o0 + nd] = idx;
-    io.out_fill[o0 + nd] = fill;
-    io.out_slack[o0 + nd] = s_k;
-    io.out_obj[o0 + nd] = obj;
-    ++nd;
   }
-  io.out_n[r] = overflow ? -1 : nd;
 }
 
 }  // namespace
@@ -216,7 +244,15 @@ int speculate_launch(sp_ctx* ctx, int n_tables, sp_table* const* tables, double 
   SpecIO io{op, n_buf, supply, now, target, rmin, rmax, slack0, flags, w_ptr, w_tab, w_eidx,
             w_count, out_off, out_idx, out_fill, out_slack, out_obj, out_n, out_delay_idx,
             out_delay_wait, R, K};
-  const int blocks = (R + 127) / 128;
+  // persistent grid: resident CTAs only (calls are taken by grid stride)
+  int per_sm = 0;
+  if (K <= 2)
+    SP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_speculate<2>, 128, 0));
+  else if (K <= 4)
+    SP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_speculate<4>, 128, 0));
+  else
+    SP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_speculate<8>, 128, 0));
+  const int blocks = std::max(1, std::min((R + 127) / 128, ctx->num_sms * std::max(per_sm, 1)));
   if (K <= 2)
     k_speculate<2><<<blocks, 128, 0, ctx->stream>>>(tb, alpha, io, sel);
   else if (K <= 4)
