@@ -79,7 +79,7 @@ struct __align__(16) SItem {
   uint32_t t;
   uint32_t pad;
 };
-constexpr int kSortThreads = 128, kSortIpt = 4, kSortTile = kSortThreads * kSortIpt;
+constexpr int kSortThreads = 256, kSortIpt = 2, kSortTile = kSortThreads * kSortIpt;
 constexpr int kSortR1 = 0, kSortR2 = 1, kSortOrder = 2;
 
 template <int KIND>
