@@ -930,29 +930,73 @@ __global__ void __launch_bounds__(1024) k_stair_lanes(int M, int K, int W, KindI
   // ---- 4. segmented prefix minimum of r1 (forward) and suffix minimum of r2 (backward) ----
   const int E = (Mk + T - 1) / T;  // list elements per thread
   const int j0 = min(t * E, Mk), j1 = min(j0 + E, Mk);
+  // a full chunk of 8 is moved with vector shared-memory accesses (one LDS.64 / LDS.128 per
+  // array instead of eight 4-byte loads at an 8-word stride, which conflict 8 ways)
+  const bool vec = E == 8 && j1 - j0 == 8;
+  uint32_t vl[8], v1[8], v2[8], vp[8];
+  if (vec) {
+    const uint2 ll = *reinterpret_cast<const uint2*>(Llane + j0);
+    const uint4 a0 = *reinterpret_cast<const uint4*>(L1 + j0);
+    const uint4 a1 = *reinterpret_cast<const uint4*>(L1 + j0 + 4);
+    const uint4 b0 = *reinterpret_cast<const uint4*>(L2 + j0);
+    const uint4 b1 = *reinterpret_cast<const uint4*>(L2 + j0 + 4);
+    const uint4 pp = *reinterpret_cast<const uint4*>(Lpos + j0);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) vl[u] = ((u < 4 ? ll.x : ll.y) >> (8 * (u & 3))) & 0xFFu;
+    v1[0] = a0.x; v1[1] = a0.y; v1[2] = a0.z; v1[3] = a0.w;
+    v1[4] = a1.x; v1[5] = a1.y; v1[6] = a1.z; v1[7] = a1.w;
+    v2[0] = b0.x; v2[1] = b0.y; v2[2] = b0.z; v2[3] = b0.w;
+    v2[4] = b1.x; v2[5] = b1.y; v2[6] = b1.z; v2[7] = b1.w;
+    const uint32_t pw[4] = {pp.x, pp.y, pp.z, pp.w};
+#pragma unroll
+    for (int u = 0; u < 8; ++u) vp[u] = (pw[u >> 1] >> (16 * (u & 1))) & 0xFFFFu;
+  }
   {
     SegMin a;
     a.seg = 0xFFFFFFFFu;
     a.val = kInf32;
-    for (int j = j0; j < j1; ++j) {
-      SegMin x;
-      x.seg = Llane[j];
-      x.val = L1[j];
-      a = (a.seg == 0xFFFFFFFFu) ? x : seg_combine(a, x);
+    if (vec) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        SegMin x;
+        x.seg = vl[u];
+        x.val = v1[u];
+        a = (a.seg == 0xFFFFFFFFu) ? x : seg_combine(a, x);
+      }
+    } else {
+      for (int j = j0; j < j1; ++j) {
+        SegMin x;
+        x.seg = Llane[j];
+        x.val = L1[j];
+        a = (a.seg == 0xFFFFFFFFu) ? x : seg_combine(a, x);
+      }
     }
     if (j0 >= j1) a.seg = 0xFFFFFFFEu;  // empty chunk: passes nothing on
     SegMin c = block_excl_segmin(a, t, s_seg, s_val);
     uint32_t rn = kInf32;
     uint32_t sg = 0xFFFFFFFFu;
-    if (j0 < j1 && c.seg == Llane[j0]) rn = c.val;
-    for (int j = j0; j < j1; ++j) {
-      const uint32_t l = Llane[j];
-      if (l != sg && j != j0) rn = kInf32;
-      sg = l;
-      const uint32_t v = L1[j];
-      impP[Lpos[j]] = v < rn;
-      rn = min(rn, v);
-      L1[j] = rn;  // inclusive prefix minimum inside the lane
+    if (j0 < j1 && c.seg == (vec ? vl[0] : (uint32_t)Llane[j0])) rn = c.val;
+    if (vec) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (vl[u] != sg && u != 0) rn = kInf32;
+        sg = vl[u];
+        impP[vp[u]] = v1[u] < rn;
+        rn = min(rn, v1[u]);
+        v1[u] = rn;  // inclusive prefix minimum inside the lane
+      }
+      *reinterpret_cast<uint4*>(L1 + j0) = make_uint4(v1[0], v1[1], v1[2], v1[3]);
+      *reinterpret_cast<uint4*>(L1 + j0 + 4) = make_uint4(v1[4], v1[5], v1[6], v1[7]);
+    } else {
+      for (int j = j0; j < j1; ++j) {
+        const uint32_t l = Llane[j];
+        if (l != sg && j != j0) rn = kInf32;
+        sg = l;
+        const uint32_t v = L1[j];
+        impP[Lpos[j]] = v < rn;
+        rn = min(rn, v);
+        L1[j] = rn;  // inclusive prefix minimum inside the lane
+      }
     }
   }
   {
@@ -961,25 +1005,48 @@ __global__ void __launch_bounds__(1024) k_stair_lanes(int M, int K, int W, KindI
     SegMin a;
     a.seg = 0xFFFFFFFFu;
     a.val = kInf32;
-    for (int j = k1 - 1; j >= k0; --j) {
-      SegMin x;
-      x.seg = Llane[j];
-      x.val = L2[j];
-      a = (a.seg == 0xFFFFFFFFu) ? x : seg_combine(a, x);
+    if (vec) {
+#pragma unroll
+      for (int u = 7; u >= 0; --u) {
+        SegMin x;
+        x.seg = vl[u];
+        x.val = v2[u];
+        a = (a.seg == 0xFFFFFFFFu) ? x : seg_combine(a, x);
+      }
+    } else {
+      for (int j = k1 - 1; j >= k0; --j) {
+        SegMin x;
+        x.seg = Llane[j];
+        x.val = L2[j];
+        a = (a.seg == 0xFFFFFFFFu) ? x : seg_combine(a, x);
+      }
     }
     if (k0 >= k1) a.seg = 0xFFFFFFFEu;
     SegMin c = block_excl_segmin(a, tm, s_seg, s_val);
     uint32_t rn = kInf32;
     uint32_t sg = 0xFFFFFFFFu;
-    if (k0 < k1 && c.seg == Llane[k1 - 1]) rn = c.val;
-    for (int j = k1 - 1; j >= k0; --j) {
-      const uint32_t l = Llane[j];
-      if (l != sg && j != k1 - 1) rn = kInf32;
-      sg = l;
-      const uint32_t v = L2[j];
-      impS[Lpos[j]] = v < rn;
-      rn = min(rn, v);
-      L2[j] = rn;  // inclusive suffix minimum inside the lane
+    if (k0 < k1 && c.seg == (vec ? vl[7] : (uint32_t)Llane[k1 - 1])) rn = c.val;
+    if (vec) {
+#pragma unroll
+      for (int u = 7; u >= 0; --u) {
+        if (vl[u] != sg && u != 7) rn = kInf32;
+        sg = vl[u];
+        impS[vp[u]] = v2[u] < rn;
+        rn = min(rn, v2[u]);
+        v2[u] = rn;  // inclusive suffix minimum inside the lane
+      }
+      *reinterpret_cast<uint4*>(L2 + j0) = make_uint4(v2[0], v2[1], v2[2], v2[3]);
+      *reinterpret_cast<uint4*>(L2 + j0 + 4) = make_uint4(v2[4], v2[5], v2[6], v2[7]);
+    } else {
+      for (int j = k1 - 1; j >= k0; --j) {
+        const uint32_t l = Llane[j];
+        if (l != sg && j != k1 - 1) rn = kInf32;
+        sg = l;
+        const uint32_t v = L2[j];
+        impS[Lpos[j]] = v < rn;
+        rn = min(rn, v);
+        L2[j] = rn;  // inclusive suffix minimum inside the lane
+      }
     }
   }
   __syncthreads();
