@@ -65,6 +65,13 @@ def _barrier(torch):
         torch.distributed.barrier()
 
 
+def _clocks(local):
+    """NVML clock / throttle-reason sampler around a timed region (bench.ClockSampler)."""
+    from bench import ClockSampler
+
+    return ClockSampler(local)
+
+
 def _peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     return float(json.loads(p.read_text())["hbm_gbs"]) if p.exists() else 6650.0
@@ -116,16 +123,31 @@ def run_c3(args):
     _barrier(torch)
     evs = _events(torch, args.steps)
     l0 = ctx.launch_count
-    for i in range(args.steps):
-        flush()
-        evs[i][0].record(stream)
-        g.slack_batch(d["ref"], d["T"], d["now"], d["Q"], out=out)
-        evs[i][1].record(stream)
-    torch.cuda.synchronize(dev)
+    with _clocks(local) as clk:
+        for i in range(args.steps):
+            flush()
+            evs[i][0].record(stream)
+            g.slack_batch(d["ref"], d["T"], d["now"], d["Q"], out=out)
+            evs[i][1].record(stream)
+        torch.cuda.synchronize(dev)
     ms = [x.elapsed_time(y) for x, y in evs]
     launches = ctx.launch_count - l0
     t = _tmax(torch, sum(ms) / 1e3, dev)
     vals = args.steps * I * V * K * world
+    got = out["slack"].cpu().numpy()
+    # checker: every slack value of this rank's launch against the C forward-DP restatement
+    from oracle import cselect
+
+    exp = cselect.slack_dp(dag, ref, T, now, Q)
+    bad = torch.tensor([int(np.count_nonzero(got.view(np.uint64) != exp.view(np.uint64))), got.size],
+                       dtype=torch.int64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(bad)
+    bad = bad.cpu().tolist()
+    parity = {"slack_values": bad[1], "mismatches": bad[0],
+              "result": ("bit-identical vs oracle_slack_dp (C forward-DP restatement of Alg. 1, "
+                         "SURVEY.md §8(c))" if bad[0] == 0 else "MISMATCH"),
+              "checked_on": f"all {world} rank(s), every (instance, op, kind) of the step"}
     # the same step through K1's per-source forward DP (SP_K1_CERT=0), reported beside it
     os.environ["SP_K1_CERT"] = "0"
     try:
@@ -156,10 +178,11 @@ def run_c3(args):
 
         chunks = np.array_split(np.arange(S), cores)
         work = [(order, preds, term, vcol, ref[c], T[c], now[c], Q[c]) for c in chunks if len(c)]
-        t0 = time.perf_counter()
-        with mp.get_context("fork").Pool(len(work)) as pool:
+        with mp.get_context("fork").Pool(len(work)) as pool:  # forked outside the timed map
+            pool.map(_c3_cpu_worker, [w[:4] + tuple(x[:1] for x in w[4:]) for w in work])
+            t0 = time.perf_counter()
             n_cpu = sum(pool.map(_c3_cpu_worker, work))
-        cpu_t = time.perf_counter() - t0
+            cpu_t = time.perf_counter() - t0
     line = {
         "workload": "c3", "metric": "Alg. 1 slack values (instance x op x kind) / s", "unit": "slack/s",
         "value": vals / t, "ms_per_step": 1e3 * t / args.steps, "steps": args.steps, "n_gpus": world,
@@ -174,10 +197,12 @@ def run_c3(args):
                      "hbm_frac": (args.steps * I * world * bytes_inst / t / 1e9) / (world * _peaks())},
         "forward_dp_step_ms": fwd_ms,
         "gpu_launches": launches,
+        "parity": parity,
         "cpu_baseline": None if world > 1 else {"value": n_cpu / cpu_t, "unit": "slack/s", "cores": cores,
                          "kind": "restatement (the reference cannot run this DAG)",
                          "sample": f"{S} instances, oracle/slack.py dp_ratios on {cores} processes"},
         "step_ms": {"median": statistics.median(ms), "min": min(ms), "max": max(ms)},
+        "clocks": clk.summary(),
     }
     print(json.dumps(line), flush=True)
 
@@ -222,43 +247,74 @@ def _c4_cpu_worker(a):
     return out
 
 
+def c4_full_parity(meta, paths_cols, ops_ref, sw, alpha, got_idx, got_code, got_obj=None):
+    """Checker: every decision of a config-4 step against the C oracle — literal Alg. 1 over the
+    AMBER path list (oracle_slack_paths, configurator.py:415-417, 493-543) then the literal
+    OpTable.select scan (oracle_select_batch, configurator.py:239-300).  Returns a parity dict."""
+    from oracle import commit as oc
+    from oracle import cselect
+
+    I, V = sw.ref.shape
+    K = sw.Q.shape[1]
+    sl = cselect.slack_paths(sw.ref, sw.target, sw.now, sw.Q, paths_cols)
+    otabs = oc.amber_tables(meta)
+    N = I * V
+    exp = cselect.select_batch(otabs, sl.reshape(N, K), alpha, sw.avail.reshape(-1),
+                               sw.supply.reshape(-1), np.ones(N, np.int32), np.ones(N, np.uint32),
+                               op=np.tile(np.arange(V, dtype=np.int32), I))
+    bad_idx = int(np.count_nonzero(exp["idx"] != got_idx))
+    bad_code = int(np.count_nonzero(exp["code"] != (got_code & 3)))
+    res = {"decisions": int(N), "instances": int(I), "index_mismatches": bad_idx,
+           "kind_code_mismatches": bad_code}
+    if got_obj is not None:
+        some = exp["code"] != 0
+        res["objective_mismatches"] = int(np.count_nonzero(
+            exp["obj"][some].view(np.uint64) != got_obj[some].view(np.uint64)))
+    res["result"] = ("bit-identical" if not any(v for k, v in res.items() if k.endswith("mismatches"))
+                     else "MISMATCH")
+    return res
+
+
+def _c4_meta():
+    with np.load(ROOT / "tests" / "golden" / "amber_trace.npz") as z:
+        meta = json.loads(bytes(z["meta_json"]).decode())
+    ops = meta["ops"]
+    ref0 = np.array([meta["tables"][o]["lat"][meta["tables"][o]["ref_index"]]
+                     if meta["tables"][o]["ref_index"] >= 0 else 1.0 for o in ops])
+    paths_cols = [[ops.index(n) for n in p] for p in meta["paths"]]
+    return meta, ops, ref0, paths_cols
+
+
 def run_c4(args):
     import torch
 
     import paper_2102_01887_b200 as sp
+    from paper_2102_01887_b200 import synth
+    from paper_2102_01887_b200.shard import shard_range
 
-    with np.load(ROOT / "tests" / "golden" / "amber_trace.npz") as z:
-        meta = json.loads(bytes(z["meta_json"]).decode())
+    meta, ops, ref0, paths_cols = _c4_meta()
     rank, world, local = _dist(torch)
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream(dev)
     ctx = sp.get_context(local)
     ctx.set_stream(stream.cuda_stream)
     tabs = _amber_tables(sp, meta)
-    ops = meta["ops"]
     V, K = len(ops), len(meta["kinds"])
     g = sp.SlackGraph.from_paths([tuple(p) for p in meta["paths"]], ops)
-    ref0 = np.array([meta["tables"][o]["lat"][meta["tables"][o]["ref_index"]]
-                     if meta["tables"][o]["ref_index"] >= 0 else 1.0 for o in ops])
-    # value order of the graph = names in path order; map
-    vpos = [ops.index(n) for n in g.value_names]
-    R, mults, S = args.c4_replicas, (0.5, 1.0, 2.0, 5.0, 10.0), 64
-    cp_min = 90.41885182994682
-    I = R * len(mults) * S
-    rng = np.random.default_rng(4 + 1000 * rank)  # rank r owns replicas [r*R, (r+1)*R)
-    target = np.repeat(np.array(mults) * cp_min, S)[None, :].repeat(R, 0).reshape(-1)
-    now = (np.tile(np.arange(S) / S, R * len(mults))) * target
-    Q = rng.exponential(1.0, size=(I, K)) * (0.02 * target)[:, None]
-    ref = (ref0[vpos][None, :] * np.exp(rng.normal(0.0, 0.2, size=(I, len(vpos)))))
+    vpos = [ops.index(n) for n in g.value_names]  # graph value order -> op column
+    mults, S = synth.SWEEP_MULTS, synth.SWEEP_SNAPSHOTS
+    # strong scaling: the job is R replicas in total (BASELINE config 4: 10k replicas sharded
+    # over the GPUs); rank g owns the contiguous replica range shard_range(R, g, G)
+    R = args.c4_replicas
+    r0, r1 = shard_range(R, rank, world)
+    sw = synth.amber_sweep(ref0, K, r0, r1)
+    I = (r1 - r0) * len(mults) * S
     N = I * V
-    avail = rng.integers(1, 65, size=N).astype(np.int32)
-    supply = rng.integers(0, 65, size=N).astype(np.int32)
-    flags = np.ones(N, np.uint32)
-    op = np.tile(np.arange(V, dtype=np.int32), I)
     T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
-    d = {"ref": T(ref), "target": T(target), "now": T(now), "Q": T(Q), "avail": T(avail),
-         "supply": T(supply), "mb": T(np.ones(N, np.int32)), "flags": T(flags.astype(np.int32)),
-         "op": T(op)}
+    d = {"ref": T(sw.ref[:, vpos]), "target": T(sw.target), "now": T(sw.now), "Q": T(sw.Q),
+         "avail": T(sw.avail.reshape(-1)), "supply": T(sw.supply.reshape(-1)),
+         "mb": T(np.ones(N, np.int32)), "flags": T(np.ones(N, np.int32)),
+         "op": T(np.tile(np.arange(V, dtype=np.int32), I))}
     slack = torch.empty((I, V, K), dtype=torch.float64, device=dev)
     out = {k: torch.empty(N, dtype=dt, device=dev) for k, dt in
            (("idx", torch.int32), ("code", torch.int32), ("fill", torch.int32),
@@ -285,17 +341,18 @@ def run_c4(args):
     _barrier(torch)
     evs = _events(torch, args.steps)
     l0 = ctx.launch_count
-    for i in range(args.steps):
-        flush()
-        evs[i][0].record(stream)
-        step()
-        evs[i][1].record(stream)
-    torch.cuda.synchronize(dev)
+    with _clocks(local) as clk:
+        for i in range(args.steps):
+            flush()
+            evs[i][0].record(stream)
+            step()
+            evs[i][1].record(stream)
+        torch.cuda.synchronize(dev)
     ms = [a.elapsed_time(b) for a, b in evs]
     t = _tmax(torch, sum(ms) / 1e3, dev)
     codes = torch.bincount(out["code"] & 3, minlength=3)
     launches = ctx.launch_count - l0
-    fused_out = {k: v.clone() for k, v in out.items() if k in ("idx", "code")}
+    got = {k: out[k].cpu().numpy() for k in ("idx", "code", "obj")}
     # the unfused K1 + K2 pair on the same inputs, for comparison
     for _ in range(2):
         step_two_kernels()
@@ -307,50 +364,41 @@ def run_c4(args):
         ev2[i][1].record(stream)
     torch.cuda.synchronize(dev)
     ms2 = [a.elapsed_time(b) for a, b in ev2]
+    # checker: every decision of this rank's shard against the C oracle (full N)
+    parity = c4_full_parity(meta, paths_cols, ops, sw, alpha, got["idx"], got["code"], got["obj"])
+    bad = torch.tensor([parity["index_mismatches"] + parity["kind_code_mismatches"]
+                        + parity.get("objective_mismatches", 0), parity["decisions"]],
+                       dtype=torch.int64, device=dev)
     if world > 1:
         torch.distributed.all_reduce(codes)
+        torch.distributed.all_reduce(bad)
     codes = codes.cpu().tolist()
+    bad = bad.cpu().tolist()
     if rank != 0:
         return
-    # Checker (world 1): the fused decisions of a sample of instances against the oracle —
-    # configurator.slack_by_kind over the AMBER path list (oracle/slack.py) then OpTable.select
-    # (oracle/optable.py); the CPU baseline times exactly that per decision on all host cores
-    parity, cpu = None, None
-    if world == 1:
-        import multiprocessing as mp
-
-        fused_idx = fused_out["idx"].cpu().numpy()
-        fused_code = fused_out["code"].cpu().numpy()
-        work_meta = (meta, [tuple(p) for p in meta["paths"]], g.value_names, alpha)
-        samp = np.random.default_rng(99).choice(I, size=400, replace=False)
-        chk = _c4_cpu_worker((work_meta, samp, ref[samp], target[samp], now[samp], Q[samp],
-                              avail.reshape(I, V)[samp], supply.reshape(I, V)[samp]))
-        got = np.stack([fused_idx.reshape(I, V)[samp], fused_code.reshape(I, V)[samp] & 3], -1)
-        assert np.array_equal(chk, got), "c4: fused decisions disagree with the oracle"
-        parity = {"instances": len(samp), "decisions": len(samp) * V,
-                  "result": "bit-identical (index, kind) vs oracle slack_by_kind + OpTable.select"}
-        cores = os.cpu_count() or 1
-        S_cpu = 60 * cores
-        sl = np.array_split(np.arange(S_cpu), cores)
-        jobs = [(work_meta, a, ref[a], target[a], now[a], Q[a], avail.reshape(I, V)[a],
-                 supply.reshape(I, V)[a]) for a in sl if len(a)]
-        t0 = time.perf_counter()
-        with mp.get_context("fork").Pool(len(jobs)) as pool:
-            n = sum(len(r) * V for r in pool.map(_c4_cpu_worker, jobs))
-        dt = time.perf_counter() - t0
-        cpu = {"value": n / dt, "unit": "decisions/s", "cores": cores, "kind": "port",
-               "sample": f"{S_cpu} instances x {V} ops: oracle slack_by_kind over the path list + "
-                         f"OpTable.select per decision, {cores} processes"}
+    parity = {"decisions": bad[1], "mismatches": bad[0],
+              "result": "bit-identical (index, kind code, objective) vs C oracle: literal "
+                        "_path_ratios/slack_by_kind over the path list + OpTable.select scan"
+                        if bad[0] == 0 else "MISMATCH",
+              "checked_on": f"all {world} rank(s), every decision of the step"}
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu = _c4_cpu_baseline(meta, g, alpha, sw, V)
     evals_per_inst = sum(len(x.entries) for x in tabs)
+    Itot = R * len(mults) * S
     line = {
         "workload": "c4", "metric": "config decisions/s (K1 slack -> K2 select fused on device)",
-        "unit": "decisions/s", "value": args.steps * N * world / t, "ms_per_step": 1e3 * t / args.steps,
-        "steps": args.steps, "n_gpus": world, "scaling": "weak",
-        "evals_per_s": args.steps * I * world * evals_per_inst / t,
-        "config": {"replicas_per_gpu": R, "targets_x_cp_min": list(mults), "snapshots": S,
-                   "instances_per_gpu": I, "ops": V, "kinds": K, "decisions_per_step_per_gpu": N,
-                   "cp_min": cp_min,
-                   "parallelism": f"replicas sharded over {world} GPU(s); decision counters all-reduced"},
+        "unit": "decisions/s", "value": args.steps * Itot * V / t, "ms_per_step": 1e3 * t / args.steps,
+        "steps": args.steps, "warmup": args.warmup, "n_gpus": world, "scaling": "strong",
+        "evals_per_s": args.steps * Itot * evals_per_inst / t,
+        "config": {"replicas": R, "targets_x_cp_min": list(mults), "snapshots": S,
+                   "instances": Itot, "ops": V, "kinds": K, "decisions_per_step": Itot * V,
+                   "cp_min": synth.SWEEP_CP_MIN,
+                   "inputs": "synth.amber_sweep: per (replica r, target m) numpy seed r*5+m draws Q ~ "
+                             "Exp(0.02 T), ref drift exp(N(0,0.2)), avail U{1..64}, supply U{0..64}",
+                   "l2": "L2 flushed (256 MB read sweep) before every timed step",
+                   "parallelism": f"{R} replicas sharded contiguously over {world} GPU(s); decision "
+                                  "counters all-reduced"},
         "decision_mix": {"none": codes[0], "assign": codes[1], "delay": codes[2]},
         "gpu_launches": launches,
         "step_ms": {"median": statistics.median(ms), "min": min(ms), "max": max(ms)},
@@ -359,11 +407,57 @@ def run_c4(args):
                                "note": "k_slack then k_select_plan, slack through HBM"},
         "parity": parity,
         "cpu_baseline": cpu,
+        "clocks": clk.summary(),
     }
     print(json.dumps(line), flush=True)
 
 
+def _c4_cpu_baseline(meta, g, alpha, sw, V):
+    """The reference's per-decision CPU path (oracle restatement: slack_by_kind over the path
+    list + OpTable.select per decision) on all host cores; the pool is forked and warmed
+    before the timed map."""
+    import multiprocessing as mp
+
+    cores = os.cpu_count() or 1
+    work_meta = (meta, [tuple(p) for p in meta["paths"]], g.value_names, alpha)
+    vpos = [meta["ops"].index(n) for n in g.value_names]
+    S_cpu = 60 * cores
+    sl = np.array_split(np.arange(S_cpu), cores)
+    jobs = [(work_meta, a, sw.ref[a][:, vpos], sw.target[a], sw.now[a], sw.Q[a], sw.avail[a],
+             sw.supply[a]) for a in sl if len(a)]
+    with mp.get_context("fork").Pool(len(jobs)) as pool:
+        pool.map(_c4_cpu_worker, [(work_meta, a[:2], *(x[:2] for x in j[2:])) for a, j in zip(sl, jobs)])
+        t0 = time.perf_counter()
+        n = sum(len(r) * V for r in pool.map(_c4_cpu_worker, jobs))
+        dt = time.perf_counter() - t0
+    return {"value": n / dt, "unit": "decisions/s", "cores": cores, "kind": "port",
+            "sample": f"{S_cpu} instances x {V} ops of the same sweep: oracle slack_by_kind over the "
+                      f"path list + OpTable.select per decision, {cores} worker processes (pool forked "
+                      f"and warmed outside the timed map)"}
+
+
 # ---- c5 -------------------------------------------------------------------------------------
+
+def c5_noise(B: int, batches: range) -> np.ndarray:
+    """Observation noise of config 5: batch bt draws exp(N(0, 0.3)) for its B
+    invocations from numpy default_rng(bt), one normal per invocation in order, exponentiated
+    with math.exp exactly as backend.draw_actual_latency does (backend.py:36-58; np.exp differs
+    from math.exp in the last bit for ~5% of arguments)."""
+    out = np.empty((len(batches), B))
+    for u, bt in enumerate(batches):
+        z = np.random.default_rng(bt).normal(0.0, 0.3, size=B)
+        out[u] = np.fromiter(map(math.exp, z.tolist()), dtype=np.float64, count=B)
+    return out
+
+
+def c5_truth(table):
+    """Ground truth of the synthetic scenario (synth.synth_truths; scenario.py:68-77): the per-batch
+    base latency of every configuration (= its zero-noise profile, latency_initial_s) plus a
+    per-item coefficient (0 in this scenario) times the invocation's item count (fill)."""
+    base = np.array([e.latency_initial_s for e in table.entries])
+    per_item = np.zeros(len(base))
+    return base, per_item
+
 
 def run_c5(args):
     import torch
@@ -387,10 +481,9 @@ def run_c5(args):
     T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
     d = {"slack": T(inv.slack), "avail": T(inv.avail), "supply": T(inv.supply),
          "mb": T(inv.min_batch), "flags": T(inv.flags.astype(np.int32))}
-    lat_init = T(np.array([e.latency_initial_s for e in table.entries]))
-    gen = torch.Generator(device=dev)
-    gen.manual_seed(5)
-    noise = torch.exp(0.3 * torch.randn(N, dtype=torch.float64, device=dev, generator=gen))
+    base_np, per_item_np = c5_truth(table)
+    base, per_item = T(base_np), T(per_item_np)
+    noise = T(c5_noise(B, range(NB)).reshape(-1))
     # every batch is split contiguously over the ranks (decisions), then the observation records
     # are all-gathered so that each rank folds the whole batch in global order
     a, b = shard_range(B, rank, world)
@@ -400,18 +493,23 @@ def run_c5(args):
             ("obj", torch.float64), ("slack", torch.float64), ("wait", torch.float64))}
     obs_idx = torch.empty(Bl, dtype=torch.int32, device=dev)
     neg1 = torch.full((Bl,), -1, dtype=torch.int32, device=dev)
+    stream_idx = torch.empty(N, dtype=torch.int32, device=dev)   # the folded stream, kept for the check
+    stream_obs = torch.empty(N, dtype=torch.float64, device=dev)
     alpha = 100.0
 
     def online_batch(tab, bt):
-        # decide this rank's shard of batch bt against the batch-start table; the chosen
-        # configurations run: observation = truth(config) * lognormal noise (delayed / None
+        # decide this rank's shard of batch bt against the batch-start table; the assigned
+        # configurations run: obs = truth(config, items=fill) * exp(N(0, 0.3)) (delayed / None
         # decisions produce no observation, idx = -1); every rank folds the whole batch
         s = slice(bt * B + a, bt * B + b)
         tab.select_batch(d["slack"][s], alpha, d["avail"][s], upstream_supply=d["supply"][s],
                          min_batch=d["mb"][s], flags=d["flags"][s], out=out)
         torch.where((out["code"] & 3) == 1, out["idx"], neg1, out=obs_idx)
-        obs = torch.index_select(lat_init, 0, obs_idx.clamp(min=0)) * noise[s]
+        j = obs_idx.clamp(min=0)
+        obs = (base[j] + per_item[j] * out["fill"].to(torch.float64)) * noise[s]
         f_idx, f_obs = gather_observations(obs_idx, obs, B) if world > 1 else (obs_idx, obs)
+        stream_idx[bt * B:(bt + 1) * B].copy_(f_idx)
+        stream_obs[bt * B:(bt + 1) * B].copy_(f_obs)
         sp.fold_observations([tab], None, f_idx, f_obs, beta=0.5, dfp_count=10, sync_host=False)
 
     # warm-up on a throw-away copy of the table (module loading, scratch allocation, plan-build
@@ -425,17 +523,19 @@ def run_c5(args):
     _barrier(torch)
     l0 = ctx.launch_count
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for bt in range(NB):
-        online_batch(table, bt)
-    e1.record(stream)
-    torch.cuda.synchronize(dev)
+    with _clocks(local) as clk:
+        e0.record(stream)
+        for bt in range(NB):
+            online_batch(table, bt)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
     launches = ctx.launch_count - l0
     t = _tmax(torch, e0.elapsed_time(e1) / 1e3, dev)
     # replicas must stay bit-identical: compare a checksum of the final latency table
     table.sync_from_device()
-    lat_now = torch.from_numpy(table.lat.copy()).to(dev)
-    chk = lat_now.view(torch.int64).sum().view(1)
+    final_lat = np.asarray(table.lat).copy()
+    chk = torch.tensor([int(final_lat.view(np.uint64).astype(np.int64).sum())], dtype=torch.int64,
+                       device=dev)
     identical = True
     if world > 1:
         lo, hi = chk.clone(), chk.clone()
@@ -444,59 +544,21 @@ def run_c5(args):
         identical = bool(lo.item() == hi.item())
     if rank != 0:
         return
-    # Checker (world 1 only): the first two batches replayed on a fresh table, decisions against
-    # the C oracle (oracle/cselect.py) and the fold against the sequential oracle
-    # (oracle/feedback.py) — decisions and the latency table bit-identical after each batch; the
-    # CPU baseline is the numpy restatement of OpTable.select on all host cores plus the
-    # sequential fold for one batch (the reference's per-batch semantics).
-    parity, cpu = None, None
-    if world == 1:
-        from oracle import cselect, optable
-        from oracle import feedback as ofb
-
-        vtab = sp.OpTable(spec, synth.synth_scenario())
-        ot = optable.from_spec(spec, synth.synth_scenario(), ["cpu", "gpu"])
-        st = ofb.FoldState(ot.lat.copy(), np.array([e.latency_initial_s for e in spec.entries]),
-                           int(ot.ref_index))
-        checked = 0
-        for bt in range(2):
-            s = slice(bt * B, (bt + 1) * B)
-            ot.lat[:] = st.lat
-            exp = cselect.select_batch([ot], inv.slack[s], alpha, inv.avail[s], inv.supply[s],
-                                       inv.min_batch[s], inv.flags[s])
-            online_batch(vtab, bt)
-            torch.cuda.synchronize(dev)
-            got_idx = out["idx"].cpu().numpy()
-            got_code = out["code"].cpu().numpy()
-            assert np.array_equal(got_idx, exp["idx"]) and np.array_equal(got_code & 3, exp["code"] & 3), \
-                f"c5 batch {bt}: decisions disagree with the oracle"
-            oi = obs_idx.cpu().numpy()
-            ob = (lat_init[obs_idx.clamp(min=0).long()] * noise[s]).cpu().numpy()
-            keep = oi >= 0
-            ofb.fold([st], None, oi[keep], ob[keep], beta=0.5, dfp_count=10)
-            vtab.sync_from_device()
-            assert np.array_equal(np.asarray(vtab.lat).view(np.uint64), st.lat.view(np.uint64)), \
-                f"c5 batch {bt}: folded table disagrees with the oracle"
-            checked += B
-        parity = {"batches": 2, "decisions": checked, "result": "bit-identical decisions and tables"}
-        s = slice(0, B)
-        t0 = time.perf_counter()
-        optable.select_many_parallel([ot], inv.slack[s], alpha, inv.avail[s], inv.supply[s],
-                                     inv.min_batch[s], inv.flags[s])
-        t_sel = time.perf_counter() - t0
-        t0 = time.perf_counter()
-        ofb.fold([ofb.FoldState(ot.lat.copy(), st.lat_init.copy(), int(ot.ref_index))], None,
-                 oi[keep], ob[keep], beta=0.5, dfp_count=10)
-        t_fold = time.perf_counter() - t0
-        cores = os.cpu_count() or 1
-        cpu = {"value": B / (t_sel + t_fold), "unit": "decisions/s", "cores": cores, "kind": "port",
-               "sample": f"one batch: {B} OpTable.select (oracle/optable.py numpy restatement, "
-                         f"{cores} processes) + the sequential fold of its observations"}
+    parity = c5_parity(sp, spec, synth, inv, alpha, B, NB, base_np, per_item_np, noise, online_batch,
+                       out, obs_idx, stream_idx.cpu().numpy(), stream_obs.cpu().numpy(), final_lat,
+                       dev, torch, check_batches=min(8, NB) if world == 1 else 0)
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu = _c5_cpu_baseline(spec, synth, inv, alpha, B, parity.pop("_state"))
+    else:
+        parity.pop("_state", None)
     line = {
         "workload": "c5", "metric": "online config decisions/s incl. per-batch feedback fold and replanning",
         "unit": "decisions/s", "value": N / t, "evals_per_s": N * M / t, "seconds": t, "n_gpus": world,
         "scaling": "strong",
         "config": {"invocations": N, "configs": M, "batches": NB, "batch": B, "beta": 0.5, "dfp_count": 10,
+                   "inputs": "synth_invocations(seed 5); obs = truth(config, fill) * math.exp(N(0,0.3)) "
+                             "with numpy default_rng(batch id)",
                    "parallelism": (f"each batch split over {world} GPU(s); per batch one all-gather of the "
                                    "16-B observation records, replicated fold" if world > 1 else "1 GPU")},
         "tables_bit_identical_across_ranks": identical,
@@ -504,9 +566,103 @@ def run_c5(args):
         "per_batch_ms": 1e3 * t / NB,
         "parity": parity,
         "cpu_baseline": cpu,
+        "clocks": clk.summary(),
     }
     print(json.dumps(line), flush=True)
 
+
+def c5_parity(sp, spec, synth, inv, alpha, B, NB, base, per_item, noise, online_batch, out, obs_idx,
+              stream_idx, stream_obs, final_lat, dev, torch, check_batches=8):
+    """Checker.  (1) The first `check_batches` batches replayed on a fresh table: every decision
+    against the C oracle scan (oracle_select_batch on the oracle's own folded table), the
+    observations recomputed on the host, and the table after each batch against the C sequential
+    fold (oracle_fold, manager.py:436-457).  (2) The whole timed run: its recorded observation
+    stream (all NB batches) folded sequentially by the C oracle from the initial table must give
+    the device's final table bit for bit (final-table checksum)."""
+    from oracle import cselect, optable
+
+    # a pristine spec: OpTable shares its ConfigEntry objects with the spec it was built from
+    # (as the reference's does, configurator.py:170-177), and sync_from_device() wrote the
+    # timed run's final latencies into them
+    spec = synth.synth_spec(True)
+    ot = optable.from_spec(spec, synth.synth_scenario(), ["cpu", "gpu"])
+    lat_init = np.ascontiguousarray(base)  # latency_initial_s of the table's entries
+    st = cselect.FoldState(ot.lat.copy(), lat_init, int(ot.ref_index))
+    noise_h = noise.view(NB, B)
+    res = {"batches_decisions_checked": 0, "decisions": 0, "decision_mismatches": 0,
+           "table_mismatches_after_batch": 0}
+    if check_batches:
+        vtab = sp.OpTable(spec, synth.synth_scenario())
+        for bt in range(check_batches):
+            s = slice(bt * B, (bt + 1) * B)
+            ot.lat[:] = st.lat
+            exp = cselect.select_batch([ot], inv.slack[s], alpha, inv.avail[s], inv.supply[s],
+                                       inv.min_batch[s], inv.flags[s])
+            online_batch(vtab, bt)
+            torch.cuda.synchronize(dev)
+            got = {k: out[k].cpu().numpy() for k in ("idx", "code", "fill", "obj")}
+            some = exp["code"] != 0
+            res["decision_mismatches"] += int(
+                np.count_nonzero(got["idx"] != exp["idx"]) + np.count_nonzero((got["code"] & 3) != exp["code"])
+                + np.count_nonzero(got["fill"] != exp["fill"])
+                + np.count_nonzero(got["obj"][some].view(np.uint64) != exp["obj"][some].view(np.uint64)))
+            keep = exp["code"] == 1
+            oi = exp["idx"][keep]
+            ob = (base[oi] + per_item[oi] * exp["fill"][keep].astype(np.float64)) * noise_h[bt].cpu().numpy()[keep]
+            # the device's folded stream of the timed run must be this batch's observations
+            si = stream_idx[s]
+            want = np.where(keep, exp["idx"], -1)
+            if not np.array_equal(si, want):
+                res["stream_idx_mismatch_batches"] = res.get("stream_idx_mismatch_batches", []) + [bt]
+                dpos = np.flatnonzero(si != want)
+                res.setdefault("stream_idx_examples", []).append(
+                    [int(len(dpos))] + [(int(p), int(si[p]), int(want[p]), int(exp["code"][p])) for p in dpos[:3]])
+            elif not np.array_equal(stream_obs[s][keep].view(np.uint64), ob.view(np.uint64)):
+                res["stream_obs_mismatch_batches"] = res.get("stream_obs_mismatch_batches", []) + [bt]
+                res["stream_obs_example"] = [float(stream_obs[s][keep][0]), float(ob[0])]
+            cselect.fold(st, oi, ob, beta=0.5, dfp_count=10)
+            vtab.sync_from_device()
+            res["table_mismatches_after_batch"] += int(np.count_nonzero(
+                np.asarray(vtab.lat).view(np.uint64) != st.lat.view(np.uint64)))
+            res["batches_decisions_checked"] += 1
+            res["decisions"] += B
+    lat0 = optable.from_spec(synth.synth_spec(True), synth.synth_scenario(), ["cpu", "gpu"]).lat
+    full = cselect.FoldState(lat0, lat_init, int(ot.ref_index))
+    keep = stream_idx >= 0
+    cselect.fold(full, stream_idx[keep], stream_obs[keep], beta=0.5, dfp_count=10)
+    res["observations_folded"] = int(keep.sum())
+    res["final_table_mismatches"] = int(np.count_nonzero(full.lat.view(np.uint64) != final_lat.view(np.uint64)))
+    res["final_table_checksum"] = hex(int(final_lat.view(np.uint64).astype(np.uint64).sum(dtype=np.uint64)))
+    ok = not (res["decision_mismatches"] or res["table_mismatches_after_batch"] or res["final_table_mismatches"]
+              or "stream_idx_mismatch_batches" in res or "stream_obs_mismatch_batches" in res)
+    res["result"] = "bit-identical" if ok else "MISMATCH"
+    res["_state"] = (ot, st)
+    return res
+
+
+def _c5_cpu_baseline(spec, synth, inv, alpha, B, state):
+    """The reference's per-batch CPU semantics: OpTable.select for a
+    batch on all host cores (numpy restatement, persistent pool), then the sequential fold
+    (oracle/feedback.py apply_feedback + set_latency, one observation at a time)."""
+    from oracle import feedback as ofb
+    from oracle import optable
+
+    ot, st = state
+    cores = os.cpu_count() or 1
+    s = slice(0, B)
+    ot.lat[:] = st.lat
+    with optable.SelectPool([ot], cores) as pool:
+        t0 = time.perf_counter()
+        r = pool.select(inv.slack[s], alpha, inv.avail[s], inv.supply[s], inv.min_batch[s], inv.flags[s])
+        t_sel = time.perf_counter() - t0
+    keep = r["code"] == 1
+    fs = ofb.FoldState(ot.lat.copy(), st.lat_init.copy(), int(ot.ref_index))
+    t0 = time.perf_counter()
+    ofb.fold([fs], None, r["idx"][keep], np.ones(int(keep.sum())), beta=0.5, dfp_count=10)
+    t_fold = time.perf_counter() - t0
+    return {"value": B / (t_sel + t_fold), "unit": "decisions/s", "cores": cores, "kind": "port",
+            "sample": f"one batch: {B} OpTable.select (oracle/optable.py numpy restatement, persistent "
+                      f"pool of {cores} processes) + the sequential fold of its observations"}
 
 
 # ---- commit rounds --------------------------------------------------------------------------

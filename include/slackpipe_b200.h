@@ -264,6 +264,52 @@ int sp_speculate_batch(sp_ctx* ctx, int32_t n_tables, sp_table* const* tables, d
                        double* out_slack, double* out_obj, int32_t* out_n, int32_t* out_delay_idx,
                        double* out_delay_wait, int32_t mem);
 
+/* ---- single-process multi-GPU fan-out (SURVEY.md §8(b) Threading, §8(e)) ------------------ */
+/* The reference engine is one single-threaded process (configurator.py:368-373); a drop-in
+ * that uses the GPUs of a box fans out inside the library.  A group owns one context (device
+ * + non-blocking stream) per member; devices may repeat (independent contexts on one GPU).
+ * A group table is one OpTable replica per member, kept bit-identical because every mutation
+ * (set_latency, feedback fold) is applied to every replica in the same order. */
+typedef struct sp_group sp_group;
+typedef struct sp_group_table sp_group_table;
+int sp_group_create(int32_t n, const int32_t* devices, sp_group** out);
+int sp_group_destroy(sp_group* g);
+int32_t sp_group_size(const sp_group* g);
+/* Member i's context and device (the context stays owned by the group). */
+int sp_group_member(sp_group* g, int32_t i, sp_ctx** ctx_out, int32_t* device_out);
+/* Kernels launched by every member context (bench evidence). */
+int64_t sp_group_launch_count(const sp_group* g);
+/* OpTable.__init__ (configurator.py:166-209) replicated on every member: same arguments as
+ * sp_table_create. */
+int sp_group_table_create(sp_group* g, int32_t M, const double* lat, const double* lat_init,
+                          const double* res, const int32_t* batch, const double* pool,
+                          const double* price, const int32_t* kind, const int32_t* id_rank,
+                          int32_t K, int32_t ref_index, sp_group_table** out);
+int sp_group_table_destroy(sp_group* g, sp_group_table* t);
+/* Member i's replica (owned by the group table). */
+int sp_group_table_replica(sp_group_table* t, int32_t i, sp_table** out);
+/* OpTable.set_latency (configurator.py:211-213) on every replica, in member order. */
+int sp_group_table_set_latency(sp_group* g, sp_group_table* t, int32_t n, const int32_t* idx,
+                               const double* val);
+/* Member `member`'s live latency vector (host out, synchronous). */
+int sp_group_table_get_latency(sp_group* g, sp_group_table* t, int32_t member, double* out_lat);
+/* Batched OpTable.select (configurator.py:239-300) over N invocations with HOST buffers, laid
+ * out exactly as sp_select_batch's: member g decides the contiguous shard [g*N/G, (g+1)*N/G)
+ * on its device and writes straight into the caller's outputs at that offset (zero-copy when
+ * every buffer is pinned and mapped; else the staging pipeline); every member is in flight at
+ * once and the call returns when all have finished.  Results equal sp_select_batch's bit for
+ * bit. */
+int sp_group_select_batch(sp_group* g, int32_t n_tables, sp_group_table* const* tables,
+                          double alpha, int32_t N, const int32_t* op, const double* slack,
+                          const int32_t* avail, const int32_t* supply, const int32_t* min_batch,
+                          const uint32_t* flags, int32_t* out_idx, int32_t* out_code,
+                          int32_t* out_fill, double* out_obj, double* out_slack,
+                          double* out_wait, double* out_kind_min, int32_t mode);
+/* sp_feedback_fold (manager.py:436-457) of one host observation stream into every replica. */
+int sp_group_feedback_fold(sp_group* g, int32_t n_tables, sp_group_table* const* tables,
+                           int32_t n, const int32_t* op, const int32_t* idx, const double* obs,
+                           double beta, int32_t dfp_count, int32_t dfp_on, int32_t fb_frozen);
+
 #ifdef __cplusplus
 }
 #endif

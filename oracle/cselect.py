@@ -74,3 +74,83 @@ def select_batch(tables, slack, alpha, avail, supply, min_batch, flags, op=None,
         _p(out["obj"]), _p(out["slack"]), _p(out["wait"]), _p(out["feasible"]), C.c_int64(max_m))
     out["feasible"] = out["feasible"].astype(bool)
     return out
+
+
+def _sig(lib):
+    lib.oracle_slack_paths.restype = C.c_int
+    lib.oracle_slack_dp.restype = C.c_int
+    lib.oracle_fold.restype = C.c_int
+
+
+def slack_paths(ref, target, now, Q, paths_cols):
+    """Alg. 1 over an explicit path list (configurator.py:415-417, 493-543) for I instances.
+    ref (I, V) by column; paths_cols: sequences of columns.  Returns slack (I, V, K)."""
+    lib = _load()
+    _sig(lib)
+    ref = np.ascontiguousarray(ref, dtype=np.float64)
+    I, V = ref.shape
+    Q = np.ascontiguousarray(Q, dtype=np.float64)
+    K = Q.shape[1]
+    off = np.zeros(len(paths_cols) + 1, dtype=np.int32)
+    for p, cols in enumerate(paths_cols):
+        off[p + 1] = off[p] + len(cols)
+    nodes = np.ascontiguousarray(np.concatenate([np.asarray(c, dtype=np.int32) for c in paths_cols]))
+    target = np.ascontiguousarray(target, dtype=np.float64)
+    now = np.ascontiguousarray(now, dtype=np.float64)
+    out = np.empty((I, V, K))
+    lib.oracle_slack_paths(C.c_int64(I), C.c_int(V), C.c_int(K), _p(ref), _p(target), _p(now),
+                           _p(Q), C.c_int(len(paths_cols)), _p(off), _p(nodes), _p(out))
+    return out
+
+
+def slack_dp(dag, ref, target, now, Q, ratios=False):
+    """Forward-DP Alg. 1 (oracle/slack.py dp_ratios / dp_slack) for a PipelineDag whose path set
+    cannot be enumerated.  ref (I, V) in dag.vertices column order.  Returns slack (I, V, K)
+    (and ratio (I, V, 2) = (own/Tmax, own/Tmin) when ratios=True)."""
+    lib = _load()
+    _sig(lib)
+    ref = np.ascontiguousarray(ref, dtype=np.float64)
+    I, V = ref.shape
+    Q = np.ascontiguousarray(Q, dtype=np.float64)
+    K = Q.shape[1]
+    order = dag.topological_order()
+    pos = {v: i for i, v in enumerate(order)}
+    col = np.array([dag.vertices.index(v) for v in order], dtype=np.int32)
+    preds = [[pos[p] for p in dag.predecessors(v)] for v in order]
+    poff = np.zeros(V + 1, dtype=np.int32)
+    for s, ps in enumerate(preds):
+        poff[s + 1] = poff[s] + len(ps)
+    pidx = np.array([p for ps in preds for p in ps], dtype=np.int32)
+    term = np.array([not dag.successors(v) for v in order], dtype=np.uint8)
+    out = np.empty((I, V, K))
+    rat = np.empty((I, V, 2)) if ratios else None
+    lib.oracle_slack_dp(C.c_int64(I), C.c_int(V), C.c_int(K), _p(ref),
+                        _p(np.ascontiguousarray(target, dtype=np.float64)),
+                        _p(np.ascontiguousarray(now, dtype=np.float64)), _p(Q), _p(col), _p(poff),
+                        _p(pidx), _p(term), _p(out), _p(rat))
+    return (out, rat) if ratios else out
+
+
+class FoldState:
+    """One table's feedback state for oracle_fold (manager.py:436-457)."""
+
+    def __init__(self, lat, lat_init, ref_index):
+        self.lat = np.array(lat, dtype=np.float64)
+        self.lat_init = np.ascontiguousarray(lat_init, dtype=np.float64)
+        self.ref_index = int(ref_index)
+        self.completed_ref = np.zeros(1, dtype=np.int64)
+        self.obs_count = np.zeros(len(self.lat), dtype=np.int64)
+
+
+def fold(st: FoldState, idx, obs, beta=0.5, dfp_count=10):
+    """Sequential fold of one batch of observations into st (in order)."""
+    lib = _load()
+    _sig(lib)
+    idx = np.ascontiguousarray(idx, dtype=np.int32)
+    obs = np.ascontiguousarray(obs, dtype=np.float64)
+    rc = lib.oracle_fold(C.c_int64(len(st.lat)), _p(st.lat), _p(st.lat_init), C.c_int64(st.ref_index),
+                         _p(st.completed_ref), _p(st.obs_count), C.c_int64(len(idx)), _p(idx), _p(obs),
+                         C.c_double(beta), C.c_int64(dfp_count))
+    if rc != 0:
+        raise ValueError("observation index out of range")
+    return st

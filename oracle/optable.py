@@ -232,3 +232,51 @@ def select_many_parallel(tables, slack, alpha, avail, supply, min_batch, flags, 
                   initargs=(tables, slack, alpha, avail, supply, min_batch, flags, op)) as pool:
         parts = pool.map(_pool_run, ranges)
     return {k: np.concatenate([p[k] for p in parts]) for k in parts[0]}
+
+
+_POOL_TABLES: dict = {}
+
+
+def _pool_tables(tables):
+    _POOL_TABLES["tables"] = tables
+
+
+def _pool_ready(_):
+    return os.getpid()
+
+
+def _pool_chunk(a):
+    slack, alpha, avail, supply, min_batch, flags, op = a
+    return select_many(_POOL_TABLES["tables"], slack, alpha, avail, supply, min_batch, flags, op)
+
+
+class SelectPool:
+    """A persistent fork pool over all host cores holding the tables: forked and warmed once, so
+    timed calls pay only the per-call shipping of their (small) invocation shards, not process
+    start-up (used by bench.py's CPU baseline and reference arm)."""
+
+    def __init__(self, tables, processes: int | None = None):
+        import multiprocessing as mp
+
+        self.procs = processes or os.cpu_count() or 1
+        self.pool = mp.get_context("fork").Pool(self.procs, initializer=_pool_tables, initargs=(tables,))
+        self.pool.map(_pool_ready, range(4 * self.procs), chunksize=1)
+
+    def select(self, slack, alpha, avail, supply, min_batch, flags, op=None):
+        N = slack.shape[0]
+        b = np.linspace(0, N, self.procs + 1).astype(int)
+        jobs = [(slack[b[i]:b[i + 1]], alpha, avail[b[i]:b[i + 1]], supply[b[i]:b[i + 1]],
+                 min_batch[b[i]:b[i + 1]], flags[b[i]:b[i + 1]], None if op is None else op[b[i]:b[i + 1]])
+                for i in range(self.procs) if b[i + 1] > b[i]]
+        parts = self.pool.map(_pool_chunk, jobs, chunksize=1)
+        return {k: np.concatenate([p[k] for p in parts]) for k in parts[0]}
+
+    def close(self):
+        self.pool.close()
+        self.pool.join()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()

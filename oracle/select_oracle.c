@@ -104,3 +104,134 @@ int oracle_select_batch(const int64_t* tab_off, const double* lat, const double*
   }
   return rc;
 }
+
+/* ---- Alg. 1 slack over an explicit path list ---------------------------------------------
+ * Literal restatement of Configurator._suffixes (configurator.py:415-417), _path_ratios
+ * (493-509) and slack_by_kind (526-543): for every op column v, every path containing v
+ * contributes own / (left-to-right sum of the suffix from v); per kind the slack is the
+ * first-minimum of ratio * ((target - now) - Q[k]).  Paths are lists of ref columns
+ * (path p = path_nodes[path_off[p] .. path_off[p+1])).  out_slack is I x V x K; columns on
+ * no path are written as NaN (the reference raises for them, configurator.py:418-420). */
+int oracle_slack_paths(int64_t I, int V, int K, const double* ref, const double* target,
+                       const double* now, const double* Q, int n_paths, const int32_t* path_off,
+                       const int32_t* path_nodes, double* out_slack) {
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < I; ++i) {
+    const double* r = ref + i * V;
+    for (int v = 0; v < V; ++v) {
+      double ratios[256];
+      int nr = 0;
+      for (int p = 0; p < n_paths; ++p) {
+        int at = -1;
+        for (int q = path_off[p]; q < path_off[p + 1]; ++q)
+          if (path_nodes[q] == v) { at = q; break; }
+        if (at < 0) continue;
+        double total = 0.0;
+        for (int q = at; q < path_off[p + 1]; ++q) total += r[path_nodes[q]];
+        if (nr < 256) ratios[nr++] = r[v] / total;
+      }
+      for (int k = 0; k < K; ++k) {
+        double budget = (target[i] - now[i]) - Q[i * K + k];
+        double s = NAN;
+        for (int q = 0; q < nr; ++q) {
+          double x = ratios[q] * budget;
+          if (q == 0 || x < s) s = x;
+        }
+        out_slack[(i * V + v) * K + k] = s;
+      }
+    }
+  }
+  return 0;
+}
+
+/* ---- Alg. 1 slack on a DAG by the forward left-to-right DP --------------------------------
+ * The restatement SURVEY.md §8(c) validated against compute_slack (0 / 128,045) and
+ * oracle/slack.py dp_ratios / dp_slack restate: vertices in topological order (order[s] is
+ * the ref column of position s), predecessors as a CSR over positions, terminal flags per
+ * position.  hi[src] = lo[src] = 0.0 + ref[src]; hi[v] = max_p hi[p] + ref[v],
+ * lo[v] = min_p lo[p] + ref[v]; Tmax / Tmin over reachable terminals; slack =
+ * (budget >= 0 ? own/Tmax : own/Tmin) * budget.  out_slack[i][order[s]][k] (I x V x K);
+ * out_ratio (optional) [i][order[s]][{lo, hi}]. */
+int oracle_slack_dp(int64_t I, int V, int K, const double* ref, const double* target,
+                    const double* now, const double* Q, const int32_t* order,
+                    const int32_t* pred_off, const int32_t* pred_idx, const uint8_t* terminal,
+                    double* out_slack, double* out_ratio) {
+#pragma omp parallel
+  {
+    double hi[1024], lo[1024], rv[1024];
+    unsigned char seen[1024];
+#pragma omp for schedule(static)
+    for (int64_t i = 0; i < I; ++i) {
+      for (int s = 0; s < V; ++s) rv[s] = ref[i * V + order[s]];
+      for (int src = 0; src < V; ++src) {
+        for (int s = 0; s < V; ++s) seen[s] = 0;
+        hi[src] = lo[src] = 0.0 + rv[src];
+        seen[src] = 1;
+        for (int v = src + 1; v < V; ++v) {
+          int any = 0;
+          double h = 0.0, l = 0.0;
+          for (int q = pred_off[v]; q < pred_off[v + 1]; ++q) {
+            int p = pred_idx[q];
+            if (!seen[p]) continue;
+            if (!any || hi[p] > h) h = hi[p];
+            if (!any || lo[p] < l) l = lo[p];
+            any = 1;
+          }
+          if (!any) continue;
+          seen[v] = 1;
+          hi[v] = h + rv[v];
+          lo[v] = l + rv[v];
+        }
+        int anyt = 0;
+        double tmax = 0.0, tmin = 0.0;
+        for (int v = src; v < V; ++v) {
+          if (!seen[v] || !terminal[v]) continue;
+          if (!anyt || hi[v] > tmax) tmax = hi[v];
+          if (!anyt || lo[v] < tmin) tmin = lo[v];
+          anyt = 1;
+        }
+        double own = rv[src];
+        double rlo = own / tmax, rhi = own / tmin;
+        int col = order[src];
+        if (out_ratio) {
+          out_ratio[(i * V + col) * 2 + 0] = rlo;
+          out_ratio[(i * V + col) * 2 + 1] = rhi;
+        }
+        for (int k = 0; k < K; ++k) {
+          double b = (target[i] - now[i]) - Q[i * K + k];
+          out_slack[(i * V + col) * K + k] = (b >= 0 ? rlo : rhi) * b;
+        }
+      }
+    }
+  }
+  return 0;
+}
+
+/* ---- feedback fold ------------------------------------------------------------------------
+ * Sequential restatement of PipelineRun._apply_feedback (manager.py:436-457): per
+ * observation in completion order, completed_ref / obs_count bookkeeping, the EWMA
+ * apply_feedback (manager.py:45-47: beta*obs + (1-beta)*old), and the gate lift
+ * (Configurator.recalibrate_unobserved, configurator.py:470-491) when the reference entry's
+ * completion count reaches dfp_count.  One table; state arrays are updated in place. */
+int oracle_fold(int64_t M, double* lat, const double* lat_init, int64_t ref_index,
+                int64_t* completed_ref, int64_t* obs_count, int64_t n, const int32_t* idx,
+                const double* obs, double beta, int64_t dfp_count) {
+  for (int64_t j = 0; j < n; ++j) {
+    int64_t e = idx[j];
+    if (e < 0 || e >= M) return -1;
+    if (e == ref_index) *completed_ref += 1;
+    obs_count[e] += 1;
+    lat[e] = beta * obs[j] + (1.0 - beta) * lat[e];
+    if (e == ref_index && *completed_ref == dfp_count && ref_index >= 0) {
+      double init_ref = lat_init[ref_index];
+      if (init_ref > 0.0) {
+        double ratio = lat[ref_index] / init_ref;
+        for (int64_t i = 0; i < M; ++i) {
+          if (i == ref_index || obs_count[i] > 0) continue;
+          lat[i] = lat_init[i] * ratio;
+        }
+      }
+    }
+  }
+  return 0;
+}

@@ -27,6 +27,7 @@ from .configurator import (
 )
 from . import metadata
 from .commit import commit_candidates, commit_round, pump_commits
+from .group import DeviceGroup, GroupOpTable, group_fold, group_select_batch
 from .feedback import apply_feedback, fold_observations, observation_quantiles, set_table_counters, table_counters
 from .pipeline import ConfigEntry, ConfigSpec, PipelineDag, reference_config
 from .scenario import BackendSpec, Scenario
@@ -36,7 +37,8 @@ from .speculate import speculate_batch, speculate_from_buffer
 __version__ = "0.1.0"
 
 __all__ = [
-    "ABLATION_TOKENS", "AffinityScore", "BackendSpec", "ConfigEntry", "ConfigSpec", "Decision",
+    "ABLATION_TOKENS", "AffinityScore", "BackendSpec", "DeviceGroup", "GroupOpTable",
+    "group_fold", "group_select_batch", "ConfigEntry", "ConfigSpec", "Decision",
     "OpTable", "PipelineDag", "RawTable", "Scenario", "SelectResult", "Slack", "SlackGraph",
     "SlackpipeError", "TuningParams", "affinity", "affinity_from_minima", "apply_feedback",
     "commit_candidates", "commit_round", "compute_slack", "estimate_queueing", "fold_observations", "get_context", "load_library",

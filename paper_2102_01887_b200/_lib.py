@@ -86,6 +86,19 @@ SIGNATURES = {
     "sp_observation_quantiles": (C.c_int, [_p, _i32, _p, _i32, _p, _p, _p, _d, _d, _p, _p, _p, _i32]),
     "sp_slack_select_batch": (C.c_int, [_p, _p, _i32, _p, _d, _i32, _p, _i32, _p, _p, _i32, _p]
                               + [_p] * 11 + [_i32]),
+    "sp_group_create": (C.c_int, [_i32, _p, _pp]),
+    "sp_group_destroy": (C.c_int, [_p]),
+    "sp_group_size": (_i32, [_p]),
+    "sp_group_member": (C.c_int, [_p, _i32, _pp, _p]),
+    "sp_group_launch_count": (_i64, [_p]),
+    "sp_group_table_create": (C.c_int, [_p, _i32, _p, _p, _p, _p, _p, _p, _p, _p, _i32, _i32, _pp]),
+    "sp_group_table_destroy": (C.c_int, [_p, _p]),
+    "sp_group_table_replica": (C.c_int, [_p, _i32, _pp]),
+    "sp_group_table_set_latency": (C.c_int, [_p, _p, _i32, _p, _p]),
+    "sp_group_table_get_latency": (C.c_int, [_p, _p, _i32, _p]),
+    "sp_group_select_batch": (C.c_int, [_p, _i32, _p, _d, _i32, _p, _p, _p, _p, _p, _p,
+                                        _p, _p, _p, _p, _p, _p, _p, _i32]),
+    "sp_group_feedback_fold": (C.c_int, [_p, _i32, _p, _i32, _p, _p, _p, _d, _i32, _i32, _i32]),
 }
 
 

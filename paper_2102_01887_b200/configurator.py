@@ -161,17 +161,23 @@ class OpTable:
             raise _lib.SlackpipeError("at most 8 backend kinds are supported")
         self._gpos = gpos
         self.gkind = np.array([gpos[e.backend_kind] for e in entries], dtype=np.int32)
+        self._create_device(device)
+
+    def _device_columns(self):
+        """sp_table_create's column arguments (kept alive by the caller across the call)."""
+        lat_init = np.array([e.latency_initial_s for e in self.entries], dtype=np.float64)
+        return (len(self.entries), self.lat, lat_init, self.res, self.batch_int.astype(np.int32),
+                self.pool, self.price, self.gkind, self.id_rank.astype(np.int32))
+
+    def _create_device(self, device) -> None:
         self._ctx = get_context(device)
-        lat_init = np.array([e.latency_initial_s for e in entries], dtype=np.float64)
-        batch32 = self.batch_int.astype(np.int32)  # kept alive across the call
-        rank32 = self.id_rank.astype(np.int32)
+        n, lat, lat_init, res, batch32, pool, price, gkind, rank32 = self._device_columns()
         h = C.c_void_p()
         check(
             self._ctx.lib.sp_table_create(
-                self._ctx.handle, n, ptr(self.lat), ptr(lat_init), ptr(self.res),
-                ptr(batch32), ptr(self.pool), ptr(self.price),
-                ptr(self.gkind), ptr(rank32), len(self.global_kinds),
-                self.ref_index, C.byref(h)),
+                self._ctx.handle, n, ptr(lat), ptr(lat_init), ptr(res), ptr(batch32), ptr(pool),
+                ptr(price), ptr(gkind), ptr(rank32), len(self.global_kinds), self.ref_index,
+                C.byref(h)),
             "sp_table_create",
         )
         self._handle = h

@@ -147,7 +147,7 @@ int sp_ctx_create(int device, sp_ctx** out) {
   int n = 0;
   SP_CUDA(cudaGetDeviceCount(&n));
   if (device < 0 || device >= n) return fail(SP_E_INVALID, "ctx_create: bad device ordinal");
-  SP_CUDA(cudaSetDevice(device));
+  DeviceScope _dev_scope(device);
   cudaDeviceProp prop;
   SP_CUDA(cudaGetDeviceProperties(&prop, device));
   if (prop.major < 10)
@@ -168,13 +168,13 @@ int sp_ctx_create(int device, sp_ctx** out) {
 }
 
 int sp_ctx_destroy(sp_ctx* ctx) {
+  DeviceScope _dev_scope(ctx ? ctx->device : -1);
   if (ctx && ctx->capture) {
     cudaStreamSynchronize(ctx->stream);
     cudaStreamDestroy(ctx->capture);
     ctx->capture = nullptr;
   }
   if (!ctx) return SP_OK;
-  cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   cudaFree(ctx->io_dev);
   cudaFree(ctx->ptr_dev);
@@ -196,6 +196,7 @@ int sp_ctx_destroy(sp_ctx* ctx) {
 }
 
 int sp_ctx_set_stream(sp_ctx* ctx, void* stream) {
+  DeviceScope _dev_scope(ctx ? ctx->device : -1);
   if (!ctx) return fail(SP_E_INVALID, "null ctx");
   SP_CUDA(cudaStreamSynchronize(ctx->stream));
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
@@ -217,6 +218,7 @@ int sp_table_create(sp_ctx* ctx, int32_t M, const double* lat, const double* lat
                     const double* res, const int32_t* batch, const double* pool,
                     const double* price, const int32_t* kind, const int32_t* id_rank,
                     int32_t K, int32_t ref_index, sp_table** out) {
+  DeviceScope _dev_scope(ctx ? ctx->device : -1);
   if (!ctx || !out) return fail(SP_E_INVALID, "table_create: null argument");
   // configurator.py:178-179
   if (M < 1) return fail(SP_E_INVALID, "operation has no schedulable configuration");
@@ -303,6 +305,7 @@ int sp_table_create(sp_ctx* ctx, int32_t M, const double* lat, const double* lat
 }
 
 int sp_table_destroy(sp_ctx* ctx, sp_table* t) {
+  DeviceScope _dev_scope(ctx ? ctx->device : -1);
   if (!t) return SP_OK;
   if (ctx) cudaStreamSynchronize(ctx->stream);
   free_table(t);
@@ -311,6 +314,7 @@ int sp_table_destroy(sp_ctx* ctx, sp_table* t) {
 
 int sp_table_set_latency(sp_ctx* ctx, sp_table* t, int32_t n, const int32_t* idx,
                          const double* val) {
+  DeviceScope _dev_scope(ctx ? ctx->device : -1);
   if (!ctx || !t || n < 0 || (n > 0 && (!idx || !val)))
     return fail(SP_E_INVALID, "set_latency: bad argument");
   // Repeated OpTable.set_latency calls: the last write to an index wins.
@@ -344,6 +348,7 @@ int sp_table_set_latency(sp_ctx* ctx, sp_table* t, int32_t n, const int32_t* idx
 }
 
 int sp_table_get_latency(sp_ctx* ctx, sp_table* t, double* out_lat) {
+  DeviceScope _dev_scope(ctx ? ctx->device : -1);
   if (!ctx || !t || !out_lat) return fail(SP_E_INVALID, "get_latency: null argument");
   SP_CUDA(cudaMemcpyAsync(out_lat, t->lat, sizeof(double) * t->M, cudaMemcpyDeviceToHost,
                           ctx->stream));
@@ -352,6 +357,7 @@ int sp_table_get_latency(sp_ctx* ctx, sp_table* t, double* out_lat) {
 }
 
 int sp_table_prepare(sp_ctx* ctx, sp_table* t, double alpha) {
+  DeviceScope _dev_scope(ctx ? ctx->device : -1);
   if (!ctx || !t) return fail(SP_E_INVALID, "prepare: null argument");
   int rc;
   Plan* p = plan_get(ctx, t, alpha, &rc);
@@ -361,6 +367,7 @@ int sp_table_prepare(sp_ctx* ctx, sp_table* t, double alpha) {
 int sp_table_plan_supported(const sp_table* t) { return t && t->plan_ok ? 1 : 0; }
 
 int sp_table_plan_bytes(sp_ctx* ctx, sp_table* t, double alpha, int64_t* out_bytes) {
+  DeviceScope _dev_scope(ctx ? ctx->device : -1);
   if (!ctx || !t || !out_bytes) return fail(SP_E_INVALID, "plan_bytes: null argument");
   int rc;
   Plan* p = plan_get(ctx, t, alpha, &rc);
@@ -380,6 +387,7 @@ int sp_table_plan_bytes(sp_ctx* ctx, sp_table* t, double alpha, int64_t* out_byt
 
 int sp_scores(sp_ctx* ctx, sp_table* t, const double* slack_by_kind, double alpha,
               double* out_score, double* out_cost) {
+  DeviceScope _dev_scope(ctx ? ctx->device : -1);
   if (!ctx || !t || !slack_by_kind || !out_score || !out_cost)
     return fail(SP_E_INVALID, "scores: null argument");
   int rc;
@@ -404,12 +412,18 @@ int sp_scores(sp_ctx* ctx, sp_table* t, const double* slack_by_kind, double alph
   return SP_OK;
 }
 
-int sp_select_batch(sp_ctx* ctx, int32_t n_tables, sp_table* const* tables, double alpha,
-                    int32_t N, const int32_t* op, const double* slack, const int32_t* avail,
-                    const int32_t* supply, const int32_t* min_batch, const uint32_t* flags,
-                    int32_t* out_idx, int32_t* out_code, int32_t* out_fill, double* out_obj,
-                    double* out_slack, double* out_wait, double* out_kind_min, int32_t mode,
-                    int32_t mem) {
+}  // extern "C"
+
+namespace sp {
+// sp_select_batch without the final synchronisation when sync == false (host I/O is then
+// complete only after select_host_wait): lets sp_group_select_batch run every member
+// device's shard concurrently from one host thread.
+int select_batch_impl(sp_ctx* ctx, int32_t n_tables, sp_table* const* tables, double alpha,
+                      int32_t N, const int32_t* op, const double* slack, const int32_t* avail,
+                      const int32_t* supply, const int32_t* min_batch, const uint32_t* flags,
+                      int32_t* out_idx, int32_t* out_code, int32_t* out_fill, double* out_obj,
+                      double* out_slack, double* out_wait, double* out_kind_min, int32_t mode,
+                      int32_t mem, bool sync) {
   if (!ctx || !tables || n_tables < 1) return fail(SP_E_INVALID, "select: null argument");
   if (N < 0) return fail(SP_E_INVALID, "select: negative N");
   if (N > 0 && (!slack || !avail || !supply || !min_batch || !flags || !out_idx || !out_code))
@@ -458,7 +472,7 @@ int sp_select_batch(sp_ctx* ctx, int32_t n_tables, sp_table* const* tables, doub
                              (int32_t*)bufs[8].d, (double*)bufs[9].d, (double*)bufs[10].d,
                              (double*)bufs[11].d, (double*)bufs[12].d, mode);
       if (rc != SP_OK) return rc;
-      SP_CUDA(cudaStreamSynchronize(ctx->stream));
+      if (sync) SP_CUDA(cudaStreamSynchronize(ctx->stream));
       return SP_OK;
     }
   }
@@ -543,14 +557,38 @@ int sp_select_batch(sp_ctx* ctx, int32_t n_tables, sp_table* const* tables, doub
     SP_CUDA(cudaEventRecord(ctx->ev_out[0], sout));
     SP_CUDA(cudaStreamWaitEvent(st, ctx->ev_out[0], 0));
   }
-  SP_CUDA(cudaStreamSynchronize(sout));
-  SP_CUDA(cudaStreamSynchronize(st));
+  if (sync) {
+    SP_CUDA(cudaStreamSynchronize(sout));
+    SP_CUDA(cudaStreamSynchronize(st));
+  }
   return SP_OK;
+}
+
+int select_host_wait(sp_ctx* ctx) {
+  if (ctx->d2h) SP_CUDA(cudaStreamSynchronize(ctx->d2h));
+  SP_CUDA(cudaStreamSynchronize(ctx->stream));
+  return SP_OK;
+}
+}  // namespace sp
+
+extern "C" {
+
+int sp_select_batch(sp_ctx* ctx, int32_t n_tables, sp_table* const* tables, double alpha,
+                    int32_t N, const int32_t* op, const double* slack, const int32_t* avail,
+                    const int32_t* supply, const int32_t* min_batch, const uint32_t* flags,
+                    int32_t* out_idx, int32_t* out_code, int32_t* out_fill, double* out_obj,
+                    double* out_slack, double* out_wait, double* out_kind_min, int32_t mode,
+                    int32_t mem) {
+  DeviceScope _dev_scope(ctx ? ctx->device : -1);
+  return select_batch_impl(ctx, n_tables, tables, alpha, N, op, slack, avail, supply, min_batch,
+                           flags, out_idx, out_code, out_fill, out_obj, out_slack, out_wait,
+                           out_kind_min, mode, mem, true);
 }
 
 int sp_affinity_from_minima(sp_ctx* ctx, int32_t N, int32_t K, const double* kind_min,
                             const int32_t* query_kind, double* out, void* reserved,
                             int32_t mem) {
+  DeviceScope _dev_scope(ctx ? ctx->device : -1);
   if (!ctx || N < 0 || K < 1 || K > kMaxKinds || reserved)
     return fail(SP_E_INVALID, "affinity: bad argument");
   if (N > 0 && (!kind_min || !query_kind || !out)) return fail(SP_E_INVALID, "affinity: null array");
@@ -581,6 +619,7 @@ int sp_affinity_from_minima(sp_ctx* ctx, int32_t N, int32_t K, const double* kin
 int sp_dag_create(sp_ctx* ctx, int32_t V, const int32_t* pred_ptr, const int32_t* pred_idx,
                   const int32_t* val_idx, const uint8_t* terminal, int32_t n_src,
                   const int32_t* sources, sp_dag** out) {
+  DeviceScope _dev_scope(ctx ? ctx->device : -1);
   if (!ctx || !out || V < 1 || !pred_ptr || !val_idx || !terminal || n_src < 1 || !sources)
     return fail(SP_E_INVALID, "dag_create: bad argument");
   if (pred_ptr[0] != 0) return fail(SP_E_INVALID, "dag_create: pred_ptr[0] must be 0");
@@ -742,6 +781,7 @@ int sp_dag_create(sp_ctx* ctx, int32_t V, const int32_t* pred_ptr, const int32_t
 }
 
 int sp_dag_destroy(sp_ctx* ctx, sp_dag* g) {
+  DeviceScope _dev_scope(ctx ? ctx->device : -1);
   if (!g) return SP_OK;
   if (ctx) cudaStreamSynchronize(ctx->stream);
   cudaFree(g->prog);
@@ -756,6 +796,7 @@ int sp_dag_destroy(sp_ctx* ctx, sp_dag* g) {
 int sp_slack_batch(sp_ctx* ctx, sp_dag* g, int32_t I, const double* ref_lat,
                    int32_t ref_stride, const double* target, const double* now, int32_t K,
                    const double* Q, double* out_slack, double* out_ratio, int32_t mem) {
+  DeviceScope _dev_scope(ctx ? ctx->device : -1);
   if (!ctx || !g || I < 0 || !ref_lat || !target || !now || K < 0 || (K > 0 && !Q))
     return fail(SP_E_INVALID, "slack_batch: bad argument");
   if (ref_stride != 0 && ref_stride < g->n_val)
@@ -798,6 +839,7 @@ int sp_slack_batch(sp_ctx* ctx, sp_dag* g, int32_t I, const double* ref_lat,
 
 int sp_queueing(sp_ctx* ctx, int32_t K, const int32_t* ptr, const double* lat,
                 const double* res, const int32_t* cnt, const double* pool, double* out) {
+  DeviceScope _dev_scope(ctx ? ctx->device : -1);
   if (!ctx || K < 1 || K > 32 || !ptr || !pool || !out)
     return fail(SP_E_INVALID, "queueing: bad argument");
   const int n = ptr[K];
@@ -831,6 +873,7 @@ int sp_queueing(sp_ctx* ctx, int32_t K, const int32_t* ptr, const double* lat,
 int sp_feedback_fold(sp_ctx* ctx, int32_t n_tables, sp_table* const* tables, int32_t n,
                      const int32_t* op, const int32_t* idx, const double* obs, double beta,
                      int32_t dfp_count, int32_t dfp_on, int32_t fb_frozen, int32_t mem) {
+  DeviceScope _dev_scope(ctx ? ctx->device : -1);
   if (!ctx || !tables || n_tables < 1 || n < 0 || (n > 0 && (!idx || !obs)))
     return fail(SP_E_INVALID, "feedback_fold: bad argument");
   if (!(beta > 0.0 && beta <= 1.0)) return fail(SP_E_INVALID, "smoothing_beta must be in (0, 1]");
@@ -867,6 +910,7 @@ int sp_feedback_fold(sp_ctx* ctx, int32_t n_tables, sp_table* const* tables, int
 
 int sp_table_get_counters(sp_ctx* ctx, sp_table* t, int32_t* completed_ref,
                           int32_t* out_obs_count) {
+  DeviceScope _dev_scope(ctx ? ctx->device : -1);
   if (!ctx || !t) return fail(SP_E_INVALID, "get_counters: null argument");
   int32_t c[4];
   SP_CUDA(cudaMemcpyAsync(c, t->dev_counters, sizeof(c), cudaMemcpyDeviceToHost, ctx->stream));
@@ -880,6 +924,7 @@ int sp_table_get_counters(sp_ctx* ctx, sp_table* t, int32_t* completed_ref,
 
 int sp_table_set_counters(sp_ctx* ctx, sp_table* t, int32_t completed_ref,
                           const int32_t* obs_count) {
+  DeviceScope _dev_scope(ctx ? ctx->device : -1);
   if (!ctx || !t) return fail(SP_E_INVALID, "set_counters: null argument");
   int32_t c[4] = {completed_ref, 0, 0, 0};
   SP_CUDA(cudaMemcpyAsync(t->dev_counters, c, sizeof(c), cudaMemcpyHostToDevice, ctx->stream));
@@ -904,6 +949,7 @@ extern "C" int sp_speculate_batch(sp_ctx* ctx, int32_t n_tables, sp_table* const
                                   int32_t* out_idx, int32_t* out_fill, double* out_slack,
                                   double* out_obj, int32_t* out_n, int32_t* out_delay_idx,
                                   double* out_delay_wait, int32_t mem) {
+  DeviceScope _dev_scope(ctx ? ctx->device : -1);
   if (!ctx || !tables || !pool) return fail(SP_E_INVALID, "speculate: null argument");
   if (n_tables < 1 || n_tables > 64) return fail(SP_E_INVALID, "speculate: n_tables must be in [1, 64]");
   if (!(alpha >= 0.0)) return fail(SP_E_INVALID, "alpha must be >= 0");  // configurator.py:37
@@ -1018,6 +1064,7 @@ extern "C" int sp_commit_round(sp_ctx* ctx, int32_t R, int32_t n_ops, sp_table* 
                                int32_t* out_idx, int32_t* out_fill, double* out_slack,
                                double* out_obj, double* out_aff, int32_t* out_best,
                                int32_t mem) {
+  DeviceScope _dev_scope(ctx ? ctx->device : -1);
   if (!ctx || !tables) return fail(SP_E_INVALID, "commit: null argument");
   if (n_ops < 1 || n_ops > 64) return fail(SP_E_INVALID, "commit: n_ops must be in [1, 64]");
   if (R < 0) return fail(SP_E_INVALID, "commit: negative round count");
@@ -1112,6 +1159,7 @@ extern "C" int sp_slack_select_batch(sp_ctx* ctx, sp_dag* g, int32_t n_tables,
                                      const uint32_t* flags, int32_t* out_idx, int32_t* out_code,
                                      int32_t* out_fill, double* out_obj, double* out_slack,
                                      double* out_wait, double* out_kslack, int32_t mem) {
+  DeviceScope _dev_scope(ctx ? ctx->device : -1);
   if (!ctx || !g || !tables || I < 0 || K < 1 || K > SP_MAX_KINDS)
     return fail(SP_E_INVALID, "slack_select: bad argument");
   for (int t = 0; t < n_tables; ++t)
@@ -1187,6 +1235,7 @@ extern "C" int sp_observation_quantiles(sp_ctx* ctx, int32_t n_tables, sp_table*
                                         int32_t n, const int32_t* op, const int32_t* idx,
                                         const double* obs, double q, double beta, double* out,
                                         int32_t* out_count, double* out_smooth, int32_t mem) {
+  DeviceScope _dev_scope(ctx ? ctx->device : -1);
   if (!ctx || !tables || n_tables < 1 || n < 0) return fail(SP_E_INVALID, "quantiles: bad argument");
   if (!(q >= 0.0 && q <= 1.0)) return fail(SP_E_INVALID, "quantiles: q must be in [0, 1]");
   if (out_smooth && !(beta >= 0.0 && beta <= 1.0))

@@ -214,6 +214,36 @@ constexpr int kCertMaxV = 253;  // node ids 0..252; 0xFE = no option, 0xFF = pat
 
 // ---- error plumbing ------------------------------------------------------------------
 namespace sp {
+// Kernel attributes (cudaFuncSetAttribute) belong to the current device's context: a
+// once-per-process flag would leave the other devices of a multi-GPU group unconfigured.
+// attr_once(mask) is true the first time it is called on each device.
+inline bool attr_once(uint64_t& mask) {
+  int d = 0;
+  cudaGetDevice(&d);
+  const uint64_t bit = 1ull << (d & 63);
+  if (mask & bit) return false;
+  mask |= bit;
+  return true;
+}
+// Every ctx entry point runs on the context's device and restores the caller's current
+// device on return (several contexts / a DeviceGroup may live in one process).
+struct DeviceScope {
+  int prev = -1;
+  explicit DeviceScope(int dev) {
+    if (dev < 0) return;
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+    else prev = -1;
+  }
+  ~DeviceScope() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+inline int cur_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d & 63;
+}
 void set_error(const std::string& msg);
 int fail(int code, const std::string& msg);
 int cuda_fail(cudaError_t e, const char* what);
@@ -286,4 +316,11 @@ int fold_launch(sp_ctx* ctx, int n_tables, sp_table* const* tables, int n, const
                 const int32_t* idx, const double* obs, double beta, int dfp_count, int dfp_on,
                 int fb_frozen);
 void* ctx_tmp(sp_ctx* ctx, size_t bytes, int* rc);
+int select_batch_impl(sp_ctx* ctx, int32_t n_tables, sp_table* const* tables, double alpha,
+                      int32_t N, const int32_t* op, const double* slack, const int32_t* avail,
+                      const int32_t* supply, const int32_t* min_batch, const uint32_t* flags,
+                      int32_t* out_idx, int32_t* out_code, int32_t* out_fill, double* out_obj,
+                      double* out_slack, double* out_wait, double* out_kind_min, int32_t mode,
+                      int32_t mem, bool sync);
+int select_host_wait(sp_ctx* ctx);
 }  // namespace sp

@@ -1546,23 +1546,21 @@ static int plan_enqueue(sp_ctx* ctx, sp_table* t, Plan& p) {
   SP_CHECK_LAUNCH(ctx);
   k_orders_out<<<nb, 256, 0, st>>>(M, oA, t->ent_r1, t->ent_r2, t->r2, oB, t->order);
   SP_CHECK_LAUNCH(ctx);
-  static bool stair_attr = false;
-  if (!stair_attr) {
+  static uint64_t stair_attr = 0;
+  if (attr_once(stair_attr)) {
     SP_CUDA(cudaFuncSetAttribute(k_stair, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  2 * kStairMaxW * 1024 * (int)sizeof(uint32_t)));
     SP_CUDA(cudaFuncSetAttribute(k_stair_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  kStairSmemBytes));
-    stair_attr = true;
   }
   int max_mk = 0;
   for (int k = 0; k < K; ++k) max_mk = std::max(max_mk, t->kind_count[k]);
-  static bool lanes_attr = false;
-  if (!lanes_attr) {
+  static uint64_t lanes_attr = 0;
+  if (attr_once(lanes_attr)) {
     SP_CUDA(cudaFuncSetAttribute(k_stair_lanes<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  kStairLanesSmem));
     SP_CUDA(cudaFuncSetAttribute(k_stair_lanes<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  kStairLanesSmem));
-    lanes_attr = true;
   }
   if (max_mk <= kStairLanesMax && !getenv("SP_STAIR_SMEM") && !getenv("SP_STAIR_GLOBAL")) {
     k_stair_stage<<<(M + 255) / 256, 256, 0, st>>>(M, K, ki, t->order, t->bidx, t->lat, t->r1,

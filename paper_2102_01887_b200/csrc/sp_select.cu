@@ -344,11 +344,10 @@ constexpr int kPlanSmemBudget = 200 * 1024;
 
 template <int KT>
 int launch_plan_t(sp_ctx* ctx, const PlanPtrs& pp, const SelectIO& io) {
-  static bool attr_done = false;
-  if (!attr_done) {
+  static uint64_t attr_done = 0;
+  if (attr_once(attr_done)) {
     SP_CUDA(cudaFuncSetAttribute(k_select_plan<KT>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kPlanSmemBudget));
-    attr_done = true;
   }
   const char* variant = getenv("SP_K2_VARIANT");
   const bool single = pp.hv && pp.n == 1 && !io.out_kind_min;
@@ -364,15 +363,14 @@ int launch_plan_t(sp_ctx* ctx, const PlanPtrs& pp, const SelectIO& io) {
       // next launch's CTAs take their place one at a time — measured 15.9 -> 15.5 us per
       // 2^20-decision step back to back) or 1024 x 1 (SP_K2F_THREADS=1024)
       const int thr = (getenv("SP_K2F_THREADS") && atoi(getenv("SP_K2F_THREADS")) == 1024) ? 1024 : 512;
-      static bool fast_attr[2] = {false, false};
-      if (!fast_attr[thr == 512]) {
+      static uint64_t fast_attr[2] = {0, 0};
+      if (attr_once(fast_attr[thr == 512])) {
         if (thr == 512)
           SP_CUDA(cudaFuncSetAttribute(k_select_fast<KT, 512>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, kPlanSmemBudget));
         else
           SP_CUDA(cudaFuncSetAttribute(k_select_fast<KT, 1024>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, kPlanSmemBudget));
-        fast_attr[thr == 512] = true;
       }
       FastIO<KT> f;
       f.slack = io.slack; f.avail = io.avail; f.supply = io.supply; f.min_batch = io.min_batch;
@@ -417,11 +415,10 @@ int launch_plan_t(sp_ctx* ctx, const PlanPtrs& pp, const SelectIO& io) {
 template <int KT>
 int launch_scan_t(sp_ctx* ctx, const ScanPtrs& sp_, size_t stage_bytes, const SelectIO& io) {
   const size_t max_stage = 200 * 1024;
-  static bool attr_done = false;
-  if (!attr_done) {
+  static uint64_t attr_done = 0;
+  if (attr_once(attr_done)) {
     SP_CUDA(cudaFuncSetAttribute(k_select_scan<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)max_stage));
-    attr_done = true;
   }
   int staged = stage_bytes <= max_stage ? 1 : 0;
   size_t smem = staged ? stage_bytes : 0;
@@ -507,15 +504,17 @@ int slack_select_launch(sp_ctx* ctx, sp_dag* g, int n_tables, sp_table* const* t
               getenv("SP_K12_GENERIC_DP") ? 0 : g->single_pred};
     K12In ki{ref, ref_stride, target, now, Q, I, out_kslack};
     auto launch = [&](auto kern) -> int {
-      static const void* attr_done[6] = {};  // one entry per k_slack_select instantiation
+      // one entry per k_slack_select instantiation, per device
+      static const void* attr_dev[64][6] = {};
+      const void** attr_done = attr_dev[cur_device()];
       bool done = false;
-      for (const void* f : attr_done) done = done || f == reinterpret_cast<const void*>(kern);
+      for (int q = 0; q < 6; ++q) done = done || attr_done[q] == reinterpret_cast<const void*>(kern);
       if (!done) {
         SP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      kPlanSmemBudget));
-        for (const void*& f : attr_done)
-          if (!f) {
-            f = reinterpret_cast<const void*>(kern);
+        for (int q = 0; q < 6; ++q)
+          if (!attr_done[q]) {
+            attr_done[q] = reinterpret_cast<const void*>(kern);
             break;
           }
       }

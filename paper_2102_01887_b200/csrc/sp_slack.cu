@@ -404,7 +404,8 @@ int slack_launch(sp_ctx* ctx, sp_dag* g, int I, const double* ref, int ref_strid
                         (size_t)kCertWarps * ((size_t)(g->V + 1) * 256 + (size_t)g->V * 160 +
                                               (size_t)nfw * 128);
     if (smem <= 227 * 1024) {
-      static size_t cert_attr = 0;
+      static size_t cert_attr_dev[64] = {};
+      size_t& cert_attr = cert_attr_dev[cur_device()];
       if (smem > 48 * 1024 && smem > cert_attr) {
         SP_CUDA(cudaFuncSetAttribute(k_slack_cert, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
@@ -425,7 +426,8 @@ int slack_launch(sp_ctx* ctx, sp_dag* g, int I, const double* ref, int ref_strid
                       (size_t)g->max_span * sizeof(int4) +
                       (size_t)g->max_preds * sizeof(uint32_t);
   if (smem > 227 * 1024) return fail(SP_E_UNSUPPORTED, "slack: DAG too wide for shared memory");
-  static size_t attr_set = 0;
+  static size_t attr_set_dev[64] = {};
+  size_t& attr_set = attr_set_dev[cur_device()];
   if (smem > 48 * 1024 && smem > attr_set) {
     SP_CUDA(cudaFuncSetAttribute(k_slack, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem));

@@ -189,3 +189,51 @@ def deep_dag_instances(dag: PipelineDag, I: int, seed: int = 3, K: int = 4):
     now = rng.uniform(0.0, 1.0, size=I) * T
     Q = rng.exponential(1.0, size=(I, K)) * (0.05 * T)[:, None]
     return np.ascontiguousarray(ref), T, now, np.ascontiguousarray(Q)
+
+
+# ---- config 4: latency-target sweep x replicas on the AMBER pipeline -----------------------
+
+SWEEP_MULTS = (0.5, 1.0, 2.0, 5.0, 10.0)
+SWEEP_SNAPSHOTS = 64
+SWEEP_CP_MIN = 90.41885182994682  # fast-anchor latency of the AMBER run
+
+
+@dataclass
+class SweepInputs:
+    """Instance-major inputs of config 4: instance i = ((r - r0) * 5 + m) * 64 + j."""
+    ref: np.ndarray      # (I, V) reference latencies by operation (meta["ops"] order)
+    target: np.ndarray   # (I,)
+    now: np.ndarray      # (I,)
+    Q: np.ndarray        # (I, K)
+    avail: np.ndarray    # (I, V) int32
+    supply: np.ndarray   # (I, V) int32
+
+
+def amber_sweep(ref0: np.ndarray, K: int, r0: int, r1: int, mults=SWEEP_MULTS,
+                snapshots: int = SWEEP_SNAPSHOTS, cp_min: float = SWEEP_CP_MIN) -> SweepInputs:
+    """SURVEY.md §8(d) config 4 for replicas [r0, r1): target T = m * CP_min; snapshot j at
+    now = j/64 * T; per (replica r, target index m) one generator seeded r*5 + m draws, in this
+    order, Q (64 x K) ~ Exp(0.02 T), the reference-latency drift (64 x V) exp(N(0, 0.2)), avail
+    (64 x V) U{1..64} and upstream supply (64 x V) U{0..64}.  Seeds depend on the global replica
+    index, so any split of [0, R) over ranks reproduces the same global workload."""
+    V = len(ref0)
+    S, nm = snapshots, len(mults)
+    n = (r1 - r0) * nm
+    ref = np.empty((n, S, V))
+    Q = np.empty((n, S, K))
+    avail = np.empty((n, S, V), np.int32)
+    supply = np.empty((n, S, V), np.int32)
+    target = np.repeat(np.array([m * cp_min for m in mults] * (r1 - r0)), S)
+    frac = np.arange(S) / S
+    for u in range(n):
+        r, m = r0 + u // nm, u % nm
+        rng = np.random.default_rng(r * 5 + m)
+        T = mults[m] * cp_min
+        Q[u] = rng.exponential(0.02 * T, size=(S, K))
+        ref[u] = ref0[None, :] * np.exp(rng.normal(0.0, 0.2, size=(S, V)))
+        avail[u] = rng.integers(1, 65, size=(S, V))
+        supply[u] = rng.integers(0, 65, size=(S, V))
+    now = np.tile(frac, n) * target
+    I = n * S
+    return SweepInputs(ref.reshape(I, V), target, now, Q.reshape(I, K), avail.reshape(I, V),
+                       supply.reshape(I, V))

@@ -153,9 +153,10 @@ def test_config5_sample_vs_reference(gpu_ctx, syn):
     t.close()
 
 
-@pytest.mark.parametrize("alpha", [100.0, 0.0])
+@pytest.mark.parametrize("alpha", [100.0, 0.0, 1.0, 1000.0])
 def test_config2_full_size_vs_c_oracle(c2_table, alpha):
-    """BASELINE config 2 at full size: 2^20 invocations x 4,096 configurations."""
+    """BASELINE config 2 at full size, every alpha of SURVEY.md §8(d): 2^20 invocations x
+    4,096 configurations, plan and scan kernels against the C oracle."""
     import paper_2102_01887_b200 as sp
     from paper_2102_01887_b200 import synth
 
@@ -406,3 +407,44 @@ def test_staircase_builder_variants_vs_oracle(gpu_ctx, variant, monkeypatch):
             j = int(rng.integers(0, M))
             tab.set_latency(np.array([j], np.int32), np.array([float(t.lat[j] * 1.7)]))
         tab.close()
+
+
+def test_device_group_fanout_matches_single_device(gpu_ctx):
+    """sp_group_select_batch (single-process multi-GPU fan-out, SURVEY.md §8(b) Threading): the
+    config-2 batch sharded over a group of member contexts (two independent contexts per
+    visible GPU here; one per GPU on a full box) equals the single-context call and the C
+    oracle bit for bit; set_latency and the feedback fold reach every replica."""
+    import torch
+
+    import paper_2102_01887_b200 as sp
+    from paper_2102_01887_b200 import synth
+
+    devs = [d for d in range(torch.cuda.device_count()) for _ in range(2)]
+    g = sp.DeviceGroup(devs)
+    spec = synth.synth_spec(False)
+    gt = g.table(spec, synth.synth_scenario())
+    t = optable.from_spec(spec, synth.synth_scenario(), ["cpu", "gpu"])
+    inv = synth.synth_invocations((1 << 18) + 7, t.lat, t.gkind, seed=77)
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+    for host in (lambda a: np.ascontiguousarray(a), pin):  # pageable staging and zero-copy
+        r = gt.select_batch(host(inv.slack), 100.0, host(inv.avail), upstream_supply=host(inv.supply),
+                            min_batch=host(inv.min_batch), flags=host(inv.flags))
+        exp = cselect.select_batch([t], inv.slack, 100.0, inv.avail, inv.supply, inv.min_batch, inv.flags)
+        assert_same_decisions(r, exp, "group")
+    # mutations go to every replica
+    rng = np.random.default_rng(3)
+    for i in rng.choice(len(gt.lat), size=20, replace=False):
+        gt.set_latency(int(i), float(gt.lat[i]) * 1.5)
+    idx = rng.integers(0, len(gt.lat), size=5000).astype(np.int32)
+    obs = rng.uniform(0.01, 3.0, size=5000)
+    gt.fold(idx, obs)
+    for m in range(len(g)):
+        assert np.array_equal(gt.replica_latency(m).view(np.uint64), np.asarray(gt.lat).view(np.uint64))
+    t.lat[:] = gt.lat
+    r = gt.select_batch(inv.slack, 1000.0, inv.avail, upstream_supply=inv.supply,
+                        min_batch=inv.min_batch, flags=inv.flags)
+    exp = cselect.select_batch([t], inv.slack, 1000.0, inv.avail, inv.supply, inv.min_batch, inv.flags)
+    assert_same_decisions(r, exp, "group-after-fold")
+    assert g.launch_count > 0
+    gt.close()
+    g.close()

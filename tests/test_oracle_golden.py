@@ -397,3 +397,64 @@ def test_speculate_oracle_matches_reference_calls():
         calls += 1
         formed += n
     assert calls == 15000 and formed > 7000
+
+
+# ---- C restatements used for full-size checks (oracle/select_oracle.c) ----------------------
+
+def test_c_dp_slack_matches_reference_compute_slack(slk):
+    """oracle_slack_dp (forward DP in C, the config-3 full-size checker) reproduces the
+    reference's compute_slack golden values on the 400 random DAGs."""
+    from oracle import cselect
+    from paper_2102_01887_b200.pipeline import PipelineDag
+
+    checked = 0
+    for c in range(len(slk["v_off"]) - 1):
+        names, edges, ref = _dag_case(slk, c)
+        dag = PipelineDag(tuple(names), tuple(edges))
+        q = np.flatnonzero(slk["q_case"] == c)
+        refm = np.repeat(np.array([ref[n] for n in names])[None, :], len(q), 0)
+        out = cselect.slack_dp(dag, refm, slk["q_target"][q], slk["q_elapsed"][q],
+                               slk["q_queue"][q].reshape(-1, 1))
+        got = out[np.arange(len(q)), slk["q_op"][q], 0]
+        assert _same(got, slk["q_expect"][q]), c
+        checked += len(q)
+    assert checked > 1000
+
+
+def test_c_path_slack_matches_reference(slk):
+    """oracle_slack_paths (literal _path_ratios / slack_by_kind in C, the config-4 checker)
+    reproduces the reference's compute_slack on the 300 golden path lists."""
+    from oracle import cselect
+
+    meta = golden_json(slk, "paths_json")
+    for i, exp in enumerate(slk["paths_expect"]):
+        names = sorted({n for p in meta["paths"][i] for n in p})
+        cols = [[names.index(n) for n in p] for p in meta["paths"][i]]
+        refv = np.array([[meta["ref"][i][n] for n in names]])
+        out = cselect.slack_paths(refv, [meta["budget"][i]], [0.0], [[0.0]], cols)
+        assert _same(out[0, names.index(meta["op"][i]), 0], exp), i
+
+
+def test_c_fold_matches_reference():
+    """oracle_fold (sequential EWMA + gate lift in C, the config-5 full-run checker) against the
+    reference's _apply_feedback golden streams (feedback on, gate on; tables are independent,
+    so each table's sub-stream is folded on its own)."""
+    from oracle import cselect
+
+    d = golden("feedback_cases")
+    lo = 0
+    checked = 0
+    for m, states, op, idx, obs in feedback_case_states(d):
+        for t, st in enumerate(states):
+            M = m["sizes"][t]
+            if m["fb"] and m["dfp_on"]:
+                cs = cselect.FoldState(st.lat, st.lat_init, st.ref_index)
+                sel = np.asarray(op) == t
+                cselect.fold(cs, np.asarray(idx)[sel], np.asarray(obs)[sel], beta=m["beta"],
+                             dfp_count=m["dfp"])
+                assert _same(cs.lat, d["final_lat"][lo:lo + M])
+                assert np.array_equal(cs.obs_count, d["final_cnt"][lo:lo + M])
+                assert int(cs.completed_ref[0]) == m["completed_ref"][t]
+                checked += 1
+            lo += M
+    assert checked > 20

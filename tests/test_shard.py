@@ -6,6 +6,7 @@ from __future__ import annotations
 
 import os
 import socket
+from pathlib import Path
 
 import numpy as np
 import pytest
@@ -149,3 +150,20 @@ def test_two_rank_online_fold_keeps_replicas_identical(tmp_path):
     assert np.array_equal(l0.view(np.uint64), l1.view(np.uint64))
     assert np.array_equal(l0.view(np.uint64), single.view(np.uint64))
     assert not np.array_equal(single, _online_batches()[0].lat)  # the fold did change the table
+
+
+def test_bench_spawns_ranks_itself():
+    """`bench.py --gpus 2` outside torchrun launches two ranks itself (torch.distributed.run on
+    127.0.0.1); in --dist-selftest mode they rendezvous over gloo on the CPU and run the shard /
+    counter / max-time / observation-gather plumbing of the GPU arms."""
+    import json
+    import subprocess
+    import sys
+
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, str(Path(__file__).resolve().parent.parent / "bench.py"),
+                        "--gpus", "2", "--dist-selftest"], capture_output=True, text=True,
+                       timeout=300, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["world"] == 2 and line["ranks_ok"] and line["t_max"] == 0.002
