@@ -101,6 +101,13 @@ int sp_table_plan_supported(const sp_table* t);
 /* Plan byte size for alpha after sp_table_prepare (synchronises); for DESIGN/bench. */
 int sp_table_plan_bytes(sp_ctx* ctx, sp_table* t, double alpha, int64_t* out_bytes);
 
+/* Diagnostic: (re)build the plan for alpha with builder 0 = the context's default, 1 = the
+ * multi-kernel builder, 2 = the one-kernel cluster builder, and copy its byte image (total
+ * bytes in *out_bytes; copied when cap is large enough).  Tests compare the builders and the
+ * CPU restatement oracle/plan.py section by section. */
+int sp_table_plan_image(sp_ctx* ctx, sp_table* t, double alpha, int32_t builder, void* out,
+                        int64_t cap, int64_t* out_bytes);
+
 /* ---- Eq. 1 vector: OpTable.scores (configurator.py:219-227) -------------------------- */
 /* slack_by_kind: K doubles (host).  Outputs length M (host, synchronous). */
 int sp_scores(sp_ctx* ctx, sp_table* t, const double* slack_by_kind, double alpha,

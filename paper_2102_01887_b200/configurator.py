@@ -222,6 +222,11 @@ class OpTable:
                                                 C.byref(out)))
         return int(out.value)
 
+    def plan_image(self, alpha: float, builder: str = "default") -> bytes:
+        """The decision plan's byte image for alpha, built by the context default, the
+        multi-kernel ("legacy") or the one-kernel cluster ("cluster") builder (diagnostic)."""
+        return _plan_image(self._ctx, self._handle, alpha, builder)
+
     # -- reference API ----------------------------------------------------------------------
     def set_latency(self, index: int, latency_s: float) -> None:
         """configurator.py:211-213 (host mirror + device copy)."""
@@ -314,6 +319,17 @@ class OpTable:
         return select_batch([self], slack, alpha, available, upstream_supply=upstream_supply,
                             min_batch=min_batch, flags=flags, kind_min=kind_min, mode=mode,
                             out=out)
+
+
+def _plan_image(ctx, handle, alpha: float, builder: str) -> bytes:
+    b = {"default": 0, "legacy": 1, "cluster": 2}[builder]
+    n = C.c_int64()
+    check(ctx.lib.sp_table_plan_image(ctx.handle, handle, float(alpha), b, None, 0, C.byref(n)),
+          "sp_table_plan_image")
+    out = np.empty(int(n.value), np.uint8)
+    check(ctx.lib.sp_table_plan_image(ctx.handle, handle, float(alpha), b, ptr(out), len(out),
+                                      C.byref(n)), "sp_table_plan_image")
+    return out.tobytes()
 
 
 def make_flags(allow_delay, excluded_mask=0) -> np.ndarray:
@@ -496,6 +512,9 @@ class _RawTable:
 
     def prepare(self, alpha: float) -> None:
         check(self._ctx.lib.sp_table_prepare(self._ctx.handle, self._handle, float(alpha)))
+
+    def plan_image(self, alpha: float, builder: str = "default") -> bytes:
+        return _plan_image(self._ctx, self._handle, alpha, builder)
 
     def close(self) -> None:
         if getattr(self, "_handle", None):

@@ -128,6 +128,9 @@ static void free_table(sp_table* t) {
   cudaFree(t->pos_r12);
   cudaFree(t->pos_meta);
   cudaFree(t->pos_lat);
+  cudaFree(t->pc_seg);
+  cudaFree(t->pc_seg_ent);
+  cudaFree(t->pc_scratch);
   for (auto& p : t->plans) plan_release(p);
   delete t;
 }
@@ -155,6 +158,7 @@ int sp_ctx_create(int device, sp_ctx** out) {
   sp_ctx* c = new (std::nothrow) sp_ctx();
   if (!c) return fail(SP_E_NOMEM, "ctx_create: host allocation");
   c->device = device;
+  c->plan_legacy = getenv("SP_PLAN_LEGACY") != nullptr;
   c->num_sms = prop.multiProcessorCount;
   c->max_smem_optin = (int)prop.sharedMemPerBlockOptin;
   cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
@@ -289,6 +293,7 @@ int sp_table_create(sp_ctx* ctx, int32_t M, const double* lat, const double* lat
     return rc;
   }
   rc = plan_scratch_alloc(t);
+  if (rc == SP_OK) rc = plan_cluster_prepare(t, kind, bidx.data());
   if (rc != SP_OK) {
     free_table(t);
     return rc;
@@ -382,6 +387,49 @@ int sp_table_plan_bytes(sp_ctx* ctx, sp_table* t, double alpha, int64_t* out_byt
   if (h.magic != kPlanMagic) return fail(SP_E_RUNTIME, "plan_bytes: plan image corrupt");
   if (h.total_bytes > p->image_cap) return fail(SP_E_RUNTIME, "plan_bytes: plan overflow");
   *out_bytes = h.total_bytes;
+  return SP_OK;
+}
+
+int sp_table_plan_image(sp_ctx* ctx, sp_table* t, double alpha, int32_t builder, void* out,
+                        int64_t cap, int64_t* out_bytes) {
+  DeviceScope _dev_scope(ctx ? ctx->device : -1);
+  if (!ctx || !t || !out_bytes || builder < 0 || builder > 2)
+    return fail(SP_E_INVALID, "plan_image: bad argument");
+  if (!t->plan_ok) return fail(SP_E_UNSUPPORTED, "plan_image: the table has no staircase plan");
+  if (builder == 2 && !t->pc_ok)
+    return fail(SP_E_UNSUPPORTED, "plan_image: the table's shape is outside the cluster builder");
+  const bool saved = ctx->plan_legacy;
+  if (builder != 0) ctx->plan_legacy = builder == 1;
+  for (auto& p : t->plans)  // force a fresh build with the requested builder
+    if (p.alpha == alpha || (p.alpha != p.alpha && alpha != alpha)) p.valid = false;
+  int rc = SP_OK;
+  Plan* p = nullptr;
+  for (auto& q : t->plans)
+    if (q.alpha == alpha || (q.alpha != q.alpha && alpha != alpha)) p = &q;
+  if (p && p->graph) {  // a captured graph replays one builder only
+    cudaGraphExecDestroy(p->graph);
+    p->graph = nullptr;
+    p->builds = 0;
+  }
+  p = plan_get(ctx, t, alpha, &rc);
+  ctx->plan_legacy = saved;
+  if (!p) return rc;
+  PlanHdr h;
+  SP_CUDA(cudaMemcpyAsync(&h, p->image, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+  SP_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (h.magic != kPlanMagic) return fail(SP_E_RUNTIME, "plan_image: plan image invalid");
+  *out_bytes = h.total_bytes;
+  if (out && cap >= h.total_bytes) {
+    SP_CUDA(cudaMemcpyAsync(out, p->image, h.total_bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    SP_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+  // the next select rebuilds with the context's own builder
+  p->valid = false;
+  if (p->graph) {
+    cudaGraphExecDestroy(p->graph);
+    p->graph = nullptr;
+    p->builds = 0;
+  }
   return SP_OK;
 }
 

@@ -124,6 +124,8 @@ struct sp_ctx {
   // a plan image was (re)written by a kernel that no select launch has waited on yet: the
   // next K2f launch must not read any plan before its griddepcontrol.wait
   bool plan_dirty = true;
+  // SP_PLAN_LEGACY (read once at creation): build plans with the multi-kernel builder
+  bool plan_legacy = false;
   // grow-only device arena for staged host I/O
   void* io_dev = nullptr;
   size_t io_cap = 0;
@@ -177,6 +179,13 @@ struct sp_table {
   uint32_t* ukr = nullptr;                      // 2M: unified candidate r1 ranks
   int32_t* uent = nullptr;                      // 2M: unified candidate entry index
   uint32_t* umap = nullptr;                     // 2M: candidate -> unified id
+  // one-kernel cluster builder (sp_plan_cluster.cu): static (kind, lane) segments + scratch
+  bool pc_ok = false;
+  int32_t pc_nseg = 0, pc_max_seg = 0;
+  int32_t pc_seg_lo[sp::kMaxKinds + 1] = {};
+  void* pc_seg = nullptr;
+  int32_t* pc_seg_ent = nullptr;
+  void* pc_scratch = nullptr;
   std::vector<sp::Plan> plans;
 };
 
@@ -269,6 +278,9 @@ int cuda_fail(cudaError_t e, const char* what);
 namespace sp {
 int plan_build(sp_ctx* ctx, sp_table* t, Plan& p);
 int plan_scratch_alloc(sp_table* t);
+int plan_cluster_prepare(sp_table* t, const int32_t* kind, const int32_t* bidx);
+int plan_cluster_launch(sp_ctx* ctx, sp_table* t, Plan& p, int W, const PlanHdr& hdr,
+                        int32_t* status);
 Plan* plan_get(sp_ctx* ctx, sp_table* t, double alpha, int* rc);
 const PlanHdr* plan_host_header(Plan& p);  // nullptr until the async copy has landed
 void plan_release(Plan& p);

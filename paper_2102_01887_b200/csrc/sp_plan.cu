@@ -1483,6 +1483,8 @@ int plan_scratch_alloc(sp_table* t) {
   return SP_OK;
 }
 
+static int plan_finish(sp_ctx* ctx, Plan& p, sp_table* t);
+
 static int plan_enqueue(sp_ctx* ctx, sp_table* t, Plan& p) {
   const int M = t->M, K = t->K;
   cudaStream_t st = ctx->stream;
@@ -1490,9 +1492,12 @@ static int plan_enqueue(sp_ctx* ctx, sp_table* t, Plan& p) {
     SP_CUDA(cudaMalloc(&p.cost, sizeof(double) * M));
     SP_CUDA(cudaMalloc(&p.costpen, sizeof(double) * M));
   }
-  k_cost<<<(M + 255) / 256, 256, 0, st>>>(M, t->lat, t->res, t->batch, t->pool, t->price,
-                                          p.alpha, p.cost, p.costpen);
-  SP_CHECK_LAUNCH(ctx);
+  const bool cluster = t->plan_ok && t->pc_ok && !ctx->plan_legacy;
+  if (!cluster) {
+    k_cost<<<(M + 255) / 256, 256, 0, st>>>(M, t->lat, t->res, t->batch, t->pool, t->price,
+                                            p.alpha, p.cost, p.costpen);
+    SP_CHECK_LAUNCH(ctx);
+  }
   if (!t->plan_ok) {
     p.valid = true;
     p.version = t->version;
@@ -1502,6 +1507,19 @@ static int plan_enqueue(sp_ctx* ctx, sp_table* t, Plan& p) {
   if (!p.image) {
     p.image_cap = plan_image_capacity(t, W);
     SP_CUDA(cudaMalloc(&p.image, (size_t)p.image_cap));
+  }
+  if (cluster) {  // one cluster kernel writes cost / costpen and the whole image
+    PlanHdr h;
+    memset(&h, 0, sizeof(h));
+    h.magic = kPlanMagic;
+    h.M = M;
+    h.nB = t->nB;
+    h.W = W;
+    h.K = K;
+    for (int b = 0; b < kMaxB; ++b) h.batch_vals[b] = b < t->nB ? t->batch_vals[b] : INT32_MAX;
+    const int rc = plan_cluster_launch(ctx, t, p, W, h, t->rows_per_kind + kMaxKinds);
+    if (rc != SP_OK) return rc;
+    return plan_finish(ctx, p, t);
   }
   KindInfo ki;
   for (int k = 0; k < kMaxKinds; ++k) {
@@ -1617,6 +1635,11 @@ static int plan_enqueue(sp_ctx* ctx, sp_table* t, Plan& p) {
       K, W, ki, t->thrscratch, t->rowscratch, t->cidf, t->cids, t->ukey, t->uent, t->umap, t->lat,
       t->batch, t->kind, p.image);
   SP_CHECK_LAUNCH(ctx);
+  return plan_finish(ctx, p, t);
+}
+
+static int plan_finish(sp_ctx* ctx, Plan& p, sp_table* t) {
+  cudaStream_t st = ctx->stream;
   ctx->plan_dirty = true;
   // fetch the header back without blocking; it becomes a kernel parameter once it lands
   if (!p.host_hdr) {

@@ -1,0 +1,73 @@
+"""The one-kernel cluster plan builder (sp_plan_cluster.cu) against the multi-kernel builder
+(sp_plan.cu) and the CPU restatement (oracle/plan.py): every section of the plan image —
+header counts, batch lookup table, per-kind thresholds, bucket tables and staircase rows, and
+the candidate records — bit-identical, on the config-2 / config-5 tables at every alpha, the
+AMBER tables, and heavily tied random tables (zero / negative latencies, 1..8 kinds, 1..16
+batch sizes)."""
+from __future__ import annotations
+
+import json
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+from oracle import optable, plan
+from test_gpu_select import _random_table, raw_table
+
+pytestmark = pytest.mark.gpu
+
+
+def _check(tab, K, alpha, arrays):
+    cl = plan.parse_image(tab.plan_image(alpha, "cluster"))
+    lg = plan.parse_image(tab.plan_image(alpha, "legacy"))
+    assert cl["magic"] == lg["magic"] == 0x53504C4E
+    assert plan.compare(cl, lg) == [], plan.compare(cl, lg)
+    exp = plan.plan_image(*arrays, K, alpha)
+    assert plan.compare(cl, exp) == [], plan.compare(cl, exp)
+    assert cl["total_bytes"] == lg["total_bytes"]
+
+
+@pytest.mark.parametrize("with_model", [False, True])
+def test_cluster_plan_synthetic_tables(gpu_ctx, with_model):
+    import paper_2102_01887_b200 as sp
+    from paper_2102_01887_b200 import synth
+
+    spec = synth.synth_spec(with_model)
+    tab = sp.OpTable(spec, synth.synth_scenario())
+    t = optable.from_spec(spec, synth.synth_scenario(), ["cpu", "gpu"])
+    arrays = (t.lat, t.res, t.batch_int, t.pool, t.price, t.gkind, t.id_rank)
+    for alpha in ((0.0, 1.0, 100.0, 1000.0) if not with_model else (100.0, 0.0)):
+        _check(tab, 2, alpha, arrays)
+    tab.close()
+
+
+def test_cluster_plan_amber_tables(gpu_ctx):
+    import bench_workloads as bw
+    import paper_2102_01887_b200 as sp
+    from oracle import commit as oc
+
+    with np.load(GOLDEN / "amber_trace.npz") as z:
+        meta = json.loads(bytes(z["meta_json"]).decode())
+    tabs = bw._amber_tables(sp, meta)
+    otabs = oc.amber_tables(meta)
+    K = len(meta["kinds"])
+    for tab, t in zip(tabs, otabs):
+        arrays = (t.lat, t.res, t.batch_int, t.pool, t.price, t.gkind, t.id_rank)
+        for alpha in (100.0, 0.0):
+            _check(tab, K, alpha, arrays)
+
+
+@pytest.mark.parametrize("seed,M,nB,K,nonpos", [(1, 3000, 8, 2, False), (2, 2000, 16, 4, False),
+                                                (3, 700, 13, 3, False), (4, 5000, 5, 8, False),
+                                                (5, 1, 1, 1, False), (6, 64, 2, 2, False),
+                                                (7, 900, 8, 2, True), (8, 300, 11, 3, True),
+                                                (9, 12000, 16, 6, False)])
+def test_cluster_plan_random_tables(gpu_ctx, seed, M, nB, K, nonpos):
+    rng = np.random.default_rng(seed)
+    t = _random_table(rng, M, nB, K, nonpos)
+    tab = raw_table(t, K)
+    arrays = (t.lat, t.res, t.batch_int, t.pool, t.price, t.gkind, t.id_rank)
+    for alpha in (0.0, 7.5, 1000.0):
+        _check(tab, K, alpha, arrays)
+    tab.close()
