@@ -57,6 +57,11 @@ __device__ __forceinline__ uint64_t okey(double x) {
   return order_key(static_cast<uint64_t>(__double_as_longlong(x)));
 }
 
+constexpr uint64_t kKeyNegZero = 0x7FFFFFFFFFFFFFFFull;  // okey(-0.0)
+constexpr uint64_t kKeyPosZero = 0x8000000000000000ull;  // okey(+0.0)
+// numeric order with -0.0 == +0.0: the order key of +0.0 for both zeros
+__device__ __forceinline__ uint64_t canon(uint64_t k) { return k == kKeyNegZero ? kKeyPosZero : k; }
+
 __device__ __forceinline__ void cluster_barrier() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
   asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
@@ -308,6 +313,8 @@ struct PcArgs {
   // global scratch (carved by the host); per segment slices at seg.off
   double *rp_lat, *rs_lat;      // P / S record latencies (position order)
   uint32_t *rp_uid, *rs_uid;    // candidate id of a record (kInfPc: not a candidate)
+  uint32_t *rp_rank, *rs_rank;  // fast path: #records of the kind with a smaller latency
+  uint32_t *rp_nrep, *rs_nrep;  // fast path: the latency also occurs earlier in the kind's lists
   // candidates (P: final P-records, S: first S-records), compact per segment slice
   uint64_t *cp_key, *cs_key;    // order key of the score (cost / costpen)
   uint64_t *cp_ck, *cs_ck;      // order key of the cost
@@ -331,6 +338,15 @@ __device__ __forceinline__ uint64_t gtimer() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
+}
+
+#define PC_STAMP(i)                                                \
+  do {                                                             \
+    if (threadIdx.x == 0) pc_stamps()[(i)] = gtimer();             \
+  } while (0)
+__device__ __forceinline__ uint64_t* pc_stamps() {
+  __shared__ uint64_t st[32];
+  return st;
 }
 
 __device__ __forceinline__ double key_double(uint64_t u) {  // inverse of okey
@@ -425,6 +441,7 @@ __device__ void pc_segment(const PcArgs& a, const PcShared& S, int s, uint8_t* s
     sv[i] = val[q];
   }
   __syncthreads();
+  PC_STAMP(1);
   bool bad = false;
 #pragma unroll
   for (int q = 0; q < E; ++q) {
@@ -439,6 +456,7 @@ __device__ void pc_segment(const PcArgs& a, const PcShared& S, int s, uint8_t* s
       if (i < n) a.ord[off + i] = (int32_t)val[q];
     }
   }
+  PC_STAMP(2);
   // 2. per position: cost / costpen (configurator.py:224-225, numpy order, no FMA), keys
   bool pos_zero = false;
 #pragma unroll
@@ -463,6 +481,7 @@ __device__ void pc_segment(const PcArgs& a, const PcShared& S, int s, uint8_t* s
     }
   }
   if (__syncthreads_or(pos_zero) && t == 0) atomicOr(&a.kinfo[2 * sg.kind + 1], 1);
+  PC_STAMP(3);
   // Key1 (the r1 order: cost key, res, id_rank) and Key2 (costpen key, then Key1)
   auto less1 = [&](int x, int y) {
     if (pck[x] != pck[y]) return pck[x] < pck[y];
@@ -489,6 +508,7 @@ __device__ void pc_segment(const PcArgs& a, const PcShared& S, int s, uint8_t* s
       fP[q] = p < n && (ex < 0 || less1(p, ex));
       carry = best1(carry, tot);
     }
+  PC_STAMP(4);
     carry = -1;
 #pragma unroll
     for (int q = E - 1; q >= 0; --q) {
@@ -513,6 +533,7 @@ __device__ void pc_segment(const PcArgs& a, const PcShared& S, int s, uint8_t* s
     nS += ts;
   }
   __syncthreads();
+  PC_STAMP(6);
   // 5. a P-record is a candidate iff no later P-record has the same latency (it is its own
   //    row's lane value); an S-record iff no earlier S-record has the same latency.  Records
   //    and candidates (with their full argmin keys) go to global scratch.
@@ -527,7 +548,9 @@ __device__ void pc_segment(const PcArgs& a, const PcShared& S, int s, uint8_t* s
     if (j < nP) {
       const int p = lP[j];
       a.rp_lat[off + j] = plat[p];
-      a.rp_uid[off + j] = kInfPc;
+      a.rp_uid[off + j] = fin ? 0u : kInfPc;
+      a.rp_rank[off + j] = 0u;
+      a.rp_nrep[off + j] = j > 0 && canon(okey(plat[lP[j - 1]])) == canon(okey(plat[p]));
       if (fin) {
         const int c = off + ncp + op;
         a.cp_key[c] = pck[p];
@@ -541,7 +564,9 @@ __device__ void pc_segment(const PcArgs& a, const PcShared& S, int s, uint8_t* s
     if (j < nS) {
       const int p = lS[j];
       a.rs_lat[off + j] = plat[p];
-      a.rs_uid[off + j] = kInfPc;
+      a.rs_uid[off + j] = fst ? 0u : kInfPc;
+      a.rs_rank[off + j] = 0u;
+      a.rs_nrep[off + j] = j > 0 && canon(okey(plat[lS[j - 1]])) == canon(okey(plat[p]));
       if (fst) {
         const int c = off + ncs + os;
         a.cs_key[c] = pcpk[p];
@@ -636,6 +661,7 @@ __device__ void pc_cand_sort(const PcArgs& a, const PcShared& S, int ncp, int nc
     sv[t + q * T] = val[q];
   }
   __syncthreads();
+  PC_STAMP(13);
   // runs of numerically equal scores: insertion sort by (cost key, res, id_rank, side)
   auto lessc = [&](uint32_t x, uint32_t y) {
     if (sck[x] != sck[y]) return sck[x] < sck[y];
@@ -660,6 +686,7 @@ __device__ void pc_cand_sort(const PcArgs& a, const PcShared& S, int ncp, int nc
     }
   }
   __syncthreads();
+  PC_STAMP(14);
   for (int u = t; u < nc; u += T) cand_out(a, S, cand_ref(a, S, s_off, ncp, (int)sv[u]), u);
   __syncthreads();
 }
@@ -721,100 +748,276 @@ __device__ void pc_candidates(const PcArgs& a, const PcShared& S, uint8_t* smem,
   __syncthreads();
 }
 
-// ---- phase 2b: a kind's thresholds and its record lists -----------------------------------
-// Every CTA working on kind k stages the kind's records (per lane: the P list, then the S list,
-// latencies in position order) in shared memory and sorts their latencies: row 0 is -inf, row
-// r the r-th distinct latency (a group's threshold is its last entry's latency in key order: for
-// the zero group +0.0 whenever the kind has a +0.0 latency, -0.0 otherwise).  Slot 0 publishes
-// the row count and the thresholds (global) for every CTA's layout.
-struct KindStage {
-  int nr, R;          // records, rows
-  int lane[kMaxB][4];  // per lane: P start, P count, S start, S count (record index space)
-  bool staged;        // records and thresholds are in shared memory
-};
-constexpr int kPcStageMax = 4096;  // records staged in shared memory per kind
+// ---- phase 2, merge form ---------------------------------------------------------------------
+// Every list phase 1 produced is already sorted: a segment's P-candidates (strictly falling
+// Key1 along the latency order, score = cost) descend in the unified order, its S-candidates
+// (strictly rising Key2, score = costpen) ascend, and every lane's P / S record lists ascend in
+// latency.  So no sort is needed: a candidate's id is the number of candidates that precede it
+// (binary searches in the other lists, spread over every CTA of the cluster), and a kind's row
+// thresholds are the distinct record latencies placed by their count of smaller latencies.
 
-template <int E>
-__device__ int pc_thr_sort(int nr, const double* L, double* thr, bool has_pz, uint8_t* scratch,
-                           int* s_w) {
-  const int T = blockDim.x, t = threadIdx.x, NE = E * T;
-  const int N2 = pow2ceil(max(nr, 2));
-  uint64_t* sk = reinterpret_cast<uint64_t*>(scratch);
-  uint32_t* sv = reinterpret_cast<uint32_t*>(sk + NE);
-  uint64_t key[E];
-  uint32_t val[E];
-#pragma unroll
-  for (int q = 0; q < E; ++q) {
-    const int j = t + q * T;
-    key[q] = j < nr ? okey(L[j]) : ~0ull;
-    val[q] = (uint32_t)j;
-  }
-  reg_bitonic<E>(key, val, N2, sk, sv);
-#pragma unroll
-  for (int q = 0; q < E; ++q) sk[t + q * T] = key[q];
-  __syncthreads();
-  int o = 0;
-#pragma unroll
-  for (int q = 0; q < E; ++q) {
-    const int j = t + q * T;
-    const bool st = j < nr && (j == 0 || key_double(sk[j]) != key_double(sk[j - 1]));
-    int tot;
-    const int ex = pc_excl_sum(st ? 1 : 0, s_w, &tot);
-    if (st) {
-      double v = key_double(sk[j]);
-      if (v == 0.0) v = has_pz ? 0.0 : -0.0;
-      thr[1 + o + ex] = v;
-    }
-    o += tot;
-  }
-  if (t == 0) thr[0] = -INFINITY;
-  __syncthreads();
-  return o + 1;
+constexpr int kPcCandMerge = 4096;   // candidates kept in shared memory by every CTA
+constexpr int kPcStageMax = 4096;    // records of one kind staged in shared memory
+// shared-memory map of phases 2 and 3 (bytes)
+constexpr int kSmCandKey = 0;                                  // u64[kPcCandMerge]
+constexpr int kSmCandEnt = kSmCandKey + 8 * kPcCandMerge;       // u32[kPcCandMerge]
+constexpr int kSmL = kSmCandEnt + 4 * kPcCandMerge;             // f64[kPcStageMax] record lats
+constexpr int kSmThr = kSmL + 8 * kPcStageMax;                  // f64[kPcStageMax + 2]
+constexpr int kSmU = kSmThr + 8 * (kPcStageMax + 2);            // u32[kPcStageMax] record ids
+constexpr int kSmWork = kSmU + 4 * kPcStageMax;                 // scratch (64 KB)
+constexpr int kSmEnd = kSmWork + 16 * kPcStageMax;
+
+struct KindStage {
+  int nr, R;           // records, rows
+  int lane[kMaxB][4];  // per lane: P start, P count, S start, S count (record index space)
+  bool staged;         // records and thresholds are in shared memory
+};
+
+struct CandLists {
+  int nl, nc;
+  int off[2 * kPcMaxSegs + 1];  // list i = 2s (P of segment s, descending), 2s+1 (S, ascending)
+};
+
+// equal scores (rare): the rest of the argmin key from global memory — kept out of line so that
+// the compiler never hoists these loads into the common comparison path
+__device__ __noinline__ bool cand_tie_less(const PcArgs& a, int eu, int ev, uint32_t su, uint32_t sv) {
+  const uint64_t cu = okey(a.cost[eu]), cv = okey(a.cost[ev]);
+  if (cu != cv) return cu < cv;
+  if (a.res[eu] != a.res[ev]) return a.res[eu] < a.res[ev];
+  if (a.id_rank[eu] != a.id_rank[ev]) return a.id_rank[eu] < a.id_rank[ev];
+  return !su && sv;
 }
 
+__device__ __forceinline__ int list_of(const CandLists& cl, int u) {
+  int lo = 0, hi = cl.nl;  // last i with off[i] <= u
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (cl.off[mid] <= u) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+// Pairwise merge tree of `nr` ascending runs (offsets off[0..nr], shared; rewritten) of n items:
+// at every level an item of run r moves to (start of the merged pair) + (its index in r) +
+// (the items of the partner run that precede it: strictly smaller ones for the left run,
+// smaller-or-equal ones for the right run — equal items keep left-run-first order).  Returns the
+// buffer (src or dst) that holds the merged items.
+template <class T, class Less>
+__device__ T* merge_runs(T* src, T* dst, int* off, int* s_nr, int n, Less less) {
+  while (*s_nr > 1) {
+    const int nr = *s_nr;
+    for (int g = threadIdx.x; g < n; g += blockDim.x) {
+      int lo = 0, hi = nr;  // run of g: last r with off[r] <= g (and a non-empty run)
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (off[mid] <= g) lo = mid; else hi = mid;
+      }
+      int r = lo;
+      while (r + 1 < nr && off[r + 1] <= g) ++r;
+      const T x = src[g];
+      const int pr = r ^ 1;
+      const int base = off[r & ~1];
+      if (pr >= nr) {
+        dst[g] = x;
+        continue;
+      }
+      const int pb = off[pr], pn = off[pr + 1] - pb;
+      int a = 0, b = pn;
+      if (r & 1) {
+        while (a < b) {
+          const int mid = (a + b) >> 1;
+          if (!less(x, src[pb + mid])) a = mid + 1; else b = mid;
+        }
+      } else {
+        while (a < b) {
+          const int mid = (a + b) >> 1;
+          if (less(src[pb + mid], x)) a = mid + 1; else b = mid;
+        }
+      }
+      dst[base + (g - off[r]) + a] = x;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int m = 0;
+      for (int i = 0; i < nr; i += 2) off[m++] = off[i];
+      off[m] = n;
+      *s_nr = m;
+    }
+    __syncthreads();
+    T* tsw = src;
+    src = dst;
+    dst = tsw;
+  }
+  return src;
+}
+
+// phase 2a: candidate ids; every CTA ranks its share of the candidates.  Returns false when
+// the merge form does not apply (too many candidates, or a -0.0 penalized score whose order
+// key would misplace it) — CTA 0 then sorts with the general path.
+__device__ bool pc_cand_merge(const PcArgs& a, const PcShared& S, CandLists& cl, uint8_t* smem,
+                              int* s_w) {
+  const int T = blockDim.x, t = threadIdx.x;
+  const int c = (int)cluster_rank();
+  if (c != 0) return true;  // CTA 0 orders the candidates
+  {
+    const int i = t;
+    const int len = i < 2 * a.nseg ? S.cnt[4 * (i >> 1) + 2 + (i & 1)] : 0;
+    int tot;
+    const int o = pc_excl_sum(len, s_w, &tot);
+    if (i <= 2 * a.nseg) cl.off[i] = o;
+    if (t == 0) {
+      cl.nl = 2 * a.nseg;
+      cl.nc = tot;
+    }
+    __syncthreads();
+  }
+  const int nc = cl.nc;
+  if (nc > kPcCandMerge) return false;
+  uint64_t* K = reinterpret_cast<uint64_t*>(smem + kSmCandKey);
+  uint32_t* Ent = reinterpret_cast<uint32_t*>(smem + kSmCandEnt);
+  bool negzero = false;
+  for (int u = t; u < nc; u += T) {
+    const int i = list_of(cl, u);
+    const int sl = S.seg[i >> 1].off + (u - cl.off[i]);
+    const uint64_t k = (i & 1) ? a.cs_key[sl] : a.cp_key[sl];
+    negzero |= (i & 1) && k == kKeyNegZero;
+    K[u] = canon(k);
+    Ent[u] = (uint32_t)(((i & 1) ? a.cs_er[sl] : a.cp_er[sl]) & 0xFFFF);
+  }
+  if (__syncthreads_or(negzero)) return false;
+  PC_STAMP(13);
+  // u precedes v in (score, cost key, res, id_rank, side); items are candidate | S-side << 31
+  auto prec = [&](uint32_t x, uint32_t y) {
+    const int u = (int)(x & 0x7FFFFFFFu), v = (int)(y & 0x7FFFFFFFu);
+    const uint64_t ku = K[u], kv = K[v];
+    if (ku != kv) return ku < kv;
+    return cand_tie_less(a, (int)Ent[u], (int)Ent[v], x >> 31, y >> 31);
+  };
+  if (c == 0) {
+    // runs ascending: P lists are read backwards
+    uint32_t* A = reinterpret_cast<uint32_t*>(smem + kSmWork);
+    uint32_t* B = A + kPcCandMerge;
+    __shared__ int s_off2[2 * kPcMaxSegs + 1];
+    __shared__ int s_nr2;
+    for (int u = t; u < nc; u += T) {
+      const int i = list_of(cl, u);
+      const int b = cl.off[i], n_i = cl.off[i + 1] - b, j = u - b;
+      A[(i & 1) ? u : b + n_i - 1 - j] = (uint32_t)u | ((i & 1) ? 0x80000000u : 0u);
+    }
+    if (t <= cl.nl) s_off2[t] = cl.off[t];
+    if (t == 0) s_nr2 = cl.nl;
+    __syncthreads();
+    PC_STAMP(15);
+    uint32_t* R = merge_runs(A, B, s_off2, &s_nr2, nc, prec);
+    PC_STAMP(14);
+    for (int r = t; r < nc; r += T) {
+      const uint32_t x = R[r];
+      const int u = (int)(x & 0x7FFFFFFFu);
+      const int i = list_of(cl, u);
+      const bool su = (i & 1) != 0;
+      const int j = u - cl.off[i];
+      const int sg = i >> 1, sl = S.seg[sg].off + j;
+      const int er = su ? a.cs_er[sl] : a.cp_er[sl];
+      const int e = er & 0xFFFF, rec = er >> 16;
+      (su ? a.rs_uid : a.rp_uid)[S.seg[sg].off + rec] = (uint32_t)r;
+      CandB cb;
+      cb.meta = (uint32_t)e | ((su ? 0u : 1u) << 16) | ((uint32_t)S.seg[sg].kind << 17);
+      cb.batch = a.hdr.batch_vals[S.seg[sg].lane];
+      a.crec[3 * r + 0] = key_double(su ? a.cs_key[sl] : a.cp_key[sl]);
+      a.crec[3 * r + 1] = su ? a.cs_lat[sl] : a.cp_lat[sl];
+      a.crec[3 * r + 2] = __longlong_as_double(*reinterpret_cast<const long long*>(&cb));
+    }
+  }
+  if (c == 0 && t == 0) {
+    int ncp = 0;
+    for (int s = 0; s < a.nseg; ++s) ncp += S.cnt[4 * s + 2];
+    a.kinfo[16] = ncp;
+    a.kinfo[17] = nc - ncp;
+  }
+  __syncthreads();
+  return true;
+}
+
+// phase 2b: the kind's records staged (latency, by lane: P list then S list) and its row
+// thresholds: row 0 is -inf, row r the r-th distinct record latency (the zero group's
+// threshold is +0.0 whenever the kind has a +0.0 latency, -0.0 otherwise).  `publish`: write
+// the row count and thresholds for every CTA's layout.
 __device__ void pc_kind_stage(const PcArgs& a, const PcShared& S, int k, bool publish, KindStage& ks,
                               uint8_t* smem, int* s_w) {
   const int T = blockDim.x, t = threadIdx.x;
   const int ext = a.base[k] + k;
   const int s0 = a.seg_lo[k], s1 = a.seg_lo[k + 1];
+  __shared__ int s_loff[2 * kMaxB + 1];  // record-list offsets (list 2q: P of the q-th segment)
   if (t == 0) {
     int acc = 0;
     for (int b = 0; b < kMaxB; ++b) ks.lane[b][0] = ks.lane[b][1] = ks.lane[b][2] = ks.lane[b][3] = 0;
     for (int s = s0; s < s1; ++s) {
-      const int b = S.seg[s].lane;
+      const int b = S.seg[s].lane, q = s - s0;
+      s_loff[2 * q] = acc;
       ks.lane[b][0] = acc;
       ks.lane[b][1] = S.cnt[4 * s + 0];
       acc += ks.lane[b][1];
+      s_loff[2 * q + 1] = acc;
       ks.lane[b][2] = acc;
       ks.lane[b][3] = S.cnt[4 * s + 1];
       acc += ks.lane[b][3];
     }
+    s_loff[2 * (s1 - s0)] = acc;
     ks.nr = acc;
     ks.staged = acc <= kPcStageMax;
+    ks.R = 0;
   }
   __syncthreads();
-  const int nr = ks.nr;
+  PC_STAMP(8);
+  const int nr = ks.nr, nl = 2 * (s1 - s0);
   if (a.count[k] == 0) {
-    if (t == 0) ks.R = 0;
     if (publish && t == 0) a.kinfo[2 * k] = 0;
     __syncthreads();
     return;
   }
   const bool has_pz = a.kinfo[2 * k + 1] != 0;
   if (ks.staged) {
-    // smem: L[nr] record latencies, U[nr] candidate ids (phase 3), thr[nr + 1], sort scratch
-    double* L = reinterpret_cast<double*>(smem);
-    double* thr = L + kPcStageMax;
-    uint8_t* scratch = reinterpret_cast<uint8_t*>(thr + kPcStageMax + 1) + 8;
-    for (int s = s0; s < s1; ++s) {
-      const int b = S.seg[s].lane, off = S.seg[s].off;
-      for (int j = t; j < ks.lane[b][1]; j += T) L[ks.lane[b][0] + j] = a.rp_lat[off + j];
-      for (int j = t; j < ks.lane[b][3]; j += T) L[ks.lane[b][2] + j] = a.rs_lat[off + j];
+    double* L = reinterpret_cast<double*>(smem + kSmL);
+    double* thr = reinterpret_cast<double*>(smem + kSmThr);
+    uint64_t* tmp = reinterpret_cast<uint64_t*>(smem + kSmWork);  // 2 x kPcStageMax
+    for (int g = t; g < nr; g += T) {
+      int q = 0;
+      while (q + 1 < nl && s_loff[q + 1] <= g) ++q;
+      const int off = S.seg[s0 + (q >> 1)].off, j = g - s_loff[q];
+      L[g] = (q & 1) ? a.rs_lat[off + j] : a.rp_lat[off + j];
     }
     __syncthreads();
-    const int R = nr <= T ? pc_thr_sort<1>(nr, L, thr, has_pz, scratch, s_w)
-                          : pc_thr_sort<4>(nr, L, thr, has_pz, scratch, s_w);
-    if (t == 0) ks.R = R;
+    PC_STAMP(9);
+    // the kind's record lists (each ascending) merged by canonical latency key, then the
+    // distinct keys in order
+    uint64_t* A = tmp;
+    uint64_t* B = tmp + kPcStageMax;
+    __shared__ int s_off3[2 * kMaxB + 1];
+    __shared__ int s_nr3;
+    for (int g = t; g < nr; g += T) A[g] = canon(okey(L[g]));
+    if (t <= nl) s_off3[t] = s_loff[t];
+    if (t == 0) s_nr3 = nl;
+    __syncthreads();
+    const uint64_t* Mg = merge_runs(A, B, s_off3, &s_nr3, nr, [](uint64_t x, uint64_t y) { return x < y; });
+    int R = 1;
+    for (int g0 = 0; g0 < nr; g0 += T) {
+      const int g = g0 + t;
+      const bool o = g < nr && (g == 0 || Mg[g] != Mg[g - 1]);
+      int tot;
+      const int ex = pc_excl_sum(o ? 1 : 0, s_w, &tot);
+      if (o) {
+        double v = key_double(Mg[g]);
+        if (v == 0.0) v = has_pz ? 0.0 : -0.0;
+        thr[R + ex] = v;
+      }
+      R += tot;
+    }
+    if (t == 0) {
+      thr[0] = -INFINITY;
+      ks.R = R;
+    }
+    __syncthreads();
+    PC_STAMP(10);
     if (publish) {
       for (int r = t; r < R; r += T) a.thr[ext + r] = thr[r];
       if (t == 0) a.kinfo[2 * k] = R;
@@ -825,17 +1028,15 @@ __device__ void pc_kind_stage(const PcArgs& a, const PcShared& S, int k, bool pu
   // large record sets: shared-memory bitonic sort of the keys, thresholds through global
   const int N2 = pow2ceil(nr);
   uint64_t* key = reinterpret_cast<uint64_t*>(smem);
-  for (int j = t; j < N2; j += T) {
+  for (int g = t; g < N2; g += T) {
     uint64_t v = ~0ull;
-    if (j < nr) {
-      int b = 0;
-      while (b + 1 < kMaxB && !(j >= ks.lane[b][0] && j < ks.lane[b][2] + ks.lane[b][3])) ++b;
-      int s = s0;
-      while (S.seg[s].lane != b) ++s;
-      v = okey(j < ks.lane[b][2] ? a.rp_lat[S.seg[s].off + j - ks.lane[b][0]]
-                                 : a.rs_lat[S.seg[s].off + j - ks.lane[b][2]]);
+    if (g < nr) {
+      int q = 0;
+      while (q + 1 < nl && s_loff[q + 1] <= g) ++q;
+      const int off = S.seg[s0 + (q >> 1)].off, j = g - s_loff[q];
+      v = okey((q & 1) ? a.rs_lat[off + j] : a.rp_lat[off + j]);
     }
-    key[j] = v;
+    key[g] = v;
   }
   __syncthreads();
   bitonic_u64(key, N2);
@@ -860,6 +1061,412 @@ __device__ void pc_kind_stage(const PcArgs& a, const PcShared& S, int k, bool pu
   }
   if (t == 0) ks.R = 1 + nd;
   __syncthreads();
+}
+
+// ---- phases 2 and 3, distributed form (the common case) ---------------------------------------
+// Every CTA stages every candidate key and every record latency (all kinds) in shared memory and
+// takes an equal slice of the (item, list) pairs: a candidate's id is the number of candidates
+// preceding it summed over all candidate lists, a record's slot among the kind's latencies the
+// number of smaller record latencies summed over the kind's lists — binary searches in the sorted
+// lists, the per-list counts added with global atomics into the record's uid / rank word.  A
+// record "represents" its latency unless an earlier list of its kind (or its own predecessor)
+// holds the same one.  After the cluster barrier every CTA reduces the representatives per kind
+// (rows, first / last threshold) for the layout; each kind's CTAs compact the thresholds by slot.
+constexpr int kFastCand = 2048, kFastRec = 4096;
+constexpr int kFKc = 0;                          // u64[kFastCand] candidate keys (canonical)
+constexpr int kFRc = kFKc + 8 * kFastCand;       // u32[kFastCand] record slot | S << 31
+constexpr int kFCs = kFRc + 4 * kFastCand;       // u32[kFastCand] candidate slot (cp_ / cs_)
+constexpr int kFKr = kFCs + 4 * kFastCand;       // u64[kFastRec] record keys (canonical)
+constexpr int kFRr = kFKr + 8 * kFastRec;        // u32[kFastRec] record slot | S << 31
+constexpr int kFThr = kFRr + 4 * kFastRec;       // f64[kFastRec + 2] thresholds
+constexpr int kFTmp = kFThr + 8 * (kFastRec + 2);  // u64[kFastRec] keys by slot
+constexpr int kFOcc = kFTmp + 8 * kFastRec;      // u8[kFastRec]
+constexpr int kFWork = kFOcc + kFastRec;         // 32 KB: bucket histogram / lane values
+constexpr int kFEnd = kFWork + 32768;
+
+struct FastLists {
+  int nseg, nc, nrec;
+  int coff[2 * kPcMaxSegs + 1];  // candidate lists: 2s = P of segment s (descending), 2s+1 = S
+  int roff[2 * kPcMaxSegs + 1];  // record lists: 2s = P records of segment s, 2s+1 = S (ascending)
+  int klo[kMaxKinds + 1];        // kind k: record lists [2 seg_lo[k], 2 seg_lo[k+1])
+  int64_t wc, wr[kMaxKinds + 1];  // pair counts: candidates, records of kinds < k
+  bool ok;
+};
+
+__device__ __forceinline__ int last_le(const int* off, int n, int g) {  // last i: off[i] <= g
+  int lo = 0, hi = n;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (off[mid] <= g) lo = mid; else hi = mid;
+  }
+  while (lo + 1 < n && off[lo + 1] <= g) ++lo;
+  return lo;
+}
+
+// phase 2 (every CTA); returns false when the shapes exceed the staging capacity or a -0.0
+// penalized score breaks the lists' order — the caller then takes the sorting path
+__device__ bool pc_fast_phase2(const PcArgs& a, const PcShared& S, FastLists& fl, uint8_t* smem,
+                               int* s_w) {
+  const int T = blockDim.x, t = threadIdx.x;
+  const int C = (int)gridDim.x, c = (int)cluster_rank();
+  const int nl = 2 * a.nseg;
+  {
+    const int lc = t < nl ? S.cnt[4 * (t >> 1) + 2 + (t & 1)] : 0;
+    const int lr = t < nl ? S.cnt[4 * (t >> 1) + (t & 1)] : 0;
+    int tc, tr;
+    const int oc = pc_excl_sum(lc, s_w, &tc);
+    const int orr = pc_excl_sum(lr, s_w, &tr);
+    if (t <= nl) {
+      fl.coff[t] = oc;
+      fl.roff[t] = orr;
+    }
+    if (t == 0) {
+      fl.nseg = a.nseg;
+      fl.nc = tc;
+      fl.nrec = tr;
+      fl.ok = tc <= kFastCand && tr <= kFastRec;
+    }
+    __syncthreads();
+    if (t == 0) {
+      fl.wc = (int64_t)fl.nc * nl;
+      fl.wr[0] = 0;
+      for (int k = 0; k < a.K; ++k) {
+        fl.klo[k] = 2 * a.seg_lo[k];
+        const int n_r = fl.roff[2 * a.seg_lo[k + 1]] - fl.roff[2 * a.seg_lo[k]];
+        fl.wr[k + 1] = fl.wr[k] + (int64_t)n_r * (2 * (a.seg_lo[k + 1] - a.seg_lo[k]));
+      }
+      fl.klo[a.K] = nl;
+    }
+    __syncthreads();
+  }
+  if (!fl.ok) return false;
+  PC_STAMP(20);
+  uint64_t* Kc = reinterpret_cast<uint64_t*>(smem + kFKc);
+  uint32_t* Rc = reinterpret_cast<uint32_t*>(smem + kFRc);
+  uint32_t* Cs = reinterpret_cast<uint32_t*>(smem + kFCs);
+  uint64_t* Kr = reinterpret_cast<uint64_t*>(smem + kFKr);
+  uint32_t* Rr = reinterpret_cast<uint32_t*>(smem + kFRr);
+  bool negzero = false;
+  for (int u = t; u < fl.nc; u += T) {
+    const int i = last_le(fl.coff, nl, u);
+    const bool sS = i & 1;
+    const int sl = S.seg[i >> 1].off + (u - fl.coff[i]);
+    const uint64_t k = sS ? a.cs_key[sl] : a.cp_key[sl];
+    const int er = sS ? a.cs_er[sl] : a.cp_er[sl];
+    negzero |= sS && k == kKeyNegZero;
+    Kc[u] = canon(k);
+    Cs[u] = (uint32_t)sl;
+    Rc[u] = (uint32_t)(S.seg[i >> 1].off + (er >> 16)) | (sS ? 0x80000000u : 0u);
+  }
+  uint8_t* own_list = smem + kFOcc;  // list of each record (phase 2 only)
+  for (int g = t; g < fl.nrec; g += T) {
+    const int i = last_le(fl.roff, nl, g);
+    const bool sS = i & 1;
+    const int sl = S.seg[i >> 1].off + (g - fl.roff[i]);
+    Kr[g] = canon(okey(sS ? a.rs_lat[sl] : a.rp_lat[sl]));
+    Rr[g] = (uint32_t)sl | (sS ? 0x80000000u : 0u);
+    own_list[g] = (uint8_t)i;
+  }
+  if (__syncthreads_or(negzero)) {
+    if (t == 0) fl.ok = false;
+    __syncthreads();
+    return false;
+  }
+  PC_STAMP(21);
+  // candidate entries for the rare equal-score comparisons
+  auto cent = [&](int u) {
+    const uint32_t sl = Cs[u];
+    return (int)(((Rc[u] >> 31) ? a.cs_er[sl] : a.cp_er[sl]) & 0xFFFF);
+  };
+  auto prec = [&](int x, int y) {  // candidate x precedes candidate y in the unified order
+    const uint64_t kx = Kc[x], ky = Kc[y];
+    if (kx != ky) return kx < ky;
+    return cand_tie_less(a, cent(x), cent(y), Rc[x] >> 31, Rc[y] >> 31);
+  };
+  // per-CTA partial counts in shared memory (the threshold area is free until phase 3), added
+  // to the global words once per touched item
+  uint32_t* accC = reinterpret_cast<uint32_t*>(smem + kFThr);
+  uint32_t* accR = accC + kFastCand;
+  for (int i = t; i < kFastCand + kFastRec; i += T) accC[i] = 0u;
+  __syncthreads();
+  // pair counts stay far below 2^31 for the staged sizes (2048 x 256 + 4096 x 32)
+  const int wc = (int)fl.wc, W = (int)(fl.wc + fl.wr[a.K]);
+  const int i0 = (int)((int64_t)W * c / C), i1 = (int)((int64_t)W * (c + 1) / C);
+  for (int it = i0 + t; it < i1; it += T) {
+    if (it < wc) {  // candidate u against candidate list m
+      const int u = it / nl, m = it - u * nl;
+      const int b = fl.coff[m], n = fl.coff[m + 1] - b;
+      if (n == 0) continue;
+      const uint64_t ku = Kc[u];
+      int lo = 0, hi = n;
+      if (u >= b && u < b + n) {  // its own list: the elements before it (ascending) / after it
+        lo = (m & 1) ? u - b : b + n - 1 - u;
+      } else if (m & 1) {  // ascending: the preceding elements are a prefix
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          const uint64_t km = Kc[b + mid];
+          if (km != ku ? km < ku : prec(b + mid, u)) lo = mid + 1; else hi = mid;
+        }
+      } else {      // descending: a suffix
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          const uint64_t km = Kc[b + mid];
+          if (!(km != ku ? km < ku : prec(b + mid, u))) lo = mid + 1; else hi = mid;
+        }
+        lo = n - lo;
+      }
+      if (lo) atomicAdd(&accC[u], (uint32_t)lo);
+    } else {           // record g against a list m of its kind
+      const int j = it - wc;
+      int k = 0;
+      while ((int)fl.wr[k + 1] <= j) ++k;
+      const int nlk = fl.klo[k + 1] - fl.klo[k];
+      const int jj = j - (int)fl.wr[k];
+      const int q = jj / nlk;
+      const int g = fl.roff[fl.klo[k]] + q, m = fl.klo[k] + (jj - q * nlk);
+      const int b = fl.roff[m], n = fl.roff[m + 1] - b;
+      if (n == 0) continue;
+      const uint64_t x = Kr[g];
+      int lo = 0, hi = n;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (Kr[b + mid] < x) lo = mid + 1; else hi = mid;
+      }
+      if (lo) atomicAdd(&accR[g], (uint32_t)lo);
+      if (m < own_list[g] && lo < n && Kr[b + lo] == x) {
+        const uint32_t r = Rr[g];
+        ((r >> 31) ? a.rs_nrep : a.rp_nrep)[r & 0x7FFFFFFFu] = 1u;
+      }
+    }
+  }
+  __syncthreads();
+  for (int u = t; u < fl.nc; u += T)
+    if (accC[u]) {
+      const uint32_t r = Rc[u];
+      atomicAdd(((r >> 31) ? a.rs_uid : a.rp_uid) + (r & 0x7FFFFFFFu), accC[u]);
+    }
+  for (int g = t; g < fl.nrec; g += T)
+    if (accR[g]) {
+      const uint32_t r = Rr[g];
+      atomicAdd(((r >> 31) ? a.rs_rank : a.rp_rank) + (r & 0x7FFFFFFFu), accR[g]);
+    }
+  __syncthreads();
+  PC_STAMP(22);
+  return true;
+}
+
+// after the barrier, every CTA: per kind the representative count and the extreme latencies
+__device__ void pc_fast_layout_inputs(const PcArgs& a, const FastLists& fl, int32_t* rows,
+                                      double* thr2, uint8_t* smem) {
+  const int T = blockDim.x, t = threadIdx.x;
+  const uint64_t* Kr = reinterpret_cast<const uint64_t*>(smem + kFKr);
+  const uint32_t* Rr = reinterpret_cast<const uint32_t*>(smem + kFRr);
+  uint8_t* occ = smem + kFOcc;  // representative flag by record
+  __shared__ int s_cnt[kMaxKinds];
+  __shared__ unsigned long long s_min[kMaxKinds], s_max[kMaxKinds];
+  if (t < kMaxKinds) {
+    s_cnt[t] = 0;
+    s_min[t] = ~0ull;
+    s_max[t] = 0ull;
+  }
+  __syncthreads();
+  for (int g = t; g < fl.nrec; g += T) {
+    const uint32_t r = Rr[g];
+    const bool rep = ((r >> 31) ? a.rs_nrep : a.rp_nrep)[r & 0x7FFFFFFFu] == 0u;
+    occ[g] = rep;
+    if (rep) {
+      int k = 0;
+      while (fl.roff[fl.klo[k + 1]] <= g) ++k;
+      atomicAdd(&s_cnt[k], 1);
+      atomicMin(&s_min[k], (unsigned long long)Kr[g]);
+      atomicMax(&s_max[k], (unsigned long long)Kr[g]);
+    }
+  }
+  __syncthreads();
+  if (t < kMaxKinds) {
+    rows[t] = t < a.K && a.count[t] > 0 ? 1 + s_cnt[t] : 0;
+    const bool has_pz = t < a.K && a.kinfo[2 * t + 1] != 0;
+    double lo = key_double(s_min[t]), hi = key_double(s_max[t]);
+    if (lo == 0.0) lo = has_pz ? 0.0 : -0.0;
+    if (hi == 0.0) hi = has_pz ? 0.0 : -0.0;
+    thr2[2 * t] = lo;
+    thr2[2 * t + 1] = hi;
+  }
+  __syncthreads();
+}
+
+// CTA 0: header, lookup table, candidate records at their ids
+__device__ void pc_fast_common(const PcArgs& a, const PcShared& S, const FastLists& fl,
+                               const PlanHdr& H, uint8_t* smem) {
+  const int T = blockDim.x, t = threadIdx.x;
+  if (t < (int)(sizeof(PlanHdr) / 4))
+    reinterpret_cast<uint32_t*>(a.image)[t] = reinterpret_cast<const uint32_t*>(&H)[t];
+  if (H.magic != kPlanMagic) return;
+  uint16_t* lut = reinterpret_cast<uint16_t*>(a.image + H.lut_off);
+  for (int v = t; v < H.lut_n; v += T) {
+    int lo = 0, le = 0;
+    for (int b = 0; b < H.nB; ++b) {
+      lo += H.batch_vals[b] < v;
+      le += H.batch_vals[b] <= v;
+    }
+    lut[v] = (uint16_t)(lo | (le << 8));
+  }
+  const uint32_t* Rc = reinterpret_cast<const uint32_t*>(smem + kFRc);
+  const uint32_t* Cs = reinterpret_cast<const uint32_t*>(smem + kFCs);
+  double* rscore = reinterpret_cast<double*>(a.image + H.score_off);
+  double* rlat = reinterpret_cast<double*>(a.image + H.lat_off);
+  CandB* recb = reinterpret_cast<CandB*>(a.image + H.recb_off);
+  const int nl = 2 * a.nseg;
+  for (int u = t; u < fl.nc; u += T) {
+    const uint32_t r = Rc[u], sl = Cs[u];
+    const bool sS = r >> 31;
+    const uint32_t id = (sS ? a.rs_uid : a.rp_uid)[r & 0x7FFFFFFFu];
+    const int i = last_le(fl.coff, nl, u);
+    const PcSegDev sg = S.seg[i >> 1];
+    const int e = (sS ? a.cs_er[sl] : a.cp_er[sl]) & 0xFFFF;
+    rscore[id] = key_double(sS ? a.cs_key[sl] : a.cp_key[sl]);
+    rlat[id] = sS ? a.cs_lat[sl] : a.cp_lat[sl];
+    CandB b;
+    b.meta = (uint32_t)e | ((sS ? 0u : 1u) << 16) | ((uint32_t)sg.kind << 17);
+    b.batch = H.batch_vals[sg.lane];
+    recb[id] = b;
+  }
+}
+
+// rows [r0, r1) of kind k (`first`: also the bucket table); thresholds compacted by slot
+__device__ void pc_fast_kind(const PcArgs& a, const PcShared& S, const FastLists& fl,
+                             const PlanHdr& H, int k, int r0, int r1, bool first, uint8_t* smem,
+                             int* s_w) {
+  const int T = blockDim.x, t = threadIdx.x;
+  const KindDesc d = H.kd[k];
+  const int R = d.R;
+  if (R == 0 || H.magic != kPlanMagic) return;
+  const uint64_t* Kr = reinterpret_cast<const uint64_t*>(smem + kFKr);
+  const uint32_t* Rr = reinterpret_cast<const uint32_t*>(smem + kFRr);
+  double* thr = reinterpret_cast<double*>(smem + kFThr);
+  uint64_t* tmp = reinterpret_cast<uint64_t*>(smem + kFTmp);
+  uint8_t* occ = smem + kFOcc;  // representatives (pc_fast_layout_inputs)
+  uint8_t* work = smem + kFWork;
+  const int g0 = fl.roff[fl.klo[k]], g1 = fl.roff[fl.klo[k + 1]], nr = g1 - g0;
+  uint8_t* slot = work;  // slot occupancy (nr bytes)
+  for (int j = t; j < nr; j += T) slot[j] = 0;
+  __syncthreads();
+  for (int g = g0 + t; g < g1; g += T) {
+    if (!occ[g]) continue;
+    const uint32_t r = Rr[g];
+    const uint32_t q = ((r >> 31) ? a.rs_rank : a.rp_rank)[r & 0x7FFFFFFFu];
+    tmp[q] = Kr[g];
+    slot[q] = 1;
+  }
+  __syncthreads();
+  const bool has_pz = a.kinfo[2 * k + 1] != 0;
+  {
+    int o = 1;
+    for (int j0 = 0; j0 < nr; j0 += T) {
+      const int j = j0 + t;
+      const bool f = j < nr && slot[j];
+      int tot;
+      const int ex = pc_excl_sum(f ? 1 : 0, s_w, &tot);
+      if (f) {
+        double v = key_double(tmp[j]);
+        if (v == 0.0) v = has_pz ? 0.0 : -0.0;
+        thr[o + ex] = v;
+      }
+      o += tot;
+    }
+    if (t == 0) thr[0] = -INFINITY;
+    __syncthreads();
+  }
+  double* ithr = reinterpret_cast<double*>(a.image + d.thr_off);
+  for (int r = r0 + t; r < r1; r += T) ithr[r] = thr[r];
+  if (first) {  // bucket table: histogram + block scan (as sp_plan.cu k_fin_buckets)
+    uint32_t* s_h = reinterpret_cast<uint32_t*>(work);
+    uint32_t* bkt = reinterpret_cast<uint32_t*>(a.image + d.bkt_off);
+    const int nbk = (int)(d.nb1_shift & 0xFFFFu) + 1, shift = (int)(d.nb1_shift >> 16);
+    for (int b = t; b < nbk; b += T) s_h[b] = 0u;
+    __syncthreads();
+    for (int j = 1 + t; j < R; j += T) {
+      const uint32_t kk = (uint32_t)__double2hiint(thr[j]);
+      atomicAdd(&s_h[min((kk - d.kmin_hi) >> shift, (uint32_t)(nbk - 1))], 1u);
+    }
+    __syncthreads();
+    const int per = (nbk + T - 1) / T;
+    const int b0 = min(t * per, nbk), b1 = min(b0 + per, nbk);
+    int loc = 0;
+    for (int b = b0; b < b1; ++b) loc += (int)s_h[b];
+    int tot = 0;
+    int below = pc_excl_sum(loc, s_w, &tot);
+    for (int b = b0; b < b1; ++b) {
+      const uint32_t cc = s_h[b];
+      bkt[b] = (uint32_t)below | (cc << 16);
+      below += (int)cc;
+    }
+    __syncthreads();
+  }
+  if (r1 <= r0) return;
+  // lane lists of the kind in the staged record keys: lane b = list pair of its segment
+  __shared__ int s_pl[kMaxB][4];
+  if (t < kMaxB) s_pl[t][0] = s_pl[t][1] = s_pl[t][2] = s_pl[t][3] = 0;
+  __syncthreads();
+  if (t < a.seg_lo[k + 1] - a.seg_lo[k]) {
+    const int sgi = a.seg_lo[k] + t;
+    const int b = S.seg[sgi].lane;
+    s_pl[b][0] = fl.roff[2 * sgi];
+    s_pl[b][1] = fl.roff[2 * sgi + 1] - fl.roff[2 * sgi];
+    s_pl[b][2] = fl.roff[2 * sgi + 1];
+    s_pl[b][3] = fl.roff[2 * sgi + 2] - fl.roff[2 * sgi + 1];
+  }
+  __syncthreads();
+  const int nB = H.nB;
+  uint32_t* lv = reinterpret_cast<uint32_t*>(work);  // rows x nB lane values, by chunks
+  const int rows = r1 - r0;
+  const int rc = max(1, 8192 / nB);
+  for (int c0 = 0; c0 < rows; c0 += rc) {
+    const int nrw = min(rc, rows - c0);
+    for (int j = t; j < nrw * nB; j += T) {
+      const int rl = j / nB, b = j - rl * nB;
+      const int r = r0 + c0 + rl;
+      // x: canonical key of the row threshold (row 0: below every latency)
+      const uint64_t x = r == 0 ? 0ull : canon(okey(thr[r]));
+      uint32_t v = kInfPc;
+      const int pb = s_pl[b][0], np = s_pl[b][1], sb = s_pl[b][2], ns = s_pl[b][3];
+      int lo = 0, hi = np;  // #P-records with lat <= x
+      if (r > 0)
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (Kr[pb + mid] <= x) lo = mid + 1; else hi = mid;
+        }
+      if (lo > 0) {
+        const uint32_t rr = Rr[pb + lo - 1];
+        v = a.rp_uid[rr & 0x7FFFFFFFu];
+      }
+      lo = 0;
+      hi = ns;  // first S-record with lat > x
+      if (r > 0)
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (Kr[sb + mid] <= x) lo = mid + 1; else hi = mid;
+        }
+      if (lo < ns) {
+        const uint32_t rr = Rr[sb + lo];
+        v = min(v, a.rs_uid[rr & 0x7FFFFFFFu]);
+      }
+      lv[j] = v;
+    }
+    __syncthreads();
+    for (int j = t; j < nrw * nB; j += T) {
+      const int rl = j / nB, lo = j - rl * nB;
+      uint16_t* out = reinterpret_cast<uint16_t*>(a.image + d.rows_off +
+                                                  (size_t)(r0 + c0 + rl) * H.row_stride);
+      const int base = lo * nB - ((lo * (lo - 1)) >> 1);
+      uint32_t m = kInfPc;
+      for (int hi = lo; hi < nB; ++hi) {
+        m = min(m, lv[rl * nB + hi]);
+        out[base + hi - lo] = m == kInfPc ? kNone16 : (uint16_t)m;
+      }
+    }
+    __syncthreads();
+  }
 }
 
 // ---- phase 3 ---------------------------------------------------------------------------------
@@ -900,10 +1507,10 @@ __device__ void pc_write_kind(const PcArgs& a, const PcShared& S, const PlanHdr&
   const int ext = a.base[k] + k;
   const int s0 = a.seg_lo[k], s1 = a.seg_lo[k + 1];
   const bool staged = ks.staged;
-  double* L = reinterpret_cast<double*>(smem);
-  const double* thr = staged ? L + kPcStageMax : a.thr + ext;
-  uint32_t* U = reinterpret_cast<uint32_t*>(const_cast<double*>(L + 2 * kPcStageMax + 1) + 1);
-  uint8_t* work = reinterpret_cast<uint8_t*>(U + kPcStageMax);
+  double* L = reinterpret_cast<double*>(smem + kSmL);
+  const double* thr = staged ? reinterpret_cast<const double*>(smem + kSmThr) : a.thr + ext;
+  uint32_t* U = reinterpret_cast<uint32_t*>(smem + kSmU);
+  uint8_t* work = smem + kSmWork;
   double* ithr = reinterpret_cast<double*>(a.image + d.thr_off);
   for (int r = r0 + t; r < r1; r += T) ithr[r] = thr[r];
   if (first) {  // bucket table: histogram + block scan (as sp_plan.cu k_fin_buckets)
@@ -932,14 +1539,20 @@ __device__ void pc_write_kind(const PcArgs& a, const PcShared& S, const PlanHdr&
   }
   if (r1 <= r0) return;
   const int nB = H.nB;
-  if (staged) {  // the candidate ids of the staged records (written by CTA 0 in phase 2)
-    for (int s = s0; s < s1; ++s) {
-      const int b = S.seg[s].lane, off = S.seg[s].off;
-      for (int j = t; j < ks.lane[b][1]; j += T) U[ks.lane[b][0] + j] = a.rp_uid[off + j];
-      for (int j = t; j < ks.lane[b][3]; j += T) U[ks.lane[b][2] + j] = a.rs_uid[off + j];
+  if (staged) {  // the candidate ids of the staged records (written in phase 2)
+    for (int g = t; g < ks.nr; g += T) {
+      int b = 0;  // record g: lane b's P list or S list
+      while (!(g >= ks.lane[b][0] && g < ks.lane[b][2] + ks.lane[b][3]) ||
+             ks.lane[b][1] + ks.lane[b][3] == 0)
+        ++b;
+      int s = s0;
+      while (S.seg[s].lane != b) ++s;
+      const int off = S.seg[s].off;
+      U[g] = g < ks.lane[b][2] ? a.rp_uid[off + g - ks.lane[b][0]] : a.rs_uid[off + g - ks.lane[b][2]];
     }
     __syncthreads();
   }
+  PC_STAMP(17);
   __shared__ int s_seg_of[kMaxB];
   if (t < kMaxB) s_seg_of[t] = -1;
   __syncthreads();
@@ -1018,6 +1631,7 @@ __global__ void __launch_bounds__(kPcThreads, 1) k_plan_cluster(const __grid_con
   uint64_t tm[6];
   tm[0] = gtimer();
   const long long ck0 = clock64();
+  if (threadIdx.x < 32) pc_stamps()[threadIdx.x] = tm[0];
   if (threadIdx.x < 2 * kMaxKinds && c == 0) a.kinfo[threadIdx.x] = 0;
   if (threadIdx.x < a.nseg) S.seg[threadIdx.x] = a.seg[threadIdx.x];
   cluster_barrier();
@@ -1028,14 +1642,20 @@ __global__ void __launch_bounds__(kPcThreads, 1) k_plan_cluster(const __grid_con
   tm[3] = gtimer();
   for (int i = threadIdx.x; i < 4 * a.nseg; i += blockDim.x) S.cnt[i] = a.seg_cnt[i];
   __syncthreads();
-  // CTA 0: the candidate order.  CTAs 1..C-1 are dealt round-robin to the kinds (w % K); every
-  // CTA of a kind stages the kind's records and thresholds, the kind's first publishes them.
-  // With fewer workers than kinds a worker handles several kinds, without staging.
+  // phase 2: every CTA ranks a share of the candidates (merge form; CTA 0 falls back to a sort
+  // when it does not apply); CTAs 1..C-1 are dealt round-robin to the kinds (w % K), every CTA
+  // of a kind stages the kind's records and thresholds, the kind's first publishes them.  With
+  // fewer workers than kinds a worker handles several kinds, without staging.
   const int nw = C > 1 ? C - 1 : 1, w = C > 1 ? c - 1 : 0;
   const bool one_kind = nw >= a.K;
-  if (c == 0) pc_candidates(a, S, smem, s_w);
+  __shared__ CandLists s_cl;
+  __shared__ FastLists s_fl;
+  const bool fast = pc_fast_phase2(a, S, s_fl, smem, s_w);
+  if (!fast) {
+    if (!pc_cand_merge(a, S, s_cl, smem, s_w) && c == 0) pc_candidates(a, S, smem, s_w);
+  }
   const uint64_t tmc = gtimer();
-  if (C == 1 || c > 0) {
+  if (!fast && (C == 1 || c > 0)) {
     if (one_kind) {
       if (w < nw) pc_kind_stage(a, S, w % a.K, w < a.K, s_ks, smem, s_w);
     } else {
@@ -1049,17 +1669,27 @@ __global__ void __launch_bounds__(kPcThreads, 1) k_plan_cluster(const __grid_con
   const uint64_t tmk = gtimer();
   cluster_barrier();
   tm[4] = gtimer();
-  {  // the layout inputs loaded in parallel (rows per kind, two thresholds per kind, counts)
+  {  // layout inputs: rows per kind, first / last threshold per kind, candidate counts
     __shared__ int32_t s_rows[kMaxKinds], s_nc[2];
     __shared__ double s_thr[kMaxKinds + 1][2];
-    const int k = threadIdx.x;
-    if (k < kMaxKinds) s_rows[k] = k < a.K ? a.kinfo[2 * k] : 0;
-    if (k < 2) s_nc[k] = a.kinfo[16 + k];
-    __syncthreads();
-    if (k < a.K && s_rows[k] >= 2) {
-      const int ext = a.base[k] + k;
-      s_thr[k][0] = a.thr[ext + 1];
-      s_thr[k][1] = a.thr[ext + s_rows[k] - 1];
+    if (fast) {
+      pc_fast_layout_inputs(a, s_fl, s_rows, &s_thr[0][0], smem);
+      if (threadIdx.x == 0) {
+        int ncp = 0;
+        for (int sgi = 0; sgi < a.nseg; ++sgi) ncp += S.cnt[4 * sgi + 2];
+        s_nc[0] = ncp;
+        s_nc[1] = s_fl.nc - ncp;
+      }
+    } else {
+      const int k = threadIdx.x;
+      if (k < kMaxKinds) s_rows[k] = k < a.K ? a.kinfo[2 * k] : 0;
+      if (k < 2) s_nc[k] = a.kinfo[16 + k];
+      __syncthreads();
+      if (k < a.K && s_rows[k] >= 2) {
+        const int ext = a.base[k] + k;
+        s_thr[k][0] = a.thr[ext + 1];
+        s_thr[k][1] = a.thr[ext + s_rows[k] - 1];
+      }
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -1069,6 +1699,24 @@ __global__ void __launch_bounds__(kPcThreads, 1) k_plan_cluster(const __grid_con
     __syncthreads();
   }
   const PlanHdr& H = s_hdr;
+  if (fast) {
+    if (c == 0) pc_fast_common(a, S, s_fl, H, smem);
+    if (C == 1 || c > 0) {
+      for (int k = 0; k < a.K; ++k) {
+        int slot = -1, cnt = 1;
+        if (one_kind) {
+          cnt = nw / a.K + (k < nw % a.K ? 1 : 0);
+          if (w % a.K == k) slot = w / a.K;
+        } else if (k % nw == w) {
+          slot = 0;
+        }
+        if (slot < 0) continue;
+        const int R = H.kd[k].R;
+        const int r0 = (int)((int64_t)R * slot / cnt), r1 = (int)((int64_t)R * (slot + 1) / cnt);
+        pc_fast_kind(a, S, s_fl, H, k, r0, r1, slot == 0, smem, s_w);
+      }
+    }
+  } else {
   if (c == 0) pc_write_common(a, H);
   if (C == 1 || c > 0) {
     for (int k = 0; k < a.K; ++k) {
@@ -1104,10 +1752,21 @@ __global__ void __launch_bounds__(kPcThreads, 1) k_plan_cluster(const __grid_con
       pc_write_kind(a, S, H, k, r0, r1, slot == 0, s_ks, smem, s_w);
     }
   }
+  }
   tm[5] = gtimer();
   const long long ck1 = clock64();
   if (a.debug && threadIdx.x == 0 && c == 0)
     printf("pc clock %.0f MHz\n", 1e3 * (double)(ck1 - ck0) / (double)(tm[5] - tm[0]));
+  if (a.debug && threadIdx.x == 0 && c < 3) {
+    uint64_t* st = pc_stamps();
+    printf("pc cta %d stamps: s1 %lld s2 %lld s3 %lld s4 %lld s6 %lld | k8 %lld k9 %lld k10 %lld | c13 %lld c14 %lld | w17 %lld\n", c,
+           (long long)(st[1] - tm[0]), (long long)(st[2] - tm[0]), (long long)(st[3] - tm[0]),
+           (long long)(st[4] - tm[0]), (long long)(st[6] - tm[0]), (long long)(st[8] - tm[0]),
+           (long long)(st[9] - tm[0]), (long long)(st[10] - tm[0]), (long long)(st[13] - tm[0]),
+           (long long)(st[14] - tm[0]), (long long)(st[17] - tm[0]));
+    printf("pc cta %d c15 %lld f20 %lld f21 %lld f22 %lld\n", c, (long long)(st[15] - tm[0]),
+           (long long)(st[20] - tm[0]), (long long)(st[21] - tm[0]), (long long)(st[22] - tm[0]));
+  }
   if (a.debug && threadIdx.x == 0)
     printf("pc cta %d: p2 cand %llu kind %llu | init %llu seg %llu bar1 %llu p2 %llu p3 %llu ns\n", c,
            (unsigned long long)(tmc - tm[3]), (unsigned long long)(tmk - tmc),
@@ -1152,7 +1811,7 @@ int plan_cluster_prepare(sp_table* t, const int32_t* kind, const int32_t* bidx) 
   SP_CUDA(cudaMemcpy(t->pc_seg_ent, ent.data(), sizeof(int32_t) * M, cudaMemcpyHostToDevice));
   int n2 = 1;
   while (n2 < 2 * M) n2 <<= 1;
-  const size_t bytes = (size_t)M * (2 * 8 + 2 * 4 + 2 * (8 * 4 + 4 * 2)) + 16u * segs.size() + 128 +
+  const size_t bytes = (size_t)M * (2 * 8 + 6 * 4 + 2 * (8 * 4 + 4 * 2)) + 16u * segs.size() + 128 +
                        48u * M + 4 * sizeof(double) * n2 + sizeof(int32_t) * n2 + 64 * 16;
   SP_CUDA(cudaMalloc(&t->pc_scratch, bytes));
   t->pc_ok = true;
@@ -1195,6 +1854,10 @@ int plan_cluster_launch(sp_ctx* ctx, sp_table* t, Plan& p, int W, const PlanHdr&
   a.rs_lat = reinterpret_cast<double*>(take(sizeof(double) * M));
   a.rp_uid = reinterpret_cast<uint32_t*>(take(4u * M));
   a.rs_uid = reinterpret_cast<uint32_t*>(take(4u * M));
+  a.rp_rank = reinterpret_cast<uint32_t*>(take(4u * M));
+  a.rs_rank = reinterpret_cast<uint32_t*>(take(4u * M));
+  a.rp_nrep = reinterpret_cast<uint32_t*>(take(4u * M));
+  a.rs_nrep = reinterpret_cast<uint32_t*>(take(4u * M));
   a.cp_key = reinterpret_cast<uint64_t*>(take(8u * M));
   a.cs_key = reinterpret_cast<uint64_t*>(take(8u * M));
   a.cp_ck = reinterpret_cast<uint64_t*>(take(8u * M));
@@ -1223,10 +1886,9 @@ int plan_cluster_launch(sp_ctx* ctx, sp_table* t, Plan& p, int W, const PlanHdr&
   // shared memory: the largest phase (segment: 60 B per slot; candidates 16 B; thresholds 8 B
   // per record in the shared-memory fallback; rows 64 KB)
   const int es = t->pc_max_seg > kPcThreads ? 2 : 1;
-  const size_t smem =
-      std::max(std::max((size_t)es * kPcThreads * 60, (size_t)2 * kPcThreads * 36),
-               std::max((size_t)2 * kPcMaxKind * 8,
-                        (size_t)kPcStageMax * (8 + 8 + 4) + 64 + (size_t)kPcRowChunk * 2));
+  const size_t smem = std::max(std::max((size_t)es * kPcThreads * 60, (size_t)2 * kPcThreads * 36),
+                               std::max(std::max((size_t)2 * kPcMaxKind * 8, (size_t)kSmEnd),
+                                        (size_t)kFEnd));
   auto kern = es == 1 ? k_plan_cluster<1> : k_plan_cluster<2>;
   static uint64_t attr[2] = {0, 0};
   static int csize[64] = {};
