@@ -492,25 +492,31 @@ def run_c5(args):
            (("idx", torch.int32), ("code", torch.int32), ("fill", torch.int32),
             ("obj", torch.float64), ("slack", torch.float64), ("wait", torch.float64))}
     obs_idx = torch.empty(Bl, dtype=torch.int32, device=dev)
-    neg1 = torch.full((Bl,), -1, dtype=torch.int32, device=dev)
+    obs_val = torch.empty(Bl, dtype=torch.float64, device=dev)
     stream_idx = torch.empty(N, dtype=torch.int32, device=dev)   # the folded stream, kept for the check
     stream_obs = torch.empty(N, dtype=torch.float64, device=dev)
     alpha = 100.0
 
     def online_batch(tab, bt):
         # decide this rank's shard of batch bt against the batch-start table; the assigned
-        # configurations run: obs = truth(config, items=fill) * exp(N(0, 0.3)) (delayed / None
-        # decisions produce no observation, idx = -1); every rank folds the whole batch
+        # configurations run (simulated backend, one kernel): obs = truth(config, items=fill) *
+        # exp(N(0, 0.3)); delayed / None decisions produce no observation (idx = -1); every rank
+        # folds the whole batch
         s = slice(bt * B + a, bt * B + b)
         tab.select_batch(d["slack"][s], alpha, d["avail"][s], upstream_supply=d["supply"][s],
                          min_batch=d["mb"][s], flags=d["flags"][s], out=out)
-        torch.where((out["code"] & 3) == 1, out["idx"], neg1, out=obs_idx)
-        j = obs_idx.clamp(min=0)
-        obs = (base[j] + per_item[j] * out["fill"].to(torch.float64)) * noise[s]
-        f_idx, f_obs = gather_observations(obs_idx, obs, B) if world > 1 else (obs_idx, obs)
-        stream_idx[bt * B:(bt + 1) * B].copy_(f_idx)
-        stream_obs[bt * B:(bt + 1) * B].copy_(f_obs)
-        sp.fold_observations([tab], None, f_idx, f_obs, beta=0.5, dfp_count=10, sync_host=False)
+        g = slice(bt * B, (bt + 1) * B)
+        if world > 1:
+            sp.simulate_observations(out, base, noise[s], truth_per_item=per_item,
+                                     out=(obs_idx, obs_val))
+            f_idx, f_obs = gather_observations(obs_idx, obs_val, B)
+            stream_idx[g].copy_(f_idx)
+            stream_obs[g].copy_(f_obs)
+        else:  # the records land straight in the run's observation stream
+            sp.simulate_observations(out, base, noise[s], truth_per_item=per_item,
+                                     out=(stream_idx[g], stream_obs[g]))
+        sp.fold_observations([tab], None, stream_idx[g], stream_obs[g], beta=0.5, dfp_count=10,
+                             sync_host=False)
 
     # warm-up on a throw-away copy of the table (module loading, scratch allocation, plan-build
     # graph capture); the timed run starts from the untouched table

@@ -271,6 +271,17 @@ int sp_speculate_batch(sp_ctx* ctx, int32_t n_tables, sp_table* const* tables, d
                        double* out_slack, double* out_obj, int32_t* out_n, int32_t* out_delay_idx,
                        double* out_delay_wait, int32_t mem);
 
+/* ---- simulated backend: observation records of a decision batch (backend.py:36-58) ------ */
+/* Device buffers, stream-ordered.  For decision i: when (code[i] & 3) == SP_DEC_ASSIGN the
+ * configuration runs and obs_idx[i] = idx[i], obs[i] = (truth_base[idx] +
+ * truth_per_item[idx] * fill[i]) * noise[i] (draw_actual_latency with the caller's
+ * multiplicative noise exp(N(0, sigma))); otherwise obs_idx[i] = -1 (nothing runs this batch).
+ * truth_per_item may be NULL (no per-item term).  The records feed sp_feedback_fold directly. */
+int sp_simulate_observations(sp_ctx* ctx, int32_t N, const int32_t* code, const int32_t* idx,
+                             const int32_t* fill, const double* truth_base,
+                             const double* truth_per_item, const double* noise, int32_t* obs_idx,
+                             double* obs);
+
 /* ---- single-process multi-GPU fan-out (SURVEY.md §8(b) Threading, §8(e)) ------------------ */
 /* The reference engine is one single-threaded process (configurator.py:368-373); a drop-in
  * that uses the GPUs of a box fans out inside the library.  A group owns one context (device

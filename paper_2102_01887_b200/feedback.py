@@ -50,6 +50,28 @@ def fold_observations(tables: Sequence, op, idx, obs, *, beta: float = 0.5,
                 t.sync_from_device()
 
 
+def simulate_observations(decisions, truth_base, noise, *, truth_per_item=None, out=None, ctx=None):
+    """Observation records of a decision batch from the simulated backend (backend.py:36-58):
+    assignments run, obs = (truth_base[idx] + truth_per_item[idx] * fill) * noise; delayed / None
+    decisions give idx -1.  ``decisions``: the device output dict of ``select_batch``
+    (``code``, ``idx``, ``fill``); torch CUDA tensors, stream-ordered.  Returns (obs_idx, obs)."""
+    import torch
+
+    from ._lib import get_context
+
+    ctx = ctx or get_context(decisions["code"].device.index)
+    n = int(decisions["code"].shape[0])
+    if out is None:
+        out = (torch.empty(n, dtype=torch.int32, device=decisions["code"].device),
+               torch.empty(n, dtype=torch.float64, device=decisions["code"].device))
+    oi, ob = out
+    check(ctx.lib.sp_simulate_observations(
+        ctx.handle, n, ptr(decisions["code"]), ptr(decisions["idx"]), ptr(decisions.get("fill")),
+        ptr(truth_base), ptr(truth_per_item), ptr(noise), ptr(oi), ptr(ob)),
+        "sp_simulate_observations")
+    return oi, ob
+
+
 def table_counters(table) -> tuple[int, np.ndarray]:
     """(completed_ref, per-entry observation counts) of a device table."""
     ctx = table._ctx
