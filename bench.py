@@ -321,6 +321,28 @@ def our_arm(args) -> None:
     evals = args.steps * N * M * world
     value = evals / t_max
 
+    # ---- plan-inclusive: every step first rebuilds its alpha's plan (SURVEY.md §8(d) config 2,
+    # "alpha in {0, 1, 100, 1000}, one launch each" with nothing precomputed) ----
+    for i in range(2):
+        table.invalidate_plans()
+        step(i)
+    torch.cuda.synchronize(dev)
+    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    lp0 = ctx.launch_count
+    torch.cuda._sleep(int(2e6 + 4e5 * args.steps))
+    p0.record(stream)
+    for i in range(args.steps):
+        table.invalidate_plans()
+        step(args.warmup + i)
+    p1.record(stream)
+    torch.cuda.synchronize(dev)
+    launches_pi = ctx.launch_count - lp0
+    t_pi = p0.elapsed_time(p1) / 1e3
+    if world > 1:
+        tt = torch.tensor([t_pi], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t_pi = float(tt.item())
+
     # ---- the same steps, one at a time: L2 flushed before, an event pair around each ----
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     torch.cuda.synchronize(dev)
@@ -392,7 +414,16 @@ def our_arm(args) -> None:
                                             if any(alpha_of(args.warmup + k) == a for k in range(args.steps))},
                                "evals_per_s": N * M * world / (statistics.median(step_ms) / 1e3)},
         "plan": {"build_ms_per_alpha": plan_ms, "bytes": plan_bytes,
-                 "note": "staircase plan built once per (profile version, alpha); table static in config 2"},
+                 "note": "value / roofline: staircase plan built once per (profile version, alpha), "
+                         "table static in config 2; value_incl_plan: every step rebuilds its plan"},
+        "value_incl_plan": evals / t_pi,
+        "roofline_incl_plan": {"bound": "hbm", "achieved": alg_bytes / (t_pi / args.steps) / 1e9,
+                               "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                               "frac": alg_bytes / (t_pi / args.steps) / 1e9 / peaks["hbm_gbs"],
+                               "ms_per_step": 1e3 * t_pi / args.steps,
+                               "gpu_launches": launches_pi,
+                               "kernels": "k_plan_cluster (one 16-CTA cluster: the whole plan) + "
+                                          "the decision kernel, per step"},
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -96,6 +96,9 @@ int sp_table_get_latency(sp_ctx* ctx, sp_table* t, double* out_lat);
 /* Build (or reuse) the per-alpha decision plan: cost/costpen precompute + staircase
  * index.  Called implicitly by the select entry points. */
 int sp_table_prepare(sp_ctx* ctx, sp_table* t, double alpha);
+/* Mark every plan of the table stale (as a latency change does) without touching the table:
+ * the next select / prepare rebuilds its plan (bench: plan-inclusive timing). */
+int sp_table_invalidate(sp_ctx* ctx, sp_table* t);
 /* 1 when the table's staircase plan is available (<= 16 distinct batch sizes, M < 32767). */
 int sp_table_plan_supported(const sp_table* t);
 /* Plan byte size for alpha after sp_table_prepare (synchronises); for DESIGN/bench. */

@@ -213,6 +213,10 @@ class OpTable:
     def prepare(self, alpha: float) -> None:
         check(self._ctx.lib.sp_table_prepare(self._ctx.handle, self._handle, float(alpha)))
 
+    def invalidate_plans(self) -> None:
+        """Every plan of the table is rebuilt by its next use (as after a latency change)."""
+        check(self._ctx.lib.sp_table_invalidate(self._ctx.handle, self._handle))
+
     def plan_supported(self) -> bool:
         return bool(self._ctx.lib.sp_table_plan_supported(self._handle))
 

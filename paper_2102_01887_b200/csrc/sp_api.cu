@@ -361,6 +361,12 @@ int sp_table_get_latency(sp_ctx* ctx, sp_table* t, double* out_lat) {
   return SP_OK;
 }
 
+int sp_table_invalidate(sp_ctx* ctx, sp_table* t) {
+  if (!ctx || !t) return fail(SP_E_INVALID, "invalidate: null argument");
+  t->version++;  // every plan of the table is rebuilt by its next use
+  return SP_OK;
+}
+
 int sp_table_prepare(sp_ctx* ctx, sp_table* t, double alpha) {
   DeviceScope _dev_scope(ctx ? ctx->device : -1);
   if (!ctx || !t) return fail(SP_E_INVALID, "prepare: null argument");

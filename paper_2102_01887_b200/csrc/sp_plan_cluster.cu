@@ -132,8 +132,9 @@ __device__ int pc_excl_sum(int v, int* s_w, int* total) {
   }
   if (lane == 31) s_w[w] = x;
   __syncthreads();
+  const int nw = blockDim.x >> 5;
   if (w == 0) {
-    int y = s_w[lane];
+    int y = lane < nw ? s_w[lane] : 0;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
       const int z = __shfl_up_sync(0xffffffffu, y, off);
@@ -143,7 +144,7 @@ __device__ int pc_excl_sum(int v, int* s_w, int* total) {
   }
   __syncthreads();
   const int r = (w ? s_w[w - 1] : 0) + x - v;
-  *total = s_w[31];
+  *total = s_w[nw - 1];
   __syncthreads();
   return r;
 }
@@ -167,7 +168,7 @@ __device__ int pc_excl_best(int v, bool rev, int* s_w, Better better) {
   if (lane == 31) s_w[w] = x;
   __syncthreads();
   if (threadIdx.x < 32) {
-    int y = s_w[threadIdx.x];
+    int y = (int)threadIdx.x < (int)(blockDim.x >> 5) ? s_w[threadIdx.x] : -1;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
       const int z = __shfl_up_sync(0xffffffffu, y, off);
@@ -272,8 +273,9 @@ __device__ int blk_best(int v, bool rev, int* s_w, int* total, Better better) {
   const int ex_in = rev ? __shfl_down_sync(0xffffffffu, x, 1) : __shfl_up_sync(0xffffffffu, x, 1);
   if (lane == 31) s_w[w] = x;
   __syncthreads();
+  const int nw = blockDim.x >> 5;
   if (threadIdx.x < 32) {
-    int y = s_w[threadIdx.x];
+    int y = (int)threadIdx.x < nw ? s_w[threadIdx.x] : -1;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
       const int z = __shfl_up_sync(0xffffffffu, y, off);
@@ -284,7 +286,7 @@ __device__ int blk_best(int v, bool rev, int* s_w, int* total, Better better) {
   __syncthreads();
   int ex = lane == 0 ? -1 : ex_in;
   if (w > 0) ex = better(s_w[32 + w - 1], ex);
-  *total = s_w[63];
+  *total = s_w[32 + nw - 1];
   __syncthreads();
   return ex;
 }
@@ -483,17 +485,19 @@ __device__ void pc_segment(const PcArgs& a, const PcShared& S, int s, uint8_t* s
   if (__syncthreads_or(pos_zero) && t == 0) atomicOr(&a.kinfo[2 * sg.kind + 1], 1);
   PC_STAMP(3);
   // Key1 (the r1 order: cost key, res, id_rank) and Key2 (costpen key, then Key1)
-  auto less1 = [&](int x, int y) {
+  // comparators capture the shared-memory pointers by value (a by-reference closure can leave
+  // them in local memory)
+  auto less1 = [=](int x, int y) {
     if (pck[x] != pck[y]) return pck[x] < pck[y];
     if (pres[x] != pres[y]) return pres[x] < pres[y];
     return pidr[x] < pidr[y];
   };
-  auto less2 = [&](int x, int y) {
+  auto less2 = [=](int x, int y) {
     if (pcpk[x] != pcpk[y]) return pcpk[x] < pcpk[y];
     return less1(x, y);
   };
-  auto best1 = [&](int x, int y) { return x < 0 ? y : (y < 0 ? x : (less1(y, x) ? y : x)); };
-  auto best2 = [&](int x, int y) { return x < 0 ? y : (y < 0 ? x : (less2(y, x) ? y : x)); };
+  auto best1 = [=](int x, int y) { return x < 0 ? y : (y < 0 ? x : (less1(y, x) ? y : x)); };
+  auto best2 = [=](int x, int y) { return x < 0 ? y : (y < 0 ? x : (less2(y, x) ? y : x)); };
   // 3. P-records (strictly below every earlier position's Key1), S-records (strictly below
   //    every later position's Key2); positions t + q*T, chunks in q order
   bool fP[E], fS[E];
@@ -1174,14 +1178,15 @@ __device__ bool pc_fast_phase2(const PcArgs& a, const PcShared& S, FastLists& fl
   }
   PC_STAMP(21);
   // candidate entries for the rare equal-score comparisons
-  auto cent = [&](int u) {
+  const PcArgs* ap = &a;
+  auto cent = [=](int u) {
     const uint32_t sl = Cs[u];
-    return (int)(((Rc[u] >> 31) ? a.cs_er[sl] : a.cp_er[sl]) & 0xFFFF);
+    return (int)(((Rc[u] >> 31) ? ap->cs_er[sl] : ap->cp_er[sl]) & 0xFFFF);
   };
-  auto prec = [&](int x, int y) {  // candidate x precedes candidate y in the unified order
+  auto prec = [=](int x, int y) {  // candidate x precedes candidate y in the unified order
     const uint64_t kx = Kc[x], ky = Kc[y];
     if (kx != ky) return kx < ky;
-    return cand_tie_less(a, cent(x), cent(y), Rc[x] >> 31, Rc[y] >> 31);
+    return cand_tie_less(*ap, cent(x), cent(y), Rc[x] >> 31, Rc[y] >> 31);
   };
   // per-CTA partial counts in shared memory (the threshold area is free until phase 3), added
   // to the global words once per touched item
@@ -1885,15 +1890,15 @@ int plan_cluster_launch(sp_ctx* ctx, sp_table* t, Plan& p, int W, const PlanHdr&
   a.debug = getenv("SP_PC_DEBUG") != nullptr;
   // shared memory: the largest phase (segment: 60 B per slot; candidates 16 B; thresholds 8 B
   // per record in the shared-memory fallback; rows 64 KB)
-  const int es = t->pc_max_seg > kPcThreads ? 2 : 1;
+  const int es = t->pc_max_seg > 2 * kPcThreads ? 4 : (t->pc_max_seg > kPcThreads ? 2 : 1);
   const size_t smem = std::max(std::max((size_t)es * kPcThreads * 60, (size_t)2 * kPcThreads * 36),
                                std::max(std::max((size_t)2 * kPcMaxKind * 8, (size_t)kSmEnd),
                                         (size_t)kFEnd));
-  auto kern = es == 1 ? k_plan_cluster<1> : k_plan_cluster<2>;
-  static uint64_t attr[2] = {0, 0};
+  auto kern = es == 1 ? k_plan_cluster<1> : (es == 2 ? k_plan_cluster<2> : k_plan_cluster<4>);
+  static uint64_t attr[3] = {0, 0, 0};
   static int csize[64] = {};
   const int dev = cur_device();
-  if (attr_once(attr[es - 1])) {
+  if (attr_once(attr[es == 4 ? 2 : es - 1])) {
     SP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     SP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   }
