@@ -77,6 +77,144 @@ def _peaks():
     return float(json.loads(p.read_text())["hbm_gbs"]) if p.exists() else 6650.0
 
 
+# ---- c1: the AMBER drop-in, one call at a time ----------------------------------------------
+
+C1_REFERENCE_DECISIONS_PER_S = 18468.0  # /root/reference/pkg/test_output.txt:171 (whole engine)
+
+
+def _c1_calls():
+    with np.load(ROOT / "tests" / "golden" / "amber_trace.npz") as z:
+        d = {k: z[k] for k in z.files}
+    meta = json.loads(bytes(d["meta_json"]).decode())
+    return d, meta
+
+
+def _c1_replay_cpu(d, meta, n):
+    """The reference's per-call path on the CPU: the numpy restatement of OpTable.select /
+    affinity / set_latency (oracle/optable.py), single-threaded like the reference engine."""
+    import math
+
+    from oracle import commit as oc
+    from oracle import optable
+
+    tabs = oc.amber_tables(meta)
+    kind, op, slack, alpha = d["kind"], d["op"], d["slack"], d["alpha"]
+    t0 = time.perf_counter()
+    for i in range(n):
+        t = tabs[op[i]]
+        k = kind[i]
+        if k == 2:
+            t.lat[int(d["lat_idx"][i])] = float(d["lat_val"][i])
+        elif k == 1:
+            optable.affinity(t, int(d["aff_kind"][i]), np.nan_to_num(slack[i]), float(alpha[i]))
+        else:
+            fl = int(d["flags"][i])
+            optable.select(t, np.nan_to_num(slack[i]), float(alpha[i]), int(d["avail"][i]),
+                           allow_delay=bool(fl & 1), upstream_supply=int(d["supply"][i]),
+                           excluded_mask=(fl >> 8) & 0xFF, min_batch=int(d["min_batch"][i]))
+    return time.perf_counter() - t0
+
+
+def run_c1(args):
+    """BASELINE config 1: every OpTable call the reference engine made on the AMBER scenario at
+    the 50% target (43,859 select, 9,962 affinity, 7,726 set_latency, in call order), replayed
+    one at a time through the drop-in object API — the path the unmodified reference engine
+    drives — on the B200; every result is compared with the recorded reference result.  Wall
+    clock (the per-call host work is part of the path)."""
+    import math
+
+    import torch
+
+    import paper_2102_01887_b200 as sp
+
+    rank, world, local = _dist(torch)
+    if rank != 0:
+        return
+    d, meta = _c1_calls()
+    kinds = meta["kinds"]
+    n = len(d["kind"])
+    bits = lambda x: np.float64(x).view(np.uint64)
+
+    def replay(check):
+        tabs = _amber_tables(sp, meta)
+        kind, op, slack, alpha = d["kind"], d["op"], d["slack"], d["alpha"]
+        sdicts = [{k: float(v) for k, v in zip(kinds, row) if not math.isnan(v)} for row in slack]
+        bad = 0
+        ctx = sp.get_context(local)
+        l0 = ctx.launch_count
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for i in range(n):
+            t = tabs[op[i]]
+            k = kind[i]
+            if k == 2:
+                t.set_latency(int(d["lat_idx"][i]), float(d["lat_val"][i]))
+            elif k == 1:
+                a = t.affinity(kinds[d["aff_kind"][i]], sdicts[i], float(alpha[i]))
+                if check:
+                    exp = d["r_obj"][i]
+                    bad += not ((a is None and math.isnan(exp)) or (a is not None and bits(a) == bits(exp)))
+            else:
+                fl = int(d["flags"][i])
+                ex = frozenset(kk for j, kk in enumerate(kinds) if (fl >> (8 + j)) & 1)
+                dec = t.select(sdicts[i], float(alpha[i]), int(d["avail"][i]), allow_delay=bool(fl & 1),
+                               upstream_supply=int(d["supply"][i]), excluded_kinds=ex,
+                               min_batch=int(d["min_batch"][i]))
+                if check:
+                    rc = d["r_code"][i]
+                    if rc == 0:
+                        bad += dec is not None
+                    else:
+                        bad += not (dec is not None and dec.entry_index == d["r_idx"][i]
+                                    and dec.fill == d["r_fill"][i]
+                                    and dec.kind == ("delay" if rc == 2 else "assign")
+                                    and bits(dec.objective_value) == bits(d["r_obj"][i])
+                                    and bits(dec.slack_s) == bits(d["r_slack"][i])
+                                    and bits(dec.wait_budget_s) == bits(d["r_wait"][i]))
+        dt = time.perf_counter() - t0
+        launches = ctx.launch_count - l0
+        for t in tabs:
+            t.close()
+        return dt, bad, launches
+
+    replay(False)  # warm-up: module load, staging allocation
+    times = []
+    bad = launches = 0
+    for rep in range(max(1, args.steps // 10)):
+        dt, b, launches = replay(rep == 0)
+        bad += b
+        times.append(dt)
+    dt = min(times)
+    n_sel = int((d["kind"] == 0).sum())
+    cpu = None
+    if not args.no_cpu_baseline:
+        cdt = _c1_replay_cpu(d, meta, n)
+        cpu = {"value": n_sel / cdt, "unit": "select decisions/s", "cores": 1, "kind": "port",
+               "calls_per_s": n / cdt,
+               "sample": f"all {n} calls, oracle/optable.py numpy restatement of OpTable.select / "
+                         f"affinity / set_latency, one call at a time on one core (the reference "
+                         f"engine is single-threaded)"}
+    line = {
+        "workload": "c1", "metric": "OpTable calls replayed one at a time through the drop-in API",
+        "unit": "select decisions/s", "value": n_sel / dt, "calls_per_s": n / dt,
+        "us_per_call": 1e6 * dt / n, "n_gpus": 1, "steps": len(times),
+        "config": {"scenario": "AMBER (branching), 50% target, recorded reference OpTable calls",
+                   "calls": n, "selects": n_sel, "affinity": int((d["kind"] == 1).sum()),
+                   "set_latency": int((d["kind"] == 2).sum()),
+                   "path": "OpTable.select / affinity / set_latency -> libslackpipe_b200 (pinned "
+                           "staging block, one launch + one sync per call; AUTO takes the scan "
+                           "while a set_latency has left the staircase plan stale)"},
+        "parity": {"calls_checked": n - int((d["kind"] == 2).sum()), "mismatches": bad,
+                   "result": "bit-identical to the recorded reference results" if bad == 0 else "MISMATCH"},
+        "gpu_launches": launches,
+        "reference_engine_decisions_per_s": {"value": C1_REFERENCE_DECISIONS_PER_S,
+                                             "source": "reference pkg/test_output.txt:171 (whole "
+                                                       "engine run, other hardware)"},
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+
+
 # ---- c3 -------------------------------------------------------------------------------------
 
 def _c3_cpu_worker(args):
@@ -959,5 +1097,5 @@ def run_speculate(args):
 
 
 def main(args):
-    {"c3": run_c3, "c4": run_c4, "c5": run_c5, "commit": run_commit,
+    {"c1": run_c1, "c3": run_c3, "c4": run_c4, "c5": run_c5, "commit": run_commit,
      "speculate": run_speculate}[args.workload](args)

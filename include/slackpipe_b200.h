@@ -135,6 +135,14 @@ int sp_select_batch(sp_ctx* ctx, int32_t n_tables, sp_table* const* tables, doub
                     double* out_slack, double* out_wait, double* out_kind_min, int32_t mode,
                     int32_t mem);
 
+/* OpTable.affinity (configurator.py:302-318) for N queries with HOST buffers in one call: the
+ * unmasked per-kind minima of invocation i (table tables[op[i]], slack row i) and out[i] =
+ * min_{k != q} minimum[k] / minimum[q], q = query_kind[i].  Queries whose kind is absent from
+ * the table must be mapped to None by the caller (configurator.py:310-315).  Synchronous. */
+int sp_affinity_batch(sp_ctx* ctx, int32_t n_tables, sp_table* const* tables, double alpha,
+                      int32_t N, const int32_t* op, const double* slack, const int32_t* query_kind,
+                      double* out, int32_t mode);
+
 /* Eq. 3 epilogue of OpTable.affinity (configurator.py:302-318) on the device: for invocation i
  * and query kind q = query_kind[i], out[i] = min_{k != q} kind_min[i*K+k] / kind_min[i*K+q]
  * (kind_min as produced by sp_select_batch; +inf marks kinds absent from the table, so an

@@ -76,6 +76,7 @@ SIGNATURES = {
     "sp_select_batch": (C.c_int, [_p, _i32, _p, _d, _i32, _p, _p, _p, _p, _p, _p,
                                   _p, _p, _p, _p, _p, _p, _p, _i32, _i32]),
     "sp_affinity_from_minima": (C.c_int, [_p, _i32, _i32, _p, _p, _p, _p, _i32]),
+    "sp_affinity_batch": (C.c_int, [_p, _i32, _p, _d, _i32, _p, _p, _p, _p, _i32]),
     "sp_dag_create": (C.c_int, [_p, _i32, _p, _p, _p, _p, _i32, _p, _pp]),
     "sp_dag_destroy": (C.c_int, [_p, _p]),
     "sp_slack_batch": (C.c_int, [_p, _p, _i32, _p, _i32, _p, _p, _i32, _p, _p, _p, _i32]),

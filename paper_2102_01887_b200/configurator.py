@@ -233,12 +233,13 @@ class OpTable:
 
     # -- reference API ----------------------------------------------------------------------
     def set_latency(self, index: int, latency_s: float) -> None:
-        """configurator.py:211-213 (host mirror + device copy)."""
+        """configurator.py:211-213 (device copy, then the host mirror — a rejected value leaves
+        both unchanged)."""
+        i = np.array([index], dtype=np.int32)
+        v = np.array([latency_s], dtype=np.float64)
+        check(self._ctx.lib.sp_table_set_latency(self._ctx.handle, self._handle, 1, ptr(i), ptr(v)))
         self.entries[index].latency_s = latency_s
         self.lat[index] = latency_s
-        i = np.array([index], dtype=np.int32)
-        v = np.array([self.lat[index]], dtype=np.float64)
-        check(self._ctx.lib.sp_table_set_latency(self._ctx.handle, self._handle, 1, ptr(i), ptr(v)))
 
     def slack_array(self, slack_by_kind: Mapping[str, float]) -> np.ndarray:
         """slack_by_kind as a K-vector in global kind order.  Table kinds must be present
@@ -278,17 +279,37 @@ class OpTable:
         excluded_kinds: frozenset[str] = frozenset(),
         min_batch: int = 1,
     ) -> Decision | None:
-        """configurator.py:239-300, one invocation through the batched kernel."""
+        """configurator.py:239-300, one invocation: the per-call drop-in path.  Arguments go
+        into persistent one-invocation buffers (pinned staging inside the library, one launch,
+        one sync)."""
+        one = self._one_call()
         flags = (_lib.SP_FLAG_ALLOW_DELAY if allow_delay else 0) | (
             self.excluded_mask(excluded_kinds) << _lib.SP_FLAG_EXCL_SHIFT)
-        r = self.select_batch(
-            self.slack_array(slack_by_kind)[None, :], alpha,
-            np.array([_i32(available, "available")], dtype=np.int32),
-            upstream_supply=np.array([_i32(upstream_supply, "upstream_supply")], dtype=np.int32),
-            min_batch=np.array([_i32(min_batch, "min_batch")], dtype=np.int32),
-            flags=np.array([flags], dtype=np.uint32),
-        )
-        return self.decision_from(r, 0)
+        one["slack"][0] = self.slack_array(slack_by_kind)
+        one["avail"][0] = _i32(available, "available")
+        one["supply"][0] = _i32(upstream_supply, "upstream_supply")
+        one["min_batch"][0] = _i32(min_batch, "min_batch")
+        one["flags"][0] = flags
+        check(self._ctx.lib.sp_select_batch(self._ctx.handle, 1, one["tables"], float(alpha), 1,
+                                            None, *one["args"], _lib.MODES["auto"],
+                                            _lib.SP_MEM_HOST), "sp_select_batch")
+        return self.decision_from(one["out"], 0)
+
+    def _one_call(self):
+        one = getattr(self, "_one", None)
+        if one is None:
+            one = {"slack": np.zeros((1, self.K)), "avail": np.zeros(1, np.int32),
+                   "supply": np.zeros(1, np.int32), "min_batch": np.zeros(1, np.int32),
+                   "flags": np.zeros(1, np.uint32), "q": np.zeros(1, np.int32), "aff": np.zeros(1)}
+            one["out"] = {"idx": np.zeros(1, np.int32), "code": np.zeros(1, np.int32),
+                          "fill": np.zeros(1, np.int32), "obj": np.zeros(1), "slack": np.zeros(1),
+                          "wait": np.zeros(1)}
+            one["args"] = [ptr(one[k]) for k in ("slack", "avail", "supply", "min_batch", "flags")] + \
+                          [ptr(one["out"][k]) for k in ("idx", "code", "fill", "obj", "slack", "wait")] + \
+                          [C.c_void_p(0)]
+            one["tables"] = C.cast((C.c_void_p * 1)(self.handle.value), C.c_void_p)
+            self._one = one
+        return one
 
     def decision_from(self, r: Mapping[str, Any], i: int) -> Decision | None:
         code = int(r["code"][i]) & 3
@@ -306,17 +327,17 @@ class OpTable:
         )
 
     def affinity(self, backend_kind: str, slack_by_kind: Mapping[str, float], alpha: float) -> float | None:
-        """Eq. 3 (configurator.py:302-318): per-kind minima from K2, ratio on the device."""
+        """Eq. 3 (configurator.py:302-318): unmasked per-kind minima and their ratio on the
+        device, one call."""
         if backend_kind not in self._kind_pos:
             return None
-        r = self.select_batch(
-            self.slack_array(slack_by_kind)[None, :], alpha,
-            np.ones(1, dtype=np.int32), upstream_supply=np.zeros(1, dtype=np.int32),
-            min_batch=np.ones(1, dtype=np.int32), flags=np.zeros(1, dtype=np.uint32),
-            kind_min=True,
-        )
-        return float(affinity_from_minima(r["kind_min"], np.array([self._gpos[backend_kind]], np.int32),
-                                          ctx=self._ctx)[0])
+        one = self._one_call()
+        one["slack"][0] = self.slack_array(slack_by_kind)
+        one["q"][0] = self._gpos[backend_kind]
+        check(self._ctx.lib.sp_affinity_batch(self._ctx.handle, 1, one["tables"], float(alpha), 1, None,
+                                              ptr(one["slack"]), ptr(one["q"]), ptr(one["aff"]),
+                                              _lib.MODES["auto"]), "sp_affinity_batch")
+        return float(one["aff"][0])
 
     def select_batch(self, slack, alpha, available, *, upstream_supply, min_batch, flags,
                      kind_min: bool = False, mode: str = "auto", out: dict | None = None) -> SelectResult:

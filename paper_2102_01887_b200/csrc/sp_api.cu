@@ -66,6 +66,28 @@ static void* ctx_io(sp_ctx* ctx, size_t bytes, int* rc) {
   return ctx->io_dev;
 }
 
+static void* ctx_pin(sp_ctx* ctx, size_t bytes, void** dev, int* rc) {
+  if (bytes > ctx->pin_cap) {
+    if (ctx->pin_host) {
+      cudaStreamSynchronize(ctx->stream);
+      cudaFreeHost(ctx->pin_host);
+      ctx->pin_host = ctx->pin_dev = nullptr;
+      ctx->pin_cap = 0;
+    }
+    size_t cap = std::max(bytes, (size_t)64 << 10);
+    cudaError_t e = cudaHostAlloc(&ctx->pin_host, cap, cudaHostAllocMapped);
+    if (e == cudaSuccess) e = cudaHostGetDevicePointer(&ctx->pin_dev, ctx->pin_host, 0);
+    if (e != cudaSuccess) {
+      *rc = cuda_fail(e, "cudaHostAlloc(staging)");
+      ctx->pin_host = ctx->pin_dev = nullptr;
+      return nullptr;
+    }
+    ctx->pin_cap = cap;
+  }
+  *dev = ctx->pin_dev;
+  return ctx->pin_host;
+}
+
 // Simple bump allocator over the I/O arena.
 struct Bump {
   uint8_t* base;
@@ -183,6 +205,7 @@ int sp_ctx_destroy(sp_ctx* ctx) {
   cudaFree(ctx->io_dev);
   cudaFree(ctx->ptr_dev);
   cudaFree(ctx->tmp_dev);
+  if (ctx->pin_host) cudaFreeHost(ctx->pin_host);
   if (ctx->h2d) {
     cudaStreamSynchronize(ctx->h2d);
     cudaStreamSynchronize(ctx->d2h);
@@ -338,13 +361,14 @@ int sp_table_set_latency(sp_ctx* ctx, sp_table* t, int32_t n, const int32_t* idx
   }
   const int m = (int)ui.size();
   int rc = SP_OK;
-  void* io = ctx_io(ctx, rsz<int32_t>(m) + rsz<double>(m), &rc);
-  if (!io) return rc;
-  Bump b{(uint8_t*)io};
-  int32_t* d_i = b.take<int32_t>(m);
-  double* d_v = b.take<double>(m);
-  SP_CUDA(cudaMemcpyAsync(d_i, ui.data(), sizeof(int32_t) * m, cudaMemcpyHostToDevice, ctx->stream));
-  SP_CUDA(cudaMemcpyAsync(d_v, uv.data(), sizeof(double) * m, cudaMemcpyHostToDevice, ctx->stream));
+  // the updates travel in the pinned staging block (read by the scatter kernel over PCIe)
+  void* dbase = nullptr;
+  uint8_t* hb = static_cast<uint8_t*>(ctx_pin(ctx, rsz<int32_t>(m) + rsz<double>(m), &dbase, &rc));
+  if (!hb) return rc;
+  memcpy(hb, ui.data(), sizeof(int32_t) * m);
+  memcpy(hb + rsz<int32_t>(m), uv.data(), sizeof(double) * m);
+  const int32_t* d_i = reinterpret_cast<const int32_t*>(dbase);
+  const double* d_v = reinterpret_cast<const double*>(static_cast<uint8_t*>(dbase) + rsz<int32_t>(m));
   k_scatter<<<(m + 255) / 256, 256, 0, ctx->stream>>>(m, d_i, d_v, t->lat);
   SP_CHECK_LAUNCH(ctx);
   SP_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -445,7 +469,7 @@ int sp_scores(sp_ctx* ctx, sp_table* t, const double* slack_by_kind, double alph
   if (!ctx || !t || !slack_by_kind || !out_score || !out_cost)
     return fail(SP_E_INVALID, "scores: null argument");
   int rc;
-  Plan* p = plan_get(ctx, t, alpha, &rc);
+  Plan* p = plan_costs(ctx, t, alpha, &rc);
   if (!p) return rc;
   size_t need = rsz<double>(t->K) + 2 * rsz<double>(t->M);
   void* io = ctx_io(ctx, need, &rc);
@@ -469,6 +493,7 @@ int sp_scores(sp_ctx* ctx, sp_table* t, const double* slack_by_kind, double alph
 }  // extern "C"
 
 namespace sp {
+constexpr int kSmallHostN = 256;  // host calls up to this size go through the pinned staging block
 // sp_select_batch without the final synchronisation when sync == false (host I/O is then
 // complete only after select_host_wait): lets sp_group_select_batch run every member
 // device's shard concurrently from one host thread.
@@ -534,6 +559,42 @@ int select_batch_impl(sp_ctx* ctx, int32_t n_tables, sp_table* const* tables, do
                 3 * rsz<int32_t>(N) + 3 * rsz<double>(N) +
                 (out_kind_min ? rsz<double>((size_t)N * K) : 0);
   int rc = SP_OK;
+  if (N <= kSmallHostN) {
+    // small calls (the reference engine's one-invocation OpTable.select): inputs copied into a
+    // pinned mapped staging block, one launch reads and writes it over PCIe, one sync
+    void* dbase = nullptr;
+    uint8_t* hb = static_cast<uint8_t*>(ctx_pin(ctx, need, &dbase, &rc));
+    if (!hb) return rc;
+    uint8_t* db = static_cast<uint8_t*>(dbase);
+    size_t o = 0;
+    auto put = [&](const void* src, size_t bytes) -> size_t {
+      const size_t at = o;
+      if (src) memcpy(hb + at, src, bytes);
+      o += (bytes + 255) & ~(size_t)255;
+      return at;
+    };
+    const size_t o_sl = put(slack, sizeof(double) * N * K), o_av = put(avail, 4u * N),
+                 o_su = put(supply, 4u * N), o_mb = put(min_batch, 4u * N), o_fl = put(flags, 4u * N),
+                 o_op = op ? put(op, 4u * N) : 0, o_ix = put(nullptr, 4u * N), o_cd = put(nullptr, 4u * N),
+                 o_fi = put(nullptr, 4u * N), o_ob = put(nullptr, 8u * N), o_sk = put(nullptr, 8u * N),
+                 o_wt = put(nullptr, 8u * N), o_km = out_kind_min ? put(nullptr, sizeof(double) * N * K) : 0;
+    rc = select_launch(ctx, n_tables, tables, alpha, N, op ? (const int32_t*)(db + o_op) : nullptr,
+                       (const double*)(db + o_sl), (const int32_t*)(db + o_av),
+                       (const int32_t*)(db + o_su), (const int32_t*)(db + o_mb),
+                       (const uint32_t*)(db + o_fl), (int32_t*)(db + o_ix), (int32_t*)(db + o_cd),
+                       (int32_t*)(db + o_fi), (double*)(db + o_ob), (double*)(db + o_sk),
+                       (double*)(db + o_wt), out_kind_min ? (double*)(db + o_km) : nullptr, mode);
+    if (rc != SP_OK) return rc;
+    SP_CUDA(cudaStreamSynchronize(ctx->stream));
+    memcpy(out_idx, hb + o_ix, 4u * N);
+    memcpy(out_code, hb + o_cd, 4u * N);
+    if (out_fill) memcpy(out_fill, hb + o_fi, 4u * N);
+    if (out_obj) memcpy(out_obj, hb + o_ob, 8u * N);
+    if (out_slack) memcpy(out_slack, hb + o_sk, 8u * N);
+    if (out_wait) memcpy(out_wait, hb + o_wt, 8u * N);
+    if (out_kind_min) memcpy(out_kind_min, hb + o_km, sizeof(double) * N * K);
+    return SP_OK;
+  }
   void* io = ctx_io(ctx, need, &rc);
   if (!io) return rc;
   Bump b{(uint8_t*)io};
@@ -637,6 +698,64 @@ int sp_select_batch(sp_ctx* ctx, int32_t n_tables, sp_table* const* tables, doub
   return select_batch_impl(ctx, n_tables, tables, alpha, N, op, slack, avail, supply, min_batch,
                            flags, out_idx, out_code, out_fill, out_obj, out_slack, out_wait,
                            out_kind_min, mode, mem, true);
+}
+
+int sp_affinity_batch(sp_ctx* ctx, int32_t n_tables, sp_table* const* tables, double alpha,
+                      int32_t N, const int32_t* op, const double* slack, const int32_t* query_kind,
+                      double* out, int32_t mode) {
+  DeviceScope _dev_scope(ctx ? ctx->device : -1);
+  if (!ctx || !tables || n_tables < 1 || N < 0 || (N > 0 && (!slack || !query_kind || !out)))
+    return fail(SP_E_INVALID, "affinity_batch: bad argument");
+  if (!(alpha >= 0.0)) return fail(SP_E_INVALID, "alpha must be >= 0");  // configurator.py:37
+  const int K = tables[0]->K;
+  for (int i = 0; i < N; ++i) {
+    if (query_kind[i] < 0 || query_kind[i] >= K) return fail(SP_E_INVALID, "affinity: kind out of range");
+    if (op && (op[i] < 0 || op[i] >= n_tables)) return fail(SP_E_INVALID, "affinity: op out of range");
+  }
+  if (N == 0) return SP_OK;
+  // one staging block: the unmasked select inputs (every kind admitted, min_batch 1), the
+  // per-kind minima and the ratios; one sync
+  int rc = SP_OK;
+  const size_t need = rsz<double>((size_t)N * K) * 2 + rsz<int32_t>(N) * 8 + rsz<double>(N);
+  void* dbase = nullptr;
+  uint8_t* hb = static_cast<uint8_t*>(ctx_pin(ctx, need, &dbase, &rc));
+  if (!hb) return rc;
+  uint8_t* db = static_cast<uint8_t*>(dbase);
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    const size_t at = o;
+    o += (bytes + 255) & ~(size_t)255;
+    return at;
+  };
+  const size_t o_sl = take(sizeof(double) * N * K), o_km = take(sizeof(double) * N * K),
+               o_av = take(4u * N), o_su = take(4u * N), o_mb = take(4u * N), o_fl = take(4u * N),
+               o_op = take(4u * N), o_q = take(4u * N), o_ix = take(4u * N), o_cd = take(4u * N),
+               o_out = take(8u * N);
+  memcpy(hb + o_sl, slack, sizeof(double) * N * K);
+  memcpy(hb + o_q, query_kind, 4u * N);
+  if (op) memcpy(hb + o_op, op, 4u * N);
+  int32_t* av = (int32_t*)(hb + o_av);
+  int32_t* su = (int32_t*)(hb + o_su);
+  int32_t* mb = (int32_t*)(hb + o_mb);
+  uint32_t* fl = (uint32_t*)(hb + o_fl);
+  for (int i = 0; i < N; ++i) {
+    av[i] = 1;
+    su[i] = 0;
+    mb[i] = 1;
+    fl[i] = 0u;
+  }
+  rc = select_launch(ctx, n_tables, tables, alpha, N, op ? (const int32_t*)(db + o_op) : nullptr,
+                     (const double*)(db + o_sl), (const int32_t*)(db + o_av),
+                     (const int32_t*)(db + o_su), (const int32_t*)(db + o_mb),
+                     (const uint32_t*)(db + o_fl), (int32_t*)(db + o_ix), (int32_t*)(db + o_cd),
+                     nullptr, nullptr, nullptr, nullptr, (double*)(db + o_km), mode);
+  if (rc != SP_OK) return rc;
+  rc = affinity_launch(ctx, N, K, (const double*)(db + o_km), (const int32_t*)(db + o_q),
+                       (double*)(db + o_out));
+  if (rc != SP_OK) return rc;
+  SP_CUDA(cudaStreamSynchronize(ctx->stream));
+  memcpy(out, hb + o_out, 8u * N);
+  return SP_OK;
 }
 
 int sp_affinity_from_minima(sp_ctx* ctx, int32_t N, int32_t K, const double* kind_min,

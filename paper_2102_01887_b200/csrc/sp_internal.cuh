@@ -93,6 +93,7 @@ __host__ __device__ __forceinline__ uint64_t order_key(uint64_t u) {
 struct Plan {
   double alpha = 0.0;
   uint64_t version = ~0ull;  // table version the plan was built for
+  uint64_t cost_version = ~0ull;  // table version cost / costpen were computed for
   bool valid = false;
   // device buffers
   double* cost = nullptr;     // M
@@ -132,6 +133,11 @@ struct sp_ctx {
   // small device scratch for pointer tables
   void* ptr_dev = nullptr;
   size_t ptr_cap = 0;
+  // pinned, mapped host staging for small host-buffer calls (one launch reads / writes it over
+  // PCIe, no copy-engine operations)
+  void* pin_host = nullptr;
+  void* pin_dev = nullptr;
+  size_t pin_cap = 0;
   // generic device scratch (sort temp etc.)
   void* tmp_dev = nullptr;
   size_t tmp_cap = 0;
@@ -282,6 +288,8 @@ int plan_cluster_prepare(sp_table* t, const int32_t* kind, const int32_t* bidx);
 int plan_cluster_launch(sp_ctx* ctx, sp_table* t, Plan& p, int W, const PlanHdr& hdr,
                         int32_t* status);
 Plan* plan_get(sp_ctx* ctx, sp_table* t, double alpha, int* rc);
+Plan* plan_costs(sp_ctx* ctx, sp_table* t, double alpha, int* rc);
+bool plan_ready(sp_table* t, double alpha);
 const PlanHdr* plan_host_header(Plan& p);  // nullptr until the async copy has landed
 void plan_release(Plan& p);
 int select_launch(sp_ctx* ctx, int n_tables, sp_table* const* tables, double alpha, int N,

@@ -1719,31 +1719,65 @@ void plan_release(Plan& p) {
   p = Plan();
 }
 
+// the table's plan slot for alpha (created empty when missing; at most 16 per table)
+static Plan* plan_entry(sp_ctx* ctx, sp_table* t, double alpha) {
+  for (auto& p : t->plans)
+    if (p.alpha == alpha || (p.alpha != p.alpha && alpha != alpha)) return &p;
+  if (t->plans.size() >= 16) {
+    // evict the oldest entry's buffers (keep memory bounded)
+    cudaStreamSynchronize(ctx->stream);
+    plan_release(t->plans.front());
+    t->plans.erase(t->plans.begin());
+  }
+  t->plans.emplace_back();
+  Plan* hit = &t->plans.back();
+  hit->alpha = alpha;
+  return hit;
+}
+
 Plan* plan_get(sp_ctx* ctx, sp_table* t, double alpha, int* rc) {
   *rc = SP_OK;
-  Plan* hit = nullptr;
-  for (auto& p : t->plans) {
-    if (p.alpha == alpha || (p.alpha != p.alpha && alpha != alpha)) {
-      hit = &p;
-      break;
-    }
-  }
-  if (!hit) {
-    if (t->plans.size() >= 16) {
-      // evict the oldest entry's buffers (keep memory bounded)
-      cudaStreamSynchronize(ctx->stream);
-      plan_release(t->plans.front());
-      t->plans.erase(t->plans.begin());
-    }
-    t->plans.emplace_back();
-    hit = &t->plans.back();
-    hit->alpha = alpha;
-  }
+  Plan* hit = plan_entry(ctx, t, alpha);
   if (!hit->valid || hit->version != t->version) {
     *rc = plan_build(ctx, t, *hit);
     if (*rc != SP_OK) return nullptr;
+    hit->cost_version = t->version;
   }
   return hit;
+}
+
+bool plan_ready(sp_table* t, double alpha) {
+  for (auto& p : t->plans)
+    if (p.alpha == alpha || (p.alpha != p.alpha && alpha != alpha))
+      return p.valid && p.version == t->version;
+  return false;
+}
+
+// cost / costpen of the current table version only (the scan kernels' inputs): one k_cost
+// launch when stale, no staircase build
+Plan* plan_costs(sp_ctx* ctx, sp_table* t, double alpha, int* rc) {
+  *rc = SP_OK;
+  Plan* p = plan_entry(ctx, t, alpha);
+  if (p->cost_version == t->version && p->cost) return p;
+  const int M = t->M;
+  if (!p->cost) {
+    cudaError_t e = cudaMalloc(&p->cost, sizeof(double) * M);
+    if (e == cudaSuccess) e = cudaMalloc(&p->costpen, sizeof(double) * M);
+    if (e != cudaSuccess) {
+      *rc = cuda_fail(e, "cudaMalloc(cost)");
+      return nullptr;
+    }
+  }
+  k_cost<<<(M + 255) / 256, 256, 0, ctx->stream>>>(M, t->lat, t->res, t->batch, t->pool, t->price,
+                                                    p->alpha, p->cost, p->costpen);
+  ctx->launches++;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    *rc = cuda_fail(e, "k_cost");
+    return nullptr;
+  }
+  p->cost_version = t->version;
+  return p;
 }
 
 }  // namespace sp

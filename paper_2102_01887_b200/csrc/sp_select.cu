@@ -558,6 +558,8 @@ int slack_select_launch(sp_ctx* ctx, sp_dag* g, int n_tables, sp_table* const* t
   return SP_OK;
 }
 
+constexpr int64_t kAutoPlanWork = (int64_t)1 << 24;
+
 int select_launch(sp_ctx* ctx, int n_tables, sp_table* const* tables, double alpha, int N,
                   const int32_t* op, const double* slack, const int32_t* avail,
                   const int32_t* supply, const int32_t* min_batch, const uint32_t* flags,
@@ -574,7 +576,20 @@ int select_launch(sp_ctx* ctx, int n_tables, sp_table* const* tables, double alp
   }
   if (mode == SP_MODE_PLAN && !plan_ok)
     return fail(SP_E_UNSUPPORTED, "select: staircase plan unsupported for this table");
-  bool use_plan = (mode == SP_MODE_PLAN) || (mode == SP_MODE_AUTO && plan_ok);
+  // AUTO: the staircase plan when it is current, or when the batch is large enough to pay for
+  // a rebuild (a plan build costs about as much as scanning ~2^24 invocation x entry pairs);
+  // otherwise the scan, which needs only cost / costpen (e.g. one call right after a
+  // set_latency in the reference engine's per-call use)
+  bool use_plan = mode == SP_MODE_PLAN;
+  if (mode == SP_MODE_AUTO && plan_ok) {
+    bool ready = true;
+    int64_t work = 0;
+    for (int t = 0; t < n_tables; ++t) {
+      ready = ready && plan_ready(tables[t], alpha);
+      work += tables[t]->M;
+    }
+    use_plan = ready || (int64_t)N * work >= kAutoPlanWork;
+  }
   if (use_plan && n_tables > kMaxPlanTables)
     return fail(SP_E_UNSUPPORTED, "select: too many tables in one plan launch (max 64)");
   if (!use_plan && n_tables > kMaxScanTables)
@@ -618,7 +633,7 @@ int select_launch(sp_ctx* ctx, int n_tables, sp_table* const* tables, double alp
   size_t stage = 0;
   for (int t = 0; t < n_tables; ++t) {
     int rc;
-    Plan* p = plan_get(ctx, tables[t], alpha, &rc);
+    Plan* p = plan_costs(ctx, tables[t], alpha, &rc);
     if (!p) return rc;
     sp_table* tb = tables[t];
     ScanTab s;
