@@ -428,10 +428,33 @@ def our_arm(args) -> None:
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args.cpu_seconds)
-    if rank == 0:
-        print(json.dumps(line), flush=True)
-    if world > 1:
-        torch.distributed.destroy_process_group()
+    return line if rank == 0 else None
+
+
+def run_extras(args, line) -> None:
+    """The other BASELINE configs on the same GPUs, attached to the headline line under
+    "configs" (each entry is that workload's own line, bench_workloads.py): config 1 (AMBER
+    drop-in, per call), 3 (deep DAG), 4 (target sweep, strong scaling) and 5 (online mode,
+    strong scaling).  Skipped with --no-extras."""
+    import copy
+
+    import torch
+
+    import bench_workloads
+
+    out = {}
+    for w in ("c1", "c3", "c4", "c5"):
+        a = copy.copy(args)
+        a.workload = w
+        a.steps = min(args.steps, 10)
+        torch.cuda.empty_cache()
+        t0 = time.perf_counter()
+        r = bench_workloads.RUNNERS[w](a)
+        if r is not None:
+            r["wall_s"] = time.perf_counter() - t0
+            out[w] = r
+    if line is not None:
+        line["configs"] = out
 
 
 def _free_port() -> int:
@@ -510,6 +533,8 @@ def main() -> None:
     ap.add_argument("--c3-cpu-instances", type=int, default=1000)
     ap.add_argument("--c4-replicas", type=int, default=10000)
     ap.add_argument("--c5-batches", type=int, default=256)
+    ap.add_argument("--no-extras", action="store_true",
+                    help="headline line only (skip configs 1, 3, 4, 5 attached under 'configs')")
     ap.add_argument("--dist-selftest", action="store_true",
                     help="CPU/gloo check of the multi-rank plumbing (tests); no GPU work")
     args = ap.parse_args()
@@ -527,8 +552,16 @@ def main() -> None:
         return
     if args.impl == "reference":
         reference_arm(args)
-    else:
-        our_arm(args)
+        return
+    line = our_arm(args)
+    if not args.no_extras:
+        run_extras(args, line)
+    if line is not None:
+        print(json.dumps(line), flush=True)
+    import torch
+
+    if torch.distributed.is_available() and torch.distributed.is_initialized():
+        torch.distributed.destroy_process_group()
 
 
 if __name__ == "__main__":

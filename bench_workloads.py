@@ -212,7 +212,7 @@ def run_c1(args):
                                                        "engine run, other hardware)"},
         "cpu_baseline": cpu,
     }
-    print(json.dumps(line), flush=True)
+    return line
 
 
 # ---- c3 -------------------------------------------------------------------------------------
@@ -342,7 +342,7 @@ def run_c3(args):
         "step_ms": {"median": statistics.median(ms), "min": min(ms), "max": max(ms)},
         "clocks": clk.summary(),
     }
-    print(json.dumps(line), flush=True)
+    return line
 
 
 # ---- c4 -------------------------------------------------------------------------------------
@@ -547,7 +547,7 @@ def run_c4(args):
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
     }
-    print(json.dumps(line), flush=True)
+    return line
 
 
 def _c4_cpu_baseline(meta, g, alpha, sw, V):
@@ -712,7 +712,7 @@ def run_c5(args):
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
     }
-    print(json.dumps(line), flush=True)
+    return line
 
 
 def c5_parity(sp, spec, synth, inv, alpha, B, NB, base, per_item, noise, online_batch, out, obs_idx,
@@ -928,7 +928,7 @@ def run_commit(args):
         "cpu_baseline": cpu,
         "step_ms": {"median": statistics.median(ms), "min": min(ms), "max": max(ms)},
     }
-    print(json.dumps(line), flush=True)
+    return line
 
 # ---- speculate ----------------------------------------------------------
 
@@ -1093,9 +1093,14 @@ def run_speculate(args):
         "cpu_baseline": cpu,
         "step_ms": {"median": statistics.median(ms), "min": min(ms), "max": max(ms)},
     }
-    print(json.dumps(line), flush=True)
+    return line
+
+
+RUNNERS = {"c1": run_c1, "c3": run_c3, "c4": run_c4, "c5": run_c5, "commit": run_commit,
+           "speculate": run_speculate}
 
 
 def main(args):
-    {"c1": run_c1, "c3": run_c3, "c4": run_c4, "c5": run_c5, "commit": run_commit,
-     "speculate": run_speculate}[args.workload](args)
+    line = RUNNERS[args.workload](args)
+    if line is not None:  # rank 0
+        print(json.dumps(line), flush=True)
