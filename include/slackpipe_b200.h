@@ -46,17 +46,22 @@ extern "C" {
 #define SP_DEC_ASSIGN 1    /* Decision(kind="assign") (configurator.py:293-300) */
 #define SP_DEC_DELAY 2     /* Decision(kind="delay")  (configurator.py:278-286) */
 #define SP_DEC_FEASIBLE 4  /* bit 2: decision-time SLO flag L(x*) < slack[kind(x*)] (configurator.py:226) */
+#define SP_DEC_ERROR 3     /* the reference raises here: a NaN score leaves _argmin's tie set empty
+                              (configurator.py:233-236, min() of an empty sequence -> ValueError) */
 
 /* per-invocation flags word (in_flags) */
 #define SP_FLAG_ALLOW_DELAY 1u       /* bit 0: allow_delay (configurator.py:245) */
-#define SP_FLAG_EXCL_SHIFT 8         /* bits 8..15: excluded_kinds as a mask over the K kinds */
+#define SP_FLAG_EXCL_SHIFT 8         /* bits 8..31: excluded_kinds as a mask over the K kinds */
 
 /* select modes */
 #define SP_MODE_AUTO 0   /* staircase kernel when the table's plan allows it, else scan */
 #define SP_MODE_PLAN 1   /* K2b: staircase (sorted prefix-min) decision kernel */
 #define SP_MODE_SCAN 2   /* K2a: brute-force fused scan over every entry */
 
-#define SP_MAX_KINDS 8
+#define SP_MAX_KINDS 24        /* backend kinds of a table (the reference has no limit; the
+                                  excluded-kind mask of the flags word holds 24) */
+#define SP_MAX_PLAN_KINDS 8    /* the staircase plan's limit; tables with more kinds are decided
+                                  by the literal scan */
 #define SP_MAX_BATCH_VALUES 16
 
 typedef struct sp_ctx sp_ctx;

@@ -197,7 +197,7 @@ def select_many(tables: Sequence[Arrays], slack: np.ndarray, alpha: float, avail
         t = tables[0 if op is None else int(op[i])]
         f = int(flags[i])
         r = select(t, slack[i], alpha, int(avail[i]), allow_delay=bool(f & 1),
-                   upstream_supply=int(supply[i]), excluded_mask=(f >> 8) & 0xFF,
+                   upstream_supply=int(supply[i]), excluded_mask=(f >> 8) & 0xFFFFFF,
                    min_batch=int(min_batch[i]))
         (out["code"][j], out["idx"][j], out["fill"][j], out["obj"][j], out["slack"][j],
          out["wait"][j], out["feasible"][j]) = r

@@ -29,6 +29,7 @@ SP_DEC_NONE = 0
 SP_DEC_ASSIGN = 1
 SP_DEC_DELAY = 2
 SP_DEC_FEASIBLE = 4
+SP_DEC_ERROR = 3  # the reference raises ValueError (NaN scores leave no tie)
 
 SP_FLAG_ALLOW_DELAY = 1
 SP_FLAG_EXCL_SHIFT = 8
@@ -46,7 +47,7 @@ SP_SPEC_HOLD_EXPIRED = 4
 SP_COMMIT_FIFO = 1
 SP_COMMIT_ESLC = 2
 
-MAX_KINDS = 8
+MAX_KINDS = 24          # table kinds (SP_MAX_KINDS); the staircase plan takes <= 8
 
 # (name, restype, argtypes) for every exported symbol; the CPU test suite checks that
 # the shared object exports exactly what include/slackpipe_b200.h declares.

@@ -158,7 +158,7 @@ class OpTable:
         if missing:
             raise ValueError(f"kinds {missing} missing from the global kind list")
         if len(self.global_kinds) > _lib.MAX_KINDS:
-            raise _lib.SlackpipeError("at most 8 backend kinds are supported")
+            raise _lib.SlackpipeError("at most 24 backend kinds are supported")
         self._gpos = gpos
         self.gkind = np.array([gpos[e.backend_kind] for e in entries], dtype=np.int32)
         self._create_device(device)
@@ -315,6 +315,9 @@ class OpTable:
         code = int(r["code"][i]) & 3
         if code == _lib.SP_DEC_NONE:
             return None
+        if code == _lib.SP_DEC_ERROR:
+            # configurator.py:236: NaN scores leave _argmin's tie set empty
+            raise ValueError("min() arg is an empty sequence")
         j = int(r["idx"][i])
         return Decision(
             kind="delay" if code == _lib.SP_DEC_DELAY else "assign",

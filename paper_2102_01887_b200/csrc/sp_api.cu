@@ -249,15 +249,13 @@ int sp_table_create(sp_ctx* ctx, int32_t M, const double* lat, const double* lat
   if (!ctx || !out) return fail(SP_E_INVALID, "table_create: null argument");
   // configurator.py:178-179
   if (M < 1) return fail(SP_E_INVALID, "operation has no schedulable configuration");
-  if (K < 1 || K > kMaxKinds) return fail(SP_E_UNSUPPORTED, "table_create: 1..8 kinds supported");
+  if (K < 1 || K > kMaxTableKinds)
+    return fail(SP_E_UNSUPPORTED, "table_create: 1..24 backend kinds supported");
   if (ref_index < -1 || ref_index >= M) return fail(SP_E_INVALID, "table_create: bad ref_index");
   std::vector<int32_t> bv;
   for (int j = 0; j < M; ++j) {
     if (kind[j] < 0 || kind[j] >= K) return fail(SP_E_INVALID, "table_create: kind out of range");
     if (batch[j] < 1) return fail(SP_E_INVALID, "table_create: batch size must be >= 1");
-    // finite latencies keep every score finite; with an infinite score the reference's
-    // masked argmin (configurator.py:230-233) would tie masked-out entries too
-    if (!isfinite(lat[j])) return fail(SP_E_INVALID, "table_create: latency must be finite");
     bv.push_back(batch[j]);
   }
   std::sort(bv.begin(), bv.end());
@@ -268,16 +266,22 @@ int sp_table_create(sp_ctx* ctx, int32_t M, const double* lat, const double* lat
   t->K = K;
   t->ref_index = ref_index;
   t->nB = (int)bv.size();
-  // unified candidate ids are u16: at most 2M - 1 < 65535 candidates
-  t->plan_ok = t->nB <= kMaxB && M < 32767;
+  t->nonfinite_entry.assign(M, 0);
+  for (int j = 0; j < M; ++j) {
+    t->nonfinite_entry[j] = !isfinite(lat[j]);
+    t->nonfinite += t->nonfinite_entry[j];
+  }
+  // unified candidate ids are u16: at most 2M - 1 < 65535 candidates; the plan header describes
+  // at most 8 kinds
+  t->plan_ok = t->nB <= kMaxB && M < 32767 && K <= kMaxKinds;
   for (int b = 0; b < kMaxB; ++b) t->batch_vals[b] = b < t->nB ? bv[b] : INT32_MAX;
   std::vector<int32_t> bidx(M), kslot(M);
   for (int j = 0; j < M; ++j)
     bidx[j] = (int32_t)(std::lower_bound(bv.begin(), bv.end(), batch[j]) - bv.begin());
-  int cnt[kMaxKinds] = {0};
+  int cnt[kMaxTableKinds] = {0};
   for (int j = 0; j < M; ++j) kslot[j] = cnt[kind[j]]++;
   int base = 0;
-  for (int k = 0; k < kMaxKinds; ++k) {
+  for (int k = 0; k < kMaxTableKinds; ++k) {
     t->kind_count[k] = k < K ? cnt[k] : 0;
     t->kind_base[k] = base;
     if (k < K) base += cnt[k];
@@ -349,8 +353,12 @@ int sp_table_set_latency(sp_ctx* ctx, sp_table* t, int32_t n, const int32_t* idx
   std::map<int32_t, double> last;
   for (int i = 0; i < n; ++i) {
     if (idx[i] < 0 || idx[i] >= t->M) return fail(SP_E_INVALID, "set_latency: index out of range");
-    if (!isfinite(val[i])) return fail(SP_E_INVALID, "set_latency: latency must be finite");
-    last[idx[i]] = val[i];
+    last[idx[i]] = val[i];  // any float, as configurator.py:211-213
+  }
+  for (auto& kv : last) {  // non-finite entries switch decisions to the literal scan
+    const uint8_t nf = !isfinite(kv.second);
+    t->nonfinite += (int)nf - (int)t->nonfinite_entry[kv.first];
+    t->nonfinite_entry[kv.first] = nf;
   }
   if (last.empty()) return SP_OK;
   std::vector<int32_t> ui;
@@ -395,7 +403,9 @@ int sp_table_prepare(sp_ctx* ctx, sp_table* t, double alpha) {
   DeviceScope _dev_scope(ctx ? ctx->device : -1);
   if (!ctx || !t) return fail(SP_E_INVALID, "prepare: null argument");
   int rc;
-  Plan* p = plan_get(ctx, t, alpha, &rc);
+  // the staircase only where it applies; otherwise the scan's cost / costpen
+  Plan* p = t->plan_ok && t->finite_safe() && isfinite(alpha) ? plan_get(ctx, t, alpha, &rc)
+                                                              : plan_costs(ctx, t, alpha, &rc);
   return p ? SP_OK : rc;
 }
 
@@ -762,7 +772,7 @@ int sp_affinity_from_minima(sp_ctx* ctx, int32_t N, int32_t K, const double* kin
                             const int32_t* query_kind, double* out, void* reserved,
                             int32_t mem) {
   DeviceScope _dev_scope(ctx ? ctx->device : -1);
-  if (!ctx || N < 0 || K < 1 || K > kMaxKinds || reserved)
+  if (!ctx || N < 0 || K < 1 || K > kMaxTableKinds || reserved)
     return fail(SP_E_INVALID, "affinity: bad argument");
   if (N > 0 && (!kind_min || !query_kind || !out)) return fail(SP_E_INVALID, "affinity: null array");
   if (mem == SP_MEM_DEVICE) return affinity_launch(ctx, N, K, kind_min, query_kind, out);
@@ -1059,6 +1069,11 @@ int sp_feedback_fold(sp_ctx* ctx, int32_t n_tables, sp_table* const* tables, int
     if (t < 0 || t >= n_tables) return fail(SP_E_INVALID, "feedback_fold: op out of range");
     if (idx[j] >= tables[t]->M)  // idx < 0: no observation (skipped)
       return fail(SP_E_INVALID, "feedback_fold: entry index out of range");
+    // a non-finite observation (or a fold into a table already holding non-finite latencies,
+    // which the gate lift can spread) leaves non-finite latencies behind: from now on the
+    // table's decisions take the literal scan
+    if (idx[j] >= 0 && !fb_frozen && (!isfinite(obs[j]) || tables[t]->nonfinite))
+      tables[t]->tainted = true;
   }
   size_t need = 2 * rsz<int32_t>(n) + rsz<double>(n);
   int rc = SP_OK;

@@ -18,7 +18,8 @@ namespace sp {
 
 constexpr uint32_t kPlanMagic = 0x53504c4eu;  // "SPLN"
 constexpr uint16_t kNone16 = 0xFFFFu;
-constexpr int kMaxKinds = SP_MAX_KINDS;
+constexpr int kMaxKinds = SP_MAX_PLAN_KINDS;    // plan / fused-kernel kind limit
+constexpr int kMaxTableKinds = SP_MAX_KINDS;    // table kind limit (literal scan beyond 8)
 constexpr int kMaxB = SP_MAX_BATCH_VALUES;
 
 // One candidate record of the staircase plan (32 B).  Candidates live in ONE id space
@@ -151,8 +152,15 @@ struct sp_ctx {
 struct sp_table {
   int32_t M = 0, K = 0, nB = 0, ref_index = -1;
   int32_t batch_vals[sp::kMaxB];
-  int32_t kind_count[sp::kMaxKinds];
-  int32_t kind_base[sp::kMaxKinds];  // entries sorted by kind: base offset per kind
+  int32_t kind_count[sp::kMaxTableKinds];
+  int32_t kind_base[sp::kMaxTableKinds];  // entries sorted by kind: base offset per kind
+  // entries whose latency is not finite (host mirror, per entry): the staircase plan and the
+  // fused kernels need finite latencies; with any non-finite entry decisions take the literal
+  // scan, which reproduces the reference's inf / NaN behaviour
+  std::vector<uint8_t> nonfinite_entry;
+  int32_t nonfinite = 0;
+  bool tainted = false;  // a host fold may have produced non-finite latencies
+  bool finite_safe() const { return nonfinite == 0 && !tainted; }
   bool plan_ok = false;
   uint64_t version = 0;
   int32_t completed_ref = 0;

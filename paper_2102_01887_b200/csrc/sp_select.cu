@@ -188,6 +188,94 @@ __device__ __forceinline__ bool better(double sc, double c, double r, int id, co
   return id < b.id;
 }
 
+// The reference's masked argmin restated literally for the cases the strict total order of
+// the fast scan cannot represent (configurator.py:229-237 with numpy / Python semantics):
+// best = min over where(mask, score, inf) (NaN propagates); ties = every index whose masked
+// score equals best — with best == inf that includes masked-out entries; the winner is the
+// first minimum of the key tuple (cost, res, id_rank) in index order under Python's tuple
+// comparison (NaN compares unequal and never smaller).  Returns the index, -1 when the mask is
+// empty, -2 when the tie set is empty (a NaN best: the reference's min() raises ValueError).
+template <int KT>
+__device__ int literal_argmin(const ScanTab& tb, const In<KT>& x, bool use_av) {
+  double best = INFINITY;
+  bool nan = false, any = false;
+  for (int j = 0; j < tb.M; ++j) {
+    const int kj = tb.kind[j];
+    const bool m = !((x.fl >> (SP_FLAG_EXCL_SHIFT + kj)) & 1u) && tb.batch[j] >= x.mb &&
+                   (!use_av || tb.batch[j] <= x.av);
+    if (!m) continue;
+    any = true;
+    const double sc = (tb.lat[j] < pick_kind<KT>(x.s, kj)) ? tb.cost[j] : tb.costpen[j];
+    if (sc != sc) nan = true;
+    else if (sc < best) best = sc;
+  }
+  if (!any) return -1;
+  if (nan) return -2;
+  int cur = -1;
+  for (int j = 0; j < tb.M; ++j) {
+    const int kj = tb.kind[j];
+    const bool m = !((x.fl >> (SP_FLAG_EXCL_SHIFT + kj)) & 1u) && tb.batch[j] >= x.mb &&
+                   (!use_av || tb.batch[j] <= x.av);
+    const double sc = m ? ((tb.lat[j] < pick_kind<KT>(x.s, kj)) ? tb.cost[j] : tb.costpen[j])
+                        : INFINITY;
+    if (!(sc == best)) continue;
+    if (cur < 0) {
+      cur = j;
+      continue;
+    }
+    const double c = tb.cost[j], cc = tb.cost[cur];
+    bool lt;
+    if (c != cc) lt = c < cc;
+    else if (tb.res[j] != tb.res[cur]) lt = tb.res[j] < tb.res[cur];
+    else lt = tb.id[j] < tb.id[cur];
+    if (lt) cur = j;
+  }
+  return cur;
+}
+
+template <int KT>
+__device__ void literal_select(const ScanTab& tb, const In<KT>& x, Out& o) {
+  int i = literal_argmin<KT>(tb, x, false);
+  o.wait = 0.0;
+  if (i < 0) {  // None (empty mask) or the reference's ValueError (NaN best)
+    o.idx = -1; o.code = i == -1 ? SP_DEC_NONE : SP_DEC_ERROR; o.fill = 0;
+    o.obj = 0.0; o.slack = 0.0;
+    return;
+  }
+  int B = tb.batch[i];
+  double sk = pick_kind<KT>(x.s, tb.kind[i]);
+  double L = tb.lat[i];
+  if ((x.fl & SP_FLAG_ALLOW_DELAY) && B > x.av &&
+      (long long)x.sup >= (long long)B - (long long)x.av) {
+    const double wait = __dsub_rn(sk, L);
+    if (wait > 0.0) {
+      o.idx = i;
+      o.code = SP_DEC_DELAY | ((L < sk) ? SP_DEC_FEASIBLE : 0);
+      o.fill = x.av;
+      o.obj = (L < sk) ? tb.cost[i] : tb.costpen[i];
+      o.slack = sk;
+      o.wait = wait;
+      return;
+    }
+  }
+  if (B > x.av) {
+    const int i2 = literal_argmin<KT>(tb, x, true);
+    if (i2 == -2) {
+      o.idx = -1; o.code = SP_DEC_ERROR; o.fill = 0; o.obj = 0.0; o.slack = 0.0;
+      return;
+    }
+    if (i2 >= 0) i = i2;
+  }
+  B = tb.batch[i];
+  sk = pick_kind<KT>(x.s, tb.kind[i]);
+  L = tb.lat[i];
+  o.idx = i;
+  o.code = SP_DEC_ASSIGN | ((L < sk) ? SP_DEC_FEASIBLE : 0);
+  o.fill = min(B, x.av);
+  o.obj = (L < sk) ? tb.cost[i] : tb.costpen[i];
+  o.slack = sk;
+}
+
 template <int KT>
 __global__ void __launch_bounds__(256) k_select_scan(ScanPtrs sp_, int staged, SelectIO io) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -237,6 +325,7 @@ __global__ void __launch_bounds__(256) k_select_scan(ScanPtrs sp_, int staged, S
     double kmin[KT];
 #pragma unroll
     for (int k = 0; k < KT; ++k) kmin[k] = INFINITY;
+    bool sawnan = false;  // a NaN score among the admitted entries: literal restatement
     for (int j = 0; j < tb.M; ++j) {
       const int kj = tb.kind[j];
       const int bj = tb.batch[j];
@@ -245,14 +334,15 @@ __global__ void __launch_bounds__(256) k_select_scan(ScanPtrs sp_, int staged, S
       const double c = tb.cost[j];
       // configurator.py:226  score = cost + where(lat < slack, 0.0, penalty)
       const double sc = (L < sk) ? c : tb.costpen[j];
-      if (want_kmin) {
+      if (want_kmin) {  // numpy's min: NaN propagates
 #pragma unroll
         for (int k = 0; k < KT; ++k)
-          if (kj == k && sc < kmin[k]) kmin[k] = sc;
+          if (kj == k && (sc < kmin[k] || sc != sc)) kmin[k] = sc;
       }
       // mask: excluded kinds (259-263) and min_batch (264-265)
       const bool in1 = !((x.fl >> (SP_FLAG_EXCL_SHIFT + kj)) & 1u) && bj >= x.mb;
       if (in1) {
+        sawnan |= sc != sc;
         const double r = tb.res[j];
         const int id = tb.id[j];
         if (better(sc, c, r, id, b1)) { b1.j = j; b1.sc = sc; b1.c = c; b1.r = r; b1.id = id; }
@@ -270,6 +360,14 @@ __global__ void __launch_bounds__(256) k_select_scan(ScanPtrs sp_, int staged, S
     if (b1.j < 0) {
       o.idx = -1; o.code = SP_DEC_NONE; o.fill = 0;
       o.obj = 0.0; o.slack = 0.0; o.wait = 0.0;
+      store_out(io, i, o);
+      continue;
+    }
+    // a non-finite best (inf / NaN scores), or an infinite downgrade best: the reference's tie
+    // set reaches beyond the strict order — restate it literally
+    if (sawnan || !(b1.sc < INFINITY) ||
+        (tb.batch[b1.j] > x.av && b2.j >= 0 && !(b2.sc < INFINITY))) {
+      literal_select<KT>(tb, x, o);
       store_out(io, i, o);
       continue;
     }
@@ -331,7 +429,7 @@ __global__ void k_affinity(int N, int K, const double* __restrict__ kmin,
   double other = INFINITY;
   for (int k = 0; k < K; ++k) {
     double v = kmin[(size_t)i * K + k];
-    if (k != c && v < other) other = v;
+    if (k != c && (v < other || v != v)) other = v;  // numpy's min: NaN propagates
   }
   // configurator.py:318  float(score[~on].min() / score[on].min())
   out[i] = __ddiv_rn(other, kmin[(size_t)i * K + c]);
@@ -459,9 +557,11 @@ int slack_select_launch(sp_ctx* ctx, sp_dag* g, int n_tables, sp_table* const* t
   pp.n = n_tables;
   pp.hv = 0;
   size_t plan_bytes = 0, lut_bytes = 0;
-  bool fused = !getenv("SP_NO_K12");
+  bool fused = !getenv("SP_NO_K12") && K <= kMaxKinds && isfinite(alpha);
+  for (int t = 0; t < n_tables && fused; ++t)
+    fused = tables[t]->plan_ok && tables[t]->finite_safe();
   bool fast_ok = !getenv("SP_K12_GENERIC");
-  for (int t = 0; t < n_tables; ++t) {
+  for (int t = 0; t < n_tables && fused; ++t) {
     int rc;
     Plan* p = plan_get(ctx, tables[t], alpha, &rc);
     if (!p) return rc;
@@ -571,11 +671,15 @@ int select_launch(sp_ctx* ctx, int n_tables, sp_table* const* tables, double alp
 
   for (int t = 0; t < n_tables; ++t) {
     if (tables[t]->K != K) return fail(SP_E_INVALID, "select: tables disagree on kind count");
-    plan_ok = plan_ok && tables[t]->plan_ok;
-
+    // the staircase needs finite latencies and scores; otherwise the literal scan reproduces
+    // the reference's inf / NaN behaviour
+    plan_ok = plan_ok && tables[t]->plan_ok && tables[t]->finite_safe();
   }
+  plan_ok = plan_ok && isfinite(alpha);
   if (mode == SP_MODE_PLAN && !plan_ok)
-    return fail(SP_E_UNSUPPORTED, "select: staircase plan unsupported for this table");
+    return fail(SP_E_UNSUPPORTED, "select: staircase plan unsupported for this table (more than "
+                                  "16 batch sizes, 8 kinds or 32766 entries, or non-finite "
+                                  "latencies / alpha)");
   // AUTO: the staircase plan when it is current, or when the batch is large enough to pay for
   // a rebuild (a plan build costs about as much as scanning ~2^24 invocation x entry pairs);
   // otherwise the scan, which needs only cost / costpen (e.g. one call right after a
@@ -606,7 +710,7 @@ int select_launch(sp_ctx* ctx, int n_tables, sp_table* const* tables, double alp
     io.aligned = al(slack) && al(avail) && al(supply) && al(min_batch) && al(flags);
   }
   if (N == 0) return SP_OK;
-  const int KT = K <= 2 ? 2 : (K <= 4 ? 4 : 8);
+  const int KT = K <= 2 ? 2 : (K <= 4 ? 4 : (K <= 8 ? 8 : 24));
   if (use_plan) {
     PlanPtrs pp;
     pp.n = n_tables;
@@ -646,7 +750,8 @@ int select_launch(sp_ctx* ctx, int n_tables, sp_table* const* tables, double alp
   }
   if (KT == 2) return launch_scan_t<2>(ctx, sp_, stage, io);
   if (KT == 4) return launch_scan_t<4>(ctx, sp_, stage, io);
-  return launch_scan_t<8>(ctx, sp_, stage, io);
+  if (KT == 8) return launch_scan_t<8>(ctx, sp_, stage, io);
+  return launch_scan_t<24>(ctx, sp_, stage, io);
 }
 
 int affinity_launch(sp_ctx* ctx, int N, int K, const double* kmin, const int32_t* q,

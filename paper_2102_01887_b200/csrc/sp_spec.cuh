@@ -215,7 +215,9 @@ int speculate_launch(sp_ctx* ctx, int n_tables, sp_table* const* tables, double 
   SpecTabs tb;
   memset(&tb, 0, sizeof(tb));
   for (int t = 0; t < n_tables; ++t) {
-    if (!tables[t]->plan_ok) return fail(SP_E_UNSUPPORTED, "speculate: table without a plan");
+    if (!tables[t]->plan_ok || !tables[t]->finite_safe() || !isfinite(alpha))
+      return fail(SP_E_UNSUPPORTED, "speculate: table without a plan (batch sizes, entries, "
+                                    "kinds or non-finite latencies)");
     int rc;
     Plan* p = plan_get(ctx, tables[t], alpha, &rc);
     if (!p) return rc;
