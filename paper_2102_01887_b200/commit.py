@@ -114,7 +114,8 @@ def commit_candidates(tables: Sequence, slacks: Sequence[Mapping[str, float]],
     for j, (t, h) in enumerate(zip(tables, heads)):
         if h is None:
             continue
-        slack[0, j] = t.slack_array(slacks[j])
+        if slacks[j] is not None:  # else the head's candidate needs no slack (see _needs_slack)
+            slack[0, j] = t.slack_array(slacks[j])
         fill[0, j] = h.fill
         hid[0, j] = h.invocation_id
         hf[0, j] = _lib.SP_HEAD_PRESENT | (_lib.SP_HEAD_FORCED if h.forced else 0)
@@ -133,6 +134,18 @@ def commit_candidates(tables: Sequence, slacks: Sequence[Mapping[str, float]],
             float(r["obj"][0, j]))
 
 
+def _needs_slack(conf, op, head, full, fifo) -> bool:
+    """Whether Configurator._commit_candidate / pump_commits (configurator.py:657-728) call
+    slack_by_kind(op) for this head."""
+    if head is None:
+        return False
+    if head.forced:
+        return conf.tables[op].ref_entry.backend_kind not in full
+    if "eslc" in conf.ablations:
+        return head.spec_entry.backend_kind not in full and not fifo
+    return True
+
+
 def pump_commits(conf, buffered_count, topup) -> int:
     """Drop-in for ``Configurator.pump_commits`` (configurator.py:693-756) on a reference-shaped
     configurator whose ``tables`` are this package's ``OpTable``s.
@@ -149,14 +162,31 @@ def pump_commits(conf, buffered_count, topup) -> int:
     ops = list(conf.tables)
     tabs = [conf.tables[o] for o in ops]
     depths = [conf.depths[o] for o in ops]
+    fifo = "pbc" in conf.ablations
     while True:
         t0 = time.perf_counter()
         full = frozenset(k for k in conf.kinds if conf._cq_length(k) >= conf.cq_capacity[k])
         heads = [conf.sq_by_op[o][0] if conf.sq_by_op[o] else None for o in ops]
-        slacks = [conf.slack_by_kind(o) if h is not None else None for o, h in zip(ops, heads)]
-        best = commit_candidates(tabs, slacks, heads, [buffered_count(o) if h is not None else 0
-                                                       for o, h in zip(ops, heads)],
-                                 depths, full, conf.params.alpha, conf.ablations)
+        # slack_by_kind only where the reference evaluates it (it caches by weight version, so
+        # an extra call would fix a value the reference computes later, at a later clock):
+        # forced heads whose reference kind has room, eslc heads whose speculated kind has room
+        # and that need the affinity key (not pbc), every other head (its re-selection)
+        slacks = [conf.slack_by_kind(o) if _needs_slack(conf, o, h, full, fifo) else None
+                  for o, h in zip(ops, heads)]
+        try:
+            best = commit_candidates(tabs, slacks, heads,
+                                     [buffered_count(o) if h is not None else 0
+                                      for o, h in zip(ops, heads)],
+                                     depths, full, conf.params.alpha, conf.ablations)
+        except _lib.SlackpipeError:
+            # a shape the batched kernel does not take: the reference's own loop (its
+            # OpTable.select / affinity calls still run on the device) from this round on
+            from .speculate import _ORIGINAL
+
+            original = _ORIGINAL.get("pump_commits")
+            if original is None:
+                raise
+            return committed + original(conf, buffered_count, topup)
         if best is None:
             return committed
         j, entry, eidx, fill_target, slack_s, obj = best

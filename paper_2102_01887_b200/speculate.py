@@ -125,9 +125,19 @@ def speculate_from_buffer(conf, op: str, buffer) -> int:
     ratios = conf._path_ratios(op)
     sl0 = conf.slack_by_kind(op)
     w = pack_weights(conf, op_index, kinds)
-    r = speculate_batch(tables, conf.params.alpha, [conf._pool[k] for k in kinds], [op_index[op]],
-                        [len(buffer)], [conf._supply(op)], [now], [conf.target_s], [min(ratios)],
-                        [max(ratios)], [[sl0[k] for k in kinds]], [flags], *w)
+    try:
+        r = speculate_batch(tables, conf.params.alpha, [conf._pool[k] for k in kinds],
+                            [op_index[op]], [len(buffer)], [conf._supply(op)], [now],
+                            [conf.target_s], [min(ratios)], [max(ratios)],
+                            [[sl0[k] for k in kinds]], [flags], *w)
+    except _lib.SlackpipeError:
+        # shapes the batched kernel does not take (a table without a staircase plan, more than
+        # 64 weight keys in one call): the reference's own loop, whose OpTable.select calls still
+        # run on the device one at a time
+        original = _ORIGINAL.get("speculate_from_buffer")
+        if original is None:
+            raise
+        return original(conf, op, buffer)
     formed = int(r["n"][0])
     dt = (time.perf_counter() - t0) / max(1, formed + (r["delay_idx"][0] >= 0))
     for j in range(formed):
@@ -144,6 +154,10 @@ def speculate_from_buffer(conf, op: str, buffer) -> int:
         conf.speculate_times.append(dt)
     d = int(r["delay_idx"][0])
     if d >= 0:  # configurator.py:606-612: arm the batching hold once, then stop
+        if formed:
+            # the reference evaluated slack_by_kind at the top of this last iteration, after
+            # the enqueues above changed the weight version: leave its cache in that state
+            conf.slack_by_kind(op)
         if conf.holds.get(op) is None:
             deadline = conf._clock() + float(r["delay_wait"][0])
             conf.holds[op] = mod._Hold(deadline, table.entries[d].batch_size)
@@ -151,3 +165,23 @@ def speculate_from_buffer(conf, op: str, buffer) -> int:
                 conf._schedule_wake(deadline, ("hold", op))
         conf.speculate_times.append(dt)
     return formed
+
+
+# the reference Configurator's own methods, kept by install() for the shapes the batched kernels
+# do not take
+_ORIGINAL: dict = {}
+
+
+def install(configurator_cls) -> None:
+    """Replace ``Configurator.speculate_from_buffer`` and ``Configurator.pump_commits`` of the
+    reference class (slackpipe.configurator.Configurator) with the device drop-ins, keeping the
+    originals as their fallback for tables without a staircase plan."""
+    from . import commit as _commit
+
+    if "speculate_from_buffer" not in _ORIGINAL:
+        _ORIGINAL["speculate_from_buffer"] = configurator_cls.speculate_from_buffer
+        _ORIGINAL["pump_commits"] = configurator_cls.pump_commits
+    configurator_cls.speculate_from_buffer = (
+        lambda self, op, buffer: speculate_from_buffer(self, op, buffer))
+    configurator_cls.pump_commits = (
+        lambda self, buffered_count, topup: _commit.pump_commits(self, buffered_count, topup))

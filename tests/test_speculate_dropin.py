@@ -138,3 +138,67 @@ def test_speculate_and_commit_dropins_reproduce_the_reference_run(ref, monkeypat
     assert row[1:] == ["142.20064921472454", "132.73451153109434", "0.9334311218977895",
                        "0.16671542613566986", "1.0", "20", "0", "0"]
     assert hashlib.sha256(log.read_bytes()).hexdigest()[:16] == "4647eeb560b36a71"
+
+
+import pytest
+
+
+def _cli_run(cli, tmp, name, extra):
+    out = tmp / f"{name}.csv"
+    log = tmp / f"{name}.tsv"
+    rc = cli.main(["run", "--pipeline", str(BUNDLE / "pipeline.json"), "--scenario",
+                   str(BUNDLE / "scenario.json"), "--trace", str(BUNDLE / "trace.jsonl"),
+                   "--target", "142.20064921472454", "--metadata-dir", str(tmp / f"md_{name}"),
+                   "--report", str(out), "--decision-log", str(log), *extra])
+    assert rc == 0
+    return out.read_text().strip().splitlines()[-1].split(",")[1:], log.read_bytes()
+
+
+@pytest.mark.parametrize("extra", [["--ablate", "eslc"], ["--ablate", "pbc"], ["--ablate", "fb"],
+                                   ["--ablate", "eslc,pbc"], ["--failure-rate", "0.05"]],
+                         ids=["eslc", "pbc", "fb", "eslc+pbc", "failures"])
+def test_dropins_under_ablations_and_failures(ref, monkeypatch, tmp_path, extra):
+    """Both drop-ins under the eslc / pbc / fb ablations and with invocation failures (retries
+    re-enter through speculate_fixed): the run's CSV row and decision log equal the unmodified
+    reference's own run with the same flags, byte for byte — which also pins that the drop-ins
+    evaluate slack_by_kind exactly where the reference does (its per-version cache)."""
+    from slackpipe import cli, configurator
+
+    import paper_2102_01887_b200.commit as cdrop
+    import paper_2102_01887_b200.speculate as dropin
+
+    want_row, want_log = _cli_run(cli, tmp_path, "ref", extra)
+    box = [None]
+    monkeypatch.setattr(dropin, "speculate_batch", _fake_batch(box))
+    from oracle import commit as oc
+
+    def fake_candidates(tables, slacks, heads, buffered, depths, full_kinds, alpha, ablations=()):
+        conf = box[0]
+        kinds = list(conf.kinds)
+        otabs = _oracle_tables(conf)
+        full = sum(1 << kinds.index(k) for k in full_kinds)
+        sl = [np.array([s[k] for k in kinds]) if s is not None else None for s in slacks]
+        hs = [oc.Head(h.fill, h.forced, h.invocation_id, h.spec_eidx, h.spec_slack_s, h.spec_objective)
+              if h is not None else None for h in heads]
+        w = oc.round_winner(otabs, sl, hs, full, buffered, depths, alpha, fifo="pbc" in ablations,
+                            eslc="eslc" in ablations)
+        if w is None:
+            return None
+        j, (e, fill, s_k, obj) = w
+        return (j, tables[j].entries[e], e, fill, s_k, obj)
+
+    monkeypatch.setattr(cdrop, "commit_candidates", fake_candidates)
+
+    def spec(self, op, buffer):
+        box[0] = self
+        return dropin.speculate_from_buffer(self, op, buffer)
+
+    def pump(self, buffered_count, topup):
+        box[0] = self
+        return cdrop.pump_commits(self, buffered_count, topup)
+
+    monkeypatch.setattr(configurator.Configurator, "speculate_from_buffer", spec)
+    monkeypatch.setattr(configurator.Configurator, "pump_commits", pump)
+    row, log = _cli_run(cli, tmp_path, "dropin", extra)
+    assert row == want_row
+    assert log == want_log
