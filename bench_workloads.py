@@ -287,7 +287,7 @@ def run_c3(args):
                          "SURVEY.md §8(c))" if bad[0] == 0 else "MISMATCH"),
               "checked_on": f"all {world} rank(s), every (instance, op, kind) of the step"}
     # the same step through K1's per-source forward DP (SP_K1_CERT=0), reported beside it
-    os.environ["SP_K1_CERT"] = "0"
+    ctx.set_option("SP_K1_CERT", 1)  # off
     try:
         evf = _events(torch, args.steps)
         for i in range(args.steps):
@@ -297,7 +297,7 @@ def run_c3(args):
             evf[i][1].record(stream)
         torch.cuda.synchronize(dev)
     finally:
-        del os.environ["SP_K1_CERT"]
+        ctx.set_option("SP_K1_CERT", 0)
     fwd_ms = statistics.median([x.elapsed_time(y) for x, y in evf])
     if rank != 0:
         return

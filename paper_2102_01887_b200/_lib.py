@@ -62,6 +62,7 @@ SIGNATURES = {
     "sp_ctx_destroy": (C.c_int, [_p]),
     "sp_ctx_set_stream": (C.c_int, [_p, _p]),
     "sp_ctx_synchronize": (C.c_int, [_p]),
+    "sp_ctx_set_option": (C.c_int, [_p, C.c_char_p, _i64]),
     "sp_last_error": (C.c_char_p, [_p]),
     "sp_ctx_launch_count": (_i64, [_p]),
     "sp_table_create": (C.c_int, [_p, _i32, _p, _p, _p, _p, _p, _p, _p, _p, _i32, _i32, _pp]),
@@ -168,6 +169,11 @@ class Context:
 
     def synchronize(self) -> None:
         check(self.lib.sp_ctx_synchronize(self.handle))
+
+    def set_option(self, name: str, value: int) -> None:
+        """Dispatch variant of this context (tests / tools; the environment is read once, at
+        creation)."""
+        check(self.lib.sp_ctx_set_option(self.handle, name.encode(), int(value)))
 
     @property
     def launch_count(self) -> int:

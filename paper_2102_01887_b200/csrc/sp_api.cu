@@ -157,6 +157,52 @@ static void free_table(sp_table* t) {
   delete t;
 }
 
+static int env_int(const char* name, int def) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : def;
+}
+
+void options_from_env(Options& o) {
+  o.zero_copy = env_int("SP_ZERO_COPY", 1);
+  o.pipe_chunks = env_int("SP_PIPE_CHUNKS", 0);
+  if (const char* e = getenv("SP_K1_CERT")) o.k1_cert = !strcmp(e, "force") ? 2 : (!strcmp(e, "0") ? 1 : 0);
+  o.fold_long_min = env_int("SP_FOLD_LONG_MIN", 0);
+  o.stair_smem = getenv("SP_STAIR_SMEM") != nullptr;
+  o.stair_global = getenv("SP_STAIR_GLOBAL") != nullptr;
+  o.no_plan_graph = getenv("SP_NO_PLAN_GRAPH") != nullptr;
+  o.plan_legacy = getenv("SP_PLAN_LEGACY") != nullptr;
+  o.pc_debug = getenv("SP_PC_DEBUG") != nullptr;
+  if (const char* e = getenv("SP_K2_VARIANT")) o.k2_plan_only = strcmp(e, "fast") != 0;
+  o.k2f_threads = env_int("SP_K2F_THREADS", 512) == 1024 ? 1024 : 512;
+  o.no_pdl = getenv("SP_NO_PDL") != nullptr;
+  o.full_smem = getenv("SP_FULL_SMEM") != nullptr;
+  o.no_k12 = getenv("SP_NO_K12") != nullptr;
+  o.k12_generic = getenv("SP_K12_GENERIC") != nullptr;
+  o.k12_outstage = getenv("SP_K12_OUTSTAGE") != nullptr;
+  o.k12_generic_dp = getenv("SP_K12_GENERIC_DP") != nullptr;
+}
+
+int options_set(Options& o, const char* name, long long v) {
+  struct {
+    const char* n;
+    int* f;
+  } tab[] = {{"SP_ZERO_COPY", &o.zero_copy},     {"SP_PIPE_CHUNKS", &o.pipe_chunks},
+             {"SP_K1_CERT", &o.k1_cert},         {"SP_FOLD_LONG_MIN", &o.fold_long_min},
+             {"SP_STAIR_SMEM", &o.stair_smem},   {"SP_STAIR_GLOBAL", &o.stair_global},
+             {"SP_NO_PLAN_GRAPH", &o.no_plan_graph}, {"SP_PLAN_LEGACY", &o.plan_legacy},
+             {"SP_PC_DEBUG", &o.pc_debug},       {"SP_K2_VARIANT", &o.k2_plan_only},
+             {"SP_K2F_THREADS", &o.k2f_threads}, {"SP_NO_PDL", &o.no_pdl},
+             {"SP_FULL_SMEM", &o.full_smem},     {"SP_NO_K12", &o.no_k12},
+             {"SP_K12_GENERIC", &o.k12_generic}, {"SP_K12_OUTSTAGE", &o.k12_outstage},
+             {"SP_K12_GENERIC_DP", &o.k12_generic_dp}};
+  for (auto& x : tab)
+    if (!strcmp(x.n, name)) {
+      *x.f = (int)v;
+      return SP_OK;
+    }
+  return fail(SP_E_INVALID, std::string("set_option: unknown option ") + name);
+}
+
 }  // namespace sp
 
 using namespace sp;
@@ -180,7 +226,7 @@ int sp_ctx_create(int device, sp_ctx** out) {
   sp_ctx* c = new (std::nothrow) sp_ctx();
   if (!c) return fail(SP_E_NOMEM, "ctx_create: host allocation");
   c->device = device;
-  c->plan_legacy = getenv("SP_PLAN_LEGACY") != nullptr;
+  options_from_env(c->opt);
   c->num_sms = prop.multiProcessorCount;
   c->max_smem_optin = (int)prop.sharedMemPerBlockOptin;
   cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
@@ -231,6 +277,11 @@ int sp_ctx_set_stream(sp_ctx* ctx, void* stream) {
   ctx->plan_dirty = true;
   ctx->own_stream = false;
   return SP_OK;
+}
+
+int sp_ctx_set_option(sp_ctx* ctx, const char* name, int64_t value) {
+  if (!ctx || !name) return fail(SP_E_INVALID, "set_option: null argument");
+  return options_set(ctx->opt, name, (long long)value);
 }
 
 int sp_ctx_synchronize(sp_ctx* ctx) {
@@ -438,8 +489,8 @@ int sp_table_plan_image(sp_ctx* ctx, sp_table* t, double alpha, int32_t builder,
   if (!t->plan_ok) return fail(SP_E_UNSUPPORTED, "plan_image: the table has no staircase plan");
   if (builder == 2 && !t->pc_ok)
     return fail(SP_E_UNSUPPORTED, "plan_image: the table's shape is outside the cluster builder");
-  const bool saved = ctx->plan_legacy;
-  if (builder != 0) ctx->plan_legacy = builder == 1;
+  const int saved = ctx->opt.plan_legacy;
+  if (builder != 0) ctx->opt.plan_legacy = builder == 1;
   for (auto& p : t->plans)  // force a fresh build with the requested builder
     if (p.alpha == alpha || (p.alpha != p.alpha && alpha != alpha)) p.valid = false;
   int rc = SP_OK;
@@ -452,7 +503,7 @@ int sp_table_plan_image(sp_ctx* ctx, sp_table* t, double alpha, int32_t builder,
     p->builds = 0;
   }
   p = plan_get(ctx, t, alpha, &rc);
-  ctx->plan_legacy = saved;
+  ctx->opt.plan_legacy = saved;
   if (!p) return rc;
   PlanHdr h;
   SP_CUDA(cudaMemcpyAsync(&h, p->image, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
@@ -535,7 +586,7 @@ int select_batch_impl(sp_ctx* ctx, int32_t n_tables, sp_table* const* tables, do
   // reads its inputs and writes its outputs over PCIe itself — one launch, both link
   // directions busy at once, no copy-engine operations.
   {
-    const bool want = !getenv("SP_ZERO_COPY") || atoi(getenv("SP_ZERO_COPY")) != 0;
+    const bool want = ctx->opt.zero_copy != 0;
     struct Buf {
       const void* h;
       size_t bytes;
@@ -628,7 +679,7 @@ int select_batch_impl(sp_ctx* ctx, int32_t n_tables, sp_table* const* tables, do
   int nchunk = N >= 2 * kChunkMin
                    ? std::min(sp_ctx::kPipeChunks, (N + kChunkMin - 1) / kChunkMin)
                    : 1;
-  if (const char* e = getenv("SP_PIPE_CHUNKS")) nchunk = std::max(1, std::min(sp_ctx::kPipeChunks, atoi(e)));
+  if (ctx->opt.pipe_chunks > 0) nchunk = std::min(sp_ctx::kPipeChunks, ctx->opt.pipe_chunks);
   if (nchunk > 1 && !ctx->h2d) {
     SP_CUDA(cudaStreamCreateWithFlags(&ctx->h2d, cudaStreamNonBlocking));
     SP_CUDA(cudaStreamCreateWithFlags(&ctx->d2h, cudaStreamNonBlocking));
@@ -916,9 +967,8 @@ int sp_dag_create(sp_ctx* ctx, int32_t V, const int32_t* pred_ptr, const int32_t
   // relax many more edges than one backward pass over the graph does
   // (SP_K1_CERT=force builds it for every eligible graph — the parity tests use that)
   int E = pred_ptr[V];
-  const char* cf = getenv("SP_K1_CERT");
-  const bool force = cf && !strcmp(cf, "force");
-  const bool off = cf && !strcmp(cf, "0");
+  const bool force = ctx->opt.k1_cert == 2;
+  const bool off = ctx->opt.k1_cert == 1;
   if (e == cudaSuccess && !off && V <= kCertMaxV && n_val < 65536 &&
       (force || (int64_t)preds.size() >= 4 * (int64_t)(E + V))) {
     auto a16 = [](int x) { return (x + 15) & ~15; };

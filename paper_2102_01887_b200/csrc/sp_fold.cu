@@ -365,7 +365,7 @@ int fold_launch(sp_ctx* ctx, int n_tables, sp_table* const* tables, int n, const
   // segments longer than two windows take the block-parallel window path (measured on config 5:
   // 2 * win = 160 beats 512 — a 512-step sequential chain in one thread is the longer pole)
   int long_min = win >= (1 << 30) ? (1 << 30) : std::max(2 * win, 128);
-  if (const char* e = getenv("SP_FOLD_LONG_MIN")) long_min = std::max(2 * win, atoi(e));
+  if (ctx->opt.fold_long_min > 0) long_min = std::max(2 * win, ctx->opt.fold_long_min);
   const int long_cap = n / (long_min + 1) + 1;
   size_t a = ((size_t)n * 4 + 255) & ~(size_t)255;
   size_t gates_bytes = ((size_t)n_tables * sizeof(Gate) + 255) & ~(size_t)255;

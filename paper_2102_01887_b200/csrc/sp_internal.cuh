@@ -116,8 +116,36 @@ struct Plan {
 
 }  // namespace sp
 
+namespace sp {
+// Dispatch options of a context: read once from the environment when the context is created
+// (variable names as below), changeable per context with sp_ctx_set_option.  Variants exist for
+// the tests and the measurement tools; the defaults are the product path.
+struct Options {
+  int zero_copy = 1;         // SP_ZERO_COPY: pinned mapped host buffers read by the kernel
+  int pipe_chunks = 0;       // SP_PIPE_CHUNKS: pageable staging chunks (0 = by size)
+  int k1_cert = 0;           // SP_K1_CERT: 0 auto, 1 off ("0"), 2 force ("force")
+  int fold_long_min = 0;     // SP_FOLD_LONG_MIN: long-segment threshold of the fold (0 = default)
+  int stair_smem = 0;        // SP_STAIR_SMEM: multi-kernel builder, shared-memory staircase
+  int stair_global = 0;      // SP_STAIR_GLOBAL: multi-kernel builder, global staircase
+  int no_plan_graph = 0;     // SP_NO_PLAN_GRAPH: no CUDA-graph replay of plan builds
+  int plan_legacy = 0;       // SP_PLAN_LEGACY: multi-kernel plan builder
+  int pc_debug = 0;          // SP_PC_DEBUG: per-phase timestamps of the cluster builder
+  int k2_plan_only = 0;      // SP_K2_VARIANT (any value but "fast"): generic K2b only
+  int k2f_threads = 512;     // SP_K2F_THREADS: K2f block size (512 or 1024)
+  int no_pdl = 0;            // SP_NO_PDL: no programmatic dependent launch for K2f
+  int full_smem = 0;         // SP_FULL_SMEM: K2b requests the whole shared-memory budget
+  int no_k12 = 0;            // SP_NO_K12: K1 then K2 instead of the fused kernel
+  int k12_generic = 0;       // SP_K12_GENERIC: fused kernel without the K2f decision core
+  int k12_outstage = 0;      // SP_K12_OUTSTAGE: staged decision stores in K12
+  int k12_generic_dp = 0;    // SP_K12_GENERIC_DP: generic DP in K12 for path-list graphs
+};
+void options_from_env(Options& o);
+int options_set(Options& o, const char* name, long long value);
+}  // namespace sp
+
 struct sp_ctx {
   int device = 0;
+  sp::Options opt;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   int num_sms = 0;
@@ -126,8 +154,7 @@ struct sp_ctx {
   // a plan image was (re)written by a kernel that no select launch has waited on yet: the
   // next K2f launch must not read any plan before its griddepcontrol.wait
   bool plan_dirty = true;
-  // SP_PLAN_LEGACY (read once at creation): build plans with the multi-kernel builder
-  bool plan_legacy = false;
+
   // grow-only device arena for staged host I/O
   void* io_dev = nullptr;
   size_t io_cap = 0;

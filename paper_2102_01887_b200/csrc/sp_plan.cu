@@ -1492,7 +1492,7 @@ static int plan_enqueue(sp_ctx* ctx, sp_table* t, Plan& p) {
     SP_CUDA(cudaMalloc(&p.cost, sizeof(double) * M));
     SP_CUDA(cudaMalloc(&p.costpen, sizeof(double) * M));
   }
-  const bool cluster = t->plan_ok && t->pc_ok && !ctx->plan_legacy;
+  const bool cluster = t->plan_ok && t->pc_ok && !ctx->opt.plan_legacy;
   if (!cluster) {
     k_cost<<<(M + 255) / 256, 256, 0, st>>>(M, t->lat, t->res, t->batch, t->pool, t->price,
                                             p.alpha, p.cost, p.costpen);
@@ -1580,7 +1580,7 @@ static int plan_enqueue(sp_ctx* ctx, sp_table* t, Plan& p) {
     SP_CUDA(cudaFuncSetAttribute(k_stair_lanes<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  kStairLanesSmem));
   }
-  if (max_mk <= kStairLanesMax && !getenv("SP_STAIR_SMEM") && !getenv("SP_STAIR_GLOBAL")) {
+  if (max_mk <= kStairLanesMax && !ctx->opt.stair_smem && !ctx->opt.stair_global) {
     k_stair_stage<<<(M + 255) / 256, 256, 0, st>>>(M, K, ki, t->order, t->bidx, t->lat, t->r1,
                                                    t->r2, t->pos_r12, t->pos_meta, t->pos_lat);
     SP_CHECK_LAUNCH(ctx);
@@ -1596,7 +1596,7 @@ static int plan_enqueue(sp_ctx* ctx, sp_table* t, Plan& p) {
                                                          t->rowscratch, t->rows_per_kind,
                                                          t->candf, t->cands, t->pos_r12,
                                                          t->pos_meta, t->pos_lat);
-  } else if (max_mk <= kStairSmemMax && !getenv("SP_STAIR_GLOBAL"))
+  } else if (max_mk <= kStairSmemMax && !ctx->opt.stair_global)
     k_stair_smem<<<K, 1024, kStairSmemBytes, st>>>(M, K, W, ki, t->order, t->bidx, t->lat, t->r1,
                                                    t->r2, t->thrscratch, t->rowscratch,
                                                    t->rows_per_kind, t->candf, t->cands);
@@ -1656,7 +1656,7 @@ static int plan_finish(sp_ctx* ctx, Plan& p, sp_table* t) {
 }
 
 int plan_build(sp_ctx* ctx, sp_table* t, Plan& p) {
-  if (p.graph && !getenv("SP_NO_PLAN_GRAPH")) {
+  if (p.graph && !ctx->opt.no_plan_graph) {
     SP_CUDA(cudaGraphLaunch(p.graph, ctx->stream));
     if (t->plan_ok) SP_CUDA(cudaEventRecord(p.hdr_ready, ctx->stream));
     ctx->launches += p.graph_kernels;
@@ -1667,7 +1667,7 @@ int plan_build(sp_ctx* ctx, sp_table* t, Plan& p) {
     p.version = t->version;
     return SP_OK;
   }
-  if (p.builds == 0 || getenv("SP_NO_PLAN_GRAPH")) {  // first build: allocations happen here
+  if (p.builds == 0 || ctx->opt.no_plan_graph) {  // first build: allocations happen here
     ++p.builds;
     const int rc = plan_enqueue(ctx, t, p);
     if (rc == SP_OK && t->plan_ok) SP_CUDA(cudaEventRecord(p.hdr_ready, ctx->stream));

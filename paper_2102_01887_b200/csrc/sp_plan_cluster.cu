@@ -1887,7 +1887,7 @@ int plan_cluster_launch(sp_ctx* ctx, sp_table* t, Plan& p, int W, const PlanHdr&
   }
   for (int k = 0; k <= kMaxKinds; ++k) a.seg_lo[k] = k <= t->K ? t->pc_seg_lo[k] : t->pc_nseg;
   a.hdr = hdr;
-  a.debug = getenv("SP_PC_DEBUG") != nullptr;
+  a.debug = ctx->opt.pc_debug;
   // shared memory: the largest phase (segment: 60 B per slot; candidates 16 B; thresholds 8 B
   // per record in the shared-memory fallback; rows 64 KB)
   const int es = t->pc_max_seg > 2 * kPcThreads ? 4 : (t->pc_max_seg > kPcThreads ? 2 : 1);

@@ -447,10 +447,9 @@ int launch_plan_t(sp_ctx* ctx, const PlanPtrs& pp, const SelectIO& io) {
     SP_CUDA(cudaFuncSetAttribute(k_select_plan<KT>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kPlanSmemBudget));
   }
-  const char* variant = getenv("SP_K2_VARIANT");
   const bool single = pp.hv && pp.n == 1 && !io.out_kind_min;
   // specialised kernel (sp_k2f.cuh) for the common shape; SP_K2_VARIANT=plan forces K2b
-  if (single && io.K == KT && !(variant && strcmp(variant, "fast"))) {
+  if (single && io.K == KT && !ctx->opt.k2_plan_only) {
     bool ok = pp.h.lut_n > 0 && io.out_idx && io.out_code && io.out_fill && io.out_obj &&
               io.out_slack && io.out_wait;
     for (int k = 0; k < KT && ok; ++k) ok = pp.h.kd[k].pad[0] == 0;  // positive thresholds
@@ -460,7 +459,7 @@ int launch_plan_t(sp_ctx* ctx, const PlanPtrs& pp, const SelectIO& io) {
       // block size: 512 threads x 2 CTAs per SM (default: as CTAs of one launch retire, the
       // next launch's CTAs take their place one at a time — measured 15.9 -> 15.5 us per
       // 2^20-decision step back to back) or 1024 x 1 (SP_K2F_THREADS=1024)
-      const int thr = (getenv("SP_K2F_THREADS") && atoi(getenv("SP_K2F_THREADS")) == 1024) ? 1024 : 512;
+      const int thr = ctx->opt.k2f_threads == 1024 ? 1024 : 512;
       static uint64_t fast_attr[2] = {0, 0};
       if (attr_once(fast_attr[thr == 512])) {
         if (thr == 512)
@@ -486,7 +485,7 @@ int launch_plan_t(sp_ctx* ctx, const PlanPtrs& pp, const SelectIO& io) {
       cfg.stream = ctx->stream;
       cudaLaunchAttribute attr[1];
       attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-      attr[0].val.programmaticStreamSerializationAllowed = getenv("SP_NO_PDL") ? 0 : 1;
+      attr[0].val.programmaticStreamSerializationAllowed = ctx->opt.no_pdl ? 0 : 1;
       cfg.attrs = attr;
       cfg.numAttrs = 1;
       if (thr == 512)
@@ -503,7 +502,7 @@ int launch_plan_t(sp_ctx* ctx, const PlanPtrs& pp, const SelectIO& io) {
   if (need < blocks) blocks = need > 0 ? need : 1;
   // request only the shared memory the staged plan needs when its size is known on the host
   int smem = kPlanSmemBudget;
-  if (pp.hv && pp.n == 1 && !getenv("SP_FULL_SMEM"))
+  if (pp.hv && pp.n == 1 && !ctx->opt.full_smem)
     smem = std::min(kPlanSmemBudget, ((pp.h.total_bytes + 1023) / 1024) * 1024);
   k_select_plan<KT><<<blocks, kPlanThreads, smem, ctx->stream>>>(pp, smem, io);
   SP_CHECK_LAUNCH(ctx);
@@ -557,10 +556,10 @@ int slack_select_launch(sp_ctx* ctx, sp_dag* g, int n_tables, sp_table* const* t
   pp.n = n_tables;
   pp.hv = 0;
   size_t plan_bytes = 0, lut_bytes = 0;
-  bool fused = !getenv("SP_NO_K12") && K <= kMaxKinds && isfinite(alpha);
+  bool fused = !ctx->opt.no_k12 && K <= kMaxKinds && isfinite(alpha);
   for (int t = 0; t < n_tables && fused; ++t)
     fused = tables[t]->plan_ok && tables[t]->finite_safe();
-  bool fast_ok = !getenv("SP_K12_GENERIC");
+  bool fast_ok = !ctx->opt.k12_generic;
   for (int t = 0; t < n_tables && fused; ++t) {
     int rc;
     Plan* p = plan_get(ctx, tables[t], alpha, &rc);
@@ -587,7 +586,7 @@ int slack_select_launch(sp_ctx* ctx, sp_dag* g, int n_tables, sp_table* const* t
   const size_t plans_all = plan_bytes + (fast_ok ? lut_bytes : 0);
   // decisions staged for coalesced stores only on request (SP_K12_OUTSTAGE=1): without it the
   // per-warp area holds just the 16 input bytes per decision and more CTAs stay resident
-  const int out_stage = (getenv("SP_K12_OUTSTAGE") || !out_fill || !out_obj || !out_slack ||
+  const int out_stage = (ctx->opt.k12_outstage || !out_fill || !out_obj || !out_slack ||
                          !out_wait) ? 1 : 0;
   const size_t stage = (size_t)kK12Warps * 32 * n_tables * (out_stage ? kK12StageBytesPerDecision : 16);
   const size_t refs = (size_t)kK12Warps * g->n_val * 32 * sizeof(double);
@@ -601,7 +600,7 @@ int slack_select_launch(sp_ctx* ctx, sp_dag* g, int n_tables, sp_table* const* t
     io.N = N; io.K = K;
     K12Dag kg{g->prog, g->prog_ptr, g->preds, g->pred_ptr, g->n_src, g->max_slots,
               (int)g->prog_len, (int)g->pred_len, g->n_val,
-              getenv("SP_K12_GENERIC_DP") ? 0 : g->single_pred};
+              ctx->opt.k12_generic_dp ? 0 : g->single_pred};
     K12In ki{ref, ref_stride, target, now, Q, I, out_kslack};
     auto launch = [&](auto kern) -> int {
       // one entry per k_slack_select instantiation, per device

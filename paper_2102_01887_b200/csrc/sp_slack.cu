@@ -397,8 +397,7 @@ int slack_launch(sp_ctx* ctx, sp_dag* g, int I, const double* ref, int ref_strid
                  const double* target, const double* now, int K, const double* Q,
                  double* out_slack, double* out_ratio) {
   if (I == 0) return SP_OK;
-  const char* ce = getenv("SP_K1_CERT");
-  if (g->cert && !(ce && !strcmp(ce, "0"))) {
+  if (g->cert && ctx->opt.k1_cert != 1) {
     const int nfw = (g->n_src + 31) / 32;
     const size_t smem = (size_t)g->cert_bytes +
                         (size_t)kCertWarps * ((size_t)(g->V + 1) * 256 + (size_t)g->V * 160 +

@@ -378,15 +378,30 @@ def test_pinned_host_buffers_zero_copy(gpu_ctx, N):
         t.close()
 
 
-@pytest.mark.parametrize("variant", ["SP_STAIR_SMEM", "SP_STAIR_GLOBAL", "SP_NO_PLAN_GRAPH"])
-def test_staircase_builder_variants_vs_oracle(gpu_ctx, variant, monkeypatch):
-    """The fallback staircase builders (shared-memory run scans for kinds of 8,193-16,384
-    entries, the global-memory builder above that) and the un-graphed rebuild path give the same
-    plans as the default lane-scan builder: forced on ordinary tables, plus a 20,000-entry kind
-    that takes the global builder on its own."""
+@pytest.mark.parametrize("variant", ["SP_STAIR_SMEM", "SP_STAIR_GLOBAL", "SP_NO_PLAN_GRAPH",
+                                     "SP_PLAN_LEGACY", "cluster"])
+def test_staircase_builder_variants_vs_oracle(gpu_ctx, variant):
+    """Every plan builder against the C oracle: the one-kernel cluster builder (default), the
+    multi-kernel builder (SP_PLAN_LEGACY) with its fallback staircases (shared-memory run scans
+    for kinds of 8,193-16,384 entries, the global-memory builder above that) and the un-graphed
+    rebuild path — on ordinary tables plus a 20,000-entry kind (beyond the cluster builder's
+    8,192, so it takes the multi-kernel global builder on its own)."""
     import paper_2102_01887_b200 as sp
 
-    monkeypatch.setenv(variant, "1")
+    opts = {"SP_STAIR_SMEM": ["SP_PLAN_LEGACY", "SP_STAIR_SMEM"],
+            "SP_STAIR_GLOBAL": ["SP_PLAN_LEGACY", "SP_STAIR_GLOBAL"],
+            "SP_NO_PLAN_GRAPH": ["SP_NO_PLAN_GRAPH"], "SP_PLAN_LEGACY": ["SP_PLAN_LEGACY"],
+            "cluster": []}[variant]
+    for o in opts:
+        gpu_ctx.set_option(o, 1)
+    try:
+        _builder_variant_cases(sp, variant)
+    finally:
+        for o in opts:
+            gpu_ctx.set_option(o, 0)
+
+
+def _builder_variant_cases(sp, variant):
     rng = np.random.default_rng(hash(variant) & 0xFFFF)
     for M, nB, K in ((3000, 8, 2), (1500, 16, 4), (20000, 8, 1)):
         t = _random_table(rng, M, nB, K)

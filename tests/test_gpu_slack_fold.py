@@ -103,9 +103,11 @@ def test_deep_dag_certified_pass_equals_forward_dp(gpu_ctx, monkeypatch):
     for refs, t, n, q in ((ref, T, now, Q), (tie, T[:4000], now[:4000], Q[:4000])):
         g = SlackGraph.from_dag(dag)
         got = g.slack_batch(refs, t, n, q, ratios=True)
-        monkeypatch.setenv("SP_K1_CERT", "0")
-        exp = g.slack_batch(refs, t, n, q, ratios=True)
-        monkeypatch.delenv("SP_K1_CERT")
+        gpu_ctx.set_option("SP_K1_CERT", 1)  # off: K1's forward DP
+        try:
+            exp = g.slack_batch(refs, t, n, q, ratios=True)
+        finally:
+            gpu_ctx.set_option("SP_K1_CERT", 0)
         g.close()
         for key in ("slack", "ratio"):
             assert np.array_equal(bits(got[key]), bits(exp[key])), key
@@ -114,8 +116,11 @@ def test_deep_dag_certified_pass_equals_forward_dp(gpu_ctx, monkeypatch):
 def test_dag_slack_certified_forced_vs_reference(gpu_ctx, monkeypatch):
     """The 400 reference DAG cases with K1c forced on every graph (SP_K1_CERT=force), small
     integer-valued refs included: bit-identical to the reference's compute_slack."""
-    monkeypatch.setenv("SP_K1_CERT", "force")
-    test_dag_slack_vs_reference_compute_slack(gpu_ctx)
+    gpu_ctx.set_option("SP_K1_CERT", 2)  # force
+    try:
+        test_dag_slack_vs_reference_compute_slack(gpu_ctx)
+    finally:
+        gpu_ctx.set_option("SP_K1_CERT", 0)
 
 
 def _fold_tables(d, m, lo):
