@@ -50,3 +50,44 @@ assert np.array_equal(a["slack"].view(np.uint64), b["slack"].view(np.uint64))
 idx = rng.integers(0, len(table.lat), 4000).astype(np.int32)
 sp.observation_quantiles([table], None, idx, rng.uniform(0.1, 2.0, 4000), 0.9)
 print("sanitize smoke ok", int((out["best"] >= 0).sum()))
+# round 2: the one-kernel cluster plan builder (cached-order and re-sorted builds, config-5
+# table), the literal scan with non-finite latencies and K > 8, the pinned per-call path,
+# affinity batch, the simulated backend and the single-process device group
+import math  # noqa: E402
+
+t5 = sp.OpTable(synth.synth_spec(True), synth.synth_scenario())
+inv5 = synth.synth_invocations(1024, t5.lat, t5.gkind, seed=3)
+for step in range(3):
+    r5 = t5.select_batch(inv5.slack, 100.0, inv5.avail, upstream_supply=inv5.supply,
+                         min_batch=inv5.min_batch, flags=inv5.flags, mode="plan")
+    t5.set_latency(int(step * 37), float(t5.lat[step * 37]) * 1.3)  # forces a re-sort
+t5.plan_image(100.0, "cluster")
+t5.select({"cpu": 1.0, "gpu": 2.0}, 100.0, 4, allow_delay=True, upstream_supply=3)
+t5.affinity("gpu", {"cpu": 1.0, "gpu": 2.0}, 100.0)
+t5.set_latency(3, math.inf)
+t5.set_latency(9, math.nan)
+try:
+    t5.select({"cpu": 1.0, "gpu": 2.0}, 100.0, 4, allow_delay=True)
+except ValueError:
+    pass
+rng = np.random.default_rng(2)
+K10 = 10
+wide = sp.RawTable(lat=rng.uniform(0.1, 3, 3000), res=rng.integers(1, 8, 3000), batch=rng.integers(1, 40, 3000),
+                   pool=np.full(3000, 64.0), price=np.full(3000, 1e-5), kind=rng.integers(0, K10, 3000),
+                   id_rank=rng.permutation(3000), K=K10)
+sp.select_batch([wide], rng.uniform(-1, 4, (300, K10)), 100.0, np.full(300, 8, np.int32),
+                upstream_supply=np.zeros(300, np.int32), min_batch=np.ones(300, np.int32),
+                flags=np.zeros(300, np.uint32), kind_min=True)
+import torch  # noqa: E402
+
+d_out = {k: torch.from_numpy(np.ascontiguousarray(v)).cuda() for k, v in
+         (("code", np.ones(64, np.int32)), ("idx", np.arange(64, dtype=np.int32)),
+          ("fill", np.ones(64, np.int32)))}
+sp.simulate_observations(d_out, torch.ones(len(t5.lat), dtype=torch.float64, device="cuda"),
+                         torch.ones(64, dtype=torch.float64, device="cuda"))
+torch.cuda.synchronize()
+grp = sp.DeviceGroup([0, 0])
+gt = grp.table(synth.synth_spec(False), synth.synth_scenario())
+gt.select_batch(inv.slack, 100.0, inv.avail, upstream_supply=inv.supply, min_batch=inv.min_batch,
+                flags=inv.flags)
+print("sanitize smoke ok")
