@@ -62,13 +62,31 @@ struct Gate {
   double ratio;
 };
 
+// Sort keys, and per table the number of keys below and equal to its reference entry's key
+// (refcnt[2t], refcnt[2t+1]; zeroed by the caller) — the reference segment's bounds in the
+// sorted order, so k_fold_ref needs no search.
 __global__ void k_fold_keys(int n, FoldTabs ft, const int32_t* __restrict__ op,
-                            const int32_t* __restrict__ idx, uint32_t* keys, uint32_t* pos) {
-  int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= n) return;
-  int t = op ? op[j] : 0;
-  keys[j] = idx[j] < 0 ? (uint32_t)ft.total : (uint32_t)(ft.t[t].gbase + idx[j]);
-  pos[j] = (uint32_t)j;
+                            const int32_t* __restrict__ idx, uint32_t* keys, uint32_t* pos,
+                            int* refcnt) {
+  __shared__ int s_c[2 * kMaxFoldTables];
+  for (int i = threadIdx.x; i < 2 * ft.n; i += blockDim.x) s_c[i] = 0;
+  __syncthreads();
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < n) {
+    const int t = op ? op[j] : 0;
+    const uint32_t key = idx[j] < 0 ? (uint32_t)ft.total : (uint32_t)(ft.t[t].gbase + idx[j]);
+    keys[j] = key;
+    pos[j] = (uint32_t)j;
+    for (int u = 0; u < ft.n; ++u) {
+      if (ft.t[u].ref_index < 0) continue;
+      const uint32_t rk = (uint32_t)(ft.t[u].gbase + ft.t[u].ref_index);
+      if (key < rk) atomicAdd(&s_c[2 * u], 1);
+      else if (key == rk) atomicAdd(&s_c[2 * u + 1], 1);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 2 * ft.n; i += blockDim.x)
+    if (s_c[i]) atomicAdd(&refcnt[i], s_c[i]);
 }
 
 __device__ __forceinline__ double ewma(double beta, double obs, double old) {
@@ -158,7 +176,21 @@ __device__ void fold_bounds(const double* __restrict__ sobs, int q, int end, dou
   __shared__ int sbad[32];
   double m = L, M = L;
   int bad = isfinite(L) ? 0 : 1;
-  for (int u = q + threadIdx.x; u < end; u += blockDim.x) {
+  // eight independent loads in flight per thread (the segment is read once, latency-bound)
+  const int step = blockDim.x;
+  int u = q + threadIdx.x;
+  for (; u + 7 * step < end; u += 8 * step) {
+    double o[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) o[k] = __ldg(sobs + u + k * step);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      bad |= isfinite(o[k]) ? 0 : 1;
+      m = o[k] < m ? o[k] : m;
+      M = o[k] > M ? o[k] : M;
+    }
+  }
+  for (; u < end; u += step) {
     const double o = __ldg(sobs + u);
     bad |= isfinite(o) ? 0 : 1;
     m = o < m ? o : m;
@@ -195,8 +227,7 @@ __device__ void fold_bounds(const double* __restrict__ sobs, int q, int end, dou
 __global__ void k_fold_ref(int n, FoldTabs ft, const uint32_t* __restrict__ skeys,
                            const uint32_t* __restrict__ spos, const double* __restrict__ sobs,
                            double beta, int win, int dfp_count, int dfp_on, int fb_frozen,
-                           Gate* gates, int* long_count) {
-  __shared__ int seg[2];
+                           Gate* gates, int* long_count, const int* __restrict__ refcnt) {
   __shared__ double bnd[2];
   __shared__ int bnd_ok;
   const int t = blockIdx.x;
@@ -206,13 +237,8 @@ __global__ void k_fold_ref(int n, FoldTabs ft, const uint32_t* __restrict__ skey
     if (threadIdx.x == 0) gates[t] = Gate{0, -1, 1.0};
     return;
   }
-  const uint32_t key = (uint32_t)(tb.gbase + tb.ref_index);
-  if (threadIdx.x == 0) {
-    seg[0] = lower_bound_u32(skeys, n, key);
-    seg[1] = lower_bound_u32(skeys, n, key + 1);
-  }
-  __syncthreads();
-  const int q = seg[0], end = seg[1], cnt = end - q;
+  // the reference entry's segment of the sorted keys: [#keys below it, + #keys equal)
+  const int q = refcnt[2 * t], cnt = refcnt[2 * t + 1], end = q + cnt;
   const double L0 = tb.lat[tb.ref_index];
   const bool bounded = !fb_frozen && cnt > win;
   if (bounded) fold_bounds(sobs, q, end, L0, bnd, &bnd_ok);
@@ -272,7 +298,15 @@ __global__ void k_fold_seg(int n, FoldTabs ft, const uint32_t* __restrict__ skey
   const FoldTab& tb = ft.t[t];
   const int e = (int)key - tb.gbase;
   if (e == tb.ref_index) return;  // folded by k_fold_ref
-  const int end = lower_bound_u32(skeys, n, key + 1);
+  // a segment longer than long_min is known from one probe; only those search for their end
+  const bool is_long = q + long_min < n && skeys[q + long_min] == key;
+  int end;
+  if (is_long) {
+    end = lower_bound_u32(skeys, n, key + 1);
+  } else {  // the end lies within the next long_min positions: a short search there
+    const int lim = min(n, q + long_min + 1);
+    end = q + 1 + lower_bound_u32(skeys + q + 1, lim - q - 1, key + 1);
+  }
   const int cnt = end - q;
   const int before = tb.obs_count[e];
   if (!fb_frozen) {
@@ -282,7 +316,7 @@ __global__ void k_fold_seg(int n, FoldTabs ft, const uint32_t* __restrict__ skey
     // rescaled by recalibrate_unobserved before its first fold
     if (g.lifted && before == 0 && (int)spos[q] > g.gate_pos)
       L = __dmul_rn(tb.lat_init[e], g.ratio);
-    if (cnt > long_min) {
+    if (is_long) {
       const int j = atomicAdd(long_count, 1);
       long_q[j] = LongSeg{q, end, tb.lat + e, L, 0};
     } else {
@@ -371,7 +405,7 @@ int fold_launch(sp_ctx* ctx, int n_tables, sp_table* const* tables, int n, const
   size_t gates_bytes = ((size_t)n_tables * sizeof(Gate) + 255) & ~(size_t)255;
   size_t long_bytes = ((size_t)long_cap * sizeof(LongSeg) + 256 + 255) & ~(size_t)255;
   size_t total = 4 * a + gates_bytes + long_bytes + cub_bytes + 256 +
-                 (((size_t)n * 8 + 255) & ~(size_t)255);
+                 (((size_t)n * 8 + 255) & ~(size_t)255) + 256 * 2;
   int rc = SP_OK;
   uint8_t* base = (uint8_t*)ctx_tmp(ctx, total, &rc);
   if (!base) return rc;
@@ -385,8 +419,10 @@ int fold_launch(sp_ctx* ctx, int n_tables, sp_table* const* tables, int n, const
   void* cub_tmp = base + 4 * a + gates_bytes + long_bytes;
   double* sobs = (double*)(base + 4 * a + gates_bytes + long_bytes +
                            ((cub_bytes + 255) & ~(size_t)255));
+  int* refcnt = (int*)((uint8_t*)sobs + (((size_t)n * 8 + 255) & ~(size_t)255));
+  SP_CUDA(cudaMemsetAsync(refcnt, 0, sizeof(int) * 2 * kMaxFoldTables, st));
   if (n > 0) {
-    k_fold_keys<<<(n + 255) / 256, 256, 0, st>>>(n, ft, op, idx, keys, pos);
+    k_fold_keys<<<(n + 255) / 256, 256, 0, st>>>(n, ft, op, idx, keys, pos, refcnt);
     SP_CHECK_LAUNCH(ctx);
     SP_CUDA(cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, keys, skeys, pos, spos, n, 0,
                                             end_bit, st));
@@ -395,7 +431,7 @@ int fold_launch(sp_ctx* ctx, int n_tables, sp_table* const* tables, int n, const
     SP_CHECK_LAUNCH(ctx);
   }
   k_fold_ref<<<n_tables, 256, 0, st>>>(n, ft, skeys, spos, sobs, beta, win, dfp_count, dfp_on,
-                                       fb_frozen, gates, long_count);
+                                       fb_frozen, gates, long_count, refcnt);
   SP_CHECK_LAUNCH(ctx);
   if (n > 0) {
     k_fold_seg<<<(n + 255) / 256, 256, 0, st>>>(n, ft, skeys, spos, sobs, beta, fb_frozen,
