@@ -279,8 +279,8 @@ int sp_commit_round(sp_ctx* ctx, int32_t R, int32_t n_ops, sp_table* const* tabl
  * invocations formed, in order, at out_off[r] .. out_off[r] + out_n[r] (the caller reserves
  * out_off[r+1] - out_off[r] >= n_buf[r] slots): out_idx entry, out_fill items, out_slack
  * Decision.slack_s, out_obj objective (NaN when forced); out_delay_idx[r] / out_delay_wait[r]
- * the delay decision that stopped the loop (-1 when the buffer emptied).  out_n[r] = -1 when a
- * call touched more than 64 distinct weight keys (SP_E_UNSUPPORTED is returned). */
+ * the delay decision that stopped the loop (-1 when the buffer emptied).  A call may touch any
+ * number of weight keys. */
 int sp_speculate_batch(sp_ctx* ctx, int32_t n_tables, sp_table* const* tables, double alpha,
                        int32_t K, const double* pool, int32_t R, const int32_t* op,
                        const int32_t* n_buf, const int32_t* supply, const double* now,

@@ -1205,7 +1205,7 @@ extern "C" int sp_speculate_batch(sp_ctx* ctx, int32_t n_tables, sp_table* const
     return speculate_launch(ctx, n_tables, tables, alpha, K, pool, R, op, n_buf, supply, now,
                             target, rmin, rmax, slack0, flags, w_ptr, w_tab, w_eidx, w_count,
                             out_off, out_idx, out_fill, out_slack, out_obj, out_n,
-                            out_delay_idx, out_delay_wait);
+                            out_delay_idx, out_delay_wait, -1, -1);
   if (mem != SP_MEM_HOST) return fail(SP_E_INVALID, "speculate: bad mem flag");
   // host-side validation of everything the kernel indexes
   const size_t nw = (size_t)2 * K * R;
@@ -1275,7 +1275,7 @@ extern "C" int sp_speculate_batch(sp_ctx* ctx, int32_t n_tables, sp_table* const
   SP_CUDA(up(d_off, out_off, 4 * (size_t)(R + 1)));
   rc = speculate_launch(ctx, n_tables, tables, alpha, K, pool, R, d_op, d_n, d_sup, d_now, d_tgt,
                         d_rmin, d_rmax, d_s0, d_fl, d_wp, d_wt, d_we, d_wc, d_off, o_idx, o_fill,
-                        o_sl, o_ob, o_n, o_di, o_dw);
+                        o_sl, o_ob, o_n, o_di, o_dw, W, O);
   if (rc != SP_OK) return rc;
   auto down = [&](void* dst, const void* src, size_t bytes) {
     return bytes ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st) : cudaSuccess;
@@ -1289,7 +1289,8 @@ extern "C" int sp_speculate_batch(sp_ctx* ctx, int32_t n_tables, sp_table* const
   SP_CUDA(down(out_delay_wait, o_dw, 8 * (size_t)R));
   SP_CUDA(cudaStreamSynchronize(st));
   for (int r = 0; r < R; ++r)
-    if (out_n[r] < 0) return fail(SP_E_UNSUPPORTED, "speculate: a call touched more than 64 weight keys");
+    if (out_n[r] < 0)  // a select with no admissible entry inside the loop (configurator.py:605)
+      return fail(SP_E_RUNTIME, "speculate: select returned None inside the speculation loop");
   return SP_OK;
 }
 

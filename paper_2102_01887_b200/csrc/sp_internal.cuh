@@ -361,7 +361,8 @@ int speculate_launch(sp_ctx* ctx, int n_tables, sp_table* const* tables, double 
                      const uint32_t* flags, const int32_t* w_ptr, const int32_t* w_tab,
                      const int32_t* w_eidx, const int32_t* w_count, const int32_t* out_off,
                      int32_t* out_idx, int32_t* out_fill, double* out_slack, double* out_obj,
-                     int32_t* out_n, int32_t* out_delay_idx, double* out_delay_wait);
+                     int32_t* out_n, int32_t* out_delay_idx, double* out_delay_wait,
+                     int n_weights = -1, int n_slots = -1);
 int slack_launch(sp_ctx* ctx, sp_dag* g, int I, const double* ref, int ref_stride,
                  const double* target, const double* now, int K, const double* Q,
                  double* out_slack, double* out_ratio);

@@ -13,12 +13,14 @@
 //            batching hold has expired (597-599); a delay decision ends the loop (606-612);
 //   update — buffered -= fill; _weights_add(SQ, kind, op, entry, +1) (553-561): an existing key
 //            is incremented in place, a new key appended after the kind's list.
-// The input weight lists are read-only; the call's increments and new keys live in a small
-// per-thread list (kMaxSpecKeys), so the Eq. 2 order is: input SQ entries (count + increment),
-// then the call's new keys of the kind in append order, then the CQ entries.
+// The input weight lists are read-only; the call's increments of input SQ keys live in a
+// global array indexed like the weights (winc, zeroed per launch) and its new keys in a global
+// list indexed like its output slots (a call forms at most as many invocations — and so new
+// keys — as it has slots), so there is no per-call key limit and no per-thread key array.  The
+// Eq. 2 order is: input SQ entries (count + increment), then the call's new keys of the kind in
+// append order, then the CQ entries.
 
 constexpr int kMaxSpecTables = 64;
-constexpr int kMaxSpecKeys = 64;
 
 struct SpecTabs {
   const double* lat[kMaxSpecTables];
@@ -48,16 +50,19 @@ struct SpecIO {
   int32_t* out_fill;
   double* out_slack;
   double* out_obj;
-  int32_t* out_n;  // -1: the call needed more than kMaxSpecKeys new / incremented keys
+  int32_t* out_n;
   int32_t* out_delay_idx;
   double* out_delay_wait;
+  int32_t* winc;     // per input weight: this call's increments (zeroed)
+  int32_t* nkey_id;  // per output slot: a new key (tab << 20 | kind << 16 | eidx)
+  int32_t* nkey_cnt;
   int R;
   int K;
 };
 
-struct SpecKey {
-  int32_t kind, tab, eidx, cnt, orig;  // orig: input SQ position incremented, -1 new key
-};
+__device__ __forceinline__ int32_t key_id(int tab, int kind, int eidx) {
+  return (tab << 20) | (kind << 16) | eidx;
+}
 
 template <int KT>
 __global__ void __launch_bounds__(128) k_speculate(SpecTabs tb, double alpha, SpecIO io,
@@ -75,8 +80,8 @@ __global__ void __launch_bounds__(128) k_speculate(SpecTabs tb, double alpha, Sp
   bool first = true, overflow = false;
   const int32_t* wp = io.w_ptr;
   View<KT> v;
-  SpecKey keys[kMaxSpecKeys];
   In<KT> x;
+  int last_id = -1, last_w = -1, last_q = -1;  // the previous formed invocation's key
   auto start = [&](int rr) {  // load call rr's state
     op = io.op[rr];
     n = io.n_buf[rr];
@@ -92,6 +97,7 @@ __global__ void __launch_bounds__(128) k_speculate(SpecTabs tb, double alpha, Sp
     nd = 0;
     first = true;
     overflow = false;
+    last_id = last_w = last_q = -1;
     io.out_delay_idx[rr] = -1;
     io.out_delay_wait[rr] = 0.0;
   };
@@ -111,16 +117,16 @@ __global__ void __launch_bounds__(128) k_speculate(SpecTabs tb, double alpha, Sp
         }
         double total = 0.0;  // configurator.py:516-522
         for (int w = wp[k]; w < wp[k + 1]; ++w) {  // SQ, in dict order
-          int c = io.w_count[w];
-          for (int q = 0; q < nk; ++q) c += keys[q].orig == w ? keys[q].cnt : 0;
+          const int c = io.w_count[w] + io.winc[w];
           const int t = io.w_tab[w], e = io.w_eidx[w];
           total = __dadd_rn(total, __dmul_rn((double)c, __dmul_rn(tb.lat[t][e], tb.res[t][e])));
         }
         for (int q = 0; q < nk; ++q) {  // keys this call appended to the kind's SQ dict
-          if (keys[q].orig >= 0 || keys[q].kind != k) continue;
-          const int t = keys[q].tab, e = keys[q].eidx;
-          total = __dadd_rn(total,
-                            __dmul_rn((double)keys[q].cnt, __dmul_rn(tb.lat[t][e], tb.res[t][e])));
+          const int id = io.nkey_id[o0 + q];
+          if (((id >> 16) & 15) != k) continue;
+          const int t = id >> 20, e = id & 0xFFFF;
+          total = __dadd_rn(total, __dmul_rn((double)io.nkey_cnt[o0 + q],
+                                             __dmul_rn(tb.lat[t][e], tb.res[t][e])));
         }
         for (int w = wp[K + k]; w < wp[K + k + 1]; ++w) {  // CQ
           const int t = io.w_tab[w], e = io.w_eidx[w];
@@ -165,24 +171,33 @@ __global__ void __launch_bounds__(128) k_speculate(SpecTabs tb, double alpha, Sp
       if (!done) {
         first = false;
         n -= fill;
-        // _weights_add(self._sq_weight, kind, op, idx, +1)
-        int hit = -1;
-        for (int q = 0; q < nk; ++q)
-          if (keys[q].kind == kd && keys[q].tab == op && keys[q].eidx == idx) hit = q;
-        if (hit < 0) {
-          int orig = -1;
+        // _weights_add(self._sq_weight, kind, op, idx, +1): an input key (increment), else a
+        // key this call appended (count), else a new key at the end of the kind's dict
+        const int id = key_id(op, kd, idx);
+        if (id == last_id) {
+          if (last_w >= 0) io.winc[last_w] += 1; else io.nkey_cnt[o0 + last_q] += 1;
+        } else {
+          int w_hit = -1;
           for (int w = wp[kd]; w < wp[kd + 1]; ++w)
-            if (io.w_tab[w] == op && io.w_eidx[w] == idx) orig = w;
-          if (nk == kMaxSpecKeys) {
-            overflow = true;
-            done = true;
+            if (io.w_tab[w] == op && io.w_eidx[w] == idx) w_hit = w;
+          int q_hit = -1;
+          if (w_hit < 0)
+            for (int q = 0; q < nk; ++q)
+              if (io.nkey_id[o0 + q] == id) q_hit = q;
+          if (w_hit >= 0) {
+            io.winc[w_hit] += 1;
+          } else if (q_hit >= 0) {
+            io.nkey_cnt[o0 + q_hit] += 1;
           } else {
-            keys[nk] = SpecKey{kd, op, idx, 0, orig};
-            hit = nk++;
+            q_hit = nk++;
+            io.nkey_id[o0 + q_hit] = id;
+            io.nkey_cnt[o0 + q_hit] = 1;
           }
+          last_id = id;
+          last_w = w_hit;
+          last_q = q_hit;
         }
-        if (!done) {
-          keys[hit].cnt += 1;
+        {
           io.out_idx[o0 + nd] = idx;
           io.out_fill[o0 + nd] = fill;
           io.out_slack[o0 + nd] = s_k;
@@ -209,7 +224,8 @@ int speculate_launch(sp_ctx* ctx, int n_tables, sp_table* const* tables, double 
                      const uint32_t* flags, const int32_t* w_ptr, const int32_t* w_tab,
                      const int32_t* w_eidx, const int32_t* w_count, const int32_t* out_off,
                      int32_t* out_idx, int32_t* out_fill, double* out_slack, double* out_obj,
-                     int32_t* out_n, int32_t* out_delay_idx, double* out_delay_wait) {
+                     int32_t* out_n, int32_t* out_delay_idx, double* out_delay_wait,
+                     int n_weights, int n_slots) {
   if (n_tables > kMaxSpecTables) return fail(SP_E_UNSUPPORTED, "speculate: more than 64 tables");
   if (K > 8) return fail(SP_E_UNSUPPORTED, "speculate: more than 8 kinds");
   SpecTabs tb;
@@ -245,7 +261,34 @@ int speculate_launch(sp_ctx* ctx, int n_tables, sp_table* const* tables, double 
   sel.K = K;
   SpecIO io{op, n_buf, supply, now, target, rmin, rmax, slack0, flags, w_ptr, w_tab, w_eidx,
             w_count, out_off, out_idx, out_fill, out_slack, out_obj, out_n, out_delay_idx,
-            out_delay_wait, R, K};
+            out_delay_wait, nullptr, nullptr, nullptr, R, K};
+  {  // per-weight increments (zeroed) and per-slot new keys, after the select outputs
+    int32_t nw = n_weights, nslots = n_slots;
+    if (nw < 0 || nslots < 0) {  // device-resident arguments: read the two totals
+      SP_CUDA(cudaMemcpyAsync(&nw, w_ptr + (size_t)2 * K * R, sizeof(int32_t),
+                              cudaMemcpyDeviceToHost, ctx->stream));
+      SP_CUDA(cudaMemcpyAsync(&nslots, out_off + R, sizeof(int32_t), cudaMemcpyDeviceToHost,
+                              ctx->stream));
+      SP_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
+    const size_t a1 = ((size_t)std::max(nw, 1) * 4 + 255) & ~(size_t)255;
+    const size_t a2 = ((size_t)std::max(nslots, 1) * 4 + 255) & ~(size_t)255;
+    uint8_t* k = static_cast<uint8_t*>(ctx_tmp(ctx, 6 * al + a1 + 2 * a2, &rc));
+    if (!k) return rc;
+    if (k != s) {  // the scratch moved: re-point the select outputs
+      s = k;
+      sel.out_idx = reinterpret_cast<int32_t*>(s);
+      sel.out_code = reinterpret_cast<int32_t*>(s + al);
+      sel.out_fill = reinterpret_cast<int32_t*>(s + 2 * al);
+      sel.out_obj = reinterpret_cast<double*>(s + 3 * al);
+      sel.out_slack = reinterpret_cast<double*>(s + 4 * al);
+      sel.out_wait = reinterpret_cast<double*>(s + 5 * al);
+    }
+    io.winc = reinterpret_cast<int32_t*>(s + 6 * al);
+    io.nkey_id = reinterpret_cast<int32_t*>(s + 6 * al + a1);
+    io.nkey_cnt = reinterpret_cast<int32_t*>(s + 6 * al + a1 + a2);
+    SP_CUDA(cudaMemsetAsync(io.winc, 0, (size_t)std::max(nw, 1) * 4, ctx->stream));
+  }
   // persistent grid: resident CTAs only (calls are taken by grid stride)
   int per_sm = 0;
   if (K <= 2)

@@ -131,9 +131,8 @@ def speculate_from_buffer(conf, op: str, buffer) -> int:
                             [conf.target_s], [min(ratios)], [max(ratios)],
                             [[sl0[k] for k in kinds]], [flags], *w)
     except _lib.SlackpipeError:
-        # shapes the batched kernel does not take (a table without a staircase plan, more than
-        # 64 weight keys in one call): the reference's own loop, whose OpTable.select calls still
-        # run on the device one at a time
+        # shapes the batched kernel does not take (a table without a staircase plan): the
+        # reference's own loop, whose OpTable.select calls still run on the device one at a time
         original = _ORIGINAL.get("speculate_from_buffer")
         if original is None:
             raise
