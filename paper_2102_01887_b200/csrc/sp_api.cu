@@ -167,6 +167,7 @@ void options_from_env(Options& o) {
   o.pipe_chunks = env_int("SP_PIPE_CHUNKS", 0);
   if (const char* e = getenv("SP_K1_CERT")) o.k1_cert = !strcmp(e, "force") ? 2 : (!strcmp(e, "0") ? 1 : 0);
   o.fold_long_min = env_int("SP_FOLD_LONG_MIN", 0);
+  o.fold_legacy = getenv("SP_FOLD_LEGACY") != nullptr;
   o.stair_smem = getenv("SP_STAIR_SMEM") != nullptr;
   o.stair_global = getenv("SP_STAIR_GLOBAL") != nullptr;
   o.no_plan_graph = getenv("SP_NO_PLAN_GRAPH") != nullptr;
@@ -188,6 +189,7 @@ int options_set(Options& o, const char* name, long long v) {
     int* f;
   } tab[] = {{"SP_ZERO_COPY", &o.zero_copy},     {"SP_PIPE_CHUNKS", &o.pipe_chunks},
              {"SP_K1_CERT", &o.k1_cert},         {"SP_FOLD_LONG_MIN", &o.fold_long_min},
+             {"SP_FOLD_LEGACY", &o.fold_legacy},
              {"SP_STAIR_SMEM", &o.stair_smem},   {"SP_STAIR_GLOBAL", &o.stair_global},
              {"SP_NO_PLAN_GRAPH", &o.no_plan_graph}, {"SP_PLAN_LEGACY", &o.plan_legacy},
              {"SP_PC_DEBUG", &o.pc_debug},       {"SP_K2_VARIANT", &o.k2_plan_only},

@@ -32,6 +32,7 @@
 #include <stdlib.h>
 
 #include <cub/cub.cuh>
+#include <cub/block/block_radix_sort.cuh>
 
 #include "sp_internal.cuh"
 
@@ -355,9 +356,9 @@ __global__ void k_fold_rescale(FoldTabs ft, const Gate* __restrict__ gates) {
 
 }  // namespace
 
-int fold_launch(sp_ctx* ctx, int n_tables, sp_table* const* tables, int n, const int32_t* op,
-                const int32_t* idx, const double* obs, double beta, int dfp_count, int dfp_on,
-                int fb_frozen) {
+static int fold_launch_legacy(sp_ctx* ctx, int n_tables, sp_table* const* tables, int n,
+                              const int32_t* op, const int32_t* idx, const double* obs,
+                              double beta, int dfp_count, int dfp_on, int fb_frozen) {
   if (n_tables > kMaxFoldTables) return fail(SP_E_UNSUPPORTED, "fold: at most 64 tables");
   FoldTabs ft;
   ft.n = n_tables;
@@ -450,6 +451,492 @@ int fold_launch(sp_ctx* ctx, int n_tables, sp_table* const* tables, int n, const
   }
   for (int t = 0; t < n_tables; ++t) tables[t]->version++;
   return SP_OK;
+}
+
+
+// ---- one-kernel fold (default) ----------------------------------------------------------------
+//
+// The multi-kernel path above sorts the whole batch with a device-wide radix sort (several
+// passes sized for millions of keys) and then folds in five more launches.  A config-5 batch is
+// 65,536 records over a few hundred distinct entries, so the fold is latency-bound, not
+// bandwidth-bound.  k_fold_coop does the whole batch in ONE cooperative launch (every CTA
+// resident, grid barriers between phases), per chunk of up to 64 tiles x 1024 records:
+//
+//   phase A (CTA per tile): a block radix sort of the tile's keys (stable: positions ascend
+//     inside a key), the sorted observations written out; every run (one entry's records inside
+//     the tile) publishes (start, length) in the entry's per-tile slot, sets the tile's bit in
+//     the entry's 64-bit tile mask (the first setter appends the entry to the touched list),
+//     and folds its min / max into the entry's bounds (warp-segmented scan, one atomic pair per
+//     run and warp); reference runs add to the table's reference count.
+//   grid barrier; every CTA evaluates, per table, whether the gate lifts in this chunk
+//     (k = dfp_count - completed_ref_before in [1, reference count]).
+//   phase B (only when a gate lifts): one warp per lifting table folds the reference entry up to
+//     its k-th observation (ratio = lat / lat_init, configurator.py:486) and on; grid barrier.
+//   phase C (warp per touched entry): the entry's runs in tile order from the mask and slots;
+//     the rescale rule of the multi-kernel path (never observed before the batch, first
+//     observation after the gate); the EWMA fold in completion order — the coalescing window
+//     over the last `win` observations when the bounds allow it, else sequentially — staged
+//     through a per-warp shared-memory buffer; counts; the entry's mask / bounds reset.
+//   grid barrier; phase D: completed_ref, the per-chunk counters reset, and (when a gate lifted)
+//     the rescale of every entry still unobserved (configurator.py:486-490).
+//
+// Splitting a batch into consecutive chunks folds exactly as one batch does (the multi-kernel
+// path's chunked tests rely on the same property).
+namespace {
+
+constexpr int kCoopThreads = 1024;
+constexpr int kCoopTile = kCoopThreads;        // records per tile (one per thread)
+constexpr int kCoopTiles = 64;                 // tiles per chunk (one mask bit each)
+constexpr int kCoopChunk = kCoopTile * kCoopTiles;
+constexpr int kCoopWarpBuf = 256;              // observations staged per warp
+constexpr int kCoopWarps = kCoopThreads / 32;
+
+struct CoopState {  // persistent per context; zero (lo: ~0) outside a launch
+  uint32_t bar[2];      // grid barrier: arrivals, generation
+  int32_t touched_n[2];  // per chunk parity
+  int32_t refcnt[2][kMaxFoldTables];
+};
+
+struct CoopArgs {
+  FoldTabs ft;
+  int n;
+  const int32_t* op;
+  const int32_t* idx;
+  const double* obs;
+  double beta;
+  int win;
+  int dfp_count, dfp_on, fb_frozen;
+  int end_bit;
+  uint32_t* skey;   // chunk: per tile sorted keys
+  uint32_t* spos;   // chunk: global stream positions in sorted order
+  double* sobs;     // chunk: observations in sorted order
+  uint64_t* mask;   // per key: tiles of the chunk holding the key
+  uint64_t* lo;     // per key: order-key minimum of the chunk's observations
+  uint64_t* hi;     // per key: order-key maximum
+  uint32_t* slot;   // per key x kCoopTiles: run start | length << 16
+  int32_t* touched; // chunk: keys with at least one observation
+  Gate* gates;      // per table
+  CoopState* st;
+};
+
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Grid-wide barrier (all CTAs are co-resident: cooperative launch).
+__device__ __forceinline__ void coop_sync(uint32_t* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t gen = ld_acquire_u32(bar + 1);
+    __threadfence();
+    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+      atomicExch(bar, 0u);
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (ld_acquire_u32(bar + 1) == gen) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ uint64_t fold_okey(double x) {
+  return order_key(static_cast<uint64_t>(__double_as_longlong(x)));
+}
+__device__ __forceinline__ double fold_unkey(uint64_t k) {
+  const uint64_t u = (k >> 63) ? (k & 0x7FFFFFFFFFFFFFFFull) : ~k;
+  return __longlong_as_double(static_cast<long long>(u));
+}
+
+// The runs of one key in tile order, staged in shared memory by a warp: rstart[r] = index of
+// the run's first record in the chunk arrays, rcum[r] = records before run r (rcum[nr] = cnt).
+struct WarpRuns {
+  int32_t rstart[kCoopTiles];
+  int32_t rcum[kCoopTiles + 1];
+  int32_t nr;
+};
+
+__device__ __forceinline__ int runs_load(const CoopArgs& a, uint32_t key, WarpRuns& R) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t m = a.mask[key];
+  int cnt = 0;
+  for (int h = 0; h < 2; ++h) {
+    const int tl = lane + 32 * h;
+    const bool has = (m >> tl) & 1ull;
+    uint32_t sv = 0;
+    if (has) sv = a.slot[(size_t)key * kCoopTiles + tl];
+    const int len = has ? (int)(sv >> 16) : 0;
+    // rank of this run among the key's runs, and records before it
+    const uint64_t below = tl ? (m & ((1ull << tl) - 1ull)) : 0ull;
+    const int r = __popcll(below);
+    int pre = len;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, pre, off);
+      if (lane >= off) pre += y;
+    }
+    pre -= len;  // exclusive within this half
+    if (has) {
+      R.rstart[r] = tl * kCoopTile + (int)(sv & 0xFFFFu);
+      R.rcum[r] = cnt + pre;
+    }
+    cnt += __shfl_sync(0xffffffffu, pre + len, 31);
+  }
+  if (lane == 0) {
+    R.nr = __popcll(m);
+    R.rcum[__popcll(m)] = cnt;
+  }
+  __syncwarp();
+  return cnt;
+}
+
+// chunk-array index of the entry's ordinal-th observation
+__device__ __forceinline__ int runs_at(const WarpRuns& R, int ordinal) {
+  int lo = 0, hi = R.nr - 1;  // last run with rcum <= ordinal
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (R.rcum[mid] <= ordinal) lo = mid; else hi = mid - 1;
+  }
+  return R.rstart[lo] + (ordinal - R.rcum[lo]);
+}
+
+// Warp-cooperative exact fold of the entry's observations [o0, o1) from L (result valid in
+// every lane).  With `bounded` (lo..hi holds every chain value) a window of the last `win`
+// observations is tried first; it returns the exact value whenever the two bound chains meet.
+__device__ double coop_fold(const CoopArgs& a, const WarpRuns& R, double* buf, double L, int o0,
+                            int o1, bool bounded, double lo, double hi) {
+  const int lane = threadIdx.x & 31;
+  const double ob = a.beta, ol = __dsub_rn(1.0, a.beta);
+  if (bounded && o1 - o0 > a.win && a.win <= kCoopWarpBuf) {
+    const int w0 = o1 - a.win;
+    for (int u = lane; u < a.win; u += 32) buf[u] = a.sobs[runs_at(R, w0 + u)];
+    __syncwarp();
+    int same = 0;
+    double v = 0.0;
+    if (lane == 0) {
+      double x = lo, y = hi;
+      for (int u = 0; u < a.win; ++u) {
+        const double t = __dmul_rn(ob, buf[u]);
+        x = __dadd_rn(t, __dmul_rn(ol, x));
+        y = __dadd_rn(t, __dmul_rn(ol, y));
+      }
+      v = x;
+      same = __double_as_longlong(x) == __double_as_longlong(y);
+    }
+    same = __shfl_sync(0xffffffffu, same, 0);
+    v = __shfl_sync(0xffffffffu, v, 0);
+    __syncwarp();
+    if (same) return v;
+  }
+  for (int p0 = o0; p0 < o1; p0 += kCoopWarpBuf) {
+    const int p1 = min(o1, p0 + kCoopWarpBuf);
+    for (int u = p0 + lane; u < p1; u += 32) buf[u - p0] = a.sobs[runs_at(R, u)];
+    __syncwarp();
+    if (lane == 0)
+      for (int u = 0; u < p1 - p0; ++u) L = __dadd_rn(__dmul_rn(ob, buf[u]), __dmul_rn(ol, L));
+    __syncwarp();
+  }
+  return __shfl_sync(0xffffffffu, L, 0);
+}
+
+// bounds of every chain value from the chunk's observation range of `key` and the start L
+__device__ __forceinline__ bool coop_bounds(const CoopArgs& a, uint32_t key, double L, double* lo,
+                                            double* hi) {
+  double m = fold_unkey(a.lo[key]), M = fold_unkey(a.hi[key]);
+  if (!(isfinite(m) && isfinite(M) && isfinite(L))) return false;
+  m = L < m ? L : m;
+  M = L > M ? L : M;
+  *lo = m - fabs(m) * 0x1p-20 - 0x1p-1000;
+  *hi = M + fabs(M) * 0x1p-20 + 0x1p-1000;
+  return true;
+}
+
+__device__ __forceinline__ bool gate_lifts(const CoopArgs& a, const FoldTab& tb, int refcnt) {
+  if (a.fb_frozen || !a.dfp_on || tb.ref_index < 0 || refcnt <= 0) return false;
+  const int k = a.dfp_count - tb.counters[0];
+  return k >= 1 && k <= refcnt && tb.lat_init[tb.ref_index] > 0.0;
+}
+
+__global__ void __launch_bounds__(kCoopThreads, 1) k_fold_coop(const __grid_constant__ CoopArgs a) {
+  using Sort = cub::BlockRadixSort<uint32_t, kCoopThreads, 1, uint32_t, 6>;
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ uint32_t s_key[kCoopTile];
+  __shared__ uint64_t s_lift;  // tables whose gate lifts in this chunk
+  auto& tmp = *reinterpret_cast<typename Sort::TempStorage*>(smem);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  WarpRuns& R = reinterpret_cast<WarpRuns*>(smem)[warp];
+  double* buf = reinterpret_cast<double*>(smem + sizeof(WarpRuns) * kCoopWarps) + warp * kCoopWarpBuf;
+  const uint32_t sent = (uint32_t)a.ft.total;
+  CoopState* st = a.st;
+  for (int c0 = 0, chunk = 0; c0 < a.n; c0 += kCoopChunk, ++chunk) {
+    const int par = chunk & 1;
+    const int nrec = min(kCoopChunk, a.n - c0);
+    const int ntiles = (nrec + kCoopTile - 1) / kCoopTile;
+    // ---- phase A ----
+    for (int tl = blockIdx.x; tl < ntiles; tl += gridDim.x) {
+      const int j = c0 + tl * kCoopTile + (int)threadIdx.x;
+      uint32_t key[1] = {sent}, val[1] = {(uint32_t)j};
+      if (j < a.n) {
+        const int e = a.idx[j];
+        if (e >= 0) key[0] = (uint32_t)(a.ft.t[a.op ? a.op[j] : 0].gbase + e);
+      }
+      __syncthreads();  // tmp / s_key reuse across tiles
+      Sort(tmp).Sort(key, val, 0, a.end_bit);
+      const uint32_t k = key[0];
+      s_key[threadIdx.x] = k;
+      const int q = tl * kCoopTile + (int)threadIdx.x;  // chunk-array index
+      const double o = k != sent ? a.obs[val[0]] : 0.0;
+      a.skey[q] = k;
+      a.spos[q] = val[0];
+      a.sobs[q] = o;
+      __syncthreads();
+      // warp-segmented min / max of the run inside this warp (keys are sorted)
+      uint64_t mn = fold_okey(o), mx = mn;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t ko = __shfl_up_sync(0xffffffffu, k, off);
+        const uint64_t a0 = __shfl_up_sync(0xffffffffu, mn, off);
+        const uint64_t a1 = __shfl_up_sync(0xffffffffu, mx, off);
+        if (lane >= off && ko == k) {
+          mn = a0 < mn ? a0 : mn;
+          mx = a1 > mx ? a1 : mx;
+        }
+      }
+      const bool last_in_warp = lane == 31 || s_key[threadIdx.x + 1] != k;
+      if (k != sent) {
+        if (last_in_warp) {
+          atomicMin(reinterpret_cast<unsigned long long*>(a.lo + k), (unsigned long long)mn);
+          atomicMax(reinterpret_cast<unsigned long long*>(a.hi + k), (unsigned long long)mx);
+        }
+        if (threadIdx.x == 0 || s_key[threadIdx.x - 1] != k) {  // run head
+          int lo = (int)threadIdx.x + 1, hi = kCoopTile;  // first position with a larger key
+          while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (s_key[mid] <= k) lo = mid + 1; else hi = mid;
+          }
+          const int len = lo - (int)threadIdx.x;
+          a.slot[(size_t)k * kCoopTiles + tl] = threadIdx.x | (uint32_t)len << 16;
+          const unsigned long long old =
+              atomicOr(reinterpret_cast<unsigned long long*>(a.mask + k), 1ull << tl);
+          if (old == 0ull) a.touched[atomicAdd(&st->touched_n[par], 1)] = (int32_t)k;
+          const int t = table_of_key(a.ft, k);
+          if ((int)k - a.ft.t[t].gbase == a.ft.t[t].ref_index) atomicAdd(&st->refcnt[par][t], len);
+        }
+      }
+    }
+    coop_sync(st->bar);
+    // ---- gates of this chunk (uniform in every CTA) ----
+    if (threadIdx.x == 0) {
+      uint64_t lift = 0;
+      for (int t = 0; t < a.ft.n; ++t)
+        if (gate_lifts(a, a.ft.t[t], ld_acquire_u32((const uint32_t*)&st->refcnt[par][t])))
+          lift |= 1ull << t;
+      s_lift = lift;
+    }
+    __syncthreads();
+    const uint64_t lift = s_lift;
+    if (lift) {  // ---- phase B: the reference entries of the lifting tables ----
+      const int gw = blockIdx.x * kCoopWarps + warp;
+      for (int t = gw; t < a.ft.n; t += gridDim.x * kCoopWarps) {
+        if (!((lift >> t) & 1ull)) continue;
+        const FoldTab& tb = a.ft.t[t];
+        const uint32_t rk = (uint32_t)(tb.gbase + tb.ref_index);
+        const int cnt = runs_load(a, rk, R);
+        const int k = a.dfp_count - tb.counters[0];
+        double L = tb.lat[tb.ref_index], lo = 0.0, hi = 0.0;
+        const bool bd = cnt > a.win && coop_bounds(a, rk, L, &lo, &hi);
+        L = coop_fold(a, R, buf, L, 0, k, bd, lo, hi);
+        const double ratio = __ddiv_rn(L, tb.lat_init[tb.ref_index]);  // configurator.py:486
+        const int gpos = (int)a.spos[runs_at(R, k - 1)];
+        L = coop_fold(a, R, buf, L, k, cnt, bd, lo, hi);
+        if (lane == 0) {
+          tb.lat[tb.ref_index] = L;
+          tb.obs_count[tb.ref_index] += cnt;
+          a.gates[t] = Gate{1, gpos, ratio};
+          a.mask[rk] = 0ull;
+          a.lo[rk] = ~0ull;
+          a.hi[rk] = 0ull;
+        }
+        __syncwarp();
+      }
+      coop_sync(st->bar);
+    }
+    // ---- phase C: every touched entry (warp each) ----
+    {
+      const int nt = ld_acquire_u32((const uint32_t*)&st->touched_n[par]);
+      for (int u = blockIdx.x * kCoopWarps + warp; u < nt; u += gridDim.x * kCoopWarps) {
+        const uint32_t key = (uint32_t)a.touched[u];
+        const int t = table_of_key(a.ft, key);
+        const FoldTab& tb = a.ft.t[t];
+        const int e = (int)key - tb.gbase;
+        if (((lift >> t) & 1ull) && e == tb.ref_index) continue;  // phase B
+        const int cnt = runs_load(a, key, R);
+        const int before = tb.obs_count[e];
+        if (!a.fb_frozen) {
+          double L = tb.lat[e];
+          if ((lift >> t) & 1ull) {
+            const Gate g = a.gates[t];
+            if (before == 0 && (int)a.spos[R.rstart[0]] > g.gate_pos)
+              L = __dmul_rn(tb.lat_init[e], g.ratio);
+          }
+          double lo = 0.0, hi = 0.0;
+          const bool bd = cnt > a.win && coop_bounds(a, key, L, &lo, &hi);
+          L = coop_fold(a, R, buf, L, 0, cnt, bd, lo, hi);
+          if (lane == 0) tb.lat[e] = L;
+        }
+        if (lane == 0) {
+          tb.obs_count[e] = before + cnt;
+          a.mask[key] = 0ull;
+          a.lo[key] = ~0ull;
+          a.hi[key] = 0ull;
+        }
+        __syncwarp();
+      }
+    }
+    coop_sync(st->bar);
+    // ---- phase D ----
+    if (blockIdx.x == 0 && threadIdx.x < a.ft.n) {
+      const int t = threadIdx.x;
+      a.ft.t[t].counters[0] += st->refcnt[par][t];
+      st->refcnt[par][t] = 0;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) st->touched_n[par] = 0;
+    if (lift) {
+      for (int t = 0; t < a.ft.n; ++t) {
+        if (!((lift >> t) & 1ull)) continue;
+        const FoldTab& tb = a.ft.t[t];
+        const double ratio = a.gates[t].ratio;
+        for (int e = blockIdx.x * kCoopThreads + threadIdx.x; e < tb.M; e += gridDim.x * kCoopThreads)
+          if (e != tb.ref_index && tb.obs_count[e] == 0)
+            tb.lat[e] = __dmul_rn(tb.lat_init[e], ratio);  // configurator.py:490
+      }
+    }
+    // the next chunk's phase C reads counters / latencies written here: its phase-A barrier
+    // orders them
+  }
+}
+
+// Persistent state of the one-kernel fold: per-key masks / bounds / slots (sized for the
+// largest key space seen), chunk arrays, the barrier and counters.
+struct CoopBuffers {
+  int64_t keys = 0;
+  uint8_t* base = nullptr;
+};
+static CoopBuffers g_coop[64];
+
+static int coop_buffers(sp_ctx* ctx, int64_t keys, CoopArgs& a) {
+  CoopBuffers& b = g_coop[ctx->device & 63];
+  auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  const size_t chunk = al(4u * kCoopChunk) * 2 + al(8u * kCoopChunk) + al(4u * kCoopChunk);
+  const size_t gates = al(sizeof(Gate) * kMaxFoldTables), stb = al(sizeof(CoopState));
+  if (keys > b.keys) {
+    int64_t cap = std::max<int64_t>(keys, 1 << 14);
+    if (b.base) {
+      SP_CUDA(cudaStreamSynchronize(ctx->stream));
+      SP_CUDA(cudaFree(b.base));
+      b.base = nullptr;
+      b.keys = 0;
+    }
+    const size_t per = al(8u * cap) * 3 + al(4u * kCoopTiles * cap);
+    SP_CUDA(cudaMalloc(&b.base, per + chunk + gates + stb));
+    uint8_t* q = b.base;
+    SP_CUDA(cudaMemset(q, 0, al(8u * cap)));                    // mask
+    SP_CUDA(cudaMemset(q + al(8u * cap), 0xFF, al(8u * cap)));  // lo
+    SP_CUDA(cudaMemset(q + 2 * al(8u * cap), 0, al(8u * cap))); // hi
+    SP_CUDA(cudaMemset(q + per + chunk + gates, 0, stb));       // barrier / counters
+    b.keys = cap;
+  }
+  const int64_t cap = b.keys;
+  uint8_t* q = b.base;
+  a.mask = reinterpret_cast<uint64_t*>(q);
+  a.lo = reinterpret_cast<uint64_t*>(q + al(8u * cap));
+  a.hi = reinterpret_cast<uint64_t*>(q + 2 * al(8u * cap));
+  a.slot = reinterpret_cast<uint32_t*>(q + 3 * al(8u * cap));
+  q += al(8u * cap) * 3 + al(4u * kCoopTiles * cap);
+  a.skey = reinterpret_cast<uint32_t*>(q);
+  a.spos = reinterpret_cast<uint32_t*>(q + al(4u * kCoopChunk));
+  a.sobs = reinterpret_cast<double*>(q + 2 * al(4u * kCoopChunk));
+  a.touched = reinterpret_cast<int32_t*>(q + 2 * al(4u * kCoopChunk) + al(8u * kCoopChunk));
+  q += chunk;
+  a.gates = reinterpret_cast<Gate*>(q);
+  a.st = reinterpret_cast<CoopState*>(q + gates);
+  return SP_OK;
+}
+
+static int fold_launch_coop(sp_ctx* ctx, int n_tables, sp_table* const* tables, int n,
+                            const int32_t* op, const int32_t* idx, const double* obs, double beta,
+                            int dfp_count, int dfp_on, int fb_frozen) {
+  CoopArgs a;
+  a.ft.n = n_tables;
+  int64_t gb = 0;
+  for (int t = 0; t < n_tables; ++t) {
+    sp_table* tb = tables[t];
+    a.ft.t[t] = FoldTab{tb->lat, tb->lat_init, tb->obs_count, tb->dev_counters, tb->M,
+                        tb->ref_index, (int32_t)gb, 0};
+    gb += tb->M;
+  }
+  if (gb >= (1ll << 31) - 1) return fail(SP_E_UNSUPPORTED, "fold: too many entries");
+  a.ft.total = (int)gb;
+  int end_bit = 1;
+  while ((1ll << end_bit) <= gb) ++end_bit;
+  a.end_bit = end_bit;
+  a.n = n;
+  a.op = op;
+  a.idx = idx;
+  a.obs = obs;
+  a.beta = beta;
+  const double ol = 1.0 - beta;
+  int win = 8;
+  if (ol > 0.0) {
+    const double w = ceil(80.0 / -log2(ol));
+    win = w > 4096.0 ? (1 << 30) : (w < 8.0 ? 8 : (int)w);
+  }
+  a.win = win;
+  a.dfp_count = dfp_count;
+  a.dfp_on = dfp_on;
+  a.fb_frozen = fb_frozen;
+  int rc = coop_buffers(ctx, gb + 1, a);
+  if (rc != SP_OK) return rc;
+  const size_t smem = std::max(sizeof(typename cub::BlockRadixSort<uint32_t, kCoopThreads, 1,
+                                                                   uint32_t, 6>::TempStorage),
+                               sizeof(WarpRuns) * kCoopWarps + 8u * kCoopWarpBuf * kCoopWarps);
+  static uint64_t attr = 0;
+  static int max_blocks[64] = {};
+  const int dev = cur_device();
+  if (attr_once(attr)) {
+    SP_CUDA(cudaFuncSetAttribute(k_fold_coop, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    int per_sm = 0;
+    SP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fold_coop, kCoopThreads, smem));
+    max_blocks[dev] = per_sm * ctx->num_sms;
+  }
+  if (max_blocks[dev] < 1) return fail(SP_E_RUNTIME, "fold: cooperative kernel cannot be resident");
+  const int tiles = (std::min(n, kCoopChunk) + kCoopTile - 1) / kCoopTile;
+  int grid = std::min(max_blocks[dev], std::max(tiles, 1));
+  void* args[] = {(void*)&a};
+  SP_CUDA(cudaLaunchCooperativeKernel((const void*)k_fold_coop, dim3(grid), dim3(kCoopThreads),
+                                      args, smem, ctx->stream));
+  SP_CHECK_LAUNCH(ctx);
+  return SP_OK;
+}
+
+}  // namespace
+
+int fold_launch(sp_ctx* ctx, int n_tables, sp_table* const* tables, int n, const int32_t* op,
+                const int32_t* idx, const double* obs, double beta, int dfp_count, int dfp_on,
+                int fb_frozen) {
+  if (n_tables > kMaxFoldTables) return fail(SP_E_UNSUPPORTED, "fold: at most 64 tables");
+  if (ctx->opt.fold_legacy || n == 0)
+    return fold_launch_legacy(ctx, n_tables, tables, n, op, idx, obs, beta, dfp_count, dfp_on,
+                              fb_frozen);
+  int rc = fold_launch_coop(ctx, n_tables, tables, n, op, idx, obs, beta, dfp_count, dfp_on,
+                            fb_frozen);
+  if (rc == SP_OK)
+    for (int t = 0; t < n_tables; ++t) tables[t]->version++;
+  return rc;
 }
 
 }  // namespace sp

@@ -125,6 +125,7 @@ struct Options {
   int pipe_chunks = 0;       // SP_PIPE_CHUNKS: pageable staging chunks (0 = by size)
   int k1_cert = 0;           // SP_K1_CERT: 0 auto, 1 off ("0"), 2 force ("force")
   int fold_long_min = 0;     // SP_FOLD_LONG_MIN: long-segment threshold of the fold (0 = default)
+  int fold_legacy = 0;       // SP_FOLD_LEGACY: multi-kernel fold (radix sort + 5 kernels)
   int stair_smem = 0;        // SP_STAIR_SMEM: multi-kernel builder, shared-memory staircase
   int stair_global = 0;      // SP_STAIR_GLOBAL: multi-kernel builder, global staircase
   int no_plan_graph = 0;     // SP_NO_PLAN_GRAPH: no CUDA-graph replay of plan builds

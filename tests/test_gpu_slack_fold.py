@@ -123,6 +123,16 @@ def test_dag_slack_certified_forced_vs_reference(gpu_ctx, monkeypatch):
         gpu_ctx.set_option("SP_K1_CERT", 0)
 
 
+@pytest.fixture(params=["coop", "legacy"])
+def fold_impl(request, gpu_ctx):
+    """Both fold implementations: the one-kernel cooperative fold (default) and the multi-kernel
+    radix-sort path (SP_FOLD_LEGACY)."""
+    gpu_ctx.set_option("SP_FOLD_LEGACY", 1 if request.param == "legacy" else 0)
+    yield request.param
+    gpu_ctx.set_option("SP_FOLD_LEGACY", 0)
+
+
+
 def _fold_tables(d, m, lo):
     import paper_2102_01887_b200 as sp
 
@@ -137,7 +147,7 @@ def _fold_tables(d, m, lo):
 
 
 @pytest.mark.parametrize("chunked", [False, True])
-def test_feedback_fold_vs_reference(gpu_ctx, chunked):
+def test_feedback_fold_vs_reference(gpu_ctx, fold_impl, chunked):
     """PipelineRun._apply_feedback streams (EWMA, counts, gate-lift rescale, fb/dfp ablations)
     folded on the device in one batch, or in random consecutive chunks."""
     import paper_2102_01887_b200 as sp
@@ -170,7 +180,7 @@ def test_feedback_fold_vs_reference(gpu_ctx, chunked):
             t.close()
 
 
-def test_feedback_fold_skips_negative_indices(gpu_ctx):
+def test_feedback_fold_skips_negative_indices(gpu_ctx, fold_impl):
     """idx < 0 marks 'no observation' (e.g. a None / delay decision passed straight through)."""
     import paper_2102_01887_b200 as sp
 
@@ -192,7 +202,7 @@ def test_feedback_fold_skips_negative_indices(gpu_ctx):
     assert cref == st.completed_ref and np.array_equal(cnt, st.obs_count)
 
 
-def test_feedback_fold_large_stream_vs_oracle(gpu_ctx):
+def test_feedback_fold_large_stream_vs_oracle(gpu_ctx, fold_impl):
     """A config-5-sized batch (65,536 observations over a 16,384-entry table, heavy skew)
     against the sequential oracle."""
     import paper_2102_01887_b200 as sp
@@ -220,7 +230,7 @@ def test_feedback_fold_large_stream_vs_oracle(gpu_ctx):
 
 
 @pytest.mark.parametrize("beta", [0.5, 0.3, 0.1, 0.9, 1.0, 0.01])
-def test_feedback_fold_long_segments_vs_oracle(gpu_ctx, beta):
+def test_feedback_fold_long_segments_vs_oracle(gpu_ctx, fold_impl, beta):
     """Hot entries with tens of thousands of observations in one batch take the coalescing
     window path (sp_fold.cu): the result must still equal the sequential fold bit for bit,
     including the gate inside a long reference segment, a segment whose range is too wide to
@@ -251,3 +261,37 @@ def test_feedback_fold_long_segments_vs_oracle(gpu_ctx, beta):
     assert np.array_equal(bits(got), bits(st.lat))
     cref, cnt = sp.table_counters(tab)
     assert cref == st.completed_ref and np.array_equal(cnt, st.obs_count)
+
+
+@pytest.mark.parametrize("dfp_count", [10, 3000, 10**9])
+def test_feedback_fold_multi_chunk_vs_oracle(gpu_ctx, fold_impl, dfp_count):
+    """One call of 200,000 records over two tables: the one-kernel fold takes it in four chunks
+    of 64 x 1024 records (the gate lifting inside a later chunk for dfp_count = 3000, never for
+    1e9), skipped records and ragged last tile included."""
+    import paper_2102_01887_b200 as sp
+
+    rng = np.random.default_rng(dfp_count % 1000 + 3)
+    sizes, n = (5000, 700), 200_003
+    lat0 = [np.exp(rng.uniform(np.log(1e-3), 0.0, size=M)) for M in sizes]
+    op = (rng.random(n) < 0.3).astype(np.int32)
+    hot = [rng.choice(M, size=12, replace=False) for M in sizes]
+    idx = np.empty(n, np.int32)
+    for t, M in enumerate(sizes):
+        sel = op == t
+        k = int(sel.sum())
+        idx[sel] = np.where(rng.random(k) < 0.7, rng.choice(hot[t], size=k), rng.integers(0, M, size=k))
+    idx[(op == 0) & (rng.random(n) < 0.02)] = 1   # table 0's reference entry
+    idx[rng.random(n) < 0.05] = -1
+    obs = np.array([lat0[t][max(i, 0)] for t, i in zip(op, idx)]) * np.exp(rng.normal(0, 0.4, size=n))
+    tabs = [sp.RawTable(lat=lat0[t] * 0.8, res=np.ones(M), batch=np.ones(M, np.int32), pool=np.ones(M),
+                        price=np.ones(M), ref_index=(1 if t == 0 else 5), lat_init=lat0[t] * 0.8)
+            for t, M in enumerate(sizes)]
+    sts = [ofb.FoldState(lat0[t] * 0.8, lat0[t] * 0.8, 1 if t == 0 else 5) for t in range(2)]
+    sp.fold_observations(tabs, op, idx, obs, beta=0.5, dfp_count=dfp_count, sync_host=False)
+    keep = idx >= 0
+    ofb.fold(sts, op[keep], idx[keep], obs[keep], beta=0.5, dfp_count=dfp_count)
+    for t in range(2):
+        assert np.array_equal(bits(tabs[t].get_latency()), bits(sts[t].lat)), t
+        cref, cnt = sp.table_counters(tabs[t])
+        assert cref == sts[t].completed_ref and np.array_equal(cnt, sts[t].obs_count), t
+        tabs[t].close()
