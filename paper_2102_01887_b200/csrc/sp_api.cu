@@ -129,9 +129,12 @@ static bool mapped_host(const void* h, size_t bytes, void** dev) {
 }
 
 __global__ void k_scatter(int m, const int32_t* __restrict__ idx, const double* __restrict__ val,
-                          double* __restrict__ dst) {
+                          double* __restrict__ dst, uint8_t* __restrict__ dirty) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < m) dst[idx[i]] = val[i];
+  if (i < m) {
+    dst[idx[i]] = val[i];
+    dirty[idx[i]] = 1;
+  }
 }
 
 static void free_table(sp_table* t) {
@@ -153,6 +156,7 @@ static void free_table(sp_table* t) {
   cudaFree(t->pc_seg);
   cudaFree(t->pc_seg_ent);
   cudaFree(t->pc_scratch);
+  cudaFree(t->dirty);
   for (auto& p : t->plans) plan_release(p);
   delete t;
 }
@@ -365,8 +369,11 @@ int sp_table_create(sp_ctx* ctx, int32_t M, const double* lat, const double* lat
   ALLOC_COPY(obs_count, (const int32_t*)nullptr, int32_t);
 #undef ALLOC_COPY
   cudaError_t e = cudaMemsetAsync(t->obs_count, 0, sizeof(int32_t) * M, st);
-  if (e == cudaSuccess) e = cudaMalloc(&t->dev_counters, sizeof(int32_t) * 4);
-  if (e == cudaSuccess) e = cudaMemsetAsync(t->dev_counters, 0, sizeof(int32_t) * 4, st);
+  if (e == cudaSuccess) e = cudaMalloc(&t->dev_counters, sizeof(int32_t) * 8);
+  if (e == cudaSuccess) e = cudaMemsetAsync(t->dev_counters, 0, sizeof(int32_t) * 8, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(t->dev_counters + 4, 1, 1, st);  // order stale
+  if (e == cudaSuccess) e = cudaMalloc(&t->dirty, (size_t)M);
+  if (e == cudaSuccess) e = cudaMemsetAsync(t->dirty, 0, (size_t)M, st);
   if (e != cudaSuccess) {
     rc = cuda_fail(e, "table_create(counters)");
     free_table(t);
@@ -430,7 +437,7 @@ int sp_table_set_latency(sp_ctx* ctx, sp_table* t, int32_t n, const int32_t* idx
   memcpy(hb + rsz<int32_t>(m), uv.data(), sizeof(double) * m);
   const int32_t* d_i = reinterpret_cast<const int32_t*>(dbase);
   const double* d_v = reinterpret_cast<const double*>(static_cast<uint8_t*>(dbase) + rsz<int32_t>(m));
-  k_scatter<<<(m + 255) / 256, 256, 0, ctx->stream>>>(m, d_i, d_v, t->lat);
+  k_scatter<<<(m + 255) / 256, 256, 0, ctx->stream>>>(m, d_i, d_v, t->lat, t->dirty);
   SP_CHECK_LAUNCH(ctx);
   SP_CUDA(cudaStreamSynchronize(ctx->stream));
   t->version++;
@@ -448,7 +455,10 @@ int sp_table_get_latency(sp_ctx* ctx, sp_table* t, double* out_lat) {
 
 int sp_table_invalidate(sp_ctx* ctx, sp_table* t) {
   if (!ctx || !t) return fail(SP_E_INVALID, "invalidate: null argument");
+  DeviceScope _dev_scope(ctx->device);
   t->version++;  // every plan of the table is rebuilt by its next use
+  // the latencies may have been written behind the library's back: full re-sort
+  SP_CUDA(cudaMemsetAsync(t->dev_counters + 4, 1, 1, ctx->stream));
   return SP_OK;
 }
 

@@ -46,6 +46,7 @@ struct FoldTab {
   const double* lat_init;
   int32_t* obs_count;
   int32_t* counters;  // [0] completed_ref
+  uint8_t* dirty;     // latency written (the plan builder's cached order, sp_plan_cluster.cu)
   int32_t M;
   int32_t ref_index;
   int32_t gbase;  // global key base
@@ -371,6 +372,7 @@ static int fold_launch_legacy(sp_ctx* ctx, int n_tables, sp_table* const* tables
     f.lat_init = tb->lat_init;
     f.obs_count = tb->obs_count;
     f.counters = tb->dev_counters;
+    f.dirty = tb->dirty;
     f.M = tb->M;
     f.ref_index = tb->ref_index;
     f.gbase = (int32_t)gb;
@@ -449,7 +451,11 @@ static int fold_launch_legacy(sp_ctx* ctx, int n_tables, sp_table* const* tables
     k_fold_rescale<<<grid, 256, 0, st>>>(ft, gates);
     SP_CHECK_LAUNCH(ctx);
   }
-  for (int t = 0; t < n_tables; ++t) tables[t]->version++;
+  for (int t = 0; t < n_tables; ++t) {
+    tables[t]->version++;
+    // this path does not track written entries: the builder's cached order is re-sorted whole
+    SP_CUDA(cudaMemsetAsync(tables[t]->dev_counters + 4, 1, 1, st));
+  }
   return SP_OK;
 }
 
@@ -517,7 +523,14 @@ struct CoopArgs {
   int32_t* touched; // chunk: keys with at least one observation
   Gate* gates;      // per table
   CoopState* st;
+  int debug;        // SP_PC_DEBUG: per-phase timestamps of CTA 0 (printf)
 };
+
+__device__ __forceinline__ uint64_t coop_timer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
   uint32_t v;
@@ -671,6 +684,8 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_fold_coop(const __grid_cons
   double* buf = reinterpret_cast<double*>(smem + sizeof(WarpRuns) * kCoopWarps) + warp * kCoopWarpBuf;
   const uint32_t sent = (uint32_t)a.ft.total;
   CoopState* st = a.st;
+  uint64_t tm[8] = {};
+  tm[0] = coop_timer();
   for (int c0 = 0, chunk = 0; c0 < a.n; c0 += kCoopChunk, ++chunk) {
     const int par = chunk & 1;
     const int nrec = min(kCoopChunk, a.n - c0);
@@ -684,7 +699,9 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_fold_coop(const __grid_cons
         if (e >= 0) key[0] = (uint32_t)(a.ft.t[a.op ? a.op[j] : 0].gbase + e);
       }
       __syncthreads();  // tmp / s_key reuse across tiles
+      if (chunk == 0) tm[1] = coop_timer();
       Sort(tmp).Sort(key, val, 0, a.end_bit);
+      if (chunk == 0) tm[2] = coop_timer();
       const uint32_t k = key[0];
       s_key[threadIdx.x] = k;
       const int q = tl * kCoopTile + (int)threadIdx.x;  // chunk-array index
@@ -727,7 +744,9 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_fold_coop(const __grid_cons
         }
       }
     }
+    if (chunk == 0) tm[3] = coop_timer();
     coop_sync(st->bar);
+    if (chunk == 0) tm[4] = coop_timer();
     // ---- gates of this chunk (uniform in every CTA) ----
     if (threadIdx.x == 0) {
       uint64_t lift = 0;
@@ -754,6 +773,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_fold_coop(const __grid_cons
         L = coop_fold(a, R, buf, L, k, cnt, bd, lo, hi);
         if (lane == 0) {
           tb.lat[tb.ref_index] = L;
+          tb.dirty[tb.ref_index] = 1;
           tb.obs_count[tb.ref_index] += cnt;
           a.gates[t] = Gate{1, gpos, ratio};
           a.mask[rk] = 0ull;
@@ -785,7 +805,10 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_fold_coop(const __grid_cons
           double lo = 0.0, hi = 0.0;
           const bool bd = cnt > a.win && coop_bounds(a, key, L, &lo, &hi);
           L = coop_fold(a, R, buf, L, 0, cnt, bd, lo, hi);
-          if (lane == 0) tb.lat[e] = L;
+          if (lane == 0) {
+            tb.lat[e] = L;
+            tb.dirty[e] = 1;
+          }
         }
         if (lane == 0) {
           tb.obs_count[e] = before + cnt;
@@ -796,7 +819,9 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_fold_coop(const __grid_cons
         __syncwarp();
       }
     }
+    if (chunk == 0) tm[5] = coop_timer();
     coop_sync(st->bar);
+    if (chunk == 0) tm[6] = coop_timer();
     // ---- phase D ----
     if (blockIdx.x == 0 && threadIdx.x < a.ft.n) {
       const int t = threadIdx.x;
@@ -810,12 +835,22 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_fold_coop(const __grid_cons
         const FoldTab& tb = a.ft.t[t];
         const double ratio = a.gates[t].ratio;
         for (int e = blockIdx.x * kCoopThreads + threadIdx.x; e < tb.M; e += gridDim.x * kCoopThreads)
-          if (e != tb.ref_index && tb.obs_count[e] == 0)
+          if (e != tb.ref_index && tb.obs_count[e] == 0) {
             tb.lat[e] = __dmul_rn(tb.lat_init[e], ratio);  // configurator.py:490
+            tb.dirty[e] = 1;
+          }
       }
     }
     // the next chunk's phase C reads counters / latencies written here: its phase-A barrier
     // orders them
+  }
+  if (a.debug && threadIdx.x == 0 && blockIdx.x < 2) {
+    tm[7] = coop_timer();
+    printf("fold cta %d: start->sort %llu sort %llu runs %llu barA %llu C %llu barC %llu D %llu ns\n",
+           blockIdx.x, (unsigned long long)(tm[1] - tm[0]), (unsigned long long)(tm[2] - tm[1]),
+           (unsigned long long)(tm[3] - tm[2]), (unsigned long long)(tm[4] - tm[3]),
+           (unsigned long long)(tm[5] - tm[4]), (unsigned long long)(tm[6] - tm[5]),
+           (unsigned long long)(tm[7] - tm[6]));
   }
 }
 
@@ -874,7 +909,7 @@ static int fold_launch_coop(sp_ctx* ctx, int n_tables, sp_table* const* tables, 
   int64_t gb = 0;
   for (int t = 0; t < n_tables; ++t) {
     sp_table* tb = tables[t];
-    a.ft.t[t] = FoldTab{tb->lat, tb->lat_init, tb->obs_count, tb->dev_counters, tb->M,
+    a.ft.t[t] = FoldTab{tb->lat, tb->lat_init, tb->obs_count, tb->dev_counters, tb->dirty, tb->M,
                         tb->ref_index, (int32_t)gb, 0};
     gb += tb->M;
   }
@@ -898,6 +933,7 @@ static int fold_launch_coop(sp_ctx* ctx, int n_tables, sp_table* const* tables, 
   a.dfp_count = dfp_count;
   a.dfp_on = dfp_on;
   a.fb_frozen = fb_frozen;
+  a.debug = ctx->opt.pc_debug;
   int rc = coop_buffers(ctx, gb + 1, a);
   if (rc != SP_OK) return rc;
   const size_t smem = std::max(sizeof(typename cub::BlockRadixSort<uint32_t, kCoopThreads, 1,

@@ -208,7 +208,11 @@ struct sp_table {
   uint32_t* rowscratch = nullptr;             // (M+K) * 2W
   double* thrscratch = nullptr;               // M+K
   int32_t* rows_per_kind = nullptr;           // K (+1 status word)
-  int32_t* dev_counters = nullptr;            // [0] = completed_ref (device copy)
+  int32_t* dev_counters = nullptr;            // [0] = completed_ref (device copy); [4] = the
+                                              // cached latency order is stale as a whole
+  // per entry: the latency changed since the cluster plan builder last sorted its cached
+  // per-segment latency order (set by every device writer of lat, cleared by the builder)
+  uint8_t* dirty = nullptr;
   uint32_t *candf = nullptr, *cands = nullptr;  // M flags each
   uint32_t *cidf = nullptr, *cids = nullptr;    // M maps each
   int2* fin_chunk = nullptr;  // 2 x ceil(M / 256): per-chunk candidate counts, then bases

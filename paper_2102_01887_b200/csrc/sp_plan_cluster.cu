@@ -305,6 +305,8 @@ struct PcArgs {
   int M, K, nB, W, nseg;
   const PcSegDev* seg;
   int32_t* ord;                 // M: per segment slice, its entries in (lat, index) order
+  uint8_t* dirty;               // M: latency changed since ord was sorted (cleared here)
+  int32_t* order_stale;         // nonzero: ord is stale as a whole (cleared here)
   const double *lat, *res, *pool, *price;
   const int32_t *batch, *kind, *id_rank;
   double alpha;
@@ -425,38 +427,121 @@ __device__ void pc_segment(const PcArgs& a, const PcShared& S, int s, uint8_t* s
   int32_t* pidr = pe + NE;
   int32_t* lP = pidr + NE;  // record positions
   int32_t* lS = lP + NE;
-  // 1. the cached (lat, index) order of the previous build; re-sorted only if it no longer
-  //    holds (a latency changed)
+  // 1. the cached (lat, index) order of the previous build.  Entries whose latency changed since
+  //    (dirty) are taken out, sorted among themselves and merged back: the clean entries keep
+  //    their relative order, so the result equals a full sort.  A stale order or many dirty
+  //    entries take the full bitonic sort.
+  const bool stale = *a.order_stale != 0;
   uint64_t key[E];
   uint32_t val[E];
+  bool dq[E];
+  int nd_local = 0;
 #pragma unroll
   for (int q = 0; q < E; ++q) {
     const int i = t + q * T;
     if (i < n) {
       val[q] = (uint32_t)a.ord[off + i];
       key[q] = okey(a.lat[val[q]]);
+      dq[q] = stale || a.dirty[val[q]] != 0;
     } else {
       val[q] = 0xFFFFFFFFu;
       key[q] = ~0ull;
+      dq[q] = false;
     }
+    nd_local += dq[q] ? 1 : 0;
     sk[i] = key[q];
     sv[i] = val[q];
   }
-  __syncthreads();
+  const int nd = __syncthreads_count(nd_local);  // threads with a dirty entry (E == 1: entries)
   PC_STAMP(1);
-  bool bad = false;
+  constexpr int kIncMax = 256;  // dirty entries merged incrementally
+  if (nd == 0) {
+    bool bad = false;
 #pragma unroll
-  for (int q = 0; q < E; ++q) {
-    const int i = t + q * T;
-    if (i + 1 < n) bad |= sk[i] > sk[i + 1] || (sk[i] == sk[i + 1] && sv[i] > sv[i + 1]);
-  }
-  if (__syncthreads_or(bad)) {
+    for (int q = 0; q < E; ++q) {
+      const int i = t + q * T;
+      if (i + 1 < n) bad |= sk[i] > sk[i + 1] || (sk[i] == sk[i + 1] && sv[i] > sv[i + 1]);
+    }
+    if (__syncthreads_or(bad)) {
+      reg_bitonic<E>(key, val, N2, sk, sv);
+#pragma unroll
+      for (int q = 0; q < E; ++q) {
+        const int i = t + q * T;
+        if (i < n) a.ord[off + i] = (int32_t)val[q];
+      }
+    }
+  } else if (stale || E > 1 || nd > kIncMax) {
     reg_bitonic<E>(key, val, N2, sk, sv);
 #pragma unroll
     for (int q = 0; q < E; ++q) {
       const int i = t + q * T;
-      if (i < n) a.ord[off + i] = (int32_t)val[q];
+      if (i < n) {
+        a.ord[off + i] = (int32_t)val[q];
+        a.dirty[val[q]] = 0;
+      }
     }
+  } else {
+    // E == 1: position i = t.  Clean entries -> uk/uv (still sorted), dirty -> dk/dv.
+    uint64_t* uk = reinterpret_cast<uint64_t*>(sv + NE);  // (the position arrays below, unused yet)
+    uint64_t* dk = uk + NE;
+    uint32_t* uv = reinterpret_cast<uint32_t*>(dk + NE);
+    uint32_t* dv = uv + NE;
+    uint64_t* dk2 = reinterpret_cast<uint64_t*>(dv + NE);
+    uint32_t* dv2 = reinterpret_cast<uint32_t*>(dk2 + kIncMax);
+    int tot;
+    const int od = pc_excl_sum(dq[0] ? 1 : 0, s_w, &tot);
+    const int nc = n - tot;
+    if (t < n) {
+      if (dq[0]) {
+        dk[od] = key[0];
+        dv[od] = val[0];
+      } else {
+        uk[t - od] = key[0];
+        uv[t - od] = val[0];
+      }
+    }
+    __syncthreads();
+    if (t < tot) {  // rank of each dirty entry among the dirty ones (distinct values: total order)
+      const uint64_t k0 = dk[t];
+      const uint32_t v0 = dv[t];
+      int r = 0;
+      for (int j = 0; j < tot; ++j) r += (dk[j] < k0 || (dk[j] == k0 && dv[j] < v0)) ? 1 : 0;
+      dk2[r] = k0;
+      dv2[r] = v0;
+    }
+    __syncthreads();
+    // merge: an element's final position = its index in its own list + the elements of the
+    // other list ordered before it
+    if (t < nc) {
+      const uint64_t k0 = uk[t];
+      const uint32_t v0 = uv[t];
+      int lo = 0, hi = tot;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (dk2[mid] < k0 || (dk2[mid] == k0 && dv2[mid] < v0)) lo = mid + 1; else hi = mid;
+      }
+      sk[t + lo] = k0;
+      sv[t + lo] = v0;
+    } else if (t < n) {
+      const int r = t - nc;
+      const uint64_t k0 = dk2[r];
+      const uint32_t v0 = dv2[r];
+      int lo = 0, hi = nc;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (uk[mid] < k0 || (uk[mid] == k0 && uv[mid] < v0)) lo = mid + 1; else hi = mid;
+      }
+      sk[r + lo] = k0;
+      sv[r + lo] = v0;
+      a.dirty[v0] = 0;
+    }
+    __syncthreads();
+    if (t < n) {
+      key[0] = sk[t];
+      val[0] = sv[t];
+      a.ord[off + t] = (int32_t)val[0];
+    }
+    __syncthreads();
   }
   PC_STAMP(2);
   // 2. per position: cost / costpen (configurator.py:224-225, numpy order, no FMA), keys
@@ -1644,6 +1729,7 @@ __global__ void __launch_bounds__(kPcThreads, 1) k_plan_cluster(const __grid_con
   for (int s = c; s < a.nseg; s += C) pc_segment<ES>(a, S, s, smem, s_w);
   tm[2] = gtimer();
   cluster_barrier();
+  if (c == 0 && threadIdx.x == 0) *a.order_stale = 0;  // every CTA has read it
   tm[3] = gtimer();
   for (int i = threadIdx.x; i < 4 * a.nseg; i += blockDim.x) S.cnt[i] = a.seg_cnt[i];
   __syncthreads();
@@ -1836,6 +1922,8 @@ int plan_cluster_launch(sp_ctx* ctx, sp_table* t, Plan& p, int W, const PlanHdr&
   a.nseg = t->pc_nseg;
   a.seg = reinterpret_cast<const PcSegDev*>(t->pc_seg);
   a.ord = t->pc_seg_ent;  // cached per-segment latency order (index order before the first build)
+  a.dirty = t->dirty;
+  a.order_stale = t->dev_counters + 4;
   a.lat = t->lat;
   a.res = t->res;
   a.pool = t->pool;

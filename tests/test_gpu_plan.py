@@ -71,3 +71,44 @@ def test_cluster_plan_random_tables(gpu_ctx, seed, M, nB, K, nonpos):
     for alpha in (0.0, 7.5, 1000.0):
         _check(tab, K, alpha, arrays)
     tab.close()
+
+
+@pytest.mark.parametrize("seed,M,nB,K,nonpos", [(11, 3000, 8, 2, False), (12, 900, 8, 2, True),
+                                                (13, 4000, 16, 3, False)])
+def test_cluster_plan_incremental_updates(gpu_ctx, seed, M, nB, K, nonpos):
+    """The cluster builder keeps each segment's latency order between builds and merges only the
+    entries whose latency changed (set_latency, the fold, the gate-lift rescale).  After every
+    kind of update — a few entries, ties with unchanged entries, moves to the extremes, zero /
+    negative values, more entries than the incremental cap — the image must equal the CPU
+    restatement built from scratch and the multi-kernel builder."""
+    import paper_2102_01887_b200 as sp
+
+    rng = np.random.default_rng(seed)
+    t = _random_table(rng, M, nB, K, nonpos)
+    tab = raw_table(t, K)
+    lat = t.lat.copy()
+    arrays = lambda: (lat, t.res, t.batch_int, t.pool, t.price, t.gkind, t.id_rank)
+    _check(tab, K, 7.5, arrays())
+    for step in range(12):
+        if step % 3 == 2:  # the fold writes the observed entries (dirty flags set on the device)
+            n = int(rng.integers(1, 400))
+            idx = rng.choice(rng.choice(M, size=int(rng.integers(1, 40)), replace=False), size=n).astype(np.int32)
+            obs = rng.uniform(0.01, 5.0, size=n)
+            sp.fold_observations([tab], None, idx, obs, beta=0.5, dfp_count=10**9, sync_host=False)
+            lat = np.asarray(tab.get_latency()).copy()
+        else:
+            m = [3, 40, 700][step % 3] if step < 9 else int(rng.integers(1, 20))
+            ix = rng.choice(M, size=min(m, M), replace=False).astype(np.int32)
+            v = rng.uniform(0.01, 5.0, size=len(ix))
+            tie = rng.random(len(ix)) < 0.4
+            v[tie] = rng.choice(lat, size=int(tie.sum()))                 # exact ties with others
+            v[rng.random(len(ix)) < 0.1] = lat.min() * 0.5                 # new minimum
+            v[rng.random(len(ix)) < 0.1] = lat.max() * 2.0                 # new maximum
+            if nonpos:
+                v[rng.random(len(ix)) < 0.1] = 0.0
+                v[rng.random(len(ix)) < 0.1] = -1.5
+            tab.set_latency(ix, v)
+            lat[ix] = v
+        for alpha in (7.5,) if step % 2 else (0.0, 1000.0):
+            _check(tab, K, alpha, arrays())
+    tab.close()
