@@ -32,7 +32,6 @@
 #include <stdlib.h>
 
 #include <cub/cub.cuh>
-#include <cub/block/block_radix_sort.cuh>
 
 #include "sp_internal.cuh"
 
@@ -532,6 +531,105 @@ __device__ __forceinline__ uint64_t coop_timer() {
   return t;
 }
 
+
+// Stable grouping of one 1024-record tile by key (one record per thread): the records of a key
+// become one contiguous run, in thread order inside the run; runs are laid out in the order the
+// keys were first inserted (the fold only needs each key's records together and in order).
+//   1. keys go into a shared-memory hash table (linear probing, 2048 slots); the inserting
+//      thread gives the key a dense id;
+//   2. per warp, __match_any_sync groups equal keys: rank inside the warp, and the group's count
+//      in cnt[id][warp] (bytes);
+//   3. per id the run length (sum over warps) and, by a block scan, the run start;
+//   4. every record scatters to run start + records of its key in earlier warps + rank.
+// On return thread i holds the record at position i and `len` = its run's length when it is the
+// run's first record (0 otherwise).  Shared memory: kTileGroupSmem bytes at `sm` (16-B aligned).
+constexpr int kTileHash = 2048;
+constexpr int kTileGroupSmem = kCoopTile * 32 + kTileHash * 4 + kTileHash * 2 + kCoopTile * 4 * 4;
+__device__ __forceinline__ void tile_group(uint32_t& key, uint32_t& val, uint32_t& len, uint8_t* sm) {
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(sm);                 // [1024 ids][32 warps] bytes
+  uint32_t* htab = cnt + kCoopTile * 8;                            // kTileHash keys
+  uint16_t* hid = reinterpret_cast<uint16_t*>(htab + kTileHash);   // kTileHash ids
+  uint32_t* start = reinterpret_cast<uint32_t*>(hid + kTileHash);  // per id: run start
+  uint32_t* sk = start + kCoopTile;
+  uint32_t* sv = sk + kCoopTile;
+  uint32_t* sl = sv + kCoopTile;
+  __shared__ uint32_t s_n, s_ws[32];
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+#pragma unroll
+  for (int u = 0; u < 8; ++u) cnt[t + u * kCoopTile] = 0;
+  htab[t] = 0xFFFFFFFFu;
+  htab[t + kCoopTile] = 0xFFFFFFFFu;
+  if (t == 0) s_n = 0;
+  __syncthreads();
+  uint32_t h = (key * 2654435761u) >> 21;  // 11 bits
+  for (;;) {
+    const uint32_t old = atomicCAS(&htab[h], 0xFFFFFFFFu, key);
+    if (old == 0xFFFFFFFFu) {
+      hid[h] = (uint16_t)atomicAdd(&s_n, 1u);
+      break;
+    }
+    if (old == key) break;
+    h = (h + 1) & (kTileHash - 1);
+  }
+  __syncthreads();
+  const uint32_t id = hid[h];
+  const uint32_t peers = __match_any_sync(0xffffffffu, key);
+  const uint32_t rank = __popc(peers & ((1u << lane) - 1u));
+  uint8_t* cb = reinterpret_cast<uint8_t*>(cnt);
+  if (rank == 0) cb[id * 32 + w] = (uint8_t)__popc(peers);
+  __syncthreads();
+  // run lengths, exclusive scan over ids (ids < s_n)
+  const uint32_t nid = s_n;
+  uint32_t tot = 0;
+  if ((uint32_t)t < nid) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) tot = __dp4a(cnt[t * 8 + u], 0x01010101u, tot);
+  }
+  uint32_t x = tot;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, off);
+    if (lane >= off) x += y;
+  }
+  if (lane == 31) s_ws[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    uint32_t y = s_ws[lane];
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const uint32_t z = __shfl_up_sync(0xffffffffu, y, off);
+      if (lane >= off) y += z;
+    }
+    s_ws[lane] = y;
+  }
+  __syncthreads();
+  if ((uint32_t)t < nid) start[t] = x - tot + (w ? s_ws[w - 1] : 0u);
+  __syncthreads();
+  // records of this key in earlier warps: bytes [0, w) of the id's row
+  uint32_t before = 0;
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const uint32_t word = cnt[id * 8 + u];
+    const int lo = 4 * u;
+    const uint32_t m = w >= lo + 4 ? 0xFFFFFFFFu : (w <= lo ? 0u : (0xFFFFFFFFu >> (8 * (lo + 4 - w))));
+    before = __dp4a(word & m, 0x01010101u, before);
+  }
+  const uint32_t pos = start[id] + before + rank;
+  sk[pos] = key;
+  sv[pos] = val;
+  uint32_t mylen = 0;
+  if (before == 0 && rank == 0) {  // first record of the key
+#pragma unroll
+    for (int u = 0; u < 8; ++u) mylen = __dp4a(cnt[id * 8 + u], 0x01010101u, mylen);
+  }
+  sl[pos] = mylen;
+  __syncthreads();
+  key = sk[t];
+  val = sv[t];
+  len = sl[t];
+  __syncthreads();
+}
+
 __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -674,11 +772,9 @@ __device__ __forceinline__ bool gate_lifts(const CoopArgs& a, const FoldTab& tb,
 }
 
 __global__ void __launch_bounds__(kCoopThreads, 1) k_fold_coop(const __grid_constant__ CoopArgs a) {
-  using Sort = cub::BlockRadixSort<uint32_t, kCoopThreads, 1, uint32_t, 6>;
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ uint32_t s_key[kCoopTile];
   __shared__ uint64_t s_lift;  // tables whose gate lifts in this chunk
-  auto& tmp = *reinterpret_cast<typename Sort::TempStorage*>(smem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   WarpRuns& R = reinterpret_cast<WarpRuns*>(smem)[warp];
   double* buf = reinterpret_cast<double*>(smem + sizeof(WarpRuns) * kCoopWarps) + warp * kCoopWarpBuf;
@@ -690,7 +786,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_fold_coop(const __grid_cons
     const int par = chunk & 1;
     const int nrec = min(kCoopChunk, a.n - c0);
     const int ntiles = (nrec + kCoopTile - 1) / kCoopTile;
-    // ---- phase A ----
+    // ---- phase A (records grouped by key, not sorted: the runs only need to be contiguous) ----
     for (int tl = blockIdx.x; tl < ntiles; tl += gridDim.x) {
       const int j = c0 + tl * kCoopTile + (int)threadIdx.x;
       uint32_t key[1] = {sent}, val[1] = {(uint32_t)j};
@@ -700,7 +796,8 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_fold_coop(const __grid_cons
       }
       __syncthreads();  // tmp / s_key reuse across tiles
       if (chunk == 0) tm[1] = coop_timer();
-      Sort(tmp).Sort(key, val, 0, a.end_bit);
+      uint32_t run_len;
+      tile_group(key[0], val[0], run_len, smem);
       if (chunk == 0) tm[2] = coop_timer();
       const uint32_t k = key[0];
       s_key[threadIdx.x] = k;
@@ -728,13 +825,8 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_fold_coop(const __grid_cons
           atomicMin(reinterpret_cast<unsigned long long*>(a.lo + k), (unsigned long long)mn);
           atomicMax(reinterpret_cast<unsigned long long*>(a.hi + k), (unsigned long long)mx);
         }
-        if (threadIdx.x == 0 || s_key[threadIdx.x - 1] != k) {  // run head
-          int lo = (int)threadIdx.x + 1, hi = kCoopTile;  // first position with a larger key
-          while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (s_key[mid] <= k) lo = mid + 1; else hi = mid;
-          }
-          const int len = lo - (int)threadIdx.x;
+        if (run_len) {  // run head
+          const int len = (int)run_len;
           a.slot[(size_t)k * kCoopTiles + tl] = threadIdx.x | (uint32_t)len << 16;
           const unsigned long long old =
               atomicOr(reinterpret_cast<unsigned long long*>(a.mask + k), 1ull << tl);
@@ -936,8 +1028,7 @@ static int fold_launch_coop(sp_ctx* ctx, int n_tables, sp_table* const* tables, 
   a.debug = ctx->opt.pc_debug;
   int rc = coop_buffers(ctx, gb + 1, a);
   if (rc != SP_OK) return rc;
-  const size_t smem = std::max(sizeof(typename cub::BlockRadixSort<uint32_t, kCoopThreads, 1,
-                                                                   uint32_t, 6>::TempStorage),
+  const size_t smem = std::max((size_t)kTileGroupSmem,
                                sizeof(WarpRuns) * kCoopWarps + 8u * kCoopWarpBuf * kCoopWarps);
   static uint64_t attr = 0;
   static int max_blocks[64] = {};
