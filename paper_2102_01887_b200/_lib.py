@@ -212,16 +212,18 @@ def get_context(device: int | None = None) -> Context:
     return c
 
 
-def ptr(a) -> C.c_void_p:
-    """Data pointer of a numpy array (host) or a torch tensor (device or host)."""
+def ptr(a):
+    """Data pointer of a torch tensor (device or host) or a numpy array (host), as an int
+    (ctypes passes it as void*; None is NULL)."""
     if a is None:
-        return C.c_void_p(0)
+        return None
+    dp = getattr(a, "data_ptr", None)
+    if dp is not None:
+        if not a.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        return dp()
     if isinstance(a, np.ndarray):
         if not a.flags["C_CONTIGUOUS"]:
             raise ValueError("array must be C-contiguous")
-        return C.c_void_p(a.ctypes.data)
-    if hasattr(a, "data_ptr"):
-        if not a.is_contiguous():
-            raise ValueError("tensor must be contiguous")
-        return C.c_void_p(a.data_ptr())
+        return a.ctypes.data
     raise TypeError(f"unsupported buffer type {type(a)!r}")

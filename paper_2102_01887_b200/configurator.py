@@ -367,6 +367,17 @@ def make_flags(allow_delay, excluded_mask=0) -> np.ndarray:
     return (ad * np.uint32(_lib.SP_FLAG_ALLOW_DELAY)) | (ex << np.uint32(_lib.SP_FLAG_EXCL_SHIFT))
 
 
+def handle_array(tables):
+    """The tables' handles as a C void* array (cached on a single table: the common call)."""
+    if len(tables) == 1:
+        h = getattr(tables[0], "_harr", None)
+        if h is None:
+            h = (C.c_void_p * 1)(tables[0].handle.value)
+            tables[0]._harr = h
+        return h
+    return (C.c_void_p * len(tables))(*[t.handle.value for t in tables])
+
+
 def _is_device(a) -> bool:
     return hasattr(a, "is_cuda") and bool(a.is_cuda)
 
@@ -390,6 +401,29 @@ def select_batch(tables: Sequence[OpTable], slack, alpha: float, available, *, u
     N = int(slack.shape[0])
     if tuple(slack.shape) != (N, K):
         raise ValueError(f"slack must have shape (N, {K})")
+    if device:
+        import torch
+
+        want = ((available, torch.int32), (upstream_supply, torch.int32), (min_batch, torch.int32))
+        if slack.dtype != torch.float64 or any(a.dtype != d or a.shape != (N,) for a, d in want) \
+                or flags.dtype not in (torch.int32, torch.uint32) or flags.shape != (N,) \
+                or (op is not None and (op.dtype != torch.int32 or op.shape != (N,))):
+            raise ValueError("select_batch: device inputs must be float64 slack (N, K) and int32 "
+                             "available / upstream_supply / min_batch / flags / op (N,)")
+    else:  # host inputs: the C-ABI reads raw int32 / uint32 / float64 buffers of length N
+        slack = np.ascontiguousarray(slack, dtype=np.float64)
+        cols = []
+        for name, a, dt in (("available", available, np.int32), ("upstream_supply", upstream_supply, np.int32),
+                            ("min_batch", min_batch, np.int32), ("flags", flags, np.uint32),
+                            ("op", op, np.int32)):
+            if a is None:
+                cols.append(None)
+                continue
+            a = np.ascontiguousarray(a, dtype=dt)
+            if a.shape != (N,):
+                raise ValueError(f"select_batch: {name} must have shape ({N},)")
+            cols.append(a)
+        available, upstream_supply, min_batch, flags, op = cols
     if out is None:
         if device:
             import torch
@@ -413,10 +447,9 @@ def select_batch(tables: Sequence[OpTable], slack, alpha: float, available, *, u
             }
             if kind_min:
                 out["kind_min"] = np.empty((N, K), np.float64)
-    arr_t = (C.c_void_p * len(tables))(*[t.handle.value for t in tables])
     check(
         ctx.lib.sp_select_batch(
-            ctx.handle, len(tables), C.cast(arr_t, C.c_void_p), float(alpha), N, ptr(op),
+            ctx.handle, len(tables), handle_array(tables), float(alpha), N, ptr(op),
             ptr(slack), ptr(available), ptr(upstream_supply), ptr(min_batch), ptr(flags),
             ptr(out["idx"]), ptr(out["code"]), ptr(out.get("fill")), ptr(out.get("obj")),
             ptr(out.get("slack")), ptr(out.get("wait")), ptr(out.get("kind_min") if kind_min else None),
@@ -524,8 +557,8 @@ class _RawTable:
         v = np.ascontiguousarray(np.atleast_1d(latency_s), dtype=np.float64)
         if i.shape != v.shape:
             raise ValueError("set_latency: index and latency_s differ in length")
-        self.lat[i] = v
         check(self._ctx.lib.sp_table_set_latency(self._ctx.handle, self._handle, len(i), ptr(i), ptr(v)))
+        self.lat[i] = v  # after the device accepted the values
 
     def get_latency(self) -> np.ndarray:
         out = np.empty(self.M, np.float64)

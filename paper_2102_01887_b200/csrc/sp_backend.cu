@@ -18,6 +18,8 @@ __global__ void k_observe(int n, const int32_t* __restrict__ code, const int32_t
                           const int32_t* __restrict__ fill, const double* __restrict__ base,
                           const double* __restrict__ per_item, const double* __restrict__ noise,
                           int32_t* __restrict__ obs_idx, double* __restrict__ obs) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the decisions are the predecessor's
+  asm volatile("griddepcontrol.launch_dependents;");
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const bool run = (code[i] & 3) == SP_DEC_ASSIGN;
@@ -48,8 +50,17 @@ extern "C" int sp_simulate_observations(sp_ctx* ctx, int32_t N, const int32_t* c
   if (truth_per_item && !fill)
     return fail(SP_E_INVALID, "simulate_observations: fill is required with per-item truth");
   if (N == 0) return SP_OK;
-  k_observe<<<(N + 255) / 256, 256, 0, ctx->stream>>>(N, code, idx, fill, truth_base,
-                                                      truth_per_item, noise, obs_idx, obs);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((N + 255) / 256);
+  cfg.blockDim = dim3(256);
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = ctx->opt.no_pdl ? 0 : 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  SP_CUDA(cudaLaunchKernelEx(&cfg, k_observe, N, code, idx, fill, truth_base, truth_per_item,
+                             noise, obs_idx, obs));
   SP_CHECK_LAUNCH(ctx);
   return SP_OK;
 }

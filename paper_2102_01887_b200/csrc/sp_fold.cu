@@ -782,6 +782,9 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_fold_coop(const __grid_cons
   CoopState* st = a.st;
   uint64_t tm[8] = {};
   tm[0] = coop_timer();
+  // programmatic dependent launch: the observation stream and the tables are the predecessors'
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
   for (int c0 = 0, chunk = 0; c0 < a.n; c0 += kCoopChunk, ++chunk) {
     const int par = chunk & 1;
     const int nrec = min(kCoopChunk, a.n - c0);
@@ -885,8 +888,11 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_fold_coop(const __grid_cons
         const FoldTab& tb = a.ft.t[t];
         const int e = (int)key - tb.gbase;
         if (((lift >> t) & 1ull) && e == tb.ref_index) continue;  // phase B
+        const uint64_t c0 = a.debug ? coop_timer() : 0;
         const int cnt = runs_load(a, key, R);
+        const uint64_t c1 = a.debug ? coop_timer() : 0;
         const int before = tb.obs_count[e];
+        uint64_t c2 = 0, c3 = 0;
         if (!a.fb_frozen) {
           double L = tb.lat[e];
           if ((lift >> t) & 1ull) {
@@ -896,7 +902,13 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_fold_coop(const __grid_cons
           }
           double lo = 0.0, hi = 0.0;
           const bool bd = cnt > a.win && coop_bounds(a, key, L, &lo, &hi);
+          c2 = a.debug ? coop_timer() : 0;
           L = coop_fold(a, R, buf, L, 0, cnt, bd, lo, hi);
+          c3 = a.debug ? coop_timer() : 0;
+          if (a.debug && lane == 0 && blockIdx.x == 0 && warp < 4)
+            printf("fold C warp %d key %u cnt %d: runs %llu bounds %llu fold %llu (from C start %llu) ns\n",
+                   warp, key, cnt, (unsigned long long)(c1 - c0), (unsigned long long)(c2 - c1),
+                   (unsigned long long)(c3 - c2), (unsigned long long)(c3 - tm[4]));
           if (lane == 0) {
             tb.lat[e] = L;
             tb.dirty[e] = 1;
@@ -1043,9 +1055,19 @@ static int fold_launch_coop(sp_ctx* ctx, int n_tables, sp_table* const* tables, 
   if (max_blocks[dev] < 1) return fail(SP_E_RUNTIME, "fold: cooperative kernel cannot be resident");
   const int tiles = (std::min(n, kCoopChunk) + kCoopTile - 1) / kCoopTile;
   int grid = std::min(max_blocks[dev], std::max(tiles, 1));
-  void* args[] = {(void*)&a};
-  SP_CUDA(cudaLaunchCooperativeKernel((const void*)k_fold_coop, dim3(grid), dim3(kCoopThreads),
-                                      args, smem, ctx->stream));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kCoopThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute la[2];
+  la[0].id = cudaLaunchAttributeCooperative;  // every CTA resident: the grid barriers
+  la[0].val.cooperative = 1;
+  la[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  la[1].val.programmaticStreamSerializationAllowed = ctx->opt.no_pdl ? 0 : 1;
+  cfg.attrs = la;
+  cfg.numAttrs = 2;
+  SP_CUDA(cudaLaunchKernelEx(&cfg, k_fold_coop, a));
   SP_CHECK_LAUNCH(ctx);
   return SP_OK;
 }

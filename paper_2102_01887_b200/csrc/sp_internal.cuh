@@ -107,6 +107,12 @@ struct Plan {
   cudaEvent_t hdr_ready = nullptr;
   bool hdr_pending = false;
   bool hdr_valid = false;
+  // cluster builds write the header (and then the build's sequence number) straight into
+  // mapped pinned memory: no copy or event between the build and the next kernel, so the
+  // programmatic-dependent-launch chain build -> select stays intact
+  volatile uint32_t* host_seq = nullptr;
+  uint32_t seq = 0;
+  bool hdr_mapped = false;
   // rebuilds after the first are replayed from a CUDA graph of the whole build (one launch
   // instead of ~12 kernel launches + 3 memory operations)
   int builds = 0;
@@ -133,7 +139,8 @@ struct Options {
   int pc_debug = 0;          // SP_PC_DEBUG: per-phase timestamps of the cluster builder
   int k2_plan_only = 0;      // SP_K2_VARIANT (any value but "fast"): generic K2b only
   int k2f_threads = 512;     // SP_K2F_THREADS: K2f block size (512 or 1024)
-  int no_pdl = 0;            // SP_NO_PDL: no programmatic dependent launch for K2f
+  int no_pdl = 0;            // SP_NO_PDL: no programmatic dependent launch (K2f, K2b, the
+                             // cluster plan build, the fold, the observation kernel)
   int full_smem = 0;         // SP_FULL_SMEM: K2b requests the whole shared-memory budget
   int no_k12 = 0;            // SP_NO_K12: K1 then K2 instead of the fused kernel
   int k12_generic = 0;       // SP_K12_GENERIC: fused kernel without the K2f decision core
@@ -326,11 +333,12 @@ int plan_build(sp_ctx* ctx, sp_table* t, Plan& p);
 int plan_scratch_alloc(sp_table* t);
 int plan_cluster_prepare(sp_table* t, const int32_t* kind, const int32_t* bidx);
 int plan_cluster_launch(sp_ctx* ctx, sp_table* t, Plan& p, int W, const PlanHdr& hdr,
-                        int32_t* status);
+                        int32_t* status, PlanHdr* host_hdr, uint32_t* host_seq, uint32_t seq);
 Plan* plan_get(sp_ctx* ctx, sp_table* t, double alpha, int* rc);
 Plan* plan_costs(sp_ctx* ctx, sp_table* t, double alpha, int* rc);
 bool plan_ready(sp_table* t, double alpha);
 const PlanHdr* plan_host_header(Plan& p);  // nullptr until the async copy has landed
+int plan_header_wait(sp_ctx* ctx, Plan& p);  // block until the header has landed
 void plan_release(Plan& p);
 int select_launch(sp_ctx* ctx, int n_tables, sp_table* const* tables, double alpha, int N,
                   const int32_t* op, const double* slack, const int32_t* avail,

@@ -210,6 +210,10 @@ __global__ void __launch_bounds__(1024, 1) k_select_plan(PlanPtrs pp, int smem_b
   __shared__ __align__(8) uint64_t s_bar;
   __shared__ int s_fit;
   const int tid = threadIdx.x;
+  // programmatic dependent launch: nothing of the predecessor's output (the plan image, the
+  // invocation stream) is touched before it has completed
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
   if (tid == 0) {
     int off = 0;
     for (int t = 0; t < pp.n; ++t) {
@@ -231,7 +235,9 @@ __global__ void __launch_bounds__(1024, 1) k_select_plan(PlanPtrs pp, int smem_b
   const int stride = gridDim.x * blockDim.x;
   const int i = blockIdx.x * blockDim.x + tid;
   const bool kmin = io.out_kind_min != nullptr;
-  const bool single = pp.hv && !kmin;
+  // one table without kind minima: the single-table loop, with the header from the kernel
+  // parameter or (a plan rebuilt after the host last saw it) from the staged image
+  const bool single = pp.n == 1 && !kmin;
   In<KT> cur, nxt;
   if (single) {
     if (i < io.N) load_in<KT>(io, i, cur);
@@ -242,7 +248,8 @@ __global__ void __launch_bounds__(1024, 1) k_select_plan(PlanPtrs pp, int smem_b
     mbar_wait(&s_bar, 0);
     if (single) {
       View<KT> v;
-      make_view<KT>(v, smem, pp.h, io.K);
+      if (pp.hv) make_view<KT>(v, smem, pp.h, io.K);
+      else make_view<KT>(v, smem, *reinterpret_cast<const PlanHdr*>(smem), io.K);
       plan_loop_single<KT>(v, io, i, cur, nxt);
     } else if (kmin) {
       plan_loop_multi<KT, true, true>(smem, pp, s_off, io, i);

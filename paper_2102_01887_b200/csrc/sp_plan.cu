@@ -1485,6 +1485,19 @@ int plan_scratch_alloc(sp_table* t) {
 
 static int plan_finish(sp_ctx* ctx, Plan& p, sp_table* t);
 
+// pinned, mapped host copy of the header (+ the build sequence word after it)
+static cudaError_t plan_host_alloc(Plan& p) {
+  if (p.host_hdr) return cudaSuccess;
+  cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&p.host_hdr), sizeof(PlanHdr) + 64,
+                                cudaHostAllocMapped);
+  if (e != cudaSuccess) return e;
+  p.host_seq = reinterpret_cast<volatile uint32_t*>(reinterpret_cast<uint8_t*>(p.host_hdr) +
+                                                    sizeof(PlanHdr));
+  *p.host_seq = 0;
+  if (!p.hdr_ready) e = cudaEventCreateWithFlags(&p.hdr_ready, cudaEventDisableTiming);
+  return e;
+}
+
 static int plan_enqueue(sp_ctx* ctx, sp_table* t, Plan& p) {
   const int M = t->M, K = t->K;
   cudaStream_t st = ctx->stream;
@@ -1508,7 +1521,7 @@ static int plan_enqueue(sp_ctx* ctx, sp_table* t, Plan& p) {
     p.image_cap = plan_image_capacity(t, W);
     SP_CUDA(cudaMalloc(&p.image, (size_t)p.image_cap));
   }
-  if (cluster) {  // one cluster kernel writes cost / costpen and the whole image
+  if (cluster) {  // one cluster kernel writes cost / costpen, the whole image and the host header
     PlanHdr h;
     memset(&h, 0, sizeof(h));
     h.magic = kPlanMagic;
@@ -1517,9 +1530,23 @@ static int plan_enqueue(sp_ctx* ctx, sp_table* t, Plan& p) {
     h.W = W;
     h.K = K;
     for (int b = 0; b < kMaxB; ++b) h.batch_vals[b] = b < t->nB ? t->batch_vals[b] : INT32_MAX;
-    const int rc = plan_cluster_launch(ctx, t, p, W, h, t->rows_per_kind + kMaxKinds);
+    SP_CUDA(plan_host_alloc(p));
+    void* dh = nullptr;
+    SP_CUDA(cudaHostGetDevicePointer(&dh, p.host_hdr, 0));
+    ++p.seq;
+    const int rc = plan_cluster_launch(ctx, t, p, W, h, t->rows_per_kind + kMaxKinds,
+                                       static_cast<PlanHdr*>(dh),
+                                       reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(dh) +
+                                                                   sizeof(PlanHdr)),
+                                       p.seq);
     if (rc != SP_OK) return rc;
-    return plan_finish(ctx, p, t);
+    ctx->plan_dirty = true;
+    p.hdr_mapped = true;
+    p.hdr_pending = true;
+    p.hdr_valid = false;
+    p.valid = true;
+    p.version = t->version;
+    return SP_OK;
   }
   KindInfo ki;
   for (int k = 0; k < kMaxKinds; ++k) {
@@ -1641,11 +1668,9 @@ static int plan_enqueue(sp_ctx* ctx, sp_table* t, Plan& p) {
 static int plan_finish(sp_ctx* ctx, Plan& p, sp_table* t) {
   cudaStream_t st = ctx->stream;
   ctx->plan_dirty = true;
+  p.hdr_mapped = false;
   // fetch the header back without blocking; it becomes a kernel parameter once it lands
-  if (!p.host_hdr) {
-    SP_CUDA(cudaMallocHost(&p.host_hdr, sizeof(PlanHdr)));
-    SP_CUDA(cudaEventCreateWithFlags(&p.hdr_ready, cudaEventDisableTiming));
-  }
+  SP_CUDA(plan_host_alloc(p));
   SP_CUDA(cudaMemcpyAsync(p.host_hdr, p.image, sizeof(PlanHdr), cudaMemcpyDeviceToHost, st));
   // (the header-ready event is recorded by plan_build, outside any graph capture)
   p.hdr_pending = true;
@@ -1656,6 +1681,9 @@ static int plan_finish(sp_ctx* ctx, Plan& p, sp_table* t) {
 }
 
 int plan_build(sp_ctx* ctx, sp_table* t, Plan& p) {
+  // the cluster builder is one kernel: launched directly (programmatic dependent launch on
+  // both sides), no graph and no header event
+  if (t->plan_ok && t->pc_ok && !ctx->opt.plan_legacy) return plan_enqueue(ctx, t, p);
   if (p.graph && !ctx->opt.no_plan_graph) {
     SP_CUDA(cudaGraphLaunch(p.graph, ctx->stream));
     if (t->plan_ok) SP_CUDA(cudaEventRecord(p.hdr_ready, ctx->stream));
@@ -1702,11 +1730,26 @@ int plan_build(sp_ctx* ctx, sp_table* t, Plan& p) {
 }
 
 const PlanHdr* plan_host_header(Plan& p) {
-  if (p.hdr_pending && cudaEventQuery(p.hdr_ready) == cudaSuccess) {
-    p.hdr_pending = false;
-    p.hdr_valid = p.host_hdr->magic == kPlanMagic;
+  if (p.hdr_pending) {
+    if (p.hdr_mapped) {
+      if (*p.host_seq == p.seq) {  // written by the build kernel after the header (system fence)
+        p.hdr_pending = false;
+        p.hdr_valid = reinterpret_cast<volatile PlanHdr*>(p.host_hdr)->magic == kPlanMagic;
+      }
+    } else if (cudaEventQuery(p.hdr_ready) == cudaSuccess) {
+      p.hdr_pending = false;
+      p.hdr_valid = p.host_hdr->magic == kPlanMagic;
+    }
   }
   return p.hdr_valid ? p.host_hdr : nullptr;
+}
+
+int plan_header_wait(sp_ctx* ctx, Plan& p) {
+  if (p.hdr_pending) {
+    if (p.hdr_mapped) SP_CUDA(cudaStreamSynchronize(ctx->stream));
+    else SP_CUDA(cudaEventSynchronize(p.hdr_ready));
+  }
+  return SP_OK;
 }
 
 void plan_release(Plan& p) {

@@ -335,6 +335,9 @@ struct PcArgs {
   int32_t base[kMaxKinds], count[kMaxKinds];
   int32_t seg_lo[kMaxKinds + 1];  // segments of kind k: [seg_lo[k], seg_lo[k+1])
   PlanHdr hdr;                    // magic, M, nB, W, K, batch_vals
+  PlanHdr* host_hdr;              // mapped pinned copy of the header for the host
+  uint32_t* host_seq;             // written after host_hdr (system fence): the build's seq
+  uint32_t seq;
   int debug;
 };
 
@@ -1722,8 +1725,12 @@ __global__ void __launch_bounds__(kPcThreads, 1) k_plan_cluster(const __grid_con
   tm[0] = gtimer();
   const long long ck0 = clock64();
   if (threadIdx.x < 32) pc_stamps()[threadIdx.x] = tm[0];
+  if (threadIdx.x < a.nseg) S.seg[threadIdx.x] = a.seg[threadIdx.x];  // static per table
+  // programmatic dependent launch: the latencies (the fold's output) are read and the plan
+  // image (the previous select's input) is written only after the predecessor has completed
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
   if (threadIdx.x < 2 * kMaxKinds && c == 0) a.kinfo[threadIdx.x] = 0;
-  if (threadIdx.x < a.nseg) S.seg[threadIdx.x] = a.seg[threadIdx.x];
   cluster_barrier();
   tm[1] = gtimer();
   for (int s = c; s < a.nseg; s += C) pc_segment<ES>(a, S, s, smem, s_w);
@@ -1788,6 +1795,16 @@ __global__ void __launch_bounds__(kPcThreads, 1) k_plan_cluster(const __grid_con
       if (c == 0) *a.status = s_hdr.magic == kPlanMagic ? 0 : -1;
     }
     __syncthreads();
+    if (c == 0 && a.host_hdr) {  // the header for the host's next kernel parameter
+      if (threadIdx.x < (int)(sizeof(PlanHdr) / 4))
+        reinterpret_cast<volatile uint32_t*>(a.host_hdr)[threadIdx.x] =
+            reinterpret_cast<const uint32_t*>(&s_hdr)[threadIdx.x];
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence_system();
+        *reinterpret_cast<volatile uint32_t*>(a.host_seq) = a.seq;
+      }
+    }
   }
   const PlanHdr& H = s_hdr;
   if (fast) {
@@ -1910,7 +1927,7 @@ int plan_cluster_prepare(sp_table* t, const int32_t* kind, const int32_t* bidx) 
 }
 
 int plan_cluster_launch(sp_ctx* ctx, sp_table* t, Plan& p, int W, const PlanHdr& hdr,
-                        int32_t* status) {
+                        int32_t* status, PlanHdr* host_hdr, uint32_t* host_seq, uint32_t seq) {
   const int M = t->M;
   int n2 = 1;
   while (n2 < 2 * M) n2 <<= 1;
@@ -1975,6 +1992,9 @@ int plan_cluster_launch(sp_ctx* ctx, sp_table* t, Plan& p, int W, const PlanHdr&
   }
   for (int k = 0; k <= kMaxKinds; ++k) a.seg_lo[k] = k <= t->K ? t->pc_seg_lo[k] : t->pc_nseg;
   a.hdr = hdr;
+  a.host_hdr = host_hdr;
+  a.host_seq = host_seq;
+  a.seq = seq;
   a.debug = ctx->opt.pc_debug;
   // shared memory: the largest phase (segment: 60 B per slot; candidates 16 B; thresholds 8 B
   // per record in the shared-memory fallback; rows 64 KB)
@@ -2015,13 +2035,15 @@ int plan_cluster_launch(sp_ctx* ctx, sp_table* t, Plan& p, int W, const PlanHdr&
   cfg.blockDim = dim3(kPcThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = ctx->stream;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = C;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = ctx->opt.no_pdl ? 0 : 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   SP_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
   SP_CHECK_LAUNCH(ctx);
   return SP_OK;

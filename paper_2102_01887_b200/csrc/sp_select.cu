@@ -504,8 +504,19 @@ int launch_plan_t(sp_ctx* ctx, const PlanPtrs& pp, const SelectIO& io) {
   int smem = kPlanSmemBudget;
   if (pp.hv && pp.n == 1 && !ctx->opt.full_smem)
     smem = std::min(kPlanSmemBudget, ((pp.h.total_bytes + 1023) / 1024) * 1024);
-  k_select_plan<KT><<<blocks, kPlanThreads, smem, ctx->stream>>>(pp, smem, io);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(blocks);
+  cfg.blockDim = dim3(kPlanThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = ctx->opt.no_pdl ? 0 : 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  SP_CUDA(cudaLaunchKernelEx(&cfg, k_select_plan<KT>, pp, smem, io));
   SP_CHECK_LAUNCH(ctx);
+  ctx->plan_dirty = false;
   return SP_OK;
 }
 
@@ -571,7 +582,8 @@ int slack_select_launch(sp_ctx* ctx, sp_dag* g, int n_tables, sp_table* const* t
     }
     const PlanHdr* h = plan_host_header(*p);
     if (!h) {
-      SP_CUDA(cudaEventSynchronize(p->hdr_ready));
+      const int rc2 = plan_header_wait(ctx, *p);
+      if (rc2 != SP_OK) return rc2;
       h = plan_host_header(*p);
     }
     if (!h) return fail(SP_E_RUNTIME, "slack_select: plan header unavailable");

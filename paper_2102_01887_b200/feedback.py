@@ -32,14 +32,16 @@ def fold_observations(tables: Sequence, op, idx, obs, *, beta: float = 0.5,
     ctx = tables[0]._ctx
     device = _is_device(obs)
     n = int(obs.shape[0])
-    arr_t = (C.c_void_p * len(tables))(*[t.handle.value for t in tables])
+    from .configurator import handle_array
+
+    arr_t = handle_array(tables)
     if not device:
         idx = np.ascontiguousarray(idx, dtype=np.int32)
         obs = np.ascontiguousarray(obs, dtype=np.float64)
         if op is not None:
             op = np.ascontiguousarray(op, dtype=np.int32)
     check(ctx.lib.sp_feedback_fold(
-        ctx.handle, len(tables), C.cast(arr_t, C.c_void_p), n, ptr(op), ptr(idx), ptr(obs),
+        ctx.handle, len(tables), arr_t, n, ptr(op), ptr(idx), ptr(obs),
         float(beta), int(dfp_count), 1 if dfp_on else 0, 1 if fb_frozen else 0,
         _lib.SP_MEM_DEVICE if device else _lib.SP_MEM_HOST), "sp_feedback_fold")
     if sync_host:
@@ -55,18 +57,19 @@ def simulate_observations(decisions, truth_base, noise, *, truth_per_item=None, 
     assignments run, obs = (truth_base[idx] + truth_per_item[idx] * fill) * noise; delayed / None
     decisions give idx -1.  ``decisions``: the device output dict of ``select_batch``
     (``code``, ``idx``, ``fill``); torch CUDA tensors, stream-ordered.  Returns (obs_idx, obs)."""
-    import torch
-
     from ._lib import get_context
 
-    ctx = ctx or get_context(decisions["code"].device.index)
-    n = int(decisions["code"].shape[0])
+    code = decisions["code"]
+    ctx = ctx or get_context(code.device.index)
+    n = int(code.shape[0])
     if out is None:
-        out = (torch.empty(n, dtype=torch.int32, device=decisions["code"].device),
-               torch.empty(n, dtype=torch.float64, device=decisions["code"].device))
+        import torch
+
+        out = (torch.empty(n, dtype=torch.int32, device=code.device),
+               torch.empty(n, dtype=torch.float64, device=code.device))
     oi, ob = out
     check(ctx.lib.sp_simulate_observations(
-        ctx.handle, n, ptr(decisions["code"]), ptr(decisions["idx"]), ptr(decisions.get("fill")),
+        ctx.handle, n, ptr(code), ptr(decisions["idx"]), ptr(decisions.get("fill")),
         ptr(truth_base), ptr(truth_per_item), ptr(noise), ptr(oi), ptr(ob)),
         "sp_simulate_observations")
     return oi, ob
@@ -129,7 +132,7 @@ def observation_quantiles(tables: Sequence, op, idx, obs, q: float, *, smooth=No
             op = np.ascontiguousarray(op, dtype=np.int32)
         out = {"quantile": np.empty(total, np.float64), "count": np.empty(total, np.int32)}
     check(ctx.lib.sp_observation_quantiles(
-        ctx.handle, len(tables), C.cast(arr_t, C.c_void_p), n, ptr(op), ptr(idx), ptr(obs),
+        ctx.handle, len(tables), arr_t, n, ptr(op), ptr(idx), ptr(obs),
         float(q), float(beta), ptr(out["quantile"]), ptr(out["count"]), ptr(smooth),
         _lib.SP_MEM_DEVICE if device else _lib.SP_MEM_HOST), "sp_observation_quantiles")
     return out
