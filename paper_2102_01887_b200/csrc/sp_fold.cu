@@ -721,6 +721,69 @@ __device__ double coop_fold(const CoopArgs& a, const WarpRuns& R, double* buf, d
                             int o1, bool bounded, double lo, double hi) {
   const int lane = threadIdx.x & 31;
   const double ob = a.beta, ol = __dsub_rn(1.0, a.beta);
+  // Narrowed window (beta >= 1/2, positive normal-range values): the chain value 24 steps
+  // before the end is bounded by interval arithmetic over the 64 observations before it —
+  // every step y -> fl(fl(b o) + fl(a y)) lies in [(1-u)^2 (b o + a y), (1+u)^2 (b o + a y)]
+  // (u = 2^-53) and is monotone in y, so from y in [lo, hi] 64 steps earlier
+  //   y >= sum_j c_lo^(64-j) a^(63-j) b o_j + (c_lo a)^64 lo   (c_lo = 1 - 2^-52 <= (1-u)^2)
+  //   y <= the same with c_hi = 1 + 2^-51 >= (1+u)^2 and hi,
+  // evaluated by the warp with directed rounding (round-down / round-up); the exact chains then
+  // run from the narrowed bounds over the last 24 observations only.  Bit-exact whenever the
+  // two chains meet (else the full window below).
+  constexpr int kNk = 64, kNw = 24;
+  if (bounded && ol <= 0.5 && ob >= 0x1p-60 && ol >= 0x1p-60 && lo > 0x1p-900 && hi < 0x1p900 &&
+      o1 - o0 >= kNk + kNw) {
+    const int base = o1 - kNw - kNk;
+    for (int u = lane; u < kNk + kNw; u += 32) buf[u] = a.sobs[runs_at(R, base + u)];
+    __syncwarp();
+    const double cl = 1.0 - 0x1p-52, ch = 1.0 + 0x1p-51;
+    const double ql = __dmul_rd(cl, ol), qh = __dmul_ru(ch, ol);
+    const double bl = __dmul_rd(cl, ob), bh = __dmul_ru(ch, ob);
+    double zl = 0.0, zh = 0.0, tl = 0.0, th = 0.0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int j = lane + 32 * h, m = kNk - 1 - j;
+      double pl = 1.0, ph = 1.0, gl = ql, gh = qh;
+#pragma unroll
+      for (int bit = 0; bit < 6; ++bit) {
+        if ((m >> bit) & 1) {
+          pl = __dmul_rd(pl, gl);
+          ph = __dmul_ru(ph, gh);
+        }
+        gl = __dmul_rd(gl, gl);
+        gh = __dmul_ru(gh, gh);
+      }
+      tl = gl;  // (c_lo a)^64, (c_hi a)^64
+      th = gh;
+      const double o = buf[j];
+      zl = __dadd_rd(zl, __dmul_rd(__dmul_rd(pl, bl), o));
+      zh = __dadd_ru(zh, __dmul_ru(__dmul_ru(ph, bh), o));
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+      zl = __dadd_rd(zl, __shfl_xor_sync(0xffffffffu, zl, off));
+      zh = __dadd_ru(zh, __shfl_xor_sync(0xffffffffu, zh, off));
+    }
+    zl = __dadd_rd(zl, __dmul_rd(tl, lo));
+    zh = __dadd_ru(zh, __dmul_ru(th, hi));
+    int same = 0;
+    double v = 0.0;
+    if (lane == 0) {
+      double x = zl > lo ? zl : lo, y = zh < hi ? zh : hi;
+#pragma unroll 4
+      for (int u = kNk; u < kNk + kNw; ++u) {
+        const double t = __dmul_rn(ob, buf[u]);
+        x = __dadd_rn(t, __dmul_rn(ol, x));
+        y = __dadd_rn(t, __dmul_rn(ol, y));
+      }
+      v = x;
+      same = __double_as_longlong(x) == __double_as_longlong(y);
+    }
+    same = __shfl_sync(0xffffffffu, same, 0);
+    v = __shfl_sync(0xffffffffu, v, 0);
+    __syncwarp();
+    if (same) return v;
+  }
   if (bounded && o1 - o0 > a.win && a.win <= kCoopWarpBuf) {
     const int w0 = o1 - a.win;
     for (int u = lane; u < a.win; u += 32) buf[u] = a.sobs[runs_at(R, w0 + u)];

@@ -295,3 +295,28 @@ def test_feedback_fold_multi_chunk_vs_oracle(gpu_ctx, fold_impl, dfp_count):
         cref, cnt = sp.table_counters(tabs[t])
         assert cref == sts[t].completed_ref and np.array_equal(cnt, sts[t].obs_count), t
         tabs[t].close()
+
+
+@pytest.mark.parametrize("beta", [0.5, 0.6, 0.75, 0.97, 0.999])
+def test_feedback_fold_narrowed_window_vs_oracle(gpu_ctx, beta):
+    """Segments just above and far above the narrowed-window length (64 + 24), observations
+    spread over six orders of magnitude, exact repeats and start values far outside the
+    observations' range: the interval-narrowed window must give the sequential fold's bits."""
+    import paper_2102_01887_b200 as sp
+
+    rng = np.random.default_rng(int(beta * 1000) + 99)
+    M = 64
+    lens = [88, 89, 90, 100, 150, 300, 1000, 4000] * 4
+    idx = np.concatenate([np.full(n, e, np.int32) for e, n in enumerate(lens)])
+    rng.shuffle(idx)
+    n = len(idx)
+    obs = np.exp(rng.normal(0.0, 2.0, size=n)) * 1e-2
+    obs[rng.random(n) < 0.1] = 0.5                  # exact repeats
+    lat0 = np.exp(rng.uniform(np.log(1e-6), np.log(1e4), size=M))
+    tab = sp.RawTable(lat=lat0, res=np.ones(M), batch=np.ones(M, np.int32), pool=np.ones(M),
+                      price=np.ones(M), ref_index=-1, lat_init=lat0)
+    st = ofb.FoldState(lat0.copy(), lat0.copy(), -1)
+    sp.fold_observations([tab], None, idx, obs, beta=beta, dfp_count=10, sync_host=False)
+    ofb.fold([st], None, idx, obs, beta=beta, dfp_count=10)
+    assert np.array_equal(bits(tab.get_latency()), bits(st.lat))
+    tab.close()
