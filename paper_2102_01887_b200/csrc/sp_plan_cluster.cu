@@ -412,6 +412,41 @@ __device__ void pc_layout(const PcArgs& a, const int32_t* rows, const double* th
   if (!ok) hdr.magic = 0;
 }
 
+
+// Full sort of a short segment (n <= 256 entries held one per thread in sk / sv, the rest of the
+// block idle) by rank: G = blockDim / pow2(n) threads per entry each count a share of the
+// entries ordered before it ((key, val) distinct), the lane group adds the counts, the entry
+// goes to its rank.  ~8 comparisons per thread instead of the bitonic network's 36 stages.
+__device__ __forceinline__ void rank_sort_small(uint64_t& key, uint32_t& val, int n, int N2,
+                                                uint64_t* sk, uint32_t* sv, uint64_t* ok,
+                                                uint32_t* ov) {
+  const int t = threadIdx.x;
+  const int G = min(32, (int)blockDim.x / N2);
+  const int r = t / G, q = t % G;
+  int cnt = 0;
+  uint64_t k0 = 0;
+  uint32_t v0 = 0;
+  if (r < n) {
+    k0 = sk[r];
+    v0 = sv[r];
+    for (int j = q; j < n; j += G) cnt += (sk[j] < k0 || (sk[j] == k0 && sv[j] < v0)) ? 1 : 0;
+  }
+  for (int o = 1; o < G; o <<= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  if (r < n && q == 0) {
+    ok[cnt] = k0;
+    ov[cnt] = v0;
+  }
+  __syncthreads();
+  if (t < n) {
+    key = ok[t];
+    val = ov[t];
+  } else {
+    key = ~0ull;
+    val = 0xFFFFFFFFu;
+  }
+  __syncthreads();
+}
+
 // ---- phase 1: one (kind, lane) segment -----------------------------------------------------
 template <int E>
 __device__ void pc_segment(const PcArgs& a, const PcShared& S, int s, uint8_t* smem, int* s_w) {
@@ -480,9 +515,13 @@ __device__ void pc_segment(const PcArgs& a, const PcShared& S, int s, uint8_t* s
     if (nd == 0) {
       const bool bad = t + 1 < n && (sk[t] > sk[t + 1] || (sk[t] == sk[t + 1] && sv[t] > sv[t + 1]));
       moved = __syncthreads_or(bad);
-      if (moved) reg_bitonic<1>(key, val, N2, sk, sv);
+      if (moved) {
+        if (N2 <= 256) rank_sort_small(key[0], val[0], n, N2, sk, sv, (uint64_t*)(sv + NE), (uint32_t*)((uint64_t*)(sv + NE) + 256));
+        else reg_bitonic<1>(key, val, N2, sk, sv);
+      }
     } else if (stale || nd > kIncMax) {
-      reg_bitonic<1>(key, val, N2, sk, sv);
+      if (N2 <= 256) rank_sort_small(key[0], val[0], n, N2, sk, sv, (uint64_t*)(sv + NE), (uint32_t*)((uint64_t*)(sv + NE) + 256));
+      else reg_bitonic<1>(key, val, N2, sk, sv);
     } else {
       // clean entries -> uk/uv (still sorted), dirty -> dk/dv (the position arrays' space)
       uint64_t* uk = reinterpret_cast<uint64_t*>(sv + NE);
