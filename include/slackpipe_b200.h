@@ -302,6 +302,30 @@ int sp_simulate_observations(sp_ctx* ctx, int32_t N, const int32_t* code, const 
                              const double* truth_per_item, const double* noise, int32_t* obs_idx,
                              double* obs);
 
+/* ---- profile generation (replaces profiler.py:35-85
+ *      profile_operation's latency loop over pipeline.py:454-475 enumerate_configs) --------- */
+/* Host buffers, synchronous.  The knob template's cross product in the reference's
+ * enumeration order (kinds in the given (sorted) order; per kind its n_res[k] resource options
+ * from res_opts (concatenated); the n_batch ascending batch sizes; the knob values in template
+ * order, last knob fastest) — n_out = sum_k n_res[k] * n_batch * prod(knob_counts) entries.
+ * Per entry the ground-truth law of scenario.py:68-77 / backend.py:52-58 per kind k:
+ *   lat = base_seconds[k] * (R / ref_resource[k]) ** -resource_exponent[k] (when nonzero)
+ *         * B ** batch_exponent[k] * multipliers[k][knob j][value] (row of sum(knob_counts),
+ *         1.0 when the scenario has none) ;  draw = lat + per_item_seconds[k] * B
+ *   out_lat = (sum over samples of draw * noise[i*S+s] * straggle[i*S+s]) / samples
+ * with noise / straggle the reference's RNG factors (exp(N(0, sigma)), straggle_factor or 1.0)
+ * or NULL (factor 1).  `**` is the correctly rounded power (see sp_profile.cu).  out_kind /
+ * out_res / out_batch (optional) receive each entry's kind index, resource and batch size. */
+int sp_profile_configs(sp_ctx* ctx, int32_t K, const int32_t* n_res, const int32_t* res_opts,
+                       const double* base_seconds, const int32_t* ref_resource,
+                       const double* resource_exponent, const double* batch_exponent,
+                       const double* per_item_seconds, int32_t n_batch, const int32_t* batch_sizes,
+                       int32_t n_knobs, const int32_t* knob_counts, const double* multipliers,
+                       int32_t samples, const double* noise, const double* straggle, int64_t n_out,
+                       double* out_lat, int32_t* out_kind, int32_t* out_res, int32_t* out_batch);
+/* Correctly rounded x[i] ** y[i] on the device (host buffers; the power of the profile law). */
+int sp_pow_correctly_rounded(sp_ctx* ctx, int32_t n, const double* x, const double* y, double* out);
+
 /* ---- single-process multi-GPU fan-out (SURVEY.md §8(b) Threading, §8(e)) ------------------ */
 /* The reference engine is one single-threaded process (configurator.py:368-373); a drop-in
  * that uses the GPUs of a box fans out inside the library.  A group owns one context (device

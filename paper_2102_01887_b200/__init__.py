@@ -29,8 +29,10 @@ from . import metadata
 from .commit import commit_candidates, commit_round, pump_commits
 from .group import DeviceGroup, GroupOpTable, group_fold, group_select_batch
 from .feedback import apply_feedback, fold_observations, observation_quantiles, set_table_counters, simulate_observations, table_counters
-from .pipeline import ConfigEntry, ConfigSpec, PipelineDag, reference_config
-from .scenario import BackendSpec, Scenario
+from .pipeline import (ConfigAssignment, ConfigEntry, ConfigSpec, Knob, KnobTemplate, OperationSpec, PipelineDag,
+                       enumerate_configs, reference_config)
+from .profiler import profile_operation
+from .scenario import BackendSpec, GroundTruthModel, OpKindTruth, Scenario
 from .slack import SlackGraph, compute_slack
 from .speculate import speculate_batch, speculate_from_buffer
 
@@ -44,5 +46,6 @@ __all__ = [
     "commit_candidates", "commit_round", "compute_slack", "estimate_queueing", "fold_observations", "get_context", "load_library",
     "make_flags", "metadata", "objective", "pump_commits", "observation_quantiles", "reference_config", "remaining_path_latency", "select_batch",
     "select_config", "set_table_counters", "simulate_observations", "speculate_batch", "speculate_from_buffer",
-    "table_counters",
+    "table_counters", "ConfigAssignment", "Knob", "KnobTemplate", "OperationSpec", "enumerate_configs",
+    "profile_operation", "GroundTruthModel", "OpKindTruth",
 ]

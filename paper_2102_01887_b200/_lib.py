@@ -92,6 +92,9 @@ SIGNATURES = {
     "sp_slack_select_batch": (C.c_int, [_p, _p, _i32, _p, _d, _i32, _p, _i32, _p, _p, _i32, _p]
                               + [_p] * 11 + [_i32]),
     "sp_simulate_observations": (C.c_int, [_p, _i32] + [_p] * 8),
+    "sp_profile_configs": (C.c_int, [_p, _i32, _p, _p, _p, _p, _p, _p, _p, _i32, _p, _i32, _p, _p,
+                                     _i32, _p, _p, _i64, _p, _p, _p, _p]),
+    "sp_pow_correctly_rounded": (C.c_int, [_p, _i32, _p, _p, _p]),
     "sp_group_create": (C.c_int, [_i32, _p, _pp]),
     "sp_group_destroy": (C.c_int, [_p]),
     "sp_group_size": (_i32, [_p]),

@@ -8,6 +8,9 @@ these are (duck typing), so the GPU path is a drop-in for the reference package.
 """
 from __future__ import annotations
 
+import hashlib
+import itertools
+import json
 from dataclasses import dataclass, field
 from typing import Any, Mapping, Sequence
 
@@ -93,6 +96,72 @@ class ConfigSpec:
         return ConfigSpec(operation=obj["operation"],
                           entries=[ConfigEntry.from_json(e) for e in obj["entries"]],
                           reference_id=obj["reference_id"])
+
+
+def canonical_json(obj: Any) -> str:
+    """pipeline.py:31-33 (sorted keys, fixed separators)."""
+    return json.dumps(obj, sort_keys=True, separators=(",", ":"))
+
+
+def content_hash(obj: Any) -> str:
+    """pipeline.py:36-37."""
+    return hashlib.sha256(canonical_json(obj).encode("utf-8")).hexdigest()
+
+
+@dataclass(frozen=True)
+class Knob:
+    """One tunable dimension (pipeline.py:66-74)."""
+
+    name: str
+    values: tuple[Any, ...]
+
+
+@dataclass(frozen=True)
+class KnobTemplate:
+    """An operation's search space (pipeline.py:93-121)."""
+
+    knobs: tuple[Knob, ...]
+    hardware_targets: tuple[str, ...]
+    batch_sizes: tuple[int, ...]
+    resource_options: Mapping[str, tuple[int, ...]]
+
+
+@dataclass(frozen=True)
+class OperationSpec:
+    """A named pipeline stage and its search space (pipeline.py:167-173)."""
+
+    name: str
+    executable_id: str
+    knob_template: KnobTemplate
+    branching: bool = False
+
+
+@dataclass(frozen=True)
+class ConfigAssignment:
+    """One point of the search space before profiling (pipeline.py:176-188)."""
+
+    backend_kind: str
+    resource_request: int
+    batch_size: int
+    knob_values: tuple[tuple[str, Any], ...]
+
+    def config_id(self) -> str:
+        return config_id_of(self.backend_kind, self.resource_request, self.batch_size, self.knob_values)
+
+
+def enumerate_configs(template) -> list[ConfigAssignment]:
+    """pipeline.py:454-475: kinds sorted, then resource options and batch sizes ascending, then
+    the knob values in template order (the host half: the assignments' ids; the device
+    enumerates the same order in sp_profile_configs)."""
+    out = []
+    names = [k.name for k in template.knobs]
+    value_lists = [k.values for k in template.knobs]
+    for kind in sorted(template.hardware_targets):
+        for resource in template.resource_options[kind]:
+            for batch in sorted(template.batch_sizes):
+                for combo in itertools.product(*value_lists):
+                    out.append(ConfigAssignment(kind, resource, batch, tuple(zip(names, combo))))
+    return out
 
 
 def config_id_of(kind: str, resource: int, batch: int, knobs: Sequence[tuple[str, Any]] = ()) -> str:
