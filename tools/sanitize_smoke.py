@@ -91,3 +91,27 @@ gt = grp.table(synth.synth_spec(False), synth.synth_scenario())
 gt.select_batch(inv.slack, 100.0, inv.avail, upstream_supply=inv.supply, min_batch=inv.min_batch,
                 flags=inv.flags)
 print("sanitize smoke ok")
+# the one-kernel cooperative fold: two chunks, a gate lifting in the second, long (narrowed-window)
+# segments; the device profile generator (noise + straggles) and the correctly rounded power
+rng = np.random.default_rng(4)
+M = 3000
+lat0 = rng.uniform(0.1, 2.0, M)
+ft = sp.RawTable(lat=lat0, res=np.ones(M), batch=np.ones(M, np.int32), pool=np.ones(M),
+                 price=np.ones(M), ref_index=0, lat_init=lat0)
+n = 140000
+idx = np.where(rng.random(n) < 0.6, rng.integers(0, 8, n), rng.integers(0, M, n)).astype(np.int32)
+idx[rng.random(n) < 0.1] = -1
+sp.fold_observations([ft], None, idx, rng.uniform(0.1, 3.0, n), beta=0.5, dfp_count=9000)
+from paper_2102_01887_b200 import profiler  # noqa: E402
+from paper_2102_01887_b200.pipeline import Knob, KnobTemplate, OperationSpec  # noqa: E402
+from paper_2102_01887_b200.scenario import BackendSpec, GroundTruthModel, OpKindTruth, Scenario  # noqa: E402
+
+tpl = KnobTemplate((Knob("m", ("a", "b")),), ("cpu", "gpu"), (1, 2, 4), {"cpu": (1, 2), "gpu": (4, 8)})
+gtm = GroundTruthModel({"op": {"cpu": OpKindTruth(1.0, 1, 0.5, 0.85, 0.1, {"m": {"a": 1.2}}),
+                               "gpu": OpKindTruth(0.1, 4, 0.3, 0.35)}}, noise_sigma=0.2, straggle_rate=0.1,
+                       straggle_factor=2.0)
+scn = Scenario("s", (BackendSpec("cpu", 2, 4, 1e-5), BackendSpec("gpu", 1, 8, 1e-4)), gtm, 3)
+profiler.profile_operation(OperationSpec("op", "x", tpl), scn, 3)
+profiler.pow_correctly_rounded(rng.uniform(0.01, 100, 500), rng.uniform(-2, 2, 500))
+print("sanitize smoke (round 2, session 2) ok")
+
