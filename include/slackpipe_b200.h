@@ -372,6 +372,89 @@ int sp_group_feedback_fold(sp_group* g, int32_t n_tables, sp_group_table* const*
                            int32_t n, const int32_t* op, const int32_t* idx, const double* obs,
                            double beta, int32_t dfp_count, int32_t dfp_on, int32_t fb_frozen);
 
+/* ---- replica-parallel run engine --------------------------------- */
+/* One tuned pipeline run of the reference — PipelineRun.run_to_completion (manager.py:535-630)
+ * over BackendSim (backend.py:125-269) and the Configurator's queues, speculation, commits and
+ * feedback (configurator.py:368-772) — executed as a sequential discrete-event loop by one GPU
+ * thread per replica.  Replicas share the run description (tables, DAG, fleet, parameters) and
+ * differ in their trace (frames), latency target and RNG draws.  Every decision, the report and
+ * the final latency tables equal the reference's run on the same inputs bit for bit. */
+typedef struct sp_des sp_des;
+
+/* Run description (built by the Python host from PipelineRun's constructor arguments). Ops are
+ * in sorted-name order (the reference's table order, manager.py:259-261); kinds in the
+ * scenario's backend order (Scenario.backend_kinds, scenario.py:139-140). */
+typedef struct {
+  int32_t n_ops, n_kinds, n_entries, n_attrs, n_cfg_ids;
+  const int32_t* entry_off;      /* [n_ops+1] the op's OpTable entries (configurator.py:166-209) */
+  const double* lat;             /* [n_entries] profiled latency (profile-scaled, manager.py:187-208) */
+  const double* lat_init;        /* [n_entries] latency_initial_s (scaled) */
+  const double* res;             /* [n_entries] resource request */
+  const int32_t* batch;          /* [n_entries] batch size */
+  const int32_t* kind;           /* [n_entries] kind index */
+  const int32_t* id_rank;        /* [n_entries] rank of config_id within the op (configurator.py:195-198) */
+  const int32_t* cfg_id;         /* [n_entries] index of the config_id string (configs_used counts strings) */
+  const double* truth_base;      /* [n_entries] OpKindTruth.base_latency of the entry (scenario.py:68-77) */
+  const double* truth_per_item;  /* [n_entries] per_item_seconds of the entry's (op, kind) */
+  const int32_t* ref_index;      /* [n_ops] OpTable.ref_index (-1: reference unschedulable) */
+  const double* ref_latency;     /* [n_ops] reference entry latency (the anchor when ref_index = -1) */
+  const int32_t* succ_off;       /* [n_ops+1] CSR of sorted successors (pipeline.py:314-315) */
+  const int32_t* succ;           /* [n_edges] */
+  const int32_t* pred_attr;      /* [n_edges] branch predicate attribute (-1: none) (pipeline.py:283-295) */
+  const int32_t* pred_cmp;       /* [n_edges] 0 <, 1 <=, 2 >, 3 >=, 4 ==, 5 != */
+  const int32_t* pred_value;     /* [n_edges] */
+  const int32_t* fanout_attr;    /* [n_ops] fan-out attribute of the destination (-1: one item) */
+  const int32_t* suffix_off;     /* [n_ops+1] path suffixes containing the op (configurator.py:413-420) */
+  const int32_t* suffix_ops;     /* per suffix: length, then the op indices */
+  const int32_t* instances;      /* [n_kinds] instance_count */
+  const int32_t* inst_resources; /* [n_kinds] resources_per_instance */
+  const double* price;           /* [n_kinds] price_rate */
+  const int32_t* cq_capacity;    /* [n_kinds] Configurator.cq_capacity (configurator.py:443-458) */
+  double alpha, beta, timeout_factor, dispatch_overhead, straggle_factor;
+  int32_t dfp_count;
+  int32_t ablations;             /* bits: 1 fb, 2 dfp, 4 sdb, 8 eslc, 16 pbc (configurator.py:23) */
+  int32_t draws;                 /* RNG draws made per start: 1 noise, 2 straggle, 4 failure (backend.py:52-57, 186) */
+} sp_des_spec;
+
+/* Per-replica result row (manager.py:577-630 RunReport inputs). status: 0 ok, 1-3 capacity,
+ * 4 livelock (RuntimeError, manager.py:563), 5 speculate_fixed found no configuration
+ * (RuntimeError, configurator.py:633-636), 6 non-finite score, 7 draw capacity, 8 weight
+ * capacity, 9 buffer capacity, 10 event cap. */
+typedef struct {
+  double latency, cost, now, pad;
+  int32_t status, met, completed, failures, duplicates, invocations, terminal_items, n_speculate,
+      n_commit, configs_used, log_len, events;
+} sp_des_out;
+
+/* One decision_log row (configurator.py:650-654, 746-749): meta = op | entry << 8 | commit << 30. */
+typedef struct {
+  double t, slack, obj;
+  int32_t iid, meta;
+} sp_des_log;
+
+int sp_des_create(sp_ctx* ctx, const sp_des_spec* spec, sp_des** out);
+int sp_des_destroy(sp_ctx* ctx, sp_des* des);
+/* Run R replicas.  Replica r's trace is frames [frame_off[r], frame_off[r+1]) of `attrs`
+ * (n_attrs ints per frame, 0 where the frame lacks the attribute), its target target_s[r].
+ * draw_factor / draw_bits (R x draw_cap, or NULL when spec.draws == 0): per start, in start order,
+ * exp(N(0, sigma)) and bit0 straggled / bit1 will_fail from the replica's numpy stream.  log
+ * (R x log_cap rows, optional), lat_out (R x n_entries final latencies, optional), out (R rows).
+ * mem: SP_MEM_HOST (copies in, launch, copies out, synchronises) or SP_MEM_DEVICE. */
+int sp_des_run(sp_ctx* ctx, sp_des* des, int32_t R, const int32_t* frame_off, const int32_t* attrs,
+               const double* target_s, int32_t draw_cap, const double* draw_factor,
+               const uint8_t* draw_bits, int32_t log_cap, sp_des_log* log, double* lat_out,
+               sp_des_out* out, int32_t mem);
+/* Size the per-replica arenas for R replicas of these traces (host frame_off / attrs) and the
+ * given draw / log capacities; sp_des_run with SP_MEM_DEVICE buffers requires it (the host-buffer
+ * form calls it itself). */
+int sp_des_prepare(sp_ctx* ctx, sp_des* des, int32_t R, const int32_t* frame_off,
+                   const int32_t* attrs, int32_t draw_cap, int32_t log_cap);
+/* Invocation capacity per buffered item (default 1.25; retries and straggler duplicates add
+ * invocations beyond one per item — a replica that runs out reports status 1). */
+int sp_des_set_capacity(sp_des* des, double invocations_per_item);
+/* Bytes of one replica's arena as last prepared. */
+int64_t sp_des_arena_bytes(sp_des* des);
+
 #ifdef __cplusplus
 }
 #endif

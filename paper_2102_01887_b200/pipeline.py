@@ -188,11 +188,27 @@ def reference_config(spec) -> Any:
     )
 
 
+_PREDICATE_OPS = ("<", "<=", ">", ">=", "==", "!=")
+
+
+@dataclass(frozen=True)
+class BranchPredicate:
+    """Comparison over one integer input attribute, e.g. persons > 0 (pipeline.py:283-295)."""
+
+    attr: str
+    op: str
+    value: int
+
+    def __post_init__(self) -> None:
+        if self.op not in _PREDICATE_OPS:
+            raise ValueError(f"unknown predicate operator {self.op!r}")
+
+
 @dataclass
 class PipelineDag:
-    """Operations wired into a DAG (pipeline.py:298-337).  Branch predicates and fan-out
-    rules do not influence Alg. 1 (every decomposed path counts), so only the structure is
-    kept here."""
+    """Operations wired into a DAG (pipeline.py:298-337).  Branch predicates and fan-out rules
+    do not influence Alg. 1 (every decomposed path counts); the run engine (engine.py) routes
+    items by them."""
 
     vertices: tuple[str, ...]
     edges: tuple[tuple[str, str], ...]
@@ -252,5 +268,7 @@ def dag_from_json(obj: Mapping[str, Any]) -> PipelineDag:
         vertices=names,
         edges=tuple((e[0], e[1]) for e in obj["edges"]),
         branching=frozenset(op["name"] for op in obj["operations"] if op.get("branching")),
+        branch_predicates={(p["src"], p["dst"]): BranchPredicate(p["attr"], p["op"], int(p["value"]))
+                           for p in obj.get("branch_predicates", [])},
         fanout_rules=dict(obj.get("fanout_rules", {})),
     )

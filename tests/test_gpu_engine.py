@@ -1,0 +1,78 @@
+"""Replica-parallel run engine on the B200 (k_des_run) against the
+reference's own runs: all 69 golden runs (tests/golden/des/runs.json) — every decision-log row,
+the report and the final latency tables bit for bit — run as replicas of one launch per run
+description; the PipelineRun drop-in's CSV row; fresh random cases against oracle/engine.py."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import des_cases as dc
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def device_engine(gpu_ctx):
+    from paper_2102_01887_b200.engine import ReplicaEngine
+
+    return lambda spec: ReplicaEngine(spec, gpu_ctx)
+
+
+def test_device_engine_matches_golden_runs(device_engine, gpu_ctx):
+    launches0 = gpu_ctx.launch_count
+    bad = []
+    n = 0
+    for group in dc.groups(dc.runs()):
+        for case, (rows, rep, lat) in zip(group, dc.run_group(device_engine, group)):
+            n += 1
+            errs = dc.check(case, rows, rep, lat)
+            if errs:
+                bad.append((case["bundle"], case["target"], case.get("ablations"), errs[:3]))
+    assert n == 69
+    assert not bad, bad
+    assert gpu_ctx.launch_count > launches0
+
+
+def test_pipeline_run_dropin_csv_row(gpu_ctx, tmp_path):
+    from paper_2102_01887_b200.engine import PipelineRun
+
+    case = dc.runs()[3]  # AMBER, 50 % target
+    doc, dag, sc, profiles, paths, frames = dc.bundle("branching")
+    spec = dc.run_spec(case)
+    run = PipelineRun(dag, {}, profiles, frames, sc, float(case["target"]), spec.params, paths=paths,
+                      pipeline_name=doc["name"], ctx=gpu_ctx)
+    rep = run.run_to_completion()
+    assert rep.csv_row().split(",")[1:] == case["expect"]["csv_row"].split(",")[1:]
+    assert dc.log_digest(run.decision_log) == case["expect"]["log_sha256"]
+    run.write_decision_log(str(tmp_path / "log.tsv"))
+    assert sum(1 for _ in open(tmp_path / "log.tsv")) == case["expect"]["log_rows"] + 1
+
+
+def test_device_engine_random_cases_vs_oracle(device_engine):
+    """Fresh traces / seeds / faults on the join bundle, checked by oracle/engine.py."""
+    from oracle import engine as oe
+    from paper_2102_01887_b200.engine import generate_trace
+
+    rng = np.random.default_rng(5)
+    base = dict(bundle="parallel", noise_sigma=0.25, failure_rate=0.08, straggle_rate=0.05,
+                straggle_factor=3.0)
+    spec = dc.run_spec(base)
+    doc, dag, sc, profiles, paths, _ = dc.bundle("parallel")
+    eng = device_engine(spec)
+    traces = [generate_trace(int(rng.integers(100, 400)), 1000 + i, {"persons": 0.7}, 3) for i in range(6)]
+    targets = [float(rng.uniform(10, 90)) for _ in traces]
+    seeds = [int(rng.integers(0, 2**31)) for _ in traces]
+    res = eng.run(traces, targets, seeds, log_cap=20000, final_tables=True)
+    t = sc.tuning
+    for tr, tg, sd, r in zip(traces, targets, seeds, res):
+        o = oe.Engine(dag, profiles, tr, sc, tg,
+                      oe.Params(t.alpha, t.cq_capacity, t.dfp_count, t.straggler_timeout_factor,
+                                t.smoothing_beta), seed=sd, paths=paths, noise_sigma=0.25,
+                      failure_rate=0.08, straggle_rate=0.05, straggle_factor=3.0)
+        want = o.run()
+        assert dc.log_digest(eng.log_rows(r.log)) == dc.log_digest(want.log)
+        assert repr(r.cost) == repr(float(want.cost))
+        assert (r.failures, r.duplicates, r.invocations) == (want.failures, want.duplicates, want.invocations)
+        lat = np.concatenate([o.t[op].lat for op in o.ops])
+        assert np.array_equal(lat.view(np.uint64), r.lat.view(np.uint64))

@@ -1,0 +1,32 @@
+"""Throughput probe of the replica-parallel run engine (k_des_run) on config-4 replicas."""
+import sys
+import time
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent / "tests"))
+import numpy as np
+
+import des_cases as dc
+import paper_2102_01887_b200 as sp
+from paper_2102_01887_b200.engine import ReplicaEngine, generate_trace
+
+CP_MIN = 90.41885182994682
+ctx = sp.get_context(0)
+case = dc.runs()[3]
+spec = dc.run_spec(case)
+eng = ReplicaEngine(spec, ctx)
+for R in [int(x) for x in (sys.argv[1:] or ["148", "1024", "4096"])]:
+    t0 = time.time()
+    traces = [generate_trace(3000, 17 + r // 5, {"cars": 0.6, "persons": 0.8}, 3) for r in range(R)]
+    targets = [(0.5, 1.0, 2.0, 5.0, 10.0)[r % 5] * CP_MIN for r in range(R)]
+    fo, at = spec.encode_frames(traces)
+    t1 = time.time()
+    res = eng.run(None, targets, None, encoded=(fo, at))
+    t2 = time.time()
+    res = eng.run(None, targets, None, encoded=(fo, at))
+    t3 = time.time()
+    dec = sum(r.decision_count for r in res)
+    print(f"R={R}: gen {t1-t0:.2f}s run {t2-t1:.3f}s / {t3-t2:.3f}s  {R/(t3-t2):.1f} runs/s  "
+          f"{dec/(t3-t2):.3e} decisions/s  arena {eng.lib.sp_des_arena_bytes(eng.handle)/1e6:.2f} MB/replica",
+          flush=True)
