@@ -421,7 +421,8 @@ typedef struct {
  * (RuntimeError, configurator.py:633-636), 6 non-finite score, 7 draw capacity, 8 weight
  * capacity, 9 buffer capacity, 10 event cap. */
 typedef struct {
-  double latency, cost, now, pad;
+  double latency, cost, now;
+  int32_t peak_slots, peak_heap;  /* most invocation slots / heap entries the replica held at once */
   int32_t status, met, completed, failures, duplicates, invocations, terminal_items, n_speculate,
       n_commit, configs_used, log_len, events;
 } sp_des_out;
@@ -434,20 +435,21 @@ typedef struct {
 
 int sp_des_create(sp_ctx* ctx, const sp_des_spec* spec, sp_des** out);
 int sp_des_destroy(sp_ctx* ctx, sp_des* des);
-/* Run R replicas.  Replica r's trace is frames [frame_off[r], frame_off[r+1]) of `attrs`
- * (n_attrs ints per frame, 0 where the frame lacks the attribute), its target target_s[r].
+/* Run R replicas over n_traces traces: trace t is frames [frame_off[t], frame_off[t+1]) of
+ * `attrs` (n_attrs ints per frame, 0 where the frame lacks the attribute); replica r runs trace
+ * trace_of[r] (NULL: trace r, n_traces == R) with target target_s[r].
  * draw_factor / draw_bits (R x draw_cap, or NULL when spec.draws == 0): per start, in start order,
  * exp(N(0, sigma)) and bit0 straggled / bit1 will_fail from the replica's numpy stream.  log
  * (R x log_cap rows, optional), lat_out (R x n_entries final latencies, optional), out (R rows).
  * mem: SP_MEM_HOST (copies in, launch, copies out, synchronises) or SP_MEM_DEVICE. */
-int sp_des_run(sp_ctx* ctx, sp_des* des, int32_t R, const int32_t* frame_off, const int32_t* attrs,
-               const double* target_s, int32_t draw_cap, const double* draw_factor,
+int sp_des_run(sp_ctx* ctx, sp_des* des, int32_t R, int32_t n_traces, const int32_t* frame_off,
+               const int32_t* attrs, const int32_t* trace_of, const double* target_s, int32_t draw_cap, const double* draw_factor,
                const uint8_t* draw_bits, int32_t log_cap, sp_des_log* log, double* lat_out,
                sp_des_out* out, int32_t mem);
 /* Size the per-replica arenas for R replicas of these traces (host frame_off / attrs) and the
  * given draw / log capacities; sp_des_run with SP_MEM_DEVICE buffers requires it (the host-buffer
  * form calls it itself). */
-int sp_des_prepare(sp_ctx* ctx, sp_des* des, int32_t R, const int32_t* frame_off,
+int sp_des_prepare(sp_ctx* ctx, sp_des* des, int32_t R, int32_t n_traces, const int32_t* frame_off,
                    const int32_t* attrs, int32_t draw_cap, int32_t log_cap);
 /* Invocation capacity per buffered item (default 1.25; retries and straggler duplicates add
  * invocations beyond one per item — a replica that runs out reports status 1). */

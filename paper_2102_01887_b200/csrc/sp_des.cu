@@ -22,6 +22,8 @@ struct sp_des {
   spdes::Image* d_image = nullptr;
   char* arena = nullptr;
   size_t arena_cap = 0;
+  void* tabs = nullptr;  // lat / cost / costpen, the 32 replicas of a warp interleaved
+  size_t tabs_cap = 0;
   int32_t prepared_R = 0;
   // staged host I/O
   void* io = nullptr;
@@ -32,13 +34,14 @@ namespace {
 
 using namespace spdes;
 
-constexpr int kThreads = 64;
+constexpr int kMaxThreads = 128;
 constexpr size_t kSmemEntriesMax = 64 * 1024;
 
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kMaxThreads)
 k_des_run(const Image* __restrict__ g_im, const double* __restrict__ g_d,
-          const int32_t* __restrict__ g_i, char* __restrict__ arena, int R,
+          const int32_t* __restrict__ g_i, char* __restrict__ arena, double* __restrict__ tabs, int R,
           const int32_t* __restrict__ frame_off, const int32_t* __restrict__ attrs,
+          const int32_t* __restrict__ trace_of,
           const double* __restrict__ targets, const double* __restrict__ dfac,
           const uint8_t* __restrict__ dbits, LogRec* __restrict__ log,
           double* __restrict__ lat_out, Out* __restrict__ out, int entries_in_smem) {
@@ -57,7 +60,8 @@ k_des_run(const Image* __restrict__ g_im, const double* __restrict__ g_d,
     double* sd = reinterpret_cast<double*>(smem + sizeof(Image));
     int32_t* si = reinterpret_cast<int32_t*>(sd + 8 * (size_t)N);
     for (int i = threadIdx.x; i < 8 * N; i += blockDim.x) sd[i] = g_d[i];
-    for (int i = threadIdx.x; i < 4 * N; i += blockDim.x) si[i] = g_i[i];
+    const int ni = 4 * N + g_im->suf_off[g_im->n_ops];
+    for (int i = threadIdx.x; i < ni; i += blockDim.x) si[i] = g_i[i];
     dcol = sd;
     icol = si;
   }
@@ -65,15 +69,17 @@ k_des_run(const Image* __restrict__ g_im, const double* __restrict__ g_d,
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= R) return;
   const Entries E = entries_view(dcol, icol, N);
-  const int f0 = frame_off[r];
-  Run run(im, E, arena + (size_t)r * im.arena_bytes, attrs + (int64_t)f0 * im.n_attrs,
-          frame_off[r + 1] - f0, targets[r], dfac ? dfac + (size_t)r * im.draw_cap : nullptr,
+  const int tr = trace_of ? trace_of[r] : r;
+  const int f0 = frame_off[tr];
+  Run run(im, E, arena + (size_t)r * im.arena_bytes, tabs + (size_t)(r >> 5) * (96 * (size_t)N) + (r & 31),
+          32, attrs + (int64_t)f0 * im.n_attrs,
+          frame_off[tr + 1] - f0, targets[r], dfac ? dfac + (size_t)r * im.draw_cap : nullptr,
           dbits ? dbits + (size_t)r * im.draw_cap : nullptr,
           log ? log + (size_t)r * im.log_cap : nullptr);
   run.run();
   run.write_out(out[r]);
   if (lat_out)
-    for (int i = 0; i < N; ++i) lat_out[(size_t)r * N + i] = run.lat[i];
+    for (int i = 0; i < N; ++i) lat_out[(size_t)r * N + i] = run.lat(i);
 }
 
 template <class T>
@@ -94,14 +100,16 @@ int grow(void** p, size_t* cap, size_t bytes) {
   return SP_OK;
 }
 
-int prepare(sp_ctx* ctx, sp_des* d, int32_t R, const int32_t* frame_off, const int32_t* attrs,
-            int32_t draw_cap, int32_t log_cap) {
+int prepare(sp_ctx* ctx, sp_des* d, int32_t R, int32_t T, const int32_t* frame_off,
+            const int32_t* attrs, int32_t draw_cap, int32_t log_cap) {
   std::string err;
-  if (!plan_run(d->h, R, frame_off, attrs, draw_cap, log_cap, err)) return sp::fail(SP_E_INVALID, err);
+  if (!plan_run(d->h, T, frame_off, attrs, draw_cap, log_cap, err)) return sp::fail(SP_E_INVALID, err);
   const size_t need = (size_t)d->h.im.arena_bytes * (size_t)R;
   void* a = d->arena;
   int rc = grow(&a, &d->arena_cap, need);
   d->arena = (char*)a;
+  if (rc != SP_OK) return rc;
+  rc = grow(&d->tabs, &d->tabs_cap, sizeof(double) * 96 * (size_t)d->h.im.n_entries * (size_t)((R + 31) / 32));
   if (rc != SP_OK) return rc;
   cudaError_t e = cudaMemcpyAsync(d->d_image, &d->h.im, sizeof(Image), cudaMemcpyHostToDevice, ctx->stream);
   if (e != cudaSuccess) return sp::cuda_fail(e, "run engine image");
@@ -110,17 +118,20 @@ int prepare(sp_ctx* ctx, sp_des* d, int32_t R, const int32_t* frame_off, const i
 }
 
 int launch(sp_ctx* ctx, sp_des* d, int32_t R, const int32_t* frame_off, const int32_t* attrs,
-           const double* targets, const double* dfac, const uint8_t* dbits, LogRec* log,
+           const int32_t* trace_of, const double* targets, const double* dfac, const uint8_t* dbits, LogRec* log,
            double* lat_out, Out* out) {
   const int N = d->h.im.n_entries;
-  const size_t ebytes = (size_t)N * (8 * sizeof(double) + 4 * sizeof(int32_t));
+  const size_t ebytes = (size_t)N * (8 * sizeof(double) + 4 * sizeof(int32_t)) +
+                        sizeof(int32_t) * (size_t)d->h.im.suf_off[d->h.im.n_ops];
   const int in_smem = ebytes <= kSmemEntriesMax;
   const size_t smem = sizeof(Image) + (in_smem ? ebytes : 0);
   cudaError_t e = cudaFuncSetAttribute(k_des_run, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return sp::cuda_fail(e, "run engine smem");
   if (R > 0) {
-    k_des_run<<<(R + kThreads - 1) / kThreads, kThreads, smem, ctx->stream>>>(
-        d->d_image, d->d_dcols, d->d_icols, d->arena, R, frame_off, attrs, targets, dfac, dbits,
+    // one replica per thread; CTAs as wide as the replica count allows while every SM gets work
+    const int threads = R >= 128 * ctx->num_sms ? 128 : (R >= 64 * ctx->num_sms ? 64 : 32);
+    k_des_run<<<(R + threads - 1) / threads, threads, smem, ctx->stream>>>(
+        d->d_image, d->d_dcols, d->d_icols, d->arena, (double*)d->tabs, R, frame_off, attrs, trace_of, targets, dfac, dbits,
         log, lat_out, out, in_smem);
     ctx->launches++;
     e = cudaGetLastError();
@@ -165,6 +176,7 @@ extern "C" int sp_des_destroy(sp_ctx* ctx, sp_des* d) {
   cudaFree(d->d_icols);
   cudaFree(d->d_image);
   cudaFree(d->arena);
+  cudaFree(d->tabs);
   cudaFree(d->io);
   delete d;
   return SP_OK;
@@ -172,13 +184,14 @@ extern "C" int sp_des_destroy(sp_ctx* ctx, sp_des* d) {
 
 extern "C" int64_t sp_des_arena_bytes(sp_des* d) { return d ? d->h.im.arena_bytes : -1; }
 
-extern "C" int sp_des_prepare(sp_ctx* ctx, sp_des* d, int32_t R, const int32_t* frame_off,
-                              const int32_t* attrs, int32_t draw_cap, int32_t log_cap) {
+extern "C" int sp_des_prepare(sp_ctx* ctx, sp_des* d, int32_t R, int32_t n_traces,
+                              const int32_t* frame_off, const int32_t* attrs, int32_t draw_cap,
+                              int32_t log_cap) {
   sp::DeviceScope _dev_scope(ctx ? ctx->device : -1);
-  if (!ctx || !d || R < 0 || !frame_off || (R > 0 && !attrs && d->h.im.n_attrs > 0) || draw_cap < 0 ||
-      log_cap < 0)
+  if (!ctx || !d || R < 0 || n_traces < 0 || !frame_off ||
+      (n_traces > 0 && !attrs && d->h.im.n_attrs > 0) || draw_cap < 0 || log_cap < 0)
     return sp::fail(SP_E_INVALID, "des_prepare: bad argument");
-  return prepare(ctx, d, R, frame_off, attrs, draw_cap, log_cap);
+  return prepare(ctx, d, R, n_traces, frame_off, attrs, draw_cap, log_cap);
 }
 
 extern "C" int sp_des_set_capacity(sp_des* d, double invocations_per_item) {
@@ -188,14 +201,16 @@ extern "C" int sp_des_set_capacity(sp_des* d, double invocations_per_item) {
   return SP_OK;
 }
 
-extern "C" int sp_des_run(sp_ctx* ctx, sp_des* d, int32_t R, const int32_t* frame_off,
-                          const int32_t* attrs, const double* target_s, int32_t draw_cap,
+extern "C" int sp_des_run(sp_ctx* ctx, sp_des* d, int32_t R, int32_t n_traces,
+                          const int32_t* frame_off, const int32_t* attrs, const int32_t* trace_of,
+                          const double* target_s, int32_t draw_cap,
                           const double* draw_factor, const uint8_t* draw_bits, int32_t log_cap,
                           sp_des_log* log, double* lat_out, sp_des_out* out, int32_t mem) {
   sp::DeviceScope _dev_scope(ctx ? ctx->device : -1);
   static_assert(sizeof(sp_des_out) == sizeof(Out), "sp_des_out layout");
   static_assert(sizeof(sp_des_log) == sizeof(LogRec), "sp_des_log layout");
-  if (!ctx || !d || R < 0 || !frame_off || !target_s || !out || draw_cap < 0 || log_cap < 0 ||
+  if (!ctx || !d || R < 0 || n_traces < 1 || !frame_off || !target_s || !out || draw_cap < 0 ||
+      log_cap < 0 || (!trace_of && n_traces != R) ||
       (mem != SP_MEM_HOST && mem != SP_MEM_DEVICE))
     return sp::fail(SP_E_INVALID, "des_run: bad argument");
   const Image& im = d->h.im;
@@ -207,13 +222,16 @@ extern "C" int sp_des_run(sp_ctx* ctx, sp_des* d, int32_t R, const int32_t* fram
   if (mem == SP_MEM_DEVICE) {
     if (d->prepared_R < R || im.draw_cap != draw_cap || im.log_cap != log_cap)
       return sp::fail(SP_E_INVALID, "des_run: device buffers need sp_des_prepare with the same R / caps");
-    int rc = launch(ctx, d, R, frame_off, attrs, target_s, draw_factor, draw_bits,
+    int rc = launch(ctx, d, R, frame_off, attrs, trace_of, target_s, draw_factor, draw_bits,
                     reinterpret_cast<LogRec*>(log), lat_out, reinterpret_cast<Out*>(out));
     return rc;
   }
-  int rc = prepare(ctx, d, R, frame_off, attrs, draw_cap, log_cap);
+  if (trace_of)
+    for (int r = 0; r < R; ++r)
+      if (trace_of[r] < 0 || trace_of[r] >= n_traces) return sp::fail(SP_E_INVALID, "des_run: bad trace_of");
+  int rc = prepare(ctx, d, R, n_traces, frame_off, attrs, draw_cap, log_cap);
   if (rc != SP_OK) return rc;
-  const int64_t F = frame_off[R];
+  const int64_t F = frame_off[n_traces];
   const int N = im.n_entries;
   // staged inputs / outputs in one device block
   size_t off = 0;
@@ -222,7 +240,8 @@ extern "C" int sp_des_run(sp_ctx* ctx, sp_des* d, int32_t R, const int32_t* fram
     off = (off + bytes + 255) & ~(size_t)255;
     return at;
   };
-  const size_t s_off = slot(4 * (size_t)(R + 1));
+  const size_t s_off = slot(4 * (size_t)(n_traces + 1));
+  const size_t s_trace = trace_of ? slot(4 * (size_t)R) : 0;
   const size_t s_attr = slot(4 * (size_t)std::max<int64_t>(F * im.n_attrs, 1));
   const size_t s_tgt = slot(8 * (size_t)R);
   const size_t s_fac = draw_factor ? slot(8 * (size_t)R * draw_cap) : 0;
@@ -234,7 +253,9 @@ extern "C" int sp_des_run(sp_ctx* ctx, sp_des* d, int32_t R, const int32_t* fram
   if (rc != SP_OK) return rc;
   char* io = (char*)d->io;
   cudaStream_t st = ctx->stream;
-  cudaError_t e = cudaMemcpyAsync(io + s_off, frame_off, 4 * (size_t)(R + 1), cudaMemcpyHostToDevice, st);
+  cudaError_t e = cudaMemcpyAsync(io + s_off, frame_off, 4 * (size_t)(n_traces + 1), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess && trace_of)
+    e = cudaMemcpyAsync(io + s_trace, trace_of, 4 * (size_t)R, cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess && F * im.n_attrs > 0)
     e = cudaMemcpyAsync(io + s_attr, attrs, 4 * (size_t)(F * im.n_attrs), cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess) e = cudaMemcpyAsync(io + s_tgt, target_s, 8 * (size_t)R, cudaMemcpyHostToDevice, st);
@@ -244,7 +265,7 @@ extern "C" int sp_des_run(sp_ctx* ctx, sp_des* d, int32_t R, const int32_t* fram
     e = cudaMemcpyAsync(io + s_bits, draw_bits, (size_t)R * draw_cap, cudaMemcpyHostToDevice, st);
   if (e != cudaSuccess) return sp::cuda_fail(e, "des_run inputs");
   rc = launch(ctx, d, R, (const int32_t*)(io + s_off), (const int32_t*)(io + s_attr),
-              (const double*)(io + s_tgt), draw_factor ? (const double*)(io + s_fac) : nullptr,
+              trace_of ? (const int32_t*)(io + s_trace) : nullptr, (const double*)(io + s_tgt), draw_factor ? (const double*)(io + s_fac) : nullptr,
               draw_bits ? (const uint8_t*)(io + s_bits) : nullptr,
               log ? (LogRec*)(io + s_log) : nullptr, lat_out ? (double*)(io + s_lat) : nullptr,
               (Out*)(io + s_out));

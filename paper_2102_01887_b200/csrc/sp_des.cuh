@@ -52,7 +52,8 @@ constexpr int kOk = 0, kErrInvCap = 1, kErrHeapCap = 2, kErrSegCap = 3, kErrLive
 // invocation states (manager.py:33-42)
 constexpr uint8_t kPending = 0, kSpeculated = 1, kCommitted = 3, kRunning = 4, kCompleted = 5,
                   kFailed = 6, kDuplicated = 7;
-constexpr uint8_t kBitForced = 1, kBitDupSpawned = 2, kBitWillFail = 4, kBitResolved = 8;
+constexpr uint8_t kBitForced = 1, kBitDupSpawned = 2, kBitWillFail = 4, kBitResolved = 8,
+                  kBitWakePending = 16;
 
 struct alignas(16) Image {  // static run description, shared by every replica (built by sp_des_create)
   int32_t n_ops, n_kinds, n_entries, n_attrs, n_cfg;
@@ -72,7 +73,6 @@ struct alignas(16) Image {  // static run description, shared by every replica (
   int32_t join_base[kMaxOps];   // staging base of a join vertex (units of frames), -1 otherwise
   int32_t fanout_attr[kMaxOps];
   int32_t suf_off[kMaxOps + 1];
-  int32_t suf[kMaxSuffixInts];  // per op: [len, ops...] per suffix
   double pool_res[kMaxKinds], price[kMaxKinds];
   int32_t inst_res[kMaxKinds], inst_off[kMaxKinds + 1], cap[kMaxKinds];
   int32_t w_off[kMaxKinds + 1];  // weight-list capacity per kind (prefix)
@@ -81,17 +81,20 @@ struct alignas(16) Image {  // static run description, shared by every replica (
   int64_t event_cap;
   int32_t buf_off[kMaxOps + 1];  // item buffer of each op (ints)
   int64_t o_lat, o_obs, o_inv, o_next, o_live, o_list, o_seg, o_buf, o_heap, o_wkey, o_wcnt,
-      o_scver, o_scval, o_holddl, o_free, o_staging, o_cfg, o_opi, arena_bytes;
+      o_scver, o_scval, o_holddl, o_free, o_staging, o_cfg, o_opi, o_free_slot, o_free_seg,
+      arena_bytes;
 };
 
 struct Entries {  // static per-entry columns (table order: ops sorted by name, entries in spec order)
   const double *lat0, *lat_init, *res, *batch, *pool, *price, *base, *per_item;
   const int32_t *bint, *kind, *rank, *cfg;
+  const int32_t* suf;  // per op: [len, ops...] per path suffix containing it (Image::suf_off)
 };
 
-struct Inv {  // 64 B (manager.py:49-80 Invocation, backend.py:86-99 RunningInvocation)
+struct Inv {  // 72 B (manager.py:49-80 Invocation, backend.py:86-99 RunningInvocation)
   double spec_slack, spec_obj, com_slack, started_at, threshold, actual;
-  int32_t unit;
+  int32_t unit;  // slot of the unit's first invocation (it holds the unit's items and counters)
+  int32_t iid;   // invocation id (manager.py:303-305)
   int16_t spec_e, com_e;
   int32_t instance;
   uint8_t op, state, bits, pad;
@@ -121,7 +124,8 @@ constexpr int kOpiBufHead = 0, kOpiBufTail = 1, kOpiSqHead = 2, kOpiSqTail = 3, 
               kOpiUnspawned = 5, kOpiCompletedRef = 6, kOpiHold = 7, kOpiN = 8;
 
 struct Out {  // per-replica result
-  double latency, cost, now, pad;
+  double latency, cost, now;
+  int32_t peak_slots, peak_heap;
   int32_t status, met, completed, failures, dups, invocations, terminal, n_spec, n_commit,
       configs_used, log_len, events;
 };
@@ -153,8 +157,11 @@ struct Run {
   const double* draw_factor;  // [draw_cap] exp(N(0, sigma)) per start, or null
   const uint8_t* draw_bits;   // [draw_cap] bit0 straggled, bit1 will_fail, or null
   LogRec* log;
+  // mutable entry columns lat / cost / cost + penalty: entry g of column c at tab[(c*N + g) * ts]
+  // (device: the 32 replicas of a warp interleaved, ts = 32, so converged scans coalesce)
+  double* tab;
+  int32_t ts;
   // arena views
-  double* lat;
   uint8_t* observed;
   Inv* inv;
   int32_t *next, *live;
@@ -164,25 +171,34 @@ struct Run {
   HeapEnt* heap;
   int32_t *wkey, *wcnt;
   int32_t* scver;
-  double *scval, *holddl;
+  double *scval, *holddl, *rmin, *rmax;
+  int32_t* rver;
   int32_t *freeres, *staging;
   uint32_t* cfg_used;
   int32_t* opi;
   // scalars
   double now = 0.0;
   int32_t version = 0, seq = 0, next_id = 0, running = 0, n_seg = 0, heap_n = 0, n_starts = 0;
+  // invocation slots and item-list segments are recycled (free stacks) once nothing refers to them
+  int32_t n_slot = 0, n_free_slot = 0, n_free_seg = 0, live_slots = 0, peak_slots = 0, peak_heap = 0;
+  int32_t *free_slot, *free_seg;
   int32_t wn[2][kMaxKinds];
+  // Eq. 2 per kind, cached until the kind's weight list or a latency of one of its entries
+  // changes (a pure function of both, so the cache never changes a value)
+  double qv[kMaxKinds];
+  int32_t qver[kMaxKinds], kver[kMaxKinds];
+  int32_t ref_version = 0;
   int32_t cq_head[kMaxKinds], cq_tail[kMaxKinds], cq_len[kMaxKinds];
   double total_cost = 0.0, last_accept = 0.0;
   int32_t failures = 0, dups = 0, completed = 0, met = 0, terminal = 0, n_spec = 0, n_commit = 0,
           log_len = 0, status = kOk;
   int64_t events = 0;
 
-  SPD_HD Run(const Image& im_, const Entries& e_, char* arena, const int32_t* attrs_, int32_t nf,
-             double tgt, const double* dfac, const uint8_t* dbits, LogRec* log_)
+  SPD_HD Run(const Image& im_, const Entries& e_, char* arena, double* tab_, int32_t ts_,
+             const int32_t* attrs_, int32_t nf, double tgt, const double* dfac, const uint8_t* dbits,
+             LogRec* log_)
       : im(im_), E(e_), attrs(attrs_), n_frames(nf), target(tgt), draw_factor(dfac),
-        draw_bits(dbits), log(log_) {
-    lat = (double*)(arena + im.o_lat);
+        draw_bits(dbits), log(log_), tab(tab_), ts(ts_) {
     observed = (uint8_t*)(arena + im.o_obs);
     inv = (Inv*)(arena + im.o_inv);
     next = (int32_t*)(arena + im.o_next);
@@ -196,27 +212,51 @@ struct Run {
     scver = (int32_t*)(arena + im.o_scver);
     scval = (double*)(arena + im.o_scval);
     holddl = (double*)(arena + im.o_holddl);
+    rmin = holddl + im.n_ops;
+    rmax = holddl + 2 * im.n_ops;
+    rver = (int32_t*)(holddl + 3 * im.n_ops);
     freeres = (int32_t*)(arena + im.o_free);
     staging = (int32_t*)(arena + im.o_staging);
     cfg_used = (uint32_t*)(arena + im.o_cfg);
     opi = (int32_t*)(arena + im.o_opi);
+    free_slot = (int32_t*)(arena + im.o_free_slot);
+    free_seg = (int32_t*)(arena + im.o_free_seg);
   }
 
   SPD_HD int32_t& OP(int op, int f) { return opi[op * kOpiN + f]; }
+  SPD_HD double lat(int g) const { return tab[(size_t)g * ts]; }
+  SPD_HD double cost(int g) const { return tab[(size_t)(im.n_entries + g) * ts]; }
+  SPD_HD double costpen(int g) const { return tab[(size_t)(2 * im.n_entries + g) * ts]; }
+  // OpTable.set_latency (configurator.py:211-213) + the Eq. 1 terms of the entry in numpy's order
+  // (configurator.py:224-225): score = lat < slack ? cost + 0.0 : cost + penalty
+  SPD_HD void set_lat(int g, double L) {
+    const double R = E.res[g], B = E.batch[g];
+    const double c = ((R * L) * E.price[g]) / B;
+    const double pen = im.alpha * ((L * R) / (B * E.pool[g]));
+    ++kver[E.kind[g]];
+    tab[(size_t)g * ts] = L;
+    tab[(size_t)(im.n_entries + g) * ts] = c;
+    tab[(size_t)(2 * im.n_entries + g) * ts] = c + pen;
+  }
   SPD_HD void error(int code) {
     if (status == kOk) status = code;
   }
 
   // ---- initial state (manager.py:210-300, configurator.py:375-438) --------------------------
   SPD_HDN void init() {
+    for (int k = 0; k < kMaxKinds; ++k) {
+      kver[k] = 0;
+      qver[k] = -1;
+    }
     for (int i = 0; i < im.n_entries; ++i) {
-      lat[i] = E.lat0[i];
+      set_lat(i, E.lat0[i]);
       observed[i] = 0;
     }
     for (int o = 0; o < im.n_ops; ++o) {
       for (int f = 0; f < kOpiN; ++f) OP(o, f) = 0;
       OP(o, kOpiSqHead) = OP(o, kOpiSqTail) = -1;
       scver[o] = -1;
+      rver[o] = -1;
     }
     for (int k = 0; k < im.n_kinds; ++k) {
       wn[0][k] = wn[1][k] = 0;
@@ -240,6 +280,7 @@ struct Run {
     ++seq;
     HeapEnt x{t, ((uint32_t)code << 31) | (uint32_t)seq, payload};
     int i = heap_n++;
+    if (heap_n > peak_heap) peak_heap = heap_n;
     while (i > 0) {
       const int p = (i - 1) >> 1;
       if (!less(x, heap[p])) break;
@@ -296,6 +337,7 @@ struct Run {
         wn[q][k] = n + 1;
       }
     }
+    ++kver[k];
     ++version;  // self.bump()
   }
 
@@ -304,51 +346,75 @@ struct Run {
     double* out = scval + op * im.n_kinds;
     if (scver[op] == version) return out;
     const int K = im.n_kinds;
-    // _path_ratios: own / (left-to-right suffix total) per suffix containing op
-    double rr[32];
-    int nr = 0;
-    const double own = ref_lat(op);
-    for (int p = im.suf_off[op]; p < im.suf_off[op + 1];) {
-      const int len = im.suf[p++];
-      double tot = 0.0;
-      for (int j = 0; j < len; ++j) tot = tot + ref_lat(im.suf[p + j]);
-      p += len;
-      if (nr < 32) rr[nr++] = own / tot;
+    // _path_ratios (configurator.py:493-509): own / (left-to-right suffix total) per suffix
+    // containing op, recomputed when a reference latency changed.  min_r fl(r * budget) is
+    // fl(r_min * budget) for budget >= 0 and fl(r_max * budget) below (rounding is monotone), so
+    // only the two extremes are kept; NaN or non-positive ratios keep the literal loop.
+    if (rver[op] != ref_version) {
+      const double own = ref_lat(op);
+      double lo = 0.0, hi = 0.0;
+      bool plain = true;
+      int nr = 0;
+      for (int p = im.suf_off[op]; p < im.suf_off[op + 1]; ++nr) {
+        const int len = E.suf[p++];
+        double tot = 0.0;
+        for (int j = 0; j < len; ++j) tot = tot + ref_lat(E.suf[p + j]);
+        p += len;
+        const double r = own / tot;
+        if (!(r > 0.0) || r == INFINITY) plain = false;
+        if (nr == 0 || r < lo) lo = r;
+        if (nr == 0 || r > hi) hi = r;
+      }
+      rmin[op] = lo;
+      rmax[op] = plain ? hi : NAN;
+      rver[op] = ref_version;
     }
     const int wtot = im.w_off[K];
     for (int k = 0; k < K; ++k) {
-      double tot = 0.0;
-      for (int q = 0; q < 2; ++q) {
-        const int32_t* key = wkey + q * wtot + im.w_off[k];
-        const int32_t* cnt = wcnt + q * wtot + im.w_off[k];
-        for (int i = 0; i < wn[q][k]; ++i) {
-          const int o = key[i] >> 16, e = key[i] & 0xffff;
-          const int g = im.entry_off[o] + e;
-          tot = tot + (double)cnt[i] * (lat[g] * E.res[g]);
+      if (qver[k] != kver[k]) {  // queueing_by_kind (configurator.py:511-524)
+        double tot = 0.0;
+        for (int q = 0; q < 2; ++q) {
+          const int32_t* key = wkey + q * wtot + im.w_off[k];
+          const int32_t* cnt = wcnt + q * wtot + im.w_off[k];
+          for (int i = 0; i < wn[q][k]; ++i) {
+            const int o = key[i] >> 16, e = key[i] & 0xffff;
+            const int g = im.entry_off[o] + e;
+            tot = tot + (double)cnt[i] * (lat(g) * E.res[g]);
+          }
         }
+        qv[k] = tot / im.pool_res[k];
+        qver[k] = kver[k];
       }
-      const double budget = (target - now) - tot / im.pool_res[k];
-      double s = 0.0;
-      for (int j = 0; j < nr; ++j) {
-        const double v = rr[j] * budget;
-        if (j == 0 || v < s) s = v;
+      const double budget = (target - now) - qv[k];
+      if (rmax[op] == rmax[op]) {
+        out[k] = (budget >= 0.0 ? rmin[op] : rmax[op]) * budget;
+      } else {  // literal min over the ratios in suffix order (configurator.py:536-541)
+        const double own = ref_lat(op);
+        double sl = 0.0;
+        int j = 0;
+        for (int p = im.suf_off[op]; p < im.suf_off[op + 1]; ++j) {
+          const int len = E.suf[p++];
+          double tot = 0.0;
+          for (int i = 0; i < len; ++i) tot = tot + ref_lat(E.suf[p + i]);
+          p += len;
+          const double v = (own / tot) * budget;
+          if (j == 0 || v < sl) sl = v;
+        }
+        out[k] = sl;
       }
-      out[k] = s;
     }
     scver[op] = version;
     return out;
   }
   SPD_HD double ref_lat(int op) const {  // _ref_latency (configurator.py:409, 463-468)
     const int ri = im.ref_index[op];
-    return ri >= 0 ? lat[im.entry_off[op] + ri] : im.ref_lat0[op];
+    return ri >= 0 ? lat(im.entry_off[op] + ri) : im.ref_lat0[op];
   }
 
   // ---- OpTable.select / affinity (configurator.py:219-318) ---------------------------------
-  SPD_HD void score_of(int g, const double* sl, double& score, double& cost) {
-    const double L = lat[g], R = E.res[g], B = E.batch[g];
-    cost = ((R * L) * E.price[g]) / B;
-    const double pen = im.alpha * ((L * R) / (B * E.pool[g]));
-    score = cost + (L < sl[E.kind[g]] ? 0.0 : pen);
+  SPD_HD void score_of(int g, const double* sl, double& score, double& c) {
+    c = cost(g);
+    score = lat(g) < sl[E.kind[g]] ? c + 0.0 : costpen(g);
   }
   SPD_HD bool key_less(double s1, double c1, int g1, double s2, double c2, int g2) const {
     if (s1 != s2) return s1 < s2;
@@ -385,7 +451,7 @@ struct Run {
     if (best < 0) return r;  // no entry survives the mask: None (configurator.py:266-267)
     const int B = E.bint[best];
     if (allow_delay && B > avail && supply >= B - avail) {
-      const double wait = sl[E.kind[best]] - lat[best];
+      const double wait = sl[E.kind[best]] - lat(best);
       if (wait > 0.0) {
         r.code = 2;
         r.e = best - b0;
@@ -431,12 +497,18 @@ struct Run {
 
   // ---- invocations and item lists (manager.py:303-329) --------------------------------------
   SPD_HDN int new_inv(int op, int unit) {
-    if (next_id >= im.inv_cap) {
+    int id;
+    if (n_free_slot > 0) {
+      id = free_slot[--n_free_slot];
+    } else if (n_slot < im.inv_cap) {
+      id = ++n_slot;  // slots 1..inv_cap (a wake payload > 0 is a slot)
+    } else {
       error(kErrInvCap);
       return -1;
     }
-    const int id = ++next_id;
+    if (++live_slots > peak_slots) peak_slots = live_slots;
     Inv& v = inv[id];
+    v.iid = ++next_id;
     v.spec_slack = v.spec_obj = v.com_slack = v.actual = v.threshold = 0.0;
     v.started_at = -1.0;
     v.unit = unit < 0 ? id : unit;
@@ -456,11 +528,15 @@ struct Run {
   }
   SPD_HDN void take_items(int unit, int op, int n) {  // buffer.popleft() x n onto the list
     if (n <= 0) return;
-    if (n_seg >= im.seg_cap) {
+    int s;
+    if (n_free_seg > 0) {
+      s = free_seg[--n_free_seg];
+    } else if (n_seg < im.seg_cap) {
+      s = n_seg++;
+    } else {
       error(kErrSegCap);
       return;
     }
-    const int s = n_seg++;
     segs[s] = Seg{OP(op, kOpiBufHead), n, -1};
     OP(op, kOpiBufHead) += n;
     List& L = lists[unit];
@@ -473,6 +549,20 @@ struct Run {
   }
   SPD_HD int buf_len(int op) { return OP(op, kOpiBufTail) - OP(op, kOpiBufHead); }
   SPD_HD int fill_of(int id) { return lists[inv[id].unit].count; }
+  // A finished invocation's slot is recycled once its straggler wake has popped; a unit's first
+  // slot (items, resolved flag, live count) only when the unit is resolved and none of its
+  // duplicates / retries is still live.  Called when one of those conditions may have changed.
+  SPD_HDN void maybe_free(int id) {
+    const Inv& v = inv[id];
+    if (v.state < kCompleted || (v.bits & kBitWakePending)) return;
+    if (v.unit == id) {
+      if (!(v.bits & kBitResolved) || live[id] != 0) return;
+      for (int sg = lists[id].first; sg >= 0; sg = segs[sg].next) free_seg[n_free_seg++] = sg;
+    }
+    inv[id].state = kPending;  // poisoned: never finished again until reused
+    free_slot[n_free_slot++] = id;
+    --live_slots;
+  }
 
   // ---- backend pools (backend.py:155-201, manager.py:331-341) -------------------------------
   SPD_HDN void submit(int id) {
@@ -530,9 +620,10 @@ struct Run {
     const int c = E.cfg[g];
     cfg_used[c >> 5] |= 1u << (c & 31);
     weights(1, k, v.op, v.com_e, -1);  // notify_started (configurator.py:758-763)
-    const double thr = im.timeout_factor * lat[g];
+    const double thr = im.timeout_factor * lat(g);
     v.threshold = thr;
     const double at = now + thr;
+    v.bits |= kBitWakePending;
     wake(at + 1e-9 * (1.0 + fabs(at)), id);
   }
 
@@ -540,7 +631,7 @@ struct Run {
   SPD_HDN void log_row(int id, int op, int e, bool commit, double slack, double obj) {
     if (log) {
       if (log_len < im.log_cap)
-        log[log_len] = LogRec{now, slack, obj, id, op | (e << 8) | (commit ? (1 << 30) : 0)};
+        log[log_len] = LogRec{now, slack, obj, inv[id].iid, op | (e << 8) | (commit ? (1 << 30) : 0)};
     }
     ++log_len;
   }
@@ -682,13 +773,13 @@ struct Run {
         }
         Key key;
         if (fifo) {
-          key = Key{0, 0.0, 0.0, head};
+          key = Key{0, 0.0, 0.0, h.iid};
         } else if (h.bits & kBitForced) {
-          key = Key{0, -(double)im.depth[op], 0.0, head};
+          key = Key{0, -(double)im.depth[op], 0.0, h.iid};
         } else {
           double aff = 0.0;
           if (!affinity(op, E.kind[b0 + e], slacks(op), aff)) aff = 0.0;
-          key = Key{1, -aff, slack, head};
+          key = Key{1, -aff, slack, h.iid};
         }
         if (bop < 0 || key_lt(key, bkey)) {
           bkey = key;
@@ -796,14 +887,15 @@ struct Run {
     if (e == ri) OP(op, kOpiCompletedRef) += 1;
     observed[g] = 1;
     if (im.abl & kAblFb) return;
-    lat[g] = im.beta * obs + (1.0 - im.beta) * lat[g];
+    set_lat(g, im.beta * obs + (1.0 - im.beta) * lat(g));
     ++version;  // bump_profiles (configurator.py:463-468); _ref_latency reads lat[ref] live
+    if (e == ri) ++ref_version;
     if (e == ri && OP(op, kOpiCompletedRef) == im.dfp_count && !(im.abl & kAblDfp)) {
       const double init = E.lat_init[g];  // recalibrate_unobserved (configurator.py:470-491)
       if (init > 0.0) {
-        const double ratio = lat[g] / init;
+        const double ratio = lat(g) / init;
         for (int j = im.entry_off[op]; j < im.entry_off[op + 1]; ++j)
-          if (j != g && !observed[j]) lat[j] = E.lat_init[j] * ratio;
+          if (j != g && !observed[j]) set_lat(j, E.lat_init[j] * ratio);
         ++version;
       }
     }
@@ -826,19 +918,21 @@ struct Run {
         const int r = new_inv(v.op, u);
         if (r >= 0) speculate_fixed(r);
       }
-      return;
+    } else {
+      feedback(id, v.actual);
+      if (inv[u].bits & kBitResolved) {
+        v.state = kDuplicated;
+      } else {
+        inv[u].bits |= kBitResolved;
+        v.state = kCompleted;
+        if (v.actual <= v.com_slack) ++met;
+        ++completed;
+        last_accept = t;
+        spawn(id);
+      }
     }
-    feedback(id, v.actual);
-    if (inv[u].bits & kBitResolved) {
-      v.state = kDuplicated;
-      return;
-    }
-    inv[u].bits |= kBitResolved;
-    v.state = kCompleted;
-    if (v.actual <= v.com_slack) ++met;
-    ++completed;
-    last_accept = t;
-    spawn(id);
+    maybe_free(id);
+    if (u != id) maybe_free(u);
   }
   SPD_HDN void straggler(int id) {  // manager.py:499-511
     Inv& v = inv[id];
@@ -891,7 +985,11 @@ struct Run {
       const HeapEnt ev = pop();
       now = ev.t;
       if (ev.key >> 31) {
-        if (ev.payload > 0) straggler(ev.payload);
+        if (ev.payload > 0) {
+          inv[ev.payload].bits &= (uint8_t)~kBitWakePending;
+          straggler(ev.payload);
+          maybe_free(ev.payload);
+        }
       } else {
         finish(ev.payload, ev.t);
       }
@@ -903,7 +1001,8 @@ struct Run {
     o.latency = last_accept;
     o.cost = total_cost;
     o.now = now;
-    o.pad = 0.0;
+    o.peak_slots = peak_slots;
+    o.peak_heap = peak_heap;
     o.status = status;
     o.met = met;
     o.completed = completed;

@@ -22,7 +22,7 @@ namespace spdes {
 struct HostImage {
   Image im;
   std::vector<double> dcols;   // lat0, lat_init, res, batch, pool, price, base, per_item
-  std::vector<int32_t> icols;  // batch, kind, rank, cfg
+  std::vector<int32_t> icols;  // batch, kind, rank, cfg, then the path suffixes
   std::vector<int32_t> preds_of;  // scratch: per op sorted predecessors (CSR)
   std::vector<int32_t> pred_off;
   double cap_scale = 1.25;
@@ -42,6 +42,7 @@ SPD_HD Entries entries_view(const double* d, const int32_t* i, int n) {
   e.kind = i + n;
   e.rank = i + 2 * (size_t)n;
   e.cfg = i + 3 * (size_t)n;
+  e.suf = i + 4 * (size_t)n;
   return e;
 }
 
@@ -152,7 +153,6 @@ inline bool build_image(const sp_des_spec& s, HostImage& h, std::string& err) {
   const int nsuf = s.suffix_off[V];
   if (nsuf > kMaxSuffixInts) return err = "run engine: path suffixes exceed 2048 ints", false;
   for (int o = 0; o <= V; ++o) im.suf_off[o] = s.suffix_off[o];
-  for (int i = 0; i < nsuf; ++i) im.suf[i] = s.suffix_ops[i];
   for (int o = 0; o < V; ++o) {
     int cnt = 0;
     for (int p = s.suffix_off[o]; p < s.suffix_off[o + 1];) {
@@ -183,7 +183,8 @@ inline bool build_image(const sp_des_spec& s, HostImage& h, std::string& err) {
   im.inst_off[K] = inst;
   // entry columns
   h.dcols.assign(8 * (size_t)N, 0.0);
-  h.icols.assign(4 * (size_t)N, 0);
+  h.icols.assign(4 * (size_t)N + nsuf, 0);
+  for (int i = 0; i < nsuf; ++i) h.icols[4 * (size_t)N + i] = s.suffix_ops[i];
   for (int g = 0; g < N; ++g) {
     const int k = s.kind[g];
     if (k < 0 || k >= K) return err = "run engine: bad entry kind", false;
@@ -214,7 +215,7 @@ static inline int64_t align16(int64_t x) { return (x + 15) & ~(int64_t)15; }
 // Size one replica's arena for this call: item bounds per op = max over replicas of the items
 // the trace can push into the op's buffer (every predicate-passing edge, fan-out counts summed
 // over a join's in-edges), invocations <= items * cap_scale.
-inline bool plan_run(HostImage& h, int R, const int32_t* frame_off, const int32_t* attrs,
+inline bool plan_run(HostImage& h, int T, const int32_t* frame_off, const int32_t* attrs,
                      int draw_cap, int log_cap, std::string& err) {
   Image& im = h.im;
   const int V = im.n_ops;
@@ -230,7 +231,7 @@ inline bool plan_run(HostImage& h, int R, const int32_t* frame_off, const int32_
       for (int q = im.succ_off[order[i]]; q < im.succ_off[order[i] + 1]; ++q)
         if (--indeg[im.succ[q]] == 0) order.push_back(im.succ[q]);
   }
-  for (int r = 0; r < R; ++r) {
+  for (int r = 0; r < T; ++r) {  // per trace
     const int f0 = frame_off[r], f1 = frame_off[r + 1];
     if (f1 < f0) return err = "run engine: bad frame_off", false;
     frames_cap = std::max(frames_cap, f1 - f0);
@@ -260,15 +261,20 @@ inline bool plan_run(HostImage& h, int R, const int32_t* frame_off, const int32_
   }
   if (off > (int64_t)1 << 30) return err = "run engine: trace too large", false;
   im.buf_off[V] = (int32_t)off;
-  const int64_t inv_cap = (int64_t)((double)items * h.cap_scale) + 256;
+  // invocation slots are recycled (sp_des.cuh maybe_free): the live set is a fraction of the
+  // invocations a run forms (AMBER: <= 1k live of ~8k formed, 17.5k items); a replica that still
+  // runs out reports a capacity status and the host re-runs it with cap_scale doubled
+  const int64_t inv_cap = std::min<int64_t>((int64_t)((double)items * h.cap_scale) + 256,
+                                            (int64_t)((double)items * h.cap_scale / 4) + 1024);
   if (inv_cap > (int64_t)1 << 30) return err = "run engine: trace too large", false;
   im.inv_cap = (int32_t)inv_cap;
   im.seg_cap = (int32_t)(2 * inv_cap);
   int64_t res_total = 0;
   for (int k = 0; k < im.n_kinds; ++k)
     res_total += (int64_t)(im.inst_off[k + 1] - im.inst_off[k]) * im.inst_res[k];
-  im.heap_cap = (int32_t)(inv_cap + res_total + V + 16);
-  im.event_cap = 64 * inv_cap + 4096;
+  (void)res_total;
+  im.heap_cap = (int32_t)(2 * inv_cap + V + 64);  // completions + straggler wakes + hold wakes
+  im.event_cap = 64 * (int64_t)((double)items * h.cap_scale + 256) + 4096;  // runaway guard
   im.frames_cap = frames_cap;
   im.draw_cap = draw_cap;
   im.log_cap = log_cap;
@@ -279,7 +285,7 @@ inline bool plan_run(HostImage& h, int R, const int32_t* frame_off, const int32_
     o = align16(o + bytes);
     return at;
   };
-  im.o_lat = take(8 * (int64_t)N);
+  im.o_lat = take(24 * (int64_t)N);  // host harness only: lat / cost / costpen, ts = 1
   im.o_obs = take(N);
   im.o_inv = take((int64_t)sizeof(Inv) * (inv_cap + 1));
   im.o_next = take(4 * (inv_cap + 1));
@@ -292,11 +298,13 @@ inline bool plan_run(HostImage& h, int R, const int32_t* frame_off, const int32_
   im.o_wcnt = take(4 * 2 * (int64_t)std::max(im.w_off[K], 1));
   im.o_scver = take(4 * (int64_t)V);
   im.o_scval = take(8 * (int64_t)V * K);
-  im.o_holddl = take(8 * (int64_t)V);
+  im.o_holddl = take(8 * (int64_t)V * 4);  // hold deadlines, r_min, r_max, ratio versions
   im.o_free = take(4 * (int64_t)std::max(im.inst_off[K], 1));
   im.o_staging = take(4 * std::max<int64_t>((int64_t)frames_cap * im.staging_per_frame, 1));
   im.o_cfg = take(4 * (int64_t)((im.n_cfg + 31) / 32));
   im.o_opi = take(4 * (int64_t)V * kOpiN);
+  im.o_free_slot = take(4 * (inv_cap + 1));
+  im.o_free_seg = take(4 * (int64_t)im.seg_cap);
   im.arena_bytes = align16(o);
   return true;
 }

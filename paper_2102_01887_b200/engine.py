@@ -43,7 +43,8 @@ STATUS = {0: "ok", 1: "invocation capacity", 2: "event heap capacity", 3: "item-
           8: "weight capacity", 9: "item-buffer capacity", 10: "event cap"}
 _CAPACITY = (1, 2, 3, 7, 9)
 
-OUT_DTYPE = np.dtype([("latency", "<f8"), ("cost", "<f8"), ("now", "<f8"), ("pad", "<f8"),
+OUT_DTYPE = np.dtype([("latency", "<f8"), ("cost", "<f8"), ("now", "<f8"),
+                      ("peak_slots", "<i4"), ("peak_heap", "<i4"),
                       ("status", "<i4"), ("met", "<i4"), ("completed", "<i4"),
                       ("failures", "<i4"), ("duplicates", "<i4"), ("invocations", "<i4"),
                       ("terminal_items", "<i4"), ("n_speculate", "<i4"), ("n_commit", "<i4"),
@@ -417,23 +418,28 @@ class ReplicaEngine:
         except Exception:
             pass
 
-    def run(self, traces, targets, seeds=None, *, log_cap: int = 0, final_tables: bool = False,
-            encoded=None) -> list[RunResult]:
+    def run(self, traces, targets, seeds=None, *, trace_of=None, log_cap: int = 0,
+            final_tables: bool = False, encoded=None) -> list[RunResult]:
+        """Run one replica per target: replica i runs trace ``trace_of[i]`` (default: trace i)
+        of ``traces`` (or of ``encoded`` = encode_frames(traces)) with seed ``seeds[i]`` (default:
+        the scenario seed, manager.py:240)."""
         spec = self.spec
         R = len(targets)
         frame_off, attrs = encoded if encoded is not None else spec.encode_frames(traces)
+        T = len(frame_off) - 1
+        trace_of = (np.arange(R, dtype=np.int32) if trace_of is None
+                    else np.ascontiguousarray(trace_of, dtype=np.int32))
+        if len(trace_of) != R or (R and (trace_of.min() < 0 or trace_of.max() >= T)):
+            raise ValueError("trace_of must give every replica a trace")
         targets = np.ascontiguousarray(targets, dtype=np.float64)
         seeds = list(seeds) if seeds is not None else [spec.scenario.seed] * R
         results: list[RunResult | None] = [None] * R
         todo = np.arange(R)
         scale = self.cap_scale
         while len(todo):
-            fo = np.concatenate([[0], np.cumsum(np.diff(frame_off)[todo])]).astype(np.int32)
-            at = (np.concatenate([attrs[frame_off[r]:frame_off[r + 1]] for r in todo])
-                  if attrs.shape[1] else np.zeros((int(fo[-1]), 0), dtype=np.int32))
-            at = np.ascontiguousarray(at, dtype=np.int32)
-            out, lg, lat = self._launch(fo, at, targets[todo], [seeds[r] for r in todo], scale,
-                                        log_cap, final_tables)
+            out, lg, lat = self._launch(frame_off, attrs, np.ascontiguousarray(trace_of[todo]),
+                                        targets[todo], [seeds[r] for r in todo], scale, log_cap,
+                                        final_tables)
             retry = []
             for j, r in enumerate(todo):
                 st = int(out["status"][j])
@@ -460,7 +466,7 @@ class ReplicaEngine:
             scale *= 2
         return results  # type: ignore[return-value]
 
-    def _launch(self, frame_off, attrs, targets, seeds, scale, log_cap, final_tables):
+    def _launch(self, frame_off, attrs, trace_of, targets, seeds, scale, log_cap, final_tables):
         spec, lib, ctx = self.spec, self.lib, self.ctx
         R = len(targets)
         _lib.check(lib.sp_des_set_capacity(self.handle, float(scale)), "sp_des_set_capacity")
@@ -473,9 +479,10 @@ class ReplicaEngine:
         lg = np.zeros((R, log_cap), dtype=LOG_DTYPE) if log_cap else None
         lat = np.zeros((R, int(spec.entry_off[-1])), dtype=np.float64) if final_tables else None
         ptr = lambda x: x.ctypes.data if x is not None else None
-        _lib.check(lib.sp_des_run(ctx.handle, self.handle, R, frame_off.ctypes.data, ptr(attrs),
-                                  targets.ctypes.data, draw_cap, ptr(fac), ptr(bits), int(log_cap),
-                                  ptr(lg), ptr(lat), out.ctypes.data, _lib.SP_MEM_HOST), "sp_des_run")
+        _lib.check(lib.sp_des_run(ctx.handle, self.handle, R, len(frame_off) - 1, frame_off.ctypes.data,
+                                  ptr(attrs), trace_of.ctypes.data, targets.ctypes.data, draw_cap,
+                                  ptr(fac), ptr(bits), int(log_cap), ptr(lg), ptr(lat), out.ctypes.data,
+                                  _lib.SP_MEM_HOST), "sp_des_run")
         return out, lg, lat
 
     # ---- decision-log rows in the reference's tuple form (configurator.py:650-654, 746-749)

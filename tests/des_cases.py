@@ -167,7 +167,7 @@ def host_engine_factory(lib):
         def close(self):
             pass
 
-        def _launch(self, frame_off, attrs, targets, seeds, scale, log_cap, final_tables):
+        def _launch(self, frame_off, attrs, trace_of, targets, seeds, scale, log_cap, final_tables):
             spec = self.spec
             R = len(targets)
             draw_cap, fac, bits = 0, None, None
@@ -179,7 +179,8 @@ def host_engine_factory(lib):
             lat = np.zeros((R, int(spec.entry_off[-1]))) if final_tables else None
             ptr = lambda x: C.c_void_p(x.ctypes.data) if x is not None else None
             cs = spec.c_spec()
-            rc = lib.des_host_run(C.byref(cs), C.c_double(scale), R, ptr(frame_off), ptr(attrs),
+            rc = lib.des_host_run(C.byref(cs), C.c_double(scale), R, len(frame_off) - 1,
+                                  ptr(frame_off), ptr(attrs), ptr(trace_of),
                                   ptr(np.ascontiguousarray(targets, dtype=np.float64)), draw_cap,
                                   ptr(fac), ptr(bits), log_cap, ptr(lg), ptr(lat), ptr(out))
             if rc:

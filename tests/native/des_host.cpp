@@ -15,28 +15,30 @@ static std::string g_err;
 
 extern "C" const char* des_host_error() { return g_err.c_str(); }
 
-extern "C" int des_host_run(const sp_des_spec* spec, double cap_scale, int32_t R,
-                            const int32_t* frame_off, const int32_t* attrs, const double* target_s,
+extern "C" int des_host_run(const sp_des_spec* spec, double cap_scale, int32_t R, int32_t T,
+                            const int32_t* frame_off, const int32_t* attrs, const int32_t* trace_of,
+                            const double* target_s,
                             int32_t draw_cap, const double* draw_factor, const uint8_t* draw_bits,
                             int32_t log_cap, sp_des_log* log, double* lat_out, sp_des_out* out) {
   HostImage h;
   h.cap_scale = cap_scale;
   if (!build_image(*spec, h, g_err)) return -1;
-  if (!plan_run(h, R, frame_off, attrs, draw_cap, log_cap, g_err)) return -1;
+  if (!plan_run(h, T, frame_off, attrs, draw_cap, log_cap, g_err)) return -1;
   const Image& im = h.im;
   std::vector<char> arena((size_t)im.arena_bytes + 16);
   char* base = (char*)(((uintptr_t)arena.data() + 15) & ~(uintptr_t)15);
   const Entries E = entries_view(h.dcols.data(), h.icols.data(), im.n_entries);
   for (int r = 0; r < R; ++r) {
-    const int f0 = frame_off[r];
-    Run run(im, E, base, attrs + (int64_t)f0 * im.n_attrs, frame_off[r + 1] - f0, target_s[r],
+    const int tr = trace_of ? trace_of[r] : r;
+    const int f0 = frame_off[tr];
+    Run run(im, E, base, (double*)(base + im.o_lat), 1, attrs + (int64_t)f0 * im.n_attrs, frame_off[tr + 1] - f0, target_s[r],
             draw_factor ? draw_factor + (size_t)r * draw_cap : nullptr,
             draw_bits ? draw_bits + (size_t)r * draw_cap : nullptr,
             log ? reinterpret_cast<LogRec*>(log) + (size_t)r * log_cap : nullptr);
     run.run();
     run.write_out(*reinterpret_cast<Out*>(out + r));
     if (lat_out)
-      for (int i = 0; i < im.n_entries; ++i) lat_out[(size_t)r * im.n_entries + i] = run.lat[i];
+      for (int i = 0; i < im.n_entries; ++i) lat_out[(size_t)r * im.n_entries + i] = run.lat(i);
   }
   return 0;
 }
