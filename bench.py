@@ -443,7 +443,7 @@ def run_extras(args, line) -> None:
     import bench_workloads
 
     out = {}
-    for w in ("c1", "c3", "c4", "c5"):
+    for w in ("c1", "c3", "c4", "c5", "c4runs"):
         a = copy.copy(args)
         a.workload = w
         a.steps = min(args.steps, 10)
@@ -528,7 +528,8 @@ def main() -> None:
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-step-s", type=float, default=4.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5", "commit", "speculate"],
+    ap.add_argument("--workload", default="c2",
+                    choices=["c1", "c2", "c3", "c4", "c5", "commit", "speculate", "c4runs"],
                     help="c2 (default): BASELINE configs[1]; c3/c4/c5: bench_workloads.py")
     ap.add_argument("--c3-cpu-instances", type=int, default=1000)
     ap.add_argument("--c4-replicas", type=int, default=10000)

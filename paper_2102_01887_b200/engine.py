@@ -485,6 +485,27 @@ class ReplicaEngine:
                                   _lib.SP_MEM_HOST), "sp_des_run")
         return out, lg, lat
 
+    # ---- device-resident form (bench `value`): inputs already in HBM, stream-ordered, no sync
+    def prepare(self, frame_off: np.ndarray, attrs: np.ndarray, R: int, *, scale: float | None = None) -> int:
+        """Size the arenas for R replicas of these (host) traces; returns bytes per replica."""
+        _lib.check(self.lib.sp_des_set_capacity(self.handle, float(scale or self.cap_scale)),
+                   "sp_des_set_capacity")
+        fo = np.ascontiguousarray(frame_off, dtype=np.int32)
+        at = np.ascontiguousarray(attrs, dtype=np.int32)
+        _lib.check(self.lib.sp_des_prepare(self.ctx.handle, self.handle, int(R), len(fo) - 1,
+                                           fo.ctypes.data, at.ctypes.data, 0, 0), "sp_des_prepare")
+        return int(self.lib.sp_des_arena_bytes(self.handle))
+
+    def run_device(self, R: int, n_traces: int, frame_off_ptr: int, attrs_ptr: int, trace_of_ptr: int,
+                   targets_ptr: int, out_ptr: int) -> None:
+        """sp_des_run over device buffers (after ``prepare`` with the same traces); ``out_ptr``
+        receives R OUT_DTYPE rows.  Noise-free scenarios only (no draw streams)."""
+        if self.spec.draws:
+            raise ValueError("run_device: scenarios with RNG draws take the host-buffer form")
+        _lib.check(self.lib.sp_des_run(self.ctx.handle, self.handle, int(R), int(n_traces), frame_off_ptr,
+                                       attrs_ptr, trace_of_ptr, targets_ptr, 0, None, None, 0, None,
+                                       None, out_ptr, _lib.SP_MEM_DEVICE), "sp_des_run")
+
     # ---- decision-log rows in the reference's tuple form (configurator.py:650-654, 746-749)
     def log_rows(self, log: np.ndarray) -> list[tuple]:
         spec = self.spec
