@@ -336,12 +336,33 @@ def our_arm(args) -> None:
         step(args.warmup + i)
     p1.record(stream)
     torch.cuda.synchronize(dev)
+    launches_pi1 = ctx.launch_count - lp0
+    t_pi1 = p0.elapsed_time(p1) / 1e3
+    # the same, but after each table change the four alphas' plans are rebuilt together: one
+    # launch, one thread-block cluster per plan (sp_table_prepare_many), then the four decision
+    # launches of the sweep
+    def group(i):
+        if i % len(ALPHAS) == 0:
+            table.invalidate_plans()
+            table.prepare_many([alpha_of(args.warmup + j) for j in range(i, min(i + len(ALPHAS), args.steps))])
+        step(args.warmup + i)
+
+    for i in range(len(ALPHAS)):
+        group(i)
+    torch.cuda.synchronize(dev)
+    lp0 = ctx.launch_count
+    torch.cuda._sleep(int(2e6 + 4e5 * args.steps))
+    p0.record(stream)
+    for i in range(args.steps):
+        group(i)
+    p1.record(stream)
+    torch.cuda.synchronize(dev)
     launches_pi = ctx.launch_count - lp0
     t_pi = p0.elapsed_time(p1) / 1e3
     if world > 1:
-        tt = torch.tensor([t_pi], dtype=torch.float64, device=dev)
+        tt = torch.tensor([t_pi, t_pi1], dtype=torch.float64, device=dev)
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        t_pi = float(tt.item())
+        t_pi, t_pi1 = (float(x) for x in tt.tolist())
 
     # ---- the same steps, one at a time: L2 flushed before, an event pair around each ----
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
@@ -415,15 +436,22 @@ def our_arm(args) -> None:
                                "evals_per_s": N * M * world / (statistics.median(step_ms) / 1e3)},
         "plan": {"build_ms_per_alpha": plan_ms, "bytes": plan_bytes,
                  "note": "value / roofline: staircase plan built once per (profile version, alpha), "
-                         "table static in config 2; value_incl_plan: every step rebuilds its plan"},
+                         "table static in config 2; value_incl_plan: the table is invalidated before "
+                         "every sweep of the four alphas and each step decides with a freshly built "
+                         "plan (the sweep's four plans built by one launch); value_incl_plan_per_step: "
+                         "every single step invalidates the table and builds its own plan alone"},
         "value_incl_plan": evals / t_pi,
+        "value_incl_plan_per_step": {"value": evals / t_pi1, "ms_per_step": 1e3 * t_pi1 / args.steps,
+                                     "gpu_launches": launches_pi1,
+                                     "roofline_frac": alg_bytes / (t_pi1 / args.steps) / 1e9 / peaks["hbm_gbs"]},
         "roofline_incl_plan": {"bound": "hbm", "achieved": alg_bytes / (t_pi / args.steps) / 1e9,
                                "peak": peaks["hbm_gbs"], "unit": "GB/s",
                                "frac": alg_bytes / (t_pi / args.steps) / 1e9 / peaks["hbm_gbs"],
                                "ms_per_step": 1e3 * t_pi / args.steps,
                                "gpu_launches": launches_pi,
-                               "kernels": "k_plan_cluster (one 16-CTA cluster: the whole plan) + "
-                                          "the decision kernel, per step"},
+                               "kernels": "per sweep of 4 steps: k_plan_cluster_multi (four 16-CTA "
+                                          "clusters, one plan each) + k_pc_commit_order, then the 4 "
+                                          "decision launches"},
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

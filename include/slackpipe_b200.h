@@ -109,12 +109,17 @@ int sp_table_prepare(sp_ctx* ctx, sp_table* t, double alpha);
  * the next select / prepare rebuilds its plan (bench: plan-inclusive timing). */
 int sp_table_invalidate(sp_ctx* ctx, sp_table* t);
 /* 1 when the table's staircase plan is available (<= 16 distinct batch sizes, M < 32767). */
+/* Make the plans of n alphas current for the table's version (OpTable.scores' alpha,
+ * configurator.py:219-227): stale staircase plans are rebuilt together, up to four per launch
+ * (one thread-block cluster each) — e.g. the alphas a sweep decides with after one table change. */
+int sp_table_prepare_many(sp_ctx* ctx, sp_table* t, int32_t n, const double* alphas);
 int sp_table_plan_supported(const sp_table* t);
 /* Plan byte size for alpha after sp_table_prepare (synchronises); for DESIGN/bench. */
 int sp_table_plan_bytes(sp_ctx* ctx, sp_table* t, double alpha, int64_t* out_bytes);
 
 /* Diagnostic: (re)build the plan for alpha with builder 0 = the context's default, 1 = the
- * multi-kernel builder, 2 = the one-kernel cluster builder, and copy its byte image (total
+ * multi-kernel builder, 2 = the one-kernel cluster builder (3 = no rebuild: the current plan, e.g.
+ * one sp_table_prepare_many built), and copy its byte image (total
  * bytes in *out_bytes; copied when cap is large enough).  Tests compare the builders and the
  * CPU restatement oracle/plan.py section by section. */
 int sp_table_plan_image(sp_ctx* ctx, sp_table* t, double alpha, int32_t builder, void* out,

@@ -71,6 +71,7 @@ SIGNATURES = {
     "sp_table_get_latency": (C.c_int, [_p, _p, _p]),
     "sp_table_prepare": (C.c_int, [_p, _p, _d]),
     "sp_table_invalidate": (C.c_int, [_p, _p]),
+    "sp_table_prepare_many": (C.c_int, [_p, _p, _i32, _p]),
     "sp_table_plan_supported": (C.c_int, [_p]),
     "sp_table_plan_bytes": (C.c_int, [_p, _p, _d, C.POINTER(_i64)]),
     "sp_table_plan_image": (C.c_int, [_p, _p, _d, _i32, _p, _i64, C.POINTER(_i64)]),

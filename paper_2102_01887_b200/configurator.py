@@ -213,6 +213,12 @@ class OpTable:
     def prepare(self, alpha: float) -> None:
         check(self._ctx.lib.sp_table_prepare(self._ctx.handle, self._handle, float(alpha)))
 
+    def prepare_many(self, alphas) -> None:
+        """The plans of several alphas current for this table version: stale ones are rebuilt
+        together, up to four per launch (one thread-block cluster each)."""
+        a = np.ascontiguousarray(alphas, dtype=np.float64)
+        check(self._ctx.lib.sp_table_prepare_many(self._ctx.handle, self._handle, len(a), ptr(a)))
+
     def invalidate_plans(self) -> None:
         """Every plan of the table is rebuilt by its next use (as after a latency change)."""
         check(self._ctx.lib.sp_table_invalidate(self._ctx.handle, self._handle))
@@ -350,7 +356,7 @@ class OpTable:
 
 
 def _plan_image(ctx, handle, alpha: float, builder: str) -> bytes:
-    b = {"default": 0, "legacy": 1, "cluster": 2}[builder]
+    b = {"default": 0, "legacy": 1, "cluster": 2, "current": 3}[builder]
     n = C.c_int64()
     check(ctx.lib.sp_table_plan_image(ctx.handle, handle, float(alpha), b, None, 0, C.byref(n)),
           "sp_table_plan_image")
@@ -576,6 +582,13 @@ class _RawTable:
 
     def plan_image(self, alpha: float, builder: str = "default") -> bytes:
         return _plan_image(self._ctx, self._handle, alpha, builder)
+
+    def prepare_many(self, alphas) -> None:
+        a = np.ascontiguousarray(alphas, dtype=np.float64)
+        check(self._ctx.lib.sp_table_prepare_many(self._ctx.handle, self._handle, len(a), ptr(a)))
+
+    def invalidate_plans(self) -> None:
+        check(self._ctx.lib.sp_table_invalidate(self._ctx.handle, self._handle))
 
     def close(self) -> None:
         if getattr(self, "_handle", None):

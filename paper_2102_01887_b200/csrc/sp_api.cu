@@ -156,6 +156,12 @@ static void free_table(sp_table* t) {
   cudaFree(t->pc_seg);
   cudaFree(t->pc_seg_ent);
   cudaFree(t->pc_scratch);
+  for (int q = 0; q < 3; ++q) {
+    cudaFree(t->pc_multi_scratch[q]);
+    cudaFree(t->pc_multi_thr[q]);
+  }
+  cudaFree(t->pc_multi_status);
+  cudaFree(t->pc_multi_ord);
   cudaFree(t->dirty);
   for (auto& p : t->plans) plan_release(p);
   delete t;
@@ -472,6 +478,12 @@ int sp_table_prepare(sp_ctx* ctx, sp_table* t, double alpha) {
   return p ? SP_OK : rc;
 }
 
+int sp_table_prepare_many(sp_ctx* ctx, sp_table* t, int32_t n, const double* alphas) {
+  DeviceScope _dev_scope(ctx ? ctx->device : -1);
+  if (!ctx || !t || n < 0 || (n > 0 && !alphas)) return fail(SP_E_INVALID, "prepare_many: bad argument");
+  return plan_prepare_many(ctx, t, n, alphas);
+}
+
 int sp_table_plan_supported(const sp_table* t) { return t && t->plan_ok ? 1 : 0; }
 
 int sp_table_plan_bytes(sp_ctx* ctx, sp_table* t, double alpha, int64_t* out_bytes) {
@@ -496,20 +508,21 @@ int sp_table_plan_bytes(sp_ctx* ctx, sp_table* t, double alpha, int64_t* out_byt
 int sp_table_plan_image(sp_ctx* ctx, sp_table* t, double alpha, int32_t builder, void* out,
                         int64_t cap, int64_t* out_bytes) {
   DeviceScope _dev_scope(ctx ? ctx->device : -1);
-  if (!ctx || !t || !out_bytes || builder < 0 || builder > 2)
+  if (!ctx || !t || !out_bytes || builder < 0 || builder > 3)
     return fail(SP_E_INVALID, "plan_image: bad argument");
   if (!t->plan_ok) return fail(SP_E_UNSUPPORTED, "plan_image: the table has no staircase plan");
   if (builder == 2 && !t->pc_ok)
     return fail(SP_E_UNSUPPORTED, "plan_image: the table's shape is outside the cluster builder");
   const int saved = ctx->opt.plan_legacy;
-  if (builder != 0) ctx->opt.plan_legacy = builder == 1;
-  for (auto& p : t->plans)  // force a fresh build with the requested builder
-    if (p.alpha == alpha || (p.alpha != p.alpha && alpha != alpha)) p.valid = false;
+  if (builder == 1 || builder == 2) ctx->opt.plan_legacy = builder == 1;
+  if (builder != 3)  // force a fresh build with the requested builder (3: the current plan)
+    for (auto& p : t->plans)
+      if (p.alpha == alpha || (p.alpha != p.alpha && alpha != alpha)) p.valid = false;
   int rc = SP_OK;
   Plan* p = nullptr;
   for (auto& q : t->plans)
     if (q.alpha == alpha || (q.alpha != q.alpha && alpha != alpha)) p = &q;
-  if (p && p->graph) {  // a captured graph replays one builder only
+  if (p && p->graph && builder != 3) {  // a captured graph replays one builder only
     cudaGraphExecDestroy(p->graph);
     p->graph = nullptr;
     p->builds = 0;

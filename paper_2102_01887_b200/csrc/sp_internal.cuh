@@ -239,6 +239,13 @@ struct sp_table {
   void* pc_seg = nullptr;
   int32_t* pc_seg_ent = nullptr;
   void* pc_scratch = nullptr;
+  size_t pc_scratch_bytes = 0;
+  // multi-plan builds (plan_prepare_many): private scratch / thresholds of plans 1..3, the
+  // per-plan status words and the new cached order
+  void* pc_multi_scratch[3] = {};
+  double* pc_multi_thr[3] = {};
+  int32_t* pc_multi_status = nullptr;
+  int32_t* pc_multi_ord = nullptr;
   std::vector<sp::Plan> plans;
 };
 
@@ -332,6 +339,10 @@ namespace sp {
 int plan_build(sp_ctx* ctx, sp_table* t, Plan& p);
 int plan_scratch_alloc(sp_table* t);
 int plan_cluster_prepare(sp_table* t, const int32_t* kind, const int32_t* bidx);
+int plan_cluster_launch_multi(sp_ctx* ctx, sp_table* t, Plan* const* ps, int n, int W,
+                              const PlanHdr& hdr, int32_t* status, void* const* scratch,
+                              double* const* thr, int32_t* ord_new);
+int plan_prepare_many(sp_ctx* ctx, sp_table* t, int n, const double* alphas);
 int plan_cluster_launch(sp_ctx* ctx, sp_table* t, Plan& p, int W, const PlanHdr& hdr,
                         int32_t* status, PlanHdr* host_hdr, uint32_t* host_seq, uint32_t seq);
 Plan* plan_get(sp_ctx* ctx, sp_table* t, double alpha, int* rc);

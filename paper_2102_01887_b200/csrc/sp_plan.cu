@@ -1789,6 +1789,92 @@ Plan* plan_get(sp_ctx* ctx, sp_table* t, double alpha, int* rc) {
   return hit;
 }
 
+// Every listed alpha's plan current for the table version; stale staircase plans of the
+// cluster builder are rebuilt together, up to four per launch (one cluster each).
+int plan_prepare_many(sp_ctx* ctx, sp_table* t, int n, const double* alphas) {
+  const bool cluster = t->plan_ok && t->pc_ok && !ctx->opt.plan_legacy && t->finite_safe();
+  std::vector<Plan*> todo;
+  for (int i = 0; i < n; ++i) {
+    const double al = alphas[i];
+    int rc = SP_OK;
+    if (!cluster || !isfinite(al)) {
+      Plan* p = t->plan_ok && t->finite_safe() && isfinite(al) ? plan_get(ctx, t, al, &rc)
+                                                               : plan_costs(ctx, t, al, &rc);
+      if (!p) return rc;
+      continue;
+    }
+    plan_entry(ctx, t, al);  // creates the slot (may grow t->plans)
+  }
+  if (cluster) {  // pointers into t->plans only once it no longer grows
+    for (int i = 0; i < n; ++i) {
+      if (!isfinite(alphas[i])) continue;
+      Plan* p = plan_entry(ctx, t, alphas[i]);
+      if (p->valid && p->version == t->version) continue;
+      bool dup = false;
+      for (Plan* q : todo) dup |= q == p;
+      if (!dup) todo.push_back(p);
+    }
+  }
+  if (todo.size() == 1) {
+    int rc = SP_OK;
+    return plan_get(ctx, t, todo[0]->alpha, &rc) ? SP_OK : rc;
+  }
+  if (todo.empty()) return SP_OK;
+  const int M = t->M, K = t->K, W = plan_width(t);
+  if (!t->pc_multi_status) SP_CUDA(cudaMalloc(&t->pc_multi_status, sizeof(int32_t) * 8));
+  if (!t->pc_multi_ord) SP_CUDA(cudaMalloc(&t->pc_multi_ord, sizeof(int32_t) * M));
+  PlanHdr h;
+  memset(&h, 0, sizeof(h));
+  h.magic = kPlanMagic;
+  h.M = M;
+  h.nB = t->nB;
+  h.W = W;
+  h.K = K;
+  for (int b = 0; b < kMaxB; ++b) h.batch_vals[b] = b < t->nB ? t->batch_vals[b] : INT32_MAX;
+  for (size_t c0 = 0; c0 < todo.size(); c0 += 4) {
+    const int nq = (int)std::min<size_t>(4, todo.size() - c0);
+    void* scratch[4];
+    double* thr[4];
+    for (int q = 0; q < nq; ++q) {
+      Plan& p = *todo[c0 + q];
+      if (!p.cost) {
+        SP_CUDA(cudaMalloc(&p.cost, sizeof(double) * M));
+        SP_CUDA(cudaMalloc(&p.costpen, sizeof(double) * M));
+      }
+      if (!p.image) {
+        p.image_cap = plan_image_capacity(t, W);
+        SP_CUDA(cudaMalloc(&p.image, (size_t)p.image_cap));
+      }
+      SP_CUDA(plan_host_alloc(p));
+      if (q == 0) {
+        scratch[q] = t->pc_scratch;
+        thr[q] = t->thrscratch;
+      } else {
+        if (!t->pc_multi_scratch[q - 1]) {
+          SP_CUDA(cudaMalloc(&t->pc_multi_scratch[q - 1], t->pc_scratch_bytes));
+          SP_CUDA(cudaMalloc(&t->pc_multi_thr[q - 1], sizeof(double) * (M + K)));
+        }
+        scratch[q] = t->pc_multi_scratch[q - 1];
+        thr[q] = t->pc_multi_thr[q - 1];
+      }
+    }
+    const int rc = plan_cluster_launch_multi(ctx, t, todo.data() + c0, nq, W, h, t->pc_multi_status,
+                                             scratch, thr, t->pc_multi_ord);
+    if (rc != SP_OK) return rc;
+    for (int q = 0; q < nq; ++q) {
+      Plan& p = *todo[c0 + q];
+      p.hdr_mapped = true;
+      p.hdr_pending = true;
+      p.hdr_valid = false;
+      p.valid = true;
+      p.version = t->version;
+      p.cost_version = t->version;
+    }
+    ctx->plan_dirty = true;
+  }
+  return SP_OK;
+}
+
 bool plan_ready(sp_table* t, double alpha) {
   for (auto& p : t->plans)
     if (p.alpha == alpha || (p.alpha != p.alpha && alpha != alpha))

@@ -72,6 +72,11 @@ __device__ __forceinline__ uint32_t cluster_rank() {
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
   return r;
 }
+__device__ __forceinline__ uint32_t cluster_size() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
 
 __device__ __forceinline__ int pow2ceil(int n) {
   int p = 1;
@@ -339,6 +344,12 @@ struct PcArgs {
   uint32_t* host_seq;             // written after host_hdr (system fence): the build's seq
   uint32_t seq;
   int debug;
+  // several plans of one table built by one launch (one cluster per plan, k_plan_cluster_multi):
+  // no cluster writes the table's cached order / dirty flags / stale word, which the others are
+  // still reading; the first plan's cluster writes the new order to ord_out and a follow-up
+  // kernel (k_pc_commit_order) installs it
+  int multi;
+  int32_t* ord_out;
 };
 
 __device__ __forceinline__ uint64_t gtimer() {
@@ -594,7 +605,9 @@ __device__ void pc_segment(const PcArgs& a, const PcShared& S, int s, uint8_t* s
     // 2. position arrays from the staged attributes; the cached order and the dirty flags
     if (t < n) {
       const int src = (int)(val[0] & 2047u), e = (int)(val[0] >> 11);
-      if (moved) {
+      if (a.multi) {
+        if (a.ord_out) a.ord_out[off + t] = e;
+      } else if (moved) {
         a.ord[off + t] = e;
         a.dirty[e] = 0;
       }
@@ -639,13 +652,22 @@ __device__ void pc_segment(const PcArgs& a, const PcShared& S, int s, uint8_t* s
   }
   if (__syncthreads_or(bad)) {
     reg_bitonic<E>(key, val, N2, sk, sv);
+    if (!a.multi) {
+#pragma unroll
+      for (int q = 0; q < E; ++q) {
+        const int i = t + q * T;
+        if (i < n) {
+          a.ord[off + i] = (int32_t)val[q];
+          a.dirty[val[q]] = 0;
+        }
+      }
+    }
+  }
+  if (a.multi && a.ord_out) {
 #pragma unroll
     for (int q = 0; q < E; ++q) {
       const int i = t + q * T;
-      if (i < n) {
-        a.ord[off + i] = (int32_t)val[q];
-        a.dirty[val[q]] = 0;
-      }
+      if (i < n) a.ord_out[off + i] = (int32_t)val[q];
     }
   }
   PC_STAMP(2);
@@ -1302,7 +1324,7 @@ __device__ __forceinline__ int last_le(const int* off, int n, int g) {  // last 
 __device__ bool pc_fast_phase2(const PcArgs& a, const PcShared& S, FastLists& fl, uint8_t* smem,
                                int* s_w) {
   const int T = blockDim.x, t = threadIdx.x;
-  const int C = (int)gridDim.x, c = (int)cluster_rank();
+  const int C = (int)cluster_size(), c = (int)cluster_rank();
   const int nl = 2 * a.nseg;
   {
     const int lc = t < nl ? S.cnt[4 * (t >> 1) + 2 + (t & 1)] : 0;
@@ -1815,13 +1837,13 @@ __device__ void pc_write_kind(const PcArgs& a, const PcShared& S, const PlanHdr&
 }
 
 template <int ES>
-__global__ void __launch_bounds__(kPcThreads, 1) k_plan_cluster(const __grid_constant__ PcArgs a) {
+__device__ __forceinline__ void pc_build(const PcArgs& a) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ int s_w[64];
   __shared__ PlanHdr s_hdr;
   __shared__ KindStage s_ks;
   __shared__ PcShared S;
-  const int C = (int)gridDim.x;  // one cluster
+  const int C = (int)cluster_size();
   const int c = (int)cluster_rank();
   uint64_t tm[6];
   tm[0] = gtimer();
@@ -1838,7 +1860,7 @@ __global__ void __launch_bounds__(kPcThreads, 1) k_plan_cluster(const __grid_con
   for (int s = c; s < a.nseg; s += C) pc_segment<ES>(a, S, s, smem, s_w);
   tm[2] = gtimer();
   cluster_barrier();
-  if (c == 0 && threadIdx.x == 0) *a.order_stale = 0;  // every CTA has read it
+  if (c == 0 && threadIdx.x == 0 && !a.multi) *a.order_stale = 0;  // every CTA has read it
   tm[3] = gtimer();
   for (int i = threadIdx.x; i < 4 * a.nseg; i += blockDim.x) S.cnt[i] = a.seg_cnt[i];
   __syncthreads();
@@ -1985,6 +2007,33 @@ __global__ void __launch_bounds__(kPcThreads, 1) k_plan_cluster(const __grid_con
            (unsigned long long)(tm[5] - tm[4]));
 }
 
+template <int ES>
+__global__ void __launch_bounds__(kPcThreads, 1) k_plan_cluster(const __grid_constant__ PcArgs a) {
+  pc_build<ES>(a);
+}
+
+constexpr int kPcMaxMulti = 4;
+struct PcMulti {
+  PcArgs a[kPcMaxMulti];
+};
+
+// one cluster per plan: cluster q builds plan q (same table, its own alpha, scratch and image)
+template <int ES>
+__global__ void __launch_bounds__(kPcThreads, 1) k_plan_cluster_multi(const __grid_constant__ PcMulti m) {
+  pc_build<ES>(m.a[blockIdx.x / cluster_size()]);
+}
+
+// after a multi-plan build: the new cached order, no entry dirty, the order no longer stale
+__global__ void k_pc_commit_order(int M, const int32_t* __restrict__ ord_new, int32_t* __restrict__ ord,
+                                  uint8_t* __restrict__ dirty, int32_t* __restrict__ order_stale) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < M) {
+    ord[i] = ord_new[i];
+    dirty[i] = 0;
+  }
+  if (i == 0) *order_stale = 0;
+}
+
 }  // namespace
 
 int plan_cluster_supported(const sp_table* t) { return t->pc_ok ? 1 : 0; }
@@ -2024,16 +2073,19 @@ int plan_cluster_prepare(sp_table* t, const int32_t* kind, const int32_t* bidx) 
   const size_t bytes = (size_t)M * (2 * 8 + 6 * 4 + 2 * (8 * 4 + 4 * 2)) + 16u * segs.size() + 128 +
                        48u * M + 4 * sizeof(double) * n2 + sizeof(int32_t) * n2 + 64 * 16;
   SP_CUDA(cudaMalloc(&t->pc_scratch, bytes));
+  t->pc_scratch_bytes = bytes;
   t->pc_ok = true;
   return SP_OK;
 }
 
-int plan_cluster_launch(sp_ctx* ctx, sp_table* t, Plan& p, int W, const PlanHdr& hdr,
-                        int32_t* status, PlanHdr* host_hdr, uint32_t* host_seq, uint32_t seq) {
+// The cluster builder's arguments for plan p of table t; `scratch` / `thr` are the plan's
+// private scratch (the table's own for a single build).
+static void pc_fill_args(sp_ctx* ctx, sp_table* t, Plan& p, int W, const PlanHdr& hdr,
+                         int32_t* status, PlanHdr* host_hdr, uint32_t* host_seq, uint32_t seq,
+                         void* scratch, double* thr, PcArgs& a) {
   const int M = t->M;
   int n2 = 1;
   while (n2 < 2 * M) n2 <<= 1;
-  PcArgs a;
   a.M = M;
   a.K = t->K;
   a.nB = t->nB;
@@ -2056,7 +2108,7 @@ int plan_cluster_launch(sp_ctx* ctx, sp_table* t, Plan& p, int W, const PlanHdr&
   a.image = p.image;
   a.image_cap = p.image_cap;
   a.status = status;
-  uint8_t* q = reinterpret_cast<uint8_t*>(t->pc_scratch);
+  uint8_t* q = reinterpret_cast<uint8_t*>(scratch);
   auto take = [&](size_t b) {
     uint8_t* r = q;
     q += (b + 15) & ~(size_t)15;
@@ -2087,7 +2139,7 @@ int plan_cluster_launch(sp_ctx* ctx, sp_table* t, Plan& p, int W, const PlanHdr&
   a.crec = reinterpret_cast<double*>(take(3 * 8u * 2 * M));
   a.gkey = reinterpret_cast<double*>(take(4 * sizeof(double) * n2));
   a.gix = reinterpret_cast<int32_t*>(take(4u * n2));
-  a.thr = t->thrscratch;
+  a.thr = thr;
   for (int k = 0; k < kMaxKinds; ++k) {
     a.base[k] = k < t->K ? t->kind_base[k] : 0;
     a.count[k] = k < t->K ? t->kind_count[k] : 0;
@@ -2098,12 +2150,24 @@ int plan_cluster_launch(sp_ctx* ctx, sp_table* t, Plan& p, int W, const PlanHdr&
   a.host_seq = host_seq;
   a.seq = seq;
   a.debug = ctx->opt.pc_debug;
+  a.multi = 0;
+  a.ord_out = nullptr;
+}
+
+static size_t pc_smem_bytes(const sp_table* t) {
   // shared memory: the largest phase (segment: 60 B per slot; candidates 16 B; thresholds 8 B
   // per record in the shared-memory fallback; rows 64 KB)
   const int es = t->pc_max_seg > 2 * kPcThreads ? 4 : (t->pc_max_seg > kPcThreads ? 2 : 1);
-  const size_t smem = std::max(std::max((size_t)es * kPcThreads * 60, (size_t)2 * kPcThreads * 36),
-                               std::max(std::max((size_t)2 * kPcMaxKind * 8, (size_t)kSmEnd),
-                                        (size_t)kFEnd));
+  return std::max(std::max((size_t)es * kPcThreads * 60, (size_t)2 * kPcThreads * 36),
+                  std::max(std::max((size_t)2 * kPcMaxKind * 8, (size_t)kSmEnd), (size_t)kFEnd));
+}
+
+int plan_cluster_launch(sp_ctx* ctx, sp_table* t, Plan& p, int W, const PlanHdr& hdr,
+                        int32_t* status, PlanHdr* host_hdr, uint32_t* host_seq, uint32_t seq) {
+  PcArgs a;
+  pc_fill_args(ctx, t, p, W, hdr, status, host_hdr, host_seq, seq, t->pc_scratch, t->thrscratch, a);
+  const int es = t->pc_max_seg > 2 * kPcThreads ? 4 : (t->pc_max_seg > kPcThreads ? 2 : 1);
+  const size_t smem = pc_smem_bytes(t);
   auto kern = es == 1 ? k_plan_cluster<1> : (es == 2 ? k_plan_cluster<2> : k_plan_cluster<4>);
   static uint64_t attr[3] = {0, 0, 0};
   static int csize[64] = {};
@@ -2147,6 +2211,84 @@ int plan_cluster_launch(sp_ctx* ctx, sp_table* t, Plan& p, int W, const PlanHdr&
   cfg.attrs = at;
   cfg.numAttrs = 2;
   SP_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
+  SP_CHECK_LAUNCH(ctx);
+  return SP_OK;
+}
+
+}  // namespace sp
+
+namespace sp {
+
+// Several plans of one table (e.g. the alphas a workload sweeps) in ONE launch: one cluster per
+// plan, each with its own scratch, threshold area, image and host header; the table's cached
+// order is read by every cluster and replaced afterwards by k_pc_commit_order.  Every image is
+// byte-identical to the plan's single build (tests/test_gpu_plan.py).
+int plan_cluster_launch_multi(sp_ctx* ctx, sp_table* t, Plan* const* ps, int n, int W,
+                              const PlanHdr& hdr, int32_t* status, void* const* scratch,
+                              double* const* thr, int32_t* ord_new) {
+  if (n < 1 || n > kPcMaxMulti) return fail(SP_E_INVALID, "plan multi: 1..4 plans");
+  PcMulti m;
+  for (int q = 0; q < n; ++q) {
+    Plan& p = *ps[q];
+    void* dh = nullptr;
+    SP_CUDA(cudaHostGetDevicePointer(&dh, p.host_hdr, 0));
+    ++p.seq;
+    pc_fill_args(ctx, t, p, W, hdr, status + q, static_cast<PlanHdr*>(dh),
+                 reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(dh) + sizeof(PlanHdr)), p.seq,
+                 scratch[q], thr[q], m.a[q]);
+    m.a[q].multi = 1;
+    m.a[q].ord_out = q == 0 ? ord_new : nullptr;
+  }
+  for (int q = n; q < kPcMaxMulti; ++q) m.a[q] = m.a[0];
+  const int es = t->pc_max_seg > 2 * kPcThreads ? 4 : (t->pc_max_seg > kPcThreads ? 2 : 1);
+  const size_t smem = pc_smem_bytes(t);
+  auto kern = es == 1 ? k_plan_cluster_multi<1>
+                      : (es == 2 ? k_plan_cluster_multi<2> : k_plan_cluster_multi<4>);
+  static uint64_t attr[3] = {0, 0, 0};
+  static int csize[64] = {};
+  const int dev = cur_device();
+  if (attr_once(attr[es == 4 ? 2 : es - 1])) {
+    SP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    SP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  }
+  if (csize[dev] == 0) {  // 16-CTA clusters when n of them fit at once, else 8
+    cudaLaunchConfig_t q = {};
+    q.gridDim = dim3(16 * n);
+    q.blockDim = dim3(kPcThreads);
+    q.dynamicSmemBytes = smem;
+    cudaLaunchAttribute qa[1];
+    qa[0].id = cudaLaunchAttributeClusterDimension;
+    qa[0].val.clusterDim.x = 16;
+    qa[0].val.clusterDim.y = 1;
+    qa[0].val.clusterDim.z = 1;
+    q.attrs = qa;
+    q.numAttrs = 1;
+    int c = 0;
+    if (cudaOccupancyMaxActiveClusters(&c, (const void*)kern, &q) != cudaSuccess || c < 1) {
+      cudaGetLastError();
+      c = 0;
+    }
+    csize[dev] = c >= kPcMaxMulti ? 16 : kPcCluster;
+  }
+  const int C = csize[dev];
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(C * n);
+  cfg.blockDim = dim3(kPcThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = C;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = ctx->opt.no_pdl ? 0 : 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  SP_CUDA(cudaLaunchKernelEx(&cfg, kern, m));
+  SP_CHECK_LAUNCH(ctx);
+  k_pc_commit_order<<<(t->M + 255) / 256, 256, 0, ctx->stream>>>(t->M, ord_new, t->pc_seg_ent,
+                                                                  t->dirty, t->dev_counters + 4);
   SP_CHECK_LAUNCH(ctx);
   return SP_OK;
 }

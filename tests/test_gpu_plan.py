@@ -112,3 +112,52 @@ def test_cluster_plan_incremental_updates(gpu_ctx, seed, M, nB, K, nonpos):
         for alpha in (7.5,) if step % 2 else (0.0, 1000.0):
             _check(tab, K, alpha, arrays())
     tab.close()
+
+
+@pytest.mark.parametrize("seed,M,nB,K,nonpos", [(21, 4096, 8, 2, False), (22, 1500, 16, 3, True),
+                                                (23, 3000, 8, 4, False)])
+def test_multi_plan_build(gpu_ctx, seed, M, nB, K, nonpos):
+    """sp_table_prepare_many: the plans of several alphas built by ONE launch (one cluster per
+    plan, the table's cached order replaced afterwards) — every image equal to the CPU
+    restatement, after from-scratch invalidations and after incremental latency changes, and the
+    decisions taken with them equal to the oracle's."""
+    import paper_2102_01887_b200 as sp
+    from oracle import cselect
+
+    rng = np.random.default_rng(seed)
+    t = _random_table(rng, M, nB, K, nonpos)
+    tab = raw_table(t, K)
+    lat = t.lat.copy()
+    alphas = [0.0, 1.0, 100.0, 1000.0]
+    for step in range(5):
+        if step == 0:
+            tab.invalidate_plans()
+        else:
+            ix = rng.choice(M, size=int(rng.integers(1, 300)), replace=False).astype(np.int32)
+            v = rng.uniform(0.01, 5.0, size=len(ix))
+            tie = rng.random(len(ix)) < 0.3
+            v[tie] = rng.choice(lat, size=int(tie.sum()))  # exact ties with other entries
+            tab.set_latency(ix, v)
+            lat[ix] = v
+        tab.prepare_many(alphas[: 2 + step % 3])
+        for al in alphas[: 2 + step % 3]:
+            img = plan.parse_image(tab.plan_image(al, "current"))
+            exp = plan.plan_image(lat, t.res, t.batch_int, t.pool, t.price, t.gkind, t.id_rank, K, al)
+            assert plan.compare(img, exp) == [], (step, al, plan.compare(img, exp))
+    # decisions on the multi-built plans
+    tab.invalidate_plans()
+    tab.prepare_many(alphas)
+    ot = optable.from_columns(lat=lat, res=t.res, batch=t.batch, pool=t.pool, price=t.price,
+                              gkind=t.gkind, id_rank=t.id_rank, n_kinds=K)
+    N = 2048
+    slack = rng.uniform(-2, 10, size=(N, K))
+    avail = rng.integers(1, 129, size=N).astype(np.int32)
+    supply = rng.integers(0, 257, size=N).astype(np.int32)
+    mb = np.ones(N, np.int32)
+    flags = sp.make_flags(rng.random(N) < 0.5, 0)
+    for al in alphas:
+        got = sp.select_batch([tab], slack, al, avail, upstream_supply=supply, min_batch=mb,
+                              flags=flags, mode="plan")
+        exp = cselect.select_batch([ot], slack, al, avail, supply, mb, flags)
+        assert np.array_equal(got["idx"], exp["idx"]), al
+        assert np.array_equal(got["code"] & 3, exp["code"]), al
