@@ -655,9 +655,11 @@ def run_c5(args):
             f_idx, f_obs = gather_observations(obs_idx, obs_val, B)
             si.copy_(f_idx)
             so.copy_(f_obs)
-        else:  # the records land straight in the run's observation stream
-            sp.simulate_observations(out, base, nz, truth_per_item=per_item, out=(si, so))
-        sp.fold_observations([tab], None, si, so, beta=0.5, dfp_count=10, sync_host=False)
+            sp.fold_observations([tab], None, si, so, beta=0.5, dfp_count=10, sync_host=False)
+        else:  # one kernel: the observations evaluated in the fold's load phase; the records
+            # still land in the run's observation stream
+            sp.simulate_and_fold(tab, out, base, nz, truth_per_item=per_item, out=(si, so), beta=0.5,
+                                 dfp_count=10)
 
     # warm-up on a throw-away copy of the table (module loading, scratch allocation, plan-build
     # graph capture); the timed run starts from the untouched table

@@ -306,6 +306,14 @@ int sp_simulate_observations(sp_ctx* ctx, int32_t N, const int32_t* code, const 
                              const int32_t* fill, const double* truth_base,
                              const double* truth_per_item, const double* noise, int32_t* obs_idx,
                              double* obs);
+/* sp_simulate_observations + sp_feedback_fold of one table in ONE cooperative kernel (device
+ * buffers, stream-ordered): the fold's load phase evaluates each decision's observation itself
+ * (same law, same bits) and also writes the records to rec_idx / rec_obs. */
+int sp_simulate_and_fold(sp_ctx* ctx, sp_table* t, int32_t N, const int32_t* code,
+                         const int32_t* idx, const int32_t* fill, const double* truth_base,
+                         const double* truth_per_item, const double* noise, double beta,
+                         int32_t dfp_count, int32_t dfp_on, int32_t fb_frozen, int32_t* rec_idx,
+                         double* rec_obs);
 
 /* ---- profile generation (replaces profiler.py:35-85
  *      profile_operation's latency loop over pipeline.py:454-475 enumerate_configs) --------- */

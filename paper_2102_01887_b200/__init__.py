@@ -28,7 +28,7 @@ from .configurator import (
 from . import metadata
 from .commit import commit_candidates, commit_round, pump_commits
 from .group import DeviceGroup, GroupOpTable, group_fold, group_select_batch
-from .feedback import apply_feedback, fold_observations, observation_quantiles, set_table_counters, simulate_observations, table_counters
+from .feedback import apply_feedback, fold_observations, observation_quantiles, set_table_counters, simulate_and_fold, simulate_observations, table_counters
 from .pipeline import (ConfigAssignment, ConfigEntry, ConfigSpec, Knob, KnobTemplate, OperationSpec, PipelineDag,
                        enumerate_configs, reference_config)
 from .profiler import profile_operation
@@ -45,7 +45,7 @@ __all__ = [
     "SlackpipeError", "TuningParams", "affinity", "affinity_from_minima", "apply_feedback",
     "commit_candidates", "commit_round", "compute_slack", "estimate_queueing", "fold_observations", "get_context", "load_library",
     "make_flags", "metadata", "objective", "pump_commits", "observation_quantiles", "reference_config", "remaining_path_latency", "select_batch",
-    "select_config", "set_table_counters", "simulate_observations", "speculate_batch", "speculate_from_buffer",
+    "select_config", "set_table_counters", "simulate_and_fold", "simulate_observations", "speculate_batch", "speculate_from_buffer",
     "table_counters", "ConfigAssignment", "Knob", "KnobTemplate", "OperationSpec", "enumerate_configs",
     "profile_operation", "GroundTruthModel", "OpKindTruth",
 ]

@@ -96,6 +96,7 @@ SIGNATURES = {
     "sp_profile_configs": (C.c_int, [_p, _i32, _p, _p, _p, _p, _p, _p, _p, _i32, _p, _i32, _p, _p,
                                      _i32, _p, _p, _i64, _p, _p, _p, _p]),
     "sp_pow_correctly_rounded": (C.c_int, [_p, _i32, _p, _p, _p]),
+    "sp_simulate_and_fold": (C.c_int, [_p, _p, _i32, _p, _p, _p, _p, _p, _p, _d, _i32, _i32, _i32, _p, _p]),
     "sp_des_create": (C.c_int, [_p, _p, _pp]),
     "sp_des_destroy": (C.c_int, [_p, _p]),
     "sp_des_prepare": (C.c_int, [_p, _p, _i32, _i32, _p, _p, _i32, _i32]),

@@ -64,3 +64,19 @@ extern "C" int sp_simulate_observations(sp_ctx* ctx, int32_t N, const int32_t* c
   SP_CHECK_LAUNCH(ctx);
   return SP_OK;
 }
+
+extern "C" int sp_simulate_and_fold(sp_ctx* ctx, sp_table* t, int32_t N, const int32_t* code,
+                                    const int32_t* idx, const int32_t* fill,
+                                    const double* truth_base, const double* truth_per_item,
+                                    const double* noise, double beta, int32_t dfp_count,
+                                    int32_t dfp_on, int32_t fb_frozen, int32_t* rec_idx,
+                                    double* rec_obs) {
+  DeviceScope _dev_scope(ctx ? ctx->device : -1);
+  if (!ctx || !t || N < 0 || (N > 0 && (!code || !idx || !truth_base || !noise || !rec_idx || !rec_obs)))
+    return fail(SP_E_INVALID, "simulate_and_fold: bad argument");
+  if (truth_per_item && !fill)
+    return fail(SP_E_INVALID, "simulate_and_fold: fill is required with per-item truth");
+  if (!(beta > 0.0 && beta <= 1.0)) return fail(SP_E_INVALID, "smoothing_beta must be in (0, 1]");
+  return simulate_and_fold(ctx, t, N, code, idx, fill, truth_base, truth_per_item, noise, beta,
+                           dfp_count, dfp_on, fb_frozen, rec_idx, rec_obs);
+}

@@ -523,7 +523,26 @@ struct CoopArgs {
   Gate* gates;      // per table
   CoopState* st;
   int debug;        // SP_PC_DEBUG: per-phase timestamps of CTA 0 (printf)
+  // simulated backend fused into the load (sp_simulate_and_fold): record j is decision j —
+  // an assignment runs and yields (base[idx] + per_item[idx] * fill) * noise (backend.py:52-54),
+  // anything else yields no observation; the records are also written to rec_idx / rec_obs
+  const int32_t *d_code, *d_idx, *d_fill;
+  const double *t_base, *t_per_item, *t_noise;
+  int32_t* rec_idx;
+  double* rec_obs;
 };
+
+__device__ __forceinline__ int coop_entry(const CoopArgs& a, int j) {
+  if (!a.d_code) return a.idx[j];
+  return (a.d_code[j] & 3) == SP_DEC_ASSIGN ? a.d_idx[j] : -1;
+}
+__device__ __forceinline__ double coop_obs(const CoopArgs& a, int j) {
+  if (!a.d_code) return a.obs[j];
+  const int e = a.d_idx[j];  // only called for records that run
+  double lat = a.t_base[e];
+  if (a.t_per_item) lat = __dadd_rn(lat, __dmul_rn(a.t_per_item[e], (double)a.d_fill[j]));
+  return __dmul_rn(lat, a.t_noise[j]);
+}
 
 __device__ __forceinline__ uint64_t coop_timer() {
   uint64_t t;
@@ -857,8 +876,12 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_fold_coop(const __grid_cons
       const int j = c0 + tl * kCoopTile + (int)threadIdx.x;
       uint32_t key[1] = {sent}, val[1] = {(uint32_t)j};
       if (j < a.n) {
-        const int e = a.idx[j];
+        const int e = coop_entry(a, j);
         if (e >= 0) key[0] = (uint32_t)(a.ft.t[a.op ? a.op[j] : 0].gbase + e);
+        if (a.rec_idx) {
+          a.rec_idx[j] = e;
+          a.rec_obs[j] = e >= 0 ? coop_obs(a, j) : 0.0;
+        }
       }
       __syncthreads();  // tmp / s_key reuse across tiles
       if (chunk == 0) tm[1] = coop_timer();
@@ -868,7 +891,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_fold_coop(const __grid_cons
       const uint32_t k = key[0];
       s_key[threadIdx.x] = k;
       const int q = tl * kCoopTile + (int)threadIdx.x;  // chunk-array index
-      const double o = k != sent ? a.obs[val[0]] : 0.0;
+      const double o = k != sent ? coop_obs(a, (int)val[0]) : 0.0;
       a.skey[q] = k;
       a.spos[q] = val[0];
       a.sobs[q] = o;
@@ -1070,8 +1093,16 @@ static int coop_buffers(sp_ctx* ctx, int64_t keys, CoopArgs& a) {
 
 static int fold_launch_coop(sp_ctx* ctx, int n_tables, sp_table* const* tables, int n,
                             const int32_t* op, const int32_t* idx, const double* obs, double beta,
-                            int dfp_count, int dfp_on, int fb_frozen) {
+                            int dfp_count, int dfp_on, int fb_frozen, const CoopArgs* sim = nullptr) {
   CoopArgs a;
+  a.d_code = sim ? sim->d_code : nullptr;
+  a.d_idx = sim ? sim->d_idx : nullptr;
+  a.d_fill = sim ? sim->d_fill : nullptr;
+  a.t_base = sim ? sim->t_base : nullptr;
+  a.t_per_item = sim ? sim->t_per_item : nullptr;
+  a.t_noise = sim ? sim->t_noise : nullptr;
+  a.rec_idx = sim ? sim->rec_idx : nullptr;
+  a.rec_obs = sim ? sim->rec_obs : nullptr;
   a.ft.n = n_tables;
   int64_t gb = 0;
   for (int t = 0; t < n_tables; ++t) {
@@ -1148,6 +1179,32 @@ int fold_launch(sp_ctx* ctx, int n_tables, sp_table* const* tables, int n, const
                             fb_frozen);
   if (rc == SP_OK)
     for (int t = 0; t < n_tables; ++t) tables[t]->version++;
+  return rc;
+}
+
+int simulate_and_fold(sp_ctx* ctx, sp_table* t, int n, const int32_t* code, const int32_t* idx,
+                      const int32_t* fill, const double* base, const double* per_item,
+                      const double* noise, double beta, int dfp_count, int dfp_on, int fb_frozen,
+                      int32_t* rec_idx, double* rec_obs) {
+  if (ctx->opt.fold_legacy || n == 0 || !rec_idx) {  // the two-kernel form
+    if (!rec_idx) return fail(SP_E_INVALID, "simulate_and_fold: record buffers required");
+    const int rc = sp_simulate_observations(ctx, n, code, idx, fill, base, per_item, noise, rec_idx,
+                                            rec_obs);
+    if (rc != SP_OK) return rc;
+    return fold_launch(ctx, 1, &t, n, nullptr, rec_idx, rec_obs, beta, dfp_count, dfp_on, fb_frozen);
+  }
+  CoopArgs sim;
+  sim.d_code = code;
+  sim.d_idx = idx;
+  sim.d_fill = fill;
+  sim.t_base = base;
+  sim.t_per_item = per_item;
+  sim.t_noise = noise;
+  sim.rec_idx = rec_idx;
+  sim.rec_obs = rec_obs;
+  const int rc = fold_launch_coop(ctx, 1, &t, n, nullptr, nullptr, nullptr, beta, dfp_count, dfp_on,
+                                  fb_frozen, &sim);
+  if (rc == SP_OK) t->version++;
   return rc;
 }
 

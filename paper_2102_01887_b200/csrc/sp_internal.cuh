@@ -343,6 +343,10 @@ int plan_cluster_launch_multi(sp_ctx* ctx, sp_table* t, Plan* const* ps, int n, 
                               const PlanHdr& hdr, int32_t* status, void* const* scratch,
                               double* const* thr, int32_t* ord_new);
 int plan_prepare_many(sp_ctx* ctx, sp_table* t, int n, const double* alphas);
+int simulate_and_fold(sp_ctx* ctx, sp_table* t, int n, const int32_t* code, const int32_t* idx,
+                      const int32_t* fill, const double* base, const double* per_item,
+                      const double* noise, double beta, int dfp_count, int dfp_on, int fb_frozen,
+                      int32_t* rec_idx, double* rec_obs);
 int plan_cluster_launch(sp_ctx* ctx, sp_table* t, Plan& p, int W, const PlanHdr& hdr,
                         int32_t* status, PlanHdr* host_hdr, uint32_t* host_seq, uint32_t seq);
 Plan* plan_get(sp_ctx* ctx, sp_table* t, double alpha, int* rc);

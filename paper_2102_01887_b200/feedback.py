@@ -75,6 +75,22 @@ def simulate_observations(decisions, truth_base, noise, *, truth_per_item=None, 
     return oi, ob
 
 
+def simulate_and_fold(table, decisions, truth_base, noise, *, truth_per_item=None, out,
+                      beta: float = 0.5, dfp_count: int = 10, dfp_on: bool = True,
+                      fb_frozen: bool = False) -> None:
+    """``simulate_observations`` then ``fold_observations`` of one table in one cooperative
+    kernel (torch CUDA tensors, stream-ordered); the observation records still land in
+    ``out = (obs_idx, obs)``."""
+    ctx = table._ctx
+    code = decisions["code"]
+    oi, ob = out
+    check(ctx.lib.sp_simulate_and_fold(
+        ctx.handle, table.handle, int(code.shape[0]), ptr(code), ptr(decisions["idx"]),
+        ptr(decisions.get("fill")), ptr(truth_base), ptr(truth_per_item), ptr(noise),
+        float(beta), int(dfp_count), 1 if dfp_on else 0, 1 if fb_frozen else 0, ptr(oi), ptr(ob)),
+        "sp_simulate_and_fold")
+
+
 def table_counters(table) -> tuple[int, np.ndarray]:
     """(completed_ref, per-entry observation counts) of a device table."""
     ctx = table._ctx

@@ -320,3 +320,46 @@ def test_feedback_fold_narrowed_window_vs_oracle(gpu_ctx, beta):
     ofb.fold([st], None, idx, obs, beta=beta, dfp_count=10)
     assert np.array_equal(bits(tab.get_latency()), bits(st.lat))
     tab.close()
+
+
+@pytest.mark.parametrize("per_item", [False, True])
+def test_simulate_and_fold_equals_two_kernels(gpu_ctx, per_item):
+    """sp_simulate_and_fold (the simulated backend's observation law evaluated inside the
+    cooperative fold's load phase) against sp_simulate_observations + sp_feedback_fold on the
+    same decision batches: identical observation records and identical tables after every
+    batch (gate lift included: the reference entry is forced into the first batches)."""
+    import torch
+
+    import paper_2102_01887_b200 as sp
+    from paper_2102_01887_b200 import synth
+
+    spec = synth.synth_spec(False)
+    tabs = [sp.OpTable(spec, synth.synth_scenario()) for _ in range(2)]
+    M = len(tabs[0].entries)
+    rng = np.random.default_rng(7 + per_item)
+    dev = torch.device("cuda", 0)
+    base = torch.from_numpy(np.array([e.latency_initial_s for e in tabs[0].entries])).to(dev)
+    pit = torch.from_numpy(rng.uniform(0.0, 0.01, size=M)).to(dev) if per_item else None
+    ref = tabs[0].ref_index
+    for bt in range(6):
+        n = int(rng.integers(1000, 70000))
+        code = rng.choice([0, 1, 2], size=n, p=[0.1, 0.8, 0.1]).astype(np.int32)
+        hot = rng.choice(M, size=40, replace=False)
+        idx = np.where(rng.random(n) < 0.7, rng.choice(hot, size=n), rng.integers(0, M, size=n)).astype(np.int32)
+        if bt < 2:
+            idx[rng.random(n) < 0.01] = ref
+        dec = {"code": torch.from_numpy(code).to(dev), "idx": torch.from_numpy(idx).to(dev),
+               "fill": torch.from_numpy(rng.integers(1, 129, size=n).astype(np.int32)).to(dev)}
+        noise = torch.from_numpy(np.exp(rng.normal(0.0, 0.3, size=n))).to(dev)
+        r1 = (torch.empty(n, dtype=torch.int32, device=dev), torch.empty(n, dtype=torch.float64, device=dev))
+        r2 = (torch.empty(n, dtype=torch.int32, device=dev), torch.empty(n, dtype=torch.float64, device=dev))
+        sp.simulate_observations(dec, base, noise, truth_per_item=pit, out=r1)
+        sp.fold_observations([tabs[0]], None, r1[0], r1[1], beta=0.5, dfp_count=10, sync_host=False)
+        sp.simulate_and_fold(tabs[1], dec, base, noise, truth_per_item=pit, out=r2, beta=0.5, dfp_count=10)
+        torch.cuda.synchronize()
+        assert torch.equal(r1[0], r2[0]), bt
+        assert torch.equal(r1[1].view(torch.int64), r2[1].view(torch.int64)), bt
+        for t in tabs:
+            t.sync_from_device()
+        a, b = np.asarray(tabs[0].lat).copy(), np.asarray(tabs[1].lat).copy()
+        assert np.array_equal(a.view(np.uint64), b.view(np.uint64)), bt
