@@ -115,3 +115,28 @@ profiler.profile_operation(OperationSpec("op", "x", tpl), scn, 3)
 profiler.pow_correctly_rounded(rng.uniform(0.01, 100, 500), rng.uniform(-2, 2, 500))
 print("sanitize smoke (round 2, session 2) ok")
 
+# session 3: the multi-plan build (one launch, four clusters) + decisions on it, the fused
+# simulate-and-fold, and the replica-parallel run engine (small traces, noise / failures / joins)
+t6 = sp.OpTable(synth.synth_spec(False), synth.synth_scenario())
+t6.invalidate_plans()
+t6.prepare_many([0.0, 1.0, 100.0, 1000.0])
+for al in (0.0, 1.0, 100.0, 1000.0):
+    t6.select_batch(inv.slack, al, inv.avail, upstream_supply=inv.supply, min_batch=inv.min_batch,
+                    flags=inv.flags, mode="plan")
+dec = {k: torch.from_numpy(np.ascontiguousarray(v)).cuda() for k, v in
+       (("code", np.ones(5000, np.int32)), ("idx", rng.integers(0, len(t6.lat), 5000).astype(np.int32)),
+        ("fill", np.ones(5000, np.int32)))}
+rec = (torch.empty(5000, dtype=torch.int32, device="cuda"), torch.empty(5000, dtype=torch.float64, device="cuda"))
+sp.simulate_and_fold(t6, dec, torch.ones(len(t6.lat), dtype=torch.float64, device="cuda"),
+                     torch.ones(5000, dtype=torch.float64, device="cuda"), out=rec)
+torch.cuda.synchronize()
+sys.path.insert(0, "tests")
+import des_cases as dc  # noqa: E402
+from paper_2102_01887_b200.engine import ReplicaEngine, generate_trace  # noqa: E402
+
+for case in (dict(bundle="branching"), dict(bundle="parallel", noise_sigma=0.2, failure_rate=0.1,
+                                            straggle_rate=0.05, straggle_factor=3.0)):
+    eng = ReplicaEngine(dc.run_spec(case))
+    traces = [generate_trace(60, 100 + i, {"cars": 0.6, "persons": 0.8}, 3) for i in range(3)]
+    eng.run(traces, [30.0, 60.0, float("inf")], [1, 2, 3], log_cap=4000, final_tables=True)
+print("sanitize smoke (round 2, session 3) ok")
