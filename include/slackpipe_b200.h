@@ -467,6 +467,11 @@ int sp_des_prepare(sp_ctx* ctx, sp_des* des, int32_t R, int32_t n_traces, const 
 /* Invocation capacity per buffered item (default 1.25; retries and straggler duplicates add
  * invocations beyond one per item — a replica that runs out reports status 1). */
 int sp_des_set_capacity(sp_des* des, double invocations_per_item);
+/* Execution form: 1 = one GPU thread per replica (the replicas of a warp diverge; the most
+ * runs per second once tens of thousands of replicas fill the GPU), 2 = one warp per replica
+ * (all lanes run the replica's serial engine, the entry scans split across the lanes: ~17x lower
+ * latency per run), 0 = default (2 below 24,576 replicas, else 1).  Results are identical. */
+int sp_des_set_mode(sp_des* des, int32_t mode);
 /* Bytes of one replica's arena as last prepared. */
 int64_t sp_des_arena_bytes(sp_des* des);
 

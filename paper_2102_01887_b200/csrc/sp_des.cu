@@ -25,6 +25,7 @@ struct sp_des {
   void* tabs = nullptr;  // lat / cost / costpen, the 32 replicas of a warp interleaved
   size_t tabs_cap = 0;
   int32_t prepared_R = 0;
+  int32_t mode = 0;  // 0: by run count, 1: one thread per run, 2: one warp per run
   // staged host I/O
   void* io = nullptr;
   size_t io_cap = 0;
@@ -82,6 +83,58 @@ k_des_run(const Image* __restrict__ g_im, const double* __restrict__ g_d,
     for (int i = 0; i < N; ++i) lat_out[(size_t)r * N + i] = run.lat(i);
 }
 
+// Warp-per-run form: the 32 lanes of a warp execute one run together — identical serial state in
+// every lane, the entry scans of OpTable.select / affinity split across the lanes and reduced by
+// shuffles — so the warp never diverges on the engine's control flow; the run's mutable entry
+// columns are contiguous in its own arena (the lanes of a scan read consecutive entries).
+__global__ void __launch_bounds__(kMaxThreads)
+k_des_run_warp(const Image* __restrict__ g_im, const double* __restrict__ g_d,
+               const int32_t* __restrict__ g_i, char* __restrict__ arena, int R,
+               const int32_t* __restrict__ frame_off, const int32_t* __restrict__ attrs,
+               const int32_t* __restrict__ trace_of, const double* __restrict__ targets,
+               const double* __restrict__ dfac, const uint8_t* __restrict__ dbits,
+               LogRec* __restrict__ log, double* __restrict__ lat_out, Out* __restrict__ out,
+               int entries_in_smem) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  Image& im = *reinterpret_cast<Image*>(smem);
+  {
+    const int4* src = reinterpret_cast<const int4*>(g_im);
+    int4* dst = reinterpret_cast<int4*>(smem);
+    for (int i = threadIdx.x; i < (int)(sizeof(Image) / 16); i += blockDim.x) dst[i] = src[i];
+  }
+  const int N = g_im->n_entries;
+  const double* dcol = g_d;
+  const int32_t* icol = g_i;
+  if (entries_in_smem) {
+    double* sd = reinterpret_cast<double*>(smem + sizeof(Image));
+    int32_t* si = reinterpret_cast<int32_t*>(sd + 8 * (size_t)N);
+    for (int i = threadIdx.x; i < 8 * N; i += blockDim.x) sd[i] = g_d[i];
+    const int ni = 4 * N + g_im->suf_off[g_im->n_ops];
+    for (int i = threadIdx.x; i < ni; i += blockDim.x) si[i] = g_i[i];
+    dcol = sd;
+    icol = si;
+  }
+  __syncthreads();
+  const int r = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= R) return;  // whole warps
+  const Entries E = entries_view(dcol, icol, N);
+  const int tr = trace_of ? trace_of[r] : r;
+  const int f0 = frame_off[tr];
+  char* ar = arena + (size_t)r * im.arena_bytes;
+  Run run(im, E, ar, reinterpret_cast<double*>(ar + im.o_lat), 1, attrs + (int64_t)f0 * im.n_attrs,
+          frame_off[tr + 1] - f0, targets[r], dfac ? dfac + (size_t)r * im.draw_cap : nullptr,
+          dbits ? dbits + (size_t)r * im.draw_cap : nullptr,
+          log ? log + (size_t)r * im.log_cap : nullptr);
+  run.lane = lane;
+  run.nl = 32;
+  run.run();
+  __syncwarp();
+  if (lane == 0) run.write_out(out[r]);
+  if (lat_out)
+    for (int i = lane; i < N; i += 32) lat_out[(size_t)r * N + i] = run.lat(i);
+}
+
 template <class T>
 int upload_vec(T** dptr, const std::vector<T>& v) {
   cudaError_t e = cudaMalloc(dptr, sizeof(T) * (v.empty() ? 1 : v.size()));
@@ -125,6 +178,24 @@ int launch(sp_ctx* ctx, sp_des* d, int32_t R, const int32_t* frame_off, const in
                         sizeof(int32_t) * (size_t)d->h.im.suf_off[d->h.im.n_ops];
   const int in_smem = ebytes <= kSmemEntriesMax;
   const size_t smem = sizeof(Image) + (in_smem ? ebytes : 0);
+  // default: a warp per run while the runs cannot fill the GPU one thread each (measured on
+  // AMBER: warp form ~0.4 s per run, saturating near 2.5k runs/s from 4k runs; thread form
+  // ~7 s per run but 3.3k runs/s at 32k and 4.1k runs/s at 65k runs)
+  const bool warp = d->mode == 2 || (d->mode == 0 && R < 24576);
+  if (warp) {
+    cudaError_t e = cudaFuncSetAttribute(k_des_run_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return sp::cuda_fail(e, "run engine smem");
+    if (R > 0) {
+      const int per_cta = kMaxThreads / 32;
+      k_des_run_warp<<<(R + per_cta - 1) / per_cta, kMaxThreads, smem, ctx->stream>>>(
+          d->d_image, d->d_dcols, d->d_icols, d->arena, R, frame_off, attrs, trace_of, targets, dfac,
+          dbits, log, lat_out, out, in_smem);
+      ctx->launches++;
+      e = cudaGetLastError();
+      if (e != cudaSuccess) return sp::cuda_fail(e, "k_des_run_warp launch");
+    }
+    return SP_OK;
+  }
   cudaError_t e = cudaFuncSetAttribute(k_des_run, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return sp::cuda_fail(e, "run engine smem");
   if (R > 0) {
@@ -192,6 +263,12 @@ extern "C" int sp_des_prepare(sp_ctx* ctx, sp_des* d, int32_t R, int32_t n_trace
       (n_traces > 0 && !attrs && d->h.im.n_attrs > 0) || draw_cap < 0 || log_cap < 0)
     return sp::fail(SP_E_INVALID, "des_prepare: bad argument");
   return prepare(ctx, d, R, n_traces, frame_off, attrs, draw_cap, log_cap);
+}
+
+extern "C" int sp_des_set_mode(sp_des* d, int32_t mode) {
+  if (!d || mode < 0 || mode > 2) return sp::fail(SP_E_INVALID, "des_set_mode: 0 (default), 1 thread, 2 warp");
+  d->mode = mode;
+  return SP_OK;
 }
 
 extern "C" int sp_des_set_capacity(sp_des* d, double invocations_per_item) {

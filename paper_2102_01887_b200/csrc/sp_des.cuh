@@ -193,6 +193,7 @@ struct Run {
   int32_t failures = 0, dups = 0, completed = 0, met = 0, terminal = 0, n_spec = 0, n_commit = 0,
           log_len = 0, status = kOk;
   int64_t events = 0;
+  int32_t lane = 0, nl = 1;  // warp-per-run mode: this lane and the lanes sharing the run
 
   SPD_HD Run(const Image& im_, const Entries& e_, char* arena, double* tab_, int32_t ts_,
              const int32_t* attrs_, int32_t nf, double tgt, const double* dfac, const uint8_t* dbits,
@@ -422,20 +423,55 @@ struct Run {
     if (E.res[g1] != E.res[g2]) return E.res[g1] < E.res[g2];
     return E.rank[g1] < E.rank[g2];
   }
+  // warp-per-run mode (nl = 32): every lane runs the same serial engine (identical state,
+  // identical stores), only the entry scans are split across the lanes and reduced
+  SPD_HD void reduce_best(int& best, double& bs, double& bc) const {
+#ifdef __CUDA_ARCH__
+    if (nl > 1) {
+      for (int o = 16; o > 0; o >>= 1) {
+        const int ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const double os = __shfl_xor_sync(0xffffffffu, bs, o);
+        const double oc = __shfl_xor_sync(0xffffffffu, bc, o);
+        if (ob >= 0 && (best < 0 || key_less(os, oc, ob, bs, bc, best))) {
+          best = ob;
+          bs = os;
+          bc = oc;
+        }
+      }
+    }
+#endif
+  }
+  SPD_HD bool any_lane(bool v) const {
+#ifdef __CUDA_ARCH__
+    if (nl > 1) return __any_sync(0xffffffffu, v);
+#endif
+    return v;
+  }
+  SPD_HD double min_lanes(double v) const {
+#ifdef __CUDA_ARCH__
+    if (nl > 1)
+      for (int o = 16; o > 0; o >>= 1) {
+        const double w = __shfl_xor_sync(0xffffffffu, v, o);
+        v = w < v ? w : v;
+      }
+#endif
+    return v;
+  }
   SPD_HDN Sel select(int op, const double* sl, int avail, bool allow_delay, int supply,
                      uint32_t excl, int min_batch) {
     Sel r{0, -1, 0, 0.0, 0.0, 0.0};
     const int b0 = im.entry_off[op], b1 = im.entry_off[op + 1];
     int best = -1, best2 = -1;
     double bs = 0, bc = 0, bs2 = 0, bc2 = 0;
-    for (int g = b0; g < b1; ++g) {
+    bool bad = false;
+    for (int g = b0 + lane; g < b1; g += nl) {
       if ((excl >> E.kind[g]) & 1u) continue;
       if (min_batch > 1 && E.bint[g] < min_batch) continue;
       double s, c;
       score_of(g, sl, s, c);
       if (!(s == s) || s == INFINITY) {
-        error(kErrNonFinite);
-        return r;
+        bad = true;
+        continue;
       }
       if (best < 0 || key_less(s, c, g, bs, bc, best)) {
         best = g;
@@ -448,6 +484,12 @@ struct Run {
         bc2 = c;
       }
     }
+    if (any_lane(bad)) {
+      error(kErrNonFinite);
+      return r;
+    }
+    reduce_best(best, bs, bc);
+    reduce_best(best2, bs2, bc2);
     if (best < 0) return r;  // no entry survives the mask: None (configurator.py:266-267)
     const int B = E.bint[best];
     if (allow_delay && B > avail && supply >= B - avail) {
@@ -477,11 +519,11 @@ struct Run {
   SPD_HDN bool affinity(int op, int kind, const double* sl, double& out) {
     const int b0 = im.entry_off[op], b1 = im.entry_off[op + 1];
     double mon = INFINITY, moff = INFINITY;
-    bool any_on = false, any_off = false;
-    for (int g = b0; g < b1; ++g) {
+    bool any_on = false, any_off = false, bad = false;
+    for (int g = b0 + lane; g < b1; g += nl) {
       double s, c;
       score_of(g, sl, s, c);
-      if (!(s == s)) error(kErrNonFinite);
+      if (!(s == s)) bad = true;
       if (E.kind[g] == kind) {
         any_on = true;
         if (s < mon) mon = s;
@@ -490,10 +532,16 @@ struct Run {
         if (s < moff) moff = s;
       }
     }
+    if (any_lane(bad)) error(kErrNonFinite);
+    any_on = any_lane(any_on);
+    any_off = any_lane(any_off);
+    mon = min_lanes(mon);
+    moff = min_lanes(moff);
     if (!any_on) return false;
     out = any_off ? moff / mon : INFINITY;
     return true;
   }
+
 
   // ---- invocations and item lists (manager.py:303-329) --------------------------------------
   SPD_HDN int new_inv(int op, int unit) {
@@ -982,6 +1030,9 @@ struct Run {
         break;
       }
       flushed = false;
+#ifdef __CUDA_ARCH__
+      if (nl > 1) __syncwarp();  // warp-per-run: the lanes' redundant stores stay in lockstep
+#endif
       const HeapEnt ev = pop();
       now = ev.t;
       if (ev.key >> 31) {

@@ -407,6 +407,12 @@ class ReplicaEngine:
         self.handle = h
         self.cap_scale = 1.25
 
+    def set_mode(self, mode: str) -> None:
+        """"default" (a warp per replica below 24,576 replicas, else a thread), "warp" or
+        "thread"."""
+        _lib.check(self.lib.sp_des_set_mode(self.handle, {"default": 0, "thread": 1, "warp": 2}[mode]),
+                   "sp_des_set_mode")
+
     def close(self) -> None:
         if self.handle:
             self.lib.sp_des_destroy(self.ctx.handle, self.handle)

@@ -19,12 +19,20 @@ def device_engine(gpu_ctx):
     return lambda spec: ReplicaEngine(spec, gpu_ctx)
 
 
-def test_device_engine_matches_golden_runs(device_engine, gpu_ctx):
+@pytest.mark.parametrize("mode", ["warp", "thread"])
+def test_device_engine_matches_golden_runs(device_engine, gpu_ctx, mode):
+    """Both execution forms: one warp per replica (default) and one thread per replica."""
     launches0 = gpu_ctx.launch_count
     bad = []
     n = 0
+
+    def make(spec):
+        eng = device_engine(spec)
+        eng.set_mode(mode)
+        return eng
+
     for group in dc.groups(dc.runs()):
-        for case, (rows, rep, lat) in zip(group, dc.run_group(device_engine, group)):
+        for case, (rows, rep, lat) in zip(group, dc.run_group(make, group)):
             n += 1
             errs = dc.check(case, rows, rep, lat)
             if errs:

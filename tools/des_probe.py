@@ -21,7 +21,9 @@ ap = argparse.ArgumentParser()
 ap.add_argument("R", nargs="*", type=int, default=[148, 1024, 4096])
 ap.add_argument("--frames", type=int, default=3000)
 ap.add_argument("--once", action="store_true")
+ap.add_argument("--mode", default="warp", choices=["warp", "thread"])
 args = ap.parse_args()
+eng.set_mode(args.mode)
 for R in args.R:
     t0 = time.time()
     uniq = [generate_trace(args.frames, 17 + i, {"cars": 0.6, "persons": 0.8}, 3) for i in range(min(R, 256))]
@@ -36,6 +38,6 @@ for R in args.R:
     t3 = time.time()
     dt = (t3 - t2) if not args.once else (t2 - t1)
     dec = sum(r.decision_count for r in res)
-    print(f"R={R}: gen {t1-t0:.2f}s run {t2-t1:.3f}s / {t3-t2:.3f}s  {R/dt:.1f} runs/s  "
+    print(f"{args.mode} R={R}: gen {t1-t0:.2f}s run {t2-t1:.3f}s / {t3-t2:.3f}s  {R/dt:.1f} runs/s  "
           f"{dec/dt:.3e} decisions/s  arena {eng.lib.sp_des_arena_bytes(eng.handle)/1e6:.2f} MB/replica",
           flush=True)
