@@ -211,8 +211,56 @@ def run_c1(args):
                                              "source": "reference pkg/test_output.txt:171 (whole "
                                                        "engine run, other hardware)"},
         "cpu_baseline": cpu,
+        "whole_run": _c1_whole_run(args),
     }
     return line
+
+
+def _c1_whole_run(args):
+    """Config 1 as the reference runs it: ONE complete AMBER run at the 50 % target (3,000
+    frames, 15,290 decisions), PipelineRun.run_to_completion through the device drop-in
+    (engine.PipelineRun: setup, H2D, one warp running the whole event loop, D2H of the report,
+    the decision log and the final tables) — wall clock, against oracle/engine.py (the Python
+    restatement of the reference engine) on one core; parity against the reference's own run."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    import des_cases as dc
+    from paper_2102_01887_b200.engine import PipelineRun
+
+    case = dc.runs()[3]
+    doc, dag, sc, profiles, paths, frames = dc.bundle("branching")
+    spec = dc.run_spec(case)
+    times, rep, run = [], None, None
+    for _ in range(4):
+        run = PipelineRun(dag, {}, profiles, frames, sc, float(case["target"]), spec.params,
+                          paths=paths, pipeline_name=doc["name"])
+        t0 = time.perf_counter()
+        rep = run.run_to_completion()
+        times.append(time.perf_counter() - t0)
+    ok = (dc.log_digest(run.decision_log) == case["expect"]["log_sha256"]
+          and rep.csv_row().split(",")[1:] == case["expect"]["csv_row"].split(",")[1:])
+    dt = min(times[1:])
+    cpu = None
+    if not args.no_cpu_baseline:
+        from oracle import engine as oe
+
+        p = spec.params
+        c0 = time.perf_counter()
+        oe.Engine(dag, profiles, frames, sc, float(case["target"]),
+                  oe.Params(p.alpha, p.cq_capacity, p.dfp_count, p.straggler_timeout_factor,
+                            p.smoothing_beta), seed=sc.seed, paths=paths).run()
+        cdt = time.perf_counter() - c0
+        cpu = {"value": rep.decision_count / cdt, "unit": "decisions/s", "cores": 1, "kind": "port",
+               "seconds_per_run": cdt,
+               "sample": "the same run through oracle/engine.py (Python restatement of PipelineRun / "
+                         "BackendSim / Configurator, pinned to the reference), one core"}
+    return {"metric": "one complete AMBER run (PipelineRun.run_to_completion) through the device drop-in",
+            "unit": "decisions/s", "value": rep.decision_count / dt, "seconds_per_run": dt,
+            "decisions": rep.decision_count, "kernel": "k_des_run_warp (one warp runs the whole event loop)",
+            "e2e": True, "note": "wall clock of run_to_completion: run-description upload, trace encoding, H2D, the run, D2H of "
+                                 "report + 15,290-row decision log + final tables",
+            "parity": {"result": "decision log sha256 and CSV row equal the reference's run" if ok
+                       else "MISMATCH", "csv_row": rep.csv_row()},
+            "cpu_baseline": cpu}
 
 
 # ---- c3 -------------------------------------------------------------------------------------
