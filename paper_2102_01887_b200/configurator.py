@@ -524,8 +524,8 @@ class _RawTable:
     """A device table from raw arrays (single kind), for spec-level helpers and benches."""
 
     def __init__(self, *, lat, res, batch, pool, price, kind=None, id_rank=None, K: int = 1,
-                 ref_index: int = -1, lat_init=None, device: int | None = None):
-        self._ctx = get_context(device)
+                 ref_index: int = -1, lat_init=None, device: int | None = None, ctx=None):
+        self._ctx = ctx or get_context(device)
         self.lat = np.ascontiguousarray(lat, dtype=np.float64)
         M = len(self.lat)
         self.M = M

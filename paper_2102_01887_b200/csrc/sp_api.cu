@@ -260,6 +260,7 @@ int sp_ctx_destroy(sp_ctx* ctx) {
   }
   if (!ctx) return SP_OK;
   cudaStreamSynchronize(ctx->stream);
+  coop_release(ctx);
   cudaFree(ctx->io_dev);
   cudaFree(ctx->ptr_dev);
   cudaFree(ctx->tmp_dev);

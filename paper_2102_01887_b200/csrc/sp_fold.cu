@@ -1050,10 +1050,11 @@ struct CoopBuffers {
   int64_t keys = 0;
   uint8_t* base = nullptr;
 };
-static CoopBuffers g_coop[64];
 
 static int coop_buffers(sp_ctx* ctx, int64_t keys, CoopArgs& a) {
-  CoopBuffers& b = g_coop[ctx->device & 63];
+  // per context: two contexts of one device may fold concurrently on their own streams
+  if (!ctx->coop) ctx->coop = new CoopBuffers();
+  CoopBuffers& b = *static_cast<CoopBuffers*>(ctx->coop);
   auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
   const size_t chunk = al(4u * kCoopChunk) * 2 + al(8u * kCoopChunk) + al(4u * kCoopChunk);
   const size_t gates = al(sizeof(Gate) * kMaxFoldTables), stb = al(sizeof(CoopState));
@@ -1068,10 +1069,12 @@ static int coop_buffers(sp_ctx* ctx, int64_t keys, CoopArgs& a) {
     const size_t per = al(8u * cap) * 3 + al(4u * kCoopTiles * cap);
     SP_CUDA(cudaMalloc(&b.base, per + chunk + gates + stb));
     uint8_t* q = b.base;
-    SP_CUDA(cudaMemset(q, 0, al(8u * cap)));                    // mask
-    SP_CUDA(cudaMemset(q + al(8u * cap), 0xFF, al(8u * cap)));  // lo
-    SP_CUDA(cudaMemset(q + 2 * al(8u * cap), 0, al(8u * cap))); // hi
-    SP_CUDA(cudaMemset(q + per + chunk + gates, 0, stb));       // barrier / counters
+    // stream-ordered before the fold kernel (the context stream is non-blocking: a legacy
+    // cudaMemset on the NULL stream would race with it)
+    SP_CUDA(cudaMemsetAsync(q, 0, al(8u * cap), ctx->stream));                    // mask
+    SP_CUDA(cudaMemsetAsync(q + al(8u * cap), 0xFF, al(8u * cap), ctx->stream));  // lo
+    SP_CUDA(cudaMemsetAsync(q + 2 * al(8u * cap), 0, al(8u * cap), ctx->stream)); // hi
+    SP_CUDA(cudaMemsetAsync(q + per + chunk + gates, 0, stb, ctx->stream));       // barrier / counters
     b.keys = cap;
   }
   const int64_t cap = b.keys;
@@ -1208,4 +1211,14 @@ int simulate_and_fold(sp_ctx* ctx, sp_table* t, int n, const int32_t* code, cons
   return rc;
 }
 
+}  // namespace sp
+
+namespace sp {
+void coop_release(sp_ctx* ctx) {
+  if (!ctx->coop) return;
+  CoopBuffers* b = static_cast<CoopBuffers*>(ctx->coop);
+  cudaFree(b->base);
+  delete b;
+  ctx->coop = nullptr;
+}
 }  // namespace sp

@@ -182,6 +182,7 @@ struct sp_ctx {
   static constexpr int kPipeChunks = 8;
   cudaEvent_t ev_in[kPipeChunks] = {}, ev_comp[kPipeChunks] = {}, ev_out[kPipeChunks] = {};
   cudaStream_t capture = nullptr;  // private stream for CUDA-graph captures
+  void* coop = nullptr;            // the cooperative fold's persistent buffers (sp_fold.cu)
 };
 
 struct sp_table {
@@ -343,6 +344,7 @@ int plan_cluster_launch_multi(sp_ctx* ctx, sp_table* t, Plan* const* ps, int n, 
                               const PlanHdr& hdr, int32_t* status, void* const* scratch,
                               double* const* thr, int32_t* ord_new);
 int plan_prepare_many(sp_ctx* ctx, sp_table* t, int n, const double* alphas);
+void coop_release(sp_ctx* ctx);
 int simulate_and_fold(sp_ctx* ctx, sp_table* t, int n, const int32_t* code, const int32_t* idx,
                       const int32_t* fill, const double* base, const double* per_item,
                       const double* noise, double beta, int dfp_count, int dfp_on, int fb_frozen,
