@@ -25,7 +25,8 @@ struct sp_des {
   void* tabs = nullptr;  // lat / cost / costpen, the 32 replicas of a warp interleaved
   size_t tabs_cap = 0;
   int32_t prepared_R = 0;
-  int32_t mode = 0;  // 0: by run count, 1: one thread per run, 2: one warp per run
+  int32_t mode = 0;  // 0: by run count, 1: one thread per run, 2: `lanes` lanes per run
+  int32_t lanes = 32;
   // staged host I/O
   void* io = nullptr;
   size_t io_cap = 0;
@@ -94,7 +95,7 @@ k_des_run_warp(const Image* __restrict__ g_im, const double* __restrict__ g_d,
                const int32_t* __restrict__ trace_of, const double* __restrict__ targets,
                const double* __restrict__ dfac, const uint8_t* __restrict__ dbits,
                LogRec* __restrict__ log, double* __restrict__ lat_out, Out* __restrict__ out,
-               int entries_in_smem) {
+               int entries_in_smem, int nl) {
   extern __shared__ __align__(16) unsigned char smem[];
   Image& im = *reinterpret_cast<Image*>(smem);
   {
@@ -115,9 +116,10 @@ k_des_run_warp(const Image* __restrict__ g_im, const double* __restrict__ g_d,
     icol = si;
   }
   __syncthreads();
-  const int r = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-  const int lane = threadIdx.x & 31;
-  if (r >= R) return;  // whole warps
+  const int lb = __ffs(nl) - 1;  // nl: lanes per run (1..32, a power of two)
+  const int r = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> lb);
+  const int lane = threadIdx.x & (nl - 1);
+  if (r >= R) return;  // whole lane groups
   const Entries E = entries_view(dcol, icol, N);
   const int tr = trace_of ? trace_of[r] : r;
   const int f0 = frame_off[tr];
@@ -127,12 +129,13 @@ k_des_run_warp(const Image* __restrict__ g_im, const double* __restrict__ g_d,
           dbits ? dbits + (size_t)r * im.draw_cap : nullptr,
           log ? log + (size_t)r * im.log_cap : nullptr);
   run.lane = lane;
-  run.nl = 32;
+  run.nl = nl;
+  run.lmask = nl == 32 ? 0xffffffffu : ((1u << nl) - 1u) << ((threadIdx.x & 31) & ~(nl - 1));
   run.run();
-  __syncwarp();
+  __syncwarp(run.lmask);
   if (lane == 0) run.write_out(out[r]);
   if (lat_out)
-    for (int i = lane; i < N; i += 32) lat_out[(size_t)r * N + i] = run.lat(i);
+    for (int i = lane; i < N; i += nl) lat_out[(size_t)r * N + i] = run.lat(i);
 }
 
 template <class T>
@@ -181,15 +184,15 @@ int launch(sp_ctx* ctx, sp_des* d, int32_t R, const int32_t* frame_off, const in
   // default: a warp per run while the runs cannot fill the GPU one thread each (measured on
   // AMBER: warp form ~0.4 s per run, saturating near 2.5k runs/s from 4k runs; thread form
   // ~7 s per run but 3.3k runs/s at 32k and 4.1k runs/s at 65k runs)
-  const bool warp = d->mode == 2 || (d->mode == 0 && R < 24576);
-  if (warp) {
+  const int nl = d->mode >= 2 ? d->lanes : (d->mode == 0 && R < 24576 ? 32 : 0);
+  if (nl) {
     cudaError_t e = cudaFuncSetAttribute(k_des_run_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return sp::cuda_fail(e, "run engine smem");
     if (R > 0) {
-      const int per_cta = kMaxThreads / 32;
+      const int per_cta = kMaxThreads / nl;
       k_des_run_warp<<<(R + per_cta - 1) / per_cta, kMaxThreads, smem, ctx->stream>>>(
           d->d_image, d->d_dcols, d->d_icols, d->arena, R, frame_off, attrs, trace_of, targets, dfac,
-          dbits, log, lat_out, out, in_smem);
+          dbits, log, lat_out, out, in_smem, nl);
       ctx->launches++;
       e = cudaGetLastError();
       if (e != cudaSuccess) return sp::cuda_fail(e, "k_des_run_warp launch");
@@ -266,8 +269,11 @@ extern "C" int sp_des_prepare(sp_ctx* ctx, sp_des* d, int32_t R, int32_t n_trace
 }
 
 extern "C" int sp_des_set_mode(sp_des* d, int32_t mode) {
-  if (!d || mode < 0 || mode > 2) return sp::fail(SP_E_INVALID, "des_set_mode: 0 (default), 1 thread, 2 warp");
-  d->mode = mode;
+  // 0 default, 1 one thread per run, 2 one warp per run, 4 / 8 / 16: that many lanes per run
+  if (!d || !(mode == 0 || mode == 1 || mode == 2 || mode == 4 || mode == 8 || mode == 16))
+    return sp::fail(SP_E_INVALID, "des_set_mode: 0 (default), 1 thread, 2 warp, 4 / 8 / 16 lanes");
+  d->mode = mode == 0 || mode == 1 ? mode : 2;
+  d->lanes = mode == 2 ? 32 : (mode >= 4 ? mode : 32);
   return SP_OK;
 }
 

@@ -193,7 +193,8 @@ struct Run {
   int32_t failures = 0, dups = 0, completed = 0, met = 0, terminal = 0, n_spec = 0, n_commit = 0,
           log_len = 0, status = kOk;
   int64_t events = 0;
-  int32_t lane = 0, nl = 1;  // warp-per-run mode: this lane and the lanes sharing the run
+  int32_t lane = 0, nl = 1;  // lanes per run: this lane's index among the run's nl lanes
+  uint32_t lmask = 0xffffffffu;  // the run's lanes within the warp
 
   SPD_HD Run(const Image& im_, const Entries& e_, char* arena, double* tab_, int32_t ts_,
              const int32_t* attrs_, int32_t nf, double tgt, const double* dfac, const uint8_t* dbits,
@@ -428,10 +429,10 @@ struct Run {
   SPD_HD void reduce_best(int& best, double& bs, double& bc) const {
 #ifdef __CUDA_ARCH__
     if (nl > 1) {
-      for (int o = 16; o > 0; o >>= 1) {
-        const int ob = __shfl_xor_sync(0xffffffffu, best, o);
-        const double os = __shfl_xor_sync(0xffffffffu, bs, o);
-        const double oc = __shfl_xor_sync(0xffffffffu, bc, o);
+      for (int o = nl >> 1; o > 0; o >>= 1) {
+        const int ob = __shfl_xor_sync(lmask, best, o);
+        const double os = __shfl_xor_sync(lmask, bs, o);
+        const double oc = __shfl_xor_sync(lmask, bc, o);
         if (ob >= 0 && (best < 0 || key_less(os, oc, ob, bs, bc, best))) {
           best = ob;
           bs = os;
@@ -443,15 +444,15 @@ struct Run {
   }
   SPD_HD bool any_lane(bool v) const {
 #ifdef __CUDA_ARCH__
-    if (nl > 1) return __any_sync(0xffffffffu, v);
+    if (nl > 1) return __any_sync(lmask, v);
 #endif
     return v;
   }
   SPD_HD double min_lanes(double v) const {
 #ifdef __CUDA_ARCH__
     if (nl > 1)
-      for (int o = 16; o > 0; o >>= 1) {
-        const double w = __shfl_xor_sync(0xffffffffu, v, o);
+      for (int o = nl >> 1; o > 0; o >>= 1) {
+        const double w = __shfl_xor_sync(lmask, v, o);
         v = w < v ? w : v;
       }
 #endif
@@ -1031,7 +1032,7 @@ struct Run {
       }
       flushed = false;
 #ifdef __CUDA_ARCH__
-      if (nl > 1) __syncwarp();  // warp-per-run: the lanes' redundant stores stay in lockstep
+      if (nl > 1) __syncwarp(lmask);  // lanes per run: their redundant stores stay in lockstep
 #endif
       const HeapEnt ev = pop();
       now = ev.t;

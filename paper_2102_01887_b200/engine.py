@@ -410,8 +410,8 @@ class ReplicaEngine:
     def set_mode(self, mode: str) -> None:
         """"default" (a warp per replica below 24,576 replicas, else a thread), "warp" or
         "thread"."""
-        _lib.check(self.lib.sp_des_set_mode(self.handle, {"default": 0, "thread": 1, "warp": 2}[mode]),
-                   "sp_des_set_mode")
+        m = {"default": 0, "thread": 1, "warp": 2, "lanes4": 4, "lanes8": 8, "lanes16": 16}[mode]
+        _lib.check(self.lib.sp_des_set_mode(self.handle, m), "sp_des_set_mode")
 
     def close(self) -> None:
         if self.handle:
