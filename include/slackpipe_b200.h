@@ -471,7 +471,7 @@ int sp_des_set_capacity(sp_des* des, double invocations_per_item);
  * runs per second once tens of thousands of replicas fill the GPU), 2 = one warp per replica
  * (all lanes run the replica's serial engine, the entry scans split across the lanes: ~17x lower
  * latency per run), 4 / 8 / 16 = that many lanes per replica (32 / n replicas per warp),
- * 0 = default (2 below 24,576 replicas, else 1).  Results are identical. */
+ * 0 = default (32 lanes below 2,048 replicas, 8 below 32,768, else 4).  Results are identical. */
 int sp_des_set_mode(sp_des* des, int32_t mode);
 /* Bytes of one replica's arena as last prepared. */
 int64_t sp_des_arena_bytes(sp_des* des);

@@ -181,10 +181,11 @@ int launch(sp_ctx* ctx, sp_des* d, int32_t R, const int32_t* frame_off, const in
                         sizeof(int32_t) * (size_t)d->h.im.suf_off[d->h.im.n_ops];
   const int in_smem = ebytes <= kSmemEntriesMax;
   const size_t smem = sizeof(Image) + (in_smem ? ebytes : 0);
-  // default: a warp per run while the runs cannot fill the GPU one thread each (measured on
-  // AMBER: warp form ~0.4 s per run, saturating near 2.5k runs/s from 4k runs; thread form
-  // ~7 s per run but 3.3k runs/s at 32k and 4.1k runs/s at 65k runs)
-  const int nl = d->mode >= 2 ? d->lanes : (d->mode == 0 && R < 24576 ? 32 : 0);
+  // default lanes per run by the number of runs (measured on AMBER, runs/s; one run per thread:
+  // 1.3k at 16k runs, 4.1k at 65k; 32 lanes: 0.42 s per run, 2.5k runs/s from 4k runs; 16 lanes:
+  // 3.1k / 3.4k; 8 lanes: 3.7k / 3.9k; 4 lanes: 3.2k / 4.6k at 16k / 65k runs)
+  const int nl = d->mode >= 2 ? d->lanes
+                              : (d->mode == 1 ? 0 : (R < 2048 ? 32 : (R < 32768 ? 8 : 4)));
   if (nl) {
     cudaError_t e = cudaFuncSetAttribute(k_des_run_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return sp::cuda_fail(e, "run engine smem");
