@@ -437,8 +437,15 @@ typedef struct {
   double latency, cost, now;
   int32_t peak_slots, peak_heap;  /* most invocation slots / heap entries the replica held at once */
   int32_t status, met, completed, failures, duplicates, invocations, terminal_items, n_speculate,
-      n_commit, configs_used, log_len, events;
+      n_commit, configs_used, log_len, events, event_len, pad;
 } sp_des_out;
+
+/* One BackendSim.trace row (backend.py:207, 243): meta = event (0 start, 1 complete, 2 fail) |
+ * backend kind << 2 | instance << 8. */
+typedef struct {
+  double t;
+  int32_t iid, meta;
+} sp_des_event;
 
 /* One decision_log row (configurator.py:650-654, 746-749): meta = op | entry << 8 | commit << 30. */
 typedef struct {
@@ -453,12 +460,13 @@ int sp_des_destroy(sp_ctx* ctx, sp_des* des);
  * trace_of[r] (NULL: trace r, n_traces == R) with target target_s[r].
  * draw_factor / draw_bits (R x draw_cap, or NULL when spec.draws == 0): per start, in start order,
  * exp(N(0, sigma)) and bit0 straggled / bit1 will_fail from the replica's numpy stream.  log
- * (R x log_cap rows, optional), lat_out (R x n_entries final latencies, optional), out (R rows).
+ * (R x log_cap rows, optional), lat_out (R x n_entries final latencies, optional), out (R rows),
+ * events (R x event_cap rows of the backend's event trace, optional).
  * mem: SP_MEM_HOST (copies in, launch, copies out, synchronises) or SP_MEM_DEVICE. */
 int sp_des_run(sp_ctx* ctx, sp_des* des, int32_t R, int32_t n_traces, const int32_t* frame_off,
                const int32_t* attrs, const int32_t* trace_of, const double* target_s, int32_t draw_cap, const double* draw_factor,
                const uint8_t* draw_bits, int32_t log_cap, sp_des_log* log, double* lat_out,
-               sp_des_out* out, int32_t mem);
+               sp_des_out* out, int32_t event_cap, sp_des_event* events, int32_t mem);
 /* Size the per-replica arenas for R replicas of these traces (host frame_off / attrs) and the
  * given draw / log capacities; sp_des_run with SP_MEM_DEVICE buffers requires it (the host-buffer
  * form calls it itself). */

@@ -46,7 +46,8 @@ k_des_run(const Image* __restrict__ g_im, const double* __restrict__ g_d,
           const int32_t* __restrict__ trace_of,
           const double* __restrict__ targets, const double* __restrict__ dfac,
           const uint8_t* __restrict__ dbits, LogRec* __restrict__ log,
-          double* __restrict__ lat_out, Out* __restrict__ out, int entries_in_smem) {
+          double* __restrict__ lat_out, Out* __restrict__ out, int entries_in_smem,
+          EvRec* __restrict__ ev) {
   static_assert(sizeof(Image) % 16 == 0, "Image is copied in 16-byte words");
   extern __shared__ __align__(16) unsigned char smem[];
   Image& im = *reinterpret_cast<Image*>(smem);
@@ -78,6 +79,7 @@ k_des_run(const Image* __restrict__ g_im, const double* __restrict__ g_d,
           frame_off[tr + 1] - f0, targets[r], dfac ? dfac + (size_t)r * im.draw_cap : nullptr,
           dbits ? dbits + (size_t)r * im.draw_cap : nullptr,
           log ? log + (size_t)r * im.log_cap : nullptr);
+  if (ev) run.evlog = ev + (size_t)r * im.ev_cap;
   run.run();
   run.write_out(out[r]);
   if (lat_out)
@@ -95,7 +97,7 @@ k_des_run_warp(const Image* __restrict__ g_im, const double* __restrict__ g_d,
                const int32_t* __restrict__ trace_of, const double* __restrict__ targets,
                const double* __restrict__ dfac, const uint8_t* __restrict__ dbits,
                LogRec* __restrict__ log, double* __restrict__ lat_out, Out* __restrict__ out,
-               int entries_in_smem, int nl) {
+               int entries_in_smem, int nl, EvRec* __restrict__ ev) {
   extern __shared__ __align__(16) unsigned char smem[];
   Image& im = *reinterpret_cast<Image*>(smem);
   {
@@ -130,6 +132,7 @@ k_des_run_warp(const Image* __restrict__ g_im, const double* __restrict__ g_d,
           log ? log + (size_t)r * im.log_cap : nullptr);
   run.lane = lane;
   run.nl = nl;
+  if (ev) run.evlog = ev + (size_t)r * im.ev_cap;
   run.lmask = nl == 32 ? 0xffffffffu : ((1u << nl) - 1u) << ((threadIdx.x & 31) & ~(nl - 1));
   run.run();
   __syncwarp(run.lmask);
@@ -157,9 +160,10 @@ int grow(void** p, size_t* cap, size_t bytes) {
 }
 
 int prepare(sp_ctx* ctx, sp_des* d, int32_t R, int32_t T, const int32_t* frame_off,
-            const int32_t* attrs, int32_t draw_cap, int32_t log_cap) {
+            const int32_t* attrs, int32_t draw_cap, int32_t log_cap, int32_t ev_cap = 0) {
   std::string err;
-  if (!plan_run(d->h, T, frame_off, attrs, draw_cap, log_cap, err)) return sp::fail(SP_E_INVALID, err);
+  if (!plan_run(d->h, T, frame_off, attrs, draw_cap, log_cap, err, ev_cap))
+    return sp::fail(SP_E_INVALID, err);
   const size_t need = (size_t)d->h.im.arena_bytes * (size_t)R;
   void* a = d->arena;
   int rc = grow(&a, &d->arena_cap, need);
@@ -175,7 +179,7 @@ int prepare(sp_ctx* ctx, sp_des* d, int32_t R, int32_t T, const int32_t* frame_o
 
 int launch(sp_ctx* ctx, sp_des* d, int32_t R, const int32_t* frame_off, const int32_t* attrs,
            const int32_t* trace_of, const double* targets, const double* dfac, const uint8_t* dbits, LogRec* log,
-           double* lat_out, Out* out) {
+           double* lat_out, Out* out, EvRec* ev) {
   const int N = d->h.im.n_entries;
   const size_t ebytes = (size_t)N * (8 * sizeof(double) + 4 * sizeof(int32_t)) +
                         sizeof(int32_t) * (size_t)d->h.im.suf_off[d->h.im.n_ops];
@@ -193,7 +197,7 @@ int launch(sp_ctx* ctx, sp_des* d, int32_t R, const int32_t* frame_off, const in
       const int per_cta = kMaxThreads / nl;
       k_des_run_warp<<<(R + per_cta - 1) / per_cta, kMaxThreads, smem, ctx->stream>>>(
           d->d_image, d->d_dcols, d->d_icols, d->arena, R, frame_off, attrs, trace_of, targets, dfac,
-          dbits, log, lat_out, out, in_smem, nl);
+          dbits, log, lat_out, out, in_smem, nl, ev);
       ctx->launches++;
       e = cudaGetLastError();
       if (e != cudaSuccess) return sp::cuda_fail(e, "k_des_run_warp launch");
@@ -207,7 +211,7 @@ int launch(sp_ctx* ctx, sp_des* d, int32_t R, const int32_t* frame_off, const in
     const int threads = R >= 128 * ctx->num_sms ? 128 : (R >= 64 * ctx->num_sms ? 64 : 32);
     k_des_run<<<(R + threads - 1) / threads, threads, smem, ctx->stream>>>(
         d->d_image, d->d_dcols, d->d_icols, d->arena, (double*)d->tabs, R, frame_off, attrs, trace_of, targets, dfac, dbits,
-        log, lat_out, out, in_smem);
+        log, lat_out, out, in_smem, ev);
     ctx->launches++;
     e = cudaGetLastError();
     if (e != cudaSuccess) return sp::cuda_fail(e, "k_des_run launch");
@@ -289,10 +293,13 @@ extern "C" int sp_des_run(sp_ctx* ctx, sp_des* d, int32_t R, int32_t n_traces,
                           const int32_t* frame_off, const int32_t* attrs, const int32_t* trace_of,
                           const double* target_s, int32_t draw_cap,
                           const double* draw_factor, const uint8_t* draw_bits, int32_t log_cap,
-                          sp_des_log* log, double* lat_out, sp_des_out* out, int32_t mem) {
+                          sp_des_log* log, double* lat_out, sp_des_out* out, int32_t event_cap,
+                          sp_des_event* events, int32_t mem) {
   sp::DeviceScope _dev_scope(ctx ? ctx->device : -1);
   static_assert(sizeof(sp_des_out) == sizeof(Out), "sp_des_out layout");
   static_assert(sizeof(sp_des_log) == sizeof(LogRec), "sp_des_log layout");
+  static_assert(sizeof(sp_des_event) == sizeof(EvRec), "sp_des_event layout");
+  if (event_cap < 0 || (event_cap > 0 && !events)) return sp::fail(SP_E_INVALID, "des_run: bad event buffer");
   if (!ctx || !d || R < 0 || n_traces < 1 || !frame_off || !target_s || !out || draw_cap < 0 ||
       log_cap < 0 || (!trace_of && n_traces != R) ||
       (mem != SP_MEM_HOST && mem != SP_MEM_DEVICE))
@@ -304,16 +311,17 @@ extern "C" int sp_des_run(sp_ctx* ctx, sp_des* d, int32_t R, int32_t n_traces,
     return sp::fail(SP_E_INVALID, "des_run: the scenario draws straggles / failures; draw_bits required");
   if (R == 0) return SP_OK;
   if (mem == SP_MEM_DEVICE) {
-    if (d->prepared_R < R || im.draw_cap != draw_cap || im.log_cap != log_cap)
+    if (d->prepared_R < R || im.draw_cap != draw_cap || im.log_cap != log_cap || im.ev_cap != event_cap)
       return sp::fail(SP_E_INVALID, "des_run: device buffers need sp_des_prepare with the same R / caps");
     int rc = launch(ctx, d, R, frame_off, attrs, trace_of, target_s, draw_factor, draw_bits,
-                    reinterpret_cast<LogRec*>(log), lat_out, reinterpret_cast<Out*>(out));
+                    reinterpret_cast<LogRec*>(log), lat_out, reinterpret_cast<Out*>(out),
+                    reinterpret_cast<EvRec*>(events));
     return rc;
   }
   if (trace_of)
     for (int r = 0; r < R; ++r)
       if (trace_of[r] < 0 || trace_of[r] >= n_traces) return sp::fail(SP_E_INVALID, "des_run: bad trace_of");
-  int rc = prepare(ctx, d, R, n_traces, frame_off, attrs, draw_cap, log_cap);
+  int rc = prepare(ctx, d, R, n_traces, frame_off, attrs, draw_cap, log_cap, event_cap);
   if (rc != SP_OK) return rc;
   const int64_t F = frame_off[n_traces];
   const int N = im.n_entries;
@@ -332,6 +340,7 @@ extern "C" int sp_des_run(sp_ctx* ctx, sp_des* d, int32_t R, int32_t n_traces,
   const size_t s_bits = draw_bits ? slot((size_t)R * draw_cap) : 0;
   const size_t s_log = log ? slot(sizeof(LogRec) * (size_t)R * log_cap) : 0;
   const size_t s_lat = lat_out ? slot(8 * (size_t)R * N) : 0;
+  const size_t s_ev = events ? slot(sizeof(EvRec) * (size_t)R * event_cap) : 0;
   const size_t s_out = slot(sizeof(Out) * (size_t)R);
   rc = grow(&d->io, &d->io_cap, off);
   if (rc != SP_OK) return rc;
@@ -352,13 +361,15 @@ extern "C" int sp_des_run(sp_ctx* ctx, sp_des* d, int32_t R, int32_t n_traces,
               trace_of ? (const int32_t*)(io + s_trace) : nullptr, (const double*)(io + s_tgt), draw_factor ? (const double*)(io + s_fac) : nullptr,
               draw_bits ? (const uint8_t*)(io + s_bits) : nullptr,
               log ? (LogRec*)(io + s_log) : nullptr, lat_out ? (double*)(io + s_lat) : nullptr,
-              (Out*)(io + s_out));
+              (Out*)(io + s_out), events ? (EvRec*)(io + s_ev) : nullptr);
   if (rc != SP_OK) return rc;
   e = cudaMemcpyAsync(out, io + s_out, sizeof(Out) * (size_t)R, cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess && log)
     e = cudaMemcpyAsync(log, io + s_log, sizeof(LogRec) * (size_t)R * log_cap, cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess && lat_out)
     e = cudaMemcpyAsync(lat_out, io + s_lat, 8 * (size_t)R * N, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess && events)
+    e = cudaMemcpyAsync(events, io + s_ev, sizeof(EvRec) * (size_t)R * event_cap, cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return sp::cuda_fail(e, "des_run");
   return SP_OK;

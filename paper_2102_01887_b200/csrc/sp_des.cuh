@@ -77,7 +77,7 @@ struct alignas(16) Image {  // static run description, shared by every replica (
   int32_t inst_res[kMaxKinds], inst_off[kMaxKinds + 1], cap[kMaxKinds];
   int32_t w_off[kMaxKinds + 1];  // weight-list capacity per kind (prefix)
   // per-replica arena layout (filled per run by sp_des_run)
-  int32_t inv_cap, seg_cap, heap_cap, log_cap, draw_cap, frames_cap, staging_per_frame;
+  int32_t inv_cap, seg_cap, heap_cap, log_cap, draw_cap, frames_cap, staging_per_frame, ev_cap, pad0;
   int64_t event_cap;
   int32_t buf_off[kMaxOps + 1];  // item buffer of each op (ints)
   int64_t o_lat, o_obs, o_inv, o_next, o_live, o_list, o_seg, o_buf, o_heap, o_wkey, o_wcnt,
@@ -112,6 +112,12 @@ struct HeapEnt {
   int32_t payload;  // complete: iid; wake: iid (timeout) or -(op + 1) (hold)
 };
 
+struct EvRec {  // one BackendSim.trace row (backend.py:207, 243): start / complete / fail
+  double t;
+  int32_t iid;
+  int32_t meta;  // event (0 start, 1 complete, 2 fail) | kind << 2 | instance << 8
+};
+
 struct LogRec {  // one decision_log row (configurator.py:608-618, 746-749)
   double t, slack, obj;
   int32_t iid;
@@ -127,7 +133,7 @@ struct Out {  // per-replica result
   double latency, cost, now;
   int32_t peak_slots, peak_heap;
   int32_t status, met, completed, failures, dups, invocations, terminal, n_spec, n_commit,
-      configs_used, log_len, events;
+      configs_used, log_len, events, ev_len, pad;
 };
 
 struct Sel {
@@ -157,6 +163,7 @@ struct Run {
   const double* draw_factor;  // [draw_cap] exp(N(0, sigma)) per start, or null
   const uint8_t* draw_bits;   // [draw_cap] bit0 straggled, bit1 will_fail, or null
   LogRec* log;
+  EvRec* evlog = nullptr;  // optional event trace (im.ev_cap rows)
   // mutable entry columns lat / cost / cost + penalty: entry g of column c at tab[(c*N + g) * ts]
   // (device: the 32 replicas of a warp interleaved, ts = 32, so converged scans coalesce)
   double* tab;
@@ -191,7 +198,7 @@ struct Run {
   int32_t cq_head[kMaxKinds], cq_tail[kMaxKinds], cq_len[kMaxKinds];
   double total_cost = 0.0, last_accept = 0.0;
   int32_t failures = 0, dups = 0, completed = 0, met = 0, terminal = 0, n_spec = 0, n_commit = 0,
-          log_len = 0, status = kOk;
+          log_len = 0, ev_len = 0, status = kOk;
   int64_t events = 0;
   int32_t lane = 0, nl = 1;  // lanes per run: this lane's index among the run's nl lanes
   uint32_t lmask = 0xffffffffu;  // the run's lanes within the warp
@@ -663,6 +670,7 @@ struct Run {
     v.instance = inst;
     ++running;
     push((now + im.dispatch) + L, 0, id);
+    ev_row(now, id, 0, k, inst);
     // on_start -> _handle_start (manager.py:331-341)
     v.state = kRunning;
     v.started_at = now;
@@ -677,6 +685,11 @@ struct Run {
   }
 
   // ---- speculation (configurator.py:563-637) ------------------------------------------------
+  SPD_HD void ev_row(double t, int id, int what, int k, int inst) {
+    if (evlog && ev_len < im.ev_cap)
+      evlog[ev_len] = EvRec{t, inv[id].iid, what | (k << 2) | ((inst - im.inst_off[k]) << 8)};
+    ++ev_len;
+  }
   SPD_HDN void log_row(int id, int op, int e, bool commit, double slack, double obj) {
     if (log) {
       if (log_len < im.log_cap)
@@ -955,6 +968,7 @@ struct Run {
     const int k = E.kind[g];
     freeres[v.instance] += (int)E.res[g];
     --running;
+    ev_row(t, id, (v.bits & kBitWillFail) ? 2 : 1, k, v.instance);
     try_start(k);  // FIFO successors start before the engine sees the event (backend.py:231)
     const double cost = (E.res[g] * v.actual) * im.price[k];  // invocation_cost (backend.py:61-63)
     total_cost = total_cost + cost;
@@ -1074,6 +1088,7 @@ struct Run {
     }
     o.configs_used = used;
     o.log_len = log_len;
+    o.ev_len = ev_len;
     o.events = (int32_t)events;
   }
 };

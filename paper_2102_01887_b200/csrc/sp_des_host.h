@@ -216,7 +216,7 @@ static inline int64_t align16(int64_t x) { return (x + 15) & ~(int64_t)15; }
 // the trace can push into the op's buffer (every predicate-passing edge, fan-out counts summed
 // over a join's in-edges), invocations <= items * cap_scale.
 inline bool plan_run(HostImage& h, int T, const int32_t* frame_off, const int32_t* attrs,
-                     int draw_cap, int log_cap, std::string& err) {
+                     int draw_cap, int log_cap, std::string& err, int ev_cap = 0) {
   Image& im = h.im;
   const int V = im.n_ops;
   std::vector<int64_t> cap(V, 0), tot(V), mult(V);
@@ -278,6 +278,7 @@ inline bool plan_run(HostImage& h, int T, const int32_t* frame_off, const int32_
   im.frames_cap = frames_cap;
   im.draw_cap = draw_cap;
   im.log_cap = log_cap;
+  im.ev_cap = ev_cap;
   const int K = im.n_kinds, N = im.n_entries;
   int64_t o = 0;
   auto take = [&](int64_t bytes) {

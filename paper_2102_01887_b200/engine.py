@@ -48,9 +48,12 @@ OUT_DTYPE = np.dtype([("latency", "<f8"), ("cost", "<f8"), ("now", "<f8"),
                       ("status", "<i4"), ("met", "<i4"), ("completed", "<i4"),
                       ("failures", "<i4"), ("duplicates", "<i4"), ("invocations", "<i4"),
                       ("terminal_items", "<i4"), ("n_speculate", "<i4"), ("n_commit", "<i4"),
-                      ("configs_used", "<i4"), ("log_len", "<i4"), ("events", "<i4")])
+                      ("configs_used", "<i4"), ("log_len", "<i4"), ("events", "<i4"),
+                      ("event_len", "<i4"), ("pad", "<i4")])
 LOG_DTYPE = np.dtype([("t", "<f8"), ("slack", "<f8"), ("obj", "<f8"), ("iid", "<i4"),
                       ("meta", "<i4")])
+EVENT_DTYPE = np.dtype([("t", "<f8"), ("iid", "<i4"), ("meta", "<i4")])
+_EVENT_KIND = ("start", "complete", "fail")
 
 
 class _Spec(C.Structure):  # sp_des_spec (include/slackpipe_b200.h)
@@ -388,6 +391,7 @@ class RunResult:
     status: int
     log: np.ndarray | None = None
     lat: np.ndarray | None = None
+    events: np.ndarray | None = None
 
     @property
     def slack_met_frac(self) -> float:
@@ -425,7 +429,7 @@ class ReplicaEngine:
             pass
 
     def run(self, traces, targets, seeds=None, *, trace_of=None, log_cap: int = 0,
-            final_tables: bool = False, encoded=None) -> list[RunResult]:
+            final_tables: bool = False, encoded=None, event_cap: int = 0) -> list[RunResult]:
         """Run one replica per target: replica i runs trace ``trace_of[i]`` (default: trace i)
         of ``traces`` (or of ``encoded`` = encode_frames(traces)) with seed ``seeds[i]`` (default:
         the scenario seed, manager.py:240)."""
@@ -443,9 +447,9 @@ class ReplicaEngine:
         todo = np.arange(R)
         scale = self.cap_scale
         while len(todo):
-            out, lg, lat = self._launch(frame_off, attrs, np.ascontiguousarray(trace_of[todo]),
-                                        targets[todo], [seeds[r] for r in todo], scale, log_cap,
-                                        final_tables)
+            out, lg, lat, ev = self._launch(frame_off, attrs, np.ascontiguousarray(trace_of[todo]),
+                                            targets[todo], [seeds[r] for r in todo], scale, log_cap,
+                                            final_tables, event_cap)
             retry = []
             for j, r in enumerate(todo):
                 st = int(out["status"][j])
@@ -465,14 +469,18 @@ class ReplicaEngine:
                     int(o["terminal_items"]), int(o["n_speculate"]) + int(o["n_commit"]),
                     int(o["configs_used"]), st,
                     lg[j, :min(int(o["log_len"]), log_cap)].copy() if lg is not None else None,
-                    lat[j].copy() if lat is not None else None)
+                    lat[j].copy() if lat is not None else None,
+                    ev[j, :min(int(o["event_len"]), event_cap)].copy() if ev is not None else None)
+                if ev is not None and int(o["event_len"]) > event_cap:
+                    raise ValueError(f"event trace of replica {r} has {int(o['event_len'])} rows > event_cap")
                 if lg is not None and int(o["log_len"]) > log_cap:
                     raise ValueError(f"decision log of replica {r} has {int(o['log_len'])} rows > log_cap")
             todo = np.asarray(retry, dtype=np.int64)
             scale *= 2
         return results  # type: ignore[return-value]
 
-    def _launch(self, frame_off, attrs, trace_of, targets, seeds, scale, log_cap, final_tables):
+    def _launch(self, frame_off, attrs, trace_of, targets, seeds, scale, log_cap, final_tables,
+                event_cap=0):
         spec, lib, ctx = self.spec, self.lib, self.ctx
         R = len(targets)
         _lib.check(lib.sp_des_set_capacity(self.handle, float(scale)), "sp_des_set_capacity")
@@ -484,12 +492,13 @@ class ReplicaEngine:
         out = np.zeros(R, dtype=OUT_DTYPE)
         lg = np.zeros((R, log_cap), dtype=LOG_DTYPE) if log_cap else None
         lat = np.zeros((R, int(spec.entry_off[-1])), dtype=np.float64) if final_tables else None
+        ev = np.zeros((R, event_cap), dtype=EVENT_DTYPE) if event_cap else None
         ptr = lambda x: x.ctypes.data if x is not None else None
         _lib.check(lib.sp_des_run(ctx.handle, self.handle, R, len(frame_off) - 1, frame_off.ctypes.data,
                                   ptr(attrs), trace_of.ctypes.data, targets.ctypes.data, draw_cap,
                                   ptr(fac), ptr(bits), int(log_cap), ptr(lg), ptr(lat), out.ctypes.data,
-                                  _lib.SP_MEM_HOST), "sp_des_run")
-        return out, lg, lat
+                                  int(event_cap), ptr(ev), _lib.SP_MEM_HOST), "sp_des_run")
+        return out, lg, lat, ev
 
     # ---- device-resident form (bench `value`): inputs already in HBM, stream-ordered, no sync
     def prepare(self, frame_off: np.ndarray, attrs: np.ndarray, R: int, *, scale: float | None = None) -> int:
@@ -510,7 +519,13 @@ class ReplicaEngine:
             raise ValueError("run_device: scenarios with RNG draws take the host-buffer form")
         _lib.check(self.lib.sp_des_run(self.ctx.handle, self.handle, int(R), int(n_traces), frame_off_ptr,
                                        attrs_ptr, trace_of_ptr, targets_ptr, 0, None, None, 0, None,
-                                       None, out_ptr, _lib.SP_MEM_DEVICE), "sp_des_run")
+                                       None, out_ptr, 0, None, _lib.SP_MEM_DEVICE), "sp_des_run")
+
+    # ---- BackendSim.trace rows in the reference's tuple form (backend.py:207, 243)
+    def event_rows(self, events: np.ndarray) -> list[tuple]:
+        kinds = self.spec.kinds
+        return [(float(ev["t"]), _EVENT_KIND[int(ev["meta"]) & 3], int(ev["iid"]),
+                 kinds[(int(ev["meta"]) >> 2) & 63], int(ev["meta"]) >> 8) for ev in events]
 
     # ---- decision-log rows in the reference's tuple form (configurator.py:650-654, 746-749)
     def log_rows(self, log: np.ndarray) -> list[tuple]:
@@ -589,6 +604,19 @@ def report_of(res: RunResult, *, target_s: float, scenario_name: str, pipeline_n
                      wall_s, flags)
 
 
+class _SimView:
+    """The finished run's backend view: BackendSim.trace and write_trace (backend.py:264-269)."""
+
+    def __init__(self, trace):
+        self.trace = trace
+
+    def write_trace(self, path: str) -> None:
+        with open(path, "w", encoding="utf-8") as fh:
+            fh.write("virtual_time\tevent_kind\tinvocation_id\tbackend\tinstance\n")
+            for t, kind, inv, backend, instance in self.trace:
+                fh.write(f"{t:.9f}\t{kind}\t{inv}\t{backend}\t{instance}\n")
+
+
 class PipelineRun:
     """Drop-in for the reference's PipelineRun (manager.py:210-300): same constructor, the run
     executes on the device."""
@@ -619,10 +647,11 @@ class PipelineRun:
         cap = log_cap if log_cap is not None else 8 * (self.spec.item_bound(fo, at) + 64)
         t0 = time.perf_counter()
         res = eng.run(None, [self.target_s], [self.seed], log_cap=cap, final_tables=True,
-                      encoded=(fo, at))[0]
+                      encoded=(fo, at), event_cap=cap)[0]
         wall = time.perf_counter() - t0
         self.decision_log = eng.log_rows(res.log)
         self.final_latency = res.lat
+        self.sim = _SimView(eng.event_rows(res.events))
         eng.close()
         return report_of(res, target_s=self.target_s, scenario_name=self.scenario.name,
                          pipeline_name=self.pipeline_name, seed=self.seed,

@@ -83,10 +83,15 @@ def lat_digest(lat: np.ndarray) -> str:
     return hashlib.sha256(np.ascontiguousarray(lat, dtype=np.float64).tobytes()).hexdigest()
 
 
-def check(case, rows, report, lat) -> list[str]:
+def check(case, rows, report, lat, events=None) -> list[str]:
     """Mismatches between one engine run and the golden reference run."""
     e = case["expect"]
     bad = []
+    if events is not None and "ev_sha256" in e:
+        if len(events) != e["ev_rows"]:
+            bad.append(f"event rows {len(events)} != {e['ev_rows']}")
+        elif log_digest(events) != e["ev_sha256"]:
+            bad.append("event trace digest")
     if len(rows) != e["log_rows"]:
         bad.append(f"log rows {len(rows)} != {e['log_rows']}")
     got_first = [[repr(float(x)) if isinstance(x, float) else x for x in r] for r in rows[:8]]
@@ -125,13 +130,14 @@ def run_group(make_engine, cases):
     targets = [float(c["target"]) for c in cases]
     seeds = [seed_of(c) for c in cases]
     cap = max(c["expect"]["log_rows"] for c in cases) + 16
-    res = eng.run(traces, targets, seeds, log_cap=cap, final_tables=True)
+    ecap = max(c["expect"].get("ev_rows", 0) for c in cases) + 16
+    res = eng.run(traces, targets, seeds, log_cap=cap, final_tables=True, event_cap=ecap)
     out = []
     for c, r in zip(cases, res):
         rep = report_of(r, target_s=float(c["target"]), scenario_name=spec.scenario.name,
                         pipeline_name=doc.get("name", "pipeline"), seed=seeds[len(out)],
                         ablations=c.get("ablations", []))
-        out.append((eng.log_rows(r.log), rep, r.lat))
+        out.append((eng.log_rows(r.log), rep, r.lat, eng.event_rows(r.events)))
     return out
 
 
@@ -167,7 +173,8 @@ def host_engine_factory(lib):
         def close(self):
             pass
 
-        def _launch(self, frame_off, attrs, trace_of, targets, seeds, scale, log_cap, final_tables):
+        def _launch(self, frame_off, attrs, trace_of, targets, seeds, scale, log_cap, final_tables,
+                    event_cap=0):
             spec = self.spec
             R = len(targets)
             draw_cap, fac, bits = 0, None, None
@@ -177,14 +184,16 @@ def host_engine_factory(lib):
             out = np.zeros(R, dtype=E.OUT_DTYPE)
             lg = np.zeros((R, log_cap), dtype=E.LOG_DTYPE) if log_cap else None
             lat = np.zeros((R, int(spec.entry_off[-1]))) if final_tables else None
+            ev = np.zeros((R, event_cap), dtype=E.EVENT_DTYPE) if event_cap else None
             ptr = lambda x: C.c_void_p(x.ctypes.data) if x is not None else None
             cs = spec.c_spec()
             rc = lib.des_host_run(C.byref(cs), C.c_double(scale), R, len(frame_off) - 1,
                                   ptr(frame_off), ptr(attrs), ptr(trace_of),
                                   ptr(np.ascontiguousarray(targets, dtype=np.float64)), draw_cap,
-                                  ptr(fac), ptr(bits), log_cap, ptr(lg), ptr(lat), ptr(out))
+                                  ptr(fac), ptr(bits), log_cap, ptr(lg), ptr(lat), ptr(out),
+                                  event_cap, ptr(ev))
             if rc:
                 raise ValueError(lib.des_host_error().decode())
-            return out, lg, lat
+            return out, lg, lat, ev
 
     return HostEngine

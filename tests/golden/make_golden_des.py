@@ -6,8 +6,9 @@ Runs the UNMODIFIED reference `PipelineRun.run_to_completion` (manager.py:535-63
 way its CLI builds a run (cli.py:193-222: profiles through MetadataStore, decomposed paths,
 fault overrides), on the three bundled scenarios and on config-4 replicas (SURVEY.md §8(d):
 `generate_trace(3000, 17 + r, {"cars": 0.6, "persons": 0.8}, 3)` at m x 90.41885182994682 s),
-and records per run the decision log (row count + sha256 of its rows in repr form), the report
-(CSV row and fields) and the final latency tables (sha256).  The bundle inputs (pipeline,
+and records per run the decision log (row count + sha256 of its rows in repr form), the backend's
+event trace (BackendSim.trace, same digest), the report (CSV row and fields) and the final latency
+tables (sha256).  The bundle inputs (pipeline,
 scenario, trace) and the profiles the reference's MetadataStore wrote are copied next to it so
 the GPU box, which has no /root/reference, can rebuild every run.  Output: tests/golden/des/.
 """
@@ -131,6 +132,7 @@ def main() -> None:
             invocations=rep.invocations, completed=rep.completed, terminal_items=rep.terminal_items,
             decision_count=rep.decision_count,
             lat_sha256=lat_digest([run.tables[o].lat for o in sorted(run.tables)]),
+            ev_rows=len(run.sim.trace), ev_sha256=log_digest(run.sim.trace),
             first_rows=[[repr(float(x)) if isinstance(x, float) else x for x in r] for r in rows[:8]],
         )
         runs.append(c)

@@ -19,11 +19,12 @@ extern "C" int des_host_run(const sp_des_spec* spec, double cap_scale, int32_t R
                             const int32_t* frame_off, const int32_t* attrs, const int32_t* trace_of,
                             const double* target_s,
                             int32_t draw_cap, const double* draw_factor, const uint8_t* draw_bits,
-                            int32_t log_cap, sp_des_log* log, double* lat_out, sp_des_out* out) {
+                            int32_t log_cap, sp_des_log* log, double* lat_out, sp_des_out* out,
+                            int32_t ev_cap, sp_des_event* events) {
   HostImage h;
   h.cap_scale = cap_scale;
   if (!build_image(*spec, h, g_err)) return -1;
-  if (!plan_run(h, T, frame_off, attrs, draw_cap, log_cap, g_err)) return -1;
+  if (!plan_run(h, T, frame_off, attrs, draw_cap, log_cap, g_err, ev_cap)) return -1;
   const Image& im = h.im;
   std::vector<char> arena((size_t)im.arena_bytes + 16);
   char* base = (char*)(((uintptr_t)arena.data() + 15) & ~(uintptr_t)15);
@@ -35,6 +36,7 @@ extern "C" int des_host_run(const sp_des_spec* spec, double cap_scale, int32_t R
             draw_factor ? draw_factor + (size_t)r * draw_cap : nullptr,
             draw_bits ? draw_bits + (size_t)r * draw_cap : nullptr,
             log ? reinterpret_cast<LogRec*>(log) + (size_t)r * log_cap : nullptr);
+    if (events) run.evlog = reinterpret_cast<EvRec*>(events) + (size_t)r * ev_cap;
     run.run();
     run.write_out(*reinterpret_cast<Out*>(out + r));
     if (lat_out)

@@ -21,9 +21,9 @@ def test_host_engine_matches_golden_runs(host_engine):
     bad = []
     n = 0
     for group in dc.groups(dc.runs()):
-        for case, (rows, rep, lat) in zip(group, dc.run_group(host_engine, group)):
+        for case, (rows, rep, lat, ev) in zip(group, dc.run_group(host_engine, group)):
             n += 1
-            errs = dc.check(case, rows, rep, lat)
+            errs = dc.check(case, rows, rep, lat, ev)
             if errs:
                 bad.append((case["bundle"], case["target"], case.get("ablations"), errs[:3]))
     assert n == 69

@@ -32,9 +32,9 @@ def test_device_engine_matches_golden_runs(device_engine, gpu_ctx, mode):
         return eng
 
     for group in dc.groups(dc.runs()):
-        for case, (rows, rep, lat) in zip(group, dc.run_group(make, group)):
+        for case, (rows, rep, lat, ev) in zip(group, dc.run_group(make, group)):
             n += 1
-            errs = dc.check(case, rows, rep, lat)
+            errs = dc.check(case, rows, rep, lat, ev)
             if errs:
                 bad.append((case["bundle"], case["target"], case.get("ablations"), errs[:3]))
     assert n == 69
@@ -55,6 +55,9 @@ def test_pipeline_run_dropin_csv_row(gpu_ctx, tmp_path):
     assert dc.log_digest(run.decision_log) == case["expect"]["log_sha256"]
     run.write_decision_log(str(tmp_path / "log.tsv"))
     assert sum(1 for _ in open(tmp_path / "log.tsv")) == case["expect"]["log_rows"] + 1
+    assert dc.log_digest(run.sim.trace) == case["expect"]["ev_sha256"]
+    run.sim.write_trace(str(tmp_path / "events.tsv"))
+    assert sum(1 for _ in open(tmp_path / "events.tsv")) == case["expect"]["ev_rows"] + 1
 
 
 def test_device_engine_random_cases_vs_oracle(device_engine):
