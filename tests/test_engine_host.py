@@ -7,6 +7,7 @@ reference on fresh random cases in the build container.  The device kernel runs 
 (tests/test_gpu_engine.py)."""
 from __future__ import annotations
 
+import numpy as np
 import pytest
 
 import des_cases as dc
@@ -44,3 +45,50 @@ def test_host_engine_capacity_retry(host_engine):
     rep = report_of(res, target_s=float(case["target"]), scenario_name=spec.scenario.name,
                     pipeline_name="x", seed=dc.seed_of(case), ablations=())
     assert not dc.check(case, eng.log_rows(res.log), rep, res.lat)
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3, 4, 5, 6])
+def test_host_engine_matches_live_reference_random(ref, host_engine, seed):
+    """Fresh random AMBER runs (trace, target, ablations, noise / straggle / failure, profile
+    scale) of the live reference engine (build container only) against the engine source."""
+    import json
+    import tempfile
+
+    from slackpipe import cli, manager, pipeline, profiler, workload
+    from slackpipe import scenario as scn
+    from paper_2102_01887_b200.engine import RunSpec, TuningParams, report_of
+
+    rng = np.random.default_rng(seed)
+    base = "/root/reference/pkg/scenarios/branching"
+    doc = json.load(open(base + "/pipeline.json"))
+    dag, ops = pipeline.load_pipeline(doc)
+    sc = scn.load_scenario(base + "/scenario.json")
+    store = profiler.MetadataStore(tempfile.mkdtemp())
+    profiles, _ = cli._ensure_profiles(store, ops, sc, sc.tuning.samples_per_config)
+    paths = cli._paths_for(store, doc, dag)
+    frames = workload.generate_trace(int(rng.integers(200, 700)), seed + 100,
+                                     {"cars": float(rng.uniform(0.2, 1.5)), "persons": float(rng.uniform(0.2, 1.5))}, 4)
+    abl = [a for a in ("fb", "dfp", "sdb", "eslc", "pbc") if rng.random() < 0.25]
+    faults = dict(noise_sigma=float(rng.choice([0.0, 0.25])), failure_rate=float(rng.choice([0.0, 0.05])),
+                  straggle_rate=float(rng.choice([0.0, 0.05])), straggle_factor=3.0)
+    rs = sc.with_fault_overrides(**faults)
+    target = float(rng.uniform(5.0, 60.0))
+    scale = float(rng.choice([1.0, 0.8, 1.3]))
+    tp = cli._tuning_params(rs, None)
+    run = manager.PipelineRun(dag, ops, profiles, frames, rs, target, tp, ablations=frozenset(abl),
+                              seed=seed, paths=paths, profile_scale=scale)
+    want = run.run_to_completion()
+    spec = RunSpec(dag, profiles, rs, TuningParams(tp.alpha, tp.cq_capacity, tp.dfp_count,
+                                                   tp.straggler_timeout_factor, tp.smoothing_beta),
+                   ablations=abl, paths=paths, profile_scale=scale)
+    eng = host_engine(spec)
+    res = eng.run([frames], [target], [seed], log_cap=len(run.configurator.decision_log) + 16,
+                  final_tables=True, event_cap=len(run.sim.trace) + 16)[0]
+    assert dc.log_digest(eng.log_rows(res.log)) == dc.log_digest(run.configurator.decision_log)
+    assert dc.log_digest(eng.event_rows(res.events)) == dc.log_digest(run.sim.trace)
+    got = report_of(res, target_s=target, scenario_name=rs.name, pipeline_name="x", seed=seed)
+    for f in ("latency_s", "cost", "slack_met_frac", "configs_used", "failures", "duplicates",
+              "invocations", "completed", "terminal_items", "decision_count"):
+        assert repr(float(getattr(got, f))) == repr(float(getattr(want, f))), f
+    lat = np.concatenate([run.tables[o].lat for o in sorted(run.tables)])
+    assert np.array_equal(lat.view(np.uint64), res.lat.view(np.uint64))
