@@ -481,6 +481,13 @@ int sp_des_set_capacity(sp_des* des, double invocations_per_item);
  * latency per run), 4 / 8 / 16 = that many lanes per replica (32 / n replicas per warp),
  * 0 = default (32 lanes below 2,048 replicas, 8 below 32,768, else 4).  Results are identical. */
 int sp_des_set_mode(sp_des* des, int32_t mode);
+/* The reference's per-start RNG draws of R runs (host, no GPU needed): replica r's numpy PCG64
+ * state (state hi, lo, inc hi, lo in pcg_state[4r..4r+3], as default_rng(seed) sets it) and, per
+ * start k < cap, in the reference's order (backend.py:52-57, 186): factor[r*cap+k] =
+ * math.exp(rng.normal(0, noise_sigma)) (1 when noise_sigma is 0), bits[r*cap+k] bit 0 = straggled,
+ * bit 1 = will fail.  Same bits as numpy + CPython. */
+int sp_des_draws(int32_t R, const uint64_t* pcg_state, int32_t cap, double noise_sigma,
+                 double straggle_rate, double failure_rate, double* factor, uint8_t* bits);
 /* Bytes of one replica's arena as last prepared. */
 int64_t sp_des_arena_bytes(sp_des* des);
 

@@ -20,7 +20,7 @@ BUILD = ROOT / "build" / "csrc"
 LIB = PKG / "libslackpipe_b200.so"
 
 SOURCES = ["sp_api.cu", "sp_plan.cu", "sp_select.cu", "sp_slack.cu", "sp_fold.cu", "sp_commit.cu",
-           "sp_quantile.cu", "sp_group.cu", "sp_plan_cluster.cu", "sp_backend.cu", "sp_profile.cu", "sp_des.cu"]
+           "sp_quantile.cu", "sp_group.cu", "sp_plan_cluster.cu", "sp_backend.cu", "sp_profile.cu", "sp_des.cu", "sp_rng.cu"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -103,6 +103,7 @@ SIGNATURES = {
     "sp_des_set_capacity": (C.c_int, [_p, _d]),
     "sp_des_set_mode": (C.c_int, [_p, _i32]),
     "sp_des_arena_bytes": (_i64, [_p]),
+    "sp_des_draws": (C.c_int, [_i32, _p, _i32, _d, _d, _d, _p, _p]),
     "sp_des_run": (C.c_int, [_p, _p, _i32, _i32, _p, _p, _p, _p, _i32, _p, _p, _i32, _p, _p, _p, _i32,
                              _p, _i32]),
     "sp_group_create": (C.c_int, [_i32, _p, _pp]),

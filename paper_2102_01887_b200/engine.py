@@ -349,30 +349,23 @@ class RunSpec:
         return int(per.sum(axis=0).max()) if per.size else 0
 
     def draws_for(self, seeds: Sequence[int], cap: int):
-        """The reference's per-start RNG draws (backend.py:52-57, 186) of each replica's
-        numpy Generator, in stream order: exp(N(0, sigma)) through CPython's math.exp, then the
-        straggle and failure Bernoulli draws."""
+        """The reference's per-start RNG draws (backend.py:52-57, 186) of each replica's numpy
+        Generator, in stream order: exp(N(0, sigma)) (CPython's math.exp), then the straggle and
+        failure Bernoulli draws — generated by sp_des_draws (PCG64 + numpy's ziggurat in C, host
+        threads)."""
         R = len(seeds)
         fac = np.ones((R, cap), dtype=np.float64) if self.draws & DRAW_NOISE else None
         bits = np.zeros((R, cap), dtype=np.uint8) if self.draws & (DRAW_STRAGGLE | DRAW_FAIL) else None
-        sig, sr, fr = self.noise_sigma, self.straggle_rate, self.failure_rate
+        st = np.empty((R, 4), dtype=np.uint64)
+        m64 = (1 << 64) - 1
         for r, seed in enumerate(seeds):
-            rng = np.random.default_rng(seed)
-            if self.draws == DRAW_NOISE:  # one normal per start: the vectorised stream is the same
-                fac[r] = [math.exp(x) for x in rng.normal(0.0, sig, size=cap)]
-                continue
-            fr_row = fac[r] if fac is not None else None
-            br = bits[r] if bits is not None else None
-            for k in range(cap):
-                if sig > 0.0:
-                    fr_row[k] = math.exp(rng.normal(0.0, sig))
-                b = 0
-                if sr > 0.0 and rng.random() < sr:
-                    b |= 1
-                if fr > 0.0 and rng.random() < fr:
-                    b |= 2
-                if br is not None:
-                    br[k] = b
+            s = np.random.default_rng(seed).bit_generator.state["state"]
+            st[r] = (s["state"] >> 64, s["state"] & m64, s["inc"] >> 64, s["inc"] & m64)
+        lib = _lib.load_library()
+        ptr = lambda x: x.ctypes.data if x is not None else None
+        _lib.check(lib.sp_des_draws(R, st.ctypes.data, int(cap), float(self.noise_sigma),
+                                    float(self.straggle_rate), float(self.failure_rate), ptr(fac),
+                                    ptr(bits)), "sp_des_draws")
         return fac, bits
 
 
