@@ -1202,7 +1202,8 @@ def _c4runs_cpu_worker(a):
                               params.straggler_timeout_factor, params.smoothing_beta), seed=sc.seed,
                     paths=paths)
     rep = eng.run()
-    return rep.decision_count
+    return (rep.decision_count, repr(float(rep.cost)), repr(float(rep.latency_s)), rep.invocations,
+            rep.completed)
 
 
 def run_c4runs(args):
@@ -1299,6 +1300,7 @@ def run_c4runs(args):
     if rank != 0:
         return
     cpu = None
+    oracle_parity = None
     if world == 1 and not args.no_cpu_baseline:
         cores = os.cpu_count() or 1
         sample = [(r, m) for r in range(max(1, cores)) for m in (mults[r % 5],)]
@@ -1307,6 +1309,17 @@ def run_c4runs(args):
             c0 = time.perf_counter()
             decs = pool.map(_c4runs_cpu_worker, sample)
             cs = time.perf_counter() - c0
+        # the CPU sample doubles as a parity check of the timed device step (replicas 0..cores-1)
+        omis = 0
+        for (r, m), (dn, cost, lat, ninv, ncomp) in zip(sample, decs):
+            o = out[r * len(mults) + mults.index(m)]
+            omis += (int(o["n_speculate"] + o["n_commit"]) != dn or repr(float(o["cost"])) != cost
+                     or repr(float(o["latency"])) != lat or int(o["invocations"]) != ninv
+                     or int(o["completed"]) != ncomp)
+        oracle_parity = {"runs": len(sample), "mismatches": omis,
+                         "fields": "decision count, cost, latency, invocations, completions of the "
+                                   "timed step vs oracle/engine.py"}
+        decs = [x[0] for x in decs]
         cpu = {"value": len(sample) / cs, "unit": "runs/s", "cores": cores, "kind": "port",
                "decisions_per_s": sum(decs) / cs,
                "sample": f"{len(sample)} complete runs (replicas 0..{len(sample) - 1}, one target each) "
@@ -1336,6 +1349,7 @@ def run_c4runs(args):
         "gpu_launches": launches,
         "step_ms": {"median": statistics.median(ms), "min": min(ms), "max": max(ms)},
         "parity": {"runs": len(gold), "mismatches": bad[1], "bad_status": bad[0],
+                   "oracle_sample": oracle_parity if cpu is not None else None,
                    "result": ("bit-identical decision logs / reports / final tables vs the reference's own runs"
                               if bad[1] == 0 and bad[0] == 0 else "MISMATCH"),
                    "checked_on": "replicas 0-7 x 5 targets (tests/golden/des/runs.json)"},
