@@ -238,7 +238,7 @@ struct Run {
   SPD_HD double costpen(int g) const { return tab[(size_t)(2 * im.n_entries + g) * ts]; }
   // OpTable.set_latency (configurator.py:211-213) + the Eq. 1 terms of the entry in numpy's order
   // (configurator.py:224-225): score = lat < slack ? cost + 0.0 : cost + penalty
-  SPD_HD void set_lat(int g, double L) {
+  SPD_HDN void set_lat(int g, double L) {
     const double R = E.res[g], B = E.batch[g];
     const double c = ((R * L) * E.price[g]) / B;
     const double pen = im.alpha * ((L * R) / (B * E.pool[g]));
@@ -253,27 +253,35 @@ struct Run {
 
   // ---- initial state (manager.py:210-300, configurator.py:375-438) --------------------------
   SPD_HDN void init() {
+    #pragma unroll 1
     for (int k = 0; k < kMaxKinds; ++k) {
       kver[k] = 0;
       qver[k] = -1;
     }
+    #pragma unroll 1
     for (int i = 0; i < im.n_entries; ++i) {
       set_lat(i, E.lat0[i]);
       observed[i] = 0;
     }
+    #pragma unroll 1
     for (int o = 0; o < im.n_ops; ++o) {
+      #pragma unroll 1
       for (int f = 0; f < kOpiN; ++f) OP(o, f) = 0;
       OP(o, kOpiSqHead) = OP(o, kOpiSqTail) = -1;
       scver[o] = -1;
       rver[o] = -1;
     }
+    #pragma unroll 1
     for (int k = 0; k < im.n_kinds; ++k) {
       wn[0][k] = wn[1][k] = 0;
       cq_head[k] = cq_tail[k] = -1;
       cq_len[k] = 0;
+      #pragma unroll 1
       for (int i = im.inst_off[k]; i < im.inst_off[k + 1]; ++i) freeres[i] = im.inst_res[k];
     }
+    #pragma unroll 1
     for (int64_t i = 0; i < (int64_t)n_frames * im.staging_per_frame; ++i) staging[i] = 0;
+    #pragma unroll 1
     for (int i = 0; i < (im.n_cfg + 31) / 32; ++i) cfg_used[i] = 0;
   }
 
@@ -290,6 +298,7 @@ struct Run {
     HeapEnt x{t, ((uint32_t)code << 31) | (uint32_t)seq, payload};
     int i = heap_n++;
     if (heap_n > peak_heap) peak_heap = heap_n;
+    #pragma unroll 1
     while (i > 0) {
       const int p = (i - 1) >> 1;
       if (!less(x, heap[p])) break;
@@ -302,6 +311,7 @@ struct Run {
     HeapEnt top = heap[0];
     const HeapEnt x = heap[--heap_n];
     int i = 0;
+    #pragma unroll 1
     for (;;) {
       int c = 2 * i + 1;
       if (c >= heap_n) break;
@@ -325,12 +335,14 @@ struct Run {
     int32_t* cnt = wcnt + q * im.w_off[im.n_kinds] + base;
     const int32_t kk = (op << 16) | e;
     int n = wn[q][k], i = 0;
+    #pragma unroll 1
     while (i < n && key[i] != kk) ++i;
     if (i < n) {
       const int32_t nv = cnt[i] + d;
       if (nv) {
         cnt[i] = nv;
       } else {  // m.pop(key): later keys keep their order
+        #pragma unroll 1
         for (int j = i + 1; j < n; ++j) {
           key[j - 1] = key[j];
           cnt[j - 1] = cnt[j];
@@ -364,9 +376,11 @@ struct Run {
       double lo = 0.0, hi = 0.0;
       bool plain = true;
       int nr = 0;
+      #pragma unroll 1
       for (int p = im.suf_off[op]; p < im.suf_off[op + 1]; ++nr) {
         const int len = E.suf[p++];
         double tot = 0.0;
+        #pragma unroll 1
         for (int j = 0; j < len; ++j) tot = tot + ref_lat(E.suf[p + j]);
         p += len;
         const double r = own / tot;
@@ -379,12 +393,15 @@ struct Run {
       rver[op] = ref_version;
     }
     const int wtot = im.w_off[K];
+    #pragma unroll 1
     for (int k = 0; k < K; ++k) {
       if (qver[k] != kver[k]) {  // queueing_by_kind (configurator.py:511-524)
         double tot = 0.0;
+        #pragma unroll 1
         for (int q = 0; q < 2; ++q) {
           const int32_t* key = wkey + q * wtot + im.w_off[k];
           const int32_t* cnt = wcnt + q * wtot + im.w_off[k];
+          #pragma unroll 1
           for (int i = 0; i < wn[q][k]; ++i) {
             const int o = key[i] >> 16, e = key[i] & 0xffff;
             const int g = im.entry_off[o] + e;
@@ -401,9 +418,11 @@ struct Run {
         const double own = ref_lat(op);
         double sl = 0.0;
         int j = 0;
+        #pragma unroll 1
         for (int p = im.suf_off[op]; p < im.suf_off[op + 1]; ++j) {
           const int len = E.suf[p++];
           double tot = 0.0;
+          #pragma unroll 1
           for (int i = 0; i < len; ++i) tot = tot + ref_lat(E.suf[p + i]);
           p += len;
           const double v = (own / tot) * budget;
@@ -472,6 +491,7 @@ struct Run {
     int best = -1, best2 = -1;
     double bs = 0, bc = 0, bs2 = 0, bc2 = 0;
     bool bad = false;
+    #pragma unroll 1
     for (int g = b0 + lane; g < b1; g += nl) {
       if ((excl >> E.kind[g]) & 1u) continue;
       if (min_batch > 1 && E.bint[g] < min_batch) continue;
@@ -528,6 +548,7 @@ struct Run {
     const int b0 = im.entry_off[op], b1 = im.entry_off[op + 1];
     double mon = INFINITY, moff = INFINITY;
     bool any_on = false, any_off = false, bad = false;
+    #pragma unroll 1
     for (int g = b0 + lane; g < b1; g += nl) {
       double s, c;
       score_of(g, sl, s, c);
@@ -613,6 +634,7 @@ struct Run {
     if (v.state < kCompleted || (v.bits & kBitWakePending)) return;
     if (v.unit == id) {
       if (!(v.bits & kBitResolved) || live[id] != 0) return;
+      #pragma unroll 1
       for (int sg = lists[id].first; sg >= 0; sg = segs[sg].next) free_seg[n_free_seg++] = sg;
     }
     inv[id].state = kPending;  // poisoned: never finished again until reused
@@ -634,11 +656,13 @@ struct Run {
     try_start(k);
   }
   SPD_HDN void try_start(int k) {
+    #pragma unroll 1
     while (cq_head[k] >= 0 && status == kOk) {
       const int id = cq_head[k];
       const int g = im.entry_off[inv[id].op] + inv[id].com_e;
       const int need = (int)E.res[g];
       int inst = -1;
+      #pragma unroll 1
       for (int i = im.inst_off[k]; i < im.inst_off[k + 1]; ++i)
         if (freeres[i] >= need) {
           inst = i;
@@ -685,7 +709,7 @@ struct Run {
   }
 
   // ---- speculation (configurator.py:563-637) ------------------------------------------------
-  SPD_HD void ev_row(double t, int id, int what, int k, int inst) {
+  SPD_HDN void ev_row(double t, int id, int what, int k, int inst) {
     if (evlog && ev_len < im.ev_cap)
       evlog[ev_len] = EvRec{t, inv[id].iid, what | (k << 2) | ((inst - im.inst_off[k]) << 8)};
     ++ev_len;
@@ -717,6 +741,7 @@ struct Run {
   SPD_HDN int speculate_buffer(int op) {
     int formed = 0;
     const int ri = im.ref_index[op];
+    #pragma unroll 1
     while (buf_len(op) > 0 && status == kOk) {
       const bool forced = !(im.abl & kAblDfp) && ri >= 0 && OP(op, kOpiCompletedRef) < im.dfp_count;
       const double* sl = slacks(op);
@@ -771,9 +796,10 @@ struct Run {
     enqueue_spec(id, d.e, d.slack, d.obj);
     ++n_spec;
   }
-  SPD_HD int supply(int op) {  // manager.py:301-305
+  SPD_HDN int supply(int op) {  // manager.py:301-305
     int s = 0;
     const uint32_t m = im.anc_mask[op];
+    #pragma unroll 1
     for (int a = 0; a < im.n_ops; ++a)
       if ((m >> a) & 1u) s += OP(a, kOpiUnspawned);
     return s;
@@ -795,13 +821,16 @@ struct Run {
     int committed = 0;
     const bool fifo = im.abl & kAblPbc;
     const bool eslc = im.abl & kAblEslc;
+    #pragma unroll 1
     while (status == kOk) {
       uint32_t full = 0;
+      #pragma unroll 1
       for (int k = 0; k < im.n_kinds; ++k)
         if (cq_len[k] >= im.cap[k]) full |= 1u << k;
       int bop = -1, be = -1, bfill = 0;
       double bslack = 0.0, bobj = 0.0;
       Key bkey{0, 0.0, 0.0, 0};
+      #pragma unroll 1
       for (int op = 0; op < im.n_ops; ++op) {
         const int head = OP(op, kOpiSqHead);
         if (head < 0) continue;
@@ -881,8 +910,10 @@ struct Run {
 
   // ---- run engine (manager.py:356-575) -------------------------------------------------------
   SPD_HDN void pump() {
+    #pragma unroll 1
     while (status == kOk) {
       int formed = 0;
+      #pragma unroll 1
       for (int j = 0; j < im.n_ops; ++j) {
         const int op = im.deep_first[j];
         if (buf_len(op) > 0) {
@@ -902,6 +933,7 @@ struct Run {
       return;
     }
     int32_t* b = items + im.buf_off[dst];
+    #pragma unroll 1
     for (int i = 0; i < n; ++i) b[tail + i] = frame;
     tail += n;
     OP(dst, kOpiUnspawned) += n;
@@ -915,10 +947,13 @@ struct Run {
       return;
     }
     const int32_t* src = items + im.buf_off[op];
+    #pragma unroll 1
     for (int s = L.first; s >= 0; s = segs[s].next) {
+      #pragma unroll 1
       for (int j = 0; j < segs[s].n; ++j) {
         const int fr = src[segs[s].pos + j];
         const int32_t* at = attrs + (int64_t)fr * im.n_attrs;
+        #pragma unroll 1
         for (int q = im.succ_off[op]; q < im.succ_off[op + 1]; ++q) {
           const int dst = im.succ[q];
           if (im.pred_attr[q] >= 0 && !pred_eval(im.pred_cmp[q], at[im.pred_attr[q]], im.pred_val[q]))
@@ -929,8 +964,10 @@ struct Run {
             int32_t* st = staging + ((int64_t)fr * im.staging_per_frame + im.join_base[dst]);
             st[im.join_pos[q]] += n;
             int m = st[0];
+            #pragma unroll 1
             for (int p = 1; p < im.indeg[dst]; ++p) m = st[p] < m ? st[p] : m;
             if (m > 0) {
+              #pragma unroll 1
               for (int p = 0; p < im.indeg[dst]; ++p) st[p] -= m;
               append_items(dst, fr, m);
             }
@@ -956,6 +993,7 @@ struct Run {
       const double init = E.lat_init[g];  // recalibrate_unobserved (configurator.py:470-491)
       if (init > 0.0) {
         const double ratio = lat(g) / init;
+        #pragma unroll 1
         for (int j = im.entry_off[op]; j < im.entry_off[op + 1]; ++j)
           if (j != g && !observed[j]) set_lat(j, E.lat_init[j] * ratio);
         ++version;
@@ -1009,29 +1047,36 @@ struct Run {
     }
   }
   SPD_HDN bool work_remains() {  // manager.py:526-533
+    #pragma unroll 1
     for (int o = 0; o < im.n_ops; ++o)
       if (buf_len(o) > 0 || OP(o, kOpiSqLen) > 0) return true;
+    #pragma unroll 1
     for (int k = 0; k < im.n_kinds; ++k)
       if (cq_len[k] > 0) return true;
     return running > 0;
   }
   SPD_HDN void run() {  // start_run + run_to_completion (manager.py:535-575)
     init();
+    #pragma unroll 1
     for (int j = 0; j < im.n_inputs; ++j) {
       const int v = im.inputs[j];
+      #pragma unroll 1
       for (int f = 0; f < n_frames; ++f) items[im.buf_off[v] + f] = f;
       OP(v, kOpiBufTail) = n_frames;
       OP(v, kOpiUnspawned) += n_frames;
     }
     pump();
     bool flushed = false;
+    #pragma unroll 1
     while (status == kOk) {
       if (heap_n == 0) {
         if (!work_remains()) break;
         bool any_hold = false;
+        #pragma unroll 1
         for (int o = 0; o < im.n_ops; ++o) any_hold |= OP(o, kOpiHold) != 0;
         if (!flushed && any_hold) {
           flushed = true;
+          #pragma unroll 1
           for (int o = 0; o < im.n_ops; ++o)
             if (OP(o, kOpiHold)) holddl[o] = now;
           pump();
@@ -1079,8 +1124,10 @@ struct Run {
     o.n_spec = n_spec;
     o.n_commit = n_commit;
     int used = 0;
+    #pragma unroll 1
     for (int i = 0; i < (im.n_cfg + 31) / 32; ++i) {
       uint32_t w = cfg_used[i];
+      #pragma unroll 1
       while (w) {
         used += w & 1u;
         w >>= 1;
