@@ -33,10 +33,10 @@
 
 namespace spdes {
 
-constexpr int kMaxOps = 32;
+constexpr int kMaxOps = 64;
 constexpr int kMaxKinds = 16;
-constexpr int kMaxEdges = 128;
-constexpr int kMaxSuffixInts = 2048;
+constexpr int kMaxEdges = 512;
+constexpr int kMaxSuffixInts = 1 << 22;  // path-suffix ints (kept with the entry columns)
 
 // ablation bits (configurator.py:23)
 constexpr int kAblFb = 1, kAblDfp = 2, kAblSdb = 4, kAblEslc = 8, kAblPbc = 16;
@@ -65,7 +65,7 @@ struct alignas(16) Image {  // static run description, shared by every replica (
   int32_t ref_index[kMaxOps];
   double ref_lat0[kMaxOps];
   int32_t depth[kMaxOps], deep_first[kMaxOps], indeg[kMaxOps];
-  uint32_t anc_mask[kMaxOps];
+  uint64_t anc_mask[kMaxOps];
   int32_t succ_off[kMaxOps + 1];
   int32_t succ[kMaxEdges];
   int32_t pred_attr[kMaxEdges], pred_cmp[kMaxEdges], pred_val[kMaxEdges];  // per succ slot
@@ -798,7 +798,7 @@ struct Run {
   }
   SPD_HDN int supply(int op) {  // manager.py:301-305
     int s = 0;
-    const uint32_t m = im.anc_mask[op];
+    const uint64_t m = im.anc_mask[op];
     #pragma unroll 1
     for (int a = 0; a < im.n_ops; ++a)
       if ((m >> a) & 1u) s += OP(a, kOpiUnspawned);

@@ -50,7 +50,7 @@ inline bool build_image(const sp_des_spec& s, HostImage& h, std::string& err) {
   Image& im = h.im;
   std::memset(&im, 0, sizeof(im));
   const int V = s.n_ops, K = s.n_kinds, N = s.n_entries;
-  if (V < 1 || V > kMaxOps) return err = "run engine: 1..32 operations", false;
+  if (V < 1 || V > kMaxOps) return err = "run engine: 1..64 operations", false;
   if (K < 1 || K > kMaxKinds) return err = "run engine: 1..16 backend kinds", false;
   if (N < 1 || s.n_attrs < 0 || s.n_cfg_ids < 1) return err = "run engine: bad sizes", false;
   if (!s.entry_off || !s.lat || !s.lat_init || !s.res || !s.batch || !s.kind || !s.id_rank ||
@@ -59,7 +59,7 @@ inline bool build_image(const sp_des_spec& s, HostImage& h, std::string& err) {
       !s.inst_resources || !s.price || !s.cq_capacity)
     return err = "run engine: missing spec array", false;
   const int n_edges = s.succ_off[V];
-  if (n_edges < 0 || n_edges > kMaxEdges) return err = "run engine: at most 128 edges", false;
+  if (n_edges < 0 || n_edges > kMaxEdges) return err = "run engine: at most 512 edges", false;
   if (n_edges > 0 && (!s.succ || !s.pred_attr || !s.pred_cmp || !s.pred_value))
     return err = "run engine: missing edge arrays", false;
   if (s.entry_off[0] != 0 || s.entry_off[V] != N) return err = "run engine: bad entry_off", false;
@@ -118,8 +118,8 @@ inline bool build_image(const sp_des_spec& s, HostImage& h, std::string& err) {
       im.depth[s.succ[q]] = std::max(im.depth[s.succ[q]], im.depth[v] + 1);
   // ancestors (pipeline.py:339-347) as bit masks, in topological order
   for (int v : order) {
-    uint32_t m = 0;
-    for (int p : preds[v]) m |= (1u << p) | im.anc_mask[p];
+    uint64_t m = 0;
+    for (int p : preds[v]) m |= (1ull << p) | im.anc_mask[p];
     im.anc_mask[v] = m;
   }
   // deep-first op order (manager.py:271): (-depth, name); ops are in name order
@@ -151,7 +151,7 @@ inline bool build_image(const sp_des_spec& s, HostImage& h, std::string& err) {
     }
   // suffixes (configurator.py:413-420)
   const int nsuf = s.suffix_off[V];
-  if (nsuf > kMaxSuffixInts) return err = "run engine: path suffixes exceed 2048 ints", false;
+  if (nsuf > kMaxSuffixInts) return err = "run engine: path suffixes exceed 4M ints", false;
   for (int o = 0; o <= V; ++o) im.suf_off[o] = s.suffix_off[o];
   for (int o = 0; o < V; ++o) {
     int cnt = 0;

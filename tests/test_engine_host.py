@@ -92,3 +92,58 @@ def test_host_engine_matches_live_reference_random(ref, host_engine, seed):
         assert repr(float(getattr(got, f))) == repr(float(getattr(want, f))), f
     lat = np.concatenate([run.tables[o].lat for o in sorted(run.tables)])
     assert np.array_equal(lat.view(np.uint64), res.lat.view(np.uint64))
+
+
+def _wide_pipeline(n_ops: int, seed: int):
+    """A synthetic pipeline of n_ops operations (chain + skip edges + one join + a predicate /
+    fan-out branch), two backend kinds, hand-made profiles and ground truth."""
+    from paper_2102_01887_b200.pipeline import BranchPredicate, ConfigEntry, ConfigSpec, PipelineDag
+    from paper_2102_01887_b200.scenario import BackendSpec, GroundTruthModel, OpKindTruth, Scenario
+
+    rng = np.random.default_rng(seed)
+    ops = [f"s{i:02d}" for i in range(n_ops)]
+    edges = [(ops[i], ops[i + 1]) for i in range(n_ops - 1)]
+    edges += [(ops[3], ops[9]), (ops[12], ops[n_ops - 5])]  # skips (ops 9 / n-5 become joins)
+    edges += [(ops[6], "br")]
+    ops.append("br")
+    preds = {(ops[6], "br"): BranchPredicate("persons", ">", 0)}
+    dag = PipelineDag(vertices=tuple(ops), edges=tuple(edges), branch_predicates=preds,
+                      fanout_rules={"br": "persons"})
+    profiles, truth = {}, {}
+    for op in ops:
+        ents = []
+        for kind, res_opts, bs in (("cpu", (1, 2, 4), (1, 4)), ("gpu", (4, 8), (1, 8))):
+            for r in res_opts:
+                for b in bs:
+                    lat = float(rng.uniform(0.05, 2.0)) * (b ** 0.7) / (r ** 0.3)
+                    ents.append(ConfigEntry(f"{kind}-r{r}-b{b}", kind, {}, b, r, lat, lat))
+        profiles[op] = ConfigSpec(op, ents, "cpu-r1-b1")
+        truth[op] = {"cpu": OpKindTruth(float(rng.uniform(0.1, 1.0)), 1, 0.3, 0.8, 0.01),
+                     "gpu": OpKindTruth(float(rng.uniform(0.02, 0.2)), 4, 0.2, 0.4, 0.001)}
+    sc = Scenario("wide", (BackendSpec("cpu", 8, 4, 1.32e-5), BackendSpec("gpu", 2, 8, 9e-4)),
+                  GroundTruthModel(truth, noise_sigma=0.2, failure_rate=0.02), 11)
+    frames = [(i, {"persons": int(x)}) for i, x in enumerate(rng.poisson(0.7, size=120))]
+    return dag, profiles, sc, frames
+
+
+@pytest.mark.parametrize("n_ops", [40, 63])
+def test_host_engine_many_operations_vs_oracle(host_engine, n_ops):
+    """Pipelines beyond the bundled 7 operations (up to 64 — ancestors as a 64-bit mask), with
+    joins, a predicate / fan-out branch, noise and failures, against oracle/engine.py."""
+    from oracle import engine as oe
+    from paper_2102_01887_b200.engine import RunSpec, TuningParams, _paths, report_of
+
+    dag, profiles, sc, frames = _wide_pipeline(n_ops, n_ops)
+    paths = _paths(dag)
+    params = TuningParams(cq_capacity=4)
+    spec = RunSpec(dag, profiles, sc, params, paths=paths)
+    eng = host_engine(spec)
+    for target, seed in ((5.0, 1), (40.0, 2), (float("inf"), 3)):
+        want = oe.Engine(dag, profiles, frames, sc, target, oe.Params(100.0, 4, 10, 1.5, 0.5),
+                         seed=seed, paths=paths).run()
+        res = eng.run([frames], [target], [seed], log_cap=len(want.log) + 16, final_tables=True)[0]
+        assert dc.log_digest(eng.log_rows(res.log)) == dc.log_digest(want.log), target
+        got = report_of(res, target_s=target, scenario_name="wide", pipeline_name="x", seed=seed)
+        for f in ("latency_s", "cost", "failures", "duplicates", "invocations", "completed",
+                  "terminal_items", "decision_count"):
+            assert repr(float(getattr(got, f))) == repr(float(getattr(want, f))), (target, f)

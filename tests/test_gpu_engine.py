@@ -87,3 +87,25 @@ def test_device_engine_random_cases_vs_oracle(device_engine):
         assert (r.failures, r.duplicates, r.invocations) == (want.failures, want.duplicates, want.invocations)
         lat = np.concatenate([o.t[op].lat for op in o.ops])
         assert np.array_equal(lat.view(np.uint64), r.lat.view(np.uint64))
+
+
+@pytest.mark.parametrize("mode", ["warp", "thread"])
+def test_device_engine_many_operations_vs_oracle(device_engine, mode):
+    """A 64-operation pipeline (entry columns + path suffixes too large for shared memory: the
+    kernels read them from global memory) against oracle/engine.py."""
+    from oracle import engine as oe
+    from paper_2102_01887_b200.engine import RunSpec, TuningParams, _paths
+    from test_engine_host import _wide_pipeline
+
+    dag, profiles, sc, frames = _wide_pipeline(63, 63)
+    paths = _paths(dag)
+    spec = RunSpec(dag, profiles, sc, TuningParams(cq_capacity=4), paths=paths)
+    eng = device_engine(spec)
+    eng.set_mode(mode)
+    targets, seeds = [5.0, 40.0, float("inf")], [1, 2, 3]
+    wants = [oe.Engine(dag, profiles, frames, sc, t, oe.Params(100.0, 4, 10, 1.5, 0.5), seed=s,
+                       paths=paths).run() for t, s in zip(targets, seeds)]
+    res = eng.run([frames] * 3, targets, seeds, log_cap=max(len(w.log) for w in wants) + 16)
+    for w, r in zip(wants, res):
+        assert dc.log_digest(eng.log_rows(r.log)) == dc.log_digest(w.log)
+        assert repr(r.cost) == repr(float(w.cost)) and r.invocations == w.invocations
