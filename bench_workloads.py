@@ -589,6 +589,12 @@ def run_c4(args):
         "gpu_launches": launches,
         "step_ms": {"median": statistics.median(ms), "min": min(ms), "max": max(ms)},
         "kernel": "k_slack_select (K1 -> K2 fused, sp_slack_select_batch)",
+        "roofline": (lambda b: {"bound": "hbm", "achieved": b / (t / args.steps) / 1e9, "peak": _peaks(),
+                                "unit": "GB/s", "frac": b / (t / args.steps) / 1e9 / _peaks(),
+                                "algorithmic_bytes_per_step": b,
+                                "bytes_model": "per instance 8V ref + 16 (target, now) + 8K Q, per "
+                                               "decision 16 B in + 36 B out (468 B per AMBER instance)"})(
+            Itot * (8 * V + 16 + 8 * K + V * (16 + 36))),
         "two_kernel_step_ms": {"median": statistics.median(ms2), "min": min(ms2),
                                "note": "k_slack then k_select_plan, slack through HBM"},
         "parity": parity,
@@ -763,6 +769,11 @@ def run_c5(args):
         "tables_bit_identical_across_ranks": identical,
         "gpu_launches": launches,
         "per_batch_ms": 1e3 * t / NB,
+        "roofline": (lambda b: {"bound": "latency (sequential chain: plan -> decisions -> fold per batch)",
+                                "achieved": b / (t / NB) / 1e9, "peak": _peaks(), "unit": "GB/s",
+                                "frac": b / (t / NB) / 1e9 / _peaks(), "algorithmic_bytes_per_batch": b,
+                                "bytes_model": "B x (32 B in + 36 B out) + M x 40 B table + 16 B per "
+                                               "observation record"})(B * (32 + 36) + M * 40 + B * 16),
         "host_enqueue_ms_per_batch": 1e3 * (h1 - h0) / NB,
         "parity": parity,
         "cpu_baseline": cpu,
