@@ -432,7 +432,8 @@ typedef struct {
 /* Per-replica result row (manager.py:577-630 RunReport inputs). status: 0 ok, 1-3 capacity,
  * 4 livelock (RuntimeError, manager.py:563), 5 speculate_fixed found no configuration
  * (RuntimeError, configurator.py:633-636), 6 non-finite score, 7 draw capacity, 8 weight
- * capacity, 9 buffer capacity, 10 event cap. */
+ * capacity, 9 buffer capacity, 10 event cap, 11 an execution of an entry without ground truth
+ * (truth_base NaN: KeyError, scenario.py:97-101). */
 typedef struct {
   double latency, cost, now;
   int32_t peak_slots, peak_heap;  /* most invocation slots / heap entries the replica held at once */

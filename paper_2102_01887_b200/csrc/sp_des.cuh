@@ -47,7 +47,7 @@ constexpr int kDrawNoise = 1, kDrawStraggle = 2, kDrawFail = 4;
 // replica status codes
 constexpr int kOk = 0, kErrInvCap = 1, kErrHeapCap = 2, kErrSegCap = 3, kErrLivelock = 4,
               kErrNoConfig = 5, kErrNonFinite = 6, kErrDrawCap = 7, kErrWeightCap = 8,
-              kErrBufCap = 9, kErrEventCap = 10;
+              kErrBufCap = 9, kErrEventCap = 10, kErrNoTruth = 11;
 
 // invocation states (manager.py:33-42)
 constexpr uint8_t kPending = 0, kSpeculated = 1, kCommitted = 3, kRunning = 4, kCompleted = 5,
@@ -678,6 +678,10 @@ struct Run {
   SPD_HDN void start(int k, int id, int inst, int need, int g) {  // backend.py:179-201
     freeres[inst] -= need;
     Inv& v = inv[id];
+    if (!(E.base[g] == E.base[g])) {  // no ground truth for (op, kind): KeyError (scenario.py:97-101)
+      error(kErrNoTruth);
+      return;
+    }
     double L = E.base[g] + E.per_item[g] * (double)fill_of(id);  // backend.py:51
     if (im.draws) {
       if (n_starts >= im.draw_cap) {

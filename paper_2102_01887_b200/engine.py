@@ -40,7 +40,7 @@ DRAW_NOISE, DRAW_STRAGGLE, DRAW_FAIL = 1, 2, 4
 
 STATUS = {0: "ok", 1: "invocation capacity", 2: "event heap capacity", 3: "item-list capacity",
           4: "livelock", 5: "no configuration", 6: "non-finite score", 7: "draw capacity",
-          8: "weight capacity", 9: "item-buffer capacity", 10: "event cap"}
+          8: "weight capacity", 9: "item-buffer capacity", 10: "event cap", 11: "no ground truth"}
 _CAPACITY = (1, 2, 3, 7, 9)
 
 OUT_DTYPE = np.dtype([("latency", "<f8"), ("cost", "<f8"), ("now", "<f8"),
@@ -185,7 +185,10 @@ class RunSpec:
             ref_index.append(ri)
             ref_lat.append(ents[ri].latency_s * profile_scale if ri >= 0 else ref.latency_s * profile_scale)
             for i, e in enumerate(ents):
-                truth = gt.kind_truth(op, e.backend_kind)
+                try:
+                    truth = gt.kind_truth(op, e.backend_kind)
+                except KeyError:  # raised by the run only if it starts such an entry (NaN marker)
+                    truth = None
                 cols["lat"].append(e.latency_s * profile_scale)
                 cols["lat_init"].append(e.latency_initial_s * profile_scale)
                 cols["res"].append(float(e.resource_request))
@@ -193,9 +196,10 @@ class RunSpec:
                 cols["kind"].append(kpos[e.backend_kind])
                 cols["id_rank"].append(rank[i])
                 cols["cfg"].append(cfg_names.setdefault(e.config_id, len(cfg_names)))
-                cols["base"].append(_base_latency(truth, e.resource_request, e.batch_size,
+                cols["base"].append(math.nan if truth is None else
+                                    _base_latency(truth, e.resource_request, e.batch_size,
                                                   dict(e.knob_values)))
-                cols["per_item"].append(float(truth.per_item_seconds))
+                cols["per_item"].append(math.nan if truth is None else float(truth.per_item_seconds))
             self.entries.append(ents)
             self.entry_off.append(self.entry_off[-1] + len(ents))
         self.cfg_names = list(cfg_names)
@@ -453,6 +457,8 @@ class ReplicaEngine:
                     raise RuntimeError("run stalled with work remaining")
                 if st == 5:
                     raise RuntimeError("no configuration can re-run a retried or duplicated invocation")
+                if st == 11:
+                    raise KeyError("no ground truth for an operation / backend kind the run executes")
                 if st != 0:
                     raise _lib.SlackpipeError(f"run engine replica {r}: {STATUS.get(st, st)}")
                 o = out[j]
