@@ -541,6 +541,63 @@ class ReplicaEngine:
         return rows
 
 
+class GroupReplicaEngine:
+    """ReplicaEngine fanned out over a DeviceGroup from one host thread's call (SURVEY.md §8(b)
+    Threading, §8(e)): the replicas are split into contiguous shards, one per member device, all in
+    flight at once (a worker thread per member; the library call releases the GIL), results in
+    replica order.  Replicas are independent: no collective."""
+
+    def __init__(self, spec: RunSpec, group):
+        self.spec = spec
+        self.engines = [ReplicaEngine(spec, m) for m in group.members]
+
+    def set_mode(self, mode: str) -> None:
+        for e in self.engines:
+            e.set_mode(mode)
+
+    def close(self) -> None:
+        for e in self.engines:
+            e.close()
+
+    def run(self, traces, targets, seeds=None, *, trace_of=None, log_cap: int = 0,
+            final_tables: bool = False, encoded=None, event_cap: int = 0) -> list[RunResult]:
+        import threading
+
+        R = len(targets)
+        fo, at = encoded if encoded is not None else self.spec.encode_frames(traces)
+        trace_of = np.arange(R, dtype=np.int32) if trace_of is None else np.asarray(trace_of, np.int32)
+        targets = np.asarray(targets, dtype=np.float64)
+        seeds = list(seeds) if seeds is not None else [self.spec.scenario.seed] * R
+        G = len(self.engines)
+        bounds = [(g * R // G, (g + 1) * R // G) for g in range(G)]
+        out: list = [None] * G
+        err: list = []
+
+        def work(g):
+            a, b = bounds[g]
+            try:
+                out[g] = self.engines[g].run(None, targets[a:b], seeds[a:b], trace_of=trace_of[a:b],
+                                             log_cap=log_cap, final_tables=final_tables,
+                                             encoded=(fo, at), event_cap=event_cap) if b > a else []
+            except BaseException as e:  # re-raised in the caller's thread
+                err.append(e)
+
+        th = [threading.Thread(target=work, args=(g,)) for g in range(G)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        if err:
+            raise err[0]
+        return [r for part in out for r in part]
+
+    def log_rows(self, log):
+        return self.engines[0].log_rows(log)
+
+    def event_rows(self, events):
+        return self.engines[0].event_rows(events)
+
+
 @dataclass
 class RunReport:
     """Aggregates of one pipeline run; the CSV schema is the reference's (manager.py:104-170)."""

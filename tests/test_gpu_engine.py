@@ -109,3 +109,19 @@ def test_device_engine_many_operations_vs_oracle(device_engine, mode):
     for w, r in zip(wants, res):
         assert dc.log_digest(eng.log_rows(r.log)) == dc.log_digest(w.log)
         assert repr(r.cost) == repr(float(w.cost)) and r.invocations == w.invocations
+
+
+def test_group_engine_fans_out_over_member_contexts(gpu_ctx):
+    """GroupReplicaEngine over two member contexts (both on device 0 here: the same code path as
+    two GPUs) gives the single-engine results for the config-4 golden runs, in replica order."""
+    import paper_2102_01887_b200 as sp
+    from paper_2102_01887_b200.engine import GroupReplicaEngine
+
+    cases = [c for c in dc.runs() if c.get("group") == "c4"][:10]
+    grp = sp.DeviceGroup([0, 0])
+
+    def make(spec):
+        return GroupReplicaEngine(spec, grp)
+
+    for case, (rows, rep, lat, ev) in zip(cases, dc.run_group(make, cases)):
+        assert not dc.check(case, rows, rep, lat, ev), case["target"]
