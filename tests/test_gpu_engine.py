@@ -125,3 +125,28 @@ def test_group_engine_fans_out_over_member_contexts(gpu_ctx):
 
     for case, (rows, rep, lat, ev) in zip(cases, dc.run_group(make, cases)):
         assert not dc.check(case, rows, rep, lat, ev), case["target"]
+
+
+@pytest.mark.parametrize("target,sha16,csv_tail", [
+    (142.20064921472454, "4647eeb560b36a71",
+     "142.20064921472454,132.73451153109434,0.9334311218977895,0.16671542613566986,1.0,20,0,0"),
+    (0.0, "04a858b09a523792", "0.0,90.41885182994682,inf,0.3916674839012888,0.0,19,0,0"),
+    (float("inf"), "3a27109b8eba0deb", "inf,193.98244659950223,0.0,0.14018874269532433,1.0,15,0,0"),
+])
+def test_amber_dropin_reproduces_survey_goldens(gpu_ctx, tmp_path, target, sha16, csv_tail):
+    """The decision-log FILE the device drop-in writes (write_decision_log, manager.py:632-646)
+    has the sha256 prefix SURVEY.md §8(c) recorded from the reference CLI's own AMBER runs, and
+    the report's CSV row the recorded values (run_id aside: it hashes the CLI's flag paths)."""
+    import hashlib
+
+    from paper_2102_01887_b200.engine import PipelineRun
+
+    doc, dag, sc, profiles, paths, frames = dc.bundle("branching")
+    spec = dc.run_spec(dict(bundle="branching"))
+    run = PipelineRun(dag, {}, profiles, frames, sc, target, spec.params, paths=paths,
+                      pipeline_name=doc["name"], ctx=gpu_ctx)
+    rep = run.run_to_completion()
+    assert rep.csv_row().split(",", 1)[1] == csv_tail
+    p = tmp_path / "decisions.tsv"
+    run.write_decision_log(str(p))
+    assert hashlib.sha256(p.read_bytes()).hexdigest()[:16] == sha16
