@@ -286,26 +286,28 @@ inline bool plan_run(HostImage& h, int T, const int32_t* frame_off, const int32_
     o = align16(o + bytes);
     return at;
   };
-  im.o_lat = take(24 * (int64_t)N);  // host harness only: lat / cost / costpen, ts = 1
+  // the small per-run state every event touches first (one contiguous block: a few cache lines
+  // and one page), then the large arrays
+  im.o_opi = take(4 * (int64_t)V * kOpiN);
+  im.o_scver = take(4 * (int64_t)V);
+  im.o_scval = take(8 * (int64_t)V * K);
+  im.o_holddl = take(8 * (int64_t)V * 4);  // hold deadlines, r_min, r_max, ratio versions
+  im.o_wkey = take(4 * 2 * (int64_t)std::max(im.w_off[K], 1));
+  im.o_wcnt = take(4 * 2 * (int64_t)std::max(im.w_off[K], 1));
+  im.o_cfg = take(4 * (int64_t)((im.n_cfg + 31) / 32));
+  im.o_lat = take(24 * (int64_t)N);  // lat / cost / costpen (host harness, lane-group forms)
   im.o_obs = take(N);
+  im.o_free = take(4 * (int64_t)std::max(im.inst_off[K], 1));
+  im.o_heap = take((int64_t)sizeof(HeapEnt) * im.heap_cap);
   im.o_inv = take((int64_t)sizeof(Inv) * (inv_cap + 1));
   im.o_next = take(4 * (inv_cap + 1));
   im.o_live = take(4 * (inv_cap + 1));
   im.o_list = take((int64_t)sizeof(List) * (inv_cap + 1));
-  im.o_seg = take((int64_t)sizeof(Seg) * im.seg_cap);
-  im.o_buf = take(4 * std::max<int64_t>(off, 1));
-  im.o_heap = take((int64_t)sizeof(HeapEnt) * im.heap_cap);
-  im.o_wkey = take(4 * 2 * (int64_t)std::max(im.w_off[K], 1));
-  im.o_wcnt = take(4 * 2 * (int64_t)std::max(im.w_off[K], 1));
-  im.o_scver = take(4 * (int64_t)V);
-  im.o_scval = take(8 * (int64_t)V * K);
-  im.o_holddl = take(8 * (int64_t)V * 4);  // hold deadlines, r_min, r_max, ratio versions
-  im.o_free = take(4 * (int64_t)std::max(im.inst_off[K], 1));
-  im.o_staging = take(4 * std::max<int64_t>((int64_t)frames_cap * im.staging_per_frame, 1));
-  im.o_cfg = take(4 * (int64_t)((im.n_cfg + 31) / 32));
-  im.o_opi = take(4 * (int64_t)V * kOpiN);
   im.o_free_slot = take(4 * (inv_cap + 1));
+  im.o_seg = take((int64_t)sizeof(Seg) * im.seg_cap);
   im.o_free_seg = take(4 * (int64_t)im.seg_cap);
+  im.o_buf = take(4 * std::max<int64_t>(off, 1));
+  im.o_staging = take(4 * std::max<int64_t>((int64_t)frames_cap * im.staging_per_frame, 1));
   im.arena_bytes = align16(o);
   return true;
 }
