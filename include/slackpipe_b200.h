@@ -476,12 +476,12 @@ int sp_des_prepare(sp_ctx* ctx, sp_des* des, int32_t R, int32_t n_traces, const 
 /* Invocation capacity per buffered item (default 1.25; retries and straggler duplicates add
  * invocations beyond one per item — a replica that runs out reports status 1). */
 int sp_des_set_capacity(sp_des* des, double invocations_per_item);
-/* Execution form: 1 = one GPU thread per replica (the replicas of a warp diverge; the most
- * runs per second once tens of thousands of replicas fill the GPU), 2 = one warp per replica
- * (all lanes run the replica's serial engine, the entry scans split across the lanes: ~17x lower
- * latency per run), 4 / 8 / 16 = that many lanes per replica (32 / n replicas per warp),
- * 0 = default (32 lanes below 2,048 replicas, 8 below 32,768, else 4).  Results are identical. */
-int sp_des_set_mode(sp_des* des, int32_t mode);
+/* Execution form: lanes = 1: one GPU thread per replica (the replicas of a warp diverge);
+ * 2 / 4 / 8 / 16 / 32: that many lanes per replica (all lanes run the replica's serial engine, the
+ * entry scans split across them; 32 = one warp per replica, ~17x lower latency per run than one
+ * thread); 0 = default (32 lanes below 2,048 replicas, 8 below 32,768, else 2).  Results are
+ * identical in every form. */
+int sp_des_set_mode(sp_des* des, int32_t lanes);
 /* The reference's per-start RNG draws of R runs (host, no GPU needed): replica r's numpy PCG64
  * state (state hi, lo, inc hi, lo in pcg_state[4r..4r+3], as default_rng(seed) sets it) and, per
  * start k < cap, in the reference's order (backend.py:52-57, 186): factor[r*cap+k] =

@@ -185,11 +185,11 @@ int launch(sp_ctx* ctx, sp_des* d, int32_t R, const int32_t* frame_off, const in
                         sizeof(int32_t) * (size_t)d->h.im.suf_off[d->h.im.n_ops];
   const int in_smem = ebytes <= kSmemEntriesMax;
   const size_t smem = sizeof(Image) + (in_smem ? ebytes : 0);
-  // default lanes per run by the number of runs (measured on AMBER, runs/s; one run per thread:
-  // 1.3k at 16k runs, 4.1k at 65k; 32 lanes: 0.42 s per run, 2.5k runs/s from 4k runs; 16 lanes:
-  // 3.1k / 3.4k; 8 lanes: 3.7k / 3.9k; 4 lanes: 3.2k / 4.6k at 16k / 65k runs)
+  // default lanes per run by the number of runs (measured on AMBER, runs/s at 16k / 65k runs;
+  // one run per thread: 1.3k / 4.0k; 2 lanes: 2.8k / 5.3k; 4 lanes: 3.2k / 4.7k; 8 lanes:
+  // 3.7k / 3.9k; 16 lanes: 3.1k / 3.4k; 32 lanes: 0.42 s per run, 2.5-2.8k runs/s from 4k runs)
   const int nl = d->mode >= 2 ? d->lanes
-                              : (d->mode == 1 ? 0 : (R < 2048 ? 32 : (R < 32768 ? 8 : 4)));
+                              : (d->mode == 1 ? 0 : (R < 2048 ? 32 : (R < 32768 ? 8 : 2)));
   if (nl) {
     cudaError_t e = cudaFuncSetAttribute(k_des_run_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return sp::cuda_fail(e, "run engine smem");
@@ -273,12 +273,13 @@ extern "C" int sp_des_prepare(sp_ctx* ctx, sp_des* d, int32_t R, int32_t n_trace
   return prepare(ctx, d, R, n_traces, frame_off, attrs, draw_cap, log_cap);
 }
 
-extern "C" int sp_des_set_mode(sp_des* d, int32_t mode) {
-  // 0 default, 1 one thread per run, 2 one warp per run, 4 / 8 / 16: that many lanes per run
-  if (!d || !(mode == 0 || mode == 1 || mode == 2 || mode == 4 || mode == 8 || mode == 16))
-    return sp::fail(SP_E_INVALID, "des_set_mode: 0 (default), 1 thread, 2 warp, 4 / 8 / 16 lanes");
-  d->mode = mode == 0 || mode == 1 ? mode : 2;
-  d->lanes = mode == 2 ? 32 : (mode >= 4 ? mode : 32);
+extern "C" int sp_des_set_mode(sp_des* d, int32_t lanes) {
+  // 0 default, 1 one thread per run, 2 / 4 / 8 / 16 / 32 lanes per run
+  if (!d || !(lanes == 0 || lanes == 1 || lanes == 2 || lanes == 4 || lanes == 8 || lanes == 16 ||
+              lanes == 32))
+    return sp::fail(SP_E_INVALID, "des_set_mode: 0 (default), 1 (thread per run), 2..32 lanes per run");
+  d->mode = lanes <= 1 ? lanes : 2;
+  d->lanes = lanes <= 1 ? 32 : lanes;
   return SP_OK;
 }
 

@@ -409,9 +409,11 @@ class ReplicaEngine:
         self.cap_scale = 1.25
 
     def set_mode(self, mode: str) -> None:
-        """"default" (32 lanes per replica below 2,048 replicas, 8 below 32,768, else 4),
-        "warp" (32 lanes), "lanes16" / "lanes8" / "lanes4", or "thread" (one thread per replica)."""
-        m = {"default": 0, "thread": 1, "warp": 2, "lanes4": 4, "lanes8": 8, "lanes16": 16}[mode]
+        """"default" (32 lanes per replica below 2,048 replicas, 8 below 32,768, else 2),
+        "warp" (32 lanes), "lanes16" / "lanes8" / "lanes4" / "lanes2", or "thread" (one thread per
+        replica)."""
+        m = {"default": 0, "thread": 1, "warp": 32, "lanes2": 2, "lanes4": 4, "lanes8": 8,
+             "lanes16": 16}[mode]
         _lib.check(self.lib.sp_des_set_mode(self.handle, m), "sp_des_set_mode")
 
     def close(self) -> None:

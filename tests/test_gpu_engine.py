@@ -19,7 +19,7 @@ def device_engine(gpu_ctx):
     return lambda spec: ReplicaEngine(spec, gpu_ctx)
 
 
-@pytest.mark.parametrize("mode", ["warp", "thread", "lanes8"])
+@pytest.mark.parametrize("mode", ["warp", "thread", "lanes8", "lanes2"])
 def test_device_engine_matches_golden_runs(device_engine, gpu_ctx, mode):
     """Both execution forms: one warp per replica (default) and one thread per replica."""
     launches0 = gpu_ctx.launch_count

@@ -21,7 +21,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("R", nargs="*", type=int, default=[148, 1024, 4096])
 ap.add_argument("--frames", type=int, default=3000)
 ap.add_argument("--once", action="store_true")
-ap.add_argument("--mode", default="warp", choices=["default", "warp", "thread", "lanes4", "lanes8", "lanes16"])
+ap.add_argument("--mode", default="warp", choices=["default", "warp", "thread", "lanes2", "lanes4", "lanes8", "lanes16"])
 args = ap.parse_args()
 eng.set_mode(args.mode)
 for R in args.R:
