@@ -1355,8 +1355,13 @@ def run_c4runs(args):
                    "arena_bytes_per_run": per_replica,
                    "parallelism": f"{R} replicas x 5 targets sharded contiguously over {world} GPU(s), "
                                   "no data-path collective"},
-        "kernel": "k_des_run (one thread per run: event heap, backend pools, speculation, commits, "
-                  "feedback in each run's HBM arena)",
+        "kernel": "k_des_run_warp (a lane group per run — 2 lanes at this run count — every lane "
+                  "running the run's event loop: heap, backend pools, speculation, commits, feedback "
+                  "in the run's HBM arena; the OpTable scans split across the lanes)",
+        "roofline": {"bound": "latency (a sequential event loop per run; throughput from runs in flight)",
+                     "achieved": None, "peak": None, "unit": None, "frac": None,
+                     "evidence": "profiles/r02/des/ncu_des_warp_summary.json (47% warps active, 23% "
+                                 "issue active, stalls: long scoreboard and instruction fetch)"},
         "gpu_launches": launches,
         "step_ms": {"median": statistics.median(ms), "min": min(ms), "max": max(ms)},
         "parity": {"runs": len(gold), "mismatches": bad[1], "bad_status": bad[0],
