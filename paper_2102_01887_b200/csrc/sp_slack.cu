@@ -148,6 +148,26 @@ __device__ __forceinline__ void store_slack(int i, int s, int n_src, double own,
   }
 }
 
+// store_slack with the K budgets b_k = (target - now) - Q[k] computed once per instance
+// (K <= 4: the per-source loop then reads no Q)
+__device__ __forceinline__ void store_slack4(int i, int s, int n_src, double own, double tmax,
+                                             double tmin, int K, const double (&bq)[4],
+                                             double* __restrict__ out_slack,
+                                             double* __restrict__ out_ratio) {
+  const double ratio_lo = __ddiv_rn(own, tmax);
+  const double ratio_hi = __ddiv_rn(own, tmin);
+  const size_t o = (size_t)i * n_src + s;
+  if (out_ratio) {
+    out_ratio[2 * o] = ratio_lo;
+    out_ratio[2 * o + 1] = ratio_hi;
+  }
+  if (out_slack) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (k < K) out_slack[o * K + k] = __dmul_rn(bq[k] >= 0.0 ? ratio_lo : ratio_hi, bq[k]);
+  }
+}
+
 // ---- K1c: certified backward pass -------------------------------------------------------
 // The forward DP above relaxes every edge of every source's descendant set (19,227 edge
 // relaxations per instance on config 3's 64-op DAG).  K1c finds each source's extremal path
@@ -287,6 +307,7 @@ __global__ void __launch_bounds__(32 * kCertWarps) k_slack_cert(
   bad |= __shfl_xor_sync(0xffffffffu, bad, 1);
   __syncwarp();
   // walk records {ref, G_max | G_min}: the even lane brings the ref, the odd lane the margins
+#pragma unroll 8
   for (int v = 0; v < V; ++v)
     A[v * 32 + side] = side ? *reinterpret_cast<const double*>(Cf + v * 32) : __ldg(r + VI[v]);
   for (int w = 0; w < nfw; ++w) Fw[w * 32] = 0u;
@@ -294,6 +315,12 @@ __global__ void __launch_bounds__(32 * kCertWarps) k_slack_cert(
 
   // configurator.py:535  budget = self.target_s - now - queueing[k]
   const double base = live ? __dsub_rn(__ldg(target + i), __ldg(now + i)) : 0.0;
+  // configurator.py:535 per kind, once per instance (K <= 4; larger K reads Q per source)
+  double bq[4] = {0.0, 0.0, 0.0, 0.0};
+  if (live && K <= 4)
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk)
+      if (kk < K) bq[kk] = __dsub_rn(base, __ldg(Q + (size_t)i * K + kk));
   // ---- per source: walk both extremal paths, certify, emit (sources by parity, 2 at once) ----
   for (int g = side; g < n_src; g += 4) {
     const int sa = g, sb = g + 2 < n_src ? g + 2 : -1;
@@ -320,7 +347,10 @@ __global__ void __launch_bounds__(32 * kCertWarps) k_slack_cert(
       if (ok) {
         if (live) {
           const double own = __dadd_rn(0.0, ws.x);
-          store_slack(i, si, n_src, own, h.acc, l.acc, base, K, Q, out_slack, out_ratio);
+          if (K <= 4)
+            store_slack4(i, si, n_src, own, h.acc, l.acc, K, bq, out_slack, out_ratio);
+          else
+            store_slack(i, si, n_src, own, h.acc, l.acc, base, K, Q, out_slack, out_ratio);
         }
       } else {
         Fw[(si >> 5) * 32] |= 1u << (si & 31);
