@@ -196,7 +196,7 @@ __device__ __forceinline__ void store_slack4(int i, int s, int n_src, double own
 // parity, two sources per lane in flight.  Per instance and node 26 bytes of shared memory:
 // {Hb, -Lb} (later the walk record {ref, G_max | G_min}), the two float margins, the two args.
 constexpr uint32_t kArgNone = 0xFE, kArgEnd = 0xFF;
-constexpr int kCertWarps = 2;  // 32 instances per block
+constexpr int kCertWarps = 2;  // 32 instances per block (4 warps per block measured the same)
 
 // one walk step along an extremal path: add the node's ref to the forward sum, follow the arg
 struct Walk {
