@@ -177,6 +177,7 @@ void options_from_env(Options& o) {
   o.pipe_chunks = env_int("SP_PIPE_CHUNKS", 0);
   if (const char* e = getenv("SP_K1_CERT")) o.k1_cert = !strcmp(e, "force") ? 2 : (!strcmp(e, "0") ? 1 : 0);
   o.fold_long_min = env_int("SP_FOLD_LONG_MIN", 0);
+  o.k1c_lanes = env_int("SP_K1C_LANES", 4) == 2 ? 2 : 4;
   o.fold_legacy = getenv("SP_FOLD_LEGACY") != nullptr;
   o.stair_smem = getenv("SP_STAIR_SMEM") != nullptr;
   o.stair_global = getenv("SP_STAIR_GLOBAL") != nullptr;
@@ -198,7 +199,7 @@ int options_set(Options& o, const char* name, long long v) {
     const char* n;
     int* f;
   } tab[] = {{"SP_ZERO_COPY", &o.zero_copy},     {"SP_PIPE_CHUNKS", &o.pipe_chunks},
-             {"SP_K1_CERT", &o.k1_cert},         {"SP_FOLD_LONG_MIN", &o.fold_long_min},
+             {"SP_K1_CERT", &o.k1_cert},         {"SP_K1C_LANES", &o.k1c_lanes},         {"SP_FOLD_LONG_MIN", &o.fold_long_min},
              {"SP_FOLD_LEGACY", &o.fold_legacy},
              {"SP_STAIR_SMEM", &o.stair_smem},   {"SP_STAIR_GLOBAL", &o.stair_global},
              {"SP_NO_PLAN_GRAPH", &o.no_plan_graph}, {"SP_PLAN_LEGACY", &o.plan_legacy},

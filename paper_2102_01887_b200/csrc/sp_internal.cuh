@@ -130,6 +130,7 @@ struct Options {
   int zero_copy = 1;         // SP_ZERO_COPY: pinned mapped host buffers read by the kernel
   int pipe_chunks = 0;       // SP_PIPE_CHUNKS: pageable staging chunks (0 = by size)
   int k1_cert = 0;           // SP_K1_CERT: 0 auto, 1 off ("0"), 2 force ("force")
+  int k1c_lanes = 4;         // SP_K1C_LANES: lanes per instance of the certified pass (4 or 2)
   int fold_long_min = 0;     // SP_FOLD_LONG_MIN: long-segment threshold of the fold (0 = default)
   int fold_legacy = 0;       // SP_FOLD_LEGACY: multi-kernel fold (radix sort + 5 kernels)
   int stair_smem = 0;        // SP_STAIR_SMEM: multi-kernel builder, shared-memory staircase

@@ -204,14 +204,14 @@ struct Walk {
   double acc;  // forward sum ((0 + r_s) + r_1) + ... along the path
 };
 
-template <bool MAX>
+template <bool MAX, int ROW = 16>
 __device__ __forceinline__ void walk_step(Walk& c, const double2* __restrict__ W,
                                           const uint16_t* __restrict__ R) {
   // branch-free: a finished chain re-reads node 0 and keeps its state
   const bool on = c.v < kArgNone;
   const uint32_t v = on ? c.v : 0u;
-  const double rv = W[v * 16].x;
-  const uint32_t rr = R[v * 16];
+  const double rv = W[v * ROW].x;
+  const uint32_t rr = R[v * ROW];
   const double acc = __dadd_rn(c.acc, rv);
   c.acc = on ? acc : c.acc;
   c.v = on ? (MAX ? (rr & 0xFFu) : (rr >> 8)) : c.v;
@@ -401,6 +401,204 @@ __global__ void __launch_bounds__(32 * kCertWarps) k_slack_cert(
   }
 }
 
+// K1c, four lanes per instance: lanes (instance k, side, sub) — 8 instances per warp, half the
+// shared memory per warp of k_slack_cert, so twice the resident warps.  The two sub-lanes of a
+// side split every node's successor groups (even / odd groups; the terminal option in sub 0)
+// and merge their (best, runner-up, arg) by one shuffle — the merged best and runner-up are the
+// sequential scan's (an exact tie leaves the runner-up equal to the best, failing the
+// certificate exactly as there); the four lanes split the per-source walks (sources L, L + 4,
+// L + 8, ... for L = 2 side + sub).  Everything else — the certificate, the forward sums, the
+// fallback forward DP — is k_slack_cert's, so the results are identical.
+__global__ void __launch_bounds__(32 * kCertWarps) k_slack_cert4(
+    const uint8_t* __restrict__ cert, int cert_bytes, int V, int n_src, int off_vidx,
+    int off_term, int off_src, int off_succ, const int4* __restrict__ prog,
+    const int32_t* __restrict__ prog_ptr, const uint32_t* __restrict__ preds,
+    const int32_t* __restrict__ pred_ptr, int I, const double* __restrict__ ref, int ref_stride,
+    const double* __restrict__ target, const double* __restrict__ now, int K,
+    const double* __restrict__ Q, double theta, double* __restrict__ out_slack,
+    double* __restrict__ out_ratio) {
+  extern __shared__ __align__(16) uint8_t smc[];
+  for (int t = threadIdx.x; t < cert_bytes / 16; t += blockDim.x)
+    reinterpret_cast<uint4*>(smc)[t] = __ldg(reinterpret_cast<const uint4*>(cert) + t);
+  __syncthreads();
+  const uint16_t* SP = reinterpret_cast<const uint16_t*>(smc);
+  const uint16_t* VI = reinterpret_cast<const uint16_t*>(smc + off_vidx);
+  const uint8_t* TE = smc + off_term;
+  const uint8_t* SRC = smc + off_src;
+  const uint16_t* SU = reinterpret_cast<const uint16_t*>(smc + off_succ);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int k = lane >> 2, side = (lane >> 1) & 1, sub = lane & 1, L = lane & 3;
+  const int nfw = (n_src + 31) >> 5;
+  const size_t arow = (size_t)(V + 1) * 128;  // [V+1][8][2] doubles (sentinel row V)
+  uint8_t* wb = smc + cert_bytes + (size_t)warp * (arow + (size_t)V * 80 + (size_t)nfw * 128);
+  // element (v, k, side) of each [V][8][2] array sits at v * 16 + 2k + side
+  double* A = reinterpret_cast<double*>(wb) + 2 * k;
+  float* Cf = reinterpret_cast<float*>(wb + arow) + 2 * k;
+  uint8_t* Rb = wb + arow + (size_t)V * 64 + 2 * k;
+  uint32_t* Fw = reinterpret_cast<uint32_t*>(wb + arow + (size_t)V * 80) + lane;
+  const char* As = reinterpret_cast<const char*>(A + side);  // + node * 128
+  const double2* W = reinterpret_cast<const double2*>(A);   // walk record (v, k) at v * 8
+  const uint16_t* R = reinterpret_cast<const uint16_t*>(Rb);
+  const int i0 = (blockIdx.x * kCertWarps + warp) * 8;
+  if (i0 >= I) return;
+  const int i = i0 + k;
+  const bool live = i < I;
+  const double* r = ref + (size_t)(live ? i : i0) * ref_stride;
+
+  A[V * 16 + side] = -INFINITY;
+  bool bad = false;
+  double rn = __ldg(r + VI[V - 1]);
+  for (int v = V - 1; v >= 0; --v) {
+    const double rv = rn;
+    if (v > 0) rn = __ldg(r + VI[v - 1]);
+    bad |= !(rv >= 0.0 && rv <= 1e300);
+    const bool te = TE[v] != 0 && sub == 0;  // the terminal option is sub 0's
+    double h1 = te ? 0.0 : -INFINITY, h2 = -INFINITY;
+    uint32_t a1 = te ? (kArgEnd << 8) : (kArgNone << 8);
+    for (int q = SP[v] + sub; q < SP[v + 1]; q += 2) {
+      const uint2 w = *reinterpret_cast<const uint2*>(SU + 4 * q);
+      const uint32_t u0 = w.x & 0xFFFFu, u1 = w.x >> 16, u2 = w.y & 0xFFFFu, u3 = w.y >> 16;
+      const double x0 = *reinterpret_cast<const double*>(As + (u0 >> 1));
+      const double x1 = *reinterpret_cast<const double*>(As + (u1 >> 1));
+      const double x2 = *reinterpret_cast<const double*>(As + (u2 >> 1));
+      const double x3 = *reinterpret_cast<const double*>(As + (u3 >> 1));
+      const bool g01 = x1 > x0, g23 = x3 > x2;
+      const double m01 = g01 ? x1 : x0, s01 = g01 ? x0 : x1;
+      const double m23 = g23 ? x3 : x2, s23 = g23 ? x2 : x3;
+      const uint32_t i01 = g01 ? u1 : u0, i23 = g23 ? u3 : u2;
+      const bool gq = m23 > m01;
+      const double M = gq ? m23 : m01;
+      const double lo = gq ? m01 : m23;
+      const double sm = s01 > s23 ? s01 : s23;
+      const double S = lo > sm ? lo : sm;
+      const uint32_t iq = gq ? i23 : i01;
+      const bool gt = M > h1;
+      const double l2 = gt ? h1 : M;
+      const double s2 = S > h2 ? S : h2;
+      h2 = l2 > s2 ? l2 : s2;
+      h1 = gt ? M : h1;
+      a1 = gt ? iq : a1;
+    }
+    {  // merge the two halves: best, runner-up (a tie makes them equal), the best's arg
+      const double ph1 = __shfl_xor_sync(0xffffffffu, h1, 1);
+      const double ph2 = __shfl_xor_sync(0xffffffffu, h2, 1);
+      const uint32_t pa1 = __shfl_xor_sync(0xffffffffu, a1, 1);
+      const double H1 = h1 > ph1 ? h1 : ph1;
+      const double lo = h1 > ph1 ? ph1 : h1;
+      const double sm = h2 > ph2 ? h2 : ph2;
+      h2 = lo > sm ? lo : sm;
+      const uint32_t a0 = sub ? pa1 : a1, a1b = sub ? a1 : pa1;  // sub 0's, sub 1's
+      const double h0 = sub ? ph1 : h1, h1b = sub ? h1 : ph1;
+      a1 = h1b > h0 ? a1b : a0;
+      h1 = H1;
+    }
+    a1 >>= 8;
+    A[v * 16 + side] = __dadd_rn(side ? -rv : rv, h1);
+    float gm = __double2float_rd(__dsub_rd(h1, h2));
+    if (a1 < kArgNone) {
+      const float gn = Cf[a1 * 16 + side];
+      gm = gn < gm ? gn : gm;
+    } else if (a1 == kArgNone) {
+      gm = -INFINITY;
+    }
+    Cf[v * 16 + side] = gm;
+    Rb[v * 16 + side] = (uint8_t)a1;
+  }
+  bad |= __shfl_xor_sync(0xffffffffu, bad, 1);
+  bad |= __shfl_xor_sync(0xffffffffu, bad, 2);
+  __syncwarp();
+  // walk records {ref, G_max | G_min}: side 0 brings the ref, side 1 the margins, sub-lanes split v
+#pragma unroll 4
+  for (int v = sub; v < V; v += 2)
+    A[v * 16 + side] = side ? *reinterpret_cast<const double*>(Cf + v * 16) : __ldg(r + VI[v]);
+  for (int w = 0; w < nfw; ++w) Fw[w * 32] = 0u;
+  __syncwarp();
+
+  const double base = live ? __dsub_rn(__ldg(target + i), __ldg(now + i)) : 0.0;
+  double bq[4] = {0.0, 0.0, 0.0, 0.0};
+  if (live && K <= 4)
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk)
+      if (kk < K) bq[kk] = __dsub_rn(base, __ldg(Q + (size_t)i * K + kk));
+  // ---- per source (sources L, L + 4, ... in pairs): walk both extremal paths, certify, emit ----
+  for (int g = L; g < n_src; g += 8) {
+    const int sa = g, sb = g + 4 < n_src ? g + 4 : -1;
+    const uint32_t va = SRC[sa], vb = sb >= 0 ? SRC[sb] : 0u;
+    Walk ha{va, 0.0}, la{va, 0.0};
+    Walk hb{sb >= 0 ? vb : kArgEnd, 0.0}, lb{sb >= 0 ? vb : kArgEnd, 0.0};
+    while (ha.v < kArgNone || la.v < kArgNone || hb.v < kArgNone || lb.v < kArgNone) {
+      walk_step<true, 8>(ha, W, R);
+      walk_step<false, 8>(la, W, R);
+      walk_step<true, 8>(hb, W, R);
+      walk_step<false, 8>(lb, W, R);
+    }
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int si = q ? sb : sa;
+      if (si < 0) continue;
+      const Walk& h = q ? hb : ha;
+      const Walk& l = q ? lb : la;
+      const double2 ws = W[SRC[si] * 8];
+      const float gh = __int_as_float(__double2loint(ws.y));
+      const float gl = __int_as_float(__double2hiint(ws.y));
+      const bool ok = !bad && (double)gh >= __dmul_ru(theta, h.acc) &&
+                      (double)gl >= __dmul_ru(theta, l.acc);
+      if (ok) {
+        if (live) {
+          const double own = __dadd_rn(0.0, ws.x);
+          if (K <= 4)
+            store_slack4(i, si, n_src, own, h.acc, l.acc, K, bq, out_slack, out_ratio);
+          else
+            store_slack(i, si, n_src, own, h.acc, l.acc, base, K, Q, out_slack, out_ratio);
+        }
+      } else {
+        Fw[(si >> 5) * 32] |= 1u << (si & 31);
+      }
+    }
+  }
+  __syncwarp();
+
+  // ---- uncertified sources: the exact forward DP, one lane of the instance at a time ----
+  double2* D = reinterpret_cast<double2*>(A);
+  for (int sd = 0; sd < 4; ++sd) {
+    if (L == sd) {
+      for (int w = 0; w < nfw; ++w) {
+        uint32_t bits = Fw[w * 32];
+        while (bits) {
+          const int si = w * 32 + __ffs(bits) - 1;
+          bits &= bits - 1;
+          const int4* Ps = prog + prog_ptr[si];
+          const int n = prog_ptr[si + 1] - prog_ptr[si];
+          const uint32_t* Gs = preds + pred_ptr[si];
+          const int4 head = Ps[0];
+          const double own = __dadd_rn(0.0, __ldg(r + head.x));
+          D[(head.y & 0xffff) * 8] = make_double2(own, own);
+          double tmax = (head.y >> 16) ? own : -INFINITY;
+          double tmin = (head.y >> 16) ? own : INFINITY;
+          for (int e = 1; e < n; ++e) {
+            const int4 pr = Ps[e];
+            const double rv = __ldg(r + pr.x);
+            double hm = -INFINITY, lm = INFINITY;
+            for (int t = 0; t < 2 * pr.w; ++t) {
+              const double2 a = D[Gs[pr.z + t] * 8];
+              hm = hm > a.x ? hm : a.x;
+              lm = lm < a.y ? lm : a.y;
+            }
+            const double h = __dadd_rn(hm, rv), l = __dadd_rn(lm, rv);
+            D[(pr.y & 0xffff) * 8] = make_double2(h, l);
+            if (pr.y >> 16) {
+              tmax = h > tmax ? h : tmax;
+              tmin = l < tmin ? l : tmin;
+            }
+          }
+          if (live) store_slack(i, si, n_src, own, tmax, tmin, base, K, Q, out_slack, out_ratio);
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
 // Eq. 2 ordered sum, one thread per kind (configurator.py:516-523 / 116-119).
 __global__ void k_queueing(int K, const int32_t* __restrict__ ptr, const double* __restrict__ lat,
                            const double* __restrict__ res, const int32_t* __restrict__ cnt,
@@ -427,6 +625,30 @@ int slack_launch(sp_ctx* ctx, sp_dag* g, int I, const double* ref, int ref_strid
                  const double* target, const double* now, int K, const double* Q,
                  double* out_slack, double* out_ratio) {
   if (I == 0) return SP_OK;
+  if (g->cert && ctx->opt.k1_cert != 1 && ctx->opt.k1c_lanes == 4) {
+    const int nfw = (g->n_src + 31) / 32;
+    const size_t smem = (size_t)g->cert_bytes +
+                        (size_t)kCertWarps * ((size_t)(g->V + 1) * 128 + (size_t)g->V * 80 +
+                                              (size_t)nfw * 128);
+    if (smem <= 227 * 1024) {
+      static size_t cert4_attr_dev[64] = {};
+      size_t& cert_attr = cert4_attr_dev[cur_device()];
+      if (smem > 48 * 1024 && smem > cert_attr) {
+        SP_CUDA(cudaFuncSetAttribute(k_slack_cert4, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+        cert_attr = smem;
+      }
+      const double u = std::ldexp(1.0, -53);
+      const double gam = g->V * u / (1.0 - g->V * u);
+      const int per_block = 8 * kCertWarps;
+      k_slack_cert4<<<(I + per_block - 1) / per_block, 32 * kCertWarps, smem, ctx->stream>>>(
+          g->cert, g->cert_bytes, g->V, g->n_src, g->off_vidx, g->off_term, g->off_src,
+          g->off_succ, g->prog, g->prog_ptr, g->preds, g->pred_ptr, I, ref, ref_stride, target,
+          now, K, Q, 5.0 * gam + 8.0 * u, out_slack, out_ratio);
+      SP_CHECK_LAUNCH(ctx);
+      return SP_OK;
+    }
+  }
   if (g->cert && ctx->opt.k1_cert != 1) {
     const int nfw = (g->n_src + 31) / 32;
     const size_t smem = (size_t)g->cert_bytes +

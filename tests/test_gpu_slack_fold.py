@@ -83,7 +83,15 @@ def test_deep_dag_config3_vs_dp_oracle(gpu_ctx):
     assert np.isfinite(r["slack"]).all()
 
 
-def test_deep_dag_certified_pass_equals_forward_dp(gpu_ctx, monkeypatch):
+@pytest.fixture(params=[4, 2])
+def k1c_lanes(request, gpu_ctx):
+    """Both forms of the certified pass: four lanes per instance (default) and two."""
+    gpu_ctx.set_option("SP_K1C_LANES", request.param)
+    yield request.param
+    gpu_ctx.set_option("SP_K1C_LANES", 4)
+
+
+def test_deep_dag_certified_pass_equals_forward_dp(gpu_ctx, k1c_lanes):
     """K1c (certified backward pass, the default for config 3) against K1's forward DP on the
     full 100k-instance launch: every slack and ratio bit-identical.  A second batch with
     quantised refs (exact ties between paths), zeros, and a few negative / inf / NaN refs
@@ -113,7 +121,7 @@ def test_deep_dag_certified_pass_equals_forward_dp(gpu_ctx, monkeypatch):
             assert np.array_equal(bits(got[key]), bits(exp[key])), key
 
 
-def test_dag_slack_certified_forced_vs_reference(gpu_ctx, monkeypatch):
+def test_dag_slack_certified_forced_vs_reference(gpu_ctx, k1c_lanes):
     """The 400 reference DAG cases with K1c forced on every graph (SP_K1_CERT=force), small
     integer-valued refs included: bit-identical to the reference's compute_slack."""
     gpu_ctx.set_option("SP_K1_CERT", 2)  # force
