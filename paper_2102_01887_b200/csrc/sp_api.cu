@@ -183,7 +183,7 @@ void options_from_env(Options& o) {
   o.stair_global = getenv("SP_STAIR_GLOBAL") != nullptr;
   o.no_plan_graph = getenv("SP_NO_PLAN_GRAPH") != nullptr;
   o.plan_legacy = getenv("SP_PLAN_LEGACY") != nullptr;
-  o.pc_debug = getenv("SP_PC_DEBUG") != nullptr;
+  o.pc_debug = getenv("SP_PC_DEBUG") ? std::max(1, env_int("SP_PC_DEBUG", 1)) : 0;
   if (const char* e = getenv("SP_K2_VARIANT")) o.k2_plan_only = strcmp(e, "fast") != 0;
   o.k2f_threads = env_int("SP_K2F_THREADS", 512) == 1024 ? 1024 : 512;
   o.no_pdl = getenv("SP_NO_PDL") != nullptr;

@@ -473,8 +473,9 @@ static int fold_launch_legacy(sp_ctx* ctx, int n_tables, sp_table* const* tables
 //     the entry's 64-bit tile mask (the first setter appends the entry to the touched list),
 //     and folds its min / max into the entry's bounds (warp-segmented scan, one atomic pair per
 //     run and warp); reference runs add to the table's reference count.
-//   grid barrier; every CTA evaluates, per table, whether the gate lifts in this chunk
-//     (k = dfp_count - completed_ref_before in [1, reference count]).
+//   grid barrier (one returning atomic per CTA); every warp evaluates, per table, whether the
+//     gate lifts in this chunk (k = dfp_count - completed_ref_before in [1, reference count]),
+//     and issues its first entry's loads in the same round trip.
 //   phase B (only when a gate lifts): one warp per lifting table folds the reference entry up to
 //     its k-th observation (ratio = lat / lat_init, configurator.py:486) and on; grid barrier.
 //   phase C (warp per touched entry): the entry's runs in tile order from the mask and slots;
@@ -483,7 +484,10 @@ static int fold_launch_legacy(sp_ctx* ctx, int n_tables, sp_table* const* tables
 //     over the last `win` observations when the bounds allow it, else sequentially — staged
 //     through a per-warp shared-memory buffer; counts; the entry's mask / bounds reset.
 //   grid barrier; phase D: completed_ref, the per-chunk counters reset, and (when a gate lifted)
-//     the rescale of every entry still unobserved (configurator.py:486-490).
+//     the rescale of every entry still unobserved (configurator.py:486-490).  In the last chunk
+//     with no gate lift there is no barrier: the last CTA to finish phase C does phase D.
+// Touched entries are dealt CTA-major so the hottest (first-touched, longest chains) run on
+// different SMs; observations are gathered by cp.async, beta * o precomputed by the lanes.
 //
 // Splitting a batch into consecutive chunks folds exactly as one batch does (the multi-kernel
 // path's chunked tests rely on the same property).
@@ -497,7 +501,7 @@ constexpr int kCoopWarpBuf = 256;              // observations staged per warp
 constexpr int kCoopWarps = kCoopThreads / 32;
 
 struct CoopState {  // persistent per context; zero (lo: ~0) outside a launch
-  uint32_t bar[2];      // grid barrier: arrivals, generation
+  uint32_t bar[2];      // grid barrier: arrival word (top bit flips per barrier); CTAs done
   int32_t touched_n[2];  // per chunk parity
   int32_t refcnt[2][kMaxFoldTables];
 };
@@ -544,6 +548,11 @@ __device__ __forceinline__ double coop_obs(const CoopArgs& a, int j) {
   return __dmul_rn(lat, a.t_noise[j]);
 }
 
+__device__ __forceinline__ unsigned coop_smid() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
 __device__ __forceinline__ uint64_t coop_timer() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -655,20 +664,18 @@ __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
   return v;
 }
 
-// Grid-wide barrier (all CTAs are co-resident: cooperative launch).
+// Grid-wide barrier (all CTAs are co-resident: cooperative launch).  One returning atomic per
+// CTA on the arrival word: CTA 0 adds 2^31 - (G - 1), every other CTA adds 1, so the G arrivals
+// add exactly 2^31 and flip the word's top bit whatever it held before (no reset, any grid size
+// from launch to launch); a CTA leaves when the top bit differs from the one it saw on arrival.
 __device__ __forceinline__ void coop_sync(uint32_t* bar) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    const uint32_t gen = ld_acquire_u32(bar + 1);
-    __threadfence();
-    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
-      atomicExch(bar, 0u);
-      __threadfence();
-      atomicAdd(bar + 1, 1u);
-    } else {
-      while (ld_acquire_u32(bar + 1) == gen) __nanosleep(32);
+    const uint32_t add = blockIdx.x == 0 ? 0x80000000u - (gridDim.x - 1u) : 1u;
+    uint32_t old;
+    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(bar), "r"(add) : "memory");
+    while (((ld_acquire_u32(bar) ^ old) & 0x80000000u) == 0u) {
     }
-    __threadfence();
   }
   __syncthreads();
 }
@@ -689,15 +696,42 @@ struct WarpRuns {
   int32_t nr;
 };
 
-__device__ __forceinline__ int runs_load(const CoopArgs& a, uint32_t key, WarpRuns& R) {
+// An entry's fold inputs, loaded in one round trip (the 64 run slots unconditionally: the mask
+// says which are live).  L2 loads (__ldcg): the chunk arrays are rewritten by other CTAs.
+// (spread over the warp to save registers: lane 0 the tile mask, 1 / 2 the order-key bounds, 3
+// obs_count, 4 the latency bits; every lane two run slots)
+struct EntryPre {
+  uint64_t w;
+  uint32_t sv0, sv1;  // slots of tiles lane, lane + 32
+  __device__ __forceinline__ uint64_t get(int l) const { return __shfl_sync(0xffffffffu, w, l); }
+  __device__ __forceinline__ uint64_t mask() const { return get(0); }
+  __device__ __forceinline__ uint64_t lo() const { return get(1); }
+  __device__ __forceinline__ uint64_t hi() const { return get(2); }
+  __device__ __forceinline__ int before() const { return (int)get(3); }
+  __device__ __forceinline__ double L() const { return __longlong_as_double((long long)get(4)); }
+};
+__device__ __forceinline__ EntryPre entry_load(const CoopArgs& a, uint32_t key, const FoldTab& tb,
+                                               int e) {
   const int lane = threadIdx.x & 31;
-  const uint64_t m = a.mask[key];
+  EntryPre p;
+  const uint64_t* src = reinterpret_cast<const uint64_t*>(lane == 1 ? a.lo : lane == 2 ? a.hi : a.mask) + key;
+  if (lane == 4) src = reinterpret_cast<const uint64_t*>(tb.lat) + e;
+  p.w = lane == 3 ? (uint64_t)(uint32_t)__ldcg(tb.obs_count + e)
+                  : __ldcg(reinterpret_cast<const unsigned long long*>(src));
+  p.sv0 = __ldcg(a.slot + (size_t)key * kCoopTiles + lane);
+  p.sv1 = __ldcg(a.slot + (size_t)key * kCoopTiles + lane + 32);
+  return p;
+}
+
+__device__ __forceinline__ int runs_load(const EntryPre& p, WarpRuns& R) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t m = p.mask();
   int cnt = 0;
+#pragma unroll
   for (int h = 0; h < 2; ++h) {
     const int tl = lane + 32 * h;
     const bool has = (m >> tl) & 1ull;
-    uint32_t sv = 0;
-    if (has) sv = a.slot[(size_t)key * kCoopTiles + tl];
+    const uint32_t sv = h ? p.sv1 : p.sv0;
     const int len = has ? (int)(sv >> 16) : 0;
     // rank of this run among the key's runs, and records before it
     const uint64_t below = tl ? (m & ((1ull << tl) - 1ull)) : 0ull;
@@ -733,6 +767,25 @@ __device__ __forceinline__ int runs_at(const WarpRuns& R, int ordinal) {
   return R.rstart[lo] + (ordinal - R.rcum[lo]);
 }
 
+// buf[0, count) = the entry's observations [base, base + count), count <= kCoopWarpBuf: every
+// lane's loads issued before any store (one memory round trip, not one per 32 observations)
+// Elements from `scaled` on are stored as fl(beta * o), the chain's independent half, so the
+// serial chains below carry one dependent DMUL + DADD per step.
+__device__ __forceinline__ void gather_obs(const CoopArgs& a, const WarpRuns& R, double* buf,
+                                           int base, int count, int scaled) {
+  // cp.async: the copies need no registers while in flight (the grid barrier's acquire has
+  // invalidated L1, so .ca sees the phase-A writes of other CTAs)
+  for (int u = (threadIdx.x & 31); u < count; u += 32) {
+    const double* src = a.sobs + runs_at(R, base + u);
+    const unsigned dst = (unsigned)__cvta_generic_to_shared(buf + u);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  for (int u = scaled + (threadIdx.x & 31) - (scaled & 31); u < count; u += 32)  // own copies
+    if (u >= scaled) buf[u] = __dmul_rn(a.beta, buf[u]);
+  __syncwarp();
+}
+
 // Warp-cooperative exact fold of the entry's observations [o0, o1) from L (result valid in
 // every lane).  With `bounded` (lo..hi holds every chain value) a window of the last `win`
 // observations is tried first; it returns the exact value whenever the two bound chains meet.
@@ -752,9 +805,7 @@ __device__ double coop_fold(const CoopArgs& a, const WarpRuns& R, double* buf, d
   constexpr int kNk = 64, kNw = 24;
   if (bounded && ol <= 0.5 && ob >= 0x1p-60 && ol >= 0x1p-60 && lo > 0x1p-900 && hi < 0x1p900 &&
       o1 - o0 >= kNk + kNw) {
-    const int base = o1 - kNw - kNk;
-    for (int u = lane; u < kNk + kNw; u += 32) buf[u] = a.sobs[runs_at(R, base + u)];
-    __syncwarp();
+    gather_obs(a, R, buf, o1 - kNw - kNk, kNk + kNw, kNk);
     const double cl = 1.0 - 0x1p-52, ch = 1.0 + 0x1p-51;
     const double ql = __dmul_rd(cl, ol), qh = __dmul_ru(ch, ol);
     const double bl = __dmul_rd(cl, ob), bh = __dmul_ru(ch, ob);
@@ -789,9 +840,9 @@ __device__ double coop_fold(const CoopArgs& a, const WarpRuns& R, double* buf, d
     double v = 0.0;
     if (lane == 0) {
       double x = zl > lo ? zl : lo, y = zh < hi ? zh : hi;
-#pragma unroll 4
+#pragma unroll
       for (int u = kNk; u < kNk + kNw; ++u) {
-        const double t = __dmul_rn(ob, buf[u]);
+        const double t = buf[u];  // fl(beta o)
         x = __dadd_rn(t, __dmul_rn(ol, x));
         y = __dadd_rn(t, __dmul_rn(ol, y));
       }
@@ -804,15 +855,14 @@ __device__ double coop_fold(const CoopArgs& a, const WarpRuns& R, double* buf, d
     if (same) return v;
   }
   if (bounded && o1 - o0 > a.win && a.win <= kCoopWarpBuf) {
-    const int w0 = o1 - a.win;
-    for (int u = lane; u < a.win; u += 32) buf[u] = a.sobs[runs_at(R, w0 + u)];
-    __syncwarp();
+    gather_obs(a, R, buf, o1 - a.win, a.win, 0);
     int same = 0;
     double v = 0.0;
     if (lane == 0) {
       double x = lo, y = hi;
+#pragma unroll 8
       for (int u = 0; u < a.win; ++u) {
-        const double t = __dmul_rn(ob, buf[u]);
+        const double t = buf[u];  // fl(beta o)
         x = __dadd_rn(t, __dmul_rn(ol, x));
         y = __dadd_rn(t, __dmul_rn(ol, y));
       }
@@ -826,19 +876,20 @@ __device__ double coop_fold(const CoopArgs& a, const WarpRuns& R, double* buf, d
   }
   for (int p0 = o0; p0 < o1; p0 += kCoopWarpBuf) {
     const int p1 = min(o1, p0 + kCoopWarpBuf);
-    for (int u = p0 + lane; u < p1; u += 32) buf[u - p0] = a.sobs[runs_at(R, u)];
-    __syncwarp();
-    if (lane == 0)
-      for (int u = 0; u < p1 - p0; ++u) L = __dadd_rn(__dmul_rn(ob, buf[u]), __dmul_rn(ol, L));
+    gather_obs(a, R, buf, p0, p1 - p0, 0);
+    if (lane == 0) {
+#pragma unroll 8
+      for (int u = 0; u < p1 - p0; ++u) L = __dadd_rn(buf[u], __dmul_rn(ol, L));  // buf: fl(beta o)
+    }
     __syncwarp();
   }
   return __shfl_sync(0xffffffffu, L, 0);
 }
 
 // bounds of every chain value from the chunk's observation range of `key` and the start L
-__device__ __forceinline__ bool coop_bounds(const CoopArgs& a, uint32_t key, double L, double* lo,
+__device__ __forceinline__ bool coop_bounds(uint64_t klo, uint64_t khi, double L, double* lo,
                                             double* hi) {
-  double m = fold_unkey(a.lo[key]), M = fold_unkey(a.hi[key]);
+  double m = fold_unkey(klo), M = fold_unkey(khi);
   if (!(isfinite(m) && isfinite(M) && isfinite(L))) return false;
   m = L < m ? L : m;
   M = L > M ? L : M;
@@ -847,23 +898,18 @@ __device__ __forceinline__ bool coop_bounds(const CoopArgs& a, uint32_t key, dou
   return true;
 }
 
-__device__ __forceinline__ bool gate_lifts(const CoopArgs& a, const FoldTab& tb, int refcnt) {
-  if (a.fb_frozen || !a.dfp_on || tb.ref_index < 0 || refcnt <= 0) return false;
-  const int k = a.dfp_count - tb.counters[0];
-  return k >= 1 && k <= refcnt && tb.lat_init[tb.ref_index] > 0.0;
-}
-
 __global__ void __launch_bounds__(kCoopThreads, 1) k_fold_coop(const __grid_constant__ CoopArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ uint32_t s_key[kCoopTile];
-  __shared__ uint64_t s_lift;  // tables whose gate lifts in this chunk
+  __shared__ uint32_t s_last;  // this CTA finished phase C last (phase D is its)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   WarpRuns& R = reinterpret_cast<WarpRuns*>(smem)[warp];
   double* buf = reinterpret_cast<double*>(smem + sizeof(WarpRuns) * kCoopWarps) + warp * kCoopWarpBuf;
   const uint32_t sent = (uint32_t)a.ft.total;
   CoopState* st = a.st;
-  uint64_t tm[8] = {};
-  tm[0] = coop_timer();
+  __shared__ uint64_t tm[8];  // SP_PC_DEBUG phase timestamps (thread 0)
+  const bool dbg = a.debug && threadIdx.x == 0;
+  if (dbg) tm[0] = coop_timer();
   // programmatic dependent launch: the observation stream and the tables are the predecessors'
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;");
@@ -884,10 +930,10 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_fold_coop(const __grid_cons
         }
       }
       __syncthreads();  // tmp / s_key reuse across tiles
-      if (chunk == 0) tm[1] = coop_timer();
+      if (dbg && chunk == 0) tm[1] = coop_timer();
       uint32_t run_len;
       tile_group(key[0], val[0], run_len, smem);
-      if (chunk == 0) tm[2] = coop_timer();
+      if (dbg && chunk == 0) tm[2] = coop_timer();
       const uint32_t k = key[0];
       s_key[threadIdx.x] = k;
       const int q = tl * kCoopTile + (int)threadIdx.x;  // chunk-array index
@@ -925,29 +971,48 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_fold_coop(const __grid_cons
         }
       }
     }
-    if (chunk == 0) tm[3] = coop_timer();
+    if (a.debug > 1) __syncthreads();
+    if (dbg && chunk == 0) tm[3] = coop_timer();
     coop_sync(st->bar);
-    if (chunk == 0) tm[4] = coop_timer();
-    // ---- gates of this chunk (uniform in every CTA) ----
-    if (threadIdx.x == 0) {
-      uint64_t lift = 0;
-      for (int t = 0; t < a.ft.n; ++t)
-        if (gate_lifts(a, a.ft.t[t], ld_acquire_u32((const uint32_t*)&st->refcnt[par][t])))
-          lift |= 1ull << t;
-      s_lift = lift;
+    if (dbg && chunk == 0) tm[4] = coop_timer();
+    // ---- gates of this chunk: every warp evaluates them itself (lane t: tables t, t + 32; the
+    // same value in every warp), with the first touched entry's loads in the same round trip ----
+    const int nt = (int)__ldcg(&st->touched_n[par]);
+    // touched entries dealt CTA-major (entry u -> CTA u mod G): the first-touched (hottest) entries
+    // land on different SMs instead of contending for one SM's FP64 pipe with their serial chains
+    const int u0 = warp * gridDim.x + blockIdx.x, ustride = gridDim.x * kCoopWarps;
+    // speculative until nt is known: clamped into the key space, used only when u0 < nt
+    const uint32_t key0 = min(__ldcg(reinterpret_cast<const uint32_t*>(a.touched) + u0), sent - 1u);
+    const int t0 = table_of_key(a.ft, key0);
+    EntryPre pre0 = entry_load(a, key0, a.ft.t[t0], (int)key0 - a.ft.t[t0].gbase);
+    uint64_t lift = 0;
+    {
+      bool g[2] = {false, false};
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int t = lane + 32 * h;
+        if (t < a.ft.n) {
+          const FoldTab& tb = a.ft.t[t];
+          const int rc = __ldcg(&st->refcnt[par][t]);
+          const int done = __ldcg(tb.counters);
+          const double li = __ldcg(tb.lat_init + (tb.ref_index > 0 ? tb.ref_index : 0));
+          const int k = a.dfp_count - done;
+          g[h] = !a.fb_frozen && a.dfp_on && tb.ref_index >= 0 && rc > 0 && k >= 1 && k <= rc && li > 0.0;
+        }
+      }
+      lift = (uint64_t)__ballot_sync(0xffffffffu, g[0]) | (uint64_t)__ballot_sync(0xffffffffu, g[1]) << 32;
     }
-    __syncthreads();
-    const uint64_t lift = s_lift;
     if (lift) {  // ---- phase B: the reference entries of the lifting tables ----
       const int gw = blockIdx.x * kCoopWarps + warp;
       for (int t = gw; t < a.ft.n; t += gridDim.x * kCoopWarps) {
         if (!((lift >> t) & 1ull)) continue;
         const FoldTab& tb = a.ft.t[t];
         const uint32_t rk = (uint32_t)(tb.gbase + tb.ref_index);
-        const int cnt = runs_load(a, rk, R);
-        const int k = a.dfp_count - tb.counters[0];
-        double L = tb.lat[tb.ref_index], lo = 0.0, hi = 0.0;
-        const bool bd = cnt > a.win && coop_bounds(a, rk, L, &lo, &hi);
+        const EntryPre pre = entry_load(a, rk, tb, tb.ref_index);
+        const int cnt = runs_load(pre, R);
+        const int k = a.dfp_count - __ldcg(tb.counters);
+        double L = pre.L(), lo = 0.0, hi = 0.0;
+        const bool bd = cnt > a.win && coop_bounds(pre.lo(), pre.hi(), L, &lo, &hi);
         L = coop_fold(a, R, buf, L, 0, k, bd, lo, hi);
         const double ratio = __ddiv_rn(L, tb.lat_init[tb.ref_index]);  // configurator.py:486
         const int gpos = (int)a.spos[runs_at(R, k - 1)];
@@ -964,37 +1029,39 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_fold_coop(const __grid_cons
         __syncwarp();
       }
       coop_sync(st->bar);
+      pre0 = entry_load(a, key0, a.ft.t[t0], (int)key0 - a.ft.t[t0].gbase);  // not kept live across B
     }
     // ---- phase C: every touched entry (warp each) ----
     {
-      const int nt = ld_acquire_u32((const uint32_t*)&st->touched_n[par]);
-      for (int u = blockIdx.x * kCoopWarps + warp; u < nt; u += gridDim.x * kCoopWarps) {
-        const uint32_t key = (uint32_t)a.touched[u];
+      uint32_t key = key0;
+      EntryPre pre = pre0;
+      for (int u = u0; u < nt;) {
         const int t = table_of_key(a.ft, key);
         const FoldTab& tb = a.ft.t[t];
         const int e = (int)key - tb.gbase;
-        if (((lift >> t) & 1ull) && e == tb.ref_index) continue;  // phase B
-        const uint64_t c0 = a.debug ? coop_timer() : 0;
-        const int cnt = runs_load(a, key, R);
-        const uint64_t c1 = a.debug ? coop_timer() : 0;
-        const int before = tb.obs_count[e];
-        uint64_t c2 = 0, c3 = 0;
+        const bool skip = ((lift >> t) & 1ull) && e == tb.ref_index;  // folded in phase B
+        if (skip) {
+          u += ustride;
+          if (u < nt) {
+            key = __ldcg(reinterpret_cast<const uint32_t*>(a.touched) + u);
+            const int tn = table_of_key(a.ft, key);
+            pre = entry_load(a, key, a.ft.t[tn], (int)key - a.ft.t[tn].gbase);
+          }
+          continue;
+        }
+        const int before = pre.before();
+        double L = pre.L();
+        const uint64_t klo = pre.lo(), khi = pre.hi();
+        const int cnt = runs_load(pre, R);
         if (!a.fb_frozen) {
-          double L = tb.lat[e];
           if ((lift >> t) & 1ull) {
             const Gate g = a.gates[t];
             if (before == 0 && (int)a.spos[R.rstart[0]] > g.gate_pos)
               L = __dmul_rn(tb.lat_init[e], g.ratio);
           }
           double lo = 0.0, hi = 0.0;
-          const bool bd = cnt > a.win && coop_bounds(a, key, L, &lo, &hi);
-          c2 = a.debug ? coop_timer() : 0;
+          const bool bd = cnt > a.win && coop_bounds(klo, khi, L, &lo, &hi);
           L = coop_fold(a, R, buf, L, 0, cnt, bd, lo, hi);
-          c3 = a.debug ? coop_timer() : 0;
-          if (a.debug && lane == 0 && blockIdx.x == 0 && warp < 4)
-            printf("fold C warp %d key %u cnt %d: runs %llu bounds %llu fold %llu (from C start %llu) ns\n",
-                   warp, key, cnt, (unsigned long long)(c1 - c0), (unsigned long long)(c2 - c1),
-                   (unsigned long long)(c3 - c2), (unsigned long long)(c3 - tm[4]));
           if (lane == 0) {
             tb.lat[e] = L;
             tb.dirty[e] = 1;
@@ -1007,11 +1074,40 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_fold_coop(const __grid_cons
           a.hi[key] = 0ull;
         }
         __syncwarp();
+        u += ustride;
+        if (u < nt) {
+          key = __ldcg(reinterpret_cast<const uint32_t*>(a.touched) + u);
+          const int tn = table_of_key(a.ft, key);
+          pre = entry_load(a, key, a.ft.t[tn], (int)key - a.ft.t[tn].gbase);
+        }
       }
     }
-    if (chunk == 0) tm[5] = coop_timer();
+    if (a.debug > 1) __syncthreads();
+    if (dbg && chunk == 0) tm[5] = coop_timer();
+    if (!lift && c0 + kCoopChunk >= a.n) {
+      // last chunk, no gate lift: nothing after phase C reads another CTA's phase-C writes in
+      // this launch, so instead of a grid barrier the last CTA to finish does phase D
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        uint32_t old;
+        asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(st->bar + 1) : "memory");
+        s_last = old == gridDim.x - 1u;
+        if (old == gridDim.x - 1u) st->bar[1] = 0u;
+      }
+      __syncthreads();
+      if (s_last) {
+        if (threadIdx.x < a.ft.n) {
+          const int t = threadIdx.x;
+          a.ft.t[t].counters[0] += st->refcnt[par][t];
+          st->refcnt[par][t] = 0;
+        }
+        if (threadIdx.x == 0) st->touched_n[par] = 0;
+      }
+      if (dbg && chunk == 0) tm[6] = coop_timer();
+      break;
+    }
     coop_sync(st->bar);
-    if (chunk == 0) tm[6] = coop_timer();
+    if (dbg && chunk == 0) tm[6] = coop_timer();
     // ---- phase D ----
     if (blockIdx.x == 0 && threadIdx.x < a.ft.n) {
       const int t = threadIdx.x;
@@ -1033,6 +1129,13 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_fold_coop(const __grid_cons
     }
     // the next chunk's phase C reads counters / latencies written here: its phase-A barrier
     // orders them
+  }
+  if (a.debug > 1 && threadIdx.x == 0) {
+    tm[7] = coop_timer();
+    printf("fold abs cta %d smid %u: t0 %llu A_end %llu barA_out %llu C_end %llu end %llu\n", blockIdx.x,
+           coop_smid(), (unsigned long long)tm[0] % 100000000ull, (unsigned long long)tm[3] % 100000000ull,
+           (unsigned long long)tm[4] % 100000000ull, (unsigned long long)tm[5] % 100000000ull,
+           (unsigned long long)tm[7] % 100000000ull);
   }
   if (a.debug && threadIdx.x == 0 && blockIdx.x < 2) {
     tm[7] = coop_timer();
@@ -1075,6 +1178,9 @@ static int coop_buffers(sp_ctx* ctx, int64_t keys, CoopArgs& a) {
     SP_CUDA(cudaMemsetAsync(q + al(8u * cap), 0xFF, al(8u * cap), ctx->stream));  // lo
     SP_CUDA(cudaMemsetAsync(q + 2 * al(8u * cap), 0, al(8u * cap), ctx->stream)); // hi
     SP_CUDA(cudaMemsetAsync(q + per + chunk + gates, 0, stb, ctx->stream));       // barrier / counters
+    // run slots and the touched list: read speculatively (ignored unless live), kept defined
+    SP_CUDA(cudaMemsetAsync(q + 3 * al(8u * cap), 0, al(4u * kCoopTiles * cap), ctx->stream));
+    SP_CUDA(cudaMemsetAsync(q + per, 0, chunk, ctx->stream));
     b.keys = cap;
   }
   const int64_t cap = b.keys;

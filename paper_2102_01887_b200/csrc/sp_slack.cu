@@ -445,7 +445,8 @@ __global__ void __launch_bounds__(32 * kCertWarps) k_slack_cert4(
   const bool live = i < I;
   const double* r = ref + (size_t)(live ? i : i0) * ref_stride;
 
-  A[V * 16 + side] = -INFINITY;
+  if (sub == 0) A[V * 16 + side] = -INFINITY;
+  __syncwarp();
   bool bad = false;
   double rn = __ldg(r + VI[V - 1]);
   for (int v = V - 1; v >= 0; --v) {
@@ -493,7 +494,6 @@ __global__ void __launch_bounds__(32 * kCertWarps) k_slack_cert4(
       h1 = H1;
     }
     a1 >>= 8;
-    A[v * 16 + side] = __dadd_rn(side ? -rv : rv, h1);
     float gm = __double2float_rd(__dsub_rd(h1, h2));
     if (a1 < kArgNone) {
       const float gn = Cf[a1 * 16 + side];
@@ -501,8 +501,12 @@ __global__ void __launch_bounds__(32 * kCertWarps) k_slack_cert4(
     } else if (a1 == kArgNone) {
       gm = -INFINITY;
     }
-    Cf[v * 16 + side] = gm;
-    Rb[v * 16 + side] = (uint8_t)a1;
+    if (sub == 0) {  // both sub-lanes hold the merged values; one writes
+      A[v * 16 + side] = __dadd_rn(side ? -rv : rv, h1);
+      Cf[v * 16 + side] = gm;
+      Rb[v * 16 + side] = (uint8_t)a1;
+    }
+    __syncwarp();
   }
   bad |= __shfl_xor_sync(0xffffffffu, bad, 1);
   bad |= __shfl_xor_sync(0xffffffffu, bad, 2);
