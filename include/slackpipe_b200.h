@@ -77,7 +77,8 @@ int sp_ctx_destroy(sp_ctx* ctx);
 int sp_ctx_set_stream(sp_ctx* ctx, void* stream);
 int sp_ctx_synchronize(sp_ctx* ctx);
 /* Dispatch variants of this context (read once from the environment at creation; names are the
- * variables: SP_ZERO_COPY, SP_PIPE_CHUNKS, SP_K1_CERT (0 auto / 1 off / 2 force), SP_NO_PDL,
+ * variables: SP_ZERO_COPY, SP_PIPE_CHUNKS, SP_K1_CERT (0 auto / 1 off / 2 force), SP_K1C_LANES
+ * (lanes per instance of the certified slack pass: 4 default / 2), SP_FOLD_LEGACY, SP_NO_PDL,
  * SP_PLAN_LEGACY, SP_K2_VARIANT, ... — see sp_internal.cuh Options).  For tests and tools. */
 int sp_ctx_set_option(sp_ctx* ctx, const char* name, int64_t value);
 /* Last error message of this thread (ctx may be NULL). */
