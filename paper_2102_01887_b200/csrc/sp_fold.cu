@@ -572,8 +572,11 @@ __device__ __forceinline__ uint64_t coop_timer() {
 // On return thread i holds the record at position i and `len` = its run's length when it is the
 // run's first record (0 otherwise).  Shared memory: kTileGroupSmem bytes at `sm` (16-B aligned).
 constexpr int kTileHash = 2048;
-constexpr int kTileGroupSmem = kCoopTile * 32 + kTileHash * 4 + kTileHash * 2 + kCoopTile * 4 * 4;
-__device__ __forceinline__ void tile_group(uint32_t& key, uint32_t& val, uint32_t& len, uint8_t* sm) {
+constexpr int kTileGroupSmem = kCoopTile * 32 + kTileHash * 4 + kTileHash * 2 + kCoopTile * 4 * 4 +
+                               kCoopTile * 8;
+// `pay` (the record's observation) travels with the record.
+__device__ __forceinline__ void tile_group(uint32_t& key, uint32_t& val, uint32_t& len, double& pay,
+                                           uint8_t* sm) {
   uint32_t* cnt = reinterpret_cast<uint32_t*>(sm);                 // [1024 ids][32 warps] bytes
   uint32_t* htab = cnt + kCoopTile * 8;                            // kTileHash keys
   uint16_t* hid = reinterpret_cast<uint16_t*>(htab + kTileHash);   // kTileHash ids
@@ -581,6 +584,7 @@ __device__ __forceinline__ void tile_group(uint32_t& key, uint32_t& val, uint32_
   uint32_t* sk = start + kCoopTile;
   uint32_t* sv = sk + kCoopTile;
   uint32_t* sl = sv + kCoopTile;
+  double* so = reinterpret_cast<double*>(sl + kCoopTile);  // 16-B aligned: offsets are multiples of 4 KB
   __shared__ uint32_t s_n, s_ws[32];
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
 #pragma unroll
@@ -645,6 +649,7 @@ __device__ __forceinline__ void tile_group(uint32_t& key, uint32_t& val, uint32_
   const uint32_t pos = start[id] + before + rank;
   sk[pos] = key;
   sv[pos] = val;
+  so[pos] = pay;
   uint32_t mylen = 0;
   if (before == 0 && rank == 0) {  // first record of the key
 #pragma unroll
@@ -655,6 +660,7 @@ __device__ __forceinline__ void tile_group(uint32_t& key, uint32_t& val, uint32_
   key = sk[t];
   val = sv[t];
   len = sl[t];
+  pay = so[t];
   __syncthreads();
 }
 
@@ -921,23 +927,26 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_fold_coop(const __grid_cons
     for (int tl = blockIdx.x; tl < ntiles; tl += gridDim.x) {
       const int j = c0 + tl * kCoopTile + (int)threadIdx.x;
       uint32_t key[1] = {sent}, val[1] = {(uint32_t)j};
+      double o = 0.0;  // loaded before the grouping, carried through it
       if (j < a.n) {
         const int e = coop_entry(a, j);
-        if (e >= 0) key[0] = (uint32_t)(a.ft.t[a.op ? a.op[j] : 0].gbase + e);
+        if (e >= 0) {
+          key[0] = (uint32_t)(a.ft.t[a.op ? a.op[j] : 0].gbase + e);
+          o = coop_obs(a, j);
+        }
         if (a.rec_idx) {
           a.rec_idx[j] = e;
-          a.rec_obs[j] = e >= 0 ? coop_obs(a, j) : 0.0;
+          a.rec_obs[j] = o;
         }
       }
       __syncthreads();  // tmp / s_key reuse across tiles
       if (dbg && chunk == 0) tm[1] = coop_timer();
       uint32_t run_len;
-      tile_group(key[0], val[0], run_len, smem);
+      tile_group(key[0], val[0], run_len, o, smem);
       if (dbg && chunk == 0) tm[2] = coop_timer();
       const uint32_t k = key[0];
       s_key[threadIdx.x] = k;
       const int q = tl * kCoopTile + (int)threadIdx.x;  // chunk-array index
-      const double o = k != sent ? coop_obs(a, (int)val[0]) : 0.0;
       a.skey[q] = k;
       a.spos[q] = val[0];
       a.sobs[q] = o;
