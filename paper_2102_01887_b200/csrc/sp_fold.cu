@@ -907,7 +907,6 @@ __device__ __forceinline__ bool coop_bounds(uint64_t klo, uint64_t khi, double L
 __global__ void __launch_bounds__(kCoopThreads, 1) k_fold_coop(const __grid_constant__ CoopArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ uint32_t s_key[kCoopTile];
-  __shared__ uint32_t s_last;  // this CTA finished phase C last (phase D is its)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   WarpRuns& R = reinterpret_cast<WarpRuns*>(smem)[warp];
   double* buf = reinterpret_cast<double*>(smem + sizeof(WarpRuns) * kCoopWarps) + warp * kCoopWarpBuf;
@@ -1011,6 +1010,30 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_fold_coop(const __grid_cons
       }
       lift = (uint64_t)__ballot_sync(0xffffffffu, g[0]) | (uint64_t)__ballot_sync(0xffffffffu, g[1]) << 32;
     }
+    // last chunk, no gate lift: nothing after this point reads the counters phase D resets, and
+    // nothing after phase C reads another CTA's phase-C writes in this launch — so no barrier
+    // after phase C: every CTA checks in here (its warps have read touched_n and the gates) and
+    // the last one to check in does phase D while the others fold
+    const bool early_d = !lift && c0 + kCoopChunk >= a.n;
+    if (early_d) {
+      __syncthreads();
+      if (warp == 0) {
+        uint32_t old = 0;
+        if (lane == 0)
+          asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(st->bar + 1) : "memory");
+        old = __shfl_sync(0xffffffffu, old, 0);
+        if (old == gridDim.x - 1u) {
+          for (int t = lane; t < a.ft.n; t += 32) {
+            a.ft.t[t].counters[0] += st->refcnt[par][t];
+            st->refcnt[par][t] = 0;
+          }
+          if (lane == 0) {
+            st->touched_n[par] = 0;
+            st->bar[1] = 0u;
+          }
+        }
+      }
+    }
     if (lift) {  // ---- phase B: the reference entries of the lifting tables ----
       const int gw = blockIdx.x * kCoopWarps + warp;
       for (int t = gw; t < a.ft.n; t += gridDim.x * kCoopWarps) {
@@ -1093,25 +1116,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_fold_coop(const __grid_cons
     }
     if (a.debug > 1) __syncthreads();
     if (dbg && chunk == 0) tm[5] = coop_timer();
-    if (!lift && c0 + kCoopChunk >= a.n) {
-      // last chunk, no gate lift: nothing after phase C reads another CTA's phase-C writes in
-      // this launch, so instead of a grid barrier the last CTA to finish does phase D
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        uint32_t old;
-        asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(st->bar + 1) : "memory");
-        s_last = old == gridDim.x - 1u;
-        if (old == gridDim.x - 1u) st->bar[1] = 0u;
-      }
-      __syncthreads();
-      if (s_last) {
-        if (threadIdx.x < a.ft.n) {
-          const int t = threadIdx.x;
-          a.ft.t[t].counters[0] += st->refcnt[par][t];
-          st->refcnt[par][t] = 0;
-        }
-        if (threadIdx.x == 0) st->touched_n[par] = 0;
-      }
+    if (early_d) {  // phase D is done (above)
       if (dbg && chunk == 0) tm[6] = coop_timer();
       break;
     }
